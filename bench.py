@@ -1,0 +1,356 @@
+#!/usr/bin/env python
+"""Benchmark of the graph-parallel EGN training step (BASELINE.json metric:
+triplet-interactions/s and train steps/s, GemNet-T / DimeNet++).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload NAME]
+
+One step = one SGD training step (forward + backward + update) over one
+synthetic batch.  Default workload = BASELINE configs[1]: GemNet-T default
+dims (emb 128, triplet emb 64, bilinear 64, 4 blocks), 32 graphs x 80 atoms
+at OC20-like density (random_cloud rho=0.06, cutoff 6 A, <=50 neighbours),
+loss w_E = w_F = 1 against a teacher model (init_params(seed=1)).
+
+Prints ONE JSON line (rank 0).  ``value`` = triplet-interactions/s of the
+whole job = N_t(batch) * blocks / t_step, device-timed with inputs resident;
+``e2e`` = the same metric through the public API with host buffers (H2D of
+positions + targets, graph build, step, D2H of the loss) inside the timed
+region.  ``--impl reference`` times the CPU reference path (the fp64 numpy
+oracle, a restatement of egn.ModelTape; see oracle/egn_oracle.py) on the
+host cores for a bounded sample of the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+WORKLOADS = {
+    # BASELINE configs[1]
+    "gemnet-t-oc20": dict(variant="gemnet-style", blocks=4, d_u=128, d_v=128, d_e=128, d_t=64, d_bil=64,
+                          k_rbf=6, l_sbf=7, cutoff=6.0, atoms=80, density=0.06, graphs=32, w_forces=1.0),
+    # BASELINE configs[0] (the reference's own CPU-runnable case)
+    "dimenet-pp-small": dict(variant="dimenet-style", blocks=4, d_u=128, d_v=128, d_e=128, d_t=64, d_bil=64,
+                             k_rbf=6, l_sbf=7, cutoff=6.0, atoms=64, density=0.06, graphs=4, w_forces=0.0),
+}
+
+
+def _args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="gemnet-t-oc20")
+    ap.add_argument("--graphs", type=int, default=None, help="override graphs per GPU")
+    ap.add_argument("--cpu-budget", type=float, default=12.0, help="seconds of CPU oracle sampling")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def _config(wl):
+    from paper_2203_09697_b200 import ModelConfig
+
+    keys = ("variant", "blocks", "d_u", "d_v", "d_e", "d_t", "d_bil", "k_rbf", "l_sbf", "cutoff")
+    return ModelConfig(**{k: wl[k] for k in keys}, seed=0)
+
+
+def _systems(wl, graphs, rank=0):
+    from paper_2203_09697_b200.system import random_cloud
+
+    base = 1000 * rank
+    return [random_cloud(wl["atoms"], wl["density"], np.random.default_rng(base + s)) for s in range(graphs)]
+
+
+# ---------------------------------------------------------------------------
+# clocks sampled during the timed region
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax = float(parts[1])
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[4:8]):
+                if val.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# CPU reference (fp64 numpy oracle, restatement of egn.ModelTape)
+# ---------------------------------------------------------------------------
+def cpu_reference(wl, systems, budget_s, min_graphs=1):
+    from oracle import egn_oracle as O
+
+    cfg = _config(wl)
+    oc = O.Config(**{k: getattr(cfg, k) for k in O.Config.__dataclass_fields__})
+    params = O.init_params(oc)
+    trip, secs, done = 0, 0.0, 0
+    for i, s in enumerate(systems):
+        g = O.build_graph(s.positions, oc.cutoff)  # graph build excluded (egn/bench.py:294-296)
+        t0 = time.perf_counter()
+        fw = O.forward(oc, params, s.positions, s.atomic_numbers, graph=g)
+        d_f = np.zeros_like(s.positions) if wl["w_forces"] else None
+        O.backward(fw, params, 1.0, d_f)
+        secs += time.perf_counter() - t0
+        trip += g.trip_in.size * oc.blocks
+        done += 1
+        if done >= min_graphs and secs >= budget_s:
+            break
+    return {"triplets_per_s": trip / secs, "graphs": done, "seconds": secs,
+            "sec_per_graph": secs / done}
+
+
+def run_reference(args, wl):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    graphs = args.graphs or wl["graphs"]
+    systems = _systems(wl, graphs)
+    cores = os.cpu_count()
+    # each step = one graph of the batch, forward + backward (bounded sample)
+    for i in range(args.warmup):
+        cpu_reference(wl, [systems[i % graphs]], 0.0)
+    trip, secs = 0.0, 0.0
+    for i in range(args.steps):
+        r = cpu_reference(wl, [systems[(args.warmup + i) % graphs]], 0.0)
+        trip += r["triplets_per_s"] * r["seconds"]
+        secs += r["seconds"]
+    value = trip / secs
+    ms_graph = 1000 * secs / args.steps
+    line = {
+        "impl": "reference", "metric": "triplet-interactions/s (train step, fwd+bwd)", "value": value,
+        "unit": "triplets/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms_graph * graphs, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic",
+        "config": {"workload": args.workload, "variant": wl["variant"], "graphs": graphs, "atoms": wl["atoms"],
+                   "cutoff": wl["cutoff"], "sample": "one graph of the batch per step"},
+        "cpu_baseline": {"value": value, "unit": "triplets/s", "cores": cores, "kind": "port",
+                         "sample": f"{args.steps} graphs x fwd+bwd of the {graphs}-graph batch"},
+        "e2e": {"value": value, "unit": "triplets/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "steps_per_s": 1.0 / (ms_graph * graphs / 1000.0),
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# GPU path
+# ---------------------------------------------------------------------------
+def _time_kernel(fn, iters, flush):
+    import torch
+
+    times = []
+    for _ in range(iters):
+        flush.zero_()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        fn()
+        e.record()
+        torch.cuda.synchronize()
+        times.append(s.elapsed_time(e) / 1000.0)
+    return float(np.median(times))
+
+
+def run_ours(args, wl):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2203_09697_b200 import _lib, init_params, ops
+    from paper_2203_09697_b200.engine import DeviceWeights, Engine
+    from paper_2203_09697_b200.graph import build_batch
+    from paper_2203_09697_b200.tasks import Trainer
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cfg = _config(wl)
+    graphs = args.graphs or wl["graphs"]
+    systems = _systems(wl, graphs, rank)
+    params = init_params(cfg)
+    teacher = Engine(DeviceWeights.from_params(init_params(cfg.replace(seed=1))))
+    bg = build_batch(systems, cfg.cutoff)
+    tf = teacher.forward(bg)
+    e_t = tf.energy.double()
+    if wl["w_forces"]:
+        f_t = tf.forces.double()
+    else:
+        f_t = None
+    del tf, teacher
+    tr = Trainer(params, None, e_t.cpu().numpy(), None if f_t is None else f_t.cpu().numpy(),
+                 1.0, wl["w_forces"], graph=bg)
+    lr = 1e-5
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        tr.step(lr)
+    torch.cuda.synchronize()
+    barrier()
+    clocks = ClockSampler(torch.cuda.current_device())
+    clocks.start()
+    time.sleep(0.3)
+    _lib.LAUNCH_COUNTER.update(calls=0, kernels=0)
+    st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    st.record()
+    for _ in range(args.steps):
+        loss = tr.step(lr)
+    en.record()
+    torch.cuda.synchronize()
+    t_dev = st.elapsed_time(en) / 1000.0 / args.steps
+    launches = _lib.LAUNCH_COUNTER["kernels"] // args.steps
+    # ---- end to end: host buffers -> device -> step -> loss back to host
+    pos_host = torch.from_numpy(np.concatenate([s.positions for s in systems])).pin_memory()
+    et_host = e_t.cpu().pin_memory()
+    ft_host = f_t.cpu().pin_memory() if f_t is not None else None
+    h2d = pos_host.numel() * 8 + et_host.numel() * 8 + (ft_host.numel() * 8 if ft_host is not None else 0)
+    sizes = [s.positions.shape[0] for s in systems]
+
+    def e2e_step():
+        pos = pos_host.to("cuda", non_blocking=True)
+        et = et_host.to("cuda", non_blocking=True)
+        ft = ft_host.to("cuda", non_blocking=True) if ft_host is not None else None
+        g = build_batch(None, cfg.cutoff, positions=pos, sizes=sizes)
+        tr.set_inputs(g, et, ft)
+        return float(tr.step(lr))
+
+    for _ in range(2):
+        e2e_step()
+    torch.cuda.synchronize()
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        e2e_step()
+    t_e2e = (time.perf_counter() - t0) / args.steps
+    clk = clocks.stop()
+
+    # max over ranks
+    tt = torch.tensor([t_dev, t_e2e], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    t_dev, t_e2e = float(tt[0]), float(tt[1])
+    trip_rank = bg.num_triplets * cfg.blocks
+    total_trip = trip_rank * world
+    value = total_trip / t_dev
+
+    # ---- roofline of the triplet-interaction kernels (block 0 operands)
+    fw = tr.engine.forward(bg)
+    st0 = fw.blocks[0]
+    dg = cfg.triplet_width
+    S_bar = torch.randn_like(st0["S"])
+    eg = torch.zeros((bg.num_edges, 4), device="cuda")
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")  # 256 MB > L2
+    t_f = _time_kernel(lambda: ops.triplet_fwd(bg.edge_ptr, bg.rev, bg.geo, st0["X"], st0["Wk"], cfg.cutoff),
+                       20, flush)
+    t_b = _time_kernel(lambda: ops.triplet_bwd(bg.edge_ptr, bg.rev, bg.geo, st0["X"], st0["Wk"], cfg.cutoff,
+                                               S_bar, eg), 20, flush)
+    ne, nt = bg.num_edges, bg.num_triplets
+    b_fwd = 12 * nt + (8 * dg + 4) * ne
+    b_bwd = 16 * nt + (12 * dg + 8) * ne
+    peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
+    hbm = peaks.get("hbm_gbs", 6650.0)
+    fma_flops_fwd = 2.0 * nt * cfg.l_sbf * dg
+    dominant = "triplet_bwd" if t_b >= t_f else "triplet_fwd"
+    ach = (b_bwd / t_b if dominant == "triplet_bwd" else b_fwd / t_f) / 1e9
+    roof = {"bound": "hbm", "kernel": dominant, "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
+            "traffic": None, "peak_source": "MEASURED_PEAKS.json" if peaks else "fallback",
+            "triplet_fwd_us": t_f * 1e6, "triplet_bwd_us": t_b * 1e6,
+            "triplet_fwd_gtrip_s": nt / t_f / 1e9, "triplet_bwd_gtrip_s": nt / t_b / 1e9,
+            "triplet_fwd_fp32_tflops": fma_flops_fwd / t_f / 1e12,
+            "algorithmic_bytes": {"fwd": b_fwd, "bwd": b_bwd}}
+
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        r = cpu_reference(wl, systems, args.cpu_budget)
+        cpu = {"value": r["triplets_per_s"], "unit": "triplets/s", "cores": os.cpu_count(), "kind": "port",
+               "sample": f"{r['graphs']} graph(s) of the batch, fwd+bwd, fp64 numpy oracle, {r['seconds']:.1f}s"}
+    if rank == 0:
+        line = {
+            "metric": "triplet-interactions/s (train step, fwd+bwd+SGD)", "value": value, "unit": "triplets/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_dev * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (random_cloud OC20-density graphs, random-init weights, teacher targets)",
+            "config": {"workload": args.workload, "variant": wl["variant"], "graphs_per_gpu": graphs,
+                       "atoms_per_graph": wl["atoms"], "cutoff": wl["cutoff"], "blocks": cfg.blocks,
+                       "d_e": cfg.d_e, "d_t": cfg.d_t, "d_bil": cfg.d_bil, "edges_per_gpu": bg.num_edges,
+                       "triplets_per_gpu": nt, "parallelism": f"replicas{world}" if world > 1 else "single",
+                       "l2": "step working set > L2 (126 MB); kernel timings flush L2 with a 256 MB write"},
+            "steps_per_s": 1.0 / t_dev,
+            "e2e": {"value": total_trip / t_e2e, "unit": "triplets/s", "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": 8, "ms_per_step": t_e2e * 1e3},
+            "gpu_launches": launches,
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "clocks": clk,
+            "loss": float(loss),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = _args()
+    wl = WORKLOADS[args.workload]
+    if args.impl == "reference":
+        run_reference(args, wl)
+    else:
+        run_ours(args, wl)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,189 @@
+/*
+ * egn_b200.h -- C ABI of the B200-native EGN (DimeNet++/GemNet-T) hot path.
+ *
+ * Every entry point takes raw device pointers, element counts and a CUDA
+ * stream (passed as void*), launches its kernels on that stream and returns
+ * 0 on success or a nonzero status; egn_last_error() then returns a
+ * thread-local message.  Outputs are caller-allocated; nothing here
+ * allocates device memory.  There is no CPU fallback: every call launches
+ * sm_100a kernels.
+ *
+ * Reference interfaces replaced (paths relative to /root/reference/pkg/src):
+ * each declaration names the egn function (file:line) whose array result it
+ * produces.  Index conventions:
+ *   - edges are sorted by (source, receiver) inside each graph and graphs
+ *     are concatenated (graph.py:93 row-major nonzero);
+ *   - edge_ptr[V+1] is the CSR of out-edges by source node;
+ *   - triplets of centre atom j occupy the contiguous range
+ *     [tri_ptr[j], tri_ptr[j+1]) with tri_ptr[j+1]-tri_ptr[j] = deg(j)(deg(j)-1),
+ *     ordered by (out-edge, in-edge) exactly as enumerate_triplets
+ *     (graph.py:106-139) orders them.
+ */
+#ifndef EGN_B200_H
+#define EGN_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef void* egn_stream_t; /* cudaStream_t */
+
+/* Thread-local description of the last failure (never NULL). */
+const char* egn_last_error(void);
+/* ABI version (bumped on any signature change). */
+int egn_abi_version(void);
+
+/* ------------------------------------------------------------------ */
+/* Graph construction: build_graph (graph.py:82-103)                   */
+/* ------------------------------------------------------------------ */
+
+/* Out-degree of every node: count of b in the node's graph with
+ * 0 < |x_b - x_a| <= cutoff, distances in fp64 as ((dx*dx+dy*dy)+dz*dz)
+ * without FMA contraction (graph.py:89-92).  node_graph[a] is a's graph;
+ * graph_ptr[G+1] the node offsets. */
+int egn_neighbors_count(const double* pos, const int64_t* graph_ptr, const int32_t* node_graph,
+                        int64_t num_nodes, double cutoff, int32_t* deg, egn_stream_t stream);
+
+/* Exclusive scan out[0]=0, out[i+1]=out[i]+in[i] (int32 in, int64 out, n+1 outputs).
+ * If square_minus_one is nonzero, scans in[i]*(in[i]-1) instead (triplet
+ * offsets tri_ptr from out-degrees, graph.py:124-139). */
+int egn_scan_counts(const int32_t* in, int64_t n, int square_minus_one, int64_t* out,
+                    egn_stream_t stream);
+
+/* Fill src/recv of every edge, row-major order (graph.py:93); edge_ptr from
+ * egn_scan_counts(deg). */
+int egn_neighbors_fill(const double* pos, const int64_t* graph_ptr, const int32_t* node_graph,
+                       int64_t num_nodes, double cutoff, const int64_t* edge_ptr, int32_t* src,
+                       int32_t* recv, egn_stream_t stream);
+
+/* rev[e] = index of the edge (recv_e, src_e)  (GraphTopology.reverse_edges,
+ * graph.py:40-55).  *missing (device int32) receives the count of edges
+ * without a reverse partner. */
+int egn_reverse_edges(const int64_t* edge_ptr, const int32_t* src, const int32_t* recv,
+                      int64_t num_edges, int32_t* rev, int32_t* missing, egn_stream_t stream);
+
+/* Materialise id3_kj (trip_in) and id3_ji (trip_out) as int64 (enumerate_triplets,
+ * graph.py:106-139); tri_ptr from egn_scan_counts(deg, square_minus_one=1). */
+int egn_triplets_fill(const int64_t* edge_ptr, const int32_t* rev, const int64_t* tri_ptr,
+                      int64_t num_nodes, int64_t* id3_kj, int64_t* id3_ji, egn_stream_t stream);
+
+/* Per-edge geometry (edge_distances / edge_unit_vectors, graph.py:142-150).
+ * geo[e] = (ux, uy, uz, d) in fp32 (the model's packed layout); dist64 [E]
+ * and unit64 [E,3] optional (NULL to skip) in fp64. */
+int egn_geometry(const double* pos, const int32_t* src, const int32_t* recv, int64_t num_edges,
+                 float* geo, double* dist64, double* unit64, egn_stream_t stream);
+
+/* Triplet angles atan2(|v1 x v2|, v1.v2) in fp64 (triplet_angles, graph.py:162-170). */
+int egn_triplet_angles(const double* pos, const int64_t* edge_ptr, const int32_t* recv,
+                       const int64_t* tri_ptr, int64_t num_nodes, double* angles,
+                       egn_stream_t stream);
+
+/* ------------------------------------------------------------------ */
+/* Basis: rbf_features / rbf_features_ddist (basis.py:35-51)           */
+/* ------------------------------------------------------------------ */
+
+/* rbf[e,k] = exp(-gamma (d_e - c_k)^2), c = linspace(0, cutoff, K) (c=[0] if K=1),
+ * gamma = (K/cutoff)^2; fp32 [E,K]. */
+int egn_rbf(const float* geo, int64_t num_edges, int k_rbf, double cutoff, float* rbf,
+            egn_stream_t stream);
+
+/* SBF rows (t, k*L+l) = rbf_k(d_kj) cos(l alpha_t) for every triplet (sbf_features,
+ * basis.py:54-73), fp32 [N_t, K*L].  Debug/parity only: the model never
+ * materialises per-triplet basis rows. */
+int egn_sbf(const float* geo, const int64_t* edge_ptr, const int64_t* tri_ptr, int64_t num_nodes,
+            int k_rbf, int l_sbf, double cutoff, float* sbf, egn_stream_t stream);
+
+/* ------------------------------------------------------------------ */
+/* Triplet interaction: record_tu (engine.py:118-149)                  */
+/* ------------------------------------------------------------------ */
+/*
+ * With rq = rev(off_j + q) the in-edge (k->j) of centre j and x_pq = u_p . u_q
+ * (= cos alpha of triplet (q -> p)):
+ *   S[off_j+p, c] = sum_{q != p} X[rq, c] * sum_l T_l(x_pq) * Rw[rq, l, c],
+ *   Rw[e, l, c]   = sum_k rbf_k(d_e) * W[k, l, c].
+ * X is the per-edge down projection (dimenet: m W_down^T; gemnet:
+ * m W_down^T A^T), W the sbf gate reshaped to [K, L, dg] (gemnet: B W_sbf).
+ * The gate by rbf(d_ji) and the up projection are applied by the caller on
+ * the per-edge result, which is exact because both are constant or linear
+ * inside a triplet segment (engine.py:138,147-148).
+ */
+int egn_triplet_fwd(const int64_t* edge_ptr, const int32_t* rev, const float* geo,
+                    int64_t num_nodes, const float* X, const float* W, int k_rbf, int l_sbf,
+                    int dg, double cutoff, float* S, egn_stream_t stream);
+
+/* Adjoint of egn_triplet_fwd (tape.py gather/segment_sum/linear/angular_sbf VJPs).
+ * Inputs S_bar [E,dg].  Outputs:
+ *   X_bar [E, dg]            (overwritten),
+ *   W_bar [K, L, dg]          (overwritten; reduced over all centres),
+ *   edge_grad [E, 4] float   (+=): (dE/dv_e (3), dE/dd_e) for the edge
+ *                              vector v_e = x_recv - x_src from the angles and the
+ *                              in-edge distance of the basis.
+ * workspace: egn_triplet_bwd_workspace_bytes(...) bytes of device memory. */
+int64_t egn_triplet_bwd_workspace_bytes(int64_t num_nodes, int k_rbf, int l_sbf, int dg);
+int egn_triplet_bwd(const int64_t* edge_ptr, const int32_t* rev, const float* geo,
+                    int64_t num_nodes, const float* X, const float* W, int k_rbf, int l_sbf,
+                    int dg, double cutoff, const float* S_bar, float* X_bar, float* W_bar,
+                    float* edge_grad, void* workspace, egn_stream_t stream);
+
+/* Per-triplet feature debug output t_feat-like rows for parity tests:
+ * P[t, c] = X[rq, c] * sum_l T_l(x_pq) Rw[rq, l, c] for every triplet t in
+ * (out, in) order (the summand of egn_triplet_fwd). */
+int egn_triplet_terms(const int64_t* edge_ptr, const int32_t* rev, const float* geo,
+                      const int64_t* tri_ptr, int64_t num_nodes, const float* X, const float* W,
+                      int k_rbf, int l_sbf, int dg, double cutoff, float* P, egn_stream_t stream);
+
+/* ------------------------------------------------------------------ */
+/* Edge/node aggregation: segment_sum / gather (tape.py:129-154)       */
+/* ------------------------------------------------------------------ */
+
+/* out[v, c] = sum over in-edges e of v (recv(e) = v, ascending e) of x[e, c];
+ * in-edges of v are rev(out-edges of v).  (record_ea_nu, engine.py:166-177) */
+int egn_aggregate_in_edges(const int64_t* edge_ptr, const int32_t* rev, int64_t num_nodes,
+                           const float* x, int64_t ld_x, int d, float* out, egn_stream_t stream);
+
+/* out[e, c] (+)= x[idx[e], c]: row gather with optional accumulate (gather, tape.py:129-139). */
+int egn_gather_rows(const int32_t* idx, int64_t rows, const float* x, int64_t ld_x, int d,
+                    float* out, int64_t ld_out, int accumulate, egn_stream_t stream);
+
+/* out[g, c] = sum_{v in graph g} x[v, c]  (sum_rows in record_gu_head, engine.py:207-211). */
+int egn_graph_sum(const int64_t* graph_ptr, int64_t num_graphs, const float* x, int d,
+                  float* out, egn_stream_t stream);
+
+/* GemNet direct force head (record_force_head, engine.py:234-246):
+ *   s_e = m_e . w ; f[v] = sum_{recv(e)=v} s_e u_e.  scale [E] is an output. */
+int egn_force_head_fwd(const int64_t* edge_ptr, const int32_t* rev, const float* geo,
+                       int64_t num_nodes, int64_t num_edges, const float* m, int d,
+                       const float* w, float* scale, float* forces, egn_stream_t stream);
+/* Adjoint: m_bar[e] += (f_bar[recv e] . u_e) w ; edge_grad[e].xyz += unit-vector adjoint
+ * (tape.py:197-209 edge_units VJP folded into dE/dv_e); w_bar_partial [blocks, d]. */
+int egn_force_head_bwd(const int32_t* recv, const float* geo, int64_t num_edges, const float* m,
+                       int d, const float* w, const float* scale, const float* f_bar,
+                       float* m_bar, float* w_bar, float* edge_grad, void* workspace,
+                       egn_stream_t stream);
+int64_t egn_force_head_bwd_workspace_bytes(int64_t num_edges, int d);
+
+/* ------------------------------------------------------------------ */
+/* Geometry adjoints (tape.py:164-242, runtime.py:626-671)             */
+/* ------------------------------------------------------------------ */
+
+/* edge_grad[e].w += sum_k rbf_bar[e,k] d rbf_k/dd (gaussian_rbf VJP, tape.py:219-228). */
+int egn_rbf_bwd(const float* geo, const float* rbf_bar, int64_t num_edges, int k_rbf,
+                double cutoff, float* edge_grad, egn_stream_t stream);
+
+/* pos_bar[a] = sum_{recv(e)=a} g_e - sum_{src(e)=a} g_e with
+ * g_e = edge_grad[e].xyz + edge_grad[e].w * u_e  (fp64 output). */
+int egn_positions_bwd(const int64_t* edge_ptr, const int32_t* rev, const float* geo,
+                      int64_t num_nodes, const float* edge_grad, double* pos_bar,
+                      egn_stream_t stream);
+
+/* ------------------------------------------------------------------ */
+/* Optimizer: train_simple SGD update (tasks.py:207-208)               */
+/* ------------------------------------------------------------------ */
+int egn_sgd(float* w, const float* g, int64_t n, float lr, egn_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* EGN_B200_H */

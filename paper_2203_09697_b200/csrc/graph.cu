@@ -1,0 +1,303 @@
+// Graph construction kernels: neighbour list, CSR scans, reverse edges,
+// triplet index materialisation and per-edge geometry.
+//
+// Reference: egn/graph.py (build_graph :82-103, enumerate_triplets :106-139,
+// reverse_edges :40-55, edge_distances/units :142-150, triplet_angles
+// :162-170).  The neighbour test is evaluated in fp64 with explicit
+// round-to-nearest intrinsics so that no FMA contraction changes a
+// distance by one ulp: d = sqrt((dx*dx + dy*dy) + dz*dz) exactly as numpy
+// evaluates (diff*diff).sum(axis=2); the edge set and its order are then
+// bit-identical to the reference's row-major np.nonzero.
+#include <cstdarg>
+#include <cstdio>
+
+#include "common.cuh"
+
+namespace egn {
+
+static thread_local char g_err[512] = "no error";
+
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+__device__ __forceinline__ double pair_dist(const double* __restrict__ pos, int64_t a, int64_t b) {
+  // diff = pos[b] - pos[a]   (graph.py:88: pos[None,:,:] - pos[:,None,:])
+  double dx = __dsub_rn(pos[3 * b + 0], pos[3 * a + 0]);
+  double dy = __dsub_rn(pos[3 * b + 1], pos[3 * a + 1]);
+  double dz = __dsub_rn(pos[3 * b + 2], pos[3 * a + 2]);
+  double s = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
+  return __dsqrt_rn(s);
+}
+
+// One warp per source atom a; lanes sweep the atoms of a's graph.
+__global__ void neighbors_count_kernel(const double* __restrict__ pos,
+                                       const int64_t* __restrict__ graph_ptr,
+                                       const int32_t* __restrict__ node_graph, int64_t n,
+                                       double cutoff, int32_t* __restrict__ deg) {
+  int lane = threadIdx.x & 31;
+  int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t a = warp; a < n; a += nwarps) {
+    int g = node_graph[a];
+    int64_t b0 = graph_ptr[g], b1 = graph_ptr[g + 1];
+    int count = 0;
+    for (int64_t b = b0 + lane; b < b1; b += 32) {
+      double d = pair_dist(pos, a, b);
+      count += (b != a) && (d > 0.0) && (d <= cutoff);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) count += __shfl_xor_sync(0xffffffffu, count, o);
+    if (lane == 0) deg[a] = count;
+  }
+}
+
+__global__ void neighbors_fill_kernel(const double* __restrict__ pos,
+                                      const int64_t* __restrict__ graph_ptr,
+                                      const int32_t* __restrict__ node_graph, int64_t n,
+                                      double cutoff, const int64_t* __restrict__ edge_ptr,
+                                      int32_t* __restrict__ src, int32_t* __restrict__ recv) {
+  int lane = threadIdx.x & 31;
+  int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t a = warp; a < n; a += nwarps) {
+    int g = node_graph[a];
+    int64_t b0 = graph_ptr[g], b1 = graph_ptr[g + 1];
+    int64_t out = edge_ptr[a];
+    for (int64_t base = b0; base < b1; base += 32) {
+      int64_t b = base + lane;
+      bool hit = false;
+      if (b < b1) {
+        double d = pair_dist(pos, a, b);
+        hit = (b != a) && (d > 0.0) && (d <= cutoff);
+      }
+      unsigned mask = __ballot_sync(0xffffffffu, hit);
+      if (hit) {
+        int64_t slot = out + __popc(mask & ((1u << lane) - 1u));
+        src[slot] = static_cast<int32_t>(a);
+        recv[slot] = static_cast<int32_t>(b);
+      }
+      out += __popc(mask);
+    }
+  }
+}
+
+// Single-CTA exclusive scan (n+1 outputs).  Graph-construction sizes
+// (nodes <= ~10^6) make one 1024-thread CTA sufficient.
+__global__ void scan_counts_kernel(const int32_t* __restrict__ in, int64_t n, int sq,
+                                   int64_t* __restrict__ out) {
+  __shared__ int64_t warp_tot[32];
+  __shared__ int64_t carry;
+  int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  if (tid == 0) carry = 0;
+  __syncthreads();
+  for (int64_t base = 0; base < n; base += blockDim.x) {
+    int64_t i = base + tid;
+    int64_t v = 0;
+    if (i < n) {
+      int64_t x = in[i];
+      v = sq ? x * (x - 1) : x;
+    }
+    int64_t incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int64_t y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (lane == 31) warp_tot[wid] = incl;
+    __syncthreads();
+    if (wid == 0) {
+      int64_t t = lane < (blockDim.x >> 5) ? warp_tot[lane] : 0;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        int64_t y = __shfl_up_sync(0xffffffffu, t, o);
+        if (lane >= o) t += y;
+      }
+      warp_tot[lane] = t;  // inclusive prefix of warp totals
+    }
+    __syncthreads();
+    int64_t before = carry + (wid > 0 ? warp_tot[wid - 1] : 0);
+    if (i < n) out[i] = before + incl - v;
+    __syncthreads();
+    if (tid == blockDim.x - 1) carry = before + incl;
+    __syncthreads();
+  }
+  if (tid == 0) out[n] = carry;
+}
+
+// rev[e]: binary search for src(e) among the receivers of recv(e)'s row.
+__global__ void reverse_edges_kernel(const int64_t* __restrict__ edge_ptr,
+                                     const int32_t* __restrict__ src,
+                                     const int32_t* __restrict__ recv, int64_t ne,
+                                     int32_t* __restrict__ rev, int32_t* __restrict__ missing) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < ne;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    int32_t a = src[e], b = recv[e];
+    int64_t lo = edge_ptr[b], hi = edge_ptr[b + 1];
+    while (lo < hi) {
+      int64_t mid = (lo + hi) >> 1;
+      if (recv[mid] < a) lo = mid + 1; else hi = mid;
+    }
+    if (lo < edge_ptr[b + 1] && recv[lo] == a) {
+      rev[e] = static_cast<int32_t>(lo);
+    } else {
+      rev[e] = -1;
+      atomicAdd(missing, 1);
+    }
+  }
+}
+
+// One CTA per centre j: triplet (p, q), q != p, lives at
+// tri_ptr[j] + p*(n-1) + (q < p ? q : q-1); id3_ji = off+p, id3_kj = rev[off+q].
+__global__ void triplets_fill_kernel(const int64_t* __restrict__ edge_ptr,
+                                     const int32_t* __restrict__ rev,
+                                     const int64_t* __restrict__ tri_ptr, int64_t nv,
+                                     int64_t* __restrict__ id3_kj, int64_t* __restrict__ id3_ji) {
+  for (int64_t j = blockIdx.x; j < nv; j += gridDim.x) {
+    int64_t off = edge_ptr[j];
+    int64_t n = edge_ptr[j + 1] - off;
+    if (n < 2) continue;
+    int64_t t0 = tri_ptr[j];
+    int64_t cnt = n * (n - 1);
+    for (int64_t k = threadIdx.x; k < cnt; k += blockDim.x) {
+      int64_t p = k / (n - 1);
+      int64_t r = k - p * (n - 1);
+      int64_t q = r < p ? r : r + 1;
+      id3_ji[t0 + k] = off + p;
+      id3_kj[t0 + k] = rev[off + q];
+    }
+  }
+}
+
+__global__ void geometry_kernel(const double* __restrict__ pos, const int32_t* __restrict__ src,
+                                const int32_t* __restrict__ recv, int64_t ne,
+                                float4* __restrict__ geo, double* __restrict__ dist64,
+                                double* __restrict__ unit64) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < ne;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t a = src[e], b = recv[e];
+    double dx = __dsub_rn(pos[3 * b + 0], pos[3 * a + 0]);
+    double dy = __dsub_rn(pos[3 * b + 1], pos[3 * a + 1]);
+    double dz = __dsub_rn(pos[3 * b + 2], pos[3 * a + 2]);
+    double d = __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz)));
+    double ux = __ddiv_rn(dx, d), uy = __ddiv_rn(dy, d), uz = __ddiv_rn(dz, d);
+    geo[e] = make_float4(static_cast<float>(ux), static_cast<float>(uy), static_cast<float>(uz),
+                         static_cast<float>(d));
+    if (dist64) dist64[e] = d;
+    if (unit64) {
+      unit64[3 * e + 0] = ux;
+      unit64[3 * e + 1] = uy;
+      unit64[3 * e + 2] = uz;
+    }
+  }
+}
+
+// Angle of triplet (q -> p) at centre j: v1 = x_k - x_j (edge off+q),
+// v2 = x_i - x_j (edge off+p); atan2(|v1 x v2|, v1 . v2) in fp64.
+__global__ void triplet_angles_kernel(const double* __restrict__ pos,
+                                      const int64_t* __restrict__ edge_ptr,
+                                      const int32_t* __restrict__ recv,
+                                      const int64_t* __restrict__ tri_ptr, int64_t nv,
+                                      double* __restrict__ angles) {
+  for (int64_t j = blockIdx.x; j < nv; j += gridDim.x) {
+    int64_t off = edge_ptr[j];
+    int64_t n = edge_ptr[j + 1] - off;
+    if (n < 2) continue;
+    int64_t t0 = tri_ptr[j];
+    int64_t cnt = n * (n - 1);
+    double xj = pos[3 * j], yj = pos[3 * j + 1], zj = pos[3 * j + 2];
+    for (int64_t k = threadIdx.x; k < cnt; k += blockDim.x) {
+      int64_t p = k / (n - 1);
+      int64_t r = k - p * (n - 1);
+      int64_t q = r < p ? r : r + 1;
+      int64_t kk = recv[off + q], ii = recv[off + p];
+      double v1x = pos[3 * kk] - xj, v1y = pos[3 * kk + 1] - yj, v1z = pos[3 * kk + 2] - zj;
+      double v2x = pos[3 * ii] - xj, v2y = pos[3 * ii + 1] - yj, v2z = pos[3 * ii + 2] - zj;
+      double cx = __dsub_rn(__dmul_rn(v1y, v2z), __dmul_rn(v1z, v2y));
+      double cy = __dsub_rn(__dmul_rn(v1z, v2x), __dmul_rn(v1x, v2z));
+      double cz = __dsub_rn(__dmul_rn(v1x, v2y), __dmul_rn(v1y, v2x));
+      double s = __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(cx, cx), __dmul_rn(cy, cy)), __dmul_rn(cz, cz)));
+      double c = __dadd_rn(__dadd_rn(__dmul_rn(v1x, v2x), __dmul_rn(v1y, v2y)), __dmul_rn(v1z, v2z));
+      angles[t0 + k] = atan2(s, c);
+    }
+  }
+}
+
+}  // namespace egn
+
+using namespace egn;
+
+extern "C" {
+
+const char* egn_last_error(void) { return g_err; }
+int egn_abi_version(void) { return 1; }
+
+int egn_neighbors_count(const double* pos, const int64_t* graph_ptr, const int32_t* node_graph,
+                        int64_t num_nodes, double cutoff, int32_t* deg, egn_stream_t stream) {
+  EGN_REQUIRE(cutoff > 0, "cutoff must be positive");
+  if (num_nodes == 0) return 0;
+  int threads = 256;
+  int grid = grid_for(num_nodes * 32, threads);
+  neighbors_count_kernel<<<grid, threads, 0, as_stream(stream)>>>(pos, graph_ptr, node_graph,
+                                                                  num_nodes, cutoff, deg);
+  return check_launch("neighbors_count");
+}
+
+int egn_scan_counts(const int32_t* in, int64_t n, int square_minus_one, int64_t* out,
+                    egn_stream_t stream) {
+  scan_counts_kernel<<<1, 1024, 0, as_stream(stream)>>>(in, n, square_minus_one, out);
+  return check_launch("scan_counts");
+}
+
+int egn_neighbors_fill(const double* pos, const int64_t* graph_ptr, const int32_t* node_graph,
+                       int64_t num_nodes, double cutoff, const int64_t* edge_ptr, int32_t* src,
+                       int32_t* recv, egn_stream_t stream) {
+  if (num_nodes == 0) return 0;
+  int threads = 256;
+  int grid = grid_for(num_nodes * 32, threads);
+  neighbors_fill_kernel<<<grid, threads, 0, as_stream(stream)>>>(
+      pos, graph_ptr, node_graph, num_nodes, cutoff, edge_ptr, src, recv);
+  return check_launch("neighbors_fill");
+}
+
+int egn_reverse_edges(const int64_t* edge_ptr, const int32_t* src, const int32_t* recv,
+                      int64_t num_edges, int32_t* rev, int32_t* missing, egn_stream_t stream) {
+  if (num_edges == 0) return 0;
+  int threads = 256;
+  reverse_edges_kernel<<<grid_for(num_edges, threads), threads, 0, as_stream(stream)>>>(
+      edge_ptr, src, recv, num_edges, rev, missing);
+  return check_launch("reverse_edges");
+}
+
+int egn_triplets_fill(const int64_t* edge_ptr, const int32_t* rev, const int64_t* tri_ptr,
+                      int64_t num_nodes, int64_t* id3_kj, int64_t* id3_ji, egn_stream_t stream) {
+  if (num_nodes == 0) return 0;
+  int grid = static_cast<int>(num_nodes < 65535 ? num_nodes : 65535);
+  triplets_fill_kernel<<<grid, 256, 0, as_stream(stream)>>>(edge_ptr, rev, tri_ptr, num_nodes,
+                                                            id3_kj, id3_ji);
+  return check_launch("triplets_fill");
+}
+
+int egn_geometry(const double* pos, const int32_t* src, const int32_t* recv, int64_t num_edges,
+                 float* geo, double* dist64, double* unit64, egn_stream_t stream) {
+  if (num_edges == 0) return 0;
+  int threads = 256;
+  geometry_kernel<<<grid_for(num_edges, threads), threads, 0, as_stream(stream)>>>(
+      pos, src, recv, num_edges, reinterpret_cast<float4*>(geo), dist64, unit64);
+  return check_launch("geometry");
+}
+
+int egn_triplet_angles(const double* pos, const int64_t* edge_ptr, const int32_t* recv,
+                       const int64_t* tri_ptr, int64_t num_nodes, double* angles,
+                       egn_stream_t stream) {
+  if (num_nodes == 0) return 0;
+  int grid = static_cast<int>(num_nodes < 65535 ? num_nodes : 65535);
+  triplet_angles_kernel<<<grid, 256, 0, as_stream(stream)>>>(pos, edge_ptr, recv, tri_ptr,
+                                                             num_nodes, angles);
+  return check_launch("triplet_angles");
+}
+
+}  // extern "C"

@@ -1,0 +1,376 @@
+// Edge/node aggregation, basis, force head, geometry adjoints and the SGD
+// update.  All reductions are gather-form over sorted CSR rows (no global
+// atomics), so results are deterministic and match the reference's
+// ascending-edge accumulation order (receiver_plan, engine.py:78-90).
+#include <algorithm>
+
+#include "common.cuh"
+
+namespace egn {
+
+// ---------------------------------------------------------------- basis
+__global__ void rbf_kernel(const float4* __restrict__ geo, int64_t ne, int K, RbfParams rp,
+                           float* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < ne * K;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t e = i / K;
+    int k = static_cast<int>(i - e * K);
+    float dd = geo[e].w - rp.step * k;
+    out[i] = __expf(-rp.gamma * dd * dd);
+  }
+}
+
+// SBF rows for every triplet (debug / parity): (t, k*L+l) = rbf_k(d_q) T_l(x_pq).
+__global__ void sbf_kernel(const float4* __restrict__ geo, const int64_t* __restrict__ edge_ptr,
+                           const int64_t* __restrict__ tri_ptr, int64_t nv, int K, int L,
+                           RbfParams rp, float* __restrict__ out) {
+  for (int64_t j = blockIdx.x; j < nv; j += gridDim.x) {
+    int64_t off = edge_ptr[j];
+    int64_t n = edge_ptr[j + 1] - off;
+    if (n < 2) continue;
+    int64_t t0 = tri_ptr[j];
+    for (int64_t k = threadIdx.x; k < n * (n - 1); k += blockDim.x) {
+      int64_t p = k / (n - 1);
+      int64_t r = k - p * (n - 1);
+      int64_t q = r < p ? r : r + 1;
+      float4 a = geo[off + p], b = geo[off + q];
+      float x = a.x * b.x + a.y * b.y + a.z * b.z;
+      float* row = out + (t0 + k) * K * L;
+      for (int kk = 0; kk < K; ++kk) {
+        float dd = b.w - rp.step * kk;
+        float rb = __expf(-rp.gamma * dd * dd);
+        float tc = 1.f, tp = x;
+        for (int l = 0; l < L; ++l) {
+          row[kk * L + l] = rb * tc;
+          float tn = 2.f * x * tc - tp;
+          tp = tc;
+          tc = tn;
+        }
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------- aggregation
+// One warp per node; lanes over channels; in-edges of v are rev(out-edges of v)
+// in ascending edge order.
+__global__ void aggregate_in_edges_kernel(const int64_t* __restrict__ edge_ptr,
+                                          const int32_t* __restrict__ rev, int64_t nv,
+                                          const float* __restrict__ x, int64_t ldx, int d,
+                                          float* __restrict__ out) {
+  int lane = threadIdx.x & 31;
+  int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t v = warp; v < nv; v += nwarps) {
+    int64_t e0 = edge_ptr[v], e1 = edge_ptr[v + 1];
+    for (int c0 = 0; c0 < d; c0 += 128) {
+      float acc[4] = {0.f, 0.f, 0.f, 0.f};
+      for (int64_t e = e0; e < e1; ++e) {
+        const float* row = x + static_cast<int64_t>(rev[e]) * ldx;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          int c = c0 + u * 32 + lane;
+          if (c < d) acc[u] += row[c];
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        int c = c0 + u * 32 + lane;
+        if (c < d) out[v * d + c] = acc[u];
+      }
+    }
+  }
+}
+
+__global__ void gather_rows_kernel(const int32_t* __restrict__ idx, int64_t rows,
+                                   const float* __restrict__ x, int64_t ldx, int d,
+                                   float* __restrict__ out, int64_t ldo, int accumulate) {
+  int lane = threadIdx.x & 31;
+  int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = warp; r < rows; r += nwarps) {
+    const float* src = x + static_cast<int64_t>(idx[r]) * ldx;
+    float* dst = out + r * ldo;
+    for (int c = lane; c < d; c += 32) dst[c] = accumulate ? dst[c] + src[c] : src[c];
+  }
+}
+
+// One CTA per (graph, 128-channel chunk); deterministic tree over nodes.
+__global__ void graph_sum_kernel(const int64_t* __restrict__ graph_ptr, int64_t ng,
+                                 const float* __restrict__ x, int d, float* __restrict__ out) {
+  __shared__ float red[8][32];
+  int chunks = (d + 31) / 32;
+  for (int64_t item = blockIdx.x; item < ng * chunks; item += gridDim.x) {
+    int64_t g = item / chunks;
+    int c = static_cast<int>(item - g * chunks) * 32 + (threadIdx.x & 31);
+    int row = threadIdx.x >> 5;  // 8 row lanes
+    float s = 0.f;
+    if (c < d)
+      for (int64_t v = graph_ptr[g] + row; v < graph_ptr[g + 1]; v += 8) s += x[v * d + c];
+    red[row][threadIdx.x & 31] = s;
+    __syncthreads();
+    if (row == 0 && c < d) {
+      float t = 0.f;
+#pragma unroll
+      for (int r = 0; r < 8; ++r) t += red[r][threadIdx.x & 31];
+      out[g * d + c] = t;
+    }
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------- force head
+// scale[e] = m_e . w  (warp per edge)
+__global__ void edge_dot_kernel(const float* __restrict__ m, int64_t ne, int d,
+                                const float* __restrict__ w, float* __restrict__ scale) {
+  int lane = threadIdx.x & 31;
+  int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t e = warp; e < ne; e += nwarps) {
+    float s = 0.f;
+    for (int c = lane; c < d; c += 32) s = fmaf(m[e * d + c], w[c], s);
+    s = warp_sum(s);
+    if (lane == 0) scale[e] = s;
+  }
+}
+
+// forces[v] = sum over in-edges e of v of scale[e] u_e
+__global__ void force_gather_kernel(const int64_t* __restrict__ edge_ptr,
+                                    const int32_t* __restrict__ rev,
+                                    const float4* __restrict__ geo, int64_t nv,
+                                    const float* __restrict__ scale, float* __restrict__ forces) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nv;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    float fx = 0.f, fy = 0.f, fz = 0.f;
+    for (int64_t e = edge_ptr[v]; e < edge_ptr[v + 1]; ++e) {
+      int64_t ie = rev[e];
+      float s = scale[ie];
+      float4 g = geo[ie];
+      fx += s * g.x;
+      fy += s * g.y;
+      fz += s * g.z;
+    }
+    forces[3 * v + 0] = fx;
+    forces[3 * v + 1] = fy;
+    forces[3 * v + 2] = fz;
+  }
+}
+
+// Adjoint of the force head, warp per edge.
+__global__ void force_bwd_kernel(const int32_t* __restrict__ recv, const float4* __restrict__ geo,
+                                 int64_t ne, const float* __restrict__ m, int d,
+                                 const float* __restrict__ w, const float* __restrict__ scale,
+                                 const float* __restrict__ fbar, float* __restrict__ mbar,
+                                 float* __restrict__ wpart, float4* __restrict__ edge_grad) {
+  int lane = threadIdx.x & 31;
+  int wib = threadIdx.x >> 5;
+  int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  // per-warp partial of w_bar, lanes over channels (d <= 32 * 16)
+  float wacc[16];
+#pragma unroll
+  for (int u = 0; u < 16; ++u) wacc[u] = 0.f;
+  for (int64_t e = warp; e < ne; e += nwarps) {
+    int64_t v = recv[e];
+    float4 g = geo[e];
+    float bx = fbar[3 * v], by = fbar[3 * v + 1], bz = fbar[3 * v + 2];
+    float sbar = bx * g.x + by * g.y + bz * g.z;
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      int c = u * 32 + lane;
+      if (c < d) {
+        mbar[e * d + c] += sbar * w[c];
+        wacc[u] = fmaf(sbar, m[e * d + c], wacc[u]);
+      }
+    }
+    if (lane == 0) {
+      float s = scale[e];
+      // units_bar = s * fbar; d(unit)/d(v) adjoint: (ub - (ub.u) u) / d
+      float ux = s * bx, uy = s * by, uz = s * bz;
+      float pr = ux * g.x + uy * g.y + uz * g.z;
+      float inv = 1.f / g.w;
+      float4 eg = edge_grad[e];
+      eg.x += (ux - pr * g.x) * inv;
+      eg.y += (uy - pr * g.y) * inv;
+      eg.z += (uz - pr * g.z) * inv;
+      edge_grad[e] = eg;
+    }
+  }
+  int64_t slot = blockIdx.x * (int64_t)(blockDim.x >> 5) + wib;
+#pragma unroll
+  for (int u = 0; u < 16; ++u) {
+    int c = u * 32 + lane;
+    if (c < d) wpart[slot * d + c] = wacc[u];
+  }
+}
+
+__global__ void reduce_rows_kernel(const float* __restrict__ part, int nparts, int64_t len,
+                                   float* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < len;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    float s = 0.f;
+    for (int p = 0; p < nparts; ++p) s += part[p * len + i];
+    out[i] = s;
+  }
+}
+
+// ---------------------------------------------------------------- geometry adjoints
+__global__ void rbf_bwd_kernel(const float4* __restrict__ geo, const float* __restrict__ rbar,
+                               int64_t ne, int K, RbfParams rp, float4* __restrict__ edge_grad) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < ne;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    float d = geo[e].w;
+    float s = 0.f;
+    for (int k = 0; k < K; ++k) {
+      float dd = d - rp.step * k;
+      float r = __expf(-rp.gamma * dd * dd);
+      s = fmaf(rbar[e * K + k], -2.f * rp.gamma * dd * r, s);
+    }
+    edge_grad[e].w += s;
+  }
+}
+
+// pos_bar[a] = sum_{e in out(a)} (g_{rev e} - g_e), g_e = grad_v(e) + dd_e * u_e.
+__global__ void positions_bwd_kernel(const int64_t* __restrict__ edge_ptr,
+                                     const int32_t* __restrict__ rev,
+                                     const float4* __restrict__ geo, int64_t nv,
+                                     const float4* __restrict__ eg, double* __restrict__ pos_bar) {
+  for (int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a < nv;
+       a += (int64_t)gridDim.x * blockDim.x) {
+    double sx = 0.0, sy = 0.0, sz = 0.0;
+    for (int64_t e = edge_ptr[a]; e < edge_ptr[a + 1]; ++e) {
+      int64_t ie = rev[e];
+      float4 gi = eg[ie], ui = geo[ie];
+      float4 go = eg[e], uo = geo[e];
+      sx += (double)fmaf(gi.w, ui.x, gi.x) - (double)fmaf(go.w, uo.x, go.x);
+      sy += (double)fmaf(gi.w, ui.y, gi.y) - (double)fmaf(go.w, uo.y, go.y);
+      sz += (double)fmaf(gi.w, ui.z, gi.z) - (double)fmaf(go.w, uo.z, go.z);
+    }
+    pos_bar[3 * a + 0] = sx;
+    pos_bar[3 * a + 1] = sy;
+    pos_bar[3 * a + 2] = sz;
+  }
+}
+
+__global__ void sgd_kernel(float* __restrict__ w, const float* __restrict__ g, int64_t n, float lr) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    w[i] -= lr * g[i];
+}
+
+}  // namespace egn
+
+using namespace egn;
+
+extern "C" {
+
+int egn_rbf(const float* geo, int64_t num_edges, int k_rbf, double cutoff, float* rbf,
+            egn_stream_t stream) {
+  EGN_REQUIRE(k_rbf >= 1, "k_rbf must be >= 1");
+  if (num_edges == 0) return 0;
+  rbf_kernel<<<grid_for(num_edges * k_rbf, 256), 256, 0, as_stream(stream)>>>(
+      reinterpret_cast<const float4*>(geo), num_edges, k_rbf, rbf_params(k_rbf, cutoff), rbf);
+  return check_launch("rbf");
+}
+
+int egn_sbf(const float* geo, const int64_t* edge_ptr, const int64_t* tri_ptr, int64_t num_nodes,
+            int k_rbf, int l_sbf, double cutoff, float* sbf, egn_stream_t stream) {
+  EGN_REQUIRE(k_rbf >= 1 && l_sbf >= 1, "k_rbf and l_sbf must be >= 1");
+  if (num_nodes == 0) return 0;
+  int grid = static_cast<int>(num_nodes < 65535 ? num_nodes : 65535);
+  sbf_kernel<<<grid, 128, 0, as_stream(stream)>>>(reinterpret_cast<const float4*>(geo), edge_ptr,
+                                                  tri_ptr, num_nodes, k_rbf, l_sbf,
+                                                  rbf_params(k_rbf, cutoff), sbf);
+  return check_launch("sbf");
+}
+
+int egn_aggregate_in_edges(const int64_t* edge_ptr, const int32_t* rev, int64_t num_nodes,
+                           const float* x, int64_t ld_x, int d, float* out, egn_stream_t stream) {
+  if (num_nodes == 0) return 0;
+  aggregate_in_edges_kernel<<<grid_for(num_nodes * 32, 256), 256, 0, as_stream(stream)>>>(
+      edge_ptr, rev, num_nodes, x, ld_x, d, out);
+  return check_launch("aggregate_in_edges");
+}
+
+int egn_gather_rows(const int32_t* idx, int64_t rows, const float* x, int64_t ld_x, int d,
+                    float* out, int64_t ld_out, int accumulate, egn_stream_t stream) {
+  if (rows == 0) return 0;
+  gather_rows_kernel<<<grid_for(rows * 32, 256), 256, 0, as_stream(stream)>>>(
+      idx, rows, x, ld_x, d, out, ld_out, accumulate);
+  return check_launch("gather_rows");
+}
+
+int egn_graph_sum(const int64_t* graph_ptr, int64_t num_graphs, const float* x, int d,
+                  float* out, egn_stream_t stream) {
+  if (num_graphs == 0) return 0;
+  int64_t items = num_graphs * ((d + 31) / 32);
+  graph_sum_kernel<<<static_cast<int>(std::min<int64_t>(items, 148 * 16)), 256, 0,
+                     as_stream(stream)>>>(graph_ptr, num_graphs, x, d, out);
+  return check_launch("graph_sum");
+}
+
+int egn_force_head_fwd(const int64_t* edge_ptr, const int32_t* rev, const float* geo,
+                       int64_t num_nodes, int64_t num_edges, const float* m, int d,
+                       const float* w, float* scale, float* forces, egn_stream_t stream) {
+  if (num_nodes == 0) return 0;
+  cudaStream_t st = as_stream(stream);
+  if (num_edges > 0) {
+    edge_dot_kernel<<<grid_for(num_edges * 32, 256), 256, 0, st>>>(m, num_edges, d, w, scale);
+    if (check_launch("force_head_dot")) return 1;
+  }
+  force_gather_kernel<<<grid_for(num_nodes, 128), 128, 0, st>>>(
+      edge_ptr, rev, reinterpret_cast<const float4*>(geo), num_nodes, scale, forces);
+  return check_launch("force_head_gather");
+}
+
+int64_t egn_force_head_bwd_workspace_bytes(int64_t num_edges, int d) {
+  int grid = grid_for(num_edges * 32, 256, 148 * 2);
+  return static_cast<int64_t>(grid) * 8 * d * 4;
+}
+
+int egn_force_head_bwd(const int32_t* recv, const float* geo, int64_t num_edges, const float* m,
+                       int d, const float* w, const float* scale, const float* f_bar,
+                       float* m_bar, float* w_bar, float* edge_grad, void* workspace,
+                       egn_stream_t stream) {
+  EGN_REQUIRE(d <= 512, "force head width must be <= 512");
+  cudaStream_t st = as_stream(stream);
+  if (num_edges == 0) {
+    cudaMemsetAsync(w_bar, 0, sizeof(float) * d, st);
+    return check_launch("force_head_bwd_empty");
+  }
+  int grid = grid_for(num_edges * 32, 256, 148 * 2);
+  float* part = reinterpret_cast<float*>(workspace);
+  force_bwd_kernel<<<grid, 256, 0, st>>>(recv, reinterpret_cast<const float4*>(geo), num_edges, m,
+                                         d, w, scale, f_bar, m_bar, part,
+                                         reinterpret_cast<float4*>(edge_grad));
+  if (check_launch("force_head_bwd")) return 1;
+  reduce_rows_kernel<<<grid_for(d, 128), 128, 0, st>>>(part, grid * 8, d, w_bar);
+  return check_launch("force_head_bwd_reduce");
+}
+
+int egn_rbf_bwd(const float* geo, const float* rbf_bar, int64_t num_edges, int k_rbf,
+                double cutoff, float* edge_grad, egn_stream_t stream) {
+  if (num_edges == 0) return 0;
+  rbf_bwd_kernel<<<grid_for(num_edges, 256), 256, 0, as_stream(stream)>>>(
+      reinterpret_cast<const float4*>(geo), rbf_bar, num_edges, k_rbf, rbf_params(k_rbf, cutoff),
+      reinterpret_cast<float4*>(edge_grad));
+  return check_launch("rbf_bwd");
+}
+
+int egn_positions_bwd(const int64_t* edge_ptr, const int32_t* rev, const float* geo,
+                      int64_t num_nodes, const float* edge_grad, double* pos_bar,
+                      egn_stream_t stream) {
+  if (num_nodes == 0) return 0;
+  positions_bwd_kernel<<<grid_for(num_nodes, 128), 128, 0, as_stream(stream)>>>(
+      edge_ptr, rev, reinterpret_cast<const float4*>(geo), num_nodes,
+      reinterpret_cast<const float4*>(edge_grad), pos_bar);
+  return check_launch("positions_bwd");
+}
+
+int egn_sgd(float* w, const float* g, int64_t n, float lr, egn_stream_t stream) {
+  if (n == 0) return 0;
+  sgd_kernel<<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(w, g, n, lr);
+  return check_launch("sgd");
+}
+
+}  // extern "C"

@@ -1,0 +1,636 @@
+// Triplet interaction (TU + TA) forward and backward for sm_100a.
+//
+// Reference: record_tu, egn/engine.py:118-149, and the tape VJPs it implies
+// (gather/segment_sum tape.py:129-154, linear :104-119, angular_sbf
+// :231-242, triplet_angles :185-195).
+//
+// Centre-tile formulation.  Edges are sorted by (src, recv), so the
+// out-edges of centre atom j are the contiguous rows [off_j, off_j + n).
+// Triplet ((k->j), (j->i)) with out-edge p = (j->i) and in-edge
+// rq = rev(off_j + q) = (k->j) exists for every ordered pair q != p of j's
+// out-edges, and all of j's triplets form one n x n block minus its
+// diagonal (enumerate_triplets, graph.py:106-139).  Hence
+//   * the segment_sum over id3_ji is a reduction inside the tile (no atomics),
+//   * every use of an edge as id3_kj lies in the tile of its receiver, so the
+//     adjoint scatter to id3_kj is tile-local as well,
+//   * the angle only needs the two out-edge unit vectors u_p, u_q of the
+//     tile: cos(alpha) = x_pq = u_p . u_q and cos(l alpha) = T_l(x_pq)
+//     (Chebyshev), and the SBF radial factor rbf(d_kj) uses d_q = d_rq.
+// The per-triplet SBF gate sbf_t W^T factorises per in-edge:
+//   g_sbf_t = sum_l T_l(x_pq) Rw[rq, l, :],  Rw[e, l, c] = sum_k rbf_k(d_e) W[k, l, c],
+// and Q[q, l, c] = X[rq, c] Rw[rq, l, c] is built once per tile in shared
+// memory.  Per triplet the kernel then spends L * dg FMAs; nothing per
+// triplet ever touches HBM.
+//
+// Backward per centre (thread = (row q, channel chunk)):
+//   Qbar[q,l,c] = sum_p T_l(x_pq) Sbar[p,c]                 -> X_bar, W_bar, dd_q
+//   y(p,q)      = xbar(p,q) + xbar(q,p),
+//   xbar(p,q)   = sum_l T_l'(x_pq) sum_c Sbar[p,c] Q[q,l,c]  -> dE/dv_q
+// with dE/dv_q += y (u_p - x u_q) / d_q, the gradient of x_pq w.r.t. the
+// edge vector v_q; using d cos(l a)/dx = T_l'(x) = l U_{l-1}(x) avoids the
+// atan2 singularity and equals the reference's zero subgradient at
+// collinear triplets (both factors vanish there).
+#include <algorithm>
+
+#include "common.cuh"
+
+namespace egn {
+
+constexpr int kThreads = 128;
+constexpr int kMaxL = 8;
+constexpr int kMaxK = 16;
+
+template <int CW, int GC>
+struct ChanMap {
+  static constexpr int VW = CW < 4 ? CW : 4;
+  static constexpr int DP = CW * GC;
+  // channel of slot i for channel-group cg: VW-wide chunks interleaved so
+  // that one warp-wide vector load covers a contiguous 16*GC-byte span.
+  __device__ __forceinline__ static int chan(int cg, int i) {
+    return (i / VW) * (VW * GC) + cg * VW + (i % VW);
+  }
+};
+
+template <int VW>
+__device__ __forceinline__ void load_vec(const float* p, float* v) {
+  if constexpr (VW == 4) {
+    float4 t = *reinterpret_cast<const float4*>(p);
+    v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w;
+  } else if constexpr (VW == 2) {
+    float2 t = *reinterpret_cast<const float2*>(p);
+    v[0] = t.x; v[1] = t.y;
+  } else {
+    v[0] = p[0];
+  }
+}
+
+// Shared-memory carve-up common to both kernels (floats, 16B aligned pieces).
+struct TileLayout {
+  int qt;      // q rows per tile
+  int k, l, dp;
+  int off_rb, off_w, off_q, off_x;  // float offsets
+  int total;
+  __host__ __device__ static int up4(int x) { return (x + 3) & ~3; }
+  __host__ __device__ TileLayout(int qt_, int k_, int l_, int dp_, int extra_rows)
+      : qt(qt_), k(k_), l(l_), dp(dp_) {
+    int o = 4 * qt;              // Us (float4 per row)
+    off_rb = o; o += up4(qt * k);  // rbf of tile rows
+    off_w = o; o += up4(k * l * dp);
+    off_q = o; o += up4(qt * l * dp);
+    off_x = o; o += up4(extra_rows);  // kernel-specific extra
+    total = o;
+  }
+};
+
+__device__ __forceinline__ float rbf_val(float d, int k, RbfParams rp) {
+  float dd = d - rp.step * k;
+  return __expf(-rp.gamma * dd * dd);
+}
+
+// Build the tile: Us[t] = geo[off+q0+t], Rb[t][k] = rbf_k(d), Qs[t][l][c] = X[rq][c] * Rw.
+template <int CW, int GC>
+__device__ __forceinline__ void build_tile(const TileLayout& Ly, float* sm, const float4* __restrict__ geo,
+                                           const int32_t* __restrict__ rev, const float* __restrict__ X,
+                                           int64_t off, int q0, int nq, int dg, RbfParams rp) {
+  using CM = ChanMap<CW, GC>;
+  constexpr int DP = CM::DP;
+  const int tid = threadIdx.x;
+  float4* Us = reinterpret_cast<float4*>(sm);
+  float* Rb = sm + Ly.off_rb;
+  const float* Wsm = sm + Ly.off_w;
+  float* Qs = sm + Ly.off_q;
+  const int K = Ly.k, L = Ly.l;
+  if (tid < nq) Us[tid] = geo[off + q0 + tid];
+  for (int idx = tid; idx < nq * K; idx += kThreads) {
+    int t = idx / K, k = idx - t * K;
+    Rb[idx] = rbf_val(geo[off + q0 + t].w, k, rp);
+  }
+  __syncthreads();
+  for (int idx = tid; idx < nq * DP; idx += kThreads) {
+    int t = idx / DP, c = idx - t * DP;
+    float xv = 0.f;
+    if (c < dg) xv = X[static_cast<int64_t>(rev[off + q0 + t]) * dg + c];
+    const float* rb = Rb + t * K;
+    for (int l = 0; l < L; ++l) {
+      float s = 0.f;
+      for (int k = 0; k < K; ++k) s = fmaf(rb[k], Wsm[(k * L + l) * DP + c], s);
+      Qs[(t * L + l) * DP + c] = xv * s;
+    }
+  }
+  __syncthreads();
+}
+
+template <int CW, int GC>
+__device__ __forceinline__ void load_weights(float* Wsm, const float* __restrict__ W, int K, int L, int dg) {
+  constexpr int DP = CW * GC;
+  for (int idx = threadIdx.x; idx < K * L * DP; idx += kThreads) {
+    int kl = idx / DP, c = idx - kl * DP;
+    Wsm[idx] = c < dg ? W[kl * dg + c] : 0.f;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// forward
+// ---------------------------------------------------------------------------
+template <int CW, int GC, int R>
+__global__ void __launch_bounds__(kThreads)
+triplet_fwd_kernel(const int64_t* __restrict__ edge_ptr, const int32_t* __restrict__ rev,
+                   const float4* __restrict__ geo, int64_t nv, const float* __restrict__ X,
+                   const float* __restrict__ W, int K, int L, int dg, int qt, RbfParams rp,
+                   float* __restrict__ S) {
+  using CM = ChanMap<CW, GC>;
+  constexpr int GP = kThreads / GC, VW = CM::VW, DP = CM::DP;
+  extern __shared__ __align__(16) float sm[];
+  TileLayout Ly(qt, K, L, DP, 0);
+  const float4* Us = reinterpret_cast<const float4*>(sm);
+  const float* Qs = sm + Ly.off_q;
+  const int tid = threadIdx.x, cg = tid % GC, pg = tid / GC;
+
+  load_weights<CW, GC>(sm + Ly.off_w, W, K, L, dg);
+  // (the first tile build synchronises before Wsm is read)
+
+  for (int64_t j = blockIdx.x; j < nv; j += gridDim.x) {
+    const int64_t off = edge_ptr[j];
+    const int n = static_cast<int>(edge_ptr[j + 1] - off);
+    if (n == 0) continue;
+    for (int p0 = 0; p0 < n; p0 += GP * R) {
+      const int reff = min(R, (n - p0 + GP - 1) / GP);  // CTA-uniform
+      float4 up[R];
+      int pidx[R];
+      float acc[R][CW];
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        pidx[r] = p0 + pg + GP * r;
+        up[r] = (r < reff && pidx[r] < n) ? geo[off + pidx[r]] : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int i = 0; i < CW; ++i) acc[r][i] = 0.f;
+      }
+      for (int q0 = 0; q0 < n; q0 += qt) {
+        const int nq = min(qt, n - q0);
+        __syncthreads();
+        build_tile<CW, GC>(Ly, sm, geo, rev, X, off, q0, nq, dg, rp);
+        for (int t = 0; t < nq; ++t) {
+          const float4 uq = Us[t];
+          const int qg = q0 + t;
+          float x2[R], tc[R], tp[R];
+#pragma unroll
+          for (int r = 0; r < R; ++r) {
+            float x = up[r].x * uq.x + up[r].y * uq.y + up[r].z * uq.z;
+            float m = pidx[r] != qg ? 1.f : 0.f;
+            x2[r] = 2.f * x;
+            tc[r] = m;       // T_0
+            tp[r] = m * x;   // T_{-1} = T_1 = x
+          }
+          const float* qrow = Qs + t * L * DP;
+          for (int l = 0; l < L; ++l) {
+            float qv[CW];
+#pragma unroll
+            for (int i = 0; i < CW; i += VW) load_vec<VW>(qrow + l * DP + CM::chan(cg, i), qv + i);
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+              if (r < reff) {
+#pragma unroll
+                for (int i = 0; i < CW; ++i) acc[r][i] = fmaf(tc[r], qv[i], acc[r][i]);
+              }
+              float tn = fmaf(x2[r], tc[r], -tp[r]);
+              tp[r] = tc[r];
+              tc[r] = tn;
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        if (r < reff && pidx[r] < n) {
+          float* dst = S + (off + pidx[r]) * dg;
+#pragma unroll
+          for (int i = 0; i < CW; ++i) {
+            int c = CM::chan(cg, i);
+            if (c < dg) dst[c] = acc[r][i];
+          }
+        }
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// backward
+// ---------------------------------------------------------------------------
+// Extra shared memory: Sbar tile [qt][DP], W_bar accumulator [K][L][DP],
+// staging for per-row R_bar [GP][L][DP] and rbf [GP][K].
+struct BwdExtra {
+  int sb, wbar, rstage, rbst, total;
+  __host__ __device__ BwdExtra(int qt, int K, int L, int DP, int GP) {
+    int o = 0;
+    sb = o; o += TileLayout::up4(qt * DP);
+    wbar = o; o += TileLayout::up4(K * L * DP);
+    rstage = o; o += TileLayout::up4(GP * L * DP);
+    rbst = o; o += TileLayout::up4(GP * K);
+    total = o;
+  }
+};
+
+template <int CW, int GC>
+__global__ void __launch_bounds__(kThreads)
+triplet_bwd_kernel(const int64_t* __restrict__ edge_ptr, const int32_t* __restrict__ rev,
+                   const float4* __restrict__ geo, int64_t nv, const float* __restrict__ X,
+                   const float* __restrict__ W, int K, int L, int dg, int qt, RbfParams rp,
+                   const float* __restrict__ Sbar, float* __restrict__ Xbar,
+                   float* __restrict__ wbar_part, float4* __restrict__ edge_grad) {
+  using CM = ChanMap<CW, GC>;
+  constexpr int GP = kThreads / GC, VW = CM::VW, DP = CM::DP;
+  extern __shared__ __align__(16) float sm[];
+  const int KLD = K * L * DP;
+  BwdExtra Bx(qt, K, L, DP, GP);
+  TileLayout Ly(qt, K, L, DP, Bx.total);
+  const float4* Us = reinterpret_cast<const float4*>(sm);
+  const float* Wsm = sm + Ly.off_w;
+  const float* Qs = sm + Ly.off_q;
+  float* ext = sm + Ly.off_x;
+  float* Sbs = ext + Bx.sb;
+  float* Wb = ext + Bx.wbar;
+  float* Rst = ext + Bx.rstage;
+  float* Rbs = ext + Bx.rbst;
+  const int tid = threadIdx.x, cg = tid % GC, pg = tid / GC;
+
+  load_weights<CW, GC>(sm + Ly.off_w, W, K, L, dg);
+  for (int idx = tid; idx < KLD; idx += kThreads) Wb[idx] = 0.f;
+
+  for (int64_t j = blockIdx.x; j < nv; j += gridDim.x) {
+    const int64_t off = edge_ptr[j];
+    const int n = static_cast<int>(edge_ptr[j + 1] - off);
+    if (n < 2) continue;  // no triplets: no gradient, edge_grad untouched
+    for (int b0 = 0; b0 < n; b0 += GP) {
+      const int q = b0 + pg;
+      const bool valid = q < n;
+      __syncthreads();  // Wsm / previous users of the tile are done
+      // own row data
+      float4 uq = valid ? geo[off + q] : make_float4(0.f, 0.f, 0.f, 1.f);
+      const int64_t rq = valid ? static_cast<int64_t>(rev[off + q]) : 0;
+      float sbo[CW], xo[CW];
+#pragma unroll
+      for (int i = 0; i < CW; ++i) {
+        int c = CM::chan(cg, i);
+        sbo[i] = (valid && c < dg) ? Sbar[(off + q) * dg + c] : 0.f;
+        xo[i] = (valid && c < dg) ? X[rq * dg + c] : 0.f;
+      }
+      float rbo[kMaxK], rdo[kMaxK];  // rbf_k(d_q) and d rbf_k / dd
+#pragma unroll
+      for (int k = 0; k < kMaxK; ++k) {
+        rbo[k] = k < K ? rbf_val(uq.w, k, rp) : 0.f;
+        rdo[k] = -2.f * rp.gamma * (uq.w - rp.step * k) * rbo[k];
+      }
+      // own Q row: Q[q,l,c] = xo * sum_k rbf_k W[k,l,c]
+      float qo[kMaxL][CW];
+#pragma unroll
+      for (int l = 0; l < kMaxL; ++l) {
+#pragma unroll
+        for (int i = 0; i < CW; ++i) {
+          float s = 0.f;
+          if (l < L) {
+            int c = CM::chan(cg, i);
+#pragma unroll
+            for (int k = 0; k < kMaxK; ++k)
+              if (k < K) s = fmaf(rbo[k], Wsm[(k * L + l) * DP + c], s);
+          }
+          qo[l][i] = xo[i] * s;
+        }
+      }
+      float qb[kMaxL][CW];
+#pragma unroll
+      for (int l = 0; l < kMaxL; ++l)
+#pragma unroll
+        for (int i = 0; i < CW; ++i) qb[l][i] = 0.f;
+      float fx = 0.f, fy = 0.f, fz = 0.f;
+
+      for (int p0 = 0; p0 < n; p0 += qt) {
+        const int np = min(qt, n - p0);
+        __syncthreads();
+        for (int idx = tid; idx < np * DP; idx += kThreads) {
+          int t = idx / DP, c = idx - t * DP;
+          Sbs[idx] = c < dg ? Sbar[(off + p0 + t) * dg + c] : 0.f;
+        }
+        build_tile<CW, GC>(Ly, sm, geo, rev, X, off, p0, np, dg, rp);  // syncs
+        for (int t = 0; t < np; ++t) {
+          const float4 up = Us[t];
+          const float x = up.x * uq.x + up.y * uq.y + up.z * uq.z;
+          const float m = (p0 + t != q) ? 1.f : 0.f;
+          float sbp[CW];
+#pragma unroll
+          for (int i = 0; i < CW; i += VW) load_vec<VW>(Sbs + t * DP + CM::chan(cg, i), sbp + i);
+          const float x2 = 2.f * x;
+          float tc = m, tp = m * x;      // T_l (masked), starting at l = 0
+          float uc = 0.f, um = 0.f;      // U_{l-1}, U_{l-2}
+          float y = 0.f;
+          const float* qrow = Qs + t * L * DP;
+#pragma unroll
+          for (int l = 0; l < kMaxL; ++l) {
+            if (l < L) {
+              float qv[CW];
+#pragma unroll
+              for (int i = 0; i < CW; i += VW) load_vec<VW>(qrow + l * DP + CM::chan(cg, i), qv + i);
+              float s = 0.f;
+#pragma unroll
+              for (int i = 0; i < CW; ++i) {
+                qb[l][i] = fmaf(tc, sbp[i], qb[l][i]);
+                s = fmaf(sbo[i], qv[i], s);
+                s = fmaf(sbp[i], qo[l][i], s);
+              }
+              // T_l'(x) = l U_{l-1}(x)
+              y = fmaf(static_cast<float>(l) * uc, s, y);
+              float tn = fmaf(x2, tc, -tp);
+              tp = tc;
+              tc = tn;
+              float un = (l == 0) ? 1.f : fmaf(x2, uc, -um);
+              um = uc;
+              uc = un;
+            }
+          }
+          // reduce y over the GC threads of this row
+#pragma unroll
+          for (int o = GC / 2; o > 0; o >>= 1) y += __shfl_xor_sync(0xffffffffu, y, o);
+          y *= m;
+          fx = fmaf(y, up.x - x * uq.x, fx);
+          fy = fmaf(y, up.y - x * uq.y, fy);
+          fz = fmaf(y, up.z - x * uq.z, fz);
+        }
+      }
+
+      // ---- row epilogue: X_bar, R_bar -> (W_bar, dd) ----
+      float xb[CW];
+      float dd = 0.f;
+#pragma unroll
+      for (int i = 0; i < CW; ++i) xb[i] = 0.f;
+      __syncthreads();  // Qs no longer needed; Rst/Rbs free
+#pragma unroll
+      for (int l = 0; l < kMaxL; ++l) {
+        if (l < L) {
+#pragma unroll
+          for (int i = 0; i < CW; ++i) {
+            int c = CM::chan(cg, i);
+            float rw = 0.f, rwd = 0.f;
+#pragma unroll
+            for (int k = 0; k < kMaxK; ++k) {
+              if (k < K) {
+                float w = Wsm[(k * L + l) * DP + c];
+                rw = fmaf(rbo[k], w, rw);
+                rwd = fmaf(rdo[k], w, rwd);
+              }
+            }
+            xb[i] = fmaf(qb[l][i], rw, xb[i]);
+            float rbar = qb[l][i] * xo[i];
+            dd = fmaf(rbar, rwd, dd);
+            Rst[(pg * L + l) * DP + c] = valid ? rbar : 0.f;
+          }
+        }
+      }
+      if (cg == 0) {
+#pragma unroll
+        for (int k = 0; k < kMaxK; ++k)
+          if (k < K) Rbs[pg * K + k] = valid ? rbo[k] : 0.f;
+      }
+#pragma unroll
+      for (int o = GC / 2; o > 0; o >>= 1) dd += __shfl_xor_sync(0xffffffffu, dd, o);
+      if (valid) {
+#pragma unroll
+        for (int i = 0; i < CW; ++i) {
+          int c = CM::chan(cg, i);
+          if (c < dg) Xbar[rq * dg + c] = xb[i];
+        }
+        if (cg == 0) {
+          float inv = 1.f / uq.w;
+          float4 g = edge_grad[off + q];
+          g.x += fx * inv;
+          g.y += fy * inv;
+          g.z += fz * inv;
+          g.w += dd;
+          edge_grad[off + q] = g;
+        }
+      }
+      __syncthreads();
+      // W_bar[k,l,c] += sum_rows rbf_k(row) * R_bar[row,l,c]  (thread-owned (l,c))
+      const int rows = min(GP, n - b0);
+      for (int idx = tid; idx < L * DP; idx += kThreads) {
+        for (int k = 0; k < K; ++k) {
+          float s = Wb[k * L * DP + idx];
+          for (int r = 0; r < rows; ++r) s = fmaf(Rbs[r * K + k], Rst[r * L * DP + idx], s);
+          Wb[k * L * DP + idx] = s;
+        }
+      }
+    }
+  }
+  __syncthreads();
+  float* dst = wbar_part + static_cast<int64_t>(blockIdx.x) * K * L * dg;
+  for (int idx = tid; idx < K * L * dg; idx += kThreads) {
+    int kl = idx / dg, c = idx - kl * dg;
+    dst[idx] = Wb[kl * DP + c];
+  }
+}
+
+__global__ void reduce_partials_kernel(const float* __restrict__ part, int nparts, int64_t len,
+                                       float* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < len;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    float s = 0.f;
+    for (int p = 0; p < nparts; ++p) s += part[p * len + i];
+    out[i] = s;
+  }
+}
+
+// Debug: per-triplet summand P[t, c] in (out, in) order.
+__global__ void triplet_terms_kernel(const int64_t* __restrict__ edge_ptr,
+                                     const int32_t* __restrict__ rev,
+                                     const float4* __restrict__ geo,
+                                     const int64_t* __restrict__ tri_ptr, int64_t nv,
+                                     const float* __restrict__ X, const float* __restrict__ W,
+                                     int K, int L, int dg, RbfParams rp, float* __restrict__ P) {
+  for (int64_t j = blockIdx.x; j < nv; j += gridDim.x) {
+    int64_t off = edge_ptr[j];
+    int64_t n = edge_ptr[j + 1] - off;
+    if (n < 2) continue;
+    int64_t t0 = tri_ptr[j];
+    int64_t cnt = n * (n - 1) * dg;
+    for (int64_t k = threadIdx.x; k < cnt; k += blockDim.x) {
+      int64_t tt = k / dg;
+      int c = static_cast<int>(k - tt * dg);
+      int64_t p = tt / (n - 1);
+      int64_t r = tt - p * (n - 1);
+      int64_t q = r < p ? r : r + 1;
+      float4 a = geo[off + p], b = geo[off + q];
+      float x = a.x * b.x + a.y * b.y + a.z * b.z;
+      int64_t rq = rev[off + q];
+      float tc = 1.f, tp = x, g = 0.f;
+      for (int l = 0; l < L; ++l) {
+        float rw = 0.f;
+        for (int kk = 0; kk < K; ++kk) rw = fmaf(rbf_val(b.w, kk, rp), W[(kk * L + l) * dg + c], rw);
+        g = fmaf(tc, rw, g);
+        float tn = 2.f * x * tc - tp;
+        tp = tc;
+        tc = tn;
+      }
+      P[(t0 + tt) * dg + c] = X[rq * dg + c] * g;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host dispatch
+// ---------------------------------------------------------------------------
+struct Variant {
+  int cw, gc, r;
+};
+
+static Variant pick_variant(int dg) {
+  if (dg <= 4) return {4, 1, 1};
+  if (dg <= 8) return {8, 1, 1};
+  if (dg <= 16) return {8, 2, 2};
+  if (dg <= 32) return {8, 4, 2};
+  if (dg <= 64) return {8, 8, 4};
+  if (dg <= 128) return {8, 16, 4};
+  return {8, 32, 4};
+}
+
+static int pick_qt(int K, int L, int DP, int extra_floats, int budget_bytes) {
+  int fixed = 4 * (K * L * DP + extra_floats) + 64;
+  int per_row = 4 * (L * DP + 4 + K);
+  int qt = (budget_bytes - fixed) / per_row;
+  if (qt > 32) qt = 32;
+  if (qt < 4) qt = 4;
+  return qt;
+}
+
+template <int CW, int GC, int R>
+static int launch_fwd(const int64_t* edge_ptr, const int32_t* rev, const float4* geo, int64_t nv,
+                      const float* X, const float* W, int K, int L, int dg, RbfParams rp, float* S,
+                      cudaStream_t st) {
+  constexpr int DP = CW * GC;
+  int qt = pick_qt(K, L, DP, 0, 48 * 1024);
+  TileLayout Ly(qt, K, L, DP, 0);
+  size_t smem = static_cast<size_t>(Ly.total) * 4;
+  auto kern = triplet_fwd_kernel<CW, GC, R>;
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, smem);
+  if (per_sm < 1) per_sm = 1;
+  int64_t grid = std::min<int64_t>(nv, static_cast<int64_t>(kNumSMs) * per_sm * 4);
+  kern<<<static_cast<int>(grid), kThreads, smem, st>>>(edge_ptr, rev, geo, nv, X, W, K, L, dg, qt, rp, S);
+  return check_launch("triplet_fwd");
+}
+
+template <int CW, int GC>
+static int bwd_grid_and_smem(int64_t nv, int K, int L, int dg, int* grid_out, size_t* smem_out, int* qt_out) {
+  constexpr int DP = CW * GC, GP = kThreads / GC;
+  int extra_guess = BwdExtra(16, K, L, DP, GP).total;
+  int qt = pick_qt(K, L, DP, extra_guess, 96 * 1024);
+  BwdExtra Bx(qt, K, L, DP, GP);
+  TileLayout Ly(qt, K, L, DP, Bx.total);
+  size_t smem = static_cast<size_t>(Ly.total) * 4;
+  auto kern = triplet_bwd_kernel<CW, GC>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, smem);
+  if (per_sm < 1) per_sm = 1;
+  if (per_sm > 4) per_sm = 4;
+  int64_t grid = std::min<int64_t>(nv, static_cast<int64_t>(kNumSMs) * per_sm);
+  if (grid < 1) grid = 1;
+  *grid_out = static_cast<int>(grid);
+  *smem_out = smem;
+  *qt_out = qt;
+  return 0;
+}
+
+template <int CW, int GC>
+static int launch_bwd(const int64_t* edge_ptr, const int32_t* rev, const float4* geo, int64_t nv,
+                      const float* X, const float* W, int K, int L, int dg, RbfParams rp,
+                      const float* Sbar, float* Xbar, float* Wbar, float4* edge_grad, void* ws,
+                      cudaStream_t st) {
+  int grid, qt;
+  size_t smem;
+  bwd_grid_and_smem<CW, GC>(nv, K, L, dg, &grid, &smem, &qt);
+  float* part = reinterpret_cast<float*>(ws);
+  triplet_bwd_kernel<CW, GC><<<grid, kThreads, smem, st>>>(edge_ptr, rev, geo, nv, X, W, K, L, dg,
+                                                           qt, rp, Sbar, Xbar, part, edge_grad);
+  if (check_launch("triplet_bwd")) return 1;
+  int64_t len = static_cast<int64_t>(K) * L * dg;
+  reduce_partials_kernel<<<grid_for(len, 256), 256, 0, st>>>(part, grid, len, Wbar);
+  return check_launch("triplet_bwd_reduce");
+}
+
+}  // namespace egn
+
+using namespace egn;
+
+#define EGN_DISPATCH_DG(dg, FN, ...)                          \
+  do {                                                        \
+    if ((dg) <= 4) return FN<4, 1>(__VA_ARGS__);              \
+    if ((dg) <= 8) return FN<8, 1>(__VA_ARGS__);              \
+    if ((dg) <= 16) return FN<8, 2>(__VA_ARGS__);             \
+    if ((dg) <= 32) return FN<8, 4>(__VA_ARGS__);             \
+    if ((dg) <= 64) return FN<8, 8>(__VA_ARGS__);             \
+    if ((dg) <= 128) return FN<8, 16>(__VA_ARGS__);           \
+    return FN<8, 32>(__VA_ARGS__);                            \
+  } while (0)
+
+static int check_dims(int K, int L, int dg) {
+  EGN_REQUIRE(K >= 1 && K <= 16, "k_rbf must be in [1, 16], got %d", K);
+  EGN_REQUIRE(L >= 1 && L <= kMaxL, "l_sbf must be in [1, %d], got %d", kMaxL, L);
+  EGN_REQUIRE(dg >= 1 && dg <= 256, "triplet width must be in [1, 256], got %d", dg);
+  return 0;
+}
+
+extern "C" {
+
+int egn_triplet_fwd(const int64_t* edge_ptr, const int32_t* rev, const float* geo,
+                    int64_t num_nodes, const float* X, const float* W, int k_rbf, int l_sbf,
+                    int dg, double cutoff, float* S, egn_stream_t stream) {
+  if (int rc = check_dims(k_rbf, l_sbf, dg)) return rc;
+  if (num_nodes == 0) return 0;
+  RbfParams rp = rbf_params(k_rbf, cutoff);
+  const float4* g4 = reinterpret_cast<const float4*>(geo);
+  cudaStream_t st = as_stream(stream);
+  if (dg <= 4) return launch_fwd<4, 1, 1>(edge_ptr, rev, g4, num_nodes, X, W, k_rbf, l_sbf, dg, rp, S, st);
+  if (dg <= 8) return launch_fwd<8, 1, 1>(edge_ptr, rev, g4, num_nodes, X, W, k_rbf, l_sbf, dg, rp, S, st);
+  if (dg <= 16) return launch_fwd<8, 2, 2>(edge_ptr, rev, g4, num_nodes, X, W, k_rbf, l_sbf, dg, rp, S, st);
+  if (dg <= 32) return launch_fwd<8, 4, 2>(edge_ptr, rev, g4, num_nodes, X, W, k_rbf, l_sbf, dg, rp, S, st);
+  if (dg <= 64) return launch_fwd<8, 8, 4>(edge_ptr, rev, g4, num_nodes, X, W, k_rbf, l_sbf, dg, rp, S, st);
+  if (dg <= 128) return launch_fwd<8, 16, 4>(edge_ptr, rev, g4, num_nodes, X, W, k_rbf, l_sbf, dg, rp, S, st);
+  return launch_fwd<8, 32, 4>(edge_ptr, rev, g4, num_nodes, X, W, k_rbf, l_sbf, dg, rp, S, st);
+}
+
+int64_t egn_triplet_bwd_workspace_bytes(int64_t num_nodes, int k_rbf, int l_sbf, int dg) {
+  int64_t grid = std::min<int64_t>(std::max<int64_t>(num_nodes, 1), static_cast<int64_t>(kNumSMs) * 4);
+  return grid * k_rbf * l_sbf * dg * 4;
+}
+
+int egn_triplet_bwd(const int64_t* edge_ptr, const int32_t* rev, const float* geo,
+                    int64_t num_nodes, const float* X, const float* W, int k_rbf, int l_sbf,
+                    int dg, double cutoff, const float* S_bar, float* X_bar, float* W_bar,
+                    float* edge_grad, void* workspace, egn_stream_t stream) {
+  if (int rc = check_dims(k_rbf, l_sbf, dg)) return rc;
+  cudaStream_t st = as_stream(stream);
+  if (num_nodes == 0) {
+    cudaMemsetAsync(W_bar, 0, sizeof(float) * k_rbf * l_sbf * dg, st);
+    return check_launch("triplet_bwd_empty");
+  }
+  RbfParams rp = rbf_params(k_rbf, cutoff);
+  const float4* g4 = reinterpret_cast<const float4*>(geo);
+  float4* eg = reinterpret_cast<float4*>(edge_grad);
+  EGN_DISPATCH_DG(dg, launch_bwd, edge_ptr, rev, g4, num_nodes, X, W, k_rbf, l_sbf, dg, rp, S_bar,
+                  X_bar, W_bar, eg, workspace, st);
+}
+
+int egn_triplet_terms(const int64_t* edge_ptr, const int32_t* rev, const float* geo,
+                      const int64_t* tri_ptr, int64_t num_nodes, const float* X, const float* W,
+                      int k_rbf, int l_sbf, int dg, double cutoff, float* P, egn_stream_t stream) {
+  EGN_REQUIRE(k_rbf >= 1 && l_sbf >= 1 && dg >= 1, "bad dims");
+  if (num_nodes == 0) return 0;
+  int grid = static_cast<int>(num_nodes < 65535 ? num_nodes : 65535);
+  triplet_terms_kernel<<<grid, 256, 0, as_stream(stream)>>>(
+      edge_ptr, rev, reinterpret_cast<const float4*>(geo), tri_ptr, num_nodes, X, W, k_rbf, l_sbf,
+      dg, rbf_params(k_rbf, cutoff), P);
+  return check_launch("triplet_terms");
+}
+
+}  // extern "C"

@@ -1,0 +1,289 @@
+"""Batched EGN forward/backward on the GPU (DimeNet++-style and GemNet-T-style).
+
+This is the device counterpart of egn/engine.py (ModelTape :320-438, stage
+recorders :99-261) and the adjoints its tape applies (egn/tape.py).  The
+graph is a BatchGraph (G graphs concatenated); every per-graph quantity of
+the reference (global state u, energy) becomes a [G, .] tensor, so one call
+reproduces the reference's per-graph loop (tasks.py:158-183).
+
+Schedule per block (engine.py:118-217), with the algebraic reorder that is
+exact in real arithmetic:
+  X  = m W_down^T [A^T]                    (gather id3_kj commutes with linear)
+  S  = triplet_fwd(X)                      (centre-tile kernel, triplet.cu)
+  ta = ((S [P^T]) * (rbf W_rbf^T)) W_up^T  (up/P/rbf-gate commute with segment_sum)
+  EU, EA+NU, [EU2 + sym], GU               (dense MLPs; EA = in-edge gather-sum)
+The backward is written out explicitly (no autograd), mirroring the
+reference's reverse walk; geometry adjoints accumulate into one per-edge
+float4 (dE/dv_e, dE/dd_e) that a final CSR gather turns into dE/dx.
+
+Dense products use fp32 GEMMs with TF32 disabled (torch.mm -> cuBLAS); the
+graph-structured work (neighbour list, basis, triplet interaction, segment
+sums, force head, geometry adjoints, SGD) runs in the native library.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+import torch.nn.functional as F
+
+from . import ops
+from .config import GEMNET, ModelConfig
+from .graph import BatchGraph
+from .params import ModelParams, param_specs
+
+torch.backends.cuda.matmul.allow_tf32 = False
+torch.backends.cudnn.allow_tf32 = False
+
+
+def _silu_bwd(g: torch.Tensor, h: torch.Tensor) -> torch.Tensor:
+    s = torch.sigmoid(h)
+    return g * s * (1.0 + h * (1.0 - s))
+
+
+class DeviceWeights:
+    """fp32 device copy of ModelParams in one flat buffer (+ a grad buffer of
+    the same layout), so the SGD update is a single native kernel."""
+
+    def __init__(self, config: ModelConfig, device="cuda"):
+        self.config = config
+        self.specs = param_specs(config)
+        sizes = [int(np.prod(s.shape)) for s in self.specs]
+        self.offsets = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+        total = int(self.offsets[-1])
+        self.flat = torch.zeros(total, dtype=torch.float32, device=device)
+        self.grad_flat = torch.zeros(total, dtype=torch.float32, device=device)
+        self.w = {}
+        self.g = {}
+        for s, a, b in zip(self.specs, self.offsets[:-1], self.offsets[1:]):
+            self.w[s.name] = self.flat[a:b].view(s.shape)
+            self.g[s.name] = self.grad_flat[a:b].view(s.shape)
+
+    @classmethod
+    def from_params(cls, params: ModelParams, device="cuda") -> "DeviceWeights":
+        dw = cls(params.config, device)
+        dw.load(params)
+        return dw
+
+    def load(self, params: ModelParams) -> None:
+        host = np.concatenate([np.asarray(params.arrays[s.name], dtype=np.float64).ravel()
+                               for s in self.specs])
+        self.flat.copy_(torch.from_numpy(host.astype(np.float32)))
+
+    def to_numpy(self, grads: bool = False) -> dict:
+        src = (self.grad_flat if grads else self.flat).detach().double().cpu().numpy()
+        return {s.name: src[a:b].reshape(s.shape).copy()
+                for s, a, b in zip(self.specs, self.offsets[:-1], self.offsets[1:])}
+
+    def sgd_(self, lr: float) -> None:
+        """w -= lr * g (tasks.py:207-208)."""
+        ops.sgd_(self.flat, self.grad_flat, lr)
+
+
+@dataclass
+class ForwardResult:
+    energy: torch.Tensor  # [G]
+    forces: torch.Tensor | None  # [V, 3] (gemnet direct head)
+    m: torch.Tensor  # final edge features [E, d_e]
+    v: torch.Tensor  # final node features [V, d_v]
+    u: torch.Tensor  # final global features [G, d_u]
+    rbf: torch.Tensor
+    blocks: list = field(default_factory=list)
+    scale: torch.Tensor | None = None
+
+
+class Engine:
+    """Forward/backward of one model configuration over BatchGraphs."""
+
+    def __init__(self, weights: DeviceWeights):
+        self.weights = weights
+        self.config = weights.config
+
+    # -- helpers -----------------------------------------------------------
+    def _sbf_weight(self, b: int) -> torch.Tensor:
+        """W[k, l, c] = W'[c, k*L + l] with W' = W_sbf (dimenet) or B W_sbf (gemnet)."""
+        c, w = self.config, self.weights.w
+        p = f"block{b}.tu."
+        wp = w[p + "sbf_gate"]
+        if c.variant == GEMNET:
+            wp = w[p + "bilinear_b"] @ wp
+        dg = wp.shape[0]
+        return wp.view(dg, c.k_rbf, c.l_sbf).permute(1, 2, 0).contiguous()
+
+    # -- forward -------------------------------------------------------------
+    def forward(self, bg: BatchGraph) -> ForwardResult:
+        c, w = self.config, self.weights.w
+        gem = c.variant == GEMNET
+        rbf = ops.rbf(bg.geo, c.k_rbf, c.cutoff)
+        m = torch.addmm(w["edge_init.b"], rbf, w["edge_init.w"].t())
+        u = torch.zeros((bg.num_graphs, c.d_u), dtype=torch.float32, device=bg.device)
+        v = None
+        blocks = []
+        for b in range(c.blocks):
+            p = f"block{b}."
+            st = {}
+            down = m @ w[p + "tu.down"].t()
+            X = down @ w[p + "tu.bilinear_a"].t() if gem else down
+            Wk = self._sbf_weight(b)
+            S = ops.triplet_fwd(bg.edge_ptr, bg.rev, bg.geo, X, Wk, c.cutoff)
+            g = rbf @ w[p + "tu.rbf_gate"].t()
+            if gem:
+                Z = S @ w[p + "tu.bilinear_proj"].t()
+                Y = Z * g
+                st["Z"] = Z
+            else:
+                Y = S * g
+            ta = Y @ w[p + "tu.up"].t()
+            xcat = torch.cat([m, ta], dim=1)
+            h = torch.addmm(w[p + "eu.b1"], xcat, w[p + "eu.w1"].t())
+            a1 = F.silu(h)
+            m_new = torch.addmm(w[p + "eu.b2"], a1, w[p + "eu.w2"].t()).add_(m)
+            st.update(down=down, X=X, Wk=Wk, S=S, g=g, Y=Y, xcat=xcat, h=h, a1=a1, m_new=m_new)
+            agg = ops.aggregate_in_edges(bg.edge_ptr, bg.rev, m_new)
+            hv = torch.addmm(w[p + "nu.b1"], agg, w[p + "nu.w1"].t())
+            av = F.silu(hv)
+            v = torch.addmm(w[p + "nu.b2"], av, w[p + "nu.w2"].t())
+            st.update(agg=agg, hv=hv, av=av, v=v)
+            if gem:
+                w1 = w[p + "eu2.w1"]
+                pv = v @ w1[:, c.d_e:].t()
+                h2 = torch.addmm(w[p + "eu2.b1"], m_new, w1[:, : c.d_e].t())
+                ops.gather_rows(bg.recv, pv, out=h2, accumulate=True)
+                a2 = F.silu(h2)
+                m2 = torch.addmm(w[p + "eu2.b2"], a2, w[p + "eu2.w2"].t()).add_(m_new)
+                m2r = ops.gather_rows(bg.rev, m2)
+                m = torch.addmm(m2, m2r, w[p + "sym.w"].t())
+                st.update(h2=h2, a2=a2, m2r=m2r)
+            else:
+                m = m_new
+            s = ops.graph_sum(bg.graph_ptr, v)
+            pre = torch.addmm(w[p + "gu.b1"], s, w[p + "gu.w1"].t())
+            act = F.silu(pre)
+            u = torch.addmm(w[p + "gu.b2"], act, w[p + "gu.w2"].t()).add_(u)
+            st.update(s=s, pre=pre, act=act)
+            blocks.append(st)
+        energy = torch.addmm(w["energy_head.b"], u, w["energy_head.w"].t()).view(-1)
+        forces = scale = None
+        if gem:
+            scale, forces = ops.force_head_fwd(bg.edge_ptr, bg.rev, bg.geo, m, w["force_head.w"].view(-1))
+        if v is None:
+            v = torch.zeros((bg.num_nodes, c.d_v), device=bg.device)
+        return ForwardResult(energy, forces, m, v, u, rbf, blocks, scale)
+
+    # -- backward ------------------------------------------------------------
+    def backward(self, bg: BatchGraph, fw: ForwardResult, d_energy: torch.Tensor,
+                 d_forces: torch.Tensor | None = None) -> torch.Tensor:
+        """Overwrite weights.grad_flat with dL/dW; return dL/dpositions (f64 [V,3])."""
+        c, w, gr = self.config, self.weights.w, self.weights.g
+        gem = c.variant == GEMNET
+        if d_forces is not None and not gem:
+            raise ValueError("force seed given but this variant has no force head")
+        de = c.d_e
+        self.weights.grad_flat.zero_()
+        eg = torch.zeros((bg.num_edges, 4), dtype=torch.float32, device=bg.device)
+        dE = d_energy.to(torch.float32).view(-1, 1)
+        torch.mm(dE.t(), fw.u, out=gr["energy_head.w"])
+        gr["energy_head.b"].copy_(dE.sum(0))
+        u_bar = dE @ w["energy_head.w"]
+        m_bar = torch.zeros((bg.num_edges, de), dtype=torch.float32, device=bg.device)
+        if gem and d_forces is not None:
+            ops.force_head_bwd(bg.recv, bg.geo, fw.m, w["force_head.w"].view(-1), fw.scale,
+                               d_forces.to(torch.float32).contiguous(), m_bar, eg,
+                               w_bar=gr["force_head.w"].view(-1))
+        rbf_bar = torch.zeros_like(fw.rbf)
+        for b in range(c.blocks - 1, -1, -1):
+            p = f"block{b}."
+            st = fw.blocks[b]
+            # GU (engine.py:207-217)
+            torch.mm(u_bar.t(), st["act"], out=gr[p + "gu.w2"])
+            gr[p + "gu.b2"].copy_(u_bar.sum(0))
+            pre_bar = _silu_bwd(u_bar @ w[p + "gu.w2"], st["pre"])
+            gr[p + "gu.b1"].copy_(pre_bar.sum(0))
+            torch.mm(pre_bar.t(), st["s"], out=gr[p + "gu.w1"])
+            s_bar = pre_bar @ w[p + "gu.w1"]
+            v_bar = ops.gather_rows(bg.node_graph, s_bar)
+            if gem:
+                # sym (engine.py:195-200)
+                torch.mm(m_bar.t(), st["m2r"], out=gr[p + "sym.w"])
+                t = m_bar @ w[p + "sym.w"]
+                m2_bar = ops.gather_rows(bg.rev, t, out=m_bar.clone(), accumulate=True)
+                # EU2 (engine.py:180-192)
+                torch.mm(m2_bar.t(), st["a2"], out=gr[p + "eu2.w2"])
+                gr[p + "eu2.b2"].copy_(m2_bar.sum(0))
+                h2_bar = _silu_bwd(m2_bar @ w[p + "eu2.w2"], st["h2"])
+                gr[p + "eu2.b1"].copy_(h2_bar.sum(0))
+                w1 = w[p + "eu2.w1"]
+                gr[p + "eu2.w1"][:, :de].copy_(h2_bar.t() @ st["m_new"])
+                pv_bar = ops.aggregate_in_edges(bg.edge_ptr, bg.rev, h2_bar)
+                gr[p + "eu2.w1"][:, de:].copy_(pv_bar.t() @ st["v"])
+                v_bar = torch.addmm(v_bar, pv_bar, w1[:, de:])
+                m_new_bar = torch.addmm(m2_bar, h2_bar, w1[:, :de])
+            else:
+                m_new_bar = m_bar
+            # EA + NU (engine.py:166-177)
+            torch.mm(v_bar.t(), st["av"], out=gr[p + "nu.w2"])
+            gr[p + "nu.b2"].copy_(v_bar.sum(0))
+            hv_bar = _silu_bwd(v_bar @ w[p + "nu.w2"], st["hv"])
+            gr[p + "nu.b1"].copy_(hv_bar.sum(0))
+            torch.mm(hv_bar.t(), st["agg"], out=gr[p + "nu.w1"])
+            agg_bar = hv_bar @ w[p + "nu.w1"]
+            if m_new_bar is m_bar:
+                m_new_bar = m_bar.clone()
+            ops.gather_rows(bg.recv, agg_bar, out=m_new_bar, accumulate=True)
+            # EU (engine.py:152-158)
+            torch.mm(m_new_bar.t(), st["a1"], out=gr[p + "eu.w2"])
+            gr[p + "eu.b2"].copy_(m_new_bar.sum(0))
+            h_bar = _silu_bwd(m_new_bar @ w[p + "eu.w2"], st["h"])
+            gr[p + "eu.b1"].copy_(h_bar.sum(0))
+            torch.mm(h_bar.t(), st["xcat"], out=gr[p + "eu.w1"])
+            x_bar = h_bar @ w[p + "eu.w1"]
+            m_in_bar = m_new_bar + x_bar[:, :de]
+            ta_bar = x_bar[:, de:]
+            # TU (engine.py:118-149)
+            torch.mm(ta_bar.t(), st["Y"], out=gr[p + "tu.up"])
+            Y_bar = ta_bar @ w[p + "tu.up"]
+            if gem:
+                Z_bar = Y_bar * st["g"]
+                g_bar = Y_bar * st["Z"]
+                torch.mm(Z_bar.t(), st["S"], out=gr[p + "tu.bilinear_proj"])
+                S_bar = Z_bar @ w[p + "tu.bilinear_proj"]
+            else:
+                S_bar = Y_bar * st["g"]
+                g_bar = Y_bar * st["S"]
+            torch.mm(g_bar.t(), fw.rbf, out=gr[p + "tu.rbf_gate"])
+            rbf_bar.addmm_(g_bar, w[p + "tu.rbf_gate"])
+            X_bar, Wk_bar = ops.triplet_bwd(bg.edge_ptr, bg.rev, bg.geo, st["X"], st["Wk"], c.cutoff,
+                                            S_bar, eg)
+            wp_bar = Wk_bar.permute(2, 0, 1).reshape(Wk_bar.shape[2], -1)  # [dg, K*L]
+            if gem:
+                torch.mm(wp_bar, w[p + "tu.sbf_gate"].t(), out=gr[p + "tu.bilinear_b"])
+                torch.mm(w[p + "tu.bilinear_b"].t(), wp_bar, out=gr[p + "tu.sbf_gate"])
+                torch.mm(X_bar.t(), st["down"], out=gr[p + "tu.bilinear_a"])
+                down_bar = X_bar @ w[p + "tu.bilinear_a"]
+            else:
+                gr[p + "tu.sbf_gate"].copy_(wp_bar)
+                down_bar = X_bar
+            m_in = st["xcat"][:, :de]
+            torch.mm(down_bar.t(), m_in, out=gr[p + "tu.down"])
+            m_bar = m_in_bar.addmm_(down_bar, w[p + "tu.down"])
+        # edge init (engine.py:109-111)
+        torch.mm(m_bar.t(), fw.rbf, out=gr["edge_init.w"])
+        gr["edge_init.b"].copy_(m_bar.sum(0))
+        rbf_bar.addmm_(m_bar, w["edge_init.w"])
+        ops.rbf_bwd(bg.geo, rbf_bar, c.cutoff, eg)
+        return ops.positions_bwd(bg.edge_ptr, bg.rev, bg.geo, eg)
+
+    # -- debug / parity ------------------------------------------------------
+    def triplet_features(self, bg: BatchGraph, fw: ForwardResult, block: int) -> torch.Tensor:
+        """t_feat of one block for every triplet in (out, in) order (engine.py:146,149)."""
+        c, w = self.config, self.weights.w
+        st = fw.blocks[block]
+        P = ops.triplet_terms(bg.edge_ptr, bg.rev, bg.geo, bg.tri_ptr, bg.num_triplets, st["X"], st["Wk"],
+                              c.cutoff)
+        _, ji = ops.triplets_fill(bg.edge_ptr, bg.rev, bg.tri_ptr, bg.num_triplets)
+        gt = st["g"].index_select(0, ji)
+        if c.variant == GEMNET:
+            return (P @ w[f"block{block}.tu.bilinear_proj"].t()) * gt
+        return P * gt

@@ -1,0 +1,187 @@
+"""Cutoff graphs on the GPU: neighbour list, triplets, reverse edges, geometry.
+
+``build_graph(system, cutoff)`` mirrors egn/graph.py:82-103 and returns the
+same two containers (GraphTopology, Geometry) holding CUDA tensors; the
+index arrays are bit-identical to the reference's (int64 at this API, int32
+inside the kernels).  ``BatchGraph`` is the model's device-resident form of
+a batch of graphs (disjoint union, graphs concatenated): it never
+materialises per-triplet arrays -- triplets are implicit in the centre
+tiles (see include/egn_b200.h).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import ops
+
+
+@dataclass
+class BatchGraph:
+    """Device-resident topology + packed geometry of G concatenated graphs."""
+
+    num_graphs: int
+    num_nodes: int
+    num_edges: int
+    num_triplets: int
+    cutoff: float
+    pos: torch.Tensor  # f64 [V, 3]
+    graph_ptr: torch.Tensor  # i64 [G+1]
+    node_graph: torch.Tensor  # i32 [V]
+    deg: torch.Tensor  # i32 [V]
+    edge_ptr: torch.Tensor  # i64 [V+1]  CSR of out-edges by source
+    src: torch.Tensor  # i32 [E]
+    recv: torch.Tensor  # i32 [E]
+    rev: torch.Tensor  # i32 [E]
+    tri_ptr: torch.Tensor  # i64 [V+1]  triplet offsets per centre
+    geo: torch.Tensor  # f32 [E, 4]  (ux, uy, uz, d)
+    graph_sizes: list  # host: atoms per graph
+    edge_counts: list | None = None  # host: edges per graph (lazily)
+
+    @property
+    def device(self):
+        return self.pos.device
+
+    def edge_graph_ptr(self) -> torch.Tensor:
+        return self.edge_ptr[self.graph_ptr]
+
+
+def _as_positions(systems) -> tuple[np.ndarray, list[int]]:
+    if hasattr(systems, "positions") or (isinstance(systems, np.ndarray) and systems.ndim == 2):
+        systems = [systems]
+    pos = [np.asarray(s.positions if hasattr(s, "positions") else s, dtype=np.float64) for s in systems]
+    return (np.concatenate(pos, axis=0) if pos else np.zeros((0, 3))), [p.shape[0] for p in pos]
+
+
+def build_batch(systems, cutoff: float, device="cuda", positions: torch.Tensor | None = None,
+                sizes: list[int] | None = None) -> BatchGraph:
+    """Build the batched device graph.  ``systems``: an AtomicSystem, a list of
+    them, or raw (n,3) position arrays; alternatively pass device ``positions``
+    (f64 [V,3]) and ``sizes`` directly (no host->device copy of positions)."""
+    if cutoff <= 0:
+        raise ValueError("cutoff must be positive")
+    if positions is None:
+        pos_np, sizes = _as_positions(systems)
+        pos = torch.from_numpy(pos_np).to(device)
+    else:
+        pos = positions.to(torch.float64).contiguous()
+        if sizes is None:
+            sizes = [pos.shape[0]]
+    dev = pos.device
+    g = len(sizes)
+    gp = np.zeros(g + 1, dtype=np.int64)
+    gp[1:] = np.cumsum(sizes)
+    graph_ptr = torch.from_numpy(gp).to(dev)
+    node_graph = torch.from_numpy(np.repeat(np.arange(g, dtype=np.int32), sizes)).to(dev)
+    deg = ops.neighbors_count(pos, graph_ptr, node_graph, cutoff)
+    edge_ptr = ops.scan_counts(deg)
+    tri_ptr = ops.scan_counts(deg, square_minus_one=True)
+    counts = torch.stack([edge_ptr[-1], tri_ptr[-1]]).cpu()  # the one host sync
+    ne, nt = int(counts[0]), int(counts[1])
+    src, recv = ops.neighbors_fill(pos, graph_ptr, node_graph, cutoff, edge_ptr, ne)
+    rev, missing = ops.reverse_edges(edge_ptr, src, recv)
+    geo, _, _ = ops.geometry(pos, src, recv)
+    return BatchGraph(g, int(pos.shape[0]), ne, nt, float(cutoff), pos, graph_ptr, node_graph, deg,
+                      edge_ptr, src, recv, rev, tri_ptr, geo, list(sizes))
+
+
+# ---------------------------------------------------------------------------
+# reference-shaped API (egn/graph.py)
+# ---------------------------------------------------------------------------
+
+
+@dataclass(frozen=True)
+class GraphTopology:
+    """Directed edges and triplets (egn/graph.py:22-70), CUDA int64 tensors."""
+
+    num_nodes: int
+    edge_src: torch.Tensor
+    edge_recv: torch.Tensor
+    trip_in: torch.Tensor  # id3_kj
+    trip_out: torch.Tensor  # id3_ji
+    _rev: torch.Tensor | None = None
+
+    @property
+    def num_edges(self) -> int:
+        return int(self.edge_src.shape[0])
+
+    @property
+    def num_triplets(self) -> int:
+        return int(self.trip_in.shape[0])
+
+    def reverse_edges(self) -> torch.Tensor:
+        """rev with edges[rev[k]] == (recv_k, src_k); ValueError if some edge has no partner."""
+        if self._rev is not None:
+            return self._rev
+        src = self.edge_src.to(torch.int32)
+        recv = self.edge_recv.to(torch.int32)
+        deg = torch.bincount(self.edge_src, minlength=self.num_nodes).to(torch.int32)
+        edge_ptr = ops.scan_counts(deg)
+        rev, missing = ops.reverse_edges(edge_ptr, src, recv)
+        if int(missing.item()):
+            bad = int(torch.nonzero(rev < 0)[0].item())
+            raise ValueError(f"edge {bad} has no reverse edge "
+                             f"{(int(self.edge_recv[bad]), int(self.edge_src[bad]))}")
+        return rev.to(torch.int64)
+
+    def validate(self) -> None:
+        s, r = self.edge_src, self.edge_recv
+        if self.num_edges and bool(((s == r) | (s < 0) | (r >= self.num_nodes)).any()):
+            raise ValueError("malformed edge list")
+        if self.num_triplets:
+            if bool(((self.trip_in >= self.num_edges) | (self.trip_out >= self.num_edges)).any()):
+                raise ValueError("triplet references edge out of range")
+            if bool((r[self.trip_in] != s[self.trip_out]).any()):
+                raise ValueError("triplet edges do not share a middle atom")
+            if bool((s[self.trip_in] == r[self.trip_out]).any()):
+                raise ValueError("triplet with k == i")
+
+
+@dataclass(frozen=True)
+class Geometry:
+    distances: torch.Tensor  # f64 [E]
+    unit_vectors: torch.Tensor  # f64 [E, 3]
+    angles: torch.Tensor  # f64 [N_t]
+
+
+def build_graph(system, cutoff: float, device="cuda") -> tuple[GraphTopology, Geometry]:
+    """Directed cutoff graph + geometry of one system (egn/graph.py:82-103)."""
+    bg = build_batch(system, cutoff, device)
+    return topology_of(bg), geometry_of(bg)
+
+
+def topology_of(bg: BatchGraph) -> GraphTopology:
+    kj, ji = ops.triplets_fill(bg.edge_ptr, bg.rev, bg.tri_ptr, bg.num_triplets)
+    return GraphTopology(bg.num_nodes, bg.src.to(torch.int64), bg.recv.to(torch.int64), kj, ji,
+                         bg.rev.to(torch.int64))
+
+
+def geometry_of(bg: BatchGraph) -> Geometry:
+    _, d64, u64 = ops.geometry(bg.pos, bg.src, bg.recv, want_fp64=True)
+    ang = ops.triplet_angles(bg.pos, bg.edge_ptr, bg.recv, bg.tri_ptr, bg.num_triplets)
+    return Geometry(d64, u64, ang)
+
+
+def enumerate_triplets(num_nodes, edge_src=None, edge_recv=None):
+    """((k->j),(j->i)) pairs with k != i sorted by (out, in) (egn/graph.py:106-139).
+
+    Accepts (num_nodes, edge_src, edge_recv) or a GraphTopology; edges must be
+    sorted by (src, recv) as build_graph produces them."""
+    if isinstance(num_nodes, GraphTopology):
+        t = num_nodes
+        num_nodes, edge_src, edge_recv = t.num_nodes, t.edge_src, t.edge_recv
+    edge_src = torch.as_tensor(edge_src, device="cuda")
+    edge_recv = torch.as_tensor(edge_recv, device="cuda")
+    if edge_src.numel() == 0:
+        e = torch.empty(0, dtype=torch.int64, device="cuda")
+        return e, e
+    deg = torch.bincount(edge_src.to(torch.int64), minlength=int(num_nodes)).to(torch.int32)
+    edge_ptr = ops.scan_counts(deg)
+    tri_ptr = ops.scan_counts(deg, square_minus_one=True)
+    rev, missing = ops.reverse_edges(edge_ptr, edge_src.to(torch.int32), edge_recv.to(torch.int32))
+    if int(missing.item()):
+        raise ValueError("edge list is not symmetric; triplets are defined on cutoff graphs")
+    return ops.triplets_fill(edge_ptr, rev, tri_ptr, int(tri_ptr[-1].item()))

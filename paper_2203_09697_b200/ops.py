@@ -1,0 +1,197 @@
+"""Torch-tensor wrappers over the C ABI (include/egn_b200.h).
+
+Each function allocates its outputs with torch (device memory + the
+caching allocator are the only things torch provides here), launches the
+native kernels on the current stream and returns.  Inputs must be CUDA
+tensors of the documented dtype; there is no CPU path.
+"""
+
+from __future__ import annotations
+
+import torch
+
+from ._lib import call, ptr, stream
+
+
+def _c(t: torch.Tensor, dtype) -> torch.Tensor:
+    if t.dtype != dtype:
+        raise TypeError(f"expected {dtype}, got {t.dtype}")
+    return t.contiguous()
+
+
+def neighbors_count(pos, graph_ptr, node_graph, cutoff):
+    n = pos.shape[0]
+    deg = torch.empty(n, dtype=torch.int32, device=pos.device)
+    call("egn_neighbors_count", ptr(pos), ptr(graph_ptr), ptr(node_graph), n, float(cutoff), ptr(deg), stream())
+    return deg
+
+
+def scan_counts(counts, square_minus_one=False):
+    out = torch.empty(counts.shape[0] + 1, dtype=torch.int64, device=counts.device)
+    call("egn_scan_counts", ptr(counts), counts.shape[0], int(square_minus_one), ptr(out), stream())
+    return out
+
+
+def neighbors_fill(pos, graph_ptr, node_graph, cutoff, edge_ptr, num_edges):
+    src = torch.empty(num_edges, dtype=torch.int32, device=pos.device)
+    recv = torch.empty(num_edges, dtype=torch.int32, device=pos.device)
+    call("egn_neighbors_fill", ptr(pos), ptr(graph_ptr), ptr(node_graph), pos.shape[0], float(cutoff),
+         ptr(edge_ptr), ptr(src), ptr(recv), stream())
+    return src, recv
+
+
+def reverse_edges(edge_ptr, src, recv, missing=None):
+    rev = torch.empty_like(src)
+    if missing is None:
+        missing = torch.zeros(1, dtype=torch.int32, device=src.device)
+    call("egn_reverse_edges", ptr(edge_ptr), ptr(src), ptr(recv), src.shape[0], ptr(rev), ptr(missing), stream())
+    return rev, missing
+
+
+def triplets_fill(edge_ptr, rev, tri_ptr, num_triplets):
+    n = edge_ptr.shape[0] - 1
+    kj = torch.empty(num_triplets, dtype=torch.int64, device=rev.device)
+    ji = torch.empty(num_triplets, dtype=torch.int64, device=rev.device)
+    call("egn_triplets_fill", ptr(edge_ptr), ptr(rev), ptr(tri_ptr), n, ptr(kj), ptr(ji), stream())
+    return kj, ji
+
+
+def geometry(pos, src, recv, want_fp64=False):
+    e = src.shape[0]
+    geo = torch.empty((e, 4), dtype=torch.float32, device=pos.device)
+    d64 = u64 = None
+    if want_fp64:
+        d64 = torch.empty(e, dtype=torch.float64, device=pos.device)
+        u64 = torch.empty((e, 3), dtype=torch.float64, device=pos.device)
+    call("egn_geometry", ptr(pos), ptr(src), ptr(recv), e, ptr(geo), ptr(d64), ptr(u64), stream())
+    return geo, d64, u64
+
+
+def triplet_angles(pos, edge_ptr, recv, tri_ptr, num_triplets):
+    out = torch.empty(num_triplets, dtype=torch.float64, device=pos.device)
+    call("egn_triplet_angles", ptr(pos), ptr(edge_ptr), ptr(recv), ptr(tri_ptr), pos.shape[0], ptr(out), stream())
+    return out
+
+
+def rbf(geo, k_rbf, cutoff):
+    out = torch.empty((geo.shape[0], k_rbf), dtype=torch.float32, device=geo.device)
+    call("egn_rbf", ptr(geo), geo.shape[0], int(k_rbf), float(cutoff), ptr(out), stream())
+    return out
+
+
+def sbf(geo, edge_ptr, tri_ptr, num_triplets, k_rbf, l_sbf, cutoff):
+    out = torch.empty((num_triplets, k_rbf * l_sbf), dtype=torch.float32, device=geo.device)
+    call("egn_sbf", ptr(geo), ptr(edge_ptr), ptr(tri_ptr), edge_ptr.shape[0] - 1, int(k_rbf), int(l_sbf),
+         float(cutoff), ptr(out), stream())
+    return out
+
+
+def triplet_fwd(edge_ptr, rev, geo, X, Wk, cutoff):
+    """S = sum over the centre tile (see include/egn_b200.h egn_triplet_fwd)."""
+    X = _c(X, torch.float32)
+    Wk = _c(Wk, torch.float32)
+    k, l, dg = Wk.shape
+    S = torch.empty_like(X)
+    call("egn_triplet_fwd", ptr(edge_ptr), ptr(rev), ptr(geo), edge_ptr.shape[0] - 1, ptr(X), ptr(Wk),
+         k, l, dg, float(cutoff), ptr(S), stream())
+    return S
+
+
+_WS: dict = {}
+
+
+def _workspace(nbytes: int, device) -> torch.Tensor:
+    key = (str(device), "ws")
+    buf = _WS.get(key)
+    if buf is None or buf.numel() < nbytes:
+        buf = torch.empty(max(nbytes, 1 << 20), dtype=torch.uint8, device=device)
+        _WS[key] = buf
+    return buf
+
+
+def triplet_bwd(edge_ptr, rev, geo, X, Wk, cutoff, S_bar, edge_grad, X_bar=None, W_bar=None):
+    X = _c(X, torch.float32)
+    Wk = _c(Wk, torch.float32)
+    S_bar = _c(S_bar, torch.float32)
+    k, l, dg = Wk.shape
+    nv = edge_ptr.shape[0] - 1
+    if X_bar is None:
+        X_bar = torch.empty_like(X)
+    if W_bar is None:
+        W_bar = torch.empty_like(Wk)
+    nbytes = call("egn_triplet_bwd_workspace_bytes", nv, k, l, dg)
+    ws = _workspace(nbytes, X.device)
+    call("egn_triplet_bwd", ptr(edge_ptr), ptr(rev), ptr(geo), nv, ptr(X), ptr(Wk), k, l, dg, float(cutoff),
+         ptr(S_bar), ptr(X_bar), ptr(W_bar), ptr(edge_grad), ptr(ws), stream())
+    return X_bar, W_bar
+
+
+def triplet_terms(edge_ptr, rev, geo, tri_ptr, num_triplets, X, Wk, cutoff):
+    k, l, dg = Wk.shape
+    out = torch.empty((num_triplets, dg), dtype=torch.float32, device=X.device)
+    call("egn_triplet_terms", ptr(edge_ptr), ptr(rev), ptr(geo), ptr(tri_ptr), edge_ptr.shape[0] - 1,
+         ptr(_c(X, torch.float32)), ptr(_c(Wk, torch.float32)), k, l, dg, float(cutoff), ptr(out), stream())
+    return out
+
+
+def aggregate_in_edges(edge_ptr, rev, x, out=None):
+    nv = edge_ptr.shape[0] - 1
+    d = x.shape[1]
+    if out is None:
+        out = torch.empty((nv, d), dtype=torch.float32, device=x.device)
+    call("egn_aggregate_in_edges", ptr(edge_ptr), ptr(rev), nv, ptr(x), x.stride(0), d, ptr(out), stream())
+    return out
+
+
+def gather_rows(idx, x, out=None, accumulate=False):
+    rows = idx.shape[0]
+    d = x.shape[1]
+    if out is None:
+        out = torch.empty((rows, d), dtype=torch.float32, device=x.device)
+    call("egn_gather_rows", ptr(idx), rows, ptr(x), x.stride(0), d, ptr(out), out.stride(0), int(accumulate),
+         stream())
+    return out
+
+
+def graph_sum(graph_ptr, x):
+    g = graph_ptr.shape[0] - 1
+    out = torch.empty((g, x.shape[1]), dtype=torch.float32, device=x.device)
+    call("egn_graph_sum", ptr(graph_ptr), g, ptr(_c(x, torch.float32)), x.shape[1], ptr(out), stream())
+    return out
+
+
+def force_head_fwd(edge_ptr, rev, geo, m, w):
+    nv = edge_ptr.shape[0] - 1
+    ne = m.shape[0]
+    scale = torch.empty(ne, dtype=torch.float32, device=m.device)
+    forces = torch.empty((nv, 3), dtype=torch.float32, device=m.device)
+    call("egn_force_head_fwd", ptr(edge_ptr), ptr(rev), ptr(geo), nv, ne, ptr(_c(m, torch.float32)), m.shape[1],
+         ptr(_c(w, torch.float32)), ptr(scale), ptr(forces), stream())
+    return scale, forces
+
+
+def force_head_bwd(recv, geo, m, w, scale, f_bar, m_bar, edge_grad, w_bar=None):
+    ne, d = m.shape
+    if w_bar is None:
+        w_bar = torch.empty(d, dtype=torch.float32, device=m.device)
+    nbytes = call("egn_force_head_bwd_workspace_bytes", ne, d)
+    ws = _workspace(nbytes, m.device)
+    call("egn_force_head_bwd", ptr(recv), ptr(geo), ne, ptr(m), d, ptr(w), ptr(scale), ptr(_c(f_bar, torch.float32)),
+         ptr(m_bar), ptr(w_bar), ptr(edge_grad), ptr(ws), stream())
+    return w_bar
+
+
+def rbf_bwd(geo, rbf_bar, cutoff, edge_grad):
+    ne, k = rbf_bar.shape
+    call("egn_rbf_bwd", ptr(geo), ptr(_c(rbf_bar, torch.float32)), ne, k, float(cutoff), ptr(edge_grad), stream())
+
+
+def positions_bwd(edge_ptr, rev, geo, edge_grad):
+    nv = edge_ptr.shape[0] - 1
+    out = torch.empty((nv, 3), dtype=torch.float64, device=geo.device)
+    call("egn_positions_bwd", ptr(edge_ptr), ptr(rev), ptr(geo), nv, ptr(edge_grad), ptr(out), stream())
+    return out
+
+
+def sgd_(w, g, lr):
+    call("egn_sgd", ptr(w), ptr(g), w.numel(), float(lr), stream())

@@ -1,0 +1,147 @@
+"""Model-level drivers on the GPU: predict, loss_and_grads, train_simple.
+
+Same signatures and semantics as egn/tasks.py:37-67 (predict), :131-185
+(loss_and_grads) and :188-209 (train_simple); the per-sample loop of the
+reference becomes one batched forward/backward over the disjoint union of
+all samples (per-graph energies and per-graph global state are kept
+separate, so the result equals the per-graph loop).  ``Trainer`` is the
+device-resident training step used by bench.py: inputs, targets and
+weights stay in HBM between steps.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from .config import GEMNET
+from .engine import DeviceWeights, Engine
+from .graph import BatchGraph, build_batch
+from .params import ModelParams
+
+
+def _check_workers(config, workers):
+    p = config.workers if workers is None else workers
+    if p < 1:
+        raise ValueError("workers must be >= 1")
+    return p
+
+
+def predict(system, params: ModelParams, workers: int | None = None, device="cuda"):
+    """Energy and forces of one system (tasks.py:37-67)."""
+    config = params.config
+    _check_workers(config, workers)
+    if config.diagnostic:
+        raise ValueError("the diagnostic quadratic-well model is a test fixture, not part of this path")
+    bg = build_batch(system, config.cutoff, device)
+    eng = Engine(DeviceWeights.from_params(params, device))
+    fw = eng.forward(bg)
+    if config.variant == GEMNET:
+        return float(fw.energy[0]), fw.forces.double().cpu().numpy()
+    pos_bar = eng.backward(bg, fw, torch.ones(1, device=bg.device))
+    return float(fw.energy[0]), (-pos_bar).cpu().numpy()
+
+
+def _seeds(energy, forces, e_target, f_target, atom_count, w_energy, w_forces, n):
+    """Loss and its seeds, per sample as tasks.py:166-176 computes them."""
+    res = energy.double() - e_target
+    loss = (w_energy * res * res).sum() / n
+    d_energy = 2.0 * w_energy * res / n
+    d_forces = None
+    if w_forces != 0.0:
+        delta = forces.double() - f_target
+        loss = loss + w_forces * ((delta * delta).sum(dim=1) / atom_count).sum() / n
+        d_forces = 2.0 * w_forces * delta / (n * atom_count[:, None])
+    return loss, d_energy, d_forces
+
+
+class Trainer:
+    """Device-resident SGD training step over a fixed batch (train_simple's inner loop)."""
+
+    def __init__(self, params: ModelParams, systems, e_target, f_target=None, w_energy=1.0,
+                 w_forces=0.0, device="cuda", graph: BatchGraph | None = None):
+        c = params.config
+        if w_forces != 0.0 and c.variant != GEMNET:
+            raise ValueError("force-loss gradients require the force-centric variant; "
+                             "set w_forces=0 for energy-centric training")
+        self.config = c
+        self.weights = DeviceWeights.from_params(params, device)
+        self.engine = Engine(self.weights)
+        self.bg = graph if graph is not None else build_batch(systems, c.cutoff, device)
+        bg = self.bg
+        self.n = bg.num_graphs
+        if self.n == 0:
+            raise ValueError("dataset is empty")
+        self.e_target = torch.as_tensor(np.asarray(e_target, dtype=np.float64), device=bg.device)
+        self.f_target = (torch.as_tensor(np.asarray(f_target, dtype=np.float64), device=bg.device)
+                         if f_target is not None else None)
+        sizes = torch.as_tensor(bg.graph_sizes, dtype=torch.float64, device=bg.device)
+        self.atom_count = sizes.repeat_interleave(torch.as_tensor(bg.graph_sizes, device=bg.device))
+        self.w_energy, self.w_forces = float(w_energy), float(w_forces)
+
+    def set_inputs(self, bg: BatchGraph, e_target: torch.Tensor, f_target: torch.Tensor | None) -> None:
+        """Swap in a new batch (same graph sizes) and targets already on the device."""
+        if bg.graph_sizes != self.bg.graph_sizes:
+            raise ValueError("set_inputs expects the same per-graph atom counts")
+        self.bg, self.e_target, self.f_target = bg, e_target, f_target
+
+    def loss_and_grads(self):
+        fw = self.engine.forward(self.bg)
+        loss, d_e, d_f = _seeds(fw.energy, fw.forces, self.e_target, self.f_target, self.atom_count,
+                                self.w_energy, self.w_forces, self.n)
+        self.engine.backward(self.bg, fw, d_e, d_f)
+        return loss
+
+    def step(self, lr: float) -> torch.Tensor:
+        loss = self.loss_and_grads()
+        if lr != 0.0:
+            self.weights.sgd_(lr)
+        return loss
+
+    def params(self) -> ModelParams:
+        return ModelParams(self.config, self.weights.to_numpy())
+
+
+def _unpack(dataset):
+    systems = [s for s, _, _ in dataset]
+    e_t = [float(e) for _, e, _ in dataset]
+    f_t = None
+    if all(f is not None for _, _, f in dataset):
+        f_t = np.concatenate([np.asarray(f, dtype=np.float64) for _, _, f in dataset], axis=0)
+    return systems, e_t, f_t
+
+
+def loss_and_grads(dataset, params: ModelParams, w_energy: float = 1.0, w_forces: float = 0.0,
+                   workers: int | None = None, device="cuda"):
+    """Mean squared loss over the dataset and its gradient (tasks.py:131-185)."""
+    config = params.config
+    if config.diagnostic:
+        raise ValueError("the diagnostic model has no trainable parameters")
+    if w_forces != 0.0 and config.variant != GEMNET:
+        raise ValueError("force-loss gradients require the force-centric variant; "
+                         "set w_forces=0 for energy-centric training")
+    _check_workers(config, workers)
+    if len(dataset) == 0:
+        raise ValueError("dataset is empty")
+    systems, e_t, f_t = _unpack(dataset)
+    tr = Trainer(params, systems, e_t, f_t if w_forces != 0.0 else None, w_energy, w_forces, device)
+    loss = float(tr.loss_and_grads())
+    return loss, tr.weights.to_numpy(grads=True)
+
+
+def train_simple(dataset, params: ModelParams, lr: float, epochs: int, w_energy: float = 1.0,
+                 w_forces: float = 0.0, workers: int | None = None, device="cuda"):
+    """Plain gradient descent; returns fitted parameters and the loss history (tasks.py:188-209)."""
+    if len(dataset) == 0:
+        raise ValueError("dataset is empty")
+    systems, e_t, f_t = _unpack(dataset)
+    tr = Trainer(params, systems, e_t, f_t if w_forces != 0.0 else None, w_energy, w_forces, device)
+    history = []
+    for _ in range(epochs):
+        loss = float(tr.loss_and_grads())
+        if not np.isfinite(loss):
+            raise RuntimeError(f"non-finite loss {loss}")
+        history.append(loss)
+        if lr != 0.0:
+            tr.weights.sgd_(lr)
+    return tr.params(), history

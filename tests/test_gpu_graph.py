@@ -1,0 +1,105 @@
+"""Neighbour list / triplets / reverse edges / geometry on the GPU vs the reference.
+
+Topology is compared bit-exactly against the golden fixtures (reference
+outputs) and against the oracle on extra random systems, including batched
+(disjoint-union) builds."""
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import max_rel
+from oracle import egn_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def _gpu_graph(pos, cutoff):
+    from paper_2203_09697_b200.graph import build_graph
+
+    topo, geom = build_graph(pos, cutoff)
+    return topo, geom
+
+
+def test_graph_fixtures_bit_exact(graphs_golden):
+    data, names = graphs_golden
+    for name in names:
+        pos = data[f"{name}/pos"]
+        topo, geom = _gpu_graph(pos, float(data[f"{name}/cutoff"]))
+        for key, val in (("src", topo.edge_src), ("recv", topo.edge_recv), ("trip_in", topo.trip_in),
+                         ("trip_out", topo.trip_out), ("rev", topo.reverse_edges())):
+            np.testing.assert_array_equal(val.cpu().numpy(), data[f"{name}/{key}"], err_msg=f"{name}/{key}")
+        np.testing.assert_array_equal(geom.distances.cpu().numpy(), data[f"{name}/dist"], err_msg=name)
+        np.testing.assert_array_equal(geom.unit_vectors.cpu().numpy(), data[f"{name}/units"], err_msg=name)
+        np.testing.assert_allclose(geom.angles.cpu().numpy(), data[f"{name}/angles"], rtol=0, atol=1e-12)
+        topo.validate()
+
+
+@pytest.mark.parametrize("seed", range(50))
+def test_random_clouds_bit_exact_vs_oracle(seed):
+    rng = np.random.default_rng(1000 + seed)
+    n = int(rng.integers(2, 120))
+    rho = float(rng.choice([0.06, 0.2, 0.9]))
+    pos, _ = O.random_cloud(n, rho, rng)
+    cutoff = float(rng.choice([1.5, 3.0, 6.0]))
+    ref = O.build_graph(pos, cutoff)
+    topo, geom = _gpu_graph(pos, cutoff)
+    np.testing.assert_array_equal(topo.edge_src.cpu().numpy(), ref.src)
+    np.testing.assert_array_equal(topo.edge_recv.cpu().numpy(), ref.recv)
+    np.testing.assert_array_equal(topo.trip_in.cpu().numpy(), ref.trip_in)
+    np.testing.assert_array_equal(topo.trip_out.cpu().numpy(), ref.trip_out)
+    np.testing.assert_array_equal(topo.reverse_edges().cpu().numpy(), ref.rev)
+    np.testing.assert_array_equal(geom.distances.cpu().numpy(), ref.dist)
+
+
+def test_batched_union_equals_per_graph():
+    from paper_2203_09697_b200.graph import build_batch, topology_of
+
+    rng = np.random.default_rng(7)
+    systems = [O.random_cloud(int(k), 0.06, rng)[0] for k in (30, 1, 45, 2, 64)]
+    bg = build_batch(systems, 6.0)
+    topo = topology_of(bg)
+    e_off = t_off = n_off = 0
+    src = topo.edge_src.cpu().numpy()
+    kj = topo.trip_in.cpu().numpy()
+    ji = topo.trip_out.cpu().numpy()
+    for pos in systems:
+        ref = O.build_graph(pos, 6.0)
+        ne, nt = ref.src.size, ref.trip_in.size
+        np.testing.assert_array_equal(src[e_off:e_off + ne], ref.src + n_off)
+        np.testing.assert_array_equal(kj[t_off:t_off + nt], ref.trip_in + e_off)
+        np.testing.assert_array_equal(ji[t_off:t_off + nt], ref.trip_out + e_off)
+        e_off += ne
+        t_off += nt
+        n_off += pos.shape[0]
+    assert (bg.num_edges, bg.num_triplets) == (e_off, t_off)
+
+
+def test_enumerate_triplets_api_and_errors():
+    from paper_2203_09697_b200.graph import GraphTopology, build_graph, enumerate_triplets
+
+    tri = np.array([[0.0, 0, 0], [1.0, 0, 0], [0.5, np.sqrt(3) / 2, 0]])
+    topo, _ = build_graph(tri, 1.5)
+    kj, ji = enumerate_triplets(topo)
+    assert torch.equal(kj, topo.trip_in) and torch.equal(ji, topo.trip_out)
+    e = torch.empty(0, dtype=torch.int64, device="cuda")
+    a, b = enumerate_triplets(3, e, e)
+    assert a.numel() == 0 and b.numel() == 0
+    lop = GraphTopology(2, torch.tensor([0], device="cuda"), torch.tensor([1], device="cuda"), e, e)
+    with pytest.raises(ValueError):
+        lop.reverse_edges()
+    with pytest.raises(ValueError):
+        build_graph(tri, 0.0)
+
+
+def test_large_graph_neighbor_counts():
+    """1k atoms, mean degree ~50: bit-exact edges and triplet count."""
+    rng = np.random.default_rng(5)
+    pos, _ = O.random_cloud(1000, 0.1, rng)
+    ref_src, ref_recv = O.neighbor_list(pos, 5.0)
+    topo, geom = _gpu_graph(pos, 5.0)
+    np.testing.assert_array_equal(topo.edge_src.cpu().numpy(), ref_src)
+    np.testing.assert_array_equal(topo.edge_recv.cpu().numpy(), ref_recv)
+    deg = np.bincount(ref_src, minlength=1000)
+    assert topo.num_triplets == int((deg * (deg - 1)).sum())
+    assert max_rel(geom.distances.cpu().numpy(), np.sqrt(((pos[ref_recv] - pos[ref_src]) ** 2).sum(1))) == 0.0

@@ -1,0 +1,175 @@
+"""Whole-model parity on the GPU: energies, forces, every parameter gradient and
+the position gradient vs the reference (golden fixtures) and the fp64 oracle.
+
+Tolerance (north star): per tensor max|a-b| / max(max|b|, 1e-8) <= 1e-4.
+"""
+
+import json
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import GOLDEN, TOL, load_golden, max_rel
+from oracle import egn_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+SMALL = ["model_dimenet_small.npz", "model_gemnet_small.npz", "model_gemnet_odd.npz", "model_dimenet_chain.npz"]
+LARGE = ["model_dimenet_c1dims.npz", "model_gemnet_c2dims.npz"]
+
+
+def _setup(gd):
+    from paper_2203_09697_b200 import ModelConfig, init_params
+    from paper_2203_09697_b200.engine import DeviceWeights, Engine
+    from paper_2203_09697_b200.graph import build_batch
+
+    cfg = ModelConfig.from_json(str(gd["config"]))
+    params = init_params(cfg)
+    eng = Engine(DeviceWeights.from_params(params))
+    bg = build_batch([gd["pos"]], cfg.cutoff)
+    return cfg, params, eng, bg
+
+
+@pytest.mark.parametrize("fname", SMALL + LARGE)
+def test_model_matches_reference_golden(fname):
+    gd = load_golden(fname)
+    cfg, params, eng, bg = _setup(gd)
+    fw = eng.forward(bg)
+    d_forces = gd.get("d_forces")
+    df = torch.tensor(d_forces, device="cuda") if d_forces is not None else None
+    pos_bar = eng.backward(bg, fw, torch.tensor([0.7], device="cuda"), df)
+    grads = eng.weights.to_numpy(grads=True)
+    e_ref = float(gd["energy"])
+    assert abs(float(fw.energy[0]) - e_ref) <= TOL * max(abs(e_ref), 1e-8)
+    assert max_rel(fw.m.cpu().numpy(), gd["m"]) < TOL
+    assert max_rel(fw.v.cpu().numpy(), gd["v"]) < TOL
+    assert max_rel(fw.u.cpu().numpy(), gd["u"]) < TOL
+    assert max_rel(pos_bar.cpu().numpy(), gd["d_positions"]) < TOL
+    if cfg.variant == "gemnet-style":
+        assert max_rel(fw.forces.cpu().numpy(), gd["forces"]) < TOL
+    t_feat = eng.triplet_features(bg, fw, cfg.blocks - 1).cpu().numpy()
+    assert max_rel(t_feat, gd["t_feat"]) < TOL
+    for name in gd["param_names"]:
+        name = str(name)
+        if f"dp/{name}" in gd:
+            assert max_rel(grads[name], gd[f"dp/{name}"]) < TOL, name
+        else:
+            ref_head = gd[f"dphead/{name}"]
+            scale = max(float(gd[f"dpnorm/{name}"]), 1e-8)
+            assert np.abs(grads[name].ravel()[:64] - ref_head).max() / scale < TOL, name
+
+
+@pytest.mark.parametrize("variant", ["dimenet-style", "gemnet-style"])
+def test_full_dims_batched_vs_oracle(variant):
+    """C1/C2 model dims, a batch of 3 OC20-density graphs; every d_param vs the live oracle."""
+    from paper_2203_09697_b200 import ModelConfig, init_params
+    from paper_2203_09697_b200.engine import DeviceWeights, Engine
+    from paper_2203_09697_b200.graph import build_batch
+
+    cfg = ModelConfig(variant=variant, blocks=4, d_u=128, d_v=128, d_e=128, d_t=64, d_bil=64, k_rbf=6,
+                      l_sbf=7, cutoff=6.0, seed=0)
+    params = init_params(cfg)
+    oc = O.Config(**{k: getattr(cfg, k) for k in O.Config.__dataclass_fields__})
+    rng = np.random.default_rng(11)
+    systems = [O.random_cloud(n, 0.06, rng) for n in (20, 33, 27)]
+    eng = Engine(DeviceWeights.from_params(params))
+    bg = build_batch([s[0] for s in systems], cfg.cutoff)
+    fw = eng.forward(bg)
+    d_e = torch.tensor([0.3, -1.1, 0.6], device="cuda")
+    df = None
+    df_np = []
+    if variant == "gemnet-style":
+        df_np = [rng.standard_normal((s[0].shape[0], 3)) for s in systems]
+        df = torch.tensor(np.concatenate(df_np), device="cuda")
+    pos_bar = eng.backward(bg, fw, d_e, df).cpu().numpy()
+    grads = eng.weights.to_numpy(grads=True)
+    ref_g = {k: np.zeros_like(v) for k, v in params.arrays.items()}
+    off = 0
+    for i, (pos, z) in enumerate(systems):
+        f = O.forward(oc, params.arrays, pos, z)
+        G, dp = O.backward(f, params.arrays, float(d_e[i]), df_np[i] if df_np else None)
+        n = pos.shape[0]
+        assert abs(float(fw.energy[i]) - f.energy) <= TOL * max(abs(f.energy), 1e-8)
+        assert max_rel(pos_bar[off:off + n], dp) < TOL
+        if variant == "gemnet-style":
+            assert max_rel(fw.forces[off:off + n].cpu().numpy(), f.forces) < TOL
+        for k in ref_g:
+            ref_g[k] += G[k]
+        off += n
+    for k in ref_g:
+        assert max_rel(grads[k], ref_g[k]) < TOL, k
+
+
+def test_nn_module_autograd_path():
+    from paper_2203_09697_b200 import EGNModel, ModelConfig, init_params
+
+    cfg = ModelConfig(variant="gemnet-style", blocks=2, seed=2)
+    params = init_params(cfg)
+    model = EGNModel(cfg, params)
+    assert list(model.state_dict().keys()) == [s for s in params.arrays]
+    pos, z = O.random_cloud(12, 0.9, np.random.default_rng(2))
+    energy, forces = model([pos])
+    oc = O.Config(**{k: getattr(cfg, k) for k in O.Config.__dataclass_fields__})
+    f = O.forward(oc, params.arrays, pos, z)
+    assert abs(float(energy[0]) - f.energy) <= TOL * max(1.0, abs(f.energy))
+    w = torch.tensor(np.random.default_rng(1).standard_normal((12, 3)), device="cuda", dtype=torch.float32)
+    loss = 0.5 * energy.sum() + (forces * w).sum()
+    loss.backward()
+    G, _ = O.backward(f, params.arrays, 0.5, w.double().cpu().numpy())
+    for name, p in model.named_parameters():
+        assert max_rel(p.grad.double().cpu().numpy(), G[name]) < TOL, name
+
+
+def test_dimenet_predict_forces_and_force_loss_error():
+    from paper_2203_09697_b200 import ModelConfig, init_params
+    from paper_2203_09697_b200.tasks import loss_and_grads, predict
+
+    cfg = ModelConfig(variant="dimenet-style", blocks=2, seed=1)
+    params = init_params(cfg)
+    pos, z = O.random_cloud(10, 0.9, np.random.default_rng(4))
+    e, f = predict(pos, params)
+    oc = O.Config(**{k: getattr(cfg, k) for k in O.Config.__dataclass_fields__})
+    e_ref, f_ref = O.predict(oc, params.arrays, pos, z)
+    assert abs(e - e_ref) <= TOL * max(1.0, abs(e_ref))
+    assert max_rel(f, f_ref) < TOL
+    # net force and torque vanish (translation/rotation invariance, test_gradients.py:128-135)
+    assert np.abs(f.sum(0)).max() < 1e-4 * np.abs(f).max()
+    with pytest.raises(ValueError):
+        loss_and_grads([(pos, 0.0, np.zeros((10, 3)))], params, w_forces=1.0)
+
+
+@pytest.mark.parametrize("variant", ["dimenet", "gemnet"])
+def test_loss_and_grads_and_training_match_reference(variant):
+    from paper_2203_09697_b200 import ModelConfig, init_params
+    from paper_2203_09697_b200.tasks import loss_and_grads, train_simple
+
+    gd = load_golden(f"train_{variant}.npz")
+    cfg = ModelConfig.from_json(str(gd["config"]))
+    params = init_params(cfg)
+    data = [(gd[f"pos{i}"], float(gd[f"e{i}"]), gd[f"f{i}"]) for i in range(3)]
+    w_f = float(gd["w_forces"])
+    loss, grads = loss_and_grads(data, params, 1.0, w_f)
+    assert abs(loss - float(gd["loss"])) <= TOL * abs(float(gd["loss"]))
+    for k, g in grads.items():
+        assert max_rel(g, gd[f"grad/{k}"]) < TOL, k
+    _, hist = train_simple(data, params, lr=0.002, epochs=4, w_energy=1.0, w_forces=w_f)
+    assert max_rel(np.array(hist), gd["history"]) < 1e-3
+    assert hist[-1] < hist[0]
+
+
+def test_rigid_motion_invariance():
+    from paper_2203_09697_b200 import ModelConfig, init_params
+    from paper_2203_09697_b200.tasks import predict
+
+    cfg = ModelConfig(variant="gemnet-style", blocks=2, seed=3)
+    params = init_params(cfg)
+    rng = np.random.default_rng(9)
+    pos, _ = O.random_cloud(14, 0.9, rng)
+    q, _ = np.linalg.qr(rng.standard_normal((3, 3)))
+    if np.linalg.det(q) < 0:
+        q[:, 0] = -q[:, 0]
+    e0, f0 = predict(pos, params)
+    e1, f1 = predict(pos @ q.T + 3.0, params)
+    assert abs(e0 - e1) < 1e-4 * max(1.0, abs(e0))
+    assert max_rel(f1, f0 @ q.T) < 1e-3

@@ -1,0 +1,144 @@
+"""Triplet-interaction kernels vs the reference's per-triplet formulation.
+
+Reference formulation (record_tu, engine.py:118-149): per triplet t,
+g_t = sbf_t @ Wmat with sbf from basis.py:54-73 and the fp64 angles of
+graph.py:162-170; S[ji] = sum_t X[kj] * g_t.  The adjoints are computed with
+the oracle's primitives (sbf_partials, angle_gradients) in fp64.
+Tolerance: fp32 kernel vs fp64 reference, max-relative <= 1e-4.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import TOL, max_rel
+from oracle import egn_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def _ref(pos, cutoff, X, W, B):
+    g = O.build_graph(pos, cutoff)
+    K, L, dg = W.shape
+    Wmat = W.reshape(K * L, dg)
+    d_in = g.dist[g.trip_in]
+    sbf = O.sbf(d_in, g.angles, K, L, cutoff) if g.trip_in.size else np.zeros((0, K * L))
+    gt = sbf @ Wmat
+    term = X[g.trip_in] * gt
+    S = O.segment_sum(term, g.trip_out, g.src.size)
+    # adjoint of J = sum(S * B)
+    Bt = B[g.trip_out]
+    X_bar = O.scatter_rows(gt * Bt, g.trip_in, g.src.size)
+    W_bar = (sbf.T @ (X[g.trip_in] * Bt)).reshape(K, L, dg)
+    sbf_bar = (X[g.trip_in] * Bt) @ Wmat.T
+    pos_bar = np.zeros_like(pos)
+    if g.trip_in.size:
+        dd, da = O.sbf_partials(d_in, g.angles, K, L, cutoff)
+        dist_bar = np.zeros(g.src.size)
+        np.add.at(dist_bar, g.trip_in, (sbf_bar * dd).sum(1))
+        ang_bar = (sbf_bar * da).sum(1)
+        gk, gj, gi = O.angle_gradients(pos, g.src, g.recv, g.trip_in, g.trip_out)
+        k, j, i = g.src[g.trip_in], g.recv[g.trip_in], g.recv[g.trip_out]
+        np.add.at(pos_bar, k, ang_bar[:, None] * gk)
+        np.add.at(pos_bar, i, ang_bar[:, None] * gi)
+        np.add.at(pos_bar, j, ang_bar[:, None] * gj)
+        c = dist_bar[:, None] * g.units
+        np.add.at(pos_bar, g.recv, c)
+        np.add.at(pos_bar, g.src, -c)
+    return g, S, X_bar, W_bar, pos_bar
+
+
+def _run(pos, cutoff, K, L, dg, seed=0):
+    from paper_2203_09697_b200 import ops
+    from paper_2203_09697_b200.graph import build_batch
+
+    bg = build_batch([pos], cutoff)
+    rng = np.random.default_rng(seed)
+    X = rng.standard_normal((bg.num_edges, dg))
+    W = rng.standard_normal((K, L, dg)) / np.sqrt(K * L)
+    B = rng.standard_normal((bg.num_edges, dg))
+    g, S_ref, Xb_ref, Wb_ref, pb_ref = _ref(pos, cutoff, X, W, B)
+    Xd = torch.tensor(X, dtype=torch.float32, device="cuda")
+    Wd = torch.tensor(W, dtype=torch.float32, device="cuda")
+    S = ops.triplet_fwd(bg.edge_ptr, bg.rev, bg.geo, Xd, Wd, cutoff)
+    eg = torch.zeros((bg.num_edges, 4), device="cuda")
+    Bd = torch.tensor(B, dtype=torch.float32, device="cuda")
+    Xb, Wb = ops.triplet_bwd(bg.edge_ptr, bg.rev, bg.geo, Xd, Wd, cutoff, Bd, eg)
+    pb = ops.positions_bwd(bg.edge_ptr, bg.rev, bg.geo, eg)
+    torch.cuda.synchronize()
+    return (S.cpu().numpy(), S_ref), (Xb.cpu().numpy(), Xb_ref), (Wb.cpu().numpy(), Wb_ref), (pb.cpu().numpy(), pb_ref), g
+
+
+CASES = [
+    # (n atoms, density, cutoff, K, L, dg)
+    (20, 0.9, 1.5, 6, 4, 4),
+    (30, 0.9, 1.5, 3, 2, 3),
+    (40, 0.06, 6.0, 6, 7, 64),
+    (40, 0.06, 6.0, 6, 7, 16),
+    (40, 0.06, 6.0, 6, 7, 32),
+    (30, 0.06, 6.0, 6, 7, 128),
+    (24, 0.06, 6.0, 5, 7, 100),
+    (30, 0.06, 6.0, 1, 1, 8),
+    (60, 0.06, 6.0, 6, 8, 5),
+    (150, 0.3, 6.0, 6, 7, 64),   # degree ~ 100: multiple row blocks and q tiles
+    (120, 0.3, 6.0, 4, 7, 256),
+]
+
+
+@pytest.mark.parametrize("case", CASES)
+def test_triplet_fwd_bwd_matches_reference(case):
+    n, rho, cutoff, K, L, dg = case
+    pos, _ = O.random_cloud(n, rho, np.random.default_rng(n + dg))
+    (S, Sr), (Xb, Xbr), (Wb, Wbr), (pb, pbr), g = _run(pos, cutoff, K, L, dg)
+    assert g.trip_in.size > 0
+    assert max_rel(S, Sr) < TOL
+    assert max_rel(Xb, Xbr) < TOL
+    assert max_rel(Wb, Wbr) < TOL
+    assert max_rel(pb, pbr) < TOL
+
+
+def test_triplet_collinear_and_low_degree():
+    # collinear chain (zero angle subgradient), dimer (no triplets), isolated atom
+    chain = np.zeros((4, 3))
+    chain[:, 2] = np.arange(4.0)
+    for pos, cutoff in ((chain, 1.5), (np.array([[0.0, 0, 0], [0, 0, 1.0]]), 1.5),
+                        (np.array([[0.0, 0, 0], [5.0, 0, 0], [5.0, 1.0, 0]]), 1.5)):
+        (S, Sr), (Xb, Xbr), (Wb, Wbr), (pb, pbr), g = _run(pos, cutoff, 6, 4, 8)
+        assert max_rel(S, Sr) < TOL and max_rel(Xb, Xbr) < TOL and max_rel(Wb, Wbr) < TOL
+        assert np.abs(pb - pbr).max() < 1e-4 * max(1.0, np.abs(pbr).max())
+
+
+def test_triplet_terms_and_sbf_debug_outputs():
+    from paper_2203_09697_b200 import ops
+    from paper_2203_09697_b200.graph import build_batch
+
+    pos, _ = O.random_cloud(25, 0.9, np.random.default_rng(3))
+    bg = build_batch([pos], 1.5)
+    g = O.build_graph(pos, 1.5)
+    K, L, dg = 6, 4, 8
+    rng = np.random.default_rng(0)
+    X = rng.standard_normal((bg.num_edges, dg))
+    W = rng.standard_normal((K, L, dg))
+    sbf = O.sbf(g.dist[g.trip_in], g.angles, K, L, 1.5)
+    P_ref = X[g.trip_in] * (sbf @ W.reshape(K * L, dg))
+    P = ops.triplet_terms(bg.edge_ptr, bg.rev, bg.geo, bg.tri_ptr, bg.num_triplets,
+                          torch.tensor(X, dtype=torch.float32, device="cuda"),
+                          torch.tensor(W, dtype=torch.float32, device="cuda"), 1.5)
+    assert max_rel(P.cpu().numpy(), P_ref) < TOL
+    sb = ops.sbf(bg.geo, bg.edge_ptr, bg.tri_ptr, bg.num_triplets, K, L, 1.5)
+    assert max_rel(sb.cpu().numpy(), sbf) < TOL
+    rb = ops.rbf(bg.geo, K, 1.5)
+    assert max_rel(rb.cpu().numpy(), O.rbf(g.dist, K, 1.5)) < TOL
+
+
+def test_triplet_dimension_errors():
+    from paper_2203_09697_b200 import ops
+    from paper_2203_09697_b200.graph import build_batch
+
+    bg = build_batch([np.array([[0.0, 0, 0], [0, 0, 1.0], [0, 1.0, 0]])], 1.5)
+    X = torch.zeros((bg.num_edges, 8), device="cuda")
+    with pytest.raises(ValueError):
+        ops.triplet_fwd(bg.edge_ptr, bg.rev, bg.geo, X, torch.zeros((6, 9, 8), device="cuda"), 1.5)
+    with pytest.raises(ValueError):
+        ops.triplet_fwd(bg.edge_ptr, bg.rev, bg.geo, torch.zeros((bg.num_edges, 300), device="cuda"),
+                        torch.zeros((6, 4, 300), device="cuda"), 1.5)

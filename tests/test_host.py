@@ -1,0 +1,114 @@
+"""Host-side logic on CPU: config, parameters, partitions, comm model, C-ABI symbols."""
+
+import json
+import re
+
+import numpy as np
+import pytest
+
+from conftest import ROOT, load_golden
+from oracle import egn_oracle as O
+from paper_2203_09697_b200 import (CommModel, ModelConfig, comm_volume, init_params, load_params,
+                                   param_specs, partition_centers, save_params, split_range)
+
+
+def test_config_validation_and_json_roundtrip():
+    c = ModelConfig(variant="gemnet-style", blocks=3, d_e=16)
+    assert ModelConfig.from_json(c.to_json()) == c
+    with pytest.raises(ValueError):
+        ModelConfig(variant="bogus")
+    with pytest.raises(ValueError):
+        ModelConfig(d_t=0)
+    with pytest.raises(ValueError):
+        ModelConfig(cutoff=0.0)
+    with pytest.raises(ValueError):
+        ModelConfig.from_json(json.dumps({"bogus": 1}))
+    assert c.triplet_width == c.d_bil and ModelConfig().triplet_width == ModelConfig().d_t
+
+
+@pytest.mark.parametrize("fname", ["model_dimenet_small.npz", "model_gemnet_odd.npz", "model_gemnet_c2dims.npz"])
+def test_init_params_matches_reference_checksums(fname):
+    gd = load_golden(fname)
+    cfg = ModelConfig.from_json(str(gd["config"]))
+    p = init_params(cfg)
+    assert [s.name for s in param_specs(cfg)] == [str(n) for n in gd["param_names"]]
+    np.testing.assert_array_equal([float(np.sum(a)) for a in p.arrays.values()], gd["param_checksum"])
+
+
+def test_param_specs_match_oracle():
+    for variant in ("dimenet-style", "gemnet-style"):
+        cfg = ModelConfig(variant=variant, blocks=2, d_bil=5)
+        oc = O.Config(**{k: getattr(cfg, k) for k in O.Config.__dataclass_fields__})
+        assert [(s.name, s.shape, s.fan_in) for s in param_specs(cfg)] == O.param_specs(oc)
+
+
+def test_egn1_container_roundtrip(tmp_path):
+    cfg = ModelConfig(variant="gemnet-style", blocks=2)
+    p = init_params(cfg)
+    save_params(p, tmp_path / "w.egn")
+    q = load_params(tmp_path / "w.egn", cutoff=cfg.cutoff)
+    assert q.config == cfg
+    for k in p.arrays:
+        np.testing.assert_array_equal(p.arrays[k], q.arrays[k])
+    blob = (tmp_path / "w.egn").read_bytes()
+    (tmp_path / "bad.egn").write_bytes(b"XXXX" + blob[4:])
+    with pytest.raises(ValueError):
+        load_params(tmp_path / "bad.egn")
+    (tmp_path / "trunc.egn").write_bytes(blob[:-8])
+    with pytest.raises(ValueError):
+        load_params(tmp_path / "trunc.egn")
+
+
+def test_split_range_and_comm_volume_known_answers():
+    assert [s.size for s in split_range(7, 3)] == [3, 2, 2]
+    assert comm_volume(CommModel(10, 40, 999, 4, 8, 16, 1, "dimenet-style"), 1).per_block == 361
+    assert comm_volume(CommModel(10, 40, 999, 4, 8, 16, 1, "gemnet-style"), 1).per_block == 681
+    m = CommModel(5, 12, 50, 3, 4, 2, 2, "gemnet-style")
+    assert comm_volume(m, 4).total == 4 * comm_volume(m, 1).per_block
+
+
+@pytest.mark.parametrize("workers", [1, 2, 3, 4, 8])
+def test_partition_centers_contiguous_and_balanced(workers):
+    rng = np.random.default_rng(workers)
+    deg = rng.integers(0, 60, size=500)
+    part = partition_centers(deg, workers)
+    assert part.node_bounds[0] == 0 and part.node_bounds[-1] == deg.size
+    assert np.all(np.diff(part.node_bounds) >= 0)
+    edge_ptr = np.concatenate([[0], np.cumsum(deg)])
+    tri_ptr = np.concatenate([[0], np.cumsum(deg * (deg - 1))])
+    np.testing.assert_array_equal(part.edge_bounds, edge_ptr[part.node_bounds])
+    np.testing.assert_array_equal(part.trip_bounds, tri_ptr[part.node_bounds])
+    cost = deg * (deg - 1) + deg
+    per = [cost[part.node_bounds[r]:part.node_bounds[r + 1]].sum() for r in range(workers)]
+    assert max(per) - min(per) <= 2 * cost.max()
+
+
+def test_abi_header_lists_every_bound_symbol():
+    from paper_2203_09697_b200 import _lib
+
+    header = set(_lib.header_symbols())
+    bound = set(_lib.SIGNATURES)
+    assert header == bound, (header ^ bound)
+
+
+def test_native_library_loads_and_exports_all_symbols():
+    """No GPU needed: dlopen the built library and resolve every declared entry point."""
+    from paper_2203_09697_b200 import _lib
+
+    if not _lib.LIB_PATH.exists():
+        pytest.skip("libegn_b200.so not built (run make)")
+    lib = _lib.lib()
+    for name in _lib.header_symbols():
+        assert hasattr(lib, name), name
+    assert lib.egn_abi_version() == 1
+    assert isinstance(lib.egn_last_error(), bytes)
+    # pure host entry point: workspace sizing
+    assert lib.egn_triplet_bwd_workspace_bytes(1000, 6, 7, 64) > 0
+
+
+def test_product_path_does_not_import_oracle():
+    pkg = ROOT / "paper_2203_09697_b200"
+    for f in pkg.rglob("*.py"):
+        text = f.read_text()
+        assert not re.search(r"^\s*(from|import)\s+oracle", text, re.M), f
+        assert "egn_oracle" not in text, f

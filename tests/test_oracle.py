@@ -1,0 +1,117 @@
+"""Pin the CPU oracle (oracle/egn_oracle.py) to the reference's own outputs.
+
+The golden fixtures were produced by running the reference package in this
+container (tests/golden/make_golden.py).  Topology must be bit-exact;
+floating-point outputs and all gradients agree to 1e-10 relative (the
+oracle is a restatement in the same fp64 operation order).
+"""
+
+import json
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, load_golden, max_rel
+from oracle import egn_oracle as O
+
+MODEL_FILES = sorted(p.name for p in GOLDEN.glob("model_*.npz"))
+
+
+def _cfg(js):
+    d = json.loads(str(js))
+    return O.Config(**{k: d[k] for k in O.Config.__dataclass_fields__})
+
+
+def test_graph_topology_bit_exact(graphs_golden):
+    data, names = graphs_golden
+    assert len(names) >= 15
+    for name in names:
+        g = O.build_graph(data[f"{name}/pos"], float(data[f"{name}/cutoff"]))
+        for key, val in (("src", g.src), ("recv", g.recv), ("trip_in", g.trip_in), ("trip_out", g.trip_out),
+                         ("rev", g.rev)):
+            np.testing.assert_array_equal(val, data[f"{name}/{key}"], err_msg=f"{name}/{key}")
+        np.testing.assert_array_equal(g.dist, data[f"{name}/dist"])
+        np.testing.assert_array_equal(g.units, data[f"{name}/units"])
+        np.testing.assert_array_equal(g.angles, data[f"{name}/angles"])
+
+
+def test_graph_edge_cases(graphs_golden):
+    data, _ = graphs_golden
+    assert data["dimer/src"].size == 2 and data["dimer/trip_in"].size == 0
+    assert data["collinear_chain/trip_in"].size == 2
+    np.testing.assert_allclose(data["collinear_chain/angles"], np.pi)
+    assert data["triangle/trip_in"].size == 6
+    assert data["zero_edge/src"].size == 0
+    assert data["single_atom/src"].size == 0
+    # spacing == cutoff: the 6 axis neighbours of an interior lattice point are edges
+    assert data["lattice_at_cutoff/src"].size == 2 * 3 * 4 * 4 * 3
+
+
+@pytest.mark.parametrize("fname", MODEL_FILES)
+def test_model_forward_backward_matches_reference(fname):
+    gd = load_golden(fname)
+    cfg = _cfg(gd["config"])
+    P = O.init_params(cfg)
+    np.testing.assert_allclose([float(np.sum(a)) for a in P.values()], gd["param_checksum"], rtol=0, atol=0)
+    fw = O.forward(cfg, P, gd["pos"], gd["z"])
+    d_forces = gd.get("d_forces")
+    G, d_pos = O.backward(fw, P, 0.7, d_forces)
+    assert abs(fw.energy - float(gd["energy"])) <= 1e-10 * max(abs(float(gd["energy"])), 1.0)
+    assert max_rel(fw.m, gd["m"]) < (1e-6 if gd["m"].dtype == np.float32 else 1e-10)
+    assert max_rel(fw.t_feat, gd["t_feat"]) < (1e-6 if gd["t_feat"].dtype == np.float32 else 1e-10)
+    assert max_rel(fw.v, gd["v"]) < 1e-10
+    assert max_rel(d_pos, gd["d_positions"]) < 1e-10
+    if cfg.variant == O.GEMNET:
+        assert max_rel(fw.forces, gd["forces"]) < 1e-10
+    else:
+        _, dp1 = O.backward(fw, P, 1.0)
+        assert max_rel(-dp1, gd["forces"]) < 1e-10
+    for name in gd["param_names"]:
+        name = str(name)
+        if f"dp/{name}" in gd:
+            assert max_rel(G[name], gd[f"dp/{name}"]) < 1e-10, name
+        else:
+            assert max_rel(G[name].ravel()[:64], gd[f"dphead/{name}"]) < 1e-10, name
+            assert abs(np.abs(G[name]).max() - float(gd[f"dpnorm/{name}"])) <= 1e-10 * max(float(gd[f"dpnorm/{name}"]), 1e-300)
+
+
+@pytest.mark.parametrize("variant", ["dimenet", "gemnet"])
+def test_loss_and_grads_matches_reference(variant):
+    gd = load_golden(f"train_{variant}.npz")
+    cfg = _cfg(gd["config"])
+    P = O.init_params(cfg)
+    data = [(gd[f"pos{i}"], gd[f"z{i}"], float(gd[f"e{i}"]), gd[f"f{i}"]) for i in range(3)]
+    w_f = float(gd["w_forces"])
+    loss, grads = O.loss_and_grads(cfg, P, data, 1.0, w_f)
+    assert abs(loss - float(gd["loss"])) <= 1e-10 * abs(float(gd["loss"]))
+    for k, g in grads.items():
+        assert max_rel(g, gd[f"grad/{k}"]) < 1e-10, k
+    # train_simple history
+    hist, cur = [], P
+    for _ in range(4):
+        l, g = O.loss_and_grads(cfg, cur, data, 1.0, w_f)
+        hist.append(l)
+        cur = O.sgd_step(cur, g, 0.002)
+    np.testing.assert_allclose(hist, gd["history"], rtol=1e-9)
+
+
+def test_oracle_fd_gradient_spot_check():
+    """Independent of the fixtures: central differences of the oracle energy."""
+    cfg = O.Config(variant=O.DIMENET, blocks=1)
+    rng = np.random.default_rng(3)
+    pos, z = O.random_cloud(6, 0.9, rng)
+    P = O.init_params(cfg)
+    fw = O.forward(cfg, P, pos, z)
+    G, dpos = O.backward(fw, P, 1.0)
+    h = 1e-6
+    for name in ("block0.tu.sbf_gate", "block0.tu.down", "edge_init.w"):
+        i = 1
+        a = P[name].ravel()
+        orig = a[i]
+        a[i] = orig + h
+        ep = O.forward(cfg, P, pos, z).energy
+        a[i] = orig - h
+        em = O.forward(cfg, P, pos, z).energy
+        a[i] = orig
+        fd = (ep - em) / (2 * h)
+        assert abs(fd - G[name].ravel()[i]) < 1e-6 * max(1.0, abs(fd))
