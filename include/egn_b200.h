@@ -120,11 +120,12 @@ int egn_triplet_fwd(const int64_t* edge_ptr, const int32_t* rev, const float* ge
  *   edge_grad [E, 4] float   (+=): (dE/dv_e (3), dE/dd_e) for the edge
  *                              vector v_e = x_recv - x_src from the angles and the
  *                              in-edge distance of the basis.
+ * max_degree bounds deg(j) over all centres (sizes shared memory).
  * workspace: egn_triplet_bwd_workspace_bytes(...) bytes of device memory. */
 int64_t egn_triplet_bwd_workspace_bytes(int64_t num_nodes, int k_rbf, int l_sbf, int dg);
 int egn_triplet_bwd(const int64_t* edge_ptr, const int32_t* rev, const float* geo,
-                    int64_t num_nodes, const float* X, const float* W, int k_rbf, int l_sbf,
-                    int dg, double cutoff, const float* S_bar, float* X_bar, float* W_bar,
+                    int64_t num_nodes, int max_degree, const float* X, const float* W, int k_rbf,
+                    int l_sbf, int dg, double cutoff, const float* S_bar, float* X_bar, float* W_bar,
                     float* edge_grad, void* workspace, egn_stream_t stream);
 
 /* Per-triplet feature debug output t_feat-like rows for parity tests:
@@ -177,6 +178,12 @@ int egn_rbf_bwd(const float* geo, const float* rbf_bar, int64_t num_edges, int k
 int egn_positions_bwd(const int64_t* edge_ptr, const int32_t* rev, const float* geo,
                       int64_t num_nodes, const float* edge_grad, double* pos_bar,
                       egn_stream_t stream);
+
+/* Column sums out[c] = sum_r x[r*ld + c] (bias adjoints of linear, tape.py:113-119),
+ * deterministic two-stage reduction; workspace from egn_column_sum_workspace_bytes. */
+int64_t egn_column_sum_workspace_bytes(int64_t rows, int d);
+int egn_column_sum(const float* x, int64_t rows, int d, int64_t ld, float* out, void* workspace,
+                   egn_stream_t stream);
 
 /* ------------------------------------------------------------------ */
 /* Optimizer: train_simple SGD update (tasks.py:207-208)               */

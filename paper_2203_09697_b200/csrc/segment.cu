@@ -252,6 +252,29 @@ __global__ void positions_bwd_kernel(const int64_t* __restrict__ edge_ptr,
   }
 }
 
+// Column sums of a row-major [rows, d] matrix: stage 1 writes one partial row per
+// 256-row chunk (threads over columns, coalesced), stage 2 sums the partials in
+// chunk order (deterministic).
+constexpr int kColChunk = 256;
+
+__global__ void column_sum_partial_kernel(const float* __restrict__ x, int64_t rows, int d, int64_t ld,
+                                          float* __restrict__ part) {
+  const int64_t r0 = static_cast<int64_t>(blockIdx.x) * kColChunk;
+  const int64_t r1 = r0 + kColChunk < rows ? r0 + kColChunk : rows;
+  for (int c = threadIdx.x; c < d; c += blockDim.x) {
+    float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+    int64_t r = r0;
+    for (; r + 3 < r1; r += 4) {
+      s0 += x[r * ld + c];
+      s1 += x[(r + 1) * ld + c];
+      s2 += x[(r + 2) * ld + c];
+      s3 += x[(r + 3) * ld + c];
+    }
+    for (; r < r1; ++r) s0 += x[r * ld + c];
+    part[static_cast<int64_t>(blockIdx.x) * d + c] = (s0 + s1) + (s2 + s3);
+  }
+}
+
 __global__ void sgd_kernel(float* __restrict__ w, const float* __restrict__ g, int64_t n, float lr) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
@@ -365,6 +388,26 @@ int egn_positions_bwd(const int64_t* edge_ptr, const int32_t* rev, const float* 
       edge_ptr, rev, reinterpret_cast<const float4*>(geo), num_nodes,
       reinterpret_cast<const float4*>(edge_grad), pos_bar);
   return check_launch("positions_bwd");
+}
+
+int64_t egn_column_sum_workspace_bytes(int64_t rows, int d) {
+  return ((rows + kColChunk - 1) / kColChunk + 1) * static_cast<int64_t>(d) * 4;
+}
+
+int egn_column_sum(const float* x, int64_t rows, int d, int64_t ld, float* out, void* workspace,
+                   egn_stream_t stream) {
+  cudaStream_t st = as_stream(stream);
+  if (rows == 0) {
+    cudaMemsetAsync(out, 0, sizeof(float) * d, st);
+    return check_launch("column_sum_empty");
+  }
+  const int chunks = static_cast<int>((rows + kColChunk - 1) / kColChunk);
+  float* part = reinterpret_cast<float*>(workspace);
+  const int threads = d >= 256 ? 256 : ((d + 31) / 32) * 32;
+  column_sum_partial_kernel<<<chunks, threads, 0, st>>>(x, rows, d, ld, part);
+  if (check_launch("column_sum_partial")) return 1;
+  reduce_rows_kernel<<<grid_for(d, 128), 128, 0, st>>>(part, chunks, d, out);
+  return check_launch("column_sum_reduce");
 }
 
 int egn_sgd(float* w, const float* g, int64_t n, float lr, egn_stream_t stream) {

@@ -22,11 +22,10 @@
 // memory.  Per triplet the kernel then spends L * dg FMAs; nothing per
 // triplet ever touches HBM.
 //
-// Backward per centre (thread = (row q, channel chunk)):
+// Backward per centre (two phases, see the backward section):
 //   Qbar[q,l,c] = sum_p T_l(x_pq) Sbar[p,c]                 -> X_bar, W_bar, dd_q
-//   y(p,q)      = xbar(p,q) + xbar(q,p),
-//   xbar(p,q)   = sum_l T_l'(x_pq) sum_c Sbar[p,c] Q[q,l,c]  -> dE/dv_q
-// with dE/dv_q += y (u_p - x u_q) / d_q, the gradient of x_pq w.r.t. the
+//   xbar(p,q)   = sum_l T_l'(x_pq) sum_c Sbar[p,c] Q[q,l,c]  -> dE/dv_p, dE/dv_q
+// with dE/dv_q += xbar (u_p - x u_q) / d_q, the gradient of x_pq w.r.t. the
 // edge vector v_q; using d cos(l a)/dx = T_l'(x) = l U_{l-1}(x) avoids the
 // atan2 singularity and equals the reference's zero subgradient at
 // collinear triplets (both factors vanish there).
@@ -217,101 +216,205 @@ triplet_fwd_kernel(const int64_t* __restrict__ edge_ptr, const int32_t* __restri
 // ---------------------------------------------------------------------------
 // backward
 // ---------------------------------------------------------------------------
-// Extra shared memory: Sbar tile [qt][DP], W_bar accumulator [K][L][DP],
-// staging for per-row R_bar [GP][L][DP] and rbf [GP][K].
-struct BwdExtra {
-  int sb, wbar, rstage, rbst, total;
-  __host__ __device__ BwdExtra(int qt, int K, int L, int DP, int GP) {
+// Two phases per centre, both atomic-free and deterministic:
+//  Phase 1 (rows p, like the forward; Q tiles in smem):
+//     xbar(p,q) = sum_l T_l'(x_pq) sum_c Sbar[p,c] Q[q,l,c]
+//     row part of dE/dv_p  += xbar(p,q) (u_q - x u_p)        (registers)
+//     column part of dE/dv_q += xbar(p,q) (u_p - x u_q)      (XB tile in smem,
+//                                                             summed by column owners)
+//  Phase 2 (rows q; Sbar tiles in smem):
+//     Qbar[q,l,c] = sum_p T_l(x_pq) Sbar[p,c]
+//     X_bar[rq,c] = sum_l Qbar[q,l,c] Rw[rq,l,c],  R_bar = Qbar * X[rq]
+//     W_bar[k,l,c] += sum_q rbf_k(d_q) R_bar[q,l,c],  dd_q = sum R_bar * dRw/dd
+// Cost: ~2x the forward's FMAs.
+struct BwdLayout {
+  int us, rb, w, qs, sbs, wb, up, xb, rbs, fs, total;
+  __host__ __device__ BwdLayout(int qt, int K, int L, int DP, int GP, int PB, int nmax) {
+    auto up4 = TileLayout::up4;
     int o = 0;
-    sb = o; o += TileLayout::up4(qt * DP);
-    wbar = o; o += TileLayout::up4(K * L * DP);
-    rstage = o; o += TileLayout::up4(GP * L * DP);
-    rbst = o; o += TileLayout::up4(GP * K);
+    us = o; o += 4 * qt;
+    rb = o; o += up4(qt * K);
+    w = o; o += up4(K * L * DP);
+    qs = o; o += up4((qt > GP ? qt : GP) * L * DP);  // Q tile (phase 1) / R_bar staging (phase 2)
+    sbs = o; o += up4(qt * DP);
+    wb = o; o += up4(K * L * DP);
+    up = o; o += 4 * PB;
+    xb = o; o += up4(PB * qt);
+    rbs = o; o += up4(GP * K);
+    fs = o; o += 4 * nmax;
     total = o;
   }
 };
 
-template <int CW, int GC>
+template <int CW, int GC, int R1>
 __global__ void __launch_bounds__(kThreads)
 triplet_bwd_kernel(const int64_t* __restrict__ edge_ptr, const int32_t* __restrict__ rev,
                    const float4* __restrict__ geo, int64_t nv, const float* __restrict__ X,
-                   const float* __restrict__ W, int K, int L, int dg, int qt, RbfParams rp,
+                   const float* __restrict__ W, int K, int L, int dg, int qt, int nmax, RbfParams rp,
                    const float* __restrict__ Sbar, float* __restrict__ Xbar,
                    float* __restrict__ wbar_part, float4* __restrict__ edge_grad) {
   using CM = ChanMap<CW, GC>;
-  constexpr int GP = kThreads / GC, VW = CM::VW, DP = CM::DP;
+  constexpr int GP = kThreads / GC, VW = CM::VW, DP = CM::DP, PB = GP * R1;
   extern __shared__ __align__(16) float sm[];
-  const int KLD = K * L * DP;
-  BwdExtra Bx(qt, K, L, DP, GP);
-  TileLayout Ly(qt, K, L, DP, Bx.total);
-  const float4* Us = reinterpret_cast<const float4*>(sm);
-  const float* Wsm = sm + Ly.off_w;
-  const float* Qs = sm + Ly.off_q;
-  float* ext = sm + Ly.off_x;
-  float* Sbs = ext + Bx.sb;
-  float* Wb = ext + Bx.wbar;
-  float* Rst = ext + Bx.rstage;
-  float* Rbs = ext + Bx.rbst;
+  const BwdLayout B(qt, K, L, DP, GP, PB, nmax);
+  TileLayout Ly(qt, K, L, DP, 0);  // for build_tile: Us at 0, Rb, W, Qs offsets must match B
+  float4* Us = reinterpret_cast<float4*>(sm + B.us);
+  const float* Wsm = sm + B.w;
+  float* Qs = sm + B.qs;
+  float* Rst = sm + B.qs;
+  float* Sbs = sm + B.sbs;
+  float* Wb = sm + B.wb;
+  float4* Up = reinterpret_cast<float4*>(sm + B.up);
+  float* XB = sm + B.xb;
+  float* Rbs = sm + B.rbs;
+  float4* Fs = reinterpret_cast<float4*>(sm + B.fs);
   const int tid = threadIdx.x, cg = tid % GC, pg = tid / GC;
 
-  load_weights<CW, GC>(sm + Ly.off_w, W, K, L, dg);
-  for (int idx = tid; idx < KLD; idx += kThreads) Wb[idx] = 0.f;
+  load_weights<CW, GC>(sm + B.w, W, K, L, dg);
+  for (int idx = tid; idx < K * L * DP; idx += kThreads) Wb[idx] = 0.f;
 
   for (int64_t j = blockIdx.x; j < nv; j += gridDim.x) {
     const int64_t off = edge_ptr[j];
     const int n = static_cast<int>(edge_ptr[j + 1] - off);
-    if (n < 2) continue;  // no triplets: no gradient, edge_grad untouched
+    if (n < 2) {
+      // no triplets at this centre: its in-edge (if any) gets a zero X_bar row
+      if (n == 1) {
+        const int64_t r0 = rev[off];
+        for (int c = tid; c < dg; c += kThreads) Xbar[r0 * dg + c] = 0.f;
+      }
+      continue;
+    }
+    __syncthreads();  // previous centre finished with every buffer
+    for (int i = tid; i < n; i += kThreads) Fs[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+
+    // ------------------------------ phase 1 ------------------------------
+    for (int p0 = 0; p0 < n; p0 += PB) {
+      const int reff = min(R1, (n - p0 + GP - 1) / GP);
+      float4 up[R1];
+      int pidx[R1];
+      float sb[R1][CW];
+      float fr[R1][3];
+#pragma unroll
+      for (int r = 0; r < R1; ++r) {
+        pidx[r] = p0 + pg + GP * r;
+        const bool ok = r < reff && pidx[r] < n;
+        up[r] = ok ? geo[off + pidx[r]] : make_float4(0.f, 0.f, 0.f, 1.f);
+#pragma unroll
+        for (int i = 0; i < CW; ++i) {
+          const int c = CM::chan(cg, i);
+          sb[r][i] = (ok && c < dg) ? Sbar[(off + pidx[r]) * dg + c] : 0.f;
+        }
+        fr[r][0] = fr[r][1] = fr[r][2] = 0.f;
+        if (cg == 0) Up[pg + GP * r] = up[r];
+      }
+      for (int q0 = 0; q0 < n; q0 += qt) {
+        const int nq = min(qt, n - q0);
+        __syncthreads();
+        build_tile<CW, GC>(Ly, sm, geo, rev, X, off, q0, nq, dg, rp);
+        for (int t = 0; t < nq; ++t) {
+          const float4 uq = Us[t];
+          const int qg = q0 + t;
+          float x[R1], x2[R1], uc[R1], um[R1], s[R1];
+#pragma unroll
+          for (int r = 0; r < R1; ++r) {
+            x[r] = up[r].x * uq.x + up[r].y * uq.y + up[r].z * uq.z;
+            x2[r] = 2.f * x[r];
+            uc[r] = 0.f;  // U_{l-1} at l = 0
+            um[r] = 0.f;
+            s[r] = 0.f;
+          }
+          const float* qrow = Qs + t * L * DP;
+#pragma unroll
+          for (int l = 0; l < kMaxL; ++l) {
+            if (l < L) {
+              float qv[CW];
+#pragma unroll
+              for (int i = 0; i < CW; i += VW) load_vec<VW>(qrow + l * DP + CM::chan(cg, i), qv + i);
+#pragma unroll
+              for (int r = 0; r < R1; ++r) {
+                if (r < reff) {
+                  float d = 0.f;
+#pragma unroll
+                  for (int i = 0; i < CW; ++i) d = fmaf(sb[r][i], qv[i], d);
+                  s[r] = fmaf(static_cast<float>(l) * uc[r], d, s[r]);
+                }
+                const float un = (l == 0) ? 1.f : fmaf(x2[r], uc[r], -um[r]);
+                um[r] = uc[r];
+                uc[r] = un;
+              }
+            }
+          }
+#pragma unroll
+          for (int r = 0; r < R1; ++r) {
+            if (r < reff) {
+              float v = s[r];
+#pragma unroll
+              for (int o = GC / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+              v = (pidx[r] < n && pidx[r] != qg) ? v : 0.f;
+              fr[r][0] = fmaf(v, uq.x - x[r] * up[r].x, fr[r][0]);
+              fr[r][1] = fmaf(v, uq.y - x[r] * up[r].y, fr[r][1]);
+              fr[r][2] = fmaf(v, uq.z - x[r] * up[r].z, fr[r][2]);
+              if (cg == 0) XB[(pg + GP * r) * qt + t] = v;
+            } else if (cg == 0) {
+              XB[(pg + GP * r) * qt + t] = 0.f;
+            }
+          }
+        }
+        __syncthreads();
+        // column owners: dE/dv_q += sum_p xbar(p,q) (u_p - x u_q), rows in fixed order
+        const int rows = min(PB, n - p0);
+        for (int t = tid; t < nq; t += kThreads) {
+          const float4 uq = Us[t];
+          float cx = 0.f, cy = 0.f, cz = 0.f;
+          for (int ri = 0; ri < rows; ++ri) {
+            const float4 u = Up[ri];
+            const float xv = XB[ri * qt + t];
+            const float x = u.x * uq.x + u.y * uq.y + u.z * uq.z;
+            cx = fmaf(xv, u.x - x * uq.x, cx);
+            cy = fmaf(xv, u.y - x * uq.y, cy);
+            cz = fmaf(xv, u.z - x * uq.z, cz);
+          }
+          float4 f = Fs[q0 + t];
+          f.x += cx;
+          f.y += cy;
+          f.z += cz;
+          Fs[q0 + t] = f;
+        }
+      }
+      __syncthreads();
+      if (cg == 0) {
+#pragma unroll
+        for (int r = 0; r < R1; ++r) {
+          if (r < reff && pidx[r] < n) {
+            float4 f = Fs[pidx[r]];
+            f.x += fr[r][0];
+            f.y += fr[r][1];
+            f.z += fr[r][2];
+            Fs[pidx[r]] = f;
+          }
+        }
+      }
+    }
+
+    // ------------------------------ phase 2 ------------------------------
     for (int b0 = 0; b0 < n; b0 += GP) {
       const int q = b0 + pg;
       const bool valid = q < n;
-      __syncthreads();  // Wsm / previous users of the tile are done
-      // own row data
-      float4 uq = valid ? geo[off + q] : make_float4(0.f, 0.f, 0.f, 1.f);
-      const int64_t rq = valid ? static_cast<int64_t>(rev[off + q]) : 0;
-      float sbo[CW], xo[CW];
-#pragma unroll
-      for (int i = 0; i < CW; ++i) {
-        int c = CM::chan(cg, i);
-        sbo[i] = (valid && c < dg) ? Sbar[(off + q) * dg + c] : 0.f;
-        xo[i] = (valid && c < dg) ? X[rq * dg + c] : 0.f;
-      }
-      float rbo[kMaxK], rdo[kMaxK];  // rbf_k(d_q) and d rbf_k / dd
-#pragma unroll
-      for (int k = 0; k < kMaxK; ++k) {
-        rbo[k] = k < K ? rbf_val(uq.w, k, rp) : 0.f;
-        rdo[k] = -2.f * rp.gamma * (uq.w - rp.step * k) * rbo[k];
-      }
-      // own Q row: Q[q,l,c] = xo * sum_k rbf_k W[k,l,c]
-      float qo[kMaxL][CW];
-#pragma unroll
-      for (int l = 0; l < kMaxL; ++l) {
-#pragma unroll
-        for (int i = 0; i < CW; ++i) {
-          float s = 0.f;
-          if (l < L) {
-            int c = CM::chan(cg, i);
-#pragma unroll
-            for (int k = 0; k < kMaxK; ++k)
-              if (k < K) s = fmaf(rbo[k], Wsm[(k * L + l) * DP + c], s);
-          }
-          qo[l][i] = xo[i] * s;
-        }
-      }
+      const float4 uq = valid ? geo[off + q] : make_float4(0.f, 0.f, 0.f, 1.f);
       float qb[kMaxL][CW];
 #pragma unroll
       for (int l = 0; l < kMaxL; ++l)
 #pragma unroll
         for (int i = 0; i < CW; ++i) qb[l][i] = 0.f;
-      float fx = 0.f, fy = 0.f, fz = 0.f;
-
       for (int p0 = 0; p0 < n; p0 += qt) {
         const int np = min(qt, n - p0);
         __syncthreads();
+        if (tid < np) Us[tid] = geo[off + p0 + tid];
         for (int idx = tid; idx < np * DP; idx += kThreads) {
-          int t = idx / DP, c = idx - t * DP;
+          const int t = idx / DP, c = idx - t * DP;
           Sbs[idx] = c < dg ? Sbar[(off + p0 + t) * dg + c] : 0.f;
         }
-        build_tile<CW, GC>(Ly, sm, geo, rev, X, off, p0, np, dg, rp);  // syncs
+        __syncthreads();
         for (int t = 0; t < np; ++t) {
           const float4 up = Us[t];
           const float x = up.x * uq.x + up.y * uq.y + up.z * uq.z;
@@ -320,66 +423,53 @@ triplet_bwd_kernel(const int64_t* __restrict__ edge_ptr, const int32_t* __restri
 #pragma unroll
           for (int i = 0; i < CW; i += VW) load_vec<VW>(Sbs + t * DP + CM::chan(cg, i), sbp + i);
           const float x2 = 2.f * x;
-          float tc = m, tp = m * x;      // T_l (masked), starting at l = 0
-          float uc = 0.f, um = 0.f;      // U_{l-1}, U_{l-2}
-          float y = 0.f;
-          const float* qrow = Qs + t * L * DP;
+          float tc = m, tp = m * x;
 #pragma unroll
           for (int l = 0; l < kMaxL; ++l) {
             if (l < L) {
-              float qv[CW];
 #pragma unroll
-              for (int i = 0; i < CW; i += VW) load_vec<VW>(qrow + l * DP + CM::chan(cg, i), qv + i);
-              float s = 0.f;
-#pragma unroll
-              for (int i = 0; i < CW; ++i) {
-                qb[l][i] = fmaf(tc, sbp[i], qb[l][i]);
-                s = fmaf(sbo[i], qv[i], s);
-                s = fmaf(sbp[i], qo[l][i], s);
-              }
-              // T_l'(x) = l U_{l-1}(x)
-              y = fmaf(static_cast<float>(l) * uc, s, y);
-              float tn = fmaf(x2, tc, -tp);
+              for (int i = 0; i < CW; ++i) qb[l][i] = fmaf(tc, sbp[i], qb[l][i]);
+              const float tn = fmaf(x2, tc, -tp);
               tp = tc;
               tc = tn;
-              float un = (l == 0) ? 1.f : fmaf(x2, uc, -um);
-              um = uc;
-              uc = un;
             }
           }
-          // reduce y over the GC threads of this row
-#pragma unroll
-          for (int o = GC / 2; o > 0; o >>= 1) y += __shfl_xor_sync(0xffffffffu, y, o);
-          y *= m;
-          fx = fmaf(y, up.x - x * uq.x, fx);
-          fy = fmaf(y, up.y - x * uq.y, fy);
-          fz = fmaf(y, up.z - x * uq.z, fz);
         }
       }
-
-      // ---- row epilogue: X_bar, R_bar -> (W_bar, dd) ----
-      float xb[CW];
-      float dd = 0.f;
+      // ---- row epilogue ----
+      const int64_t rq = valid ? static_cast<int64_t>(rev[off + q]) : 0;
+      float xo[CW], xb[CW];
 #pragma unroll
-      for (int i = 0; i < CW; ++i) xb[i] = 0.f;
-      __syncthreads();  // Qs no longer needed; Rst/Rbs free
+      for (int i = 0; i < CW; ++i) {
+        const int c = CM::chan(cg, i);
+        xo[i] = (valid && c < dg) ? X[rq * dg + c] : 0.f;
+        xb[i] = 0.f;
+      }
+      float rbo[kMaxK], rdo[kMaxK];  // rbf_k(d_q), d rbf_k / dd
+#pragma unroll
+      for (int k = 0; k < kMaxK; ++k) {
+        rbo[k] = k < K ? rbf_val(uq.w, k, rp) : 0.f;
+        rdo[k] = -2.f * rp.gamma * (uq.w - rp.step * k) * rbo[k];
+      }
+      float dd = 0.f;
+      __syncthreads();  // Rst (aliases the Q tile) is free
 #pragma unroll
       for (int l = 0; l < kMaxL; ++l) {
         if (l < L) {
 #pragma unroll
           for (int i = 0; i < CW; ++i) {
-            int c = CM::chan(cg, i);
+            const int c = CM::chan(cg, i);
             float rw = 0.f, rwd = 0.f;
 #pragma unroll
             for (int k = 0; k < kMaxK; ++k) {
               if (k < K) {
-                float w = Wsm[(k * L + l) * DP + c];
+                const float w = Wsm[(k * L + l) * DP + c];
                 rw = fmaf(rbo[k], w, rw);
                 rwd = fmaf(rdo[k], w, rwd);
               }
             }
             xb[i] = fmaf(qb[l][i], rw, xb[i]);
-            float rbar = qb[l][i] * xo[i];
+            const float rbar = qb[l][i] * xo[i];
             dd = fmaf(rbar, rwd, dd);
             Rst[(pg * L + l) * DP + c] = valid ? rbar : 0.f;
           }
@@ -395,21 +485,22 @@ triplet_bwd_kernel(const int64_t* __restrict__ edge_ptr, const int32_t* __restri
       if (valid) {
 #pragma unroll
         for (int i = 0; i < CW; ++i) {
-          int c = CM::chan(cg, i);
+          const int c = CM::chan(cg, i);
           if (c < dg) Xbar[rq * dg + c] = xb[i];
         }
         if (cg == 0) {
-          float inv = 1.f / uq.w;
+          const float inv = 1.f / uq.w;
+          const float4 f = Fs[q];
           float4 g = edge_grad[off + q];
-          g.x += fx * inv;
-          g.y += fy * inv;
-          g.z += fz * inv;
+          g.x += f.x * inv;
+          g.y += f.y * inv;
+          g.z += f.z * inv;
           g.w += dd;
           edge_grad[off + q] = g;
         }
       }
       __syncthreads();
-      // W_bar[k,l,c] += sum_rows rbf_k(row) * R_bar[row,l,c]  (thread-owned (l,c))
+      // W_bar[k,l,c] += sum_rows rbf_k(row) R_bar[row,l,c]   (thread-owned (l,c): no atomics)
       const int rows = min(GP, n - b0);
       for (int idx = tid; idx < L * DP; idx += kThreads) {
         for (int k = 0; k < K; ++k) {
@@ -423,7 +514,7 @@ triplet_bwd_kernel(const int64_t* __restrict__ edge_ptr, const int32_t* __restri
   __syncthreads();
   float* dst = wbar_part + static_cast<int64_t>(blockIdx.x) * K * L * dg;
   for (int idx = tid; idx < K * L * dg; idx += kThreads) {
-    int kl = idx / dg, c = idx - kl * dg;
+    const int kl = idx / dg, c = idx - kl * dg;
     dst[idx] = Wb[kl * DP + c];
   }
 }
@@ -477,20 +568,6 @@ __global__ void triplet_terms_kernel(const int64_t* __restrict__ edge_ptr,
 // ---------------------------------------------------------------------------
 // host dispatch
 // ---------------------------------------------------------------------------
-struct Variant {
-  int cw, gc, r;
-};
-
-static Variant pick_variant(int dg) {
-  if (dg <= 4) return {4, 1, 1};
-  if (dg <= 8) return {8, 1, 1};
-  if (dg <= 16) return {8, 2, 2};
-  if (dg <= 32) return {8, 4, 2};
-  if (dg <= 64) return {8, 8, 4};
-  if (dg <= 128) return {8, 16, 4};
-  return {8, 32, 4};
-}
-
 static int pick_qt(int K, int L, int DP, int extra_floats, int budget_bytes) {
   int fixed = 4 * (K * L * DP + extra_floats) + 64;
   int per_row = 4 * (L * DP + 4 + K);
@@ -519,41 +596,30 @@ static int launch_fwd(const int64_t* edge_ptr, const int32_t* rev, const float4*
   return check_launch("triplet_fwd");
 }
 
-template <int CW, int GC>
-static int bwd_grid_and_smem(int64_t nv, int K, int L, int dg, int* grid_out, size_t* smem_out, int* qt_out) {
-  constexpr int DP = CW * GC, GP = kThreads / GC;
-  int extra_guess = BwdExtra(16, K, L, DP, GP).total;
-  int qt = pick_qt(K, L, DP, extra_guess, 96 * 1024);
-  BwdExtra Bx(qt, K, L, DP, GP);
-  TileLayout Ly(qt, K, L, DP, Bx.total);
-  size_t smem = static_cast<size_t>(Ly.total) * 4;
-  auto kern = triplet_bwd_kernel<CW, GC>;
+template <int CW, int GC, int R>
+static int launch_bwd(const int64_t* edge_ptr, const int32_t* rev, const float4* geo, int64_t nv,
+                      const float* X, const float* W, int K, int L, int dg, int max_deg, RbfParams rp,
+                      const float* Sbar, float* Xbar, float* Wbar, float4* edge_grad, void* ws,
+                      cudaStream_t st) {
+  constexpr int DP = CW * GC, GP = kThreads / GC, PB = GP * R;
+  const int nmax = max_deg > 2 ? max_deg : 2;
+  // pick the largest tile (<= 32 rows) that keeps shared memory under ~100 KB
+  int qt = 32;
+  while (qt > 4 && BwdLayout(qt, K, L, DP, GP, PB, nmax).total * 4 > 100 * 1024) qt -= 4;
+  const size_t smem = static_cast<size_t>(BwdLayout(qt, K, L, DP, GP, PB, nmax).total) * 4;
+  EGN_REQUIRE(smem <= 227 * 1024, "triplet backward needs %zu bytes of shared memory (max degree %d)", smem, max_deg);
+  auto kern = triplet_bwd_kernel<CW, GC, R>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, smem);
   if (per_sm < 1) per_sm = 1;
   if (per_sm > 4) per_sm = 4;
-  int64_t grid = std::min<int64_t>(nv, static_cast<int64_t>(kNumSMs) * per_sm);
-  if (grid < 1) grid = 1;
-  *grid_out = static_cast<int>(grid);
-  *smem_out = smem;
-  *qt_out = qt;
-  return 0;
-}
-
-template <int CW, int GC>
-static int launch_bwd(const int64_t* edge_ptr, const int32_t* rev, const float4* geo, int64_t nv,
-                      const float* X, const float* W, int K, int L, int dg, RbfParams rp,
-                      const float* Sbar, float* Xbar, float* Wbar, float4* edge_grad, void* ws,
-                      cudaStream_t st) {
-  int grid, qt;
-  size_t smem;
-  bwd_grid_and_smem<CW, GC>(nv, K, L, dg, &grid, &smem, &qt);
+  const int grid = static_cast<int>(std::min<int64_t>(nv, static_cast<int64_t>(kNumSMs) * per_sm));
   float* part = reinterpret_cast<float*>(ws);
-  triplet_bwd_kernel<CW, GC><<<grid, kThreads, smem, st>>>(edge_ptr, rev, geo, nv, X, W, K, L, dg,
-                                                           qt, rp, Sbar, Xbar, part, edge_grad);
+  kern<<<grid, kThreads, smem, st>>>(edge_ptr, rev, geo, nv, X, W, K, L, dg, qt, nmax, rp, Sbar, Xbar, part,
+                                     edge_grad);
   if (check_launch("triplet_bwd")) return 1;
-  int64_t len = static_cast<int64_t>(K) * L * dg;
+  const int64_t len = static_cast<int64_t>(K) * L * dg;
   reduce_partials_kernel<<<grid_for(len, 256), 256, 0, st>>>(part, grid, len, Wbar);
   return check_launch("triplet_bwd_reduce");
 }
@@ -562,16 +628,6 @@ static int launch_bwd(const int64_t* edge_ptr, const int32_t* rev, const float4*
 
 using namespace egn;
 
-#define EGN_DISPATCH_DG(dg, FN, ...)                          \
-  do {                                                        \
-    if ((dg) <= 4) return FN<4, 1>(__VA_ARGS__);              \
-    if ((dg) <= 8) return FN<8, 1>(__VA_ARGS__);              \
-    if ((dg) <= 16) return FN<8, 2>(__VA_ARGS__);             \
-    if ((dg) <= 32) return FN<8, 4>(__VA_ARGS__);             \
-    if ((dg) <= 64) return FN<8, 8>(__VA_ARGS__);             \
-    if ((dg) <= 128) return FN<8, 16>(__VA_ARGS__);           \
-    return FN<8, 32>(__VA_ARGS__);                            \
-  } while (0)
 
 static int check_dims(int K, int L, int dg) {
   EGN_REQUIRE(K >= 1 && K <= 16, "k_rbf must be in [1, 16], got %d", K);
@@ -605,8 +661,8 @@ int64_t egn_triplet_bwd_workspace_bytes(int64_t num_nodes, int k_rbf, int l_sbf,
 }
 
 int egn_triplet_bwd(const int64_t* edge_ptr, const int32_t* rev, const float* geo,
-                    int64_t num_nodes, const float* X, const float* W, int k_rbf, int l_sbf,
-                    int dg, double cutoff, const float* S_bar, float* X_bar, float* W_bar,
+                    int64_t num_nodes, int max_degree, const float* X, const float* W, int k_rbf,
+                    int l_sbf, int dg, double cutoff, const float* S_bar, float* X_bar, float* W_bar,
                     float* edge_grad, void* workspace, egn_stream_t stream) {
   if (int rc = check_dims(k_rbf, l_sbf, dg)) return rc;
   cudaStream_t st = as_stream(stream);
@@ -617,8 +673,17 @@ int egn_triplet_bwd(const int64_t* edge_ptr, const int32_t* rev, const float* ge
   RbfParams rp = rbf_params(k_rbf, cutoff);
   const float4* g4 = reinterpret_cast<const float4*>(geo);
   float4* eg = reinterpret_cast<float4*>(edge_grad);
-  EGN_DISPATCH_DG(dg, launch_bwd, edge_ptr, rev, g4, num_nodes, X, W, k_rbf, l_sbf, dg, rp, S_bar,
-                  X_bar, W_bar, eg, workspace, st);
+#define EGN_BWD(CW, GC, R) \
+  return launch_bwd<CW, GC, R>(edge_ptr, rev, g4, num_nodes, X, W, k_rbf, l_sbf, dg, max_degree, rp, S_bar, X_bar, \
+                               W_bar, eg, workspace, st)
+  if (dg <= 4) EGN_BWD(4, 1, 1);
+  if (dg <= 8) EGN_BWD(8, 1, 1);
+  if (dg <= 16) EGN_BWD(8, 2, 2);
+  if (dg <= 32) EGN_BWD(8, 4, 2);
+  if (dg <= 64) EGN_BWD(8, 8, 4);
+  if (dg <= 128) EGN_BWD(8, 16, 4);
+  EGN_BWD(8, 32, 4);
+#undef EGN_BWD
 }
 
 int egn_triplet_terms(const int64_t* edge_ptr, const int32_t* rev, const float* geo,

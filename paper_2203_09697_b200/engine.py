@@ -181,6 +181,7 @@ class Engine:
         if d_forces is not None and not gem:
             raise ValueError("force seed given but this variant has no force head")
         de = c.d_e
+        wg, cs = ops.wgrad, ops.column_sum
         self.weights.grad_flat.zero_()
         eg = torch.zeros((bg.num_edges, 4), dtype=torch.float32, device=bg.device)
         dE = d_energy.to(torch.float32).view(-1, 1)
@@ -206,71 +207,69 @@ class Engine:
             v_bar = ops.gather_rows(bg.node_graph, s_bar)
             if gem:
                 # sym (engine.py:195-200)
-                torch.mm(m_bar.t(), st["m2r"], out=gr[p + "sym.w"])
+                wg(m_bar, st["m2r"], out=gr[p + "sym.w"])
                 t = m_bar @ w[p + "sym.w"]
                 m2_bar = ops.gather_rows(bg.rev, t, out=m_bar.clone(), accumulate=True)
                 # EU2 (engine.py:180-192)
-                torch.mm(m2_bar.t(), st["a2"], out=gr[p + "eu2.w2"])
-                gr[p + "eu2.b2"].copy_(m2_bar.sum(0))
+                wg(m2_bar, st["a2"], out=gr[p + "eu2.w2"])
+                cs(m2_bar, out=gr[p + "eu2.b2"])
                 h2_bar = _silu_bwd(m2_bar @ w[p + "eu2.w2"], st["h2"])
-                gr[p + "eu2.b1"].copy_(h2_bar.sum(0))
+                cs(h2_bar, out=gr[p + "eu2.b1"])
                 w1 = w[p + "eu2.w1"]
-                gr[p + "eu2.w1"][:, :de].copy_(h2_bar.t() @ st["m_new"])
+                gr[p + "eu2.w1"][:, :de].copy_(wg(h2_bar, st["m_new"]))
                 pv_bar = ops.aggregate_in_edges(bg.edge_ptr, bg.rev, h2_bar)
                 gr[p + "eu2.w1"][:, de:].copy_(pv_bar.t() @ st["v"])
                 v_bar = torch.addmm(v_bar, pv_bar, w1[:, de:])
                 m_new_bar = torch.addmm(m2_bar, h2_bar, w1[:, :de])
             else:
-                m_new_bar = m_bar
+                m_new_bar = m_bar.clone()
             # EA + NU (engine.py:166-177)
             torch.mm(v_bar.t(), st["av"], out=gr[p + "nu.w2"])
-            gr[p + "nu.b2"].copy_(v_bar.sum(0))
+            cs(v_bar, out=gr[p + "nu.b2"])
             hv_bar = _silu_bwd(v_bar @ w[p + "nu.w2"], st["hv"])
-            gr[p + "nu.b1"].copy_(hv_bar.sum(0))
+            cs(hv_bar, out=gr[p + "nu.b1"])
             torch.mm(hv_bar.t(), st["agg"], out=gr[p + "nu.w1"])
             agg_bar = hv_bar @ w[p + "nu.w1"]
-            if m_new_bar is m_bar:
-                m_new_bar = m_bar.clone()
             ops.gather_rows(bg.recv, agg_bar, out=m_new_bar, accumulate=True)
             # EU (engine.py:152-158)
-            torch.mm(m_new_bar.t(), st["a1"], out=gr[p + "eu.w2"])
-            gr[p + "eu.b2"].copy_(m_new_bar.sum(0))
+            wg(m_new_bar, st["a1"], out=gr[p + "eu.w2"])
+            cs(m_new_bar, out=gr[p + "eu.b2"])
             h_bar = _silu_bwd(m_new_bar @ w[p + "eu.w2"], st["h"])
-            gr[p + "eu.b1"].copy_(h_bar.sum(0))
-            torch.mm(h_bar.t(), st["xcat"], out=gr[p + "eu.w1"])
+            cs(h_bar, out=gr[p + "eu.b1"])
+            wg(h_bar, st["xcat"], out=gr[p + "eu.w1"])
             x_bar = h_bar @ w[p + "eu.w1"]
-            m_in_bar = m_new_bar + x_bar[:, :de]
+            m_in_bar = m_new_bar.add_(x_bar[:, :de])
             ta_bar = x_bar[:, de:]
             # TU (engine.py:118-149)
-            torch.mm(ta_bar.t(), st["Y"], out=gr[p + "tu.up"])
+            wg(ta_bar, st["Y"], out=gr[p + "tu.up"])
             Y_bar = ta_bar @ w[p + "tu.up"]
             if gem:
                 Z_bar = Y_bar * st["g"]
                 g_bar = Y_bar * st["Z"]
-                torch.mm(Z_bar.t(), st["S"], out=gr[p + "tu.bilinear_proj"])
+                wg(Z_bar, st["S"], out=gr[p + "tu.bilinear_proj"])
                 S_bar = Z_bar @ w[p + "tu.bilinear_proj"]
             else:
                 S_bar = Y_bar * st["g"]
                 g_bar = Y_bar * st["S"]
-            torch.mm(g_bar.t(), fw.rbf, out=gr[p + "tu.rbf_gate"])
+            wg(g_bar, fw.rbf, out=gr[p + "tu.rbf_gate"])
             rbf_bar.addmm_(g_bar, w[p + "tu.rbf_gate"])
             X_bar, Wk_bar = ops.triplet_bwd(bg.edge_ptr, bg.rev, bg.geo, st["X"], st["Wk"], c.cutoff,
-                                            S_bar, eg)
+                                            S_bar, eg, max_degree=bg.max_deg)
             wp_bar = Wk_bar.permute(2, 0, 1).reshape(Wk_bar.shape[2], -1)  # [dg, K*L]
             if gem:
                 torch.mm(wp_bar, w[p + "tu.sbf_gate"].t(), out=gr[p + "tu.bilinear_b"])
                 torch.mm(w[p + "tu.bilinear_b"].t(), wp_bar, out=gr[p + "tu.sbf_gate"])
-                torch.mm(X_bar.t(), st["down"], out=gr[p + "tu.bilinear_a"])
+                wg(X_bar, st["down"], out=gr[p + "tu.bilinear_a"])
                 down_bar = X_bar @ w[p + "tu.bilinear_a"]
             else:
                 gr[p + "tu.sbf_gate"].copy_(wp_bar)
                 down_bar = X_bar
             m_in = st["xcat"][:, :de]
-            torch.mm(down_bar.t(), m_in, out=gr[p + "tu.down"])
+            wg(down_bar, m_in, out=gr[p + "tu.down"])
             m_bar = m_in_bar.addmm_(down_bar, w[p + "tu.down"])
         # edge init (engine.py:109-111)
-        torch.mm(m_bar.t(), fw.rbf, out=gr["edge_init.w"])
-        gr["edge_init.b"].copy_(m_bar.sum(0))
+        wg(m_bar, fw.rbf, out=gr["edge_init.w"])
+        cs(m_bar, out=gr["edge_init.b"])
         rbf_bar.addmm_(m_bar, w["edge_init.w"])
         ops.rbf_bwd(bg.geo, rbf_bar, c.cutoff, eg)
         return ops.positions_bwd(bg.edge_ptr, bg.rev, bg.geo, eg)

@@ -40,6 +40,7 @@ class BatchGraph:
     geo: torch.Tensor  # f32 [E, 4]  (ux, uy, uz, d)
     graph_sizes: list  # host: atoms per graph
     edge_counts: list | None = None  # host: edges per graph (lazily)
+    max_deg: int = 0  # host: max out-degree (sizes the backward tile)
 
     @property
     def device(self):
@@ -79,13 +80,14 @@ def build_batch(systems, cutoff: float, device="cuda", positions: torch.Tensor |
     deg = ops.neighbors_count(pos, graph_ptr, node_graph, cutoff)
     edge_ptr = ops.scan_counts(deg)
     tri_ptr = ops.scan_counts(deg, square_minus_one=True)
-    counts = torch.stack([edge_ptr[-1], tri_ptr[-1]]).cpu()  # the one host sync
-    ne, nt = int(counts[0]), int(counts[1])
+    dmax = deg.max().to(torch.int64) if pos.shape[0] else edge_ptr[-1]
+    counts = torch.stack([edge_ptr[-1], tri_ptr[-1], dmax]).cpu()  # the one host sync
+    ne, nt, max_deg = int(counts[0]), int(counts[1]), int(counts[2])
     src, recv = ops.neighbors_fill(pos, graph_ptr, node_graph, cutoff, edge_ptr, ne)
     rev, missing = ops.reverse_edges(edge_ptr, src, recv)
     geo, _, _ = ops.geometry(pos, src, recv)
     return BatchGraph(g, int(pos.shape[0]), ne, nt, float(cutoff), pos, graph_ptr, node_graph, deg,
-                      edge_ptr, src, recv, rev, tri_ptr, geo, list(sizes))
+                      edge_ptr, src, recv, rev, tri_ptr, geo, list(sizes), max_deg=max_deg)
 
 
 # ---------------------------------------------------------------------------

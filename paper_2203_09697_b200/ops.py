@@ -109,7 +109,7 @@ def _workspace(nbytes: int, device) -> torch.Tensor:
     return buf
 
 
-def triplet_bwd(edge_ptr, rev, geo, X, Wk, cutoff, S_bar, edge_grad, X_bar=None, W_bar=None):
+def triplet_bwd(edge_ptr, rev, geo, X, Wk, cutoff, S_bar, edge_grad, X_bar=None, W_bar=None, max_degree=None):
     X = _c(X, torch.float32)
     Wk = _c(Wk, torch.float32)
     S_bar = _c(S_bar, torch.float32)
@@ -119,9 +119,12 @@ def triplet_bwd(edge_ptr, rev, geo, X, Wk, cutoff, S_bar, edge_grad, X_bar=None,
         X_bar = torch.empty_like(X)
     if W_bar is None:
         W_bar = torch.empty_like(Wk)
+    if max_degree is None:
+        max_degree = int((edge_ptr[1:] - edge_ptr[:-1]).max().item()) if nv else 0
     nbytes = call("egn_triplet_bwd_workspace_bytes", nv, k, l, dg)
     ws = _workspace(nbytes, X.device)
-    call("egn_triplet_bwd", ptr(edge_ptr), ptr(rev), ptr(geo), nv, ptr(X), ptr(Wk), k, l, dg, float(cutoff),
+    call("egn_triplet_bwd", ptr(edge_ptr), ptr(rev), ptr(geo), nv, int(max_degree), ptr(X), ptr(Wk), k, l, dg,
+         float(cutoff),
          ptr(S_bar), ptr(X_bar), ptr(W_bar), ptr(edge_grad), ptr(ws), stream())
     return X_bar, W_bar
 
@@ -191,6 +194,50 @@ def positions_bwd(edge_ptr, rev, geo, edge_grad):
     out = torch.empty((nv, 3), dtype=torch.float64, device=geo.device)
     call("egn_positions_bwd", ptr(edge_ptr), ptr(rev), ptr(geo), nv, ptr(edge_grad), ptr(out), stream())
     return out
+
+
+def column_sum(x, out=None):
+    """out[c] = sum_r x[r, c] (deterministic)."""
+    rows, d = x.shape
+    if x.stride(1) != 1:
+        x = x.contiguous()
+    if out is None:
+        out = torch.empty(d, dtype=torch.float32, device=x.device)
+    nbytes = call("egn_column_sum_workspace_bytes", rows, d)
+    ws = _workspace_named("colsum", nbytes, x.device)
+    call("egn_column_sum", ptr(x), rows, d, x.stride(0), ptr(out), ptr(ws), stream())
+    return out
+
+
+def _workspace_named(name: str, nbytes: int, device) -> torch.Tensor:
+    key = (str(device), name)
+    buf = _WS.get(key)
+    if buf is None or buf.numel() < nbytes:
+        buf = torch.empty(max(nbytes, 1 << 16), dtype=torch.uint8, device=device)
+        _WS[key] = buf
+    return buf
+
+
+def wgrad(g: torch.Tensor, x: torch.Tensor, out: torch.Tensor | None = None, splits: int = 64) -> torch.Tensor:
+    """g^T x for tall-skinny operands (rows >> cols): split-K batched GEMM + ordered sum.
+
+    cuBLAS runs a [a, b] = [E, a]^T [E, b] product with only (a/64)(b/64)
+    CTAs; splitting the E dimension into `splits` batches fills the GPU."""
+    rows = g.shape[0]
+    chunk = rows // splits
+    if chunk < 256:
+        res = g.t() @ x
+    else:
+        n = chunk * splits
+        gb = g[:n].reshape(splits, chunk, g.shape[1])
+        xb = x[:n].reshape(splits, chunk, x.shape[1])
+        res = torch.bmm(gb.transpose(1, 2), xb).sum(0)
+        if n < rows:
+            res = res.addmm_(g[n:].t(), x[n:])
+    if out is not None:
+        out.copy_(res)
+        return out
+    return res
 
 
 def sgd_(w, g, lr):

@@ -108,6 +108,27 @@ def test_triplet_collinear_and_low_degree():
         assert np.abs(pb - pbr).max() < 1e-4 * max(1.0, np.abs(pbr).max())
 
 
+def test_degree_one_centres_zero_their_in_edge_gradient():
+    """A centre of degree 1 has no triplets; its in-edge must get X_bar == 0 even
+    when the output buffer starts as garbage."""
+    from paper_2203_09697_b200 import ops
+    from paper_2203_09697_b200.graph import build_batch
+
+    # atom 3 is bonded only to atom 2 (degree 1); the rest form a triangle
+    pos = np.array([[0.0, 0, 0], [1.0, 0, 0], [0.5, 0.8, 0], [0.5, 2.0, 0.0]])
+    bg = build_batch([pos], 1.3)
+    dg = 8
+    X = torch.randn((bg.num_edges, dg), device="cuda")
+    W = torch.randn((6, 4, dg), device="cuda")
+    B = torch.randn((bg.num_edges, dg), device="cuda")
+    eg = torch.zeros((bg.num_edges, 4), device="cuda")
+    Xb = torch.full_like(X, float("nan"))
+    ops.triplet_bwd(bg.edge_ptr, bg.rev, bg.geo, X, W, 1.3, B, eg, X_bar=Xb)
+    assert torch.isfinite(Xb).all()
+    _, _, Xb_ref, _, _ = _ref(pos, 1.3, X.double().cpu().numpy(), W.double().cpu().numpy(), B.double().cpu().numpy())
+    assert max_rel(Xb.cpu().numpy(), Xb_ref) < TOL
+
+
 def test_triplet_terms_and_sbf_debug_outputs():
     from paper_2203_09697_b200 import ops
     from paper_2203_09697_b200.graph import build_batch
