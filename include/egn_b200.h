@@ -108,10 +108,11 @@ int egn_sbf(const float* geo, const int64_t* edge_ptr, const int64_t* tri_ptr, i
  * The gate by rbf(d_ji) and the up projection are applied by the caller on
  * the per-edge result, which is exact because both are constant or linear
  * inside a triplet segment (engine.py:138,147-148).
+ * max_degree: max deg(j) if known (selects the deg<=64 fast path alone), -1 if not.
  */
 int egn_triplet_fwd(const int64_t* edge_ptr, const int32_t* rev, const float* geo,
-                    int64_t num_nodes, const float* X, const float* W, int k_rbf, int l_sbf,
-                    int dg, double cutoff, float* S, egn_stream_t stream);
+                    int64_t num_nodes, int max_degree, const float* X, const float* W, int k_rbf,
+                    int l_sbf, int dg, double cutoff, float* S, egn_stream_t stream);
 
 /* Adjoint of egn_triplet_fwd (tape.py gather/segment_sum/linear/angular_sbf VJPs).
  * Inputs S_bar [E,dg].  Outputs:
@@ -122,11 +123,13 @@ int egn_triplet_fwd(const int64_t* edge_ptr, const int32_t* rev, const float* ge
  *                              in-edge distance of the basis.
  * max_degree bounds deg(j) over all centres (sizes shared memory).
  * workspace: egn_triplet_bwd_workspace_bytes(...) bytes of device memory. */
-int64_t egn_triplet_bwd_workspace_bytes(int64_t num_nodes, int k_rbf, int l_sbf, int dg);
+int64_t egn_triplet_bwd_workspace_bytes(int64_t num_nodes, int64_t num_edges, int k_rbf, int l_sbf,
+                                        int dg);
 int egn_triplet_bwd(const int64_t* edge_ptr, const int32_t* rev, const float* geo,
-                    int64_t num_nodes, int max_degree, const float* X, const float* W, int k_rbf,
-                    int l_sbf, int dg, double cutoff, const float* S_bar, float* X_bar, float* W_bar,
-                    float* edge_grad, void* workspace, egn_stream_t stream);
+                    int64_t num_nodes, int64_t num_edges, int max_degree, const float* X,
+                    const float* W, int k_rbf, int l_sbf, int dg, double cutoff, const float* S_bar,
+                    float* X_bar, float* W_bar, float* edge_grad, void* workspace,
+                    egn_stream_t stream);
 
 /* Per-triplet feature debug output t_feat-like rows for parity tests:
  * P[t, c] = X[rq, c] * sum_l T_l(x_pq) Rw[rq, l, c] for every triplet t in
@@ -147,6 +150,12 @@ int egn_aggregate_in_edges(const int64_t* edge_ptr, const int32_t* rev, int64_t 
 /* out[e, c] (+)= x[idx[e], c]: row gather with optional accumulate (gather, tape.py:129-139). */
 int egn_gather_rows(const int32_t* idx, int64_t rows, const float* x, int64_t ld_x, int d,
                     float* out, int64_t ld_out, int accumulate, egn_stream_t stream);
+
+/* out[dst[r], c] (+)= x[src[r], c] with distinct dst within one call: the adjoint of a
+ * row gather restricted to one rank's rows (graph-parallel backward, runtime.py). */
+int egn_scatter_rows(const int32_t* dst, const int32_t* src, int64_t rows, const float* x,
+                     int64_t ld_x, int d, float* out, int64_t ld_out, int accumulate,
+                     egn_stream_t stream);
 
 /* out[g, c] = sum_{v in graph g} x[v, c]  (sum_rows in record_gu_head, engine.py:207-211). */
 int egn_graph_sum(const int64_t* graph_ptr, int64_t num_graphs, const float* x, int d,

@@ -36,12 +36,14 @@ SIGNATURES: dict[str, tuple] = {
     "egn_triplet_angles": (_i32, [_p, _p, _p, _p, _i64, _p, _p]),
     "egn_rbf": (_i32, [_p, _i64, _i32, _f64, _p, _p]),
     "egn_sbf": (_i32, [_p, _p, _p, _i64, _i32, _i32, _f64, _p, _p]),
-    "egn_triplet_fwd": (_i32, [_p, _p, _p, _i64, _p, _p, _i32, _i32, _i32, _f64, _p, _p]),
-    "egn_triplet_bwd_workspace_bytes": (_i64, [_i64, _i32, _i32, _i32]),
-    "egn_triplet_bwd": (_i32, [_p, _p, _p, _i64, _i32, _p, _p, _i32, _i32, _i32, _f64, _p, _p, _p, _p, _p, _p]),
+    "egn_triplet_fwd": (_i32, [_p, _p, _p, _i64, _i32, _p, _p, _i32, _i32, _i32, _f64, _p, _p]),
+    "egn_triplet_bwd_workspace_bytes": (_i64, [_i64, _i64, _i32, _i32, _i32]),
+    "egn_triplet_bwd": (_i32, [_p, _p, _p, _i64, _i64, _i32, _p, _p, _i32, _i32, _i32, _f64, _p, _p, _p, _p, _p,
+                               _p]),
     "egn_triplet_terms": (_i32, [_p, _p, _p, _p, _i64, _p, _p, _i32, _i32, _i32, _f64, _p, _p]),
     "egn_aggregate_in_edges": (_i32, [_p, _p, _i64, _p, _i64, _i32, _p, _p]),
     "egn_gather_rows": (_i32, [_p, _i64, _p, _i64, _i32, _p, _i64, _i32, _p]),
+    "egn_scatter_rows": (_i32, [_p, _p, _i64, _p, _i64, _i32, _p, _i64, _i32, _p]),
     "egn_graph_sum": (_i32, [_p, _i64, _p, _i32, _p, _p]),
     "egn_force_head_fwd": (_i32, [_p, _p, _p, _i64, _i64, _p, _i32, _p, _p, _p, _p]),
     "egn_force_head_bwd_workspace_bytes": (_i64, [_i64, _i32]),
@@ -93,7 +95,7 @@ def stream() -> int:
 
 # Kernels launched per successful ABI call (for the bench's gpu_launches count).
 KERNELS_PER_CALL = {
-    "egn_triplet_bwd": 2, "egn_force_head_fwd": 2, "egn_force_head_bwd": 2, "egn_column_sum": 2,
+    "egn_triplet_bwd": 4, "egn_force_head_fwd": 2, "egn_force_head_bwd": 2, "egn_column_sum": 2,
 }
 LAUNCH_COUNTER = {"calls": 0, "kernels": 0}
 

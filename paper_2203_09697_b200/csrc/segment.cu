@@ -95,6 +95,20 @@ __global__ void gather_rows_kernel(const int32_t* __restrict__ idx, int64_t rows
   }
 }
 
+// out[dst[r]] (+)= x[src[r]]; destinations are distinct within one call (no races).
+__global__ void scatter_rows_kernel(const int32_t* __restrict__ dst, const int32_t* __restrict__ src, int64_t rows,
+                                    const float* __restrict__ x, int64_t ldx, int d, float* __restrict__ out,
+                                    int64_t ldo, int accumulate) {
+  int lane = threadIdx.x & 31;
+  int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = warp; r < rows; r += nwarps) {
+    const float* s = x + static_cast<int64_t>(src[r]) * ldx;
+    float* o = out + static_cast<int64_t>(dst[r]) * ldo;
+    for (int c = lane; c < d; c += 32) o[c] = accumulate ? o[c] + s[c] : s[c];
+  }
+}
+
 // One CTA per (graph, 128-channel chunk); deterministic tree over nodes.
 __global__ void graph_sum_kernel(const int64_t* __restrict__ graph_ptr, int64_t ng,
                                  const float* __restrict__ x, int d, float* __restrict__ out) {
@@ -321,6 +335,14 @@ int egn_gather_rows(const int32_t* idx, int64_t rows, const float* x, int64_t ld
   gather_rows_kernel<<<grid_for(rows * 32, 256), 256, 0, as_stream(stream)>>>(
       idx, rows, x, ld_x, d, out, ld_out, accumulate);
   return check_launch("gather_rows");
+}
+
+int egn_scatter_rows(const int32_t* dst, const int32_t* src, int64_t rows, const float* x, int64_t ld_x, int d,
+                     float* out, int64_t ld_out, int accumulate, egn_stream_t stream) {
+  if (rows == 0) return 0;
+  scatter_rows_kernel<<<grid_for(rows * 32, 256), 256, 0, as_stream(stream)>>>(dst, src, rows, x, ld_x, d, out,
+                                                                               ld_out, accumulate);
+  return check_launch("scatter_rows");
 }
 
 int egn_graph_sum(const int64_t* graph_ptr, int64_t num_graphs, const float* x, int d,

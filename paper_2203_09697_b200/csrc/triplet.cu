@@ -136,7 +136,7 @@ __global__ void __launch_bounds__(kThreads)
 triplet_fwd_kernel(const int64_t* __restrict__ edge_ptr, const int32_t* __restrict__ rev,
                    const float4* __restrict__ geo, int64_t nv, const float* __restrict__ X,
                    const float* __restrict__ W, int K, int L, int dg, int qt, RbfParams rp,
-                   float* __restrict__ S) {
+                   float* __restrict__ S, int min_n) {
   using CM = ChanMap<CW, GC>;
   constexpr int GP = kThreads / GC, VW = CM::VW, DP = CM::DP;
   extern __shared__ __align__(16) float sm[];
@@ -151,7 +151,7 @@ triplet_fwd_kernel(const int64_t* __restrict__ edge_ptr, const int32_t* __restri
   for (int64_t j = blockIdx.x; j < nv; j += gridDim.x) {
     const int64_t off = edge_ptr[j];
     const int n = static_cast<int>(edge_ptr[j + 1] - off);
-    if (n == 0) continue;
+    if (n == 0 || n <= min_n) continue;  // centres with n <= min_n run on the fast path
     for (int p0 = 0; p0 < n; p0 += GP * R) {
       const int reff = min(R, (n - p0 + GP - 1) / GP);  // CTA-uniform
       float4 up[R];
@@ -250,7 +250,7 @@ template <int CW, int GC, int R1>
 __global__ void __launch_bounds__(kThreads)
 triplet_bwd_kernel(const int64_t* __restrict__ edge_ptr, const int32_t* __restrict__ rev,
                    const float4* __restrict__ geo, int64_t nv, const float* __restrict__ X,
-                   const float* __restrict__ W, int K, int L, int dg, int qt, int nmax, RbfParams rp,
+                   const float* __restrict__ W, int K, int L, int dg, int qt, int nmax, int min_n, RbfParams rp,
                    const float* __restrict__ Sbar, float* __restrict__ Xbar,
                    float* __restrict__ wbar_part, float4* __restrict__ edge_grad) {
   using CM = ChanMap<CW, GC>;
@@ -276,6 +276,7 @@ triplet_bwd_kernel(const int64_t* __restrict__ edge_ptr, const int32_t* __restri
   for (int64_t j = blockIdx.x; j < nv; j += gridDim.x) {
     const int64_t off = edge_ptr[j];
     const int n = static_cast<int>(edge_ptr[j + 1] - off);
+    if (n <= min_n) continue;  // handled by the fast path
     if (n < 2) {
       // no triplets at this centre: its in-edge (if any) gets a zero X_bar row
       if (n == 1) {
@@ -520,14 +521,24 @@ triplet_bwd_kernel(const int64_t* __restrict__ edge_ptr, const int32_t* __restri
 }
 
 __global__ void reduce_partials_kernel(const float* __restrict__ part, int nparts, int64_t len,
-                                       float* __restrict__ out) {
+                                       float* __restrict__ out, int accumulate) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < len;
        i += (int64_t)gridDim.x * blockDim.x) {
     float s = 0.f;
     for (int p = 0; p < nparts; ++p) s += part[p * len + i];
-    out[i] = s;
+    out[i] = accumulate ? out[i] + s : s;
   }
 }
+
+// fast path (triplet_fast.cu): centres with deg <= 64 and (K, L) = (6, 7)
+bool fast_supported(int K, int L, int dg);
+int fast_fwd(const int64_t* edge_ptr, const int32_t* rev, const float4* geo, int64_t nv, const float* X,
+             const float* W, int K, int L, int dg, RbfParams rp, float* S, cudaStream_t st);
+int64_t fast_bwd_workspace_bytes(int64_t nv, int64_t ne, int K, int L, int dg);
+int fast_bwd(const int64_t* edge_ptr, const int32_t* rev, const float4* geo, int64_t nv, int64_t ne,
+             const float* X, const float* W, int K, int L, int dg, RbfParams rp, const float* Sbar, float* Xbar,
+             float* Wbar, float4* edge_grad, void* ws, cudaStream_t st);
+constexpr int kFastMaxDeg = 64;
 
 // Debug: per-triplet summand P[t, c] in (out, in) order.
 __global__ void triplet_terms_kernel(const int64_t* __restrict__ edge_ptr,
@@ -580,7 +591,7 @@ static int pick_qt(int K, int L, int DP, int extra_floats, int budget_bytes) {
 template <int CW, int GC, int R>
 static int launch_fwd(const int64_t* edge_ptr, const int32_t* rev, const float4* geo, int64_t nv,
                       const float* X, const float* W, int K, int L, int dg, RbfParams rp, float* S,
-                      cudaStream_t st) {
+                      int min_n, cudaStream_t st) {
   constexpr int DP = CW * GC;
   int qt = pick_qt(K, L, DP, 0, 48 * 1024);
   TileLayout Ly(qt, K, L, DP, 0);
@@ -592,7 +603,7 @@ static int launch_fwd(const int64_t* edge_ptr, const int32_t* rev, const float4*
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, smem);
   if (per_sm < 1) per_sm = 1;
   int64_t grid = std::min<int64_t>(nv, static_cast<int64_t>(kNumSMs) * per_sm * 4);
-  kern<<<static_cast<int>(grid), kThreads, smem, st>>>(edge_ptr, rev, geo, nv, X, W, K, L, dg, qt, rp, S);
+  kern<<<static_cast<int>(grid), kThreads, smem, st>>>(edge_ptr, rev, geo, nv, X, W, K, L, dg, qt, rp, S, min_n);
   return check_launch("triplet_fwd");
 }
 
@@ -600,8 +611,9 @@ template <int CW, int GC, int R>
 static int launch_bwd(const int64_t* edge_ptr, const int32_t* rev, const float4* geo, int64_t nv,
                       const float* X, const float* W, int K, int L, int dg, int max_deg, RbfParams rp,
                       const float* Sbar, float* Xbar, float* Wbar, float4* edge_grad, void* ws,
-                      cudaStream_t st) {
+                      int min_n, int accumulate, cudaStream_t st) {
   constexpr int DP = CW * GC, GP = kThreads / GC, PB = GP * R;
+  EGN_REQUIRE(max_deg >= 0, "triplet backward needs the maximum centre degree");
   const int nmax = max_deg > 2 ? max_deg : 2;
   // pick the largest tile (<= 32 rows) that keeps shared memory under ~100 KB
   int qt = 32;
@@ -616,11 +628,11 @@ static int launch_bwd(const int64_t* edge_ptr, const int32_t* rev, const float4*
   if (per_sm > 4) per_sm = 4;
   const int grid = static_cast<int>(std::min<int64_t>(nv, static_cast<int64_t>(kNumSMs) * per_sm));
   float* part = reinterpret_cast<float*>(ws);
-  kern<<<grid, kThreads, smem, st>>>(edge_ptr, rev, geo, nv, X, W, K, L, dg, qt, nmax, rp, Sbar, Xbar, part,
+  kern<<<grid, kThreads, smem, st>>>(edge_ptr, rev, geo, nv, X, W, K, L, dg, qt, nmax, min_n, rp, Sbar, Xbar, part,
                                      edge_grad);
   if (check_launch("triplet_bwd")) return 1;
   const int64_t len = static_cast<int64_t>(K) * L * dg;
-  reduce_partials_kernel<<<grid_for(len, 256), 256, 0, st>>>(part, grid, len, Wbar);
+  reduce_partials_kernel<<<grid_for(len, 256), 256, 0, st>>>(part, grid, len, Wbar, accumulate);
   return check_launch("triplet_bwd_reduce");
 }
 
@@ -639,31 +651,46 @@ static int check_dims(int K, int L, int dg) {
 extern "C" {
 
 int egn_triplet_fwd(const int64_t* edge_ptr, const int32_t* rev, const float* geo,
-                    int64_t num_nodes, const float* X, const float* W, int k_rbf, int l_sbf,
-                    int dg, double cutoff, float* S, egn_stream_t stream) {
+                    int64_t num_nodes, int max_degree, const float* X, const float* W, int k_rbf,
+                    int l_sbf, int dg, double cutoff, float* S, egn_stream_t stream) {
   if (int rc = check_dims(k_rbf, l_sbf, dg)) return rc;
   if (num_nodes == 0) return 0;
   RbfParams rp = rbf_params(k_rbf, cutoff);
   const float4* g4 = reinterpret_cast<const float4*>(geo);
   cudaStream_t st = as_stream(stream);
-  if (dg <= 4) return launch_fwd<4, 1, 1>(edge_ptr, rev, g4, num_nodes, X, W, k_rbf, l_sbf, dg, rp, S, st);
-  if (dg <= 8) return launch_fwd<8, 1, 1>(edge_ptr, rev, g4, num_nodes, X, W, k_rbf, l_sbf, dg, rp, S, st);
-  if (dg <= 16) return launch_fwd<8, 2, 2>(edge_ptr, rev, g4, num_nodes, X, W, k_rbf, l_sbf, dg, rp, S, st);
-  if (dg <= 32) return launch_fwd<8, 4, 2>(edge_ptr, rev, g4, num_nodes, X, W, k_rbf, l_sbf, dg, rp, S, st);
-  if (dg <= 64) return launch_fwd<8, 8, 4>(edge_ptr, rev, g4, num_nodes, X, W, k_rbf, l_sbf, dg, rp, S, st);
-  if (dg <= 128) return launch_fwd<8, 16, 4>(edge_ptr, rev, g4, num_nodes, X, W, k_rbf, l_sbf, dg, rp, S, st);
-  return launch_fwd<8, 32, 4>(edge_ptr, rev, g4, num_nodes, X, W, k_rbf, l_sbf, dg, rp, S, st);
+  int min_n = 0;
+  if (fast_supported(k_rbf, l_sbf, dg)) {
+    if (int rc = fast_fwd(edge_ptr, rev, g4, num_nodes, X, W, k_rbf, l_sbf, dg, rp, S, st)) return rc;
+    if (max_degree >= 0 && max_degree <= kFastMaxDeg) return 0;
+    min_n = kFastMaxDeg;
+  }
+#define EGN_FWD(CW, GC, R) \
+  return launch_fwd<CW, GC, R>(edge_ptr, rev, g4, num_nodes, X, W, k_rbf, l_sbf, dg, rp, S, min_n, st)
+  if (dg <= 4) EGN_FWD(4, 1, 1);
+  if (dg <= 8) EGN_FWD(8, 1, 1);
+  if (dg <= 16) EGN_FWD(8, 2, 2);
+  if (dg <= 32) EGN_FWD(8, 4, 2);
+  if (dg <= 64) EGN_FWD(8, 8, 4);
+  if (dg <= 128) EGN_FWD(8, 16, 4);
+  EGN_FWD(8, 32, 4);
+#undef EGN_FWD
 }
 
-int64_t egn_triplet_bwd_workspace_bytes(int64_t num_nodes, int k_rbf, int l_sbf, int dg) {
+static int64_t generic_ws_bytes(int64_t num_nodes, int k_rbf, int l_sbf, int dg) {
   int64_t grid = std::min<int64_t>(std::max<int64_t>(num_nodes, 1), static_cast<int64_t>(kNumSMs) * 4);
   return grid * k_rbf * l_sbf * dg * 4;
 }
 
+int64_t egn_triplet_bwd_workspace_bytes(int64_t num_nodes, int64_t num_edges, int k_rbf, int l_sbf, int dg) {
+  int64_t b = generic_ws_bytes(num_nodes, k_rbf, l_sbf, dg);
+  if (fast_supported(k_rbf, l_sbf, dg)) b += fast_bwd_workspace_bytes(num_nodes, num_edges, k_rbf, l_sbf, dg);
+  return b;
+}
+
 int egn_triplet_bwd(const int64_t* edge_ptr, const int32_t* rev, const float* geo,
-                    int64_t num_nodes, int max_degree, const float* X, const float* W, int k_rbf,
-                    int l_sbf, int dg, double cutoff, const float* S_bar, float* X_bar, float* W_bar,
-                    float* edge_grad, void* workspace, egn_stream_t stream) {
+                    int64_t num_nodes, int64_t num_edges, int max_degree, const float* X, const float* W,
+                    int k_rbf, int l_sbf, int dg, double cutoff, const float* S_bar, float* X_bar,
+                    float* W_bar, float* edge_grad, void* workspace, egn_stream_t stream) {
   if (int rc = check_dims(k_rbf, l_sbf, dg)) return rc;
   cudaStream_t st = as_stream(stream);
   if (num_nodes == 0) {
@@ -673,9 +700,19 @@ int egn_triplet_bwd(const int64_t* edge_ptr, const int32_t* rev, const float* ge
   RbfParams rp = rbf_params(k_rbf, cutoff);
   const float4* g4 = reinterpret_cast<const float4*>(geo);
   float4* eg = reinterpret_cast<float4*>(edge_grad);
+  int min_n = 0, accumulate = 0;
+  if (fast_supported(k_rbf, l_sbf, dg)) {
+    char* fws = reinterpret_cast<char*>(workspace) + generic_ws_bytes(num_nodes, k_rbf, l_sbf, dg);
+    if (int rc = fast_bwd(edge_ptr, rev, g4, num_nodes, num_edges, X, W, k_rbf, l_sbf, dg, rp, S_bar, X_bar,
+                          W_bar, eg, fws, st))
+      return rc;
+    if (max_degree >= 0 && max_degree <= kFastMaxDeg) return 0;
+    min_n = kFastMaxDeg;
+    accumulate = 1;
+  }
 #define EGN_BWD(CW, GC, R) \
   return launch_bwd<CW, GC, R>(edge_ptr, rev, g4, num_nodes, X, W, k_rbf, l_sbf, dg, max_degree, rp, S_bar, X_bar, \
-                               W_bar, eg, workspace, st)
+                               W_bar, eg, workspace, min_n, accumulate, st)
   if (dg <= 4) EGN_BWD(4, 1, 1);
   if (dg <= 8) EGN_BWD(8, 1, 1);
   if (dg <= 16) EGN_BWD(8, 2, 2);

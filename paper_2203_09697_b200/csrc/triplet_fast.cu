@@ -1,0 +1,526 @@
+// Fast path of the triplet interaction for centres with deg(j) <= 64 and the
+// model's basis sizes known at compile time (K = 6 radial, L = 7 angular).
+//
+// Same mathematics as triplet.cu (see the derivation there and DESIGN.md);
+// the work per centre is reorganised as small dense products so that the
+// inner loops are pure FFMA with register blocking:
+//
+//   forward   S[p, c]      = sum_{(q,l)} C[(q,l), p] * Q[(q,l), c]
+//             C[(q,l), p]  = T_l(x_pq) (0 on the diagonal)         -- Chebyshev table
+//             Q[(q,l), c]  = X[rq, c] * sum_k rbf_k(d_q) W[k, l, c]  -- gate table
+//   backward  (kernel bw1)  xbar(p, q) = sum_c Sbar[p, c] sum_l T_l'(x_pq) Q[(q,l), c]
+//             -> dE/dv_p, dE/dv_q (row / column passes over an XB tile)
+//             (kernel bw2)  Qbar[(q,l), c] = sum_p C[(q,l), p] Sbar[p, c]
+//             -> X_bar[rq], R_bar -> W_bar partials, dd_q partials
+//
+// Threads: 128 = 16 row groups x 8 channel groups; a thread owns rows
+// {rg, rg+16, rg+32, rg+48} (first TMR of them) and channels
+// {4cg..4cg+3, 32+4cg..32+4cg+3} of a 64-channel block, so every shared
+// load is a 128-bit vector that 8 (or 16) lanes share.
+#include <algorithm>
+
+#include "common.cuh"
+
+namespace egn {
+namespace fast {
+
+constexpr int kT = 128;
+constexpr int kN = 64;    // max centre degree on this path
+constexpr int kCB = 64;   // channels per block
+constexpr int kQC = 8;    // q rows per table chunk (forward / bw1)
+
+__device__ __forceinline__ int chan(int cg, int i) { return i < 4 ? cg * 4 + i : 32 + cg * 4 + (i - 4); }
+// permuted row slot: thread group rg reads rows rg, rg+16, rg+32, rg+48 as one float4
+__device__ __forceinline__ int rslot(int p) { return (p & 15) * 4 + (p >> 4); }
+
+__device__ __forceinline__ float rbf1(float d, int k, RbfParams rp) {
+  const float dd = d - rp.step * k;
+  return __expf(-rp.gamma * dd * dd);
+}
+
+template <int K>
+__device__ __forceinline__ void load_center(float4* Us, float* Rb, const float4* __restrict__ geo, int64_t off,
+                                            int n, RbfParams rp) {
+  for (int i = threadIdx.x; i < n; i += kT) Us[i] = geo[off + i];
+  for (int i = threadIdx.x; i < n * K; i += kT) {
+    const int q = i / K, k = i - q * K;
+    Rb[i] = rbf1(geo[off + q].w, k, rp);
+  }
+}
+
+// Q chunk: rows (t, l) for t < nq, natural channel order; thread (cq = tid & 63, half = tid >> 6)
+template <int K, int L>
+__device__ __forceinline__ void build_q(float* Qs, const float (&wreg)[K][L], const float* Rb,
+                                        const int32_t* __restrict__ rev, const float* __restrict__ X,
+                                        int64_t off, int q0, int nq, int dg, int c0) {
+  const int cq = threadIdx.x & 63, half = threadIdx.x >> 6;
+  const int c = c0 + cq;
+  // issue every gather of this chunk before any use (hides the L2/HBM latency once)
+  float xs[kQC / 2];
+#pragma unroll
+  for (int i = 0; i < kQC / 2; ++i) {
+    const int t = half + 2 * i;
+    xs[i] = (t < nq && c < dg) ? __ldg(X + static_cast<int64_t>(rev[off + q0 + t]) * dg + c) : 0.f;
+  }
+#pragma unroll
+  for (int i = 0; i < kQC / 2; ++i) {
+    const int t = half + 2 * i;
+    if (t >= nq) break;
+    const float xv = xs[i];
+    const float* rb = Rb + (q0 + t) * K;
+    float r[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) r[k] = rb[k];
+#pragma unroll
+    for (int l = 0; l < L; ++l) {
+      float s = 0.f;
+#pragma unroll
+      for (int k = 0; k < K; ++k) s = fmaf(r[k], wreg[k][l], s);
+      Qs[(t * L + l) * kCB + cq] = xv * s;
+    }
+  }
+}
+
+// Chebyshev chunk Ct[(t,l)][rslot(p)] = T_l(x_pq) or T_l'(x_pq), masked on p == q / p >= n.
+template <int L, bool DERIV>
+__device__ __forceinline__ void build_c(float* Ct, const float4* Us, int n, int rows, int q0, int nq) {
+  for (int i = threadIdx.x; i < nq * rows; i += kT) {
+    const int t = i / rows, p = i - t * rows;
+    const int q = q0 + t;
+    const bool ok = p < n && p != q;
+    float4 a = Us[q];
+    float4 b = ok ? Us[p] : a;
+    const float x = a.x * b.x + a.y * b.y + a.z * b.z;
+    const float m = ok ? 1.f : 0.f;
+    float* dst = Ct + t * L * kCB + rslot(p);
+    if (!DERIV) {
+      float tp = m * x, tc = m;
+#pragma unroll
+      for (int l = 0; l < L; ++l) {
+        dst[l * kCB] = tc;
+        const float tn = fmaf(2.f * x, tc, -tp);
+        tp = tc;
+        tc = tn;
+      }
+    } else {
+      // T_l'(x) = l U_{l-1}(x)
+      float um = 0.f, uc = 0.f;
+#pragma unroll
+      for (int l = 0; l < L; ++l) {
+        dst[l * kCB] = m * static_cast<float>(l) * uc;
+        const float un = (l == 0) ? 1.f : fmaf(2.f * x, uc, -um);
+        um = uc;
+        uc = un;
+      }
+    }
+  }
+}
+
+template <int TMR>
+__device__ __forceinline__ void micro(const float* __restrict__ A, const float* __restrict__ B, int nkk,
+                                      int rg, int cg, float (&acc)[4][8]) {
+#pragma unroll 4
+  for (int kk = 0; kk < nkk; ++kk) {
+    const float4 a = *reinterpret_cast<const float4*>(A + kk * kCB + rg * 4);
+    const float4 b0 = *reinterpret_cast<const float4*>(B + kk * kCB + cg * 4);
+    const float4 b1 = *reinterpret_cast<const float4*>(B + kk * kCB + 32 + cg * 4);
+    const float av[4] = {a.x, a.y, a.z, a.w};
+    const float bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+#pragma unroll
+    for (int r = 0; r < TMR; ++r)
+#pragma unroll
+      for (int i = 0; i < 8; ++i) acc[r][i] = fmaf(av[r], bv[i], acc[r][i]);
+  }
+}
+
+template <int K, int L>
+__device__ __forceinline__ void load_wreg(float (&wreg)[K][L], const float* __restrict__ W, int dg, int c) {
+#pragma unroll
+  for (int k = 0; k < K; ++k)
+#pragma unroll
+    for (int l = 0; l < L; ++l) wreg[k][l] = c < dg ? W[(k * L + l) * dg + c] : 0.f;
+}
+
+// ---------------------------------------------------------------------------
+template <int K, int L>
+__global__ void __launch_bounds__(kT, 4)
+fwd_kernel(const int64_t* __restrict__ edge_ptr, const int32_t* __restrict__ rev,
+           const float4* __restrict__ geo, int64_t nv, const float* __restrict__ X,
+           const float* __restrict__ W, int dg, RbfParams rp, float* __restrict__ S) {
+  __shared__ float4 Us[kN];
+  __shared__ float Rb[kN * K];
+  __shared__ __align__(16) float Ct[kQC * L * kCB];
+  __shared__ __align__(16) float Qs[kQC * L * kCB];
+  const int tid = threadIdx.x, cg = tid & 7, rg = tid >> 3;
+  for (int64_t j = blockIdx.x; j < nv; j += gridDim.x) {
+    const int64_t off = edge_ptr[j];
+    const int n = static_cast<int>(edge_ptr[j + 1] - off);
+    if (n == 0 || n > kN) continue;
+    const int tmr = (n + 15) >> 4;
+    const int rows = tmr * 16;
+    __syncthreads();
+    load_center<K>(Us, Rb, geo, off, n, rp);
+    for (int c0 = 0; c0 < dg; c0 += kCB) {
+      float wreg[K][L];
+      load_wreg<K, L>(wreg, W, dg, c0 + (tid & 63));
+      float acc[4][8];
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int i = 0; i < 8; ++i) acc[r][i] = 0.f;
+      for (int q0 = 0; q0 < n; q0 += kQC) {
+        const int nq = min(kQC, n - q0);
+        __syncthreads();
+        build_q<K, L>(Qs, wreg, Rb, rev, X, off, q0, nq, dg, c0);
+        build_c<L, false>(Ct, Us, n, rows, q0, nq);
+        __syncthreads();
+        const int nkk = nq * L;
+        switch (tmr) {
+          case 1: micro<1>(Ct, Qs, nkk, rg, cg, acc); break;
+          case 2: micro<2>(Ct, Qs, nkk, rg, cg, acc); break;
+          case 3: micro<3>(Ct, Qs, nkk, rg, cg, acc); break;
+          default: micro<4>(Ct, Qs, nkk, rg, cg, acc); break;
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const int p = rg + 16 * r;
+        if (r < tmr && p < n) {
+          float* dst = S + (off + p) * dg + c0;
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int c = chan(cg, i);
+            if (c0 + c < dg) dst[c] = acc[r][i];
+          }
+        }
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// bw1: xbar(p,q) -> dE/dv (rows p and columns q), edge_grad.xyz += F / d
+template <int K, int L>
+__global__ void __launch_bounds__(kT, 4)
+bw1_kernel(const int64_t* __restrict__ edge_ptr, const int32_t* __restrict__ rev,
+           const float4* __restrict__ geo, int64_t nv, const float* __restrict__ X,
+           const float* __restrict__ W, int dg, RbfParams rp, const float* __restrict__ Sbar,
+           float4* __restrict__ edge_grad) {
+  __shared__ float4 Us[kN];
+  __shared__ float Rb[kN * K];
+  __shared__ __align__(16) float Dt[kQC * L * kCB];  // T' chunk
+  __shared__ __align__(16) float Qs[kQC * L * kCB];
+  __shared__ float XB[kN * (kN + 1)];                // xbar(p, q), padded rows
+  const int tid = threadIdx.x, cg = tid & 7, rg = tid >> 3;
+  for (int64_t j = blockIdx.x; j < nv; j += gridDim.x) {
+    const int64_t off = edge_ptr[j];
+    const int n = static_cast<int>(edge_ptr[j + 1] - off);
+    if (n < 2 || n > kN) continue;
+    const int tmr = (n + 15) >> 4;
+    const int rows = tmr * 16;
+    __syncthreads();
+    load_center<K>(Us, Rb, geo, off, n, rp);
+    for (int i = tid; i < n * (kN + 1); i += kT) XB[i] = 0.f;
+    for (int c0 = 0; c0 < dg; c0 += kCB) {
+      float wreg[K][L];
+      load_wreg<K, L>(wreg, W, dg, c0 + (tid & 63));
+      float sb[4][8];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const int p = rg + 16 * r;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int c = c0 + chan(cg, i);
+          sb[r][i] = (r < tmr && p < n && c < dg) ? Sbar[(off + p) * dg + c] : 0.f;
+        }
+      }
+      for (int q0 = 0; q0 < n; q0 += kQC) {
+        const int nq = min(kQC, n - q0);
+        __syncthreads();
+        build_q<K, L>(Qs, wreg, Rb, rev, X, off, q0, nq, dg, c0);
+        build_c<L, true>(Dt, Us, n, rows, q0, nq);
+        __syncthreads();
+        for (int t = 0; t < nq; ++t) {
+          float acc[4][8];
+#pragma unroll
+          for (int r = 0; r < 4; ++r)
+#pragma unroll
+            for (int i = 0; i < 8; ++i) acc[r][i] = 0.f;
+          switch (tmr) {
+            case 1: micro<1>(Dt + t * L * kCB, Qs + t * L * kCB, L, rg, cg, acc); break;
+            case 2: micro<2>(Dt + t * L * kCB, Qs + t * L * kCB, L, rg, cg, acc); break;
+            case 3: micro<3>(Dt + t * L * kCB, Qs + t * L * kCB, L, rg, cg, acc); break;
+            default: micro<4>(Dt + t * L * kCB, Qs + t * L * kCB, L, rg, cg, acc); break;
+          }
+#pragma unroll
+          for (int r = 0; r < 4; ++r) {
+            if (r < tmr) {
+              float v = 0.f;
+#pragma unroll
+              for (int i = 0; i < 8; ++i) v = fmaf(sb[r][i], acc[r][i], v);
+              v += __shfl_xor_sync(0xffffffffu, v, 1);
+              v += __shfl_xor_sync(0xffffffffu, v, 2);
+              v += __shfl_xor_sync(0xffffffffu, v, 4);
+              const int p = rg + 16 * r;
+              if (cg == 0 && p < n) XB[p * (kN + 1) + q0 + t] += v;  // row owner, ordered over c0
+            }
+          }
+        }
+      }
+    }
+    __syncthreads();
+    // dE/dv_e for every out-edge e of the centre: rows then columns (fixed order)
+    for (int e = tid; e < n; e += kT) {
+      const float4 ue = Us[e];
+      float fx = 0.f, fy = 0.f, fz = 0.f;
+      for (int o = 0; o < n; ++o) {
+        if (o == e) continue;
+        const float4 uo = Us[o];
+        const float x = ue.x * uo.x + ue.y * uo.y + ue.z * uo.z;
+        const float v = XB[e * (kN + 1) + o] + XB[o * (kN + 1) + e];
+        fx = fmaf(v, uo.x - x * ue.x, fx);
+        fy = fmaf(v, uo.y - x * ue.y, fy);
+        fz = fmaf(v, uo.z - x * ue.z, fz);
+      }
+      const float inv = 1.f / ue.w;
+      float4 g = edge_grad[off + e];
+      g.x += fx * inv;
+      g.y += fy * inv;
+      g.z += fz * inv;
+      edge_grad[off + e] = g;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// bw2: Qbar = C^T Sbar per (centre, 64-channel block); X_bar, W_bar partials, dd partials.
+// grid = (centre CTAs, channel blocks).  Thread (rg, cg): q = q0 + rg, all L, 8 channels.
+template <int K, int L>
+__global__ void __launch_bounds__(kT, 3)
+bw2_kernel(const int64_t* __restrict__ edge_ptr, const int32_t* __restrict__ rev,
+           const float4* __restrict__ geo, int64_t nv, const float* __restrict__ X,
+           const float* __restrict__ W, int dg, RbfParams rp, const float* __restrict__ Sbar,
+           float* __restrict__ Xbar, float* __restrict__ wbar_part, float* __restrict__ dd_part,
+           int64_t num_edges) {
+  static_assert(L <= 8, "L <= 8");
+  extern __shared__ __align__(16) float dsm[];
+  float4* Us = reinterpret_cast<float4*>(dsm);      // [64]
+  float* Rb = dsm + 4 * kN;                          // [64 * K]
+  float* Cb = Rb + ((kN * K + 3) & ~3);              // [p][rg*8 + l]  (one q per row group)
+  float* Sb = Cb + kN * 16 * 8;                      // Sbar rows of the centre, this channel block
+  float* Wsm = Sb + kN * kCB;
+  float* Wb = Wsm + K * L * kCB;
+  float* Rst = Cb;                                   // R_bar staging [16][L][64] aliases Cb
+  const int tid = threadIdx.x, cg = tid & 7, rg = tid >> 3;
+  const int c0 = blockIdx.y * kCB;
+  for (int i = tid; i < K * L * kCB; i += kT) {
+    const int kl = i / kCB, c = i - kl * kCB;
+    Wsm[i] = c0 + c < dg ? W[kl * dg + c0 + c] : 0.f;
+    Wb[i] = 0.f;
+  }
+  for (int64_t j = blockIdx.x; j < nv; j += gridDim.x) {
+    const int64_t off = edge_ptr[j];
+    const int n = static_cast<int>(edge_ptr[j + 1] - off);
+    if (n > kN || n == 0) continue;
+    if (n == 1) {
+      const int64_t r0 = rev[off];
+      for (int c = tid; c < kCB; c += kT)
+        if (c0 + c < dg) Xbar[r0 * dg + c0 + c] = 0.f;
+      if (tid == 0) dd_part[blockIdx.y * num_edges + off] = 0.f;
+      continue;
+    }
+    __syncthreads();
+    load_center<K>(Us, Rb, geo, off, n, rp);
+    for (int i = tid; i < n * kCB; i += kT) {
+      const int p = i >> 6, c = i & 63;
+      Sb[i] = c0 + c < dg ? Sbar[(off + p) * dg + c0 + c] : 0.f;
+    }
+    for (int qb0 = 0; qb0 < n; qb0 += 16) {
+      __syncthreads();
+      // Cb[p][rg*8 + l] = T_l(x_{p, qb0+rg}) (masked)
+      for (int i = tid; i < n * 16; i += kT) {
+        const int p = i >> 4, g = i & 15;
+        const int q = qb0 + g;
+        const bool ok = q < n && p != q;
+        const float4 a = Us[p];
+        const float4 b = ok ? Us[q] : a;
+        const float x = a.x * b.x + a.y * b.y + a.z * b.z;
+        const float m = ok ? 1.f : 0.f;
+        float* dst = Cb + p * 128 + g * 8;
+        float tp = m * x, tc = m;
+#pragma unroll
+        for (int l = 0; l < 8; ++l) {
+          dst[l] = l < L ? tc : 0.f;
+          const float tn = fmaf(2.f * x, tc, -tp);
+          tp = tc;
+          tc = tn;
+        }
+      }
+      __syncthreads();
+      float qb[8][8];
+#pragma unroll
+      for (int l = 0; l < 8; ++l)
+#pragma unroll
+        for (int i = 0; i < 8; ++i) qb[l][i] = 0.f;
+#pragma unroll 2
+      for (int p = 0; p < n; ++p) {
+        const float4 a0 = *reinterpret_cast<const float4*>(Cb + p * 128 + rg * 8);
+        const float4 a1 = *reinterpret_cast<const float4*>(Cb + p * 128 + rg * 8 + 4);
+        const float4 b0 = *reinterpret_cast<const float4*>(Sb + p * kCB + cg * 4);
+        const float4 b1 = *reinterpret_cast<const float4*>(Sb + p * kCB + 32 + cg * 4);
+        const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+        const float bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+#pragma unroll
+        for (int l = 0; l < L; ++l)
+#pragma unroll
+          for (int i = 0; i < 8; ++i) qb[l][i] = fmaf(av[l], bv[i], qb[l][i]);
+      }
+      // epilogue for row q
+      const int q = qb0 + rg;
+      const bool valid = q < n;
+      const float4 uq = valid ? Us[q] : make_float4(0.f, 0.f, 0.f, 1.f);
+      const int64_t rq = valid ? static_cast<int64_t>(rev[off + q]) : 0;
+      float rbo[K], rdo[K];
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        rbo[k] = valid ? Rb[q * K + k] : 0.f;
+        rdo[k] = -2.f * rp.gamma * (uq.w - rp.step * k) * rbo[k];
+      }
+      float xo[8], xb[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int c = c0 + chan(cg, i);
+        xo[i] = (valid && c < dg) ? X[rq * dg + c] : 0.f;
+        xb[i] = 0.f;
+      }
+      float dd = 0.f;
+      __syncthreads();  // Cb reads done: Rst may overwrite it
+#pragma unroll
+      for (int l = 0; l < L; ++l) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int c = chan(cg, i);
+          float rw = 0.f, rwd = 0.f;
+#pragma unroll
+          for (int k = 0; k < K; ++k) {
+            const float w = Wsm[(k * L + l) * kCB + c];
+            rw = fmaf(rbo[k], w, rw);
+            rwd = fmaf(rdo[k], w, rwd);
+          }
+          xb[i] = fmaf(qb[l][i], rw, xb[i]);
+          const float rbar = qb[l][i] * xo[i];
+          dd = fmaf(rbar, rwd, dd);
+          Rst[(rg * L + l) * kCB + c] = rbar;  // zero for invalid rows (xo == 0)
+        }
+      }
+      dd += __shfl_xor_sync(0xffffffffu, dd, 1);
+      dd += __shfl_xor_sync(0xffffffffu, dd, 2);
+      dd += __shfl_xor_sync(0xffffffffu, dd, 4);
+      if (valid) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int c = c0 + chan(cg, i);
+          if (c < dg) Xbar[rq * dg + c] = xb[i];
+        }
+        if (cg == 0) dd_part[blockIdx.y * num_edges + off + q] = dd;
+      }
+      __syncthreads();
+      // W_bar[k,l,c] += sum_{rows} rbf_k(q) R_bar[q,l,c]; thread-owned (l, c) entries
+      const int nrow = min(16, n - qb0);
+      for (int idx = tid; idx < L * kCB; idx += kT) {
+        float s[K];
+#pragma unroll
+        for (int k = 0; k < K; ++k) s[k] = Wb[k * L * kCB + idx];
+        for (int r = 0; r < nrow; ++r) {
+          const float rv = Rst[r * L * kCB + idx];
+#pragma unroll
+          for (int k = 0; k < K; ++k) s[k] = fmaf(Rb[(qb0 + r) * K + k], rv, s[k]);
+        }
+#pragma unroll
+        for (int k = 0; k < K; ++k) Wb[k * L * kCB + idx] = s[k];
+      }
+    }
+  }
+  __syncthreads();
+  // partial layout [gridDim.y][gridDim.x][K*L*64]
+  float* dst = wbar_part + (static_cast<int64_t>(blockIdx.y) * gridDim.x + blockIdx.x) * (K * L * kCB);
+  for (int i = tid; i < K * L * kCB; i += kT) dst[i] = Wb[i];
+}
+
+// W_bar[k,l,c] = sum over x-CTAs of the partials of channel block c / 64
+__global__ void reduce_wbar_kernel(const float* __restrict__ part, int gx, int K, int L, int dg,
+                                   float* __restrict__ out) {
+  const int total = K * L * dg;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const int kl = i / dg, c = i - kl * dg;
+    const int cb = c / kCB, cc = c - cb * kCB;
+    const float* src = part + static_cast<int64_t>(cb) * gx * (K * L * kCB) + kl * kCB + cc;
+    float s = 0.f;
+    for (int x = 0; x < gx; ++x) s += src[static_cast<int64_t>(x) * (K * L * kCB)];
+    out[i] = s;
+  }
+}
+
+// edge_grad[e].w += sum over channel blocks of dd partials (only centres handled here, n <= 64)
+__global__ void add_dd_kernel(const int64_t* __restrict__ edge_ptr, int64_t nv, const float* __restrict__ dd_part,
+                              int ncb, int64_t ne, float4* __restrict__ edge_grad) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nv; v += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e0 = edge_ptr[v], e1 = edge_ptr[v + 1];
+    if (e1 - e0 < 2 || e1 - e0 > kN) continue;
+    for (int64_t e = e0; e < e1; ++e) {
+      float s = 0.f;
+      for (int b = 0; b < ncb; ++b) s += dd_part[b * ne + e];
+      edge_grad[e].w += s;
+    }
+  }
+}
+
+}  // namespace fast
+
+// ---------------------------------------------------------------------------
+// host side (called from triplet.cu's ABI functions)
+// ---------------------------------------------------------------------------
+bool fast_supported(int K, int L, int dg) { return K == 6 && L == 7 && dg >= 32; }
+
+int fast_fwd(const int64_t* edge_ptr, const int32_t* rev, const float4* geo, int64_t nv, const float* X,
+             const float* W, int K, int L, int dg, RbfParams rp, float* S, cudaStream_t st) {
+  auto kern = fast::fwd_kernel<6, 7>;
+  // one centre per CTA: no tail imbalance from static round-robin over unequal degrees
+  const int grid = static_cast<int>(std::min<int64_t>(nv, 1 << 30));
+  kern<<<grid, fast::kT, 0, st>>>(edge_ptr, rev, geo, nv, X, W, dg, rp, S);
+  return check_launch("triplet_fwd_fast");
+}
+
+int64_t fast_bwd_workspace_bytes(int64_t nv, int64_t ne, int K, int L, int dg) {
+  const int64_t ncb = (dg + fast::kCB - 1) / fast::kCB;
+  const int64_t gx = std::min<int64_t>(std::max<int64_t>(nv, 1), kNumSMs * 3);
+  return (ncb * gx * K * L * fast::kCB + ncb * std::max<int64_t>(ne, 1)) * 4;
+}
+
+int fast_bwd(const int64_t* edge_ptr, const int32_t* rev, const float4* geo, int64_t nv, int64_t ne,
+             const float* X, const float* W, int K, int L, int dg, RbfParams rp, const float* Sbar, float* Xbar,
+             float* Wbar, float4* edge_grad, void* ws, cudaStream_t st) {
+  const int ncb = (dg + fast::kCB - 1) / fast::kCB;
+  {
+    auto kern = fast::bw1_kernel<6, 7>;
+    const int grid = static_cast<int>(std::min<int64_t>(nv, 1 << 30));
+    kern<<<grid, fast::kT, 0, st>>>(edge_ptr, rev, geo, nv, X, W, dg, rp, Sbar, edge_grad);
+    if (check_launch("triplet_bw1_fast")) return 1;
+  }
+  const int gx = static_cast<int>(std::min<int64_t>(nv, static_cast<int64_t>(kNumSMs) * 3));
+  float* wpart = reinterpret_cast<float*>(ws);
+  float* ddpart = wpart + static_cast<int64_t>(ncb) * gx * K * L * fast::kCB;
+  const size_t smem = (4 * fast::kN + ((fast::kN * 6 + 3) & ~3) + fast::kN * 128 + fast::kN * fast::kCB +
+                       2 * 6 * 7 * fast::kCB) * sizeof(float);
+  auto k2 = fast::bw2_kernel<6, 7>;
+  cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  k2<<<dim3(gx, ncb), fast::kT, smem, st>>>(edge_ptr, rev, geo, nv, X, W, dg, rp, Sbar, Xbar, wpart, ddpart, ne);
+  if (check_launch("triplet_bw2_fast")) return 1;
+  fast::reduce_wbar_kernel<<<grid_for(static_cast<int64_t>(K) * L * dg, 256), 256, 0, st>>>(wpart, gx, K, L, dg,
+                                                                                          Wbar);
+  if (check_launch("triplet_bw2_reduce")) return 1;
+  fast::add_dd_kernel<<<grid_for(nv, 128), 128, 0, st>>>(edge_ptr, nv, ddpart, ncb, ne, edge_grad);
+  return check_launch("triplet_bw_dd");
+}
+
+}  // namespace egn

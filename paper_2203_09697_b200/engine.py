@@ -127,7 +127,7 @@ class Engine:
             down = m @ w[p + "tu.down"].t()
             X = down @ w[p + "tu.bilinear_a"].t() if gem else down
             Wk = self._sbf_weight(b)
-            S = ops.triplet_fwd(bg.edge_ptr, bg.rev, bg.geo, X, Wk, c.cutoff)
+            S = ops.triplet_fwd(bg.edge_ptr, bg.rev, bg.geo, X, Wk, c.cutoff, max_degree=bg.max_deg)
             g = rbf @ w[p + "tu.rbf_gate"].t()
             if gem:
                 Z = S @ w[p + "tu.bilinear_proj"].t()

@@ -8,6 +8,8 @@ tensors of the documented dtype; there is no CPU path.
 
 from __future__ import annotations
 
+import threading
+
 import torch
 
 from ._lib import call, ptr, stream
@@ -86,14 +88,14 @@ def sbf(geo, edge_ptr, tri_ptr, num_triplets, k_rbf, l_sbf, cutoff):
     return out
 
 
-def triplet_fwd(edge_ptr, rev, geo, X, Wk, cutoff):
+def triplet_fwd(edge_ptr, rev, geo, X, Wk, cutoff, max_degree=-1):
     """S = sum over the centre tile (see include/egn_b200.h egn_triplet_fwd)."""
     X = _c(X, torch.float32)
     Wk = _c(Wk, torch.float32)
     k, l, dg = Wk.shape
     S = torch.empty_like(X)
-    call("egn_triplet_fwd", ptr(edge_ptr), ptr(rev), ptr(geo), edge_ptr.shape[0] - 1, ptr(X), ptr(Wk),
-         k, l, dg, float(cutoff), ptr(S), stream())
+    call("egn_triplet_fwd", ptr(edge_ptr), ptr(rev), ptr(geo), edge_ptr.shape[0] - 1, int(max_degree), ptr(X),
+         ptr(Wk), k, l, dg, float(cutoff), ptr(S), stream())
     return S
 
 
@@ -101,7 +103,8 @@ _WS: dict = {}
 
 
 def _workspace(nbytes: int, device) -> torch.Tensor:
-    key = (str(device), "ws")
+    # per thread: in-process graph-parallel ranks (runtime.ThreadComm) share a stream
+    key = (str(device), "ws", threading.get_ident())
     buf = _WS.get(key)
     if buf is None or buf.numel() < nbytes:
         buf = torch.empty(max(nbytes, 1 << 20), dtype=torch.uint8, device=device)
@@ -121,11 +124,11 @@ def triplet_bwd(edge_ptr, rev, geo, X, Wk, cutoff, S_bar, edge_grad, X_bar=None,
         W_bar = torch.empty_like(Wk)
     if max_degree is None:
         max_degree = int((edge_ptr[1:] - edge_ptr[:-1]).max().item()) if nv else 0
-    nbytes = call("egn_triplet_bwd_workspace_bytes", nv, k, l, dg)
+    ne = X.shape[0]
+    nbytes = call("egn_triplet_bwd_workspace_bytes", nv, ne, k, l, dg)
     ws = _workspace(nbytes, X.device)
-    call("egn_triplet_bwd", ptr(edge_ptr), ptr(rev), ptr(geo), nv, int(max_degree), ptr(X), ptr(Wk), k, l, dg,
-         float(cutoff),
-         ptr(S_bar), ptr(X_bar), ptr(W_bar), ptr(edge_grad), ptr(ws), stream())
+    call("egn_triplet_bwd", ptr(edge_ptr), ptr(rev), ptr(geo), nv, ne, int(max_degree), ptr(X), ptr(Wk), k, l, dg,
+         float(cutoff), ptr(S_bar), ptr(X_bar), ptr(W_bar), ptr(edge_grad), ptr(ws), stream())
     return X_bar, W_bar
 
 
@@ -153,6 +156,14 @@ def gather_rows(idx, x, out=None, accumulate=False):
         out = torch.empty((rows, d), dtype=torch.float32, device=x.device)
     call("egn_gather_rows", ptr(idx), rows, ptr(x), x.stride(0), d, ptr(out), out.stride(0), int(accumulate),
          stream())
+    return out
+
+
+def scatter_rows(dst, src, x, out, accumulate=True):
+    """out[dst[r]] (+)= x[src[r]] (distinct dst)."""
+    rows = dst.shape[0]
+    call("egn_scatter_rows", ptr(dst), ptr(src), rows, ptr(x), x.stride(0), x.shape[1], ptr(out), out.stride(0),
+         int(accumulate), stream())
     return out
 
 
@@ -210,7 +221,7 @@ def column_sum(x, out=None):
 
 
 def _workspace_named(name: str, nbytes: int, device) -> torch.Tensor:
-    key = (str(device), name)
+    key = (str(device), name, threading.get_ident())
     buf = _WS.get(key)
     if buf is None or buf.numel() < nbytes:
         buf = torch.empty(max(nbytes, 1 << 16), dtype=torch.uint8, device=device)

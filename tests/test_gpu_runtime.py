@@ -1,0 +1,101 @@
+"""Graph-parallel runtime on one GPU: P in-process ranks vs the single-rank engine
+and vs the fp64 oracle (egn/runtime.py parallel == sequential, tests/test_runtime.py:115-175)."""
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import TOL, max_rel
+from oracle import egn_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def _case(variant, n=40, seed=3):
+    from paper_2203_09697_b200 import ModelConfig, init_params
+
+    cfg = ModelConfig(variant=variant, blocks=3, d_u=16, d_v=24, d_e=32, d_t=32, d_bil=32, k_rbf=6, l_sbf=7,
+                      cutoff=6.0, seed=seed)
+    pos, z = O.random_cloud(n, 0.06, np.random.default_rng(seed))
+    return cfg, init_params(cfg), pos, z
+
+
+@pytest.mark.parametrize("variant", ["dimenet-style", "gemnet-style"])
+@pytest.mark.parametrize("workers", [1, 2, 3, 4])
+def test_parallel_matches_oracle(variant, workers):
+    from paper_2203_09697_b200 import ModelParams
+    from paper_2203_09697_b200.runtime import WorkerGroup
+
+    cfg, params, pos, z = _case(variant)
+    run = ModelParams(cfg.replace(workers=workers), params.arrays)
+    rng = np.random.default_rng(5)
+    df = rng.standard_normal((pos.shape[0], 3)) if variant == "gemnet-style" else None
+    res, bundle = WorkerGroup(pos, run).forward_backward(d_energy=0.8, d_forces=df)
+    oc = O.Config(**{k: getattr(cfg, k) for k in O.Config.__dataclass_fields__})
+    fw = O.forward(oc, params.arrays, pos, z)
+    G, dpos = O.backward(fw, params.arrays, 0.8, df)
+    assert abs(res.energy - fw.energy) <= TOL * max(1.0, abs(fw.energy))
+    if variant == "gemnet-style":
+        assert max_rel(res.forces, fw.forces) < TOL
+    assert max_rel(bundle.d_positions, dpos) < TOL
+    for k, g in G.items():
+        assert max_rel(bundle.d_params[k], g) < TOL, k
+
+
+@pytest.mark.parametrize("variant", ["dimenet-style", "gemnet-style"])
+def test_parallel_equals_single_rank_engine(variant):
+    """P = 1, 2, 4 agree with each other to fp32 summation-order noise."""
+    from paper_2203_09697_b200 import ModelParams
+    from paper_2203_09697_b200.runtime import WorkerGroup
+
+    cfg, params, pos, _ = _case(variant, n=60, seed=7)
+    outs = {}
+    for p in (1, 2, 4):
+        run = ModelParams(cfg.replace(workers=p), params.arrays)
+        outs[p] = WorkerGroup(pos, run).forward_backward(d_energy=1.0)
+    r1, b1 = outs[1]
+    for p in (2, 4):
+        rp, bp = outs[p]
+        assert abs(rp.energy - r1.energy) <= 1e-5 * max(1.0, abs(r1.energy))
+        assert max_rel(bp.d_positions, b1.d_positions) < 1e-5
+        for k in b1.d_params:
+            assert max_rel(bp.d_params[k], b1.d_params[k]) < 1e-5, k
+
+
+@pytest.mark.parametrize("variant", ["dimenet-style", "gemnet-style"])
+def test_comm_volume_independent_of_triplets(variant):
+    """Forward exchange per block: N_e d_e + G d_v (+ N_e d_e + N_v d_v for gemnet); no triplet level."""
+    from paper_2203_09697_b200 import ModelParams
+    from paper_2203_09697_b200.runtime import WorkerGroup
+
+    cfg, params, pos, _ = _case(variant)
+    for d_t in (16, 48):
+        c2 = cfg.replace(workers=3, d_t=d_t)
+        from paper_2203_09697_b200 import init_params
+
+        wg = WorkerGroup(pos, init_params(c2))
+        res = wg.forward()
+        ne, nv = wg.bg.num_edges, wg.bg.num_nodes
+        expect = ne * c2.d_e + c2.d_v
+        if variant == "gemnet-style":
+            expect += ne * c2.d_e + nv * c2.d_v
+        assert res.comm_log.forward_blocks() == {b: expect for b in range(c2.blocks)}
+        assert "triplet" not in res.comm_log.levels()
+
+
+def test_fault_injection_and_errors():
+    from paper_2203_09697_b200 import ModelParams
+    from paper_2203_09697_b200.runtime import WorkerGroup
+
+    cfg, params, pos, _ = _case("dimenet-style")
+    good = WorkerGroup(pos, ModelParams(cfg.replace(workers=2), params.arrays)).forward()
+    bad = WorkerGroup(pos, ModelParams(cfg.replace(workers=2), params.arrays), fault="drop-last")
+    # a dropped contribution is either detected as diverged replicas or yields a different energy
+    try:
+        res = bad.forward()
+        assert abs(res.energy - good.energy) > 1e-6
+    except Exception as exc:  # noqa: BLE001
+        assert "WorkerGroupError" in type(exc).__name__
+    with pytest.raises(ValueError):
+        WorkerGroup(pos, ModelParams(cfg.replace(workers=2), params.arrays)).forward_backward(
+            d_forces=np.zeros((pos.shape[0], 3)))

@@ -103,7 +103,7 @@ def test_native_library_loads_and_exports_all_symbols():
     assert lib.egn_abi_version() == 1
     assert isinstance(lib.egn_last_error(), bytes)
     # pure host entry point: workspace sizing
-    assert lib.egn_triplet_bwd_workspace_bytes(1000, 6, 7, 64) > 0
+    assert lib.egn_triplet_bwd_workspace_bytes(1000, 20000, 6, 7, 64) > 0
 
 
 def test_product_path_does_not_import_oracle():
