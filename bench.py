@@ -3,20 +3,28 @@
 triplet-interactions/s and train steps/s, GemNet-T / DimeNet++).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload NAME]
+    torchrun --nproc-per-node N --master-addr 127.0.0.1 bench.py --gpus N ...
 
 One step = one SGD training step (forward + backward + update) over one
 synthetic batch.  Default workload = BASELINE configs[1]: GemNet-T default
 dims (emb 128, triplet emb 64, bilinear 64, 4 blocks), 32 graphs x 80 atoms
-at OC20-like density (random_cloud rho=0.06, cutoff 6 A, <=50 neighbours),
-loss w_E = w_F = 1 against a teacher model (init_params(seed=1)).
+per GPU at OC20-like density (random_cloud rho=0.06, cutoff 6 A, <=50
+neighbours), loss w_E = w_F = 1 against a teacher model (init_params(seed=1)).
+
+N > 1 (weak scaling, 32 graphs per GPU): graph parallelism over the global
+batch (runtime.GraphParallelEngine, NCCL).  ``--partition aligned`` (default)
+splits the centre range at graph boundaries, so edge/node exchanges are empty
+and only the per-graph GU sums, the loss, the position and the parameter
+gradients are all-reduced; ``--partition balanced`` splits by triplet count
+inside graphs (full edge/node all-gathers every block).
 
 Prints ONE JSON line (rank 0).  ``value`` = triplet-interactions/s of the
-whole job = N_t(batch) * blocks / t_step, device-timed with inputs resident;
-``e2e`` = the same metric through the public API with host buffers (H2D of
-positions + targets, graph build, step, D2H of the loss) inside the timed
-region.  ``--impl reference`` times the CPU reference path (the fp64 numpy
-oracle, a restatement of egn.ModelTape; see oracle/egn_oracle.py) on the
-host cores for a bounded sample of the same workload.
+whole job = N_t(global batch) * blocks / t_step, device-timed (CUDA events,
+max over ranks) with inputs resident; ``e2e`` = the same metric with host
+buffers: H2D of positions + targets, graph build, step, D2H of the loss
+inside the timed region.  ``--impl reference`` times the CPU reference path
+(the fp64 numpy oracle, a restatement of egn.ModelTape; oracle/egn_oracle.py)
+on the host cores for a bounded sample of the same workload.
 """
 
 from __future__ import annotations
@@ -53,8 +61,10 @@ def _args():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="gemnet-t-oc20")
     ap.add_argument("--graphs", type=int, default=None, help="override graphs per GPU")
+    ap.add_argument("--partition", choices=["aligned", "balanced"], default="aligned")
     ap.add_argument("--cpu-budget", type=float, default=12.0, help="seconds of CPU oracle sampling")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-kernel-timing", action="store_true")
     return ap.parse_args()
 
 
@@ -135,7 +145,7 @@ def cpu_reference(wl, systems, budget_s, min_graphs=1):
     oc = O.Config(**{k: getattr(cfg, k) for k in O.Config.__dataclass_fields__})
     params = O.init_params(oc)
     trip, secs, done = 0, 0.0, 0
-    for i, s in enumerate(systems):
+    for s in systems:
         g = O.build_graph(s.positions, oc.cutoff)  # graph build excluded (egn/bench.py:294-296)
         t0 = time.perf_counter()
         fw = O.forward(oc, params, s.positions, s.atomic_numbers, graph=g)
@@ -146,8 +156,7 @@ def cpu_reference(wl, systems, budget_s, min_graphs=1):
         done += 1
         if done >= min_graphs and secs >= budget_s:
             break
-    return {"triplets_per_s": trip / secs, "graphs": done, "seconds": secs,
-            "sec_per_graph": secs / done}
+    return {"triplets_per_s": trip / secs, "graphs": done, "seconds": secs, "sec_per_graph": secs / done}
 
 
 def run_reference(args, wl):
@@ -157,27 +166,27 @@ def run_reference(args, wl):
     graphs = args.graphs or wl["graphs"]
     systems = _systems(wl, graphs)
     cores = os.cpu_count()
-    # each step = one graph of the batch, forward + backward (bounded sample)
     for i in range(args.warmup):
         cpu_reference(wl, [systems[i % graphs]], 0.0)
     trip, secs = 0.0, 0.0
-    for i in range(args.steps):
+    for i in range(args.steps):  # each step = one graph of the batch, forward + backward (bounded sample)
         r = cpu_reference(wl, [systems[(args.warmup + i) % graphs]], 0.0)
         trip += r["triplets_per_s"] * r["seconds"]
         secs += r["seconds"]
     value = trip / secs
     ms_graph = 1000 * secs / args.steps
     line = {
-        "impl": "reference", "metric": "triplet-interactions/s (train step, fwd+bwd)", "value": value,
+        "impl": "reference", "metric": "triplet-interactions/s (train step, fwd+bwd+SGD)", "value": value,
         "unit": "triplets/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": ms_graph * graphs, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "f64", "data": "synthetic",
-        "config": {"workload": args.workload, "variant": wl["variant"], "graphs": graphs, "atoms": wl["atoms"],
-                   "cutoff": wl["cutoff"], "sample": "one graph of the batch per step"},
+        "ms_per_step": ms_graph * graphs * args.gpus, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": args.workload, "variant": wl["variant"], "graphs_per_gpu": graphs,
+                   "atoms_per_graph": wl["atoms"], "cutoff": wl["cutoff"],
+                   "sample": "one graph of the batch per step (fwd+bwd), host cores"},
         "cpu_baseline": {"value": value, "unit": "triplets/s", "cores": cores, "kind": "port",
-                         "sample": f"{args.steps} graphs x fwd+bwd of the {graphs}-graph batch"},
+                         "sample": f"{args.steps} graphs x fwd+bwd of the {graphs}-graph batch, fp64 numpy oracle"},
         "e2e": {"value": value, "unit": "triplets/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "steps_per_s": 1.0 / (ms_graph * graphs / 1000.0),
+        "steps_per_s": 1000.0 / (ms_graph * graphs * args.gpus),
     }
     print(json.dumps(line), flush=True)
 
@@ -200,52 +209,104 @@ def _time_kernel(fn, iters, flush):
     return float(np.median(times))
 
 
+def _kernel_roofline(tr, bg, cfg):
+    """Triplet-interaction kernels on block-0 operands, L2 flushed between launches."""
+    import torch
+
+    from paper_2203_09697_b200 import ops
+
+    eng = tr.engine
+    fw = eng.forward(bg)
+    st0 = fw.blocks[0]
+    dg = cfg.triplet_width
+    S_bar = torch.randn_like(st0["S"])
+    eg = torch.zeros((bg.num_edges, 4), device="cuda")
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")  # 256 MB > L2
+    X, Wk = st0["X"], st0["Wk"]
+    t_f = _time_kernel(lambda: ops.triplet_fwd(bg.edge_ptr, bg.rev, bg.geo, X, Wk, cfg.cutoff, bg.max_deg), 20,
+                       flush)
+    t_b = _time_kernel(lambda: ops.triplet_bwd(bg.edge_ptr, bg.rev, bg.geo, X, Wk, cfg.cutoff, S_bar, eg,
+                                               max_degree=bg.max_deg), 20, flush)
+    ne, nt = bg.num_edges, bg.num_triplets
+    b_fwd = 12 * nt + (8 * dg + 4) * ne  # SURVEY.md 8(d) algorithmic bytes
+    b_bwd = 16 * nt + (12 * dg + 8) * ne
+    peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
+    hbm = peaks.get("hbm_gbs", 6650.0)
+    fma = 2.0 * nt * cfg.l_sbf * dg
+    dominant = "triplet_bwd" if t_b >= t_f else "triplet_fwd"
+    ach = (b_bwd / t_b if dominant == "triplet_bwd" else b_fwd / t_f) / 1e9
+    return {"bound": "hbm", "kernel": dominant, "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
+            "traffic": None, "peak_source": "MEASURED_PEAKS.json" if peaks else "fallback",
+            "triplet_fwd_us": t_f * 1e6, "triplet_bwd_us": t_b * 1e6,
+            "triplet_fwd_gtrip_s": nt / t_f / 1e9, "triplet_bwd_gtrip_s": nt / t_b / 1e9,
+            "triplet_fwd_fp32_tflops": fma / t_f / 1e12, "triplet_bwd_fp32_tflops": 2 * fma / t_b / 1e12,
+            "algorithmic_bytes": {"fwd": b_fwd, "bwd": b_bwd}}
+
+
 def run_ours(args, wl):
     import torch
     import torch.distributed as dist
 
-    from paper_2203_09697_b200 import _lib, init_params, ops
+    from paper_2203_09697_b200 import _lib, init_params
     from paper_2203_09697_b200.engine import DeviceWeights, Engine
     from paper_2203_09697_b200.graph import build_batch
+    from paper_2203_09697_b200.partition import partition_centers
+    from paper_2203_09697_b200.runtime import DistComm, GPTrainer
     from paper_2203_09697_b200.tasks import Trainer
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
+    backend = os.environ.get("EGN_DIST_BACKEND", "nccl")  # gloo: single-GPU smoke test of the N>1 path
+    ndev = torch.cuda.device_count()
+    torch.cuda.set_device(local % ndev)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     cfg = _config(wl)
     graphs = args.graphs or wl["graphs"]
-    systems = _systems(wl, graphs, rank)
+    # weak scaling: every rank contributes `graphs` graphs to the global batch
+    systems = [s for r in range(world) for s in _systems(wl, graphs, r)]
     params = init_params(cfg)
-    teacher = Engine(DeviceWeights.from_params(init_params(cfg.replace(seed=1))))
     bg = build_batch(systems, cfg.cutoff)
+    teacher = Engine(DeviceWeights.from_params(init_params(cfg.replace(seed=1))))
     tf = teacher.forward(bg)
-    e_t = tf.energy.double()
-    if wl["w_forces"]:
-        f_t = tf.forces.double()
-    else:
-        f_t = None
+    e_t = tf.energy.double().cpu().numpy()
+    f_t = tf.forces.double().cpu().numpy() if wl["w_forces"] else None
     del tf, teacher
-    tr = Trainer(params, None, e_t.cpu().numpy(), None if f_t is None else f_t.cpu().numpy(),
-                 1.0, wl["w_forces"], graph=bg)
-    lr = 1e-5
+    if world == 1:
+        tr = Trainer(params, None, e_t, f_t, 1.0, wl["w_forces"], graph=bg)
+        comm = None
+        parallelism = "single"
+    else:
+        comm = DistComm()
+        cand = bg.graph_ptr.cpu().numpy() if args.partition == "aligned" else None
+        part = partition_centers(bg.deg.cpu().numpy(), world, candidates=cand)
+        tr = GPTrainer(params, bg, e_t, f_t, 1.0, wl["w_forces"], comm, part)
+        parallelism = f"gp{world} ({args.partition} centre partition, {backend})"
 
     def barrier():
         if world > 1:
             dist.barrier()
 
+    # SGD step size from the first gradient (keeps the synthetic run finite); lr=0 step is outside timing
+    loss0 = float(tr.step(0.0))
+    gnorm = float(tr.weights.grad_flat.norm())
+    lr = 1e-2 / max(gnorm, 1.0)
     for _ in range(args.warmup):
         tr.step(lr)
     torch.cuda.synchronize()
     barrier()
-    clocks = ClockSampler(torch.cuda.current_device())
-    clocks.start()
-    time.sleep(0.3)
+    clocks = ClockSampler(torch.cuda.current_device()) if rank == 0 else None
+    if clocks:
+        clocks.start()
+        time.sleep(0.3)
     _lib.LAUNCH_COUNTER.update(calls=0, kernels=0)
     st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
+    barrier()
     st.record()
     for _ in range(args.steps):
         loss = tr.step(lr)
@@ -253,10 +314,11 @@ def run_ours(args, wl):
     torch.cuda.synchronize()
     t_dev = st.elapsed_time(en) / 1000.0 / args.steps
     launches = _lib.LAUNCH_COUNTER["kernels"] // args.steps
+    loss_last = float(loss)
     # ---- end to end: host buffers -> device -> step -> loss back to host
     pos_host = torch.from_numpy(np.concatenate([s.positions for s in systems])).pin_memory()
-    et_host = e_t.cpu().pin_memory()
-    ft_host = f_t.cpu().pin_memory() if f_t is not None else None
+    et_host = torch.from_numpy(e_t).pin_memory()
+    ft_host = torch.from_numpy(f_t).pin_memory() if f_t is not None else None
     h2d = pos_host.numel() * 8 + et_host.numel() * 8 + (ft_host.numel() * 8 if ft_host is not None else 0)
     sizes = [s.positions.shape[0] for s in systems]
 
@@ -265,7 +327,12 @@ def run_ours(args, wl):
         et = et_host.to("cuda", non_blocking=True)
         ft = ft_host.to("cuda", non_blocking=True) if ft_host is not None else None
         g = build_batch(None, cfg.cutoff, positions=pos, sizes=sizes)
-        tr.set_inputs(g, et, ft)
+        if world == 1:
+            tr.set_inputs(g, et, ft)
+        else:
+            n0, n1 = tr.engine.n0, tr.engine.n1
+            tr.bg, tr.e_target = g, et
+            tr.f_target = ft[n0:n1] if ft is not None else None
         return float(tr.step(lr))
 
     for _ in range(2):
@@ -276,46 +343,25 @@ def run_ours(args, wl):
     for _ in range(args.steps):
         e2e_step()
     t_e2e = (time.perf_counter() - t0) / args.steps
-    clk = clocks.stop()
+    clk = clocks.stop() if clocks else None
 
-    # max over ranks
     tt = torch.tensor([t_dev, t_e2e], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
     t_dev, t_e2e = float(tt[0]), float(tt[1])
-    trip_rank = bg.num_triplets * cfg.blocks
-    total_trip = trip_rank * world
+    total_trip = bg.num_triplets * cfg.blocks  # global batch (all ranks)
     value = total_trip / t_dev
-
-    # ---- roofline of the triplet-interaction kernels (block 0 operands)
-    fw = tr.engine.forward(bg)
-    st0 = fw.blocks[0]
-    dg = cfg.triplet_width
-    S_bar = torch.randn_like(st0["S"])
-    eg = torch.zeros((bg.num_edges, 4), device="cuda")
-    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")  # 256 MB > L2
-    t_f = _time_kernel(lambda: ops.triplet_fwd(bg.edge_ptr, bg.rev, bg.geo, st0["X"], st0["Wk"], cfg.cutoff),
-                       20, flush)
-    t_b = _time_kernel(lambda: ops.triplet_bwd(bg.edge_ptr, bg.rev, bg.geo, st0["X"], st0["Wk"], cfg.cutoff,
-                                               S_bar, eg), 20, flush)
-    ne, nt = bg.num_edges, bg.num_triplets
-    b_fwd = 12 * nt + (8 * dg + 4) * ne
-    b_bwd = 16 * nt + (12 * dg + 8) * ne
-    peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
-    hbm = peaks.get("hbm_gbs", 6650.0)
-    fma_flops_fwd = 2.0 * nt * cfg.l_sbf * dg
-    dominant = "triplet_bwd" if t_b >= t_f else "triplet_fwd"
-    ach = (b_bwd / t_b if dominant == "triplet_bwd" else b_fwd / t_f) / 1e9
-    roof = {"bound": "hbm", "kernel": dominant, "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
-            "traffic": None, "peak_source": "MEASURED_PEAKS.json" if peaks else "fallback",
-            "triplet_fwd_us": t_f * 1e6, "triplet_bwd_us": t_b * 1e6,
-            "triplet_fwd_gtrip_s": nt / t_f / 1e9, "triplet_bwd_gtrip_s": nt / t_b / 1e9,
-            "triplet_fwd_fp32_tflops": fma_flops_fwd / t_f / 1e12,
-            "algorithmic_bytes": {"fwd": b_fwd, "bwd": b_bwd}}
-
+    roof = None
+    if rank == 0 and not args.no_kernel_timing:
+        rb = bg if world == 1 else build_batch(systems[:graphs], cfg.cutoff)
+        if world > 1:
+            rtr = Trainer(params, None, e_t[:graphs], None, 1.0, 0.0, graph=rb)
+        else:
+            rtr = tr
+        roof = _kernel_roofline(rtr, rb, cfg)
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
-        r = cpu_reference(wl, systems, args.cpu_budget)
+        r = cpu_reference(wl, systems[:graphs], args.cpu_budget)
         cpu = {"value": r["triplets_per_s"], "unit": "triplets/s", "cores": os.cpu_count(), "kind": "port",
                "sample": f"{r['graphs']} graph(s) of the batch, fwd+bwd, fp64 numpy oracle, {r['seconds']:.1f}s"}
     if rank == 0:
@@ -326,8 +372,8 @@ def run_ours(args, wl):
             "data": "synthetic (random_cloud OC20-density graphs, random-init weights, teacher targets)",
             "config": {"workload": args.workload, "variant": wl["variant"], "graphs_per_gpu": graphs,
                        "atoms_per_graph": wl["atoms"], "cutoff": wl["cutoff"], "blocks": cfg.blocks,
-                       "d_e": cfg.d_e, "d_t": cfg.d_t, "d_bil": cfg.d_bil, "edges_per_gpu": bg.num_edges,
-                       "triplets_per_gpu": nt, "parallelism": f"replicas{world}" if world > 1 else "single",
+                       "d_e": cfg.d_e, "d_t": cfg.d_t, "d_bil": cfg.d_bil, "edges_total": bg.num_edges,
+                       "triplets_total": bg.num_triplets, "parallelism": parallelism,
                        "l2": "step working set > L2 (126 MB); kernel timings flush L2 with a 256 MB write"},
             "steps_per_s": 1.0 / t_dev,
             "e2e": {"value": total_trip / t_e2e, "unit": "triplets/s", "h2d_bytes_per_step": h2d,
@@ -336,10 +382,11 @@ def run_ours(args, wl):
             "roofline": roof,
             "cpu_baseline": cpu,
             "clocks": clk,
-            "loss": float(loss),
+            "loss": {"first": loss0, "last": loss_last, "lr": lr},
         }
         print(json.dumps(line), flush=True)
     if world > 1:
+        dist.barrier()
         dist.destroy_process_group()
 
 

@@ -68,12 +68,15 @@ class CenterPartition:
                 int(self.trip_bounds[r]), int(self.trip_bounds[r + 1]))
 
 
-def partition_centers(deg: np.ndarray, workers: int, weight: str = "triplets") -> CenterPartition:
+def partition_centers(deg: np.ndarray, workers: int, weight: str = "triplets",
+                      candidates: np.ndarray | None = None) -> CenterPartition:
     """Split centre atoms into contiguous ranges balancing sum deg(deg-1) (+ edges).
 
     The cost of a centre is its triplet count plus its out-edge count (the
     per-edge dense work), so edge-heavy but triplet-light graphs still
-    balance."""
+    balance.  ``candidates`` (e.g. the graph offsets of a batch) restricts the
+    split points; a partition aligned to graph boundaries has no cross-rank
+    edges, so its edge/node exchanges are empty."""
     if workers < 1:
         raise ValueError("workers must be >= 1")
     deg = np.asarray(deg, dtype=np.int64)
@@ -86,9 +89,13 @@ def partition_centers(deg: np.ndarray, workers: int, weight: str = "triplets") -
     cum = np.concatenate([[0], np.cumsum(cost)])
     total = cum[-1]
     bounds = np.zeros(workers + 1, dtype=np.int64)
+    cand = None if candidates is None else np.unique(np.asarray(candidates, dtype=np.int64))
     for r in range(1, workers):
         target = total * r / workers
-        bounds[r] = int(np.searchsorted(cum, target, side="left"))
+        if cand is None:
+            bounds[r] = int(np.searchsorted(cum, target, side="left"))
+        else:
+            bounds[r] = int(cand[np.argmin(np.abs(cum[cand] - target))])
         bounds[r] = max(bounds[r], bounds[r - 1])
     bounds[workers] = n
     bounds = np.minimum(bounds, n)

@@ -290,13 +290,30 @@ class ThreadComm(Comm):
 # graph-parallel engine (one rank)
 # ---------------------------------------------------------------------------
 class GraphParallelEngine:
-    """Forward/backward of one rank's centre shard; P = 1 reproduces Engine."""
+    """Forward/backward of one rank's centre shard; P = 1 reproduces Engine.
+
+    When no edge crosses a rank boundary (a partition aligned to graph
+    boundaries of a batch: the "halo" is empty) the edge/node exchanges are
+    skipped and the redundant all-row products are restricted to the owned
+    rows; only the per-graph GU sums, the loss and the gradients are reduced
+    (graph parallelism degenerates to data parallelism over whole graphs)."""
 
     def __init__(self, weights: DeviceWeights, comm: Comm, part: CenterPartition):
         self.weights, self.comm, self.part = weights, comm, part
         self.config = weights.config
         r = comm.rank
         self.n0, self.n1, self.e0, self.e1, self.t0, self.t1 = part.rank(r)
+        self._halo = {}
+
+    def halo_free(self, bg: BatchGraph) -> bool:
+        key = id(bg)
+        if key not in self._halo:
+            rv = bg.rev[self.e0:self.e1]
+            local = bool(((rv >= self.e0) & (rv < self.e1)).all()) if self.e1 > self.e0 else True
+            flag = torch.tensor([0.0 if local else 1.0], device=bg.device)
+            self.comm.all_reduce_(flag, phase="setup", block=-1, stage="halo", level="global")
+            self._halo = {key: bool(flag.item() == 0.0)}
+        return self._halo[key]
 
     def _slices(self, bg: BatchGraph):
         n0, n1 = self.n0, self.n1
@@ -317,17 +334,26 @@ class GraphParallelEngine:
         gem = c.variant == GEMNET
         e0, e1, n0, n1 = self.e0, self.e1, self.n0, self.n1
         eb, nb = self.part.edge_bounds, self.part.node_bounds
+        hf = self.halo_free(bg)
+        lo, hi = (e0, e1) if hf else (0, bg.num_edges)  # rows of the redundant products
         ep_own, gp_own = self._slices(bg)
-        E, V = bg.num_edges, bg.num_nodes
+        E, V, dev = bg.num_edges, bg.num_nodes, bg.device
         rbf = ops.rbf(bg.geo, c.k_rbf, c.cutoff)
-        m = torch.addmm(w["edge_init.b"], rbf, w["edge_init.w"].t())  # all rows (redundant)
-        u = torch.zeros((bg.num_graphs, c.d_u), dtype=torch.float32, device=bg.device)
+        m = torch.zeros((E, c.d_e), dtype=torch.float32, device=dev)
+        torch.addmm(w["edge_init.b"], rbf[lo:hi], w["edge_init.w"].t(), out=m[lo:hi])
+        u = torch.zeros((bg.num_graphs, c.d_u), dtype=torch.float32, device=dev)
         blocks, v_own = [], None
+        dg = c.triplet_width
         for b in range(c.blocks):
             p = f"block{b}."
             st = {"m": m}
-            down = m @ w[p + "tu.down"].t()
-            X = down @ w[p + "tu.bilinear_a"].t() if gem else down
+            down = torch.zeros((E, c.d_t), dtype=torch.float32, device=dev)
+            torch.mm(m[lo:hi], w[p + "tu.down"].t(), out=down[lo:hi])
+            if gem:
+                X = torch.zeros((E, dg), dtype=torch.float32, device=dev)
+                torch.mm(down[lo:hi], w[p + "tu.bilinear_a"].t(), out=X[lo:hi])
+            else:
+                X = down
             Wk = self._sbf_weight(b)
             S = torch.zeros_like(X)
             if n1 > n0:
@@ -345,10 +371,11 @@ class GraphParallelEngine:
             xcat = torch.cat([m_o, ta], dim=1)
             h = torch.addmm(w[p + "eu.b1"], xcat, w[p + "eu.w1"].t())
             a1 = F.silu(h)
-            m_new = torch.empty((E, c.d_e), dtype=torch.float32, device=bg.device)
+            m_new = torch.zeros((E, c.d_e), dtype=torch.float32, device=dev)
             torch.addmm(w[p + "eu.b2"], a1, w[p + "eu.w2"].t(), out=m_new[e0:e1])
             m_new[e0:e1] += m_o
-            cm.all_gather_rows(m_new, eb, phase="forward", block=b, stage="m_new", level="edge")
+            if not hf:
+                cm.all_gather_rows(m_new, eb, phase="forward", block=b, stage="m_new", level="edge")
             agg = ops.aggregate_in_edges(ep_own, bg.rev, m_new)
             hv = torch.addmm(w[p + "nu.b1"], agg, w[p + "nu.w1"].t())
             av = F.silu(hv)
@@ -356,24 +383,28 @@ class GraphParallelEngine:
             st.update(down=down, X=X, Wk=Wk, S=S, g=g, Y=Y, xcat=xcat, h=h, a1=a1, m_new=m_new, agg=agg, hv=hv,
                       av=av, v_own=v_own)
             if gem:
-                v_full = torch.empty((V, c.d_v), dtype=torch.float32, device=bg.device)
+                v_full = torch.zeros((V, c.d_v), dtype=torch.float32, device=dev)
                 v_full[n0:n1] = v_own
-                cm.all_gather_rows(v_full, nb, phase="forward", block=b, stage="v", level="node")
+                if not hf:
+                    cm.all_gather_rows(v_full, nb, phase="forward", block=b, stage="v", level="node")
                 w1 = w[p + "eu2.w1"]
                 pv = v_full @ w1[:, c.d_e:].t()
                 h2 = torch.addmm(w[p + "eu2.b1"], m_new[e0:e1], w1[:, :c.d_e].t())
                 ops.gather_rows(bg.recv[e0:e1], pv, out=h2, accumulate=True)
                 a2 = F.silu(h2)
-                m2 = torch.empty((E, c.d_e), dtype=torch.float32, device=bg.device)
+                m2 = torch.zeros((E, c.d_e), dtype=torch.float32, device=dev)
                 torch.addmm(w[p + "eu2.b2"], a2, w[p + "eu2.w2"].t(), out=m2[e0:e1])
                 m2[e0:e1] += m_new[e0:e1]
-                cm.all_gather_rows(m2, eb, phase="forward", block=b, stage="m2", level="edge")
-                m2r = ops.gather_rows(bg.rev, m2)
-                m = torch.addmm(m2, m2r, w[p + "sym.w"].t())  # all rows (redundant)
+                if not hf:
+                    cm.all_gather_rows(m2, eb, phase="forward", block=b, stage="m2", level="edge")
+                m2r = torch.zeros_like(m2)
+                ops.gather_rows(bg.rev[lo:hi], m2, out=m2r[lo:hi])
+                m = torch.zeros_like(m2)
+                torch.addmm(m2[lo:hi], m2r[lo:hi], w[p + "sym.w"].t(), out=m[lo:hi])
                 st.update(v_full=v_full, h2=h2, a2=a2, m2r=m2r)
             else:
                 m = m_new
-            s = ops.graph_sum(gp_own, v_own) if n1 > n0 else torch.zeros((bg.num_graphs, c.d_v), device=bg.device)
+            s = ops.graph_sum(gp_own, v_own) if n1 > n0 else torch.zeros((bg.num_graphs, c.d_v), device=dev)
             cm.all_reduce_(s, phase="forward", block=b, stage="gu", level="global")
             pre = torch.addmm(w[p + "gu.b1"], s, w[p + "gu.w1"].t())
             act = F.silu(pre)
@@ -394,25 +425,26 @@ class GraphParallelEngine:
         de = c.d_e
         e0, e1, n0, n1 = self.e0, self.e1, self.n0, self.n1
         eb, nb = self.part.edge_bounds, self.part.node_bounds
+        hf = self.halo_free(bg)
+        lo, hi = (e0, e1) if hf else (0, bg.num_edges)
         ep_own, gp_own = self._slices(bg)
-        E, V = bg.num_edges, bg.num_nodes
+        E, V, dev = bg.num_edges, bg.num_nodes, bg.device
         lead = cm.rank == 0
         wg, cs = ops.wgrad, ops.column_sum
         self.weights.grad_flat.zero_()
-        eg = torch.zeros((E, 4), dtype=torch.float32, device=bg.device)
+        eg = torch.zeros((E, 4), dtype=torch.float32, device=dev)
         dE = d_energy.to(torch.float32).view(-1, 1)
         if lead:
             torch.mm(dE.t(), fw.u, out=gr["energy_head.w"])
             gr["energy_head.b"].copy_(dE.sum(0))
         u_bar = dE @ w["energy_head.w"]
-        m_bar = torch.zeros((E, de), dtype=torch.float32, device=bg.device)  # partial adjoint, all rows
+        m_bar = torch.zeros((E, de), dtype=torch.float32, device=dev)  # partial adjoint
         if gem and d_forces_own is not None:
-            f_bar = torch.zeros((V, 3), dtype=torch.float32, device=bg.device)
+            f_bar = torch.zeros((V, 3), dtype=torch.float32, device=dev)
             f_bar[n0:n1] = d_forces_own.to(torch.float32)
             ops.force_head_bwd(bg.recv, bg.geo, fw.m, w["force_head.w"].view(-1), fw.scale, f_bar, m_bar, eg,
                                w_bar=gr["force_head.w"].view(-1))
         rbf_bar = torch.zeros_like(fw.rbf)
-        own_e = torch.arange(e0, e1, dtype=torch.int32, device=bg.device)
         for b in range(c.blocks - 1, -1, -1):
             p = f"block{b}."
             st = fw.blocks[b]
@@ -426,25 +458,35 @@ class GraphParallelEngine:
             s_bar = pre_bar @ w[p + "gu.w1"]
             v_bar = ops.gather_rows(bg.node_graph[n0:n1], s_bar)
             if gem:
-                wg(m_bar, st["m2r"], out=gr[p + "sym.w"])
-                t = m_bar @ w[p + "sym.w"]
-                m2_bar = ops.gather_rows(bg.rev, t, out=m_bar.clone(), accumulate=True)
-                m2_bar_o = cm.reduce_scatter_rows(m2_bar, eb, phase="backward", block=b, stage="m2", level="edge")
+                # sym (rows lo:hi) and its adjoint
+                wg(m_bar[lo:hi], st["m2r"][lo:hi], out=gr[p + "sym.w"])
+                t = m_bar[lo:hi] @ w[p + "sym.w"]
+                m2_bar = m_bar.clone()
+                ops.scatter_rows(bg.rev[lo:hi], torch.arange(hi - lo, dtype=torch.int32, device=dev), t, m2_bar)
+                if hf:
+                    m2_bar_o = m2_bar[e0:e1]
+                else:
+                    m2_bar_o = cm.reduce_scatter_rows(m2_bar, eb, phase="backward", block=b, stage="m2",
+                                                      level="edge")
                 wg(m2_bar_o, st["a2"], out=gr[p + "eu2.w2"])
                 cs(m2_bar_o, out=gr[p + "eu2.b2"])
                 h2_bar = _silu_bwd(m2_bar_o @ w[p + "eu2.w2"], st["h2"])
                 cs(h2_bar, out=gr[p + "eu2.b1"])
                 w1 = w[p + "eu2.w1"]
-                m_new_o = st["m_new"][e0:e1]
-                gr[p + "eu2.w1"][:, :de].copy_(wg(h2_bar, m_new_o))
-                h2_full = torch.zeros((E, de), dtype=torch.float32, device=bg.device)
+                gr[p + "eu2.w1"][:, :de].copy_(wg(h2_bar, st["m_new"][e0:e1]))
+                h2_full = torch.zeros((E, de), dtype=torch.float32, device=dev)
                 h2_full[e0:e1] = h2_bar
-                pv_bar = ops.aggregate_in_edges(bg.edge_ptr, bg.rev, h2_full)  # [V, d_e], partial
-                gr[p + "eu2.w1"][:, de:].copy_(pv_bar.t() @ st["v_full"])
-                v_bar_full = pv_bar @ w1[:, de:]
-                v_bar_o = cm.reduce_scatter_rows(v_bar_full, nb, phase="backward", block=b, stage="v", level="node")
-                v_bar = v_bar + v_bar_o
-                mnb = torch.zeros((E, de), dtype=torch.float32, device=bg.device)
+                if hf:
+                    pv_bar = ops.aggregate_in_edges(ep_own, bg.rev, h2_full)  # own nodes, complete
+                    gr[p + "eu2.w1"][:, de:].copy_(pv_bar.t() @ st["v_own"])
+                    v_bar = v_bar + pv_bar @ w1[:, de:]
+                else:
+                    pv_bar = ops.aggregate_in_edges(bg.edge_ptr, bg.rev, h2_full)  # all nodes, partial
+                    gr[p + "eu2.w1"][:, de:].copy_(pv_bar.t() @ st["v_full"])
+                    v_bar_full = pv_bar @ w1[:, de:]
+                    v_bar = v_bar + cm.reduce_scatter_rows(v_bar_full, nb, phase="backward", block=b, stage="v",
+                                                           level="node")
+                mnb = torch.zeros((E, de), dtype=torch.float32, device=dev)
                 torch.addmm(m2_bar_o, h2_bar, w1[:, :de], out=mnb[e0:e1])
             else:
                 mnb = m_bar
@@ -459,7 +501,10 @@ class GraphParallelEngine:
             if e1 > e0:
                 src_local = (bg.src[e0:e1] - n0).to(torch.int32)
                 ops.scatter_rows(bg.rev[e0:e1], src_local, agg_bar, mnb, accumulate=True)
-            m_new_bar = cm.reduce_scatter_rows(mnb, eb, phase="backward", block=b, stage="m_new", level="edge")
+            if hf:
+                m_new_bar = mnb[e0:e1]
+            else:
+                m_new_bar = cm.reduce_scatter_rows(mnb, eb, phase="backward", block=b, stage="m_new", level="edge")
             # EU (own edges)
             wg(m_new_bar, st["a1"], out=gr[p + "eu.w2"])
             cs(m_new_bar, out=gr[p + "eu.b2"])
@@ -490,21 +535,23 @@ class GraphParallelEngine:
                 ops.triplet_bwd(ep_own, bg.rev, bg.geo, st["X"], st["Wk"], c.cutoff, S_bar, eg, X_bar=X_bar,
                                 W_bar=Wk_bar, max_degree=bg.max_deg)
             wp_bar = Wk_bar.permute(2, 0, 1).reshape(Wk_bar.shape[2], -1)
+            Xb = X_bar[lo:hi]
             if gem:
                 torch.mm(wp_bar, w[p + "tu.sbf_gate"].t(), out=gr[p + "tu.bilinear_b"])
                 torch.mm(w[p + "tu.bilinear_b"].t(), wp_bar, out=gr[p + "tu.sbf_gate"])
-                wg(X_bar, st["down"], out=gr[p + "tu.bilinear_a"])
-                down_bar = X_bar @ w[p + "tu.bilinear_a"]
+                wg(Xb, st["down"][lo:hi], out=gr[p + "tu.bilinear_a"])
+                down_bar = Xb @ w[p + "tu.bilinear_a"]
             else:
                 gr[p + "tu.sbf_gate"].copy_(wp_bar)
-                down_bar = X_bar
-            wg(down_bar, st["m"], out=gr[p + "tu.down"])
-            m_bar = down_bar @ w[p + "tu.down"]  # partial, rows rev(own)
+                down_bar = Xb
+            wg(down_bar, st["m"][lo:hi], out=gr[p + "tu.down"])
+            m_bar = torch.zeros((E, de), dtype=torch.float32, device=dev)
+            torch.mm(down_bar, w[p + "tu.down"], out=m_bar[lo:hi])  # partial, rows rev(own)
             m_bar[e0:e1] += m_in_o
-        # edge init (all rows, redundant forward; partial adjoint)
-        wg(m_bar, fw.rbf, out=gr["edge_init.w"])
-        cs(m_bar, out=gr["edge_init.b"])
-        rbf_bar.addmm_(m_bar, w["edge_init.w"])
+        # edge init (rows lo:hi; partial adjoint)
+        wg(m_bar[lo:hi], fw.rbf[lo:hi], out=gr["edge_init.w"])
+        cs(m_bar[lo:hi], out=gr["edge_init.b"])
+        rbf_bar[lo:hi].addmm_(m_bar[lo:hi], w["edge_init.w"])
         ops.rbf_bwd(bg.geo, rbf_bar, c.cutoff, eg)
         pos_bar = ops.positions_bwd(bg.edge_ptr, bg.rev, bg.geo, eg)
         cm.all_reduce_(pos_bar, phase="backward", block=-1, stage="positions", level="position")
@@ -520,6 +567,46 @@ def _triplet_fwd_into(ep_own, bg, X, Wk, cutoff, S):
     call("egn_triplet_fwd", ptr(ep_own), ptr(bg.rev), ptr(bg.geo), ep_own.shape[0] - 1, int(bg.max_deg),
          ptr(X.contiguous()), ptr(Wk), k, l, dg, float(cutoff), ptr(S), stream())
     return S
+
+
+class GPTrainer:
+    """Graph-parallel SGD step for one rank over a replicated BatchGraph
+    (tasks.loss_and_grads semantics, egn/tasks.py:131-185): energies are
+    replicated, force residuals and seeds are rank-local for the owned atoms,
+    the loss value is all-reduced for reporting."""
+
+    def __init__(self, params, bg: BatchGraph, e_target, f_target, w_energy: float, w_forces: float, comm: Comm,
+                 part: CenterPartition, device="cuda"):
+        self.config = params.config
+        self.bg, self.comm, self.part = bg, comm, part
+        self.weights = DeviceWeights.from_params(params, device)
+        self.engine = GraphParallelEngine(self.weights, comm, part)
+        self.n = bg.num_graphs
+        self.e_target = torch.as_tensor(np.asarray(e_target), dtype=torch.float64, device=bg.device)
+        n0, n1 = self.engine.n0, self.engine.n1
+        self.f_target = (torch.as_tensor(np.asarray(f_target), dtype=torch.float64, device=bg.device)[n0:n1]
+                         if f_target is not None else None)
+        sizes = torch.as_tensor(bg.graph_sizes, dtype=torch.float64, device=bg.device)
+        self.atom_count = sizes.repeat_interleave(torch.as_tensor(bg.graph_sizes, device=bg.device))[n0:n1]
+        self.w_energy, self.w_forces = float(w_energy), float(w_forces)
+
+    def step(self, lr: float) -> torch.Tensor:
+        fw = self.engine.forward(self.bg)
+        res = fw.energy.double() - self.e_target
+        loss = torch.zeros(1, dtype=torch.float64, device=self.bg.device)
+        if self.comm.rank == 0:
+            loss += (self.w_energy * res * res).sum() / self.n
+        d_e = 2.0 * self.w_energy * res / self.n
+        d_f = None
+        if self.w_forces != 0.0:
+            delta = fw.forces.double() - self.f_target
+            loss += self.w_forces * ((delta * delta).sum(dim=1) / self.atom_count).sum() / self.n
+            d_f = 2.0 * self.w_forces * delta / (self.n * self.atom_count[:, None])
+        self.engine.backward(self.bg, fw, d_e, d_f)
+        self.comm.all_reduce_(loss, phase="backward", block=-1, stage="loss", level="global")
+        if lr != 0.0:
+            self.weights.sgd_(lr)
+        return loss
 
 
 # ---------------------------------------------------------------------------
@@ -547,7 +634,8 @@ class WorkerGroup:
     forward_backward(d_energy, d_forces) -> (ParallelRunResult, GradientBundle);
     worker failures surface as WorkerGroupError(stage, rank)."""
 
-    def __init__(self, system, params, timeout: float = 60.0, fault: str | None = None, device="cuda"):
+    def __init__(self, system, params, timeout: float = 60.0, fault: str | None = None, device="cuda",
+                 align_graphs: bool = False):
         from .graph import build_batch
 
         self.params = params
@@ -555,7 +643,8 @@ class WorkerGroup:
         self.workers = self.config.workers
         self.timeout, self.fault, self.device = timeout, fault, device
         self.bg = build_batch(system, self.config.cutoff, device)
-        self.partition = partition_centers(self.bg.deg.cpu().numpy(), self.workers)
+        cand = self.bg.graph_ptr.cpu().numpy() if align_graphs else None
+        self.partition = partition_centers(self.bg.deg.cpu().numpy(), self.workers, candidates=cand)
 
     def forward(self) -> ParallelRunResult:
         res, _ = self._run(False, 0.0, None)
@@ -593,7 +682,9 @@ class WorkerGroup:
                         df = None
                         if d_forces is not None:
                             df = torch.as_tensor(np.asarray(d_forces), device=dev)[eng.n0:eng.n1]
-                        pos_bar = eng.backward(self.bg, fw, torch.tensor([d_energy], device=dev), df)
+                        de = torch.as_tensor(np.broadcast_to(np.asarray(d_energy, dtype=np.float64),
+                                                             (self.bg.num_graphs,)).copy(), device=dev)
+                        pos_bar = eng.backward(self.bg, fw, de, df)
                         bundle = (eng.weights.to_numpy(grads=True), pos_bar.cpu().numpy())
                     outs[rank] = (fw, eng, bundle)
             except BaseException as exc:  # noqa: BLE001 - reported to the caller
@@ -616,13 +707,14 @@ class WorkerGroup:
         if primary is not None:
             raise WorkerGroupError(stages[primary[0]], primary[0], primary[1]) from primary[1]
         fw0 = outs[0][0]
-        energies = {float(o[0].energy[0]) for o in outs}
+        energies = {tuple(o[0].energy.tolist()) for o in outs}
         if len(energies) != 1:
             raise WorkerGroupError("finalize", 0, AssertionError("worker outputs diverged"))
         forces = None
         if self.config.variant == GEMNET:
             forces = np.concatenate([o[0].forces.double().cpu().numpy() for o in outs], axis=0)
-        result = ParallelRunResult(float(fw0.energy[0]), forces, log, self.partition)
+        energy = float(fw0.energy[0]) if fw0.energy.numel() == 1 else fw0.energy.double().cpu().numpy()
+        result = ParallelRunResult(energy, forces, log, self.partition)
         bundle = None
         if backward:
             grads, pos = outs[0][2]

@@ -83,6 +83,33 @@ def test_comm_volume_independent_of_triplets(variant):
         assert "triplet" not in res.comm_log.levels()
 
 
+@pytest.mark.parametrize("variant", ["dimenet-style", "gemnet-style"])
+def test_graph_aligned_partition_is_halo_free_and_exact(variant):
+    """A batch split at graph boundaries needs no edge/node exchange; results equal the
+    single-rank engine over the same batch."""
+    from paper_2203_09697_b200 import ModelParams
+    from paper_2203_09697_b200.engine import DeviceWeights, Engine
+    from paper_2203_09697_b200.runtime import WorkerGroup
+
+    cfg, params, _, _ = _case(variant)
+    rng = np.random.default_rng(21)
+    systems = [O.random_cloud(n, 0.06, rng)[0] for n in (30, 41, 25, 37)]
+    wg = WorkerGroup(systems, ModelParams(cfg.replace(workers=2), params.arrays), align_graphs=True)
+    de = np.array([0.5, -1.0, 0.25, 2.0])
+    df = rng.standard_normal((sum(s.shape[0] for s in systems), 3)) if variant == "gemnet-style" else None
+    res, bundle = wg.forward_backward(d_energy=de, d_forces=df)
+    assert {r.level for r in res.comm_log.records} <= {"global", "position", "param"}
+    eng = Engine(DeviceWeights.from_params(params))
+    fw = eng.forward(wg.bg)
+    pos = eng.backward(wg.bg, fw, torch.tensor(de, device="cuda"),
+                       torch.tensor(df, device="cuda") if df is not None else None).cpu().numpy()
+    g = eng.weights.to_numpy(grads=True)
+    assert max_rel(res.energy, fw.energy.double().cpu().numpy()) < 1e-5
+    assert max_rel(bundle.d_positions, pos) < 1e-5
+    for k in g:
+        assert max_rel(bundle.d_params[k], g[k]) < 1e-5, k
+
+
 def test_fault_injection_and_errors():
     from paper_2203_09697_b200 import ModelParams
     from paper_2203_09697_b200.runtime import WorkerGroup
