@@ -195,6 +195,24 @@ int egn_column_sum(const float* x, int64_t rows, int d, int64_t ld, float* out, 
                    egn_stream_t stream);
 
 /* ------------------------------------------------------------------ */
+/* Dense layers: linear (tape.py:104-119) on tcgen05 tensor cores      */
+/* ------------------------------------------------------------------ */
+/* out[M, N] = sum over nseg (1 or 2) segments of A_s[M, K_s] B_s[N, K_s]^T, fp32-accurate
+ * (3 x TF32 split on tcgen05.mma kind::tf32, TMEM accumulator), then the fused epilogue
+ * selected by flags (applied in this order):
+ *   1  += bias[n]            2  += resid[m*ldr + n]     4  += gsrc[gidx[m]*ldg + n]
+ *   32 *= silu'(aux[m*ldaux + n])
+ *   16 out2 = value; value *= aux[m*ldaux + n]
+ *   8  out2 = silu(value) after storing value to out.
+ * A/B are row-major with K contiguous (B = weights stored (out, in)); K_s % 4 == 0,
+ * N % 16 == 0, pointers 16-byte aligned, row strides multiples of 4 elements. */
+int egn_gemm(int64_t M, int N, int nseg, const float* a0, int64_t lda0, const float* b0, int64_t ldb0,
+             int k0, const float* a1, int64_t lda1, const float* b1, int64_t ldb1, int k1,
+             const float* bias, const float* resid, int64_t ldr, const float* gsrc,
+             const int32_t* gidx, int64_t ldg, const float* aux, int64_t ldaux, int flags,
+             float* out, int64_t ldo, float* out2, int64_t ldo2, egn_stream_t stream);
+
+/* ------------------------------------------------------------------ */
 /* Optimizer: train_simple SGD update (tasks.py:207-208)               */
 /* ------------------------------------------------------------------ */
 int egn_sgd(float* w, const float* g, int64_t n, float lr, egn_stream_t stream);

@@ -52,6 +52,8 @@ SIGNATURES: dict[str, tuple] = {
     "egn_positions_bwd": (_i32, [_p, _p, _p, _i64, _p, _p, _p]),
     "egn_column_sum_workspace_bytes": (_i64, [_i64, _i32]),
     "egn_column_sum": (_i32, [_p, _i64, _i32, _i64, _p, _p, _p]),
+    "egn_gemm": (_i32, [_i64, _i32, _i32, _p, _i64, _p, _i64, _i32, _p, _i64, _p, _i64, _i32, _p, _p, _i64, _p,
+                        _p, _i64, _p, _i64, _i32, _p, _i64, _p, _i64, _p]),
     "egn_sgd": (_i32, [_p, _p, _i64, _f32, _p]),
 }
 

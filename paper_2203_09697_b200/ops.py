@@ -251,5 +251,45 @@ def wgrad(g: torch.Tensor, x: torch.Tensor, out: torch.Tensor | None = None, spl
     return res
 
 
+EPI_BIAS, EPI_RESID, EPI_GATHER, EPI_SILU_OUT2, EPI_MUL_AUX, EPI_DSILU_AUX = 1, 2, 4, 8, 16, 32
+
+
+def _rowmajor(t):
+    return t if t.stride(1) == 1 else t.contiguous()
+
+
+def gemm(a, b, a2=None, b2=None, bias=None, resid=None, gather=None, aux=None, flags=0, out=None, out2=None):
+    """out = a b^T (+ a2 b2^T) with the fused epilogue of egn_gemm (tcgen05, 3xTF32).
+
+    a: [M, K] rows, b: [N, K] (weights stored (out, in)); gather = (src [*, N], idx int32 [M])."""
+    a, b = _rowmajor(a), _rowmajor(b)
+    M, K = a.shape
+    N = b.shape[0]
+    nseg = 1 if a2 is None else 2
+    if nseg == 2:
+        a2, b2 = _rowmajor(a2), _rowmajor(b2)
+    if out is None:
+        out = torch.empty((M, N), dtype=torch.float32, device=a.device)
+    if bias is not None:
+        flags |= EPI_BIAS
+    if resid is not None:
+        flags |= EPI_RESID
+    gsrc = gidx = None
+    if gather is not None:
+        gsrc, gidx = gather
+        flags |= EPI_GATHER
+    need2 = flags & (EPI_SILU_OUT2 | EPI_MUL_AUX)
+    if need2 and out2 is None:
+        out2 = torch.empty((M, N), dtype=torch.float32, device=a.device)
+    call("egn_gemm", M, N, nseg, ptr(a), a.stride(0), ptr(b), b.stride(0), K,
+         ptr(a2) if nseg == 2 else None, a2.stride(0) if nseg == 2 else 0,
+         ptr(b2) if nseg == 2 else None, b2.stride(0) if nseg == 2 else 0, a2.shape[1] if nseg == 2 else 0,
+         ptr(bias), ptr(resid), resid.stride(0) if resid is not None else 0,
+         ptr(gsrc), ptr(gidx), gsrc.stride(0) if gsrc is not None else 0,
+         ptr(aux), aux.stride(0) if aux is not None else 0, int(flags),
+         ptr(out), out.stride(0), ptr(out2), out2.stride(0) if out2 is not None else 0, stream())
+    return (out, out2) if need2 else out
+
+
 def sgd_(w, g, lr):
     call("egn_sgd", ptr(w), ptr(g), w.numel(), float(lr), stream())

@@ -1,0 +1,76 @@
+"""tcgen05 3xTF32 GEMM with fused epilogues vs a float64 torch reference.
+
+The dense layers of the model (linear, egn/tape.py:104-119) must be fp32-accurate:
+tolerance 2e-6 relative to max|ref| (plain TF32 would be ~1e-3)."""
+
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+TOL = 2e-6
+
+
+def _rel(a, b):
+    return float((a.double() - b).abs().max() / max(b.abs().max().item(), 1e-30))
+
+
+@pytest.mark.parametrize("M,N,K", [(128, 64, 32), (1000, 64, 128), (4097, 128, 256), (300, 256, 64),
+                                   (77, 384, 96), (2560, 16, 128), (58644, 128, 128)])
+def test_plain_gemm(M, N, K):
+    from paper_2203_09697_b200 import ops
+
+    g = torch.Generator(device="cuda").manual_seed(M + N + K)
+    a = torch.randn((M, K), device="cuda", generator=g)
+    b = torch.randn((N, K), device="cuda", generator=g) / K ** 0.5
+    out = ops.gemm(a, b)
+    ref = a.double() @ b.double().t()
+    assert _rel(out, ref) < TOL
+
+
+def test_two_segments_and_epilogues():
+    from paper_2203_09697_b200 import ops
+
+    g = torch.Generator(device="cuda").manual_seed(0)
+    M, N, K0, K1 = 3000, 128, 128, 128
+    a0 = torch.randn((M, K0), device="cuda", generator=g)
+    a1 = torch.randn((M, K1), device="cuda", generator=g)
+    w = torch.randn((N, K0 + K1), device="cuda", generator=g) / 16
+    bias = torch.randn(N, device="cuda", generator=g)
+    resid = torch.randn((M, N), device="cuda", generator=g)
+    # concat-free linear with bias and SiLU side output: h = [a0, a1] W^T + b, a = silu(h)
+    h, act = ops.gemm(a0, w[:, :K0], a2=a1, b2=w[:, K0:], bias=bias, flags=ops.EPI_SILU_OUT2)
+    ref = torch.cat([a0, a1], 1).double() @ w.double().t() + bias.double()
+    assert _rel(h, ref) < TOL
+    assert _rel(act, torch.nn.functional.silu(ref)) < 1e-5
+    # residual
+    out = ops.gemm(a0, w[:, :K0], bias=bias, resid=resid)
+    assert _rel(out, a0.double() @ w[:, :K0].double().t() + bias.double() + resid.double()) < TOL
+    # gathered-row add
+    src = torch.randn((500, N), device="cuda", generator=g)
+    idx = torch.randint(0, 500, (M,), device="cuda", generator=g, dtype=torch.int32)
+    out = ops.gemm(a0, w[:, :K0], gather=(src, idx))
+    assert _rel(out, a0.double() @ w[:, :K0].double().t() + src.double()[idx.long()]) < TOL
+    # gate multiply with pre-gate side output
+    aux = torch.randn((M, N), device="cuda", generator=g)
+    y, z = ops.gemm(a0, w[:, :K0], aux=aux, flags=ops.EPI_MUL_AUX)
+    zr = a0.double() @ w[:, :K0].double().t()
+    assert _rel(z, zr) < TOL and _rel(y, zr * aux.double()) < TOL
+    # SiLU backward
+    out = ops.gemm(a0, w[:, :K0], aux=aux, flags=ops.EPI_DSILU_AUX)
+    s = torch.sigmoid(aux.double())
+    assert _rel(out, zr * s * (1 + aux.double() * (1 - s))) < 1e-5
+
+
+def test_strided_operands_and_errors():
+    from paper_2203_09697_b200 import ops
+
+    g = torch.Generator(device="cuda").manual_seed(1)
+    big = torch.randn((1000, 256), device="cuda", generator=g)
+    w = torch.randn((64, 256), device="cuda", generator=g)
+    out = ops.gemm(big[:, 128:], w[:, 128:])  # row stride 256, K = 128
+    assert _rel(out, big[:, 128:].double() @ w[:, 128:].double().t()) < TOL
+    with pytest.raises(ValueError):
+        ops.gemm(torch.randn((10, 6), device="cuda"), torch.randn((16, 6), device="cuda"))  # K % 4
+    with pytest.raises(ValueError):
+        ops.gemm(torch.randn((10, 8), device="cuda"), torch.randn((12, 8), device="cuda"))  # N % 16
