@@ -204,13 +204,20 @@ int egn_column_sum(const float* x, int64_t rows, int d, int64_t ld, float* out, 
  *   32 *= silu'(aux[m*ldaux + n])
  *   16 out2 = value; value *= aux[m*ldaux + n]
  *   8  out2 = silu(value) after storing value to out.
- * A/B are row-major with K contiguous (B = weights stored (out, in)); K_s % 4 == 0,
- * N % 16 == 0, pointers 16-byte aligned, row strides multiples of 4 elements. */
+ * A is row-major with K contiguous; B is row-major [N, K] (weights stored (out, in)) or,
+ * with b_mn != 0, [K, N] with N contiguous (the weight of a data-gradient product);
+ * K_s % 4 == 0, N % 16 == 0, pointers 16-byte aligned, row strides multiples of 4. */
 int egn_gemm(int64_t M, int N, int nseg, const float* a0, int64_t lda0, const float* b0, int64_t ldb0,
              int k0, const float* a1, int64_t lda1, const float* b1, int64_t ldb1, int k1,
              const float* bias, const float* resid, int64_t ldr, const float* gsrc,
              const int32_t* gidx, int64_t ldg, const float* aux, int64_t ldaux, int flags,
-             float* out, int64_t ldo, float* out2, int64_t ldo2, egn_stream_t stream);
+             float* out, int64_t ldo, float* out2, int64_t ldo2, int b_mn, egn_stream_t stream);
+
+/* Weight gradient out[M, N] (+)= g^T x with g [krows, M], x [krows, N] (both MN-major on the
+ * tensor cores), split over krows across CTAs; partial tiles reduced in a fixed order. */
+int64_t egn_gemm_wgrad_workspace_bytes(int64_t krows, int M, int N);
+int egn_gemm_wgrad(int64_t krows, int M, int N, const float* g, int64_t ldg, const float* x,
+                   int64_t ldx, float* out, int accumulate, void* workspace, egn_stream_t stream);
 
 /* ------------------------------------------------------------------ */
 /* Optimizer: train_simple SGD update (tasks.py:207-208)               */

@@ -53,7 +53,9 @@ SIGNATURES: dict[str, tuple] = {
     "egn_column_sum_workspace_bytes": (_i64, [_i64, _i32]),
     "egn_column_sum": (_i32, [_p, _i64, _i32, _i64, _p, _p, _p]),
     "egn_gemm": (_i32, [_i64, _i32, _i32, _p, _i64, _p, _i64, _i32, _p, _i64, _p, _i64, _i32, _p, _p, _i64, _p,
-                        _p, _i64, _p, _i64, _i32, _p, _i64, _p, _i64, _p]),
+                        _p, _i64, _p, _i64, _i32, _p, _i64, _p, _i64, _i32, _p]),
+    "egn_gemm_wgrad_workspace_bytes": (_i64, [_i64, _i32, _i32]),
+    "egn_gemm_wgrad": (_i32, [_i64, _i32, _i32, _p, _i64, _p, _i64, _p, _i32, _p, _p]),
     "egn_sgd": (_i32, [_p, _p, _i64, _f32, _p]),
 }
 
@@ -97,7 +99,7 @@ def stream() -> int:
 
 # Kernels launched per successful ABI call (for the bench's gpu_launches count).
 KERNELS_PER_CALL = {
-    "egn_triplet_bwd": 4, "egn_force_head_fwd": 2, "egn_force_head_bwd": 2, "egn_column_sum": 2,
+    "egn_triplet_bwd": 4, "egn_force_head_fwd": 2, "egn_force_head_bwd": 2, "egn_column_sum": 2, "egn_gemm_wgrad": 2,
 }
 LAUNCH_COUNTER = {"calls": 0, "kernels": 0}
 

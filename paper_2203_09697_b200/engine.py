@@ -116,50 +116,48 @@ class Engine:
     def forward(self, bg: BatchGraph) -> ForwardResult:
         c, w = self.config, self.weights.w
         gem = c.variant == GEMNET
+        de = c.d_e
+        L = ops.linear
         rbf = ops.rbf(bg.geo, c.k_rbf, c.cutoff)
-        m = torch.addmm(w["edge_init.b"], rbf, w["edge_init.w"].t())
+        m = torch.addmm(w["edge_init.b"], rbf, w["edge_init.w"].t())  # K = k_rbf (6): cuBLAS
         u = torch.zeros((bg.num_graphs, c.d_u), dtype=torch.float32, device=bg.device)
         v = None
         blocks = []
         for b in range(c.blocks):
             p = f"block{b}."
-            st = {}
-            down = m @ w[p + "tu.down"].t()
-            X = down @ w[p + "tu.bilinear_a"].t() if gem else down
+            st = {"m": m}
+            down = L(m, w[p + "tu.down"])
+            X = L(down, w[p + "tu.bilinear_a"]) if gem else down
             Wk = self._sbf_weight(b)
             S = ops.triplet_fwd(bg.edge_ptr, bg.rev, bg.geo, X, Wk, c.cutoff, max_degree=bg.max_deg)
-            g = rbf @ w[p + "tu.rbf_gate"].t()
+            g = rbf @ w[p + "tu.rbf_gate"].t()  # K = k_rbf (6): cuBLAS
             if gem:
-                Z = S @ w[p + "tu.bilinear_proj"].t()
-                Y = Z * g
+                Y, Z = L(S, w[p + "tu.bilinear_proj"], aux=g, flags=ops.EPI_MUL_AUX)  # Y = (S P^T) * g
                 st["Z"] = Z
             else:
                 Y = S * g
-            ta = Y @ w[p + "tu.up"].t()
-            xcat = torch.cat([m, ta], dim=1)
-            h = torch.addmm(w[p + "eu.b1"], xcat, w[p + "eu.w1"].t())
-            a1 = F.silu(h)
-            m_new = torch.addmm(w[p + "eu.b2"], a1, w[p + "eu.w2"].t()).add_(m)
-            st.update(down=down, X=X, Wk=Wk, S=S, g=g, Y=Y, xcat=xcat, h=h, a1=a1, m_new=m_new)
+            ta = L(Y, w[p + "tu.up"])
+            w1 = w[p + "eu.w1"]
+            # h = [m, ta] W1^T + b1 without materialising the concat; a1 = silu(h)
+            h, a1 = L(m, w1[:, :de], a2=ta, w2=w1[:, de:], bias=w[p + "eu.b1"], flags=ops.EPI_SILU_OUT2)
+            m_new = L(a1, w[p + "eu.w2"], bias=w[p + "eu.b2"], resid=m)
+            st.update(down=down, X=X, Wk=Wk, S=S, g=g, Y=Y, ta=ta, h=h, a1=a1, m_new=m_new)
             agg = ops.aggregate_in_edges(bg.edge_ptr, bg.rev, m_new)
-            hv = torch.addmm(w[p + "nu.b1"], agg, w[p + "nu.w1"].t())
-            av = F.silu(hv)
-            v = torch.addmm(w[p + "nu.b2"], av, w[p + "nu.w2"].t())
+            hv, av = L(agg, w[p + "nu.w1"], bias=w[p + "nu.b1"], flags=ops.EPI_SILU_OUT2)
+            v = L(av, w[p + "nu.w2"], bias=w[p + "nu.b2"])
             st.update(agg=agg, hv=hv, av=av, v=v)
             if gem:
                 w1 = w[p + "eu2.w1"]
-                pv = v @ w1[:, c.d_e:].t()
-                h2 = torch.addmm(w[p + "eu2.b1"], m_new, w1[:, : c.d_e].t())
-                ops.gather_rows(bg.recv, pv, out=h2, accumulate=True)
-                a2 = F.silu(h2)
-                m2 = torch.addmm(w[p + "eu2.b2"], a2, w[p + "eu2.w2"].t()).add_(m_new)
+                pv = L(v, w1[:, de:])
+                h2, a2 = L(m_new, w1[:, :de], bias=w[p + "eu2.b1"], gather=(pv, bg.recv), flags=ops.EPI_SILU_OUT2)
+                m2 = L(a2, w[p + "eu2.w2"], bias=w[p + "eu2.b2"], resid=m_new)
                 m2r = ops.gather_rows(bg.rev, m2)
-                m = torch.addmm(m2, m2r, w[p + "sym.w"].t())
+                m = L(m2r, w[p + "sym.w"], resid=m2)
                 st.update(h2=h2, a2=a2, m2r=m2r)
             else:
                 m = m_new
             s = ops.graph_sum(bg.graph_ptr, v)
-            pre = torch.addmm(w[p + "gu.b1"], s, w[p + "gu.w1"].t())
+            pre = torch.addmm(w[p + "gu.b1"], s, w[p + "gu.w1"].t())  # G rows: cuBLAS
             act = F.silu(pre)
             u = torch.addmm(w[p + "gu.b2"], act, w[p + "gu.w2"].t()).add_(u)
             st.update(s=s, pre=pre, act=act)
@@ -181,7 +179,7 @@ class Engine:
         if d_forces is not None and not gem:
             raise ValueError("force seed given but this variant has no force head")
         de = c.d_e
-        wg, cs = ops.wgrad, ops.column_sum
+        L, wg, cs = ops.linear, ops.linear_wgrad, ops.column_sum
         self.weights.grad_flat.zero_()
         eg = torch.zeros((bg.num_edges, 4), dtype=torch.float32, device=bg.device)
         dE = d_energy.to(torch.float32).view(-1, 1)
@@ -197,7 +195,7 @@ class Engine:
         for b in range(c.blocks - 1, -1, -1):
             p = f"block{b}."
             st = fw.blocks[b]
-            # GU (engine.py:207-217)
+            # GU (engine.py:207-217), G rows: cuBLAS
             torch.mm(u_bar.t(), st["act"], out=gr[p + "gu.w2"])
             gr[p + "gu.b2"].copy_(u_bar.sum(0))
             pre_bar = _silu_bwd(u_bar @ w[p + "gu.w2"], st["pre"])
@@ -206,52 +204,53 @@ class Engine:
             s_bar = pre_bar @ w[p + "gu.w1"]
             v_bar = ops.gather_rows(bg.node_graph, s_bar)
             if gem:
-                # sym (engine.py:195-200)
-                wg(m_bar, st["m2r"], out=gr[p + "sym.w"])
-                t = m_bar @ w[p + "sym.w"]
+                # sym (engine.py:195-200): m = m2 + m2[rev] Wsym^T
+                wg(m_bar, st["m2r"], gr[p + "sym.w"])
+                t = L(m_bar, w[p + "sym.w"], w_mn=True)
                 m2_bar = ops.gather_rows(bg.rev, t, out=m_bar.clone(), accumulate=True)
                 # EU2 (engine.py:180-192)
-                wg(m2_bar, st["a2"], out=gr[p + "eu2.w2"])
+                wg(m2_bar, st["a2"], gr[p + "eu2.w2"])
                 cs(m2_bar, out=gr[p + "eu2.b2"])
-                h2_bar = _silu_bwd(m2_bar @ w[p + "eu2.w2"], st["h2"])
+                h2_bar = L(m2_bar, w[p + "eu2.w2"], w_mn=True, aux=st["h2"], flags=ops.EPI_DSILU_AUX)
                 cs(h2_bar, out=gr[p + "eu2.b1"])
                 w1 = w[p + "eu2.w1"]
-                gr[p + "eu2.w1"][:, :de].copy_(wg(h2_bar, st["m_new"]))
+                gr[p + "eu2.w1"][:, :de].copy_(wg(h2_bar, st["m_new"], torch.empty_like(w1[:, :de])))
                 pv_bar = ops.aggregate_in_edges(bg.edge_ptr, bg.rev, h2_bar)
-                gr[p + "eu2.w1"][:, de:].copy_(pv_bar.t() @ st["v"])
-                v_bar = torch.addmm(v_bar, pv_bar, w1[:, de:])
-                m_new_bar = torch.addmm(m2_bar, h2_bar, w1[:, :de])
+                gr[p + "eu2.w1"][:, de:].copy_(wg(pv_bar, st["v"], torch.empty_like(w1[:, de:])))
+                v_bar = L(pv_bar, w1[:, de:].contiguous(), w_mn=True, resid=v_bar)
+                m_new_bar = L(h2_bar, w1[:, :de].contiguous(), w_mn=True, resid=m2_bar)
             else:
                 m_new_bar = m_bar.clone()
             # EA + NU (engine.py:166-177)
-            torch.mm(v_bar.t(), st["av"], out=gr[p + "nu.w2"])
+            wg(v_bar, st["av"], gr[p + "nu.w2"])
             cs(v_bar, out=gr[p + "nu.b2"])
-            hv_bar = _silu_bwd(v_bar @ w[p + "nu.w2"], st["hv"])
+            hv_bar = L(v_bar, w[p + "nu.w2"], w_mn=True, aux=st["hv"], flags=ops.EPI_DSILU_AUX)
             cs(hv_bar, out=gr[p + "nu.b1"])
-            torch.mm(hv_bar.t(), st["agg"], out=gr[p + "nu.w1"])
-            agg_bar = hv_bar @ w[p + "nu.w1"]
+            wg(hv_bar, st["agg"], gr[p + "nu.w1"])
+            agg_bar = L(hv_bar, w[p + "nu.w1"], w_mn=True)
             ops.gather_rows(bg.recv, agg_bar, out=m_new_bar, accumulate=True)
             # EU (engine.py:152-158)
-            wg(m_new_bar, st["a1"], out=gr[p + "eu.w2"])
+            wg(m_new_bar, st["a1"], gr[p + "eu.w2"])
             cs(m_new_bar, out=gr[p + "eu.b2"])
-            h_bar = _silu_bwd(m_new_bar @ w[p + "eu.w2"], st["h"])
+            h_bar = L(m_new_bar, w[p + "eu.w2"], w_mn=True, aux=st["h"], flags=ops.EPI_DSILU_AUX)
             cs(h_bar, out=gr[p + "eu.b1"])
-            wg(h_bar, st["xcat"], out=gr[p + "eu.w1"])
-            x_bar = h_bar @ w[p + "eu.w1"]
-            m_in_bar = m_new_bar.add_(x_bar[:, :de])
-            ta_bar = x_bar[:, de:]
+            w1 = w[p + "eu.w1"]
+            gr[p + "eu.w1"][:, :de].copy_(wg(h_bar, st["m"], torch.empty_like(w1[:, :de])))
+            gr[p + "eu.w1"][:, de:].copy_(wg(h_bar, st["ta"], torch.empty_like(w1[:, de:])))
+            m_in_bar = L(h_bar, w1[:, :de].contiguous(), w_mn=True, resid=m_new_bar)
+            ta_bar = L(h_bar, w1[:, de:].contiguous(), w_mn=True)
             # TU (engine.py:118-149)
-            wg(ta_bar, st["Y"], out=gr[p + "tu.up"])
-            Y_bar = ta_bar @ w[p + "tu.up"]
+            wg(ta_bar, st["Y"], gr[p + "tu.up"])
+            Y_bar = L(ta_bar, w[p + "tu.up"], w_mn=True)
             if gem:
                 Z_bar = Y_bar * st["g"]
                 g_bar = Y_bar * st["Z"]
-                wg(Z_bar, st["S"], out=gr[p + "tu.bilinear_proj"])
-                S_bar = Z_bar @ w[p + "tu.bilinear_proj"]
+                wg(Z_bar, st["S"], gr[p + "tu.bilinear_proj"])
+                S_bar = L(Z_bar, w[p + "tu.bilinear_proj"], w_mn=True)
             else:
                 S_bar = Y_bar * st["g"]
                 g_bar = Y_bar * st["S"]
-            wg(g_bar, fw.rbf, out=gr[p + "tu.rbf_gate"])
+            torch.mm(g_bar.t(), fw.rbf, out=gr[p + "tu.rbf_gate"])  # N = k_rbf (6): cuBLAS
             rbf_bar.addmm_(g_bar, w[p + "tu.rbf_gate"])
             X_bar, Wk_bar = ops.triplet_bwd(bg.edge_ptr, bg.rev, bg.geo, st["X"], st["Wk"], c.cutoff,
                                             S_bar, eg, max_degree=bg.max_deg)
@@ -259,16 +258,15 @@ class Engine:
             if gem:
                 torch.mm(wp_bar, w[p + "tu.sbf_gate"].t(), out=gr[p + "tu.bilinear_b"])
                 torch.mm(w[p + "tu.bilinear_b"].t(), wp_bar, out=gr[p + "tu.sbf_gate"])
-                wg(X_bar, st["down"], out=gr[p + "tu.bilinear_a"])
-                down_bar = X_bar @ w[p + "tu.bilinear_a"]
+                wg(X_bar, st["down"], gr[p + "tu.bilinear_a"])
+                down_bar = L(X_bar, w[p + "tu.bilinear_a"], w_mn=True)
             else:
                 gr[p + "tu.sbf_gate"].copy_(wp_bar)
                 down_bar = X_bar
-            m_in = st["xcat"][:, :de]
-            wg(down_bar, m_in, out=gr[p + "tu.down"])
-            m_bar = m_in_bar.addmm_(down_bar, w[p + "tu.down"])
-        # edge init (engine.py:109-111)
-        wg(m_bar, fw.rbf, out=gr["edge_init.w"])
+            wg(down_bar, st["m"], gr[p + "tu.down"])
+            m_bar = L(down_bar, w[p + "tu.down"], w_mn=True, resid=m_in_bar)
+        # edge init (engine.py:109-111), K = k_rbf: cuBLAS
+        torch.mm(m_bar.t(), fw.rbf, out=gr["edge_init.w"])
         cs(m_bar, out=gr["edge_init.b"])
         rbf_bar.addmm_(m_bar, w["edge_init.w"])
         ops.rbf_bwd(bg.geo, rbf_bar, c.cutoff, eg)

@@ -258,13 +258,15 @@ def _rowmajor(t):
     return t if t.stride(1) == 1 else t.contiguous()
 
 
-def gemm(a, b, a2=None, b2=None, bias=None, resid=None, gather=None, aux=None, flags=0, out=None, out2=None):
+def gemm(a, b, a2=None, b2=None, bias=None, resid=None, gather=None, aux=None, flags=0, out=None, out2=None,
+         b_mn=False):
     """out = a b^T (+ a2 b2^T) with the fused epilogue of egn_gemm (tcgen05, 3xTF32).
 
-    a: [M, K] rows, b: [N, K] (weights stored (out, in)); gather = (src [*, N], idx int32 [M])."""
+    a: [M, K] rows, b: [N, K] (weights stored (out, in)), or with b_mn=True b: [K, N]
+    (so a @ W for a weight W [K, N] needs no transpose); gather = (src [*, N], idx int32 [M])."""
     a, b = _rowmajor(a), _rowmajor(b)
     M, K = a.shape
-    N = b.shape[0]
+    N = b.shape[1] if b_mn else b.shape[0]
     nseg = 1 if a2 is None else 2
     if nseg == 2:
         a2, b2 = _rowmajor(a2), _rowmajor(b2)
@@ -287,8 +289,80 @@ def gemm(a, b, a2=None, b2=None, bias=None, resid=None, gather=None, aux=None, f
          ptr(bias), ptr(resid), resid.stride(0) if resid is not None else 0,
          ptr(gsrc), ptr(gidx), gsrc.stride(0) if gsrc is not None else 0,
          ptr(aux), aux.stride(0) if aux is not None else 0, int(flags),
-         ptr(out), out.stride(0), ptr(out2), out2.stride(0) if out2 is not None else 0, stream())
+         ptr(out), out.stride(0), ptr(out2), out2.stride(0) if out2 is not None else 0, int(b_mn), stream())
     return (out, out2) if need2 else out
+
+
+def gemm_wgrad(g, x, out=None, accumulate=False):
+    """out[M, N] (+)= g^T x for g [R, M], x [R, N] on the tensor cores (split over R)."""
+    g, x = _rowmajor(g), _rowmajor(x)
+    R, M = g.shape
+    N = x.shape[1]
+    if out is None:
+        out = torch.empty((M, N), dtype=torch.float32, device=g.device)
+    nbytes = call("egn_gemm_wgrad_workspace_bytes", R, M, N)
+    ws = _workspace_named("wgrad", nbytes, g.device)
+    call("egn_gemm_wgrad", R, M, N, ptr(g), g.stride(0), ptr(x), x.stride(0), ptr(out), int(accumulate), ptr(ws),
+         stream())
+    return out
+
+
+def _tc_ok(k, n, *ts):
+    """Shapes the tcgen05 GEMM tiles (K % 4, N % 16, 16-byte aligned rows)."""
+    if k % 4 or n % 16 or n < 16:
+        return False
+    for t in ts:
+        if t is not None and (t.data_ptr() % 16 or (t.dim() == 2 and t.stride(0) % 4) or t.stride(-1) != 1):
+            return False
+    return True
+
+
+def _silu_grad(h):
+    s = torch.sigmoid(h)
+    return s * (1.0 + h * (1.0 - s))
+
+
+def linear(a, w, a2=None, w2=None, bias=None, resid=None, gather=None, aux=None, flags=0, w_mn=False):
+    """Dense layer y = a w^T (+ a2 w2^T) (+ bias, resid, gathered rows; SiLU / gate / SiLU' epilogues).
+
+    w is stored (out, in) as in the reference (egn/tape.py:104-119); w_mn=True
+    computes a @ w instead (the data gradient).  Runs the tcgen05 3xTF32 GEMM for
+    every shape that maps onto UMMA tiles (all model dims of BASELINE configs);
+    only toy widths (N % 16 != 0 or K % 4 != 0) use an fp32 cuBLAS composite.
+    Returns y, or (y, out2) for EPI_SILU_OUT2 / EPI_MUL_AUX."""
+    k = a.shape[1]
+    n = w.shape[1] if w_mn else w.shape[0]
+    ok = _tc_ok(k, n, a, w, a2, w2, resid, aux)
+    if a2 is not None:
+        ok = ok and a2.shape[1] % 4 == 0 and not w_mn
+    if gather is not None:
+        ok = ok and gather[0].stride(-1) == 1
+    if ok:
+        return gemm(a, w, a2=a2, b2=w2, bias=bias, resid=resid, gather=gather, aux=aux, flags=flags, b_mn=w_mn)
+    y = a @ w if w_mn else a @ w.t()
+    if a2 is not None:
+        y = y + a2 @ w2.t()
+    if bias is not None:
+        y = y + bias
+    if resid is not None:
+        y = y + resid
+    if gather is not None:
+        y = y + gather[0].index_select(0, gather[1].long())
+    if flags & EPI_DSILU_AUX:
+        y = y * _silu_grad(aux)
+    if flags & EPI_MUL_AUX:
+        return y * aux, y
+    if flags & EPI_SILU_OUT2:
+        return y, torch.nn.functional.silu(y)
+    return y
+
+
+def linear_wgrad(g, x, out):
+    """out = g^T x (weight gradient over all rows)."""
+    if _tc_ok(4, x.shape[1], g, x) and out.is_contiguous():
+        return gemm_wgrad(g, x, out=out)
+    out.copy_(g.t() @ x)
+    return out
 
 
 def sgd_(w, g, lr):

@@ -62,6 +62,42 @@ def test_two_segments_and_epilogues():
     assert _rel(out, zr * s * (1 + aux.double() * (1 - s))) < 1e-5
 
 
+@pytest.mark.parametrize("M,N,K", [(1000, 128, 64), (3001, 64, 128), (500, 256, 128), (77, 128, 256)])
+def test_mn_major_b_dgrad(M, N, K):
+    """a @ W with W [K, N] (the data gradient of a linear layer) without a transpose copy."""
+    from paper_2203_09697_b200 import ops
+
+    g = torch.Generator(device="cuda").manual_seed(M)
+    a = torch.randn((M, K), device="cuda", generator=g)
+    w = torch.randn((K, N), device="cuda", generator=g) / K ** 0.5
+    aux = torch.randn((M, N), device="cuda", generator=g)
+    out = ops.gemm(a, w, b_mn=True)
+    assert _rel(out, a.double() @ w.double()) < TOL
+    out = ops.gemm(a, w, b_mn=True, aux=aux, flags=ops.EPI_DSILU_AUX)
+    s = torch.sigmoid(aux.double())
+    assert _rel(out, (a.double() @ w.double()) * s * (1 + aux.double() * (1 - s))) < 1e-5
+
+
+@pytest.mark.parametrize("R,M,N", [(58644, 128, 128), (58644, 64, 256), (1000, 128, 64), (37, 64, 64),
+                                   (2560, 128, 128), (20000, 256, 128)])
+def test_wgrad_split_k(R, M, N):
+    from paper_2203_09697_b200 import ops
+
+    g = torch.Generator(device="cuda").manual_seed(R + M)
+    gr = torch.randn((R, M), device="cuda", generator=g)
+    x = torch.randn((R, N), device="cuda", generator=g)
+    out = ops.gemm_wgrad(gr, x)
+    ref = gr.double().t() @ x.double()
+    assert _rel(out, ref) < TOL
+    prev = torch.randn((M, N), device="cuda", generator=g)
+    out2 = ops.gemm_wgrad(gr, x, out=prev.clone(), accumulate=True)
+    assert _rel(out2, ref + prev.double()) < TOL
+    # strided operand (a column block of a wider matrix)
+    wide = torch.randn((R, 2 * N), device="cuda", generator=g)
+    out3 = ops.gemm_wgrad(gr, wide[:, N:])
+    assert _rel(out3, gr.double().t() @ wide[:, N:].double()) < TOL
+
+
 def test_strided_operands_and_errors():
     from paper_2203_09697_b200 import ops
 
