@@ -24,6 +24,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <unordered_map>
@@ -35,8 +36,6 @@ namespace gemm {
 
 constexpr int BM = 128;
 constexpr int BK = 32;                 // fp32 elements per 128-byte swizzled row
-constexpr int kStages = 3;
-constexpr int kThreads = 128;
 
 enum Epi : int {
   EPI_BIAS = 1,        // C += bias[n]
@@ -64,6 +63,8 @@ struct Params {
   float* out2;
   int64_t ldo2;
   int kb_per_split;        // split-K: k-blocks per blockIdx.z (0 = all)
+  int flush_steps;         // k-steps (of 8) per TMEM->register flush (0 = whole tile)
+  int tma_out;             // single-output epilogues store through mapOut (TMA)
   int64_t split_stride;    // split-K: elements between partial outputs
   long long* trace;        // debug timeline (EGN_GEMM_TRACE), CTA 0 only
 };
@@ -83,9 +84,9 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
       "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
-      "r"(parity)
+      "r"(parity), "r"(1000000)
       : "memory");
 }
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
@@ -93,6 +94,11 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
       "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];"
       ::"r"(smem_u32(dst)), "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
       : "memory");
+}
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, const void* src, int c0, int c1, int c2) {
+  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(map), "r"(c0),
+               "r"(c1), "r"(c2), "r"(smem_u32(src))
+               : "memory");
 }
 __device__ __forceinline__ uint64_t sw128_kmajor_desc(const void* smem_tile) {
   // start address >> 4 | LBO (unused for swizzled K-major) = 1 | SBO = 1024 B (8 rows x 128 B)
@@ -118,6 +124,21 @@ __device__ __forceinline__ uint64_t sw128_mnmajor_desc(const void* smem_tile) {
   d |= static_cast<uint64_t>(1) << 46;
   d |= static_cast<uint64_t>(1) << 61;
   return d;
+}
+__device__ __forceinline__ uint64_t sw128_kmajor_desc_u(uint32_t saddr) {
+  return static_cast<uint64_t>((saddr >> 4) & 0x3FFF) | (static_cast<uint64_t>(1) << 16) |
+         (static_cast<uint64_t>(1024 >> 4) << 32) | (static_cast<uint64_t>(1) << 46) | (static_cast<uint64_t>(2) << 61);
+}
+__device__ __forceinline__ uint64_t sw128_mnmajor_desc_u(uint32_t saddr) {
+  return static_cast<uint64_t>((saddr >> 4) & 0x3FFF) | (static_cast<uint64_t>(4096 >> 4) << 16) |
+         (static_cast<uint64_t>(512 >> 4) << 32) | (static_cast<uint64_t>(1) << 46) | (static_cast<uint64_t>(1) << 61);
+}
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n\t.reg .pred P;\n\telect.sync _|P, 0xffffffff;\n\tselp.b32 %0, 1, 0, P;\n\t}"
+      : "=r"(pred));
+  return pred != 0;
 }
 __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
                                          uint32_t accumulate) {
@@ -160,60 +181,115 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
   do {                                                                                  \
     if (P.trace && blockIdx.x == 0 && (idx) < 64 && ((threadIdx.x & 31) == 0)) {        \
       long long t_;                                                                     \
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                            \
+      asm volatile("mov.u64 %0, %%clock64;" : "=l"(t_));                                 \
       P.trace[(role) * 64 + (idx)] = t_;                                                \
     }                                                                                   \
   } while (0)
 
-// Persistent, warp-specialised 3xTF32 GEMM (BN = 64 output columns per tile).
-//   warp 0       : TMA producer (S-deep ring of raw fp32 A/B k-blocks)
-//   warp 1       : MMA issuer (one elected thread)
-//   warps 2..5   : split each landed k-block into hi (in place) / lo buffers
+// Persistent, warp-specialised 3xTF32 GEMM, 128 x 64 output tiles.
+//   warp 0       : TMA producer: raw fp32 A/B k-blocks into a kTmaRing-deep ring
+//   warp 1       : MMA issuer (whole warp walks the loop, one elected lane issues)
+//   warps 2..5   : split each landed k-block and release its TMA slot at once:
+//                  A rows (thread = row) go to a TMEM slot as hi = rna_tf32(a),
+//                  lo = a - hi (tcgen05.st); B goes to a shared hi/lo slot (same
+//                  swizzled layout, elementwise).  kOpRing operand slots.
 //   warps 6..13  : two accumulator groups of 4 warps; group = tile parity, so one
 //                  group's epilogue overlaps the other group's main loop.
 //                  TMEM lane quarter = warp % 4.
-// Accuracy: the big term A_hi.B_hi goes to a fresh TMEM tile every kFlush k-steps
-// (double buffered per group) that the group adds into fp32 registers, so the
-// tensor core's truncating accumulation spans kFlush steps only; the small terms
-// (A_lo.B_hi, A_hi.B_lo, ~2^-11 smaller) accumulate in TMEM over the whole K range.
-constexpr int kFlush = 2;
+// Per k-step the three products A_lo.B_hi, A_hi.B_lo, A_hi.B_hi read A from TMEM,
+// so shared-memory traffic per k-step is the B operand only.
+// Accuracy: the tensor core accumulates with truncation, a bias that grows with
+// the number of k-steps summed in TMEM.  All three products of a k-step go to a
+// TMEM tile (double buffered per group) that is restarted every P.flush_steps
+// k-steps; the group adds each finished window into fp32 registers (round to
+// nearest).
+// TMEM columns: [0, 256) accumulators (group, buffer) x 64; [256, 256 + 64 kOpRing)
+// A operand slots (hi at +0, lo at +32).
+// Epilogue: each warp owns a [2 chunks][32 rows][32 cols] fp32 buffer (16-byte
+// granules XOR-swizzled by row), prefetched with the operand rows (residual /
+// gathered rows / aux) during the main loop; thread = row combines in place,
+// then lanes = columns copy out coalesced.
+constexpr int BN = 64;
+constexpr int kTmaRing = 5;
+constexpr int kOpRing = 2;
+constexpr int kTmaSlot = BM * BK * 4 + BN * BK * 4;  // 24 KB raw A + raw B
+constexpr int kOpSlot = 2 * BN * BK * 4;            // 16 KB B hi + lo
+constexpr int kEpiWarp = 2 * 32 * 32 * 4;           // 8 KB per accumulator warp
+constexpr size_t kGemmSmem = static_cast<size_t>(kTmaRing) * kTmaSlot + kOpRing * kOpSlot + 8 * kEpiWarp + 1024;
 
-template <int BN, bool AMN, bool BMN>
+__device__ __forceinline__ void mma_tf32_ta(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc,
+                                            uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const float* v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
+          taddr),
+      "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])), "r"(__float_as_uint(v[3])),
+      "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])), "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7])),
+      "r"(__float_as_uint(v[8])), "r"(__float_as_uint(v[9])), "r"(__float_as_uint(v[10])),
+      "r"(__float_as_uint(v[11])), "r"(__float_as_uint(v[12])), "r"(__float_as_uint(v[13])),
+      "r"(__float_as_uint(v[14])), "r"(__float_as_uint(v[15]))
+      : "memory");
+}
+// round-to-nearest (ties away) to tf32 with integer ops: add half an ulp of the
+// 10-bit mantissa to the magnitude bits and clear the 13 low bits
+__device__ __forceinline__ float tf32_rna_int(float x) {
+  return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xffffe000u);
+}
+__device__ __forceinline__ float dsilu(float o) {
+  const float sg = __fdividef(1.f, 1.f + __expf(-o));
+  return sg * (1.f + o * (1.f - sg));
+}
+// element (r, c) of a [32][32] epilogue chunk (granule swizzled by row)
+__device__ __forceinline__ int epi_idx(int r, int c) { return r * 32 + ((((c >> 2) ^ (r & 7))) << 2) + (c & 3); }
+
+template <bool AMN, bool BMN>
 __global__ void __launch_bounds__(448, 1)
 gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_constant__ CUtensorMap mapB0,
                    const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ CUtensorMap mapB1,
-                   Params P, int tiles_n, int splits, int total_items) {
-  static_assert(BN == 64, "tile width");
-  constexpr int A_BYTES = BM * BK * 4;  // 16 KB
+                   const __grid_constant__ CUtensorMap mapOut, Params P, int tiles_n, int splits, int total_items) {
+  constexpr int A_BYTES = BM * BK * 4;  // 16 KB raw A k-block
   constexpr int B_BYTES = BN * BK * 4;  // 8 KB
-  constexpr int STAGE = 2 * A_BYTES + 2 * B_BYTES;
-  constexpr int S = 3;
-  constexpr uint32_t TMEM_COLS = 512;  // 2 groups x (big[2] + small) x 64
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  constexpr uint32_t TMEM_COLS = 512;
+  constexpr uint32_t A_TMEM = 256;
+  extern __shared__ __align__(16) uint8_t smem_raw[];
   // 1024-byte alignment for SWIZZLE_128B by offsetting the __shared__ array itself
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  float* stile_all = reinterpret_cast<float*>(smem + S * STAGE);  // 8 warps x [32][33]
-  __shared__ __align__(8) uint64_t full_bar[S], conv_bar[S], empty_bar[S];
-  __shared__ __align__(8) uint64_t accf_bar[2][2], acce_bar[2][2], small_bar[2];
+  uint8_t* opring = smem + kTmaRing * kTmaSlot;
+  float* epi_all = reinterpret_cast<float*>(opring + kOpRing * kOpSlot);
+  __shared__ __align__(8) uint64_t tma_full[kTmaRing], tma_empty[kTmaRing], op_full[kOpRing], op_empty[kOpRing];
+  __shared__ __align__(8) uint64_t accf_bar[2][2], acce_bar[2][2];
   __shared__ uint32_t tmem_base;
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int nk0 = (P.k0 + BK - 1) / BK;
   const int nk_all = nk0 + (P.nseg > 1 ? (P.k1 + BK - 1) / BK : 0);
   const int kbps = P.kb_per_split > 0 ? P.kb_per_split : nk_all;
+  if (P.trace && tid == 0) {
+    long long g;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+    P.trace[1024 + 4 * blockIdx.x] = g;
+  }
 
   if (tid == 0) {
-    for (int s = 0; s < S; ++s) {
-      mbar_init(&full_bar[s], 1);
-      mbar_init(&conv_bar[s], 1);
-      mbar_init(&empty_bar[s], 1);
+    for (int s = 0; s < kTmaRing; ++s) {
+      mbar_init(&tma_full[s], 1);
+      mbar_init(&tma_empty[s], 1);
+    }
+    for (int s = 0; s < kOpRing; ++s) {
+      mbar_init(&op_full[s], 1);
+      mbar_init(&op_empty[s], 1);
     }
     for (int gr = 0; gr < 2; ++gr) {
       for (int b = 0; b < 2; ++b) {
         mbar_init(&accf_bar[gr][b], 1);
         mbar_init(&acce_bar[gr][b], 4);
       }
-      mbar_init(&small_bar[gr], 4);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -241,133 +317,160 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_const
 
   if (warp == 0) {
     // ---------------- TMA producer
-    if (lane == 0) {
-      uint32_t it = 0;
-      for (int item = blockIdx.x; item < total_items; item += gridDim.x) {
-        int64_t m0;
-        int n0, kbeg, nk;
-        item_coords(item, m0, n0, kbeg, nk);
-        for (int kbl = 0; kbl < nk; ++kbl, ++it) {
-          const int s = it % S;
-          mbar_wait(&empty_bar[s], ((it / S) & 1) ^ 1);
-          EGN_TRACE(0, it);
-          uint8_t* st = smem + s * STAGE;
-          mbar_expect_tx(&full_bar[s], A_BYTES + B_BYTES);
-          const int kb = kbeg + kbl;
-          const bool first = kb < nk0;
-          const int kk = (first ? kb : kb - nk0) * BK;
-          const CUtensorMap* ma = first ? &mapA0 : &mapA1;
-          const CUtensorMap* mb = first ? &mapB0 : &mapB1;
-          if (AMN) {
-#pragma unroll
-            for (int i = 0; i < BM / 32; ++i)
-              tma_load_2d(st + i * 4096, ma, &full_bar[s], static_cast<int>(m0) + 32 * i, kk);
-          } else {
-            tma_load_2d(st, ma, &full_bar[s], kk, static_cast<int>(m0));
-          }
-          if (BMN) {
-#pragma unroll
-            for (int i = 0; i < BN / 32; ++i) tma_load_2d(st + 2 * A_BYTES + i * 4096, mb, &full_bar[s], n0 + 32 * i, kk);
-          } else {
-            tma_load_2d(st + 2 * A_BYTES, mb, &full_bar[s], kk, n0);
-          }
-        }
-      }
-    }
-  } else if (warp == 1) {
-    // ---------------- MMA issuer
-    if (lane == 0) {
-      const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((AMN ? 1u : 0u) << 15) |
-                             ((BMN ? 1u : 0u) << 16) | (static_cast<uint32_t>(BN >> 3) << 17) |
-                             (static_cast<uint32_t>(BM >> 4) << 24);
-      uint32_t it = 0, t = 0;
-      uint32_t fc[2] = {0, 0};  // flush counter per group
-      for (int item = blockIdx.x; item < total_items; item += gridDim.x, ++t) {
-        int64_t m0;
-        int n0, kbeg, nk;
-        item_coords(item, m0, n0, kbeg, nk);
-        const int gr = t & 1;
-        const uint32_t tg = tmem + gr * (3 * BN);
-        const uint32_t t_small = tg + 2 * BN;
-        mbar_wait(&small_bar[gr], ((t >> 1) & 1) ^ 1);  // this group's previous tile drained
-        asm volatile("tcgen05.fence::after_thread_sync;");
-        uint32_t b = 0, tbig = tg;
-        for (int kbl = 0; kbl < nk; ++kbl, ++it) {
-          const int s = it % S;
-          mbar_wait(&conv_bar[s], (it / S) & 1);
-          EGN_TRACE(1, it);
-          asm volatile("tcgen05.fence::after_thread_sync;");
-          const uint8_t* st = smem + s * STAGE;
-          const uint8_t* ahi = st;
-          const uint8_t* alo = st + A_BYTES;
-          const uint8_t* bhi = st + 2 * A_BYTES;
-          const uint8_t* blo = st + 2 * A_BYTES + B_BYTES;
-#pragma unroll
-          for (int k = 0; k < BK / 8; ++k) {
-            const int oa = AMN ? k * 1024 : k * 32;
-            const int ob = BMN ? k * 1024 : k * 32;
-            const uint64_t dah = AMN ? sw128_mnmajor_desc(ahi + oa) : sw128_kmajor_desc(ahi + oa);
-            const uint64_t dal = AMN ? sw128_mnmajor_desc(alo + oa) : sw128_kmajor_desc(alo + oa);
-            const uint64_t dbh = BMN ? sw128_mnmajor_desc(bhi + ob) : sw128_kmajor_desc(bhi + ob);
-            const uint64_t dbl = BMN ? sw128_mnmajor_desc(blo + ob) : sw128_kmajor_desc(blo + ob);
-            const bool fstart = (k % kFlush) == 0;
-            if (fstart) {
-              b = fc[gr] & 1;
-              mbar_wait(&acce_bar[gr][b], ((fc[gr] >> 1) & 1) ^ 1);
-              asm volatile("tcgen05.fence::after_thread_sync;");
-              tbig = tg + b * BN;
-            }
-            const uint32_t first_small = (kbl == 0 && k == 0) ? 0u : 1u;
-            mma_tf32(t_small, dal, dbh, idesc, first_small);
-            mma_tf32(t_small, dah, dbl, idesc, 1u);
-            mma_tf32(tbig, dah, dbh, idesc, fstart ? 0u : 1u);
-            if ((k % kFlush) == kFlush - 1) {
-              mma_commit(&accf_bar[gr][b]);
-              ++fc[gr];
-            }
-          }
-          mma_commit(&empty_bar[s]);
-        }
-      }
-    }
-  } else if (warp < 6) {
-    // ---------------- hi/lo split of each landed k-block (128 threads)
-    const int ct = tid - 64;
     uint32_t it = 0;
     for (int item = blockIdx.x; item < total_items; item += gridDim.x) {
       int64_t m0;
       int n0, kbeg, nk;
       item_coords(item, m0, n0, kbeg, nk);
       for (int kbl = 0; kbl < nk; ++kbl, ++it) {
-        const int s = it % S;
-        mbar_wait(&full_bar[s], (it / S) & 1);
-        if (ct == 0) EGN_TRACE(2, it);
-        uint8_t* st = smem + s * STAGE;
-        float4* a = reinterpret_cast<float4*>(st);
-        float4* alo = reinterpret_cast<float4*>(st + A_BYTES);
-#pragma unroll 4
-        for (int i = ct; i < A_BYTES / 16; i += 128) {
-          const float4 v = a[i];
-          float4 h;
-          h.x = tf32_rna(v.x); h.y = tf32_rna(v.y); h.z = tf32_rna(v.z); h.w = tf32_rna(v.w);
-          a[i] = h;
-          alo[i] = make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w);
+        const int s = it % kTmaRing;
+        mbar_wait(&tma_empty[s], ((it / kTmaRing) & 1) ^ 1);
+        EGN_TRACE(0, it);
+        if (elect_one()) {
+          uint8_t* st = smem + s * kTmaSlot;
+          mbar_expect_tx(&tma_full[s], A_BYTES + B_BYTES);
+          const int kb = kbeg + kbl;
+          const bool first = kb < nk0;
+          const int kk = (first ? kb : kb - nk0) * BK;
+          const CUtensorMap* ma = first ? &mapA0 : &mapA1;
+          const CUtensorMap* mb = first ? &mapB0 : &mapB1;
+          if (AMN) {
+            tma_load_2d(st, ma, &tma_full[s], static_cast<int>(m0), kk);  // [32 k][128 m], unswizzled
+          } else {
+            tma_load_2d(st, ma, &tma_full[s], kk, static_cast<int>(m0));  // [128 m][32 k], SW128
+          }
+          if (BMN) {
+#pragma unroll
+            for (int i = 0; i < BN / 32; ++i) tma_load_2d(st + A_BYTES + i * 4096, mb, &tma_full[s], n0 + 32 * i, kk);
+          } else {
+            tma_load_2d(st + A_BYTES, mb, &tma_full[s], kk, n0);
+          }
         }
-        float4* bb = reinterpret_cast<float4*>(st + 2 * A_BYTES);
-        float4* blo = reinterpret_cast<float4*>(st + 2 * A_BYTES + B_BYTES);
-#pragma unroll 4
+        __syncwarp();
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer
+    const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((BMN ? 1u : 0u) << 16) |
+                           (static_cast<uint32_t>(BN >> 3) << 17) | (static_cast<uint32_t>(BM >> 4) << 24);
+    uint32_t it = 0, t = 0;
+    uint32_t fc0 = 0, fc1 = 0;  // window counters per accumulator group
+    for (int item = blockIdx.x; item < total_items; item += gridDim.x, ++t) {
+      int64_t m0;
+      int n0, kbeg, nk;
+      item_coords(item, m0, n0, kbeg, nk);
+      const int gr = t & 1;
+      uint32_t& fc = gr ? fc1 : fc0;
+      const uint32_t tg = tmem + gr * (2 * BN);
+      uint32_t tacc = tg, bsel = 0;
+      const int nsteps = nk * (BK / 8);
+      const int win = P.flush_steps > 0 ? P.flush_steps : nsteps;
+      int j = 0, wpos = 0;
+      for (int kbl = 0; kbl < nk; ++kbl, ++it) {
+        const int o = it % kOpRing;
+        mbar_wait(&op_full[o], (it / kOpRing) & 1);
+        EGN_TRACE(1, it);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        const uint32_t bhi = smem_u32(opring + o * kOpSlot);
+        const uint32_t blo = bhi + B_BYTES;
+        const uint32_t ta = tmem + A_TMEM + o * 64;
+#pragma unroll
+        for (int k = 0; k < BK / 8; ++k) {
+          const bool fstart = wpos == 0;
+          if (fstart) {
+            bsel = fc & 1;
+            mbar_wait(&acce_bar[gr][bsel], ((fc >> 1) & 1) ^ 1);
+            asm volatile("tcgen05.fence::after_thread_sync;");
+            tacc = tg + bsel * BN;
+          }
+          ++j;
+          const bool fend = (++wpos == win) || (j == nsteps);
+          if (elect_one()) {
+            const uint32_t ob = BMN ? k * 1024 : k * 32;
+            const uint64_t dbh = BMN ? sw128_mnmajor_desc_u(bhi + ob) : sw128_kmajor_desc_u(bhi + ob);
+            const uint64_t dbl = BMN ? sw128_mnmajor_desc_u(blo + ob) : sw128_kmajor_desc_u(blo + ob);
+            // small terms first into the fresh window tile, then the big term
+            mma_tf32_ta(tacc, ta + 32 + k * 8, dbh, idesc, fstart ? 0u : 1u);
+            mma_tf32_ta(tacc, ta + k * 8, dbl, idesc, 1u);
+            mma_tf32_ta(tacc, ta + k * 8, dbh, idesc, 1u);
+            if (fend) mma_commit(&accf_bar[gr][bsel]);
+          }
+          __syncwarp();
+          if (fend) {
+            ++fc;
+            wpos = 0;
+          }
+        }
+        EGN_TRACE(4, it);
+        if (elect_one()) mma_commit(&op_empty[o]);
+        __syncwarp();
+      }
+    }
+  } else if (warp < 6) {
+    // ---------------- split (128 threads): raw TMA slot -> operand slot, release
+    const int ct = tid - 64;
+    const int q = warp & 3;
+    const int r = q * 32 + lane;  // A row of this thread == its TMEM lane
+    const uint32_t lane_off = static_cast<uint32_t>(q * 32) << 16;
+    uint32_t it = 0;
+    for (int item = blockIdx.x; item < total_items; item += gridDim.x) {
+      int64_t m0;
+      int n0, kbeg, nk;
+      item_coords(item, m0, n0, kbeg, nk);
+      for (int kbl = 0; kbl < nk; ++kbl, ++it) {
+        const int s = it % kTmaRing;
+        const int o = it % kOpRing;
+        mbar_wait(&tma_full[s], (it / kTmaRing) & 1);
+        if (ct == 0) EGN_TRACE(2, it);
+        mbar_wait(&op_empty[o], ((it / kOpRing) & 1) ^ 1);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        const uint8_t* st = smem + s * kTmaSlot;
+        const uint32_t ta = tmem + lane_off + A_TMEM + o * 64;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          float hi[16], lo[16];
+#pragma unroll
+          for (int g = 0; g < 4; ++g) {
+            float4 v;
+            if (AMN) {
+              const float* col = reinterpret_cast<const float*>(st) + r;
+              v = make_float4(col[(h * 16 + g * 4 + 0) * BM], col[(h * 16 + g * 4 + 1) * BM],
+                              col[(h * 16 + g * 4 + 2) * BM], col[(h * 16 + g * 4 + 3) * BM]);
+            } else {
+              const int gran = h * 4 + g;
+              v = *reinterpret_cast<const float4*>(st + r * 128 + ((gran ^ (r & 7)) << 4));
+            }
+            hi[g * 4 + 0] = tf32_rna_int(v.x);
+            hi[g * 4 + 1] = tf32_rna_int(v.y);
+            hi[g * 4 + 2] = tf32_rna_int(v.z);
+            hi[g * 4 + 3] = tf32_rna_int(v.w);
+            lo[g * 4 + 0] = v.x - hi[g * 4 + 0];
+            lo[g * 4 + 1] = v.y - hi[g * 4 + 1];
+            lo[g * 4 + 2] = v.z - hi[g * 4 + 2];
+            lo[g * 4 + 3] = v.w - hi[g * 4 + 3];
+          }
+          tmem_st16(ta + h * 16, hi);
+          tmem_st16(ta + 32 + h * 16, lo);
+        }
+        const float4* braw = reinterpret_cast<const float4*>(st + A_BYTES);
+        float4* bhi = reinterpret_cast<float4*>(opring + o * kOpSlot);
+        float4* blo = reinterpret_cast<float4*>(opring + o * kOpSlot + B_BYTES);
+#pragma unroll
         for (int i = ct; i < B_BYTES / 16; i += 128) {
-          const float4 v = bb[i];
+          const float4 v = braw[i];
           float4 h;
-          h.x = tf32_rna(v.x); h.y = tf32_rna(v.y); h.z = tf32_rna(v.z); h.w = tf32_rna(v.w);
-          bb[i] = h;
+          h.x = tf32_rna_int(v.x); h.y = tf32_rna_int(v.y); h.z = tf32_rna_int(v.z); h.w = tf32_rna_int(v.w);
+          bhi[i] = h;
           blo[i] = make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w);
         }
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("tcgen05.fence::before_thread_sync;");
         named_bar_sync(1, 128);
         if (ct == 0) {
           EGN_TRACE(3, it);
-          mbar_arrive(&conv_bar[s]);
+          mbar_arrive(&tma_empty[s]);
+          mbar_arrive(&op_full[o]);
         }
       }
     }
@@ -376,8 +479,8 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_const
     const int gr = (warp - 6) >> 2;
     const int q = warp & 3;  // TMEM lane quarter == this warp's 32 tile rows
     const uint32_t lane_off = static_cast<uint32_t>(q * 32) << 16;
-    const uint32_t tg = tmem + gr * (3 * BN) + lane_off;
-    float* stile = stile_all + (warp - 6) * (32 * 33);
+    const uint32_t tg = tmem + gr * (2 * BN) + lane_off;
+    float* ebuf = epi_all + (warp - 6) * (2 * 32 * 32);
     const int opkind = (P.flags & EPI_RESID) ? 1 : ((P.flags & EPI_GATHER) ? 2 : ((P.flags & (EPI_DSILU_AUX | EPI_MUL_AUX)) ? 3 : 0));
     uint32_t fcount = 0;
     uint32_t t = 0;
@@ -388,10 +491,36 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_const
       int n0, kbeg, nk;
       const int z = item_coords(item, m0, n0, kbeg, nk);
       const int64_t rbase = m0 + q * 32;
+      const int nrows = P.M - rbase < 32 ? static_cast<int>(P.M - rbase) : 32;
+      if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      __syncwarp();  // previous tile's copy-out / TMA store done with the buffer
+      // prefetch this warp's operand rows into the swizzled buffer (16 B cp.async,
+      // two rows per instruction), overlapped with the main loop
+      if (opkind) {
+        int32_t gi = 0;
+        if (opkind == 2 && lane < nrows) gi = P.gidx[rbase + lane];
+        const int half = lane >> 4, gcol = lane & 15;  // 16 granules = 64 columns per row
+        const int ch = gcol >> 3, g = gcol & 7;
+        for (int rr = half; rr < 32; rr += 2) {
+          const int32_t grow = __shfl_sync(0xffffffffu, gi, rr);
+          if (rr < nrows && n0 + gcol * 4 < P.N) {
+            const int64_t row = rbase + rr;
+            const float* src = opkind == 1 ? P.resid + row * P.ldr
+                             : opkind == 2 ? P.gsrc + static_cast<int64_t>(grow) * P.ldg
+                                           : P.aux + row * P.ldaux;
+            float* dst = ebuf + ch * 1024 + rr * 32 + ((g ^ (rr & 7)) << 2);
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src + n0 + gcol * 4)
+                         : "memory");
+          }
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+      }
       float acc[BN];
 #pragma unroll
       for (int i = 0; i < BN; ++i) acc[i] = 0.f;
-      const int nflush = nk * (BK / 8) / kFlush;
+      const int nsteps = nk * (BK / 8);
+      const int win = P.flush_steps > 0 ? P.flush_steps : nsteps;
+      const int nflush = nsteps > 0 ? (nsteps + win - 1) / win : 0;
       for (int j = 0; j < nflush; ++j, ++fcount) {
         const uint32_t b = fcount & 1;
         mbar_wait(&accf_bar[gr][b], (fcount >> 1) & 1);
@@ -410,76 +539,139 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_const
         __syncwarp();
         if (lane == 0) mbar_arrive(&acce_bar[gr][b]);
       }
-      if (nflush > 0) {
-#pragma unroll
-        for (int c = 0; c < BN; c += 16) {
-          float v[16];
-          tmem_ld16<16>(tg + 2 * BN + c, v);
-#pragma unroll
-          for (int i = 0; i < 16; ++i) acc[c + i] += v[i];
-        }
-        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-      }
-      asm volatile("tcgen05.fence::before_thread_sync;");
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&small_bar[gr]);
       if (q == 0 && gr == 0) EGN_TRACE(6, t);
-      // epilogue: per 32-column chunk, transpose through smem; lanes over columns,
-      // operand loads batched 8 rows deep
-      float* out_base = P.out + static_cast<int64_t>(z) * P.split_stride;
-      const int nrows = P.M - rbase < 32 ? static_cast<int>(P.M - rbase) : 32;
+      if (opkind) asm volatile("cp.async.wait_all;" ::: "memory");
+      __syncwarp();
+      if (q == 0 && gr == 0) EGN_TRACE(8, t);
+      // thread = row: combine with the operand in place.  Variant loops are
+      // hoisted so each unrolled body is branch-free; an additive bias is applied
+      // in the copy-out (lane = column), a bias under a product here.
+      const int fl = P.flags;
+      const bool has_bias = fl & EPI_BIAS;
+      const int variant = opkind == 0 ? 0 : (fl & (EPI_RESID | EPI_GATHER)) ? 1 : (fl & EPI_DSILU_AUX) ? 2 : 3;
+#define EGN_SLOT(c4) reinterpret_cast<float4*>(ebuf + ((c4) >> 3) * 1024 + epi_idx(lane, ((c4) & 7) * 4))
+#define EGN_ACC4(c4) make_float4(acc[(c4) * 4], acc[(c4) * 4 + 1], acc[(c4) * 4 + 2], acc[(c4) * 4 + 3])
+      const bool silu2 = fl & EPI_SILU_OUT2;
+      const bool tma_store = P.tma_out && variant <= 1 && !silu2;
+      if (tma_store && has_bias) {
+        // bias here (the TMA store has no lane = column pass); broadcast loads
 #pragma unroll
-      for (int c0 = 0; c0 < BN; c0 += 32) {
-        __syncwarp();
-#pragma unroll
-        for (int i = 0; i < 32; ++i) stile[lane * 33 + i] = acc[c0 + i];
-        __syncwarp();
-        const int col = n0 + c0 + lane;
-        if (col >= P.N) continue;
-        const float bv = (P.flags & EPI_BIAS) ? P.bias[col] : 0.f;
-        const float* sv = stile + lane;
-        float* dst = out_base + rbase * P.ldo + col;
-        float* dst2 = P.out2 ? P.out2 + rbase * P.ldo2 + col : nullptr;
-        const int64_t ldo = P.ldo, ldo2 = P.ldo2;
-        const bool silu2 = P.flags & EPI_SILU_OUT2;
-        for (int r0 = 0; r0 < nrows; r0 += 8) {
-          float o[8];
-          if (opkind) {
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-              const int64_t row = rbase + r0 + i;
-              o[i] = 0.f;
-              if (r0 + i < nrows)
-                o[i] = opkind == 1 ? P.resid[row * P.ldr + col]
-                     : opkind == 2 ? P.gsrc[static_cast<int64_t>(P.gidx[row]) * P.ldg + col]
-                                   : P.aux[row * P.ldaux + col];
-            }
+        for (int c4 = 0; c4 < BN / 4; ++c4) {
+          const int col = min(n0 + c4 * 4, P.N - 4);
+          const float4 bv = make_float4(__ldg(P.bias + col), __ldg(P.bias + col + 1), __ldg(P.bias + col + 2),
+                                        __ldg(P.bias + col + 3));
+          float4 a = EGN_ACC4(c4);
+          if (variant == 1) {
+            const float4 o = *EGN_SLOT(c4);
+            a.x += o.x; a.y += o.y; a.z += o.z; a.w += o.w;
           }
+          *EGN_SLOT(c4) = make_float4(a.x + bv.x, a.y + bv.y, a.z + bv.z, a.w + bv.w);
+        }
+      } else if (variant == 0) {
 #pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const int rr = r0 + i;
-            if (rr >= nrows) break;
-            float v = sv[rr * 33] + bv;
-            if (opkind == 1 || opkind == 2) v += o[i];
-            if (P.flags & EPI_DSILU_AUX) {
-              const float sg = 1.f / (1.f + __expf(-o[i]));
-              v *= sg * (1.f + o[i] * (1.f - sg));
+        for (int c4 = 0; c4 < BN / 4; ++c4) *EGN_SLOT(c4) = EGN_ACC4(c4);
+      } else if (variant == 1) {
+#pragma unroll
+        for (int c4 = 0; c4 < BN / 4; ++c4) {
+          const float4 o = *EGN_SLOT(c4);
+          const float4 a = EGN_ACC4(c4);
+          *EGN_SLOT(c4) = make_float4(a.x + o.x, a.y + o.y, a.z + o.z, a.w + o.w);
+        }
+      } else {
+        const bool dsl = variant == 2;
+#pragma unroll
+        for (int c4 = 0; c4 < BN / 4; ++c4) {
+          const float4 o = *EGN_SLOT(c4);
+          float4 a = EGN_ACC4(c4);
+          const int col = n0 + c4 * 4;
+          if (has_bias && col < P.N) {
+            a.x += __ldg(P.bias + col); a.y += __ldg(P.bias + col + 1);
+            a.z += __ldg(P.bias + col + 2); a.w += __ldg(P.bias + col + 3);
+          }
+          const float4 f = dsl ? make_float4(dsilu(o.x), dsilu(o.y), dsilu(o.z), dsilu(o.w)) : o;
+          *EGN_SLOT(c4) = make_float4(a.x * f.x, a.y * f.y, a.z * f.z, a.w * f.w);
+        }
+      }
+      if (tma_store) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) {
+          // [split][M][N] output map: rows >= M clip per split
+          tma_store_3d(&mapOut, ebuf, n0, static_cast<int>(rbase), z);
+          if (n0 + 32 < P.N) tma_store_3d(&mapOut, ebuf + 1024, n0 + 32, static_cast<int>(rbase), z);
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+        if (q == 0 && gr == 0) EGN_TRACE(9, t);
+        continue;
+      }
+      __syncwarp();
+      if (q == 0 && gr == 0) EGN_TRACE(9, t);
+      float* out_base = P.out + static_cast<int64_t>(z) * P.split_stride;
+      const int64_t ldo = P.ldo, ldo2 = P.ldo2;
+#pragma unroll
+      for (int ch = 0; ch < 2; ++ch) {
+        const int col = n0 + ch * 32 + lane;
+        if (col < P.N) {
+          const float b = (variant <= 1 && has_bias) ? __ldg(P.bias + col) : 0.f;
+          const float* src = ebuf + ch * 1024;
+          float* dst = out_base + rbase * ldo + col;
+          if (!silu2) {
+#pragma unroll 8
+            for (int rr = 0; rr < nrows; ++rr) dst[rr * ldo] = src[epi_idx(rr, lane)] + b;
+          } else {
+            float* dst2 = P.out2 + rbase * ldo2 + col;
+#pragma unroll 4
+            for (int rr = 0; rr < nrows; ++rr) {
+              const float v = src[epi_idx(rr, lane)] + b;
+              dst[rr * ldo] = v;
+              dst2[rr * ldo2] = __fdividef(v, 1.f + __expf(-v));
             }
-            if (P.flags & EPI_MUL_AUX) {
-              dst2[rr * ldo2] = v;
-              v *= o[i];
-            }
-            dst[rr * ldo] = v;
-            if (silu2) dst2[rr * ldo2] = v / (1.f + __expf(-v));
           }
         }
       }
+      if (q == 0 && gr == 0) EGN_TRACE(10, t);
+      if (variant == 3) {
+        // out2 = the pre-gate value acc + bias: second pass through the buffer
+        __syncwarp();
+#pragma unroll
+        for (int c4 = 0; c4 < BN / 4; ++c4) *EGN_SLOT(c4) = EGN_ACC4(c4);
+        __syncwarp();
+#pragma unroll
+        for (int ch = 0; ch < 2; ++ch) {
+          const int col = n0 + ch * 32 + lane;
+          if (col < P.N) {
+            const float b = has_bias ? __ldg(P.bias + col) : 0.f;
+            const float* src = ebuf + ch * 1024;
+            float* dst2 = P.out2 + rbase * ldo2 + col;
+#pragma unroll 8
+            for (int rr = 0; rr < nrows; ++rr) dst2[rr * ldo2] = src[epi_idx(rr, lane)] + b;
+          }
+        }
+      }
+#undef EGN_SLOT
+#undef EGN_ACC4
     }
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  }
+  if (P.trace && tid == 32) {
+    long long g;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+    P.trace[1025 + 4 * blockIdx.x] = g;
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
+  if (P.trace && tid == 32) {
+    long long g;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+    P.trace[1026 + 4 * blockIdx.x] = g;
+  }
   if (warp == 1) {
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
+  }
+  if (P.trace && tid == 32) {
+    long long g;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+    P.trace[1027 + 4 * blockIdx.x] = g;
   }
 }
 
@@ -501,32 +693,60 @@ static EncodeFn get_encode() {
   return fn;
 }
 
-// 2-D fp32 tensor map: `outer` rows of `inner` contiguous elements (row stride ld elements);
-// box = 32 (inner, 128 B) x box_outer, SWIZZLE_128B, zero fill out of bounds.
+// 2-D fp32 tensor maps (`outer` rows of `inner` contiguous elements, row stride ld),
+// zero fill out of bounds:
+//   kMapK     : box 32 (inner, 128 B) x box_outer, SWIZZLE_128B (K-major MMA operand)
+//   kMapMN    : box 32 x box_outer, SWIZZLE_128B_ATOM_32B (MN-major MMA operand)
+//   kMapPlain : box BM (inner) x box_outer, no swizzle (MN-major A, read by threads)
+enum MapKind { kMapK, kMapMN, kMapPlain };
 static int make_map(CUtensorMap* map, const float* ptr, int64_t outer, int64_t inner, int64_t ld, int box_outer,
-                    bool mn_major = false) {
+                    MapKind kind) {
   EncodeFn enc = get_encode();
   EGN_REQUIRE(enc != nullptr, "cuTensorMapEncodeTiled unavailable");
   EGN_REQUIRE((reinterpret_cast<uintptr_t>(ptr) & 15) == 0, "GEMM operand must be 16-byte aligned");
   EGN_REQUIRE((ld * 4) % 16 == 0, "GEMM operand row stride must be a multiple of 16 bytes");
   cuuint64_t dims[2] = {static_cast<cuuint64_t>(inner), static_cast<cuuint64_t>(outer)};
   cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld * 4)};
-  cuuint32_t box[2] = {32u, static_cast<cuuint32_t>(box_outer)};
+  cuuint32_t box[2] = {kind == kMapPlain ? static_cast<cuuint32_t>(BM) : 32u, static_cast<cuuint32_t>(box_outer)};
   cuuint32_t estr[2] = {1, 1};
+  const CUtensorMapSwizzle swz = kind == kMapK    ? CU_TENSOR_MAP_SWIZZLE_128B
+                                 : kind == kMapMN ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B
+                                                  : CU_TENSOR_MAP_SWIZZLE_NONE;
   CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(ptr), dims, strides, box, estr,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE,
-                   mn_major ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
-                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   EGN_REQUIRE(r == CUDA_SUCCESS, "cuTensorMapEncodeTiled failed (%d)", static_cast<int>(r));
   return 0;
 }
 
-template <int BN, bool AMN, bool BMN>
+constexpr int kGemmThreads = 448;
+
+// Output map [splits][M][N] (row stride ld, split stride M * ld), box 32 x 32 x 1,
+// SWIZZLE_128B: the epilogue buffer layout (16-byte granules XOR row % 8).
+static int make_out_map(CUtensorMap* map, const float* ptr, int64_t M, int N, int64_t ld, int splits) {
+  EncodeFn enc = get_encode();
+  EGN_REQUIRE(enc != nullptr, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[3] = {static_cast<cuuint64_t>(N), static_cast<cuuint64_t>(M), static_cast<cuuint64_t>(splits)};
+  cuuint64_t strides[2] = {static_cast<cuuint64_t>(ld * 4), static_cast<cuuint64_t>(M * ld * 4)};
+  cuuint32_t box[3] = {32u, 32u, 1u};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(ptr), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  EGN_REQUIRE(r == CUDA_SUCCESS, "cuTensorMapEncodeTiled (output) failed (%d)", static_cast<int>(r));
+  return 0;
+}
+
+// TMA stores need a 16-byte aligned base and row stride
+static bool out_map_ok(const float* out, int64_t ldo) {
+  return (reinterpret_cast<uintptr_t>(out) & 15) == 0 && (ldo * 4) % 16 == 0;
+}
+
+template <bool AMN, bool BMN>
 static int launch(const CUtensorMap& a0, const CUtensorMap& b0, const CUtensorMap& a1, const CUtensorMap& b1,
-                  const Params& P, int splits, cudaStream_t st) {
-  constexpr int STAGE = 2 * BM * BK * 4 + 2 * BN * BK * 4;
-  const size_t smem = static_cast<size_t>(3) * STAGE + 8 * 32 * 33 * 4 + 1024;
-  auto kern = gemm_tf32x3_kernel<BN, AMN, BMN>;
+                  const CUtensorMap& mo, const Params& P, int splits, cudaStream_t st) {
+  const size_t smem = kGemmSmem;
+  auto kern = gemm_tf32x3_kernel<AMN, BMN>;
   static bool configured = false;
   if (!configured) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
@@ -536,36 +756,41 @@ static int launch(const CUtensorMap& a0, const CUtensorMap& b0, const CUtensorMa
   const int tiles_n = (P.N + BN - 1) / BN;
   const int total = tiles_m * tiles_n * splits;
   const int grid = std::min(total, kNumSMs);
-  if (getenv("EGN_GEMM_TRACE")) {  // debug timeline of CTA 0 (ns since its first event)
+  if (getenv("EGN_GEMM_TRACE")) {  // debug timeline of CTA 0 (SM cycles since its first event)
     Params Q = P;
     long long* d = nullptr;
-    cudaMalloc(&d, 8 * 64 * sizeof(long long));
-    cudaMemset(d, 0, 8 * 64 * sizeof(long long));
+    cudaMalloc(&d, (1024 + 4 * kNumSMs) * sizeof(long long));
+    cudaMemset(d, 0, (1024 + 4 * kNumSMs) * sizeof(long long));
     Q.trace = d;
-    kern<<<grid, 448, smem, st>>>(a0, b0, a1, b1, Q, tiles_n, splits, total);
-    long long h[8 * 64];
+    kern<<<grid, kGemmThreads, smem, st>>>(a0, b0, a1, b1, mo, Q, tiles_n, splits, total);
+    long long h[1024 + 4 * kNumSMs];
     cudaStreamSynchronize(st);
     cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
+    {
+      long long g0 = h[1024], g1 = 0;
+      for (int c = 0; c < grid; ++c) g0 = std::min(g0, h[1024 + 4 * c]);
+      printf("cta entry/alloc/done/exit (us after first entry):");
+      for (int c = 0; c < grid; c += 8) {
+        printf("\n  %3d: %5.1f %5.1f %5.1f %5.1f", c, (h[1024 + 4 * c] - g0) * 1e-3, (h[1025 + 4 * c] - g0) * 1e-3,
+               (h[1026 + 4 * c] - g0) * 1e-3, (h[1027 + 4 * c] - g0) * 1e-3);
+      }
+      for (int c = 0; c < grid; ++c) g1 = std::max(g1, h[1027 + 4 * c]);
+      printf("\n  kernel span %.1f us\n", (g1 - g0) * 1e-3);
+    }
     cudaFree(d);
     long long t0 = h[0];
-    const char* names[8] = {"prod_issue", "mma_conv_ok", "conv_full_ok", "conv_done", "-", "acc0_flush", "epi0_start",
-                            "tile0_begin"};
-    for (int r = 0; r < 8; ++r) {
+    const char* names[11] = {"prod_issue", "mma_conv_ok", "conv_full_ok", "conv_done", "mma_issued", "acc0_flush",
+                             "epi0_start", "tile0_begin", "epi0_opwait", "epi0_rows", "epi0_out"};
+    for (int r = 0; r < 11; ++r) {
       printf("%-14s", names[r]);
-      for (int i = 0; i < 24; ++i) printf(" %7lld", h[r * 64 + i] ? (h[r * 64 + i] - t0) : -1);
+      for (int i = 0; i < 30; ++i) printf(" %6lld", h[r * 64 + i] ? (h[r * 64 + i] - t0) / 100 : -1);
       printf("\n");
     }
     fflush(stdout);
     return check_launch("gemm_tf32x3");
   }
-  kern<<<grid, 448, smem, st>>>(a0, b0, a1, b1, P, tiles_n, splits, total);
+  kern<<<grid, kGemmThreads, smem, st>>>(a0, b0, a1, b1, mo, P, tiles_n, splits, total);
   return check_launch("gemm_tf32x3");
-}
-
-template <bool AMN, bool BMN>
-static int launch_bn(int, const CUtensorMap& a0, const CUtensorMap& b0, const CUtensorMap& a1,
-                     const CUtensorMap& b1, const Params& P, int splits, cudaStream_t st) {
-  return launch<64, AMN, BMN>(a0, b0, a1, b1, P, splits, st);
 }
 
 __global__ void reduce_splits_kernel(const float* __restrict__ part, int splits, int64_t len, float* __restrict__ out,
@@ -596,13 +821,21 @@ __global__ void reduce_splits_kernel(const float* __restrict__ part, int splits,
 }
 
 static void wgrad_split(int64_t krows, int M, int N, int* splits, int* kbps) {
-  const int BNsel = 64;
-  const int tiles = static_cast<int>(((M + BM - 1) / BM) * ((N + BNsel - 1) / BNsel));
+  const int tiles = static_cast<int>(((M + BM - 1) / BM) * ((N + BN - 1) / BN));
   const int nk = static_cast<int>((krows + BK - 1) / BK);
   int want = std::max(1, kNumSMs / tiles);      // one wave of CTAs
   want = std::min(want, std::max(1, nk / 8));   // >= 8 k-blocks per CTA
   *kbps = (nk + want - 1) / want;
   *splits = (nk + *kbps - 1) / *kbps;
+}
+
+// k-steps per TMEM->register flush: long-K products (weight gradients over edge
+// rows) flush every few steps, short-K products once per tile.  EGN_GEMM_FLUSH /
+// EGN_GEMM_FLUSH_SHORT override for precision experiments.
+static int flush_window(bool long_k) {
+  static const int lw = [] { const char* e = std::getenv("EGN_GEMM_FLUSH"); return e ? std::atoi(e) : 4; }();
+  static const int sw = [] { const char* e = std::getenv("EGN_GEMM_FLUSH_SHORT"); return e ? std::atoi(e) : 2; }();
+  return long_k ? lw : sw;
 }
 
 }  // namespace gemm
@@ -622,21 +855,26 @@ extern "C" int egn_gemm(int64_t M, int N, int nseg, const float* a0, int64_t lda
   if (M == 0) return 0;
   Params P{M, N, nseg, k0, nseg > 1 ? k1 : 0, bias, resid, ldr, gsrc, gidx, ldg, aux, ldaux, flags, out, ldo, out2,
            ldo2, 0, 0};
-  const int BNsel = 64;
+  P.flush_steps = (k0 + (nseg > 1 ? k1 : 0)) > 512 ? flush_window(true) : flush_window(false);
   CUtensorMap ma0, mb0, ma1, mb1;
   // A: K-major [M, K]; B: K-major [N, K] (weights (out, in)) or MN-major [K, N] (b_mn)
-  if (int rc = make_map(&ma0, a0, M, k0, lda0, BM)) return rc;
-  if (int rc = b_mn ? make_map(&mb0, b0, k0, N, ldb0, BK, true) : make_map(&mb0, b0, N, k0, ldb0, BNsel)) return rc;
+  if (int rc = make_map(&ma0, a0, M, k0, lda0, BM, kMapK)) return rc;
+  if (int rc = b_mn ? make_map(&mb0, b0, k0, N, ldb0, BK, kMapMN) : make_map(&mb0, b0, N, k0, ldb0, BN, kMapK)) return rc;
   if (nseg > 1) {
-    if (int rc = make_map(&ma1, a1, M, k1, lda1, BM)) return rc;
-    if (int rc = b_mn ? make_map(&mb1, b1, k1, N, ldb1, BK, true) : make_map(&mb1, b1, N, k1, ldb1, BNsel)) return rc;
+    if (int rc = make_map(&ma1, a1, M, k1, lda1, BM, kMapK)) return rc;
+    if (int rc = b_mn ? make_map(&mb1, b1, k1, N, ldb1, BK, kMapMN) : make_map(&mb1, b1, N, k1, ldb1, BN, kMapK)) return rc;
   } else {
     ma1 = ma0;
     mb1 = mb0;
   }
+  CUtensorMap mo = ma0;
+  if (out_map_ok(out, ldo) && !(flags & (EPI_SILU_OUT2 | EPI_MUL_AUX))) {
+    if (int rc = make_out_map(&mo, out, M, N, ldo, 1)) return rc;
+    P.tma_out = 1;
+  }
   cudaStream_t st = as_stream(stream);
-  if (b_mn) return launch_bn<false, true>(BNsel, ma0, mb0, ma1, mb1, P, 1, st);
-  return launch_bn<false, false>(BNsel, ma0, mb0, ma1, mb1, P, 1, st);
+  if (b_mn) return launch<false, true>(ma0, mb0, ma1, mb1, mo, P, 1, st);
+  return launch<false, false>(ma0, mb0, ma1, mb1, mo, P, 1, st);
 }
 
 extern "C" int64_t egn_gemm_wgrad_workspace_bytes(int64_t krows, int M, int N) {
@@ -656,15 +894,19 @@ extern "C" int egn_gemm_wgrad(int64_t krows, int M, int N, const float* g, int64
   }
   int splits, kbps;
   wgrad_split(krows, M, N, &splits, &kbps);
-  const int BNsel = 64;
   float* part = reinterpret_cast<float*>(workspace);
   Params P{M, N, 1, static_cast<int>(krows), 0, nullptr, nullptr, 0, nullptr, nullptr, 0, nullptr, 0, 0,
-           part, N, nullptr, 0, kbps, static_cast<int64_t>(M) * N};
+           part, N, nullptr, 0, kbps, flush_window(true), 0, static_cast<int64_t>(M) * N};
   CUtensorMap ma, mb;
   // A = g^T: g is [krows, M] with M contiguous (MN-major); B = x^T likewise
-  if (int rc = make_map(&ma, g, krows, M, ldg, BK, true)) return rc;
-  if (int rc = make_map(&mb, x, krows, N, ldx, BK, true)) return rc;
-  if (int rc = launch_bn<true, true>(BNsel, ma, mb, ma, mb, P, splits, st)) return rc;
+  if (int rc = make_map(&ma, g, krows, M, ldg, BK, kMapPlain)) return rc;
+  if (int rc = make_map(&mb, x, krows, N, ldx, BK, kMapMN)) return rc;
+  CUtensorMap mo = ma;
+  if (out_map_ok(part, N)) {
+    if (int rc = make_out_map(&mo, part, M, N, N, splits)) return rc;
+    P.tma_out = 1;
+  }
+  if (int rc = launch<true, true>(ma, mb, ma, mb, mo, P, splits, st)) return rc;
   const int64_t len = static_cast<int64_t>(M) * N;
   reduce_splits_kernel<<<static_cast<int>(std::min<int64_t>((len + 31) / 32, 4096)), 256, 0, st>>>(part, splits, len, out, accumulate);
   return check_launch("gemm_wgrad_reduce");

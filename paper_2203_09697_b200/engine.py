@@ -250,7 +250,7 @@ class Engine:
             else:
                 S_bar = Y_bar * st["g"]
                 g_bar = Y_bar * st["S"]
-            torch.mm(g_bar.t(), fw.rbf, out=gr[p + "tu.rbf_gate"])  # N = k_rbf (6): cuBLAS
+            ops.wgrad(g_bar, fw.rbf, out=gr[p + "tu.rbf_gate"])  # N = k_rbf (6): split-K
             rbf_bar.addmm_(g_bar, w[p + "tu.rbf_gate"])
             X_bar, Wk_bar = ops.triplet_bwd(bg.edge_ptr, bg.rev, bg.geo, st["X"], st["Wk"], c.cutoff,
                                             S_bar, eg, max_degree=bg.max_deg)
@@ -266,7 +266,7 @@ class Engine:
             wg(down_bar, st["m"], gr[p + "tu.down"])
             m_bar = L(down_bar, w[p + "tu.down"], w_mn=True, resid=m_in_bar)
         # edge init (engine.py:109-111), K = k_rbf: cuBLAS
-        torch.mm(m_bar.t(), fw.rbf, out=gr["edge_init.w"])
+        ops.wgrad(m_bar, fw.rbf, out=gr["edge_init.w"])
         cs(m_bar, out=gr["edge_init.b"])
         rbf_bar.addmm_(m_bar, w["edge_init.w"])
         ops.rbf_bwd(bg.geo, rbf_bar, c.cutoff, eg)
