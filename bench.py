@@ -235,8 +235,19 @@ def _kernel_roofline(tr, bg, cfg):
     fma = 2.0 * nt * cfg.l_sbf * dg
     dominant = "triplet_bwd" if t_b >= t_f else "triplet_fwd"
     ach = (b_bwd / t_b if dominant == "triplet_bwd" else b_fwd / t_f) / 1e9
+    # DRAM traffic of the same kernel from the committed ncu capture (same workload only)
+    traffic = None
+    tpath = ROOT / "profiles" / "r1_traffic.json"
+    if tpath.exists():
+        tj = json.loads(tpath.read_text())
+        if tj.get("workload", {}).get("edges") == ne and tj.get("workload", {}).get("triplets") == nt:
+            rec = tj.get(dominant, {})
+            traffic = rec.get("dram_read", 0) + rec.get("dram_write", 0) or None
+    fp32_peak = 148 * 128 * 2 * 1.965e9  # FFMA pipe: the bound of this formulation
     return {"bound": "hbm", "kernel": dominant, "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
-            "traffic": None, "peak_source": "MEASURED_PEAKS.json" if peaks else "fallback",
+            "traffic": traffic, "traffic_source": "profiles/r1_traffic.json (ncu --set full)" if traffic else None,
+            "fp32_pipe_frac": (2 * fma / t_b if dominant == "triplet_bwd" else fma / t_f) / fp32_peak,
+            "peak_source": "MEASURED_PEAKS.json" if peaks else "fallback",
             "triplet_fwd_us": t_f * 1e6, "triplet_bwd_us": t_b * 1e6,
             "triplet_fwd_gtrip_s": nt / t_f / 1e9, "triplet_bwd_gtrip_s": nt / t_b / 1e9,
             "triplet_fwd_fp32_tflops": fma / t_f / 1e12, "triplet_bwd_fp32_tflops": 2 * fma / t_b / 1e12,

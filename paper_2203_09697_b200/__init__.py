@@ -17,7 +17,8 @@ __all__ = [
     "param_specs", "save_params", "zero_params", "CenterPartition", "CommModel", "CommVolume",
     "GraphPartition", "comm_volume", "partition_centers", "partition_graph", "split_range",
     "AtomicSystem", "random_cloud", "build_graph", "build_batch", "EGNModel", "predict",
-    "loss_and_grads", "train_simple", "Trainer",
+    "loss_and_grads", "train_simple", "Trainer", "enumerate_triplets", "WorkerGroup", "ParallelRunResult",
+    "GradientBundle", "CollectiveShapeError", "CollectiveTimeoutError", "WorkerGroupError",
 ]
 
 
@@ -33,6 +34,10 @@ def __getattr__(name):
     if name in ("predict", "loss_and_grads", "train_simple", "Trainer"):
         from . import tasks
         return getattr(tasks, name)
+    if name in ("WorkerGroup", "ParallelRunResult", "GradientBundle", "CollectiveError", "CollectiveShapeError",
+                "CollectiveTimeoutError", "WorkerGroupError", "GraphParallelEngine", "GPTrainer"):
+        from . import runtime
+        return getattr(runtime, name)
     if name in ("Engine", "DeviceWeights"):
         from . import engine
         return getattr(engine, name)
