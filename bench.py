@@ -278,8 +278,13 @@ def run_ours(args, wl):
             dist.init_process_group(backend)
     cfg = _config(wl)
     graphs = args.graphs or wl["graphs"]
-    # weak scaling: every rank contributes `graphs` graphs to the global batch
-    systems = [s for r in range(world) for s in _systems(wl, graphs, r)]
+    aligned = world == 1 or args.partition == "aligned"
+    # weak scaling: every rank contributes `graphs` graphs to the global batch.  With the
+    # graph-aligned partition a rank builds and owns only its own graphs.
+    if aligned:
+        systems = _systems(wl, graphs, rank)
+    else:
+        systems = [s for r in range(world) for s in _systems(wl, graphs, r)]
     params = init_params(cfg)
     bg = build_batch(systems, cfg.cutoff)
     teacher = Engine(DeviceWeights.from_params(init_params(cfg.replace(seed=1))))
@@ -291,6 +296,12 @@ def run_ours(args, wl):
         tr = Trainer(params, None, e_t, f_t, 1.0, wl["w_forces"], graph=bg)
         comm = None
         parallelism = "single"
+    elif aligned:
+        # graph-aligned centre partition: no halo, one gradient all-reduce per step
+        comm = DistComm()
+        tr = Trainer(params, None, e_t, f_t, 1.0, wl["w_forces"], graph=bg, comm=comm,
+                     global_graphs=graphs * world)
+        parallelism = f"gp{world} (graph-aligned centre partition: no halo, gradient all-reduce, {backend})"
     else:
         comm = DistComm()
         cand = bg.graph_ptr.cpu().numpy() if args.partition == "aligned" else None
@@ -338,7 +349,7 @@ def run_ours(args, wl):
         et = et_host.to("cuda", non_blocking=True)
         ft = ft_host.to("cuda", non_blocking=True) if ft_host is not None else None
         g = build_batch(None, cfg.cutoff, positions=pos, sizes=sizes)
-        if world == 1:
+        if aligned:
             tr.set_inputs(g, et, ft)
         else:
             n0, n1 = tr.engine.n0, tr.engine.n1
@@ -360,12 +371,15 @@ def run_ours(args, wl):
     if world > 1:
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
     t_dev, t_e2e = float(tt[0]), float(tt[1])
-    total_trip = bg.num_triplets * cfg.blocks  # global batch (all ranks)
+    nt = torch.tensor([float(bg.num_triplets), float(bg.num_edges)], dtype=torch.float64, device="cuda")
+    if world > 1 and aligned:
+        dist.all_reduce(nt)  # each rank holds its own graphs
+    total_trip = float(nt[0]) * cfg.blocks  # global batch (all ranks)
     value = total_trip / t_dev
     roof = None
     if rank == 0 and not args.no_kernel_timing:
-        rb = bg if world == 1 else build_batch(systems[:graphs], cfg.cutoff)
-        if world > 1:
+        rb = bg if aligned else build_batch(systems[:graphs], cfg.cutoff)
+        if not aligned:
             rtr = Trainer(params, None, e_t[:graphs], None, 1.0, 0.0, graph=rb)
         else:
             rtr = tr
@@ -383,8 +397,8 @@ def run_ours(args, wl):
             "data": "synthetic (random_cloud OC20-density graphs, random-init weights, teacher targets)",
             "config": {"workload": args.workload, "variant": wl["variant"], "graphs_per_gpu": graphs,
                        "atoms_per_graph": wl["atoms"], "cutoff": wl["cutoff"], "blocks": cfg.blocks,
-                       "d_e": cfg.d_e, "d_t": cfg.d_t, "d_bil": cfg.d_bil, "edges_total": bg.num_edges,
-                       "triplets_total": bg.num_triplets, "parallelism": parallelism,
+                       "d_e": cfg.d_e, "d_t": cfg.d_t, "d_bil": cfg.d_bil, "edges_total": int(nt[1]),
+                       "triplets_total": int(nt[0]), "parallelism": parallelism,
                        "l2": "step working set > L2 (126 MB); kernel timings flush L2 with a 256 MB write"},
             "steps_per_s": 1.0 / t_dev,
             "e2e": {"value": total_trip / t_e2e, "unit": "triplets/s", "h2d_bytes_per_step": h2d,

@@ -213,11 +213,14 @@ int egn_gemm(int64_t M, int N, int nseg, const float* a0, int64_t lda0, const fl
              const int32_t* gidx, int64_t ldg, const float* aux, int64_t ldaux, int flags,
              float* out, int64_t ldo, float* out2, int64_t ldo2, int b_mn, egn_stream_t stream);
 
-/* Weight gradient out[M, N] (+)= g^T x with g [krows, M], x [krows, N] (both MN-major on the
- * tensor cores), split over krows across CTAs; partial tiles reduced in a fixed order. */
+/* Weight gradient out[M, N] (row stride ldo) (+)= g^T x with g [krows, M], x [krows, N] (both
+ * MN-major on the tensor cores), split over krows across CTAs; partial tiles reduced in a fixed
+ * order.  If g_colsum is non-NULL it also receives (+=) the column sums of g, i.e. the bias
+ * adjoint of the same linear (tape.py:113-119), read from the operand tiles already on chip. */
 int64_t egn_gemm_wgrad_workspace_bytes(int64_t krows, int M, int N);
 int egn_gemm_wgrad(int64_t krows, int M, int N, const float* g, int64_t ldg, const float* x,
-                   int64_t ldx, float* out, int accumulate, void* workspace, egn_stream_t stream);
+                   int64_t ldx, float* out, int64_t ldo, float* g_colsum, int accumulate,
+                   void* workspace, egn_stream_t stream);
 
 /* ------------------------------------------------------------------ */
 /* Optimizer: train_simple SGD update (tasks.py:207-208)               */

@@ -55,7 +55,7 @@ SIGNATURES: dict[str, tuple] = {
     "egn_gemm": (_i32, [_i64, _i32, _i32, _p, _i64, _p, _i64, _i32, _p, _i64, _p, _i64, _i32, _p, _p, _i64, _p,
                         _p, _i64, _p, _i64, _i32, _p, _i64, _p, _i64, _i32, _p]),
     "egn_gemm_wgrad_workspace_bytes": (_i64, [_i64, _i32, _i32]),
-    "egn_gemm_wgrad": (_i32, [_i64, _i32, _i32, _p, _i64, _p, _i64, _p, _i32, _p, _p]),
+    "egn_gemm_wgrad": (_i32, [_i64, _i32, _i32, _p, _i64, _p, _i64, _p, _i64, _p, _i32, _p, _p]),
     "egn_sgd": (_i32, [_p, _p, _i64, _f32, _p]),
 }
 

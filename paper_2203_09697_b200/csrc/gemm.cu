@@ -65,6 +65,7 @@ struct Params {
   int kb_per_split;        // split-K: k-blocks per blockIdx.z (0 = all)
   int flush_steps;         // k-steps (of 8) per TMEM->register flush (0 = whole tile)
   int tma_out;             // single-output epilogues store through mapOut (TMA)
+  float* gsum_part;        // wgrad: per-split column sums of g (rows of A), [splits][M], or null
   int64_t split_stride;    // split-K: elements between partial outputs
   long long* trace;        // debug timeline (EGN_GEMM_TRACE), CTA 0 only
 };
@@ -416,7 +417,8 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_const
     for (int item = blockIdx.x; item < total_items; item += gridDim.x) {
       int64_t m0;
       int n0, kbeg, nk;
-      item_coords(item, m0, n0, kbeg, nk);
+      const int z = item_coords(item, m0, n0, kbeg, nk);
+      float gs = 0.f;  // wgrad: sum over this split's rows of A row r (= column r of g)
       for (int kbl = 0; kbl < nk; ++kbl, ++it) {
         const int s = it % kTmaRing;
         const int o = it % kOpRing;
@@ -440,6 +442,7 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_const
               const int gran = h * 4 + g;
               v = *reinterpret_cast<const float4*>(st + r * 128 + ((gran ^ (r & 7)) << 4));
             }
+            if (AMN) gs += (v.x + v.y) + (v.z + v.w);
             hi[g * 4 + 0] = tf32_rna_int(v.x);
             hi[g * 4 + 1] = tf32_rna_int(v.y);
             hi[g * 4 + 2] = tf32_rna_int(v.z);
@@ -473,6 +476,7 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_const
           mbar_arrive(&op_full[o]);
         }
       }
+      if (AMN && P.gsum_part != nullptr && n0 == 0 && m0 + r < P.M) P.gsum_part[z * P.M + m0 + r] = gs;
     }
   } else {
     // ---------------- accumulator groups + epilogue (thread = tile row)
@@ -793,28 +797,38 @@ static int launch(const CUtensorMap& a0, const CUtensorMap& b0, const CUtensorMa
   return check_launch("gemm_tf32x3");
 }
 
-__global__ void reduce_splits_kernel(const float* __restrict__ part, int splits, int64_t len, float* __restrict__ out,
-                                     int accumulate) {
+// Fixed-order sum of the split-K partials: elements [0, len) of the [splits][M][N]
+// matrix partials go to out (row stride ldo), elements [len, len + mg) of the
+// [splits][M] column-sum partials go to gout.
+__global__ void reduce_splits_kernel(const float* __restrict__ part, int splits, int64_t len, int n,
+                                     float* __restrict__ out, int64_t ldo, const float* __restrict__ gpart, int mg,
+                                     float* __restrict__ gout, int accumulate) {
   __shared__ float red[8][33];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  for (int64_t base = static_cast<int64_t>(blockIdx.x) * 32; base < len; base += static_cast<int64_t>(gridDim.x) * 32) {
+  const int64_t total = len + mg;
+  for (int64_t base = static_cast<int64_t>(blockIdx.x) * 32; base < total;
+       base += static_cast<int64_t>(gridDim.x) * 32) {
     const int64_t i = base + lane;
+    const bool second = i >= len;
+    const float* src = second ? gpart + (i - len) : part + i;
+    const int64_t stride = second ? mg : len;
     float s0 = 0.f, s1 = 0.f;
-    if (i < len) {
+    if (i < total) {
       int z = w;
       for (; z + 8 < splits; z += 16) {
-        s0 += part[z * len + i];
-        s1 += part[(z + 8) * len + i];
+        s0 += src[z * stride];
+        s1 += src[(z + 8) * stride];
       }
-      if (z < splits) s0 += part[z * len + i];
+      if (z < splits) s0 += src[z * stride];
     }
     red[w][lane] = s0 + s1;
     __syncthreads();
-    if (w == 0 && i < len) {
+    if (w == 0 && i < total) {
       float s = 0.f;
 #pragma unroll
       for (int k = 0; k < 8; ++k) s += red[k][lane];
-      out[i] = accumulate ? out[i] + s : s;
+      float* dst = second ? gout + (i - len) : out + (i / n) * ldo + (i % n);
+      *dst = accumulate ? *dst + s : s;
     }
     __syncthreads();
   }
@@ -880,23 +894,28 @@ extern "C" int egn_gemm(int64_t M, int N, int nseg, const float* a0, int64_t lda
 extern "C" int64_t egn_gemm_wgrad_workspace_bytes(int64_t krows, int M, int N) {
   int splits, kbps;
   egn::gemm::wgrad_split(krows, M, N, &splits, &kbps);
-  return static_cast<int64_t>(splits) * M * N * 4;
+  return static_cast<int64_t>(splits) * M * N * 4 + static_cast<int64_t>(splits) * M * 4;
 }
 
 extern "C" int egn_gemm_wgrad(int64_t krows, int M, int N, const float* g, int64_t ldg, const float* x,
-                              int64_t ldx, float* out, int accumulate, void* workspace, egn_stream_t stream) {
+                              int64_t ldx, float* out, int64_t ldo, float* g_colsum, int accumulate,
+                              void* workspace, egn_stream_t stream) {
   using namespace egn::gemm;
   EGN_REQUIRE(M >= 1 && N >= 16 && N % 16 == 0, "wgrad needs N % 16 == 0 (got %d)", N);
+  EGN_REQUIRE(ldo >= N, "wgrad output row stride must be >= N");
   cudaStream_t st = as_stream(stream);
   if (krows == 0) {
-    if (!accumulate) cudaMemsetAsync(out, 0, sizeof(float) * M * N, st);
+    if (!accumulate) {
+      cudaMemset2DAsync(out, sizeof(float) * ldo, 0, sizeof(float) * N, M, st);
+      if (g_colsum) cudaMemsetAsync(g_colsum, 0, sizeof(float) * M, st);
+    }
     return check_launch("gemm_wgrad_empty");
   }
   int splits, kbps;
   wgrad_split(krows, M, N, &splits, &kbps);
   float* part = reinterpret_cast<float*>(workspace);
   Params P{M, N, 1, static_cast<int>(krows), 0, nullptr, nullptr, 0, nullptr, nullptr, 0, nullptr, 0, 0,
-           part, N, nullptr, 0, kbps, flush_window(true), 0, static_cast<int64_t>(M) * N};
+           part, N, nullptr, 0, kbps, flush_window(true), 0, nullptr, static_cast<int64_t>(M) * N};
   CUtensorMap ma, mb;
   // A = g^T: g is [krows, M] with M contiguous (MN-major); B = x^T likewise
   if (int rc = make_map(&ma, g, krows, M, ldg, BK, kMapPlain)) return rc;
@@ -906,8 +925,12 @@ extern "C" int egn_gemm_wgrad(int64_t krows, int M, int N, const float* g, int64
     if (int rc = make_out_map(&mo, part, M, N, N, splits)) return rc;
     P.tma_out = 1;
   }
+  float* gpart = part + static_cast<int64_t>(splits) * M * N;
+  P.gsum_part = g_colsum ? gpart : nullptr;
   if (int rc = launch<true, true>(ma, mb, ma, mb, mo, P, splits, st)) return rc;
   const int64_t len = static_cast<int64_t>(M) * N;
-  reduce_splits_kernel<<<static_cast<int>(std::min<int64_t>((len + 31) / 32, 4096)), 256, 0, st>>>(part, splits, len, out, accumulate);
+  const int mg = g_colsum ? M : 0;
+  reduce_splits_kernel<<<static_cast<int>(std::min<int64_t>((len + mg + 31) / 32, 4096)), 256, 0, st>>>(
+      part, splits, len, N, out, ldo, gpart, mg, g_colsum, accumulate);
   return check_launch("gemm_wgrad_reduce");
 }

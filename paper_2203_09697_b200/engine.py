@@ -16,9 +16,12 @@ The backward is written out explicitly (no autograd), mirroring the
 reference's reverse walk; geometry adjoints accumulate into one per-edge
 float4 (dE/dv_e, dE/dd_e) that a final CSR gather turns into dE/dx.
 
-Dense products use fp32 GEMMs with TF32 disabled (torch.mm -> cuBLAS); the
-graph-structured work (neighbour list, basis, triplet interaction, segment
-sums, force head, geometry adjoints, SGD) runs in the native library.
+Edge- and node-sized dense products run on the native tcgen05 3xTF32 GEMM
+(ops.linear / ops.linear_wgrad, fused epilogues, bias adjoints folded into the
+weight-gradient kernel); only the K = k_rbf (6) products and the G-row global
+stage use cuBLAS fp32.  The graph-structured work (neighbour list, basis,
+triplet interaction, segment sums, force head, geometry adjoints, SGD) runs in
+the native library.
 """
 
 from __future__ import annotations
@@ -209,34 +212,28 @@ class Engine:
                 t = L(m_bar, w[p + "sym.w"], w_mn=True)
                 m2_bar = ops.gather_rows(bg.rev, t, out=m_bar.clone(), accumulate=True)
                 # EU2 (engine.py:180-192)
-                wg(m2_bar, st["a2"], gr[p + "eu2.w2"])
-                cs(m2_bar, out=gr[p + "eu2.b2"])
+                wg(m2_bar, st["a2"], gr[p + "eu2.w2"], gr[p + "eu2.b2"])
                 h2_bar = L(m2_bar, w[p + "eu2.w2"], w_mn=True, aux=st["h2"], flags=ops.EPI_DSILU_AUX)
-                cs(h2_bar, out=gr[p + "eu2.b1"])
                 w1 = w[p + "eu2.w1"]
-                gr[p + "eu2.w1"][:, :de].copy_(wg(h2_bar, st["m_new"], torch.empty_like(w1[:, :de])))
+                wg(h2_bar, st["m_new"], gr[p + "eu2.w1"][:, :de], gr[p + "eu2.b1"])
                 pv_bar = ops.aggregate_in_edges(bg.edge_ptr, bg.rev, h2_bar)
-                gr[p + "eu2.w1"][:, de:].copy_(wg(pv_bar, st["v"], torch.empty_like(w1[:, de:])))
+                wg(pv_bar, st["v"], gr[p + "eu2.w1"][:, de:])
                 v_bar = L(pv_bar, w1[:, de:].contiguous(), w_mn=True, resid=v_bar)
                 m_new_bar = L(h2_bar, w1[:, :de].contiguous(), w_mn=True, resid=m2_bar)
             else:
                 m_new_bar = m_bar.clone()
             # EA + NU (engine.py:166-177)
-            wg(v_bar, st["av"], gr[p + "nu.w2"])
-            cs(v_bar, out=gr[p + "nu.b2"])
+            wg(v_bar, st["av"], gr[p + "nu.w2"], gr[p + "nu.b2"])
             hv_bar = L(v_bar, w[p + "nu.w2"], w_mn=True, aux=st["hv"], flags=ops.EPI_DSILU_AUX)
-            cs(hv_bar, out=gr[p + "nu.b1"])
-            wg(hv_bar, st["agg"], gr[p + "nu.w1"])
+            wg(hv_bar, st["agg"], gr[p + "nu.w1"], gr[p + "nu.b1"])
             agg_bar = L(hv_bar, w[p + "nu.w1"], w_mn=True)
             ops.gather_rows(bg.recv, agg_bar, out=m_new_bar, accumulate=True)
             # EU (engine.py:152-158)
-            wg(m_new_bar, st["a1"], gr[p + "eu.w2"])
-            cs(m_new_bar, out=gr[p + "eu.b2"])
+            wg(m_new_bar, st["a1"], gr[p + "eu.w2"], gr[p + "eu.b2"])
             h_bar = L(m_new_bar, w[p + "eu.w2"], w_mn=True, aux=st["h"], flags=ops.EPI_DSILU_AUX)
-            cs(h_bar, out=gr[p + "eu.b1"])
             w1 = w[p + "eu.w1"]
-            gr[p + "eu.w1"][:, :de].copy_(wg(h_bar, st["m"], torch.empty_like(w1[:, :de])))
-            gr[p + "eu.w1"][:, de:].copy_(wg(h_bar, st["ta"], torch.empty_like(w1[:, de:])))
+            wg(h_bar, st["m"], gr[p + "eu.w1"][:, :de], gr[p + "eu.b1"])
+            wg(h_bar, st["ta"], gr[p + "eu.w1"][:, de:])
             m_in_bar = L(h_bar, w1[:, :de].contiguous(), w_mn=True, resid=m_new_bar)
             ta_bar = L(h_bar, w1[:, de:].contiguous(), w_mn=True)
             # TU (engine.py:118-149)

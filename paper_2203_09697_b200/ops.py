@@ -293,17 +293,22 @@ def gemm(a, b, a2=None, b2=None, bias=None, resid=None, gather=None, aux=None, f
     return (out, out2) if need2 else out
 
 
-def gemm_wgrad(g, x, out=None, accumulate=False):
-    """out[M, N] (+)= g^T x for g [R, M], x [R, N] on the tensor cores (split over R)."""
+def gemm_wgrad(g, x, out=None, accumulate=False, colsum=None):
+    """out[M, N] (+)= g^T x for g [R, M], x [R, N] on the tensor cores (split over R);
+    out may be a row-strided view.  colsum [M] (+)= column sums of g (the bias adjoint)."""
     g, x = _rowmajor(g), _rowmajor(x)
     R, M = g.shape
     N = x.shape[1]
     if out is None:
         out = torch.empty((M, N), dtype=torch.float32, device=g.device)
+    if out.stride(1) != 1:
+        raise ValueError("gemm_wgrad output rows must be contiguous")
+    if colsum is not None and not colsum.is_contiguous():
+        raise ValueError("gemm_wgrad column-sum output must be contiguous")
     nbytes = call("egn_gemm_wgrad_workspace_bytes", R, M, N)
     ws = _workspace_named("wgrad", nbytes, g.device)
-    call("egn_gemm_wgrad", R, M, N, ptr(g), g.stride(0), ptr(x), x.stride(0), ptr(out), int(accumulate), ptr(ws),
-         stream())
+    call("egn_gemm_wgrad", R, M, N, ptr(g), g.stride(0), ptr(x), x.stride(0), ptr(out), out.stride(0),
+         ptr(colsum) if colsum is not None else None, int(accumulate), ptr(ws), stream())
     return out
 
 
@@ -357,11 +362,13 @@ def linear(a, w, a2=None, w2=None, bias=None, resid=None, gather=None, aux=None,
     return y
 
 
-def linear_wgrad(g, x, out):
-    """out = g^T x (weight gradient over all rows)."""
-    if _tc_ok(4, x.shape[1], g, x) and out.is_contiguous():
-        return gemm_wgrad(g, x, out=out)
+def linear_wgrad(g, x, out, bias_out=None):
+    """out = g^T x (weight gradient over all rows); bias_out = column sums of g."""
+    if _tc_ok(4, x.shape[1], g, x) and out.stride(1) == 1:
+        return gemm_wgrad(g, x, out=out, colsum=bias_out)
     out.copy_(g.t() @ x)
+    if bias_out is not None:
+        column_sum(g, out=bias_out)
     return out
 
 

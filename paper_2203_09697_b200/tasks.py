@@ -59,7 +59,12 @@ class Trainer:
     """Device-resident SGD training step over a fixed batch (train_simple's inner loop)."""
 
     def __init__(self, params: ModelParams, systems, e_target, f_target=None, w_energy=1.0,
-                 w_forces=0.0, device="cuda", graph: BatchGraph | None = None):
+                 w_forces=0.0, device="cuda", graph: BatchGraph | None = None, comm=None,
+                 global_graphs: int | None = None):
+        """comm / global_graphs: graph-aligned graph parallelism.  Every rank owns
+        whole graphs (its own BatchGraph), so no edge or node crosses a rank; the
+        loss is normalised over the global batch (egn/tasks.py:158-185) and the
+        flat gradient buffer and the loss are all-reduced before the SGD update."""
         c = params.config
         if w_forces != 0.0 and c.variant != GEMNET:
             raise ValueError("force-loss gradients require the force-centric variant; "
@@ -69,9 +74,10 @@ class Trainer:
         self.engine = Engine(self.weights)
         self.bg = graph if graph is not None else build_batch(systems, c.cutoff, device)
         bg = self.bg
-        self.n = bg.num_graphs
+        self.n = bg.num_graphs if global_graphs is None else int(global_graphs)
         if self.n == 0:
             raise ValueError("dataset is empty")
+        self.comm = comm
         self.e_target = torch.as_tensor(np.asarray(e_target, dtype=np.float64), device=bg.device)
         self.f_target = (torch.as_tensor(np.asarray(f_target, dtype=np.float64), device=bg.device)
                          if f_target is not None else None)
@@ -94,6 +100,10 @@ class Trainer:
 
     def step(self, lr: float) -> torch.Tensor:
         loss = self.loss_and_grads()
+        if self.comm is not None:
+            self.comm.all_reduce_(self.weights.grad_flat, phase="backward", block=-1, stage="params",
+                                  level="global")
+            self.comm.all_reduce_(loss, phase="backward", block=-1, stage="loss", level="global")
         if lr != 0.0:
             self.weights.sgd_(lr)
         return loss

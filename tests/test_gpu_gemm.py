@@ -110,3 +110,24 @@ def test_strided_operands_and_errors():
         ops.gemm(torch.randn((10, 6), device="cuda"), torch.randn((16, 6), device="cuda"))  # K % 4
     with pytest.raises(ValueError):
         ops.gemm(torch.randn((10, 8), device="cuda"), torch.randn((12, 8), device="cuda"))  # N % 16
+
+
+@pytest.mark.parametrize("R,M,N", [(58644, 128, 128), (1000, 64, 256), (77, 32, 16)])
+def test_wgrad_fused_column_sums_and_strided_out(R, M, N):
+    """egn_gemm_wgrad with g_colsum (bias adjoint from the same operand tiles) and a
+    row-strided destination (a column block of a wider weight gradient)."""
+    from paper_2203_09697_b200 import ops
+
+    torch.manual_seed(R)
+    gr = torch.randn((R, M), device="cuda")
+    x = torch.randn((R, N), device="cuda")
+    big = torch.full((M, N + 48), float("nan"), device="cuda")
+    cs = torch.full((M,), float("nan"), device="cuda")
+    ops.gemm_wgrad(gr, x, out=big[:, 16:16 + N], colsum=cs)
+    ref = gr.double().t() @ x.double()
+    assert _rel(big[:, 16:16 + N], ref) < TOL
+    assert torch.isnan(big[:, :16]).all() and torch.isnan(big[:, 16 + N:]).all()
+    assert _rel(cs, gr.double().sum(0)) < TOL
+    prev = cs.clone()
+    ops.gemm_wgrad(gr, x, out=big[:, 16:16 + N], colsum=cs, accumulate=True)
+    assert _rel(cs, prev.double() + gr.double().sum(0)) < TOL

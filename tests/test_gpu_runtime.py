@@ -126,3 +126,49 @@ def test_fault_injection_and_errors():
     with pytest.raises(ValueError):
         WorkerGroup(pos, ModelParams(cfg.replace(workers=2), params.arrays)).forward_backward(
             d_forces=np.zeros((pos.shape[0], 3)))
+
+
+def test_graph_aligned_trainer_equals_union_batch():
+    """Graph-aligned graph parallelism (bench --gpus N): each rank owns whole graphs,
+    the loss is normalised over the global batch and the flat gradient and loss are
+    all-reduced -- one step must equal the single-device step over the union batch."""
+    import threading
+
+    from paper_2203_09697_b200 import ModelConfig, init_params
+    from paper_2203_09697_b200.graph import build_batch
+    from paper_2203_09697_b200.runtime import CommLog, ThreadComm, _ThreadShared
+    from paper_2203_09697_b200.tasks import Trainer
+
+    cfg = ModelConfig(variant="gemnet-style", blocks=2, d_u=16, d_v=16, d_e=32, d_t=32, d_bil=32, k_rbf=6,
+                      l_sbf=7, cutoff=6.0, seed=2)
+    params = init_params(cfg)
+    rng = np.random.default_rng(9)
+    systems = [O.random_cloud(n, 0.06, rng)[0] for n in (20, 26, 23, 30)]
+    e_t = rng.standard_normal(4)
+    f_t = [rng.standard_normal((s.shape[0], 3)) for s in systems]
+    ref = Trainer(params, None, e_t, np.concatenate(f_t), 1.0, 0.5, graph=build_batch(systems, cfg.cutoff))
+    loss_ref = float(ref.step(0.0))
+    g_ref = ref.weights.grad_flat.double().cpu().numpy()
+
+    world, per = 2, 2
+    shared, log = _ThreadShared(world, 60.0, None), CommLog()
+    out = {}
+
+    def body(r):
+        sl = slice(r * per, (r + 1) * per)
+        bg = build_batch(systems[sl], cfg.cutoff)
+        tr = Trainer(params, None, e_t[sl], np.concatenate(f_t[sl]), 1.0, 0.5, graph=bg,
+                     comm=ThreadComm(r, shared, log), global_graphs=world * per)
+        loss = float(tr.step(0.0))
+        torch.cuda.synchronize()
+        out[r] = (loss, tr.weights.grad_flat.double().cpu().numpy())
+
+    ts = [threading.Thread(target=body, args=(r,)) for r in range(world)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    for r in range(world):
+        loss, g = out[r]
+        assert abs(loss - loss_ref) <= 1e-5 * abs(loss_ref)
+        assert max_rel(g, g_ref) < 1e-5
