@@ -170,9 +170,10 @@ __global__ void force_gather_kernel(const int64_t* __restrict__ edge_ptr,
   }
 }
 
-// Adjoint of the force head, warp per edge.
+// Adjoint of the force head, warp per edge, columns [c0, c0 + 512) of the edge
+// features (launched once per 512-column chunk; the geometry term on chunk 0).
 __global__ void force_bwd_kernel(const int32_t* __restrict__ recv, const float4* __restrict__ geo,
-                                 int64_t ne, const float* __restrict__ m, int d,
+                                 int64_t ne, const float* __restrict__ m, int d, int c0,
                                  const float* __restrict__ w, const float* __restrict__ scale,
                                  const float* __restrict__ fbar, float* __restrict__ mbar,
                                  float* __restrict__ wpart, float4* __restrict__ edge_grad) {
@@ -180,7 +181,7 @@ __global__ void force_bwd_kernel(const int32_t* __restrict__ recv, const float4*
   int wib = threadIdx.x >> 5;
   int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  // per-warp partial of w_bar, lanes over channels (d <= 32 * 16)
+  // per-warp partial of w_bar for this chunk, lanes over channels
   float wacc[16];
 #pragma unroll
   for (int u = 0; u < 16; ++u) wacc[u] = 0.f;
@@ -191,13 +192,13 @@ __global__ void force_bwd_kernel(const int32_t* __restrict__ recv, const float4*
     float sbar = bx * g.x + by * g.y + bz * g.z;
 #pragma unroll
     for (int u = 0; u < 16; ++u) {
-      int c = u * 32 + lane;
+      int c = c0 + u * 32 + lane;
       if (c < d) {
         mbar[e * d + c] += sbar * w[c];
         wacc[u] = fmaf(sbar, m[e * d + c], wacc[u]);
       }
     }
-    if (lane == 0) {
+    if (lane == 0 && c0 == 0) {
       float s = scale[e];
       // units_bar = s * fbar; d(unit)/d(v) adjoint: (ub - (ub.u) u) / d
       float ux = s * bx, uy = s * by, uz = s * bz;
@@ -213,7 +214,7 @@ __global__ void force_bwd_kernel(const int32_t* __restrict__ recv, const float4*
   int64_t slot = blockIdx.x * (int64_t)(blockDim.x >> 5) + wib;
 #pragma unroll
   for (int u = 0; u < 16; ++u) {
-    int c = u * 32 + lane;
+    int c = c0 + u * 32 + lane;
     if (c < d) wpart[slot * d + c] = wacc[u];
   }
 }
@@ -377,7 +378,6 @@ int egn_force_head_bwd(const int32_t* recv, const float* geo, int64_t num_edges,
                        int d, const float* w, const float* scale, const float* f_bar,
                        float* m_bar, float* w_bar, float* edge_grad, void* workspace,
                        egn_stream_t stream) {
-  EGN_REQUIRE(d <= 512, "force head width must be <= 512");
   cudaStream_t st = as_stream(stream);
   if (num_edges == 0) {
     cudaMemsetAsync(w_bar, 0, sizeof(float) * d, st);
@@ -385,10 +385,11 @@ int egn_force_head_bwd(const int32_t* recv, const float* geo, int64_t num_edges,
   }
   int grid = grid_for(num_edges * 32, 256, 148 * 2);
   float* part = reinterpret_cast<float*>(workspace);
-  force_bwd_kernel<<<grid, 256, 0, st>>>(recv, reinterpret_cast<const float4*>(geo), num_edges, m,
-                                         d, w, scale, f_bar, m_bar, part,
-                                         reinterpret_cast<float4*>(edge_grad));
-  if (check_launch("force_head_bwd")) return 1;
+  for (int c0 = 0; c0 < d; c0 += 512) {
+    force_bwd_kernel<<<grid, 256, 0, st>>>(recv, reinterpret_cast<const float4*>(geo), num_edges, m, d, c0, w,
+                                           scale, f_bar, m_bar, part, reinterpret_cast<float4*>(edge_grad));
+    if (check_launch("force_head_bwd")) return 1;
+  }
   reduce_rows_kernel<<<grid_for(d, 128), 128, 0, st>>>(part, grid * 8, d, w_bar);
   return check_launch("force_head_bwd_reduce");
 }

@@ -88,11 +88,28 @@ def sbf(geo, edge_ptr, tri_ptr, num_triplets, k_rbf, l_sbf, cutoff):
     return out
 
 
+# the native triplet kernels take up to 256 channels per call; wider triplet
+# embeddings (GemNet-XL d_bil = 288) are processed in channel chunks, which is
+# exact because the contraction is independent per channel (the geometry
+# adjoint edge_grad accumulates over chunks).
+MAX_TRIPLET_WIDTH = 256
+
+
+def _channel_chunks(dg):
+    return [(c0, min(dg, c0 + MAX_TRIPLET_WIDTH)) for c0 in range(0, dg, MAX_TRIPLET_WIDTH)]
+
+
 def triplet_fwd(edge_ptr, rev, geo, X, Wk, cutoff, max_degree=-1):
     """S = sum over the centre tile (see include/egn_b200.h egn_triplet_fwd)."""
     X = _c(X, torch.float32)
     Wk = _c(Wk, torch.float32)
     k, l, dg = Wk.shape
+    if dg > MAX_TRIPLET_WIDTH:
+        S = torch.empty_like(X)
+        for c0, c1 in _channel_chunks(dg):
+            S[:, c0:c1] = triplet_fwd(edge_ptr, rev, geo, X[:, c0:c1].contiguous(), Wk[:, :, c0:c1].contiguous(),
+                                      cutoff, max_degree)
+        return S
     S = torch.empty_like(X)
     call("egn_triplet_fwd", ptr(edge_ptr), ptr(rev), ptr(geo), edge_ptr.shape[0] - 1, int(max_degree), ptr(X),
          ptr(Wk), k, l, dg, float(cutoff), ptr(S), stream())
@@ -124,6 +141,13 @@ def triplet_bwd(edge_ptr, rev, geo, X, Wk, cutoff, S_bar, edge_grad, X_bar=None,
         W_bar = torch.empty_like(Wk)
     if max_degree is None:
         max_degree = int((edge_ptr[1:] - edge_ptr[:-1]).max().item()) if nv else 0
+    if dg > MAX_TRIPLET_WIDTH:
+        for c0, c1 in _channel_chunks(dg):
+            xb, wb = triplet_bwd(edge_ptr, rev, geo, X[:, c0:c1].contiguous(), Wk[:, :, c0:c1].contiguous(), cutoff,
+                                 S_bar[:, c0:c1].contiguous(), edge_grad, max_degree=max_degree)
+            X_bar[:, c0:c1] = xb
+            W_bar[:, :, c0:c1] = wb
+        return X_bar, W_bar
     ne = X.shape[0]
     nbytes = call("egn_triplet_bwd_workspace_bytes", nv, ne, k, l, dg)
     ws = _workspace(nbytes, X.device)

@@ -173,3 +173,42 @@ def test_rigid_motion_invariance():
     e1, f1 = predict(pos @ q.T + 3.0, params)
     assert abs(e0 - e1) < 1e-4 * max(1.0, abs(e0))
     assert max_rel(f1, f0 @ q.T) < 1e-3
+
+
+XL = {
+    # C3 DimeNet++-XL (d_e 2048, d_v = d_u 1536, d_t 256) and C4 GemNet-XL
+    # (d_v = d_u 2320, d_e 1302, d_t 512, d_bil 288 > 256: channel-chunked triplet
+    # kernels, non-tile-aligned dims on the cuBLAS composite), 2 blocks, small graph
+    "c3-dimenet-xl": dict(variant="dimenet-style", blocks=2, d_u=1536, d_v=1536, d_e=2048, d_t=256, d_bil=64),
+    "c4-gemnet-xl": dict(variant="gemnet-style", blocks=2, d_u=2320, d_v=2320, d_e=1302, d_t=512, d_bil=288),
+}
+
+
+@pytest.mark.parametrize("name", sorted(XL))
+def test_xl_dims_match_oracle(name):
+    """SURVEY 8(d) C3/C4 widths on a 14-atom graph vs the fp64 oracle (energy, forces,
+    every parameter gradient, position gradient)."""
+    from paper_2203_09697_b200 import ModelConfig, init_params
+    from paper_2203_09697_b200.engine import DeviceWeights, Engine
+    from paper_2203_09697_b200.graph import build_batch
+
+    cfg = ModelConfig(k_rbf=6, l_sbf=7, cutoff=6.0, seed=4, **XL[name])
+    params = init_params(cfg)
+    pos, z = O.random_cloud(14, 0.06, np.random.default_rng(21))
+    eng = Engine(DeviceWeights.from_params(params))
+    bg = build_batch([pos], cfg.cutoff)
+    fw = eng.forward(bg)
+    gem = cfg.variant == "gemnet-style"
+    df = np.random.default_rng(3).standard_normal(pos.shape) if gem else None
+    pos_bar = eng.backward(bg, fw, torch.tensor([0.9], device="cuda"),
+                           torch.tensor(df, device="cuda") if gem else None)
+    grads = eng.weights.to_numpy(grads=True)
+    oc = O.Config(**{k: getattr(cfg, k) for k in O.Config.__dataclass_fields__})
+    ofw = O.forward(oc, params.arrays, pos, z)
+    G, dpos = O.backward(ofw, params.arrays, 0.9, df)
+    assert abs(float(fw.energy[0]) - ofw.energy) <= TOL * max(abs(ofw.energy), 1e-8)
+    if gem:
+        assert max_rel(fw.forces.double().cpu().numpy(), ofw.forces) < TOL
+    assert max_rel(pos_bar.cpu().numpy(), dpos) < TOL
+    for k, g in G.items():
+        assert max_rel(grads[k], g) < TOL, k
