@@ -539,6 +539,10 @@ int fast_bwd(const int64_t* edge_ptr, const int32_t* rev, const float4* geo, int
              const float* X, const float* W, int K, int L, int dg, RbfParams rp, const float* Sbar, float* Xbar,
              float* Wbar, float4* edge_grad, void* ws, cudaStream_t st);
 constexpr int kFastMaxDeg = 64;
+bool tc_fwd_supported(int K, int L, int dg, int max_degree);
+int tc_fwd(const int64_t* edge_ptr, const int32_t* rev, const float4* geo, int64_t nv, int max_degree,
+           const float* X, const float* W, int K, int L, int dg, RbfParams rp, float* S, int min_n,
+           cudaStream_t st);
 
 // Debug: per-triplet summand P[t, c] in (out, in) order.
 __global__ void triplet_terms_kernel(const int64_t* __restrict__ edge_ptr,
@@ -658,12 +662,17 @@ int egn_triplet_fwd(const int64_t* edge_ptr, const int32_t* rev, const float* ge
   RbfParams rp = rbf_params(k_rbf, cutoff);
   const float4* g4 = reinterpret_cast<const float4*>(geo);
   cudaStream_t st = as_stream(stream);
+  // centres with deg <= 64: CUDA-core centre-tile kernel (triplet_fast.cu); larger
+  // centres: tensor-core kernel (triplet_tc.cu) when the degree bound is known, else
+  // the generic CUDA-core kernel
   int min_n = 0;
   if (fast_supported(k_rbf, l_sbf, dg)) {
     if (int rc = fast_fwd(edge_ptr, rev, g4, num_nodes, X, W, k_rbf, l_sbf, dg, rp, S, st)) return rc;
     if (max_degree >= 0 && max_degree <= kFastMaxDeg) return 0;
     min_n = kFastMaxDeg;
   }
+  if (tc_fwd_supported(k_rbf, l_sbf, dg, max_degree))
+    return tc_fwd(edge_ptr, rev, g4, num_nodes, max_degree, X, W, k_rbf, l_sbf, dg, rp, S, min_n, st);
 #define EGN_FWD(CW, GC, R) \
   return launch_fwd<CW, GC, R>(edge_ptr, rev, g4, num_nodes, X, W, k_rbf, l_sbf, dg, rp, S, min_n, st)
   if (dg <= 4) EGN_FWD(4, 1, 1);

@@ -1,0 +1,351 @@
+// Triplet-interaction forward on the 5th-generation tensor cores (tcgen05).
+//
+// For centre atom j with n out-edges (rows p) and their reverses rq = rev(off_j+q)
+// (the in-edges k->j), the forward of egn_triplet_fwd is
+//
+//   S[off_j+p, c] = sum_{q != p} sum_l T_l(u_p . u_q) * Y[q, l, c],
+//   Y[q, l, c]    = X[rq, c] * sum_k rbf_k(d_q) W[k, l, c]
+//
+// (record_tu, egn/engine.py:136-148, after the algebraic reorder of DESIGN.md 4.1).
+// Per centre that is one GEMM with one K = 8 step per in-edge q (l padded to 8):
+//
+//   D[c, p] = sum_q A_q[c, 0..7] . B_q[p, 0..7],  A_q = Y[q, :, c]^T,  B_q = T(x_pq) (0 if p == q)
+//
+// M = channel block (64 or 128 channels), N = rows p (<= 256 per pass), fp32-accurate
+// through the 3xTF32 split (A_lo.B_hi + A_hi.B_lo + A_hi.B_hi).
+//
+// Warp roles (288 threads, persistent CTAs over centres):
+//   warps 0-3 : operand builders -- per slab of 4 in-edges they write A (thread = channel:
+//               X gather, rbf, W column in registers) and B (Chebyshev table of the
+//               centre's angles) as hi/lo in the K-major SWIZZLE_128B layout;
+//   warp 4    : MMA issuer (one elected lane), D double-buffered in TMEM per pass;
+//   warps 5-8 : epilogue -- TMEM -> registers -> S rows (lanes = channels, coalesced).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <cstdlib>
+
+#include "common.cuh"
+
+namespace egn {
+namespace tc {
+
+constexpr int kThreads = 288;
+constexpr int kBuilders = 128;
+constexpr int kMaxDeg = 1024;  // centre geometry staged in shared memory
+constexpr int kMaxNB = 256;    // rows p per pass (MMA N)
+constexpr int kMaxK = 8;
+
+__device__ __forceinline__ uint32_t su32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t c) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(c));
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tW_%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t@!p bra W_%=;\n\t}" ::"r"(
+          su32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(b)) : "memory");
+}
+__device__ __forceinline__ void mma_commit(uint64_t* b) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(b)) : "memory");
+}
+__device__ __forceinline__ uint64_t kdesc(uint32_t saddr) {
+  return static_cast<uint64_t>((saddr >> 4) & 0x3FFF) | (static_cast<uint64_t>(1) << 16) |
+         (static_cast<uint64_t>(1024 >> 4) << 32) | (static_cast<uint64_t>(1) << 46) | (static_cast<uint64_t>(2) << 61);
+}
+__device__ __forceinline__ void mma_tf32(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\ttcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile("{\n\t.reg .pred P;\n\telect.sync _|P, 0xffffffff;\n\tselp.b32 %0, 1, 0, P;\n\t}" : "=r"(pred));
+  return pred != 0;
+}
+__device__ __forceinline__ float tf32_rna(float x) { return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xffffe000u); }
+__device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+
+// 16-byte granule g (0..7) of row r in a K-major SWIZZLE_128B slab (128 B rows, 8-row atoms)
+__device__ __forceinline__ int sw_off(int r, int g) { return r * 128 + ((g ^ (r & 7)) << 4); }
+
+// write 8 consecutive k values (k-step j of the slab) of row r as hi and lo
+__device__ __forceinline__ void put8(uint8_t* hi, uint8_t* lo, int r, int j, const float* v) {
+  float h[8], l[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    h[i] = tf32_rna(v[i]);
+    l[i] = v[i] - h[i];
+  }
+  *reinterpret_cast<float4*>(hi + sw_off(r, 2 * j)) = make_float4(h[0], h[1], h[2], h[3]);
+  *reinterpret_cast<float4*>(hi + sw_off(r, 2 * j + 1)) = make_float4(h[4], h[5], h[6], h[7]);
+  *reinterpret_cast<float4*>(lo + sw_off(r, 2 * j)) = make_float4(l[0], l[1], l[2], l[3]);
+  *reinterpret_cast<float4*>(lo + sw_off(r, 2 * j + 1)) = make_float4(l[4], l[5], l[6], l[7]);
+}
+
+struct Args {
+  const int64_t* edge_ptr;
+  const int32_t* rev;
+  const float4* geo;
+  int64_t nv;
+  const float* X;
+  const float* W;
+  float* S;
+  int K, L, ld, c0;  // channel block [c0, c0 + M) of rows with stride ld
+  float gamma, step;
+  int nbmax, nslot, gcap;  // rows per pass (TMEM columns per buffer), ring slots, staged degree cap
+  int min_n;               // centres with n <= min_n are left to the CUDA-core small-degree kernel
+};
+
+template <int M>
+__global__ void __launch_bounds__(kThreads, 1) fwd_kernel(Args a) {
+  constexpr int A_BYTES = M * 128;
+  extern __shared__ __align__(16) uint8_t raw[];
+  uint8_t* sm = raw + ((1024u - (su32(raw) & 1023u)) & 1023u);
+  const int B_BYTES = a.nbmax * 128;
+  const int SLOT = 2 * A_BYTES + 2 * B_BYTES;
+  uint8_t* ring = sm;
+  float4* U = reinterpret_cast<float4*>(sm + a.nslot * SLOT);  // [gcap] centre out-edge geometry
+  int32_t* RQ = reinterpret_cast<int32_t*>(U + a.gcap);        // [gcap] in-edge ids
+  __shared__ __align__(8) uint64_t full[4], empty[4], dfull[2], dempty[2];
+  __shared__ uint32_t tbase;
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int NS = a.nslot;
+  if (tid == 0) {
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&dfull[b], 1);
+      mbar_init(&dempty[b], 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  uint32_t tcols = 32;
+  while (tcols < 2u * a.nbmax) tcols <<= 1;
+  if (warp == 4) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(&tbase)), "r"(tcols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = tbase;
+
+  if (warp < 4) {
+    // ------------------------------------------------ builders
+    // thread -> channel c (fixed), k-steps j = jt, jt + JS, ... of each slab
+    constexpr int JS = kBuilders / M;  // 2 (M = 64) or 1 (M = 128)
+    const int c = tid % M, jt = tid / M;
+    float w[kMaxK][8];
+#pragma unroll
+    for (int k = 0; k < kMaxK; ++k)
+#pragma unroll
+      for (int l = 0; l < 8; ++l)
+        w[k][l] = (k < a.K && l < a.L) ? a.W[(static_cast<int64_t>(k) * a.L + l) * a.ld + a.c0 + c] : 0.f;
+    uint32_t it = 0;
+    for (int64_t j = blockIdx.x; j < a.nv; j += gridDim.x) {
+      const int64_t off = a.edge_ptr[j];
+      const int n = static_cast<int>(a.edge_ptr[j + 1] - off);
+      if (n <= 0 || n <= a.min_n) continue;
+      named_sync(1, kBuilders);  // previous centre's readers of U/RQ are done
+      for (int q = tid; q < n; q += kBuilders) {
+        U[q] = a.geo[off + q];
+        RQ[q] = a.rev[off + q];
+      }
+      named_sync(1, kBuilders);
+      const int nslab = (n + 3) >> 2;
+      for (int p0 = 0; p0 < n; p0 += kMaxNB) {
+        const int np = min(kMaxNB, n - p0);
+        const int nb = (np + 15) & ~15;
+        for (int s = 0; s < nslab; ++s, ++it) {
+          const int slot = it % NS;
+          mbar_wait(&empty[slot], ((it / NS) & 1) ^ 1);
+          uint8_t* ahi = ring + slot * SLOT;
+          uint8_t* alo = ahi + A_BYTES;
+          uint8_t* bhi = alo + A_BYTES;
+          uint8_t* blo = bhi + B_BYTES;
+          // A: Y[q, l, c] for the slab's 4 in-edges
+#pragma unroll
+          for (int jj = 0; jj < 4 / JS; ++jj) {
+            const int js = jt + jj * JS;
+            const int q = 4 * s + js;
+            float y[8];
+            if (q < n) {
+              const float4 g = U[q];
+              const float x = a.X[static_cast<int64_t>(RQ[q]) * a.ld + a.c0 + c];
+              float rb[kMaxK];
+#pragma unroll
+              for (int k = 0; k < kMaxK; ++k) {
+                const float dd = g.w - a.step * k;
+                rb[k] = k < a.K ? __expf(-a.gamma * dd * dd) : 0.f;
+              }
+#pragma unroll
+              for (int l = 0; l < 8; ++l) {
+                float r = 0.f;
+#pragma unroll
+                for (int k = 0; k < kMaxK; ++k) r = fmaf(rb[k], w[k][l], r);
+                y[l] = x * r;
+              }
+            } else {
+#pragma unroll
+              for (int l = 0; l < 8; ++l) y[l] = 0.f;
+            }
+            put8(ahi, alo, c, js, y);
+          }
+          // B: Chebyshev T_l(u_p . u_q), zero on the diagonal and in padding
+          for (int idx = tid; idx < nb * 4; idx += kBuilders) {
+            const int pr = idx >> 2, js = idx & 3;
+            const int p = p0 + pr, q = 4 * s + js;
+            float t[8];
+            if (pr < np && q < n && p != q) {
+              const float4 up = U[p], uq = U[q];
+              const float xx = up.x * uq.x + up.y * uq.y + up.z * uq.z;
+              t[0] = 1.f;
+              t[1] = xx;
+#pragma unroll
+              for (int l = 2; l < 8; ++l) t[l] = 2.f * xx * t[l - 1] - t[l - 2];
+#pragma unroll
+              for (int l = 0; l < 8; ++l)
+                if (l >= a.L) t[l] = 0.f;
+            } else {
+#pragma unroll
+              for (int l = 0; l < 8; ++l) t[l] = 0.f;
+            }
+            put8(bhi, blo, pr, js, t);
+          }
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          named_sync(1, kBuilders);
+          if (tid == 0) mbar_arrive(&full[slot]);
+        }
+      }
+    }
+  } else if (warp == 4) {
+    // ------------------------------------------------ MMA issuer
+    uint32_t it = 0, pass = 0;
+    for (int64_t j = blockIdx.x; j < a.nv; j += gridDim.x) {
+      const int64_t off = a.edge_ptr[j];
+      const int n = static_cast<int>(a.edge_ptr[j + 1] - off);
+      if (n <= 0 || n <= a.min_n) continue;
+      const int nslab = (n + 3) >> 2;
+      for (int p0 = 0; p0 < n; p0 += kMaxNB, ++pass) {
+        const int nb = (min(kMaxNB, n - p0) + 15) & ~15;
+        const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | (static_cast<uint32_t>(nb >> 3) << 17) |
+                               (static_cast<uint32_t>(M >> 4) << 24);
+        const uint32_t b = pass & 1;
+        mbar_wait(&dempty[b], ((pass >> 1) & 1) ^ 1);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        const uint32_t d = tmem + b * a.nbmax;
+        for (int s = 0; s < nslab; ++s, ++it) {
+          const int slot = it % NS;
+          mbar_wait(&full[slot], (it / NS) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;");
+          const uint32_t ahi = su32(ring + slot * SLOT);
+          const uint32_t alo = ahi + A_BYTES, bhi = alo + A_BYTES, blo = bhi + B_BYTES;
+          if (elect_one()) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              const uint32_t acc = (s == 0 && k == 0) ? 0u : 1u;
+              mma_tf32(d, kdesc(alo + 32 * k), kdesc(bhi + 32 * k), idesc, acc);
+              mma_tf32(d, kdesc(ahi + 32 * k), kdesc(blo + 32 * k), idesc, 1u);
+              mma_tf32(d, kdesc(ahi + 32 * k), kdesc(bhi + 32 * k), idesc, 1u);
+            }
+            mma_commit(&empty[slot]);
+            if (s == nslab - 1) mma_commit(&dfull[b]);
+          }
+          __syncwarp();
+        }
+      }
+    }
+  } else {
+    // ------------------------------------------------ epilogue (warps 5..8)
+    const int qd = warp & 3;  // TMEM lane quarter
+    // M = 128: row c = 32 qd + lane; M = 64: row c = 16 qd + lane (lanes 0..15)
+    const int c = M == 128 ? 32 * qd + lane : 16 * qd + lane;
+    const bool active = M == 128 || lane < 16;
+    uint32_t pass = 0;
+    for (int64_t j = blockIdx.x; j < a.nv; j += gridDim.x) {
+      const int64_t off = a.edge_ptr[j];
+      const int n = static_cast<int>(a.edge_ptr[j + 1] - off);
+      if (n <= 0 || n <= a.min_n) continue;
+      for (int p0 = 0; p0 < n; p0 += kMaxNB, ++pass) {
+        const int np = min(kMaxNB, n - p0);
+        const uint32_t b = pass & 1;
+        mbar_wait(&dfull[b], (pass >> 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        const uint32_t taddr = tmem + b * a.nbmax + (static_cast<uint32_t>(qd * 32) << 16);
+        float* dst = a.S + (off + p0) * a.ld + a.c0 + c;
+        for (int cb = 0; cb < np; cb += 16) {
+          uint32_t r[16];
+          asm volatile(
+              "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+              : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+                "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+              : "r"(taddr + cb));
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+          if (active) {
+#pragma unroll
+            for (int i = 0; i < 16; ++i)
+              if (cb + i < np) dst[static_cast<int64_t>(cb + i) * a.ld] = __uint_as_float(r[i]);
+          }
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;");
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&dempty[b]);
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 4) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(tcols));
+}
+
+}  // namespace tc
+
+// ---------------------------------------------------------------------------
+// host side (called from egn_triplet_fwd)
+// ---------------------------------------------------------------------------
+bool tc_fwd_supported(int K, int L, int dg, int max_degree) {
+  static const bool enabled = [] {
+    const char* e = std::getenv("EGN_TRIPLET_TC");
+    return !(e && e[0] == '0');
+  }();
+  return enabled && K >= 1 && K <= tc::kMaxK && L >= 1 && L <= 8 && dg % 64 == 0 && max_degree >= 0 &&
+         max_degree <= tc::kMaxDeg;
+}
+
+int tc_fwd(const int64_t* edge_ptr, const int32_t* rev, const float4* geo, int64_t nv, int max_degree,
+           const float* X, const float* W, int K, int L, int dg, RbfParams rp, float* S, int min_n,
+           cudaStream_t st) {
+  const int nbmax = std::max(16, (std::min(max_degree, tc::kMaxNB) + 15) & ~15);
+  for (int c0 = 0; c0 < dg; c0 += 128) {
+    const int M = (dg - c0) >= 128 ? 128 : 64;
+    const int slot = 2 * M * 128 + 2 * nbmax * 128;
+    const int gcap = std::max(4, (max_degree + 3) & ~3);
+    const int geo_bytes = gcap * 20;
+    // ring depth: up to 4 slots, fewer to fit two CTAs per SM when possible
+    int nslot = 4;
+    while (nslot > 2 && static_cast<size_t>(nslot) * slot + geo_bytes + 1024 > 110 * 1024) --nslot;
+    const size_t smem = static_cast<size_t>(nslot) * slot + geo_bytes + 1024;
+    tc::Args a{edge_ptr, rev, geo, nv, X, W, S, K, L, dg, c0, rp.gamma, rp.step, nbmax, nslot, gcap, min_n};
+    auto kern = M == 128 ? tc::fwd_kernel<128> : tc::fwd_kernel<64>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    int per_sm = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, tc::kThreads, smem);
+    per_sm = std::max(1, std::min(per_sm, 2 * nbmax <= 256 ? 2 : 1));  // TMEM: 512 columns per SM
+    const int grid = static_cast<int>(std::min<int64_t>(nv, static_cast<int64_t>(kNumSMs) * per_sm));
+    kern<<<grid, tc::kThreads, smem, st>>>(a);
+    if (int rc = check_launch("triplet_fwd_tc")) return rc;
+    if (M == 64) break;
+  }
+  return 0;
+}
+
+}  // namespace egn

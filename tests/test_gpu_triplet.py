@@ -60,7 +60,10 @@ def _run(pos, cutoff, K, L, dg, seed=0):
     g, S_ref, Xb_ref, Wb_ref, pb_ref = _ref(pos, cutoff, X, W, B)
     Xd = torch.tensor(X, dtype=torch.float32, device="cuda")
     Wd = torch.tensor(W, dtype=torch.float32, device="cuda")
-    S = ops.triplet_fwd(bg.edge_ptr, bg.rev, bg.geo, Xd, Wd, cutoff)
+    # max_degree known: tensor-core forward when d_g % 64 == 0 (triplet_tc.cu); unknown: CUDA-core kernels
+    S = ops.triplet_fwd(bg.edge_ptr, bg.rev, bg.geo, Xd, Wd, cutoff, max_degree=bg.max_deg)
+    S_cc = ops.triplet_fwd(bg.edge_ptr, bg.rev, bg.geo, Xd, Wd, cutoff)
+    assert max_rel(S_cc.cpu().numpy(), S_ref) < TOL
     eg = torch.zeros((bg.num_edges, 4), device="cuda")
     Bd = torch.tensor(B, dtype=torch.float32, device="cuda")
     Xb, Wb = ops.triplet_bwd(bg.edge_ptr, bg.rev, bg.geo, Xd, Wd, cutoff, Bd, eg)
@@ -160,6 +163,15 @@ def test_triplet_dimension_errors():
     X = torch.zeros((bg.num_edges, 8), device="cuda")
     with pytest.raises(ValueError):
         ops.triplet_fwd(bg.edge_ptr, bg.rev, bg.geo, X, torch.zeros((6, 9, 8), device="cuda"), 1.5)
-    with pytest.raises(ValueError):
-        ops.triplet_fwd(bg.edge_ptr, bg.rev, bg.geo, torch.zeros((bg.num_edges, 300), device="cuda"),
-                        torch.zeros((6, 4, 300), device="cuda"), 1.5)
+    with pytest.raises(ValueError):  # the C ABI takes <= 256 channels per call
+        from paper_2203_09697_b200._lib import call, ptr, stream
+        X3, W3 = torch.zeros((bg.num_edges, 300), device="cuda"), torch.zeros((6, 4, 300), device="cuda")
+        S3 = torch.empty_like(X3)
+        call("egn_triplet_fwd", ptr(bg.edge_ptr), ptr(bg.rev), ptr(bg.geo), bg.num_nodes, -1, ptr(X3), ptr(W3), 6, 4,
+             300, 1.5, ptr(S3), stream())
+    # ... and ops.triplet_fwd chunks wider embeddings exactly (per-channel independence)
+    X3 = torch.randn((bg.num_edges, 300), device="cuda")
+    W3 = torch.randn((6, 4, 300), device="cuda")
+    S3 = ops.triplet_fwd(bg.edge_ptr, bg.rev, bg.geo, X3, W3, 1.5)
+    S_lo = ops.triplet_fwd(bg.edge_ptr, bg.rev, bg.geo, X3[:, :256].contiguous(), W3[:, :, :256].contiguous(), 1.5)
+    assert torch.equal(S3[:, :256], S_lo)
