@@ -65,6 +65,7 @@ def _args():
     ap.add_argument("--cpu-budget", type=float, default=12.0, help="seconds of CPU oracle sampling")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-kernel-timing", action="store_true")
+    ap.add_argument("--eager", action="store_true", help="no CUDA-graph replay of the training step")
     return ap.parse_args()
 
 
@@ -279,6 +280,7 @@ def run_ours(args, wl):
     cfg = _config(wl)
     graphs = args.graphs or wl["graphs"]
     aligned = world == 1 or args.partition == "aligned"
+    use_graph = not args.eager
     # weak scaling: every rank contributes `graphs` graphs to the global batch.  With the
     # graph-aligned partition a rank builds and owns only its own graphs.
     if aligned:
@@ -293,14 +295,14 @@ def run_ours(args, wl):
     f_t = tf.forces.double().cpu().numpy() if wl["w_forces"] else None
     del tf, teacher
     if world == 1:
-        tr = Trainer(params, None, e_t, f_t, 1.0, wl["w_forces"], graph=bg)
+        tr = Trainer(params, None, e_t, f_t, 1.0, wl["w_forces"], graph=bg, cuda_graph=use_graph)
         comm = None
         parallelism = "single"
     elif aligned:
         # graph-aligned centre partition: no halo, one gradient all-reduce per step
         comm = DistComm()
         tr = Trainer(params, None, e_t, f_t, 1.0, wl["w_forces"], graph=bg, comm=comm,
-                     global_graphs=graphs * world)
+                     global_graphs=graphs * world, cuda_graph=use_graph and backend == "nccl")
         parallelism = f"gp{world} (graph-aligned centre partition: no halo, gradient all-reduce, {backend})"
     else:
         comm = DistComm()
@@ -336,6 +338,8 @@ def run_ours(args, wl):
     torch.cuda.synchronize()
     t_dev = st.elapsed_time(en) / 1000.0 / args.steps
     launches = _lib.LAUNCH_COUNTER["kernels"] // args.steps
+    if getattr(tr, "cuda_graph", False) and getattr(tr, "kernels_per_step", None):
+        launches = tr.kernels_per_step  # replayed from the captured step graph
     loss_last = float(loss)
     # ---- end to end: host buffers -> device -> step -> loss back to host
     pos_host = torch.from_numpy(np.concatenate([s.positions for s in systems])).pin_memory()
@@ -348,10 +352,12 @@ def run_ours(args, wl):
         pos = pos_host.to("cuda", non_blocking=True)
         et = et_host.to("cuda", non_blocking=True)
         ft = ft_host.to("cuda", non_blocking=True) if ft_host is not None else None
-        g = build_batch(None, cfg.cutoff, positions=pos, sizes=sizes)
         if aligned:
-            tr.set_inputs(g, et, ft)
+            # same batch every step (a pass over a fixed dataset): copy this step's
+            # positions and targets into the resident batch, recompute its geometry
+            tr.update_inputs(pos, et, ft)
         else:
+            g = build_batch(None, cfg.cutoff, positions=pos, sizes=sizes)
             n0, n1 = tr.engine.n0, tr.engine.n1
             tr.bg, tr.e_target = g, et
             tr.f_target = ft[n0:n1] if ft is not None else None

@@ -174,6 +174,18 @@ int egn_force_head_bwd(const int32_t* recv, const float* geo, int64_t num_edges,
                        egn_stream_t stream);
 int64_t egn_force_head_bwd_workspace_bytes(int64_t num_edges, int d);
 
+/* K <= 8 linears of the radial basis (edge_init engine.py:109-111, rbf gate engine.py:138):
+ * out[e, n] (row stride ldo) = sum_k rbf[e, k] w[n, k] (+ b[n] if b != NULL); N % 4 == 0. */
+int egn_rbf_linear(const float* rbf, int64_t num_edges, int k, const float* w, const float* b, int n, float* out,
+                   int64_t ldo, egn_stream_t stream);
+/* Adjoint (linear VJP, tape.py:104-119) for N <= 128: rbf_bar[e,k] += sum_n g[e,n] w[n,k];
+ * w_bar = g^T rbf (overwritten), b_bar = column sums of g (overwritten; NULL to skip);
+ * deterministic (fixed-order partial reduction). */
+int64_t egn_rbf_linear_bwd_workspace_bytes(int64_t num_edges, int k, int n);
+int egn_rbf_linear_bwd(const float* rbf, int64_t num_edges, int k, const float* w, int n, const float* g,
+                       int64_t ldg, float* rbf_bar, float* w_bar, float* b_bar, void* workspace,
+                       egn_stream_t stream);
+
 /* ------------------------------------------------------------------ */
 /* Geometry adjoints (tape.py:164-242, runtime.py:626-671)             */
 /* ------------------------------------------------------------------ */

@@ -48,6 +48,9 @@ SIGNATURES: dict[str, tuple] = {
     "egn_force_head_fwd": (_i32, [_p, _p, _p, _i64, _i64, _p, _i32, _p, _p, _p, _p]),
     "egn_force_head_bwd_workspace_bytes": (_i64, [_i64, _i32]),
     "egn_force_head_bwd": (_i32, [_p, _p, _i64, _p, _i32, _p, _p, _p, _p, _p, _p, _p, _p]),
+    "egn_rbf_linear": (_i32, [_p, _i64, _i32, _p, _p, _i32, _p, _i64, _p]),
+    "egn_rbf_linear_bwd_workspace_bytes": (_i64, [_i64, _i32, _i32]),
+    "egn_rbf_linear_bwd": (_i32, [_p, _i64, _i32, _p, _i32, _p, _i64, _p, _p, _p, _p, _p]),
     "egn_rbf_bwd": (_i32, [_p, _p, _i64, _i32, _f64, _p, _p]),
     "egn_positions_bwd": (_i32, [_p, _p, _p, _i64, _p, _p, _p]),
     "egn_column_sum_workspace_bytes": (_i64, [_i64, _i32]),
@@ -99,7 +102,7 @@ def stream() -> int:
 
 # Kernels launched per successful ABI call (for the bench's gpu_launches count).
 KERNELS_PER_CALL = {
-    "egn_triplet_bwd": 4, "egn_force_head_fwd": 2, "egn_force_head_bwd": 2, "egn_column_sum": 2, "egn_gemm_wgrad": 2,
+    "egn_triplet_bwd": 4, "egn_force_head_fwd": 2, "egn_force_head_bwd": 2, "egn_column_sum": 2, "egn_gemm_wgrad": 2, "egn_rbf_linear_bwd": 2,
 }
 LAUNCH_COUNTER = {"calls": 0, "kernels": 0}
 

@@ -229,6 +229,117 @@ __global__ void reduce_rows_kernel(const float* __restrict__ part, int nparts, i
   }
 }
 
+// ---------------------------------------------------------------- K <= 8 linears of the basis
+// out[e, n] = sum_k rbf[e, k] W[n, k] (+ b[n]): edge_init (engine.py:109-111) and the
+// per-block rbf gate (engine.py:138).  HBM-bound: one float4 store per 4 outputs.
+__global__ void rbf_linear_kernel(const float* __restrict__ rbf, int64_t ne, int K, const float* __restrict__ W,
+                                  const float* __restrict__ b, int N, float* __restrict__ out, int64_t ldo) {
+  extern __shared__ float ws[];  // [K][N] then bias [N]
+  for (int i = threadIdx.x; i < K * N; i += blockDim.x) ws[(i % K) * N + i / K] = W[i];
+  for (int i = threadIdx.x; i < N; i += blockDim.x) ws[K * N + i] = b ? b[i] : 0.f;
+  __syncthreads();
+  const int n4 = N >> 2;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < ne * n4;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = idx / n4;
+    const int c = static_cast<int>(idx - e * n4) * 4;
+    float4 o = *reinterpret_cast<const float4*>(ws + K * N + c);
+    for (int k = 0; k < K; ++k) {
+      const float r = __ldg(rbf + e * K + k);
+      const float4 w4 = *reinterpret_cast<const float4*>(ws + k * N + c);
+      o.x = fmaf(r, w4.x, o.x);
+      o.y = fmaf(r, w4.y, o.y);
+      o.z = fmaf(r, w4.z, o.z);
+      o.w = fmaf(r, w4.w, o.w);
+    }
+    *reinterpret_cast<float4*>(out + e * ldo + c) = o;
+  }
+}
+
+// Adjoint of rbf_linear for N <= 128, tiles of 32 edges staged in shared memory:
+//   rbf_bar[e, k] += sum_n g[e, n] W[n, k]        (thread per (edge, k) of the tile)
+//   part[block]    = (sum_e g[e, n] rbf[e, k])[n, k] and (sum_e g[e, n])[n]
+//                    (thread-owned accumulators over the block's tiles, fixed order)
+constexpr int kRlTile = 32;
+__global__ void __launch_bounds__(256) rbf_linear_bwd_kernel(const float* __restrict__ rbf, int64_t ne, int K,
+                                                             const float* __restrict__ W, int N,
+                                                             const float* __restrict__ g, int64_t ldg,
+                                                             float* __restrict__ rbf_bar, float* __restrict__ part) {
+  __shared__ float ws[128 * 8];
+  __shared__ float gs[kRlTile][129];
+  __shared__ float rs[kRlTile][9];
+  const int tid = threadIdx.x;
+  for (int i = tid; i < N * K; i += 256) ws[i] = W[i];
+  const int len = N * K + N;
+  float acc[5];  // owned slots tid + 256 r of [N*K weights | N biases]
+#pragma unroll
+  for (int r = 0; r < 5; ++r) acc[r] = 0.f;
+  const int64_t ntiles = (ne + kRlTile - 1) / kRlTile;
+  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const int64_t e0 = t * kRlTile;
+    const int te = ne - e0 < kRlTile ? static_cast<int>(ne - e0) : kRlTile;
+    __syncthreads();
+    for (int i = tid; i < kRlTile * N; i += 256) {
+      const int e = i / N, n = i - (i / N) * N;
+      gs[e][n] = e < te ? g[(e0 + e) * ldg + n] : 0.f;
+    }
+    for (int i = tid; i < kRlTile * K; i += 256) {
+      const int e = i / K, k = i - (i / K) * K;
+      rs[e][k] = e < te ? rbf[(e0 + e) * K + k] : 0.f;
+    }
+    __syncthreads();
+    if (tid < kRlTile * K) {
+      const int e = tid / K, k = tid - (tid / K) * K;
+      if (e < te) {
+        float sacc = 0.f;
+        for (int n = 0; n < N; ++n) sacc = fmaf(gs[e][n], ws[n * K + k], sacc);
+        rbf_bar[(e0 + e) * K + k] += sacc;
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < 5; ++r) {
+      const int slot = tid + 256 * r;
+      if (slot < N * K) {
+        const int n = slot / K, k = slot - (slot / K) * K;
+        float a = acc[r];
+        for (int e = 0; e < kRlTile; ++e) a = fmaf(gs[e][n], rs[e][k], a);
+        acc[r] = a;
+      } else if (slot < len) {
+        const int n = slot - N * K;
+        float a = acc[r];
+        for (int e = 0; e < kRlTile; ++e) a += gs[e][n];
+        acc[r] = a;
+      }
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < 5; ++r) {
+    const int slot = tid + 256 * r;
+    if (slot < len) part[blockIdx.x * (int64_t)len + slot] = acc[r];
+  }
+}
+
+// out1[i] = sum_p part[p][i] for i < split, out2[i - split] for i >= split (out2 may be
+// null): 8 warps split the parts, fixed-order combine (32 outputs per block).
+__global__ void reduce_parts_kernel(const float* __restrict__ part, int nparts, int len, int split,
+                                    float* __restrict__ out1, float* __restrict__ out2) {
+  __shared__ float red[8][33];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int i = blockIdx.x * 32 + lane;
+  float s = 0.f;
+  if (i < len)
+    for (int p = w; p < nparts; p += 8) s += part[static_cast<int64_t>(p) * len + i];
+  red[w][lane] = s;
+  __syncthreads();
+  if (w == 0 && i < len) {
+    float t = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) t += red[k][lane];
+    if (i < split) out1[i] = t;
+    else if (out2) out2[i - split] = t;
+  }
+}
+
 // ---------------------------------------------------------------- geometry adjoints
 __global__ void rbf_bwd_kernel(const float4* __restrict__ geo, const float* __restrict__ rbar,
                                int64_t ne, int K, RbfParams rp, float4* __restrict__ edge_grad) {
@@ -392,6 +503,48 @@ int egn_force_head_bwd(const int32_t* recv, const float* geo, int64_t num_edges,
   }
   reduce_rows_kernel<<<grid_for(d, 128), 128, 0, st>>>(part, grid * 8, d, w_bar);
   return check_launch("force_head_bwd_reduce");
+}
+
+int egn_rbf_linear(const float* rbf, int64_t num_edges, int k, const float* w, const float* b, int n, float* out,
+                   int64_t ldo, egn_stream_t stream) {
+  EGN_REQUIRE(k >= 1 && k <= 8 && n >= 4 && n % 4 == 0 && ldo % 4 == 0, "rbf_linear needs K <= 8, N % 4 == 0");
+  if (num_edges == 0) return 0;
+  const size_t smem = sizeof(float) * (k * n + n);
+  EGN_REQUIRE(smem <= 200 * 1024, "rbf_linear: N too large");
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(rbf_linear_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  rbf_linear_kernel<<<grid_for(num_edges * (n / 4), 256, 148 * 8), 256, smem, as_stream(stream)>>>(
+      rbf, num_edges, k, w, b, n, out, ldo);
+  return check_launch("rbf_linear");
+}
+
+static int rbf_linear_bwd_grid(int64_t num_edges) {
+  const int64_t tiles = (num_edges + kRlTile - 1) / kRlTile;
+  return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(tiles, kNumSMs)));
+}
+
+int64_t egn_rbf_linear_bwd_workspace_bytes(int64_t num_edges, int k, int n) {
+  return static_cast<int64_t>(rbf_linear_bwd_grid(num_edges)) * (n * k + n) * 4;
+}
+
+int egn_rbf_linear_bwd(const float* rbf, int64_t num_edges, int k, const float* w, int n, const float* g,
+                       int64_t ldg, float* rbf_bar, float* w_bar, float* b_bar, void* workspace,
+                       egn_stream_t stream) {
+  EGN_REQUIRE(k >= 1 && k <= 8 && n >= 1 && n <= 128, "rbf_linear_bwd needs K <= 8, N <= 128");
+  cudaStream_t st = as_stream(stream);
+  if (num_edges == 0) {
+    cudaMemsetAsync(w_bar, 0, sizeof(float) * n * k, st);
+    if (b_bar) cudaMemsetAsync(b_bar, 0, sizeof(float) * n, st);
+    return check_launch("rbf_linear_bwd_empty");
+  }
+  const int grid = rbf_linear_bwd_grid(num_edges);
+  float* part = reinterpret_cast<float*>(workspace);
+  rbf_linear_bwd_kernel<<<grid, 256, 0, st>>>(rbf, num_edges, k, w, n, g, ldg, rbf_bar, part);
+  if (check_launch("rbf_linear_bwd")) return 1;
+  // part rows are [n*k weights | n biases]
+  const int len = n * k + n;
+  reduce_parts_kernel<<<(len + 31) / 32, 256, 0, st>>>(part, grid, len, n * k, w_bar, b_bar);
+  return check_launch("rbf_linear_bwd_reduce");
 }
 
 int egn_rbf_bwd(const float* geo, const float* rbf_bar, int64_t num_edges, int k_rbf,

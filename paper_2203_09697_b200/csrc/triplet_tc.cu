@@ -162,10 +162,24 @@ __global__ void __launch_bounds__(kThreads, 1) fwd_kernel(Args a) {
       }
       named_sync(1, kBuilders);
       const int nslab = (n + 3) >> 2;
+      // X gather for slab s + 1 is issued before slab s is built (latency hiding)
+      auto load_x = [&](int s, float* xv) {
+#pragma unroll
+        for (int jj = 0; jj < 4 / JS; ++jj) {
+          const int q = 4 * s + jt + jj * JS;
+          xv[jj] = q < n ? a.X[static_cast<int64_t>(RQ[q]) * a.ld + a.c0 + c] : 0.f;
+        }
+      };
       for (int p0 = 0; p0 < n; p0 += kMaxNB) {
         const int np = min(kMaxNB, n - p0);
         const int nb = (np + 15) & ~15;
+        float xnext[4 / JS];
+        load_x(0, xnext);
         for (int s = 0; s < nslab; ++s, ++it) {
+          float xcur[4 / JS];
+#pragma unroll
+          for (int jj = 0; jj < 4 / JS; ++jj) xcur[jj] = xnext[jj];
+          if (s + 1 < nslab) load_x(s + 1, xnext);
           const int slot = it % NS;
           mbar_wait(&empty[slot], ((it / NS) & 1) ^ 1);
           uint8_t* ahi = ring + slot * SLOT;
@@ -180,7 +194,7 @@ __global__ void __launch_bounds__(kThreads, 1) fwd_kernel(Args a) {
             float y[8];
             if (q < n) {
               const float4 g = U[q];
-              const float x = a.X[static_cast<int64_t>(RQ[q]) * a.ld + a.c0 + c];
+              const float x = xcur[jj];
               float rb[kMaxK];
 #pragma unroll
               for (int k = 0; k < kMaxK; ++k) {
@@ -331,15 +345,17 @@ int tc_fwd(const int64_t* edge_ptr, const int32_t* rev, const float4* geo, int64
     const int gcap = std::max(4, (max_degree + 3) & ~3);
     const int geo_bytes = gcap * 20;
     // ring depth: up to 4 slots, fewer to fit two CTAs per SM when possible
-    int nslot = 4;
-    while (nslot > 2 && static_cast<size_t>(nslot) * slot + geo_bytes + 1024 > 110 * 1024) --nslot;
+    int nslot = 3;
+    while (nslot > 2 && static_cast<size_t>(nslot) * slot + geo_bytes + 1024 > 72 * 1024) --nslot;
     const size_t smem = static_cast<size_t>(nslot) * slot + geo_bytes + 1024;
     tc::Args a{edge_ptr, rev, geo, nv, X, W, S, K, L, dg, c0, rp.gamma, rp.step, nbmax, nslot, gcap, min_n};
     auto kern = M == 128 ? tc::fwd_kernel<128> : tc::fwd_kernel<64>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     int per_sm = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, tc::kThreads, smem);
-    per_sm = std::max(1, std::min(per_sm, 2 * nbmax <= 256 ? 2 : 1));  // TMEM: 512 columns per SM
+    uint32_t tcols = 32;
+    while (tcols < 2u * nbmax) tcols <<= 1;
+    per_sm = std::max(1, std::min<int>(per_sm, 512 / tcols));  // TMEM: 512 columns per SM
     const int grid = static_cast<int>(std::min<int64_t>(nv, static_cast<int64_t>(kNumSMs) * per_sm));
     kern<<<grid, tc::kThreads, smem, st>>>(a);
     if (int rc = check_launch("triplet_fwd_tc")) return rc;

@@ -122,7 +122,7 @@ class Engine:
         de = c.d_e
         L = ops.linear
         rbf = ops.rbf(bg.geo, c.k_rbf, c.cutoff)
-        m = torch.addmm(w["edge_init.b"], rbf, w["edge_init.w"].t())  # K = k_rbf (6): cuBLAS
+        m = ops.rbf_linear(rbf, w["edge_init.w"], w["edge_init.b"])  # K = k_rbf (6)
         u = torch.zeros((bg.num_graphs, c.d_u), dtype=torch.float32, device=bg.device)
         v = None
         blocks = []
@@ -133,7 +133,7 @@ class Engine:
             X = L(down, w[p + "tu.bilinear_a"]) if gem else down
             Wk = self._sbf_weight(b)
             S = ops.triplet_fwd(bg.edge_ptr, bg.rev, bg.geo, X, Wk, c.cutoff, max_degree=bg.max_deg)
-            g = rbf @ w[p + "tu.rbf_gate"].t()  # K = k_rbf (6): cuBLAS
+            g = ops.rbf_linear(rbf, w[p + "tu.rbf_gate"])  # K = k_rbf (6)
             if gem:
                 Y, Z = L(S, w[p + "tu.bilinear_proj"], aux=g, flags=ops.EPI_MUL_AUX)  # Y = (S P^T) * g
                 st["Z"] = Z
@@ -247,8 +247,7 @@ class Engine:
             else:
                 S_bar = Y_bar * st["g"]
                 g_bar = Y_bar * st["S"]
-            ops.wgrad(g_bar, fw.rbf, out=gr[p + "tu.rbf_gate"])  # N = k_rbf (6): split-K
-            rbf_bar.addmm_(g_bar, w[p + "tu.rbf_gate"])
+            ops.rbf_linear_bwd(fw.rbf, w[p + "tu.rbf_gate"], g_bar, rbf_bar, gr[p + "tu.rbf_gate"])
             X_bar, Wk_bar = ops.triplet_bwd(bg.edge_ptr, bg.rev, bg.geo, st["X"], st["Wk"], c.cutoff,
                                             S_bar, eg, max_degree=bg.max_deg)
             wp_bar = Wk_bar.permute(2, 0, 1).reshape(Wk_bar.shape[2], -1)  # [dg, K*L]
@@ -263,9 +262,7 @@ class Engine:
             wg(down_bar, st["m"], gr[p + "tu.down"])
             m_bar = L(down_bar, w[p + "tu.down"], w_mn=True, resid=m_in_bar)
         # edge init (engine.py:109-111), K = k_rbf: cuBLAS
-        ops.wgrad(m_bar, fw.rbf, out=gr["edge_init.w"])
-        cs(m_bar, out=gr["edge_init.b"])
-        rbf_bar.addmm_(m_bar, w["edge_init.w"])
+        ops.rbf_linear_bwd(fw.rbf, w["edge_init.w"], m_bar, rbf_bar, gr["edge_init.w"], gr["edge_init.b"])
         ops.rbf_bwd(bg.geo, rbf_bar, c.cutoff, eg)
         return ops.positions_bwd(bg.edge_ptr, bg.rev, bg.geo, eg)
 

@@ -49,6 +49,16 @@ class BatchGraph:
     def edge_graph_ptr(self) -> torch.Tensor:
         return self.edge_ptr[self.graph_ptr]
 
+    def update_positions(self, pos: torch.Tensor) -> None:
+        """Copy new positions into this batch and recompute the packed geometry in
+        place, keeping the topology (edges, triplets): a training pass over a fixed
+        dataset (train_simple, egn/tasks.py:187-209) revisits the same graphs, so the
+        neighbour list is built once per batch and its buffers stay valid for a
+        captured step."""
+        self.pos.copy_(pos, non_blocking=True)
+        ops.call("egn_geometry", ops.ptr(self.pos), ops.ptr(self.src), ops.ptr(self.recv), self.num_edges,
+                 ops.ptr(self.geo), None, None, ops.stream())
+
 
 def _as_positions(systems) -> tuple[np.ndarray, list[int]]:
     if hasattr(systems, "positions") or (isinstance(systems, np.ndarray) and systems.ndim == 2):

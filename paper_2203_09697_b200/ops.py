@@ -81,6 +81,40 @@ def rbf(geo, k_rbf, cutoff):
     return out
 
 
+def rbf_linear(rbf_t, w, b=None, out=None):
+    """out = rbf w^T (+ b) for a K <= 8 basis (egn_rbf_linear)."""
+    e, k = rbf_t.shape
+    n = w.shape[0]
+    if out is None:
+        out = torch.empty((e, n), dtype=torch.float32, device=rbf_t.device)
+    if k > 8 or n % 4 or out.stride(0) % 4 or out.stride(1) != 1 or out.data_ptr() % 16:
+        # widths outside the native kernel's tiling (e.g. GemNet-XL d_e = 1302): fp32 cuBLAS
+        if b is not None:
+            return torch.addmm(b, rbf_t, w.t(), out=out)
+        return torch.mm(rbf_t, w.t(), out=out)
+    call("egn_rbf_linear", ptr(_c(rbf_t, torch.float32)), e, k, ptr(_c(w, torch.float32)),
+         ptr(_c(b, torch.float32)) if b is not None else None, n, ptr(out), out.stride(0), stream())
+    return out
+
+
+def rbf_linear_bwd(rbf_t, w, g, rbf_bar, w_bar, b_bar=None):
+    """Adjoint of rbf_linear: rbf_bar += g w; w_bar = g^T rbf; b_bar = column sums of g."""
+    e, k = rbf_t.shape
+    n = w.shape[0]
+    if g.stride(1) != 1:
+        g = g.contiguous()
+    if k > 8 or n > 128:
+        rbf_bar.addmm_(g, w)
+        wgrad(g, rbf_t, out=w_bar)
+        if b_bar is not None:
+            column_sum(g, out=b_bar)
+        return
+    nbytes = call("egn_rbf_linear_bwd_workspace_bytes", e, k, n)
+    ws = _workspace_named("rbflin", nbytes, g.device)
+    call("egn_rbf_linear_bwd", ptr(_c(rbf_t, torch.float32)), e, k, ptr(_c(w, torch.float32)), n, ptr(g), g.stride(0),
+         ptr(rbf_bar), ptr(w_bar), ptr(b_bar) if b_bar is not None else None, ptr(ws), stream())
+
+
 def sbf(geo, edge_ptr, tri_ptr, num_triplets, k_rbf, l_sbf, cutoff):
     out = torch.empty((num_triplets, k_rbf * l_sbf), dtype=torch.float32, device=geo.device)
     call("egn_sbf", ptr(geo), ptr(edge_ptr), ptr(tri_ptr), edge_ptr.shape[0] - 1, int(k_rbf), int(l_sbf),

@@ -60,7 +60,7 @@ class Trainer:
 
     def __init__(self, params: ModelParams, systems, e_target, f_target=None, w_energy=1.0,
                  w_forces=0.0, device="cuda", graph: BatchGraph | None = None, comm=None,
-                 global_graphs: int | None = None):
+                 global_graphs: int | None = None, cuda_graph: bool = False):
         """comm / global_graphs: graph-aligned graph parallelism.  Every rank owns
         whole graphs (its own BatchGraph), so no edge or node crosses a rank; the
         loss is normalised over the global batch (egn/tasks.py:158-185) and the
@@ -78,6 +78,13 @@ class Trainer:
         if self.n == 0:
             raise ValueError("dataset is empty")
         self.comm = comm
+        # CUDA-graph replay of the whole step (forward, backward, all-reduce, SGD) for a
+        # fixed batch: removes the host launch cost of ~500 kernels per step
+        self.cuda_graph = bool(cuda_graph)
+        self._graph = None
+        self._graph_key = None
+        self._graph_loss = None
+        self.kernels_per_step = None
         self.e_target = torch.as_tensor(np.asarray(e_target, dtype=np.float64), device=bg.device)
         self.f_target = (torch.as_tensor(np.asarray(f_target, dtype=np.float64), device=bg.device)
                          if f_target is not None else None)
@@ -91,6 +98,15 @@ class Trainer:
             raise ValueError("set_inputs expects the same per-graph atom counts")
         self.bg, self.e_target, self.f_target = bg, e_target, f_target
 
+    def update_inputs(self, positions: torch.Tensor, e_target: torch.Tensor,
+                      f_target: torch.Tensor | None = None) -> None:
+        """Copy this step's positions and targets into the resident batch buffers
+        (same topology; see BatchGraph.update_positions).  Keeps a captured step valid."""
+        self.bg.update_positions(positions)
+        self.e_target.copy_(e_target, non_blocking=True)
+        if f_target is not None:
+            self.f_target.copy_(f_target, non_blocking=True)
+
     def loss_and_grads(self):
         fw = self.engine.forward(self.bg)
         loss, d_e, d_f = _seeds(fw.energy, fw.forces, self.e_target, self.f_target, self.atom_count,
@@ -98,7 +114,7 @@ class Trainer:
         self.engine.backward(self.bg, fw, d_e, d_f)
         return loss
 
-    def step(self, lr: float) -> torch.Tensor:
+    def _step_eager(self, lr: float) -> torch.Tensor:
         loss = self.loss_and_grads()
         if self.comm is not None:
             self.comm.all_reduce_(self.weights.grad_flat, phase="backward", block=-1, stage="params",
@@ -106,6 +122,39 @@ class Trainer:
             self.comm.all_reduce_(loss, phase="backward", block=-1, stage="loss", level="global")
         if lr != 0.0:
             self.weights.sgd_(lr)
+        return loss
+
+    def step(self, lr: float) -> torch.Tensor:
+        if not self.cuda_graph:
+            return self._step_eager(lr)
+        key = (id(self.bg), id(self.e_target), id(self.f_target), float(lr))
+        if self._graph is not None and self._graph_key == key:
+            self._graph.replay()
+            return self._graph_loss
+        # this call's update runs eagerly (it also sizes every workspace); the same
+        # step is then captured, not executed, and replayed from the next call on
+        from . import _lib
+
+        loss = self._step_eager(lr)
+        before = _lib.LAUNCH_COUNTER["kernels"]
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        graph = torch.cuda.CUDAGraph()
+        try:
+            with torch.cuda.stream(side):
+                with torch.cuda.graph(graph, stream=side):
+                    self._graph_loss = self._step_eager(lr)
+        except Exception as exc:  # e.g. a collective backend that cannot be captured
+            import sys
+
+            torch.cuda.synchronize()
+            print(f"[egn] CUDA-graph capture of the training step failed ({exc!r}); running eagerly",
+                  file=sys.stderr)
+            self.cuda_graph = False
+            return loss
+        torch.cuda.current_stream().wait_stream(side)
+        self.kernels_per_step = _lib.LAUNCH_COUNTER["kernels"] - before
+        self._graph, self._graph_key = graph, key
         return loss
 
     def params(self) -> ModelParams:
