@@ -31,6 +31,8 @@
 // collinear triplets (both factors vanish there).
 #include <algorithm>
 
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace egn {
@@ -666,7 +668,8 @@ int egn_triplet_fwd(const int64_t* edge_ptr, const int32_t* rev, const float* ge
   // centres: tensor-core kernel (triplet_tc.cu) when the degree bound is known, else
   // the generic CUDA-core kernel
   int min_n = 0;
-  if (fast_supported(k_rbf, l_sbf, dg)) {
+  static const bool tc_all = [] { const char* e = std::getenv("EGN_TRIPLET_TC_ALL"); return e && e[0] == '1'; }();
+  if (fast_supported(k_rbf, l_sbf, dg) && !(tc_all && tc_fwd_supported(k_rbf, l_sbf, dg, max_degree))) {
     if (int rc = fast_fwd(edge_ptr, rev, g4, num_nodes, X, W, k_rbf, l_sbf, dg, rp, S, st)) return rc;
     if (max_degree >= 0 && max_degree <= kFastMaxDeg) return 0;
     min_n = kFastMaxDeg;

@@ -513,7 +513,11 @@ int fast_bwd(const int64_t* edge_ptr, const int32_t* rev, const float4* geo, int
   const size_t smem = (4 * fast::kN + ((fast::kN * 6 + 3) & ~3) + fast::kN * 128 + fast::kN * fast::kCB +
                        2 * 6 * 7 * fast::kCB) * sizeof(float);
   auto k2 = fast::bw2_kernel<6, 7>;
-  cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  static bool k2_configured = false;
+  if (!k2_configured) {
+    cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    k2_configured = true;
+  }
   k2<<<dim3(gx, ncb), fast::kT, smem, st>>>(edge_ptr, rev, geo, nv, X, W, dg, rp, Sbar, Xbar, wpart, ddpart, ne);
   if (check_launch("triplet_bw2_fast")) return 1;
   fast::reduce_wbar_kernel<<<grid_for(static_cast<int64_t>(K) * L * dg, 256), 256, 0, st>>>(wpart, gx, K, L, dg,

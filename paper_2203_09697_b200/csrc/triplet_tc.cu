@@ -14,16 +14,17 @@
 // M = channel block (64 or 128 channels), N = rows p (<= 256 per pass), fp32-accurate
 // through the 3xTF32 split (A_lo.B_hi + A_hi.B_lo + A_hi.B_hi).
 //
-// Warp roles (288 threads, persistent CTAs over centres):
-//   warps 0-3 : operand builders -- per slab of 4 in-edges they write A (thread = channel:
+// Warp roles (416 threads, persistent CTAs over centres):
+//   warps 0-7 : operand builders -- per slab of 4 in-edges they write A (thread = channel:
 //               X gather, rbf, W column in registers) and B (Chebyshev table of the
 //               centre's angles) as hi/lo in the K-major SWIZZLE_128B layout;
-//   warp 4    : MMA issuer (one elected lane), D double-buffered in TMEM per pass;
-//   warps 5-8 : epilogue -- TMEM -> registers -> S rows (lanes = channels, coalesced).
+//   warp 8    : MMA issuer (one elected lane), D double-buffered in TMEM per pass;
+//   warps 9-12: epilogue -- TMEM -> registers -> S rows (lanes = channels, coalesced).
 #include <cuda_runtime.h>
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdio>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -31,8 +32,10 @@
 namespace egn {
 namespace tc {
 
-constexpr int kThreads = 288;
-constexpr int kBuilders = 128;
+constexpr int kBuilders = 256;             // warps 0-7
+constexpr int kMmaWarp = kBuilders / 32;   // warp 8
+constexpr int kThreads = kBuilders + 32 + 128;  // + MMA warp + 4 epilogue warps
+constexpr int kQChunk = 64;                // in-edges whose X rows are staged at once
 constexpr int kMaxDeg = 1024;  // centre geometry staged in shared memory
 constexpr int kMaxNB = 256;    // rows p per pass (MMA N)
 constexpr int kMaxK = 8;
@@ -100,7 +103,17 @@ struct Args {
   float gamma, step;
   int nbmax, nslot, gcap;  // rows per pass (TMEM columns per buffer), ring slots, staged degree cap
   int min_n;               // centres with n <= min_n are left to the CUDA-core small-degree kernel
+  long long* trace;        // debug timeline (EGN_TC_TRACE): CTA 0, [role][centre]
+  int qchunk;              // in-edges staged per X/rbf chunk (power of two, multiple of 4)
 };
+#define TC_TRACE(role, idx)                                                            \
+  do {                                                                                 \
+    if (a.trace && blockIdx.x == 0 && (idx) < 32 && (threadIdx.x & 31) == 0) {         \
+      long long t_;                                                                    \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                           \
+      a.trace[(role) * 32 + (idx)] = t_;                                               \
+    }                                                                                  \
+  } while (0)
 
 template <int M>
 __global__ void __launch_bounds__(kThreads, 1) fwd_kernel(Args a) {
@@ -112,6 +125,8 @@ __global__ void __launch_bounds__(kThreads, 1) fwd_kernel(Args a) {
   uint8_t* ring = sm;
   float4* U = reinterpret_cast<float4*>(sm + a.nslot * SLOT);  // [gcap] centre out-edge geometry
   int32_t* RQ = reinterpret_cast<int32_t*>(U + a.gcap);        // [gcap] in-edge ids
+  float* XS = reinterpret_cast<float*>(RQ + a.gcap);           // [kQChunk][M] staged X rows
+  float* RB = XS + a.qchunk * M;                               // [qchunk][kMaxK] rbf values
   __shared__ __align__(8) uint64_t full[4], empty[4], dfull[2], dempty[2];
   __shared__ uint32_t tbase;
 
@@ -130,7 +145,7 @@ __global__ void __launch_bounds__(kThreads, 1) fwd_kernel(Args a) {
   }
   uint32_t tcols = 32;
   while (tcols < 2u * a.nbmax) tcols <<= 1;
-  if (warp == 4) {
+  if (warp == kMmaWarp) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(&tbase)), "r"(tcols));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
@@ -138,11 +153,12 @@ __global__ void __launch_bounds__(kThreads, 1) fwd_kernel(Args a) {
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem = tbase;
+  if (tid == 0) TC_TRACE(7, 0);
 
-  if (warp < 4) {
+  if (warp < kBuilders / 32) {
     // ------------------------------------------------ builders
     // thread -> channel c (fixed), k-steps j = jt, jt + JS, ... of each slab
-    constexpr int JS = kBuilders / M;  // 2 (M = 64) or 1 (M = 128)
+    constexpr int JS = kBuilders / M;  // 4 (M = 64) or 2 (M = 128)
     const int c = tid % M, jt = tid / M;
     float w[kMaxK][8];
 #pragma unroll
@@ -151,35 +167,41 @@ __global__ void __launch_bounds__(kThreads, 1) fwd_kernel(Args a) {
       for (int l = 0; l < 8; ++l)
         w[k][l] = (k < a.K && l < a.L) ? a.W[(static_cast<int64_t>(k) * a.L + l) * a.ld + a.c0 + c] : 0.f;
     uint32_t it = 0;
+    int ci = -1;
     for (int64_t j = blockIdx.x; j < a.nv; j += gridDim.x) {
       const int64_t off = a.edge_ptr[j];
       const int n = static_cast<int>(a.edge_ptr[j + 1] - off);
       if (n <= 0 || n <= a.min_n) continue;
+      ++ci;
+      if (tid == 0) TC_TRACE(0, ci);
       named_sync(1, kBuilders);  // previous centre's readers of U/RQ are done
       for (int q = tid; q < n; q += kBuilders) {
         U[q] = a.geo[off + q];
         RQ[q] = a.rev[off + q];
       }
       named_sync(1, kBuilders);
+      if (tid == 0) TC_TRACE(1, ci);
       const int nslab = (n + 3) >> 2;
-      // X gather for slab s + 1 is issued before slab s is built (latency hiding)
-      auto load_x = [&](int s, float* xv) {
-#pragma unroll
-        for (int jj = 0; jj < 4 / JS; ++jj) {
-          const int q = 4 * s + jt + jj * JS;
-          xv[jj] = q < n ? a.X[static_cast<int64_t>(RQ[q]) * a.ld + a.c0 + c] : 0.f;
-        }
-      };
       for (int p0 = 0; p0 < n; p0 += kMaxNB) {
         const int np = min(kMaxNB, n - p0);
         const int nb = (np + 15) & ~15;
-        float xnext[4 / JS];
-        load_x(0, xnext);
         for (int s = 0; s < nslab; ++s, ++it) {
-          float xcur[4 / JS];
-#pragma unroll
-          for (int jj = 0; jj < 4 / JS; ++jj) xcur[jj] = xnext[jj];
-          if (s + 1 < nslab) load_x(s + 1, xnext);
+          if ((s & (a.qchunk / 4 - 1)) == 0) {
+            // stage X rows and rbf values of the next qchunk in-edges (coalesced rows)
+            const int q0 = 4 * s, nq = min(a.qchunk, n - q0);
+            named_sync(1, kBuilders);
+            for (int i = tid; i < nq * (M / 4); i += kBuilders) {
+              const int qq = i / (M / 4), c4 = i - qq * (M / 4);
+              *reinterpret_cast<float4*>(XS + qq * M + 4 * c4) = __ldg(reinterpret_cast<const float4*>(
+                  a.X + static_cast<int64_t>(RQ[q0 + qq]) * a.ld + a.c0 + 4 * c4));
+            }
+            for (int i = tid; i < nq * kMaxK; i += kBuilders) {
+              const int qq = i / kMaxK, k = i - qq * kMaxK;
+              const float dd = U[q0 + qq].w - a.step * k;
+              RB[i] = k < a.K ? __expf(-a.gamma * dd * dd) : 0.f;
+            }
+            named_sync(1, kBuilders);
+          }
           const int slot = it % NS;
           mbar_wait(&empty[slot], ((it / NS) & 1) ^ 1);
           uint8_t* ahi = ring + slot * SLOT;
@@ -191,16 +213,13 @@ __global__ void __launch_bounds__(kThreads, 1) fwd_kernel(Args a) {
           for (int jj = 0; jj < 4 / JS; ++jj) {
             const int js = jt + jj * JS;
             const int q = 4 * s + js;
+            const int qq = q & (a.qchunk - 1);
             float y[8];
             if (q < n) {
-              const float4 g = U[q];
-              const float x = xcur[jj];
+              const float x = XS[qq * M + c];
               float rb[kMaxK];
 #pragma unroll
-              for (int k = 0; k < kMaxK; ++k) {
-                const float dd = g.w - a.step * k;
-                rb[k] = k < a.K ? __expf(-a.gamma * dd * dd) : 0.f;
-              }
+              for (int k = 0; k < kMaxK; ++k) rb[k] = RB[qq * kMaxK + k];
 #pragma unroll
               for (int l = 0; l < 8; ++l) {
                 float r = 0.f;
@@ -240,14 +259,17 @@ __global__ void __launch_bounds__(kThreads, 1) fwd_kernel(Args a) {
           if (tid == 0) mbar_arrive(&full[slot]);
         }
       }
+      if (tid == 0) TC_TRACE(2, ci);
     }
-  } else if (warp == 4) {
+  } else if (warp == kMmaWarp) {
     // ------------------------------------------------ MMA issuer
     uint32_t it = 0, pass = 0;
+    int ci = -1;
     for (int64_t j = blockIdx.x; j < a.nv; j += gridDim.x) {
       const int64_t off = a.edge_ptr[j];
       const int n = static_cast<int>(a.edge_ptr[j + 1] - off);
       if (n <= 0 || n <= a.min_n) continue;
+      ++ci;
       const int nslab = (n + 3) >> 2;
       for (int p0 = 0; p0 < n; p0 += kMaxNB, ++pass) {
         const int nb = (min(kMaxNB, n - p0) + 15) & ~15;
@@ -260,6 +282,7 @@ __global__ void __launch_bounds__(kThreads, 1) fwd_kernel(Args a) {
         for (int s = 0; s < nslab; ++s, ++it) {
           const int slot = it % NS;
           mbar_wait(&full[slot], (it / NS) & 1);
+          if (s == 0) TC_TRACE(3, ci);
           asm volatile("tcgen05.fence::after_thread_sync;");
           const uint32_t ahi = su32(ring + slot * SLOT);
           const uint32_t alo = ahi + A_BYTES, bhi = alo + A_BYTES, blo = bhi + B_BYTES;
@@ -276,6 +299,7 @@ __global__ void __launch_bounds__(kThreads, 1) fwd_kernel(Args a) {
           }
           __syncwarp();
         }
+        TC_TRACE(4, ci);
       }
     }
   } else {
@@ -285,14 +309,17 @@ __global__ void __launch_bounds__(kThreads, 1) fwd_kernel(Args a) {
     const int c = M == 128 ? 32 * qd + lane : 16 * qd + lane;
     const bool active = M == 128 || lane < 16;
     uint32_t pass = 0;
+    int ci = -1;
     for (int64_t j = blockIdx.x; j < a.nv; j += gridDim.x) {
       const int64_t off = a.edge_ptr[j];
       const int n = static_cast<int>(a.edge_ptr[j + 1] - off);
       if (n <= 0 || n <= a.min_n) continue;
+      ++ci;
       for (int p0 = 0; p0 < n; p0 += kMaxNB, ++pass) {
         const int np = min(kMaxNB, n - p0);
         const uint32_t b = pass & 1;
         mbar_wait(&dfull[b], (pass >> 1) & 1);
+        if (qd == 1) TC_TRACE(5, ci);
         asm volatile("tcgen05.fence::after_thread_sync;");
         const uint32_t taddr = tmem + b * a.nbmax + (static_cast<uint32_t>(qd * 32) << 16);
         float* dst = a.S + (off + p0) * a.ld + a.c0 + c;
@@ -313,12 +340,13 @@ __global__ void __launch_bounds__(kThreads, 1) fwd_kernel(Args a) {
         asm volatile("tcgen05.fence::before_thread_sync;");
         __syncwarp();
         if (lane == 0) mbar_arrive(&dempty[b]);
+        if (qd == 1) TC_TRACE(6, ci);
       }
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
-  if (warp == 4) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(tcols));
+  if (warp == kMmaWarp) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(tcols));
 }
 
 }  // namespace tc
@@ -343,22 +371,50 @@ int tc_fwd(const int64_t* edge_ptr, const int32_t* rev, const float4* geo, int64
     const int M = (dg - c0) >= 128 ? 128 : 64;
     const int slot = 2 * M * 128 + 2 * nbmax * 128;
     const int gcap = std::max(4, (max_degree + 3) & ~3);
-    const int geo_bytes = gcap * 20;
-    // ring depth: up to 4 slots, fewer to fit two CTAs per SM when possible
+    // ring depth 2-3 slots; the X/rbf staging chunk shrinks until everything fits
+    int qchunk = tc::kQChunk;
+    auto stage_bytes = [&](int qc) { return gcap * 20 + qc * (M + tc::kMaxK) * 4; };
     int nslot = 3;
-    while (nslot > 2 && static_cast<size_t>(nslot) * slot + geo_bytes + 1024 > 72 * 1024) --nslot;
-    const size_t smem = static_cast<size_t>(nslot) * slot + geo_bytes + 1024;
-    tc::Args a{edge_ptr, rev, geo, nv, X, W, S, K, L, dg, c0, rp.gamma, rp.step, nbmax, nslot, gcap, min_n};
+    while (nslot > 2 && static_cast<size_t>(nslot) * slot + stage_bytes(qchunk) + 1024 > 72 * 1024) --nslot;
+    while (qchunk > 4 && static_cast<size_t>(nslot) * slot + stage_bytes(qchunk) + 1024 > 225 * 1024) qchunk >>= 1;
+    const size_t smem = static_cast<size_t>(nslot) * slot + stage_bytes(qchunk) + 1024;
+    EGN_REQUIRE(smem <= 227 * 1024, "triplet_fwd_tc: %zu bytes of shared memory (max degree %d)", smem, max_degree);
+    static long long* trace = nullptr;
+    const bool tracing = std::getenv("EGN_TC_TRACE") != nullptr;
+    if (tracing && !trace) cudaMalloc(&trace, 8 * 32 * sizeof(long long));
+    if (tracing) cudaMemsetAsync(trace, 0, 8 * 32 * sizeof(long long), st);
+    tc::Args a{edge_ptr, rev, geo, nv, X, W, S, K, L, dg, c0, rp.gamma, rp.step, nbmax, nslot, gcap, min_n,
+               tracing ? trace : nullptr, qchunk};
     auto kern = M == 128 ? tc::fwd_kernel<128> : tc::fwd_kernel<64>;
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    int per_sm = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, tc::kThreads, smem);
+    // host-side launch configuration is cached per (kernel, shared-memory size)
+    static size_t configured[2] = {0, 0};
+    static int occ[2] = {1, 1};
+    const int ki = M == 128 ? 1 : 0;
+    if (configured[ki] != smem) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[ki], kern, tc::kThreads, smem);
+      configured[ki] = smem;
+    }
+    int per_sm = occ[ki];
     uint32_t tcols = 32;
     while (tcols < 2u * nbmax) tcols <<= 1;
     per_sm = std::max(1, std::min<int>(per_sm, 512 / tcols));  // TMEM: 512 columns per SM
     const int grid = static_cast<int>(std::min<int64_t>(nv, static_cast<int64_t>(kNumSMs) * per_sm));
     kern<<<grid, tc::kThreads, smem, st>>>(a);
     if (int rc = check_launch("triplet_fwd_tc")) return rc;
+    if (tracing) {
+      long long h[8 * 32];
+      cudaMemcpyAsync(h, trace, sizeof(h), cudaMemcpyDeviceToHost, st);
+      cudaStreamSynchronize(st);
+      const char* names[8] = {"b_centre", "b_geo", "b_done", "mma_first", "mma_done", "epi_full", "epi_done",
+                              "start"};
+      std::printf("tc fwd trace CTA 0 (us after start), grid %d, smem %zu, per_sm %d\n", grid, smem, per_sm);
+      for (int r = 0; r < 7; ++r) {
+        std::printf("%-10s", names[r]);
+        for (int i = 0; i < 12; ++i) std::printf(" %7.2f", h[r * 32 + i] ? (h[r * 32 + i] - h[7 * 32]) * 1e-3 : -1.0);
+        std::printf("\n");
+      }
+    }
     if (M == 64) break;
   }
   return 0;

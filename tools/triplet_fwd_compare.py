@@ -4,11 +4,32 @@ import numpy as np, torch
 from paper_2203_09697_b200 import ops
 from paper_2203_09697_b200.graph import build_batch
 sys.path.insert(0, '/root/repo/tools')
-from c5_sweep import cloud, time_it
+from c5_sweep import cloud
+
+
+def time_it(fn, iters, flush):
+    """Device time of fn from CUDA-graph replay (no host launch cost)."""
+    fn()
+    torch.cuda.synchronize()
+    st = torch.cuda.Stream()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(st):
+        with torch.cuda.graph(g, stream=st):
+            for _ in range(iters):
+                fn()
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    g.replay()
+    e.record()
+    torch.cuda.synchronize()
+    return s.elapsed_time(e) / 1000.0 / iters
 flush = torch.empty(64*1024*1024, device='cuda')
-for deg in (32, 128, 500):
-    bg = build_batch([cloud(1000, deg, 6.0, deg)], 6.0)
-    for dg in (64, 128):
+import bench
+wl = bench.WORKLOADS['gemnet-t-oc20']
+cases = [('C2', build_batch(bench._systems(wl, wl['graphs']), 6.0))] + [(d, build_batch([cloud(1000, d, 6.0, d)], 6.0)) for d in (32, 128, 500)]
+for deg, bg in cases:
+    for dg in (64,):
         X = torch.randn((bg.num_edges, dg), device='cuda'); W = torch.randn((6, 7, dg), device='cuda') / 6.5
         # force the tensor-core path for all centres (max_degree > 64 and dg % 64 == 0): call the C ABI with min_n=0 via a
         # large max_degree and the fast path disabled is not exposed; time the default dispatch and the generic path
