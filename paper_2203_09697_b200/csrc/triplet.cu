@@ -542,6 +542,11 @@ int fast_bwd(const int64_t* edge_ptr, const int32_t* rev, const float4* geo, int
              float* Wbar, float4* edge_grad, void* ws, cudaStream_t st);
 constexpr int kFastMaxDeg = 64;
 bool tc_fwd_supported(int K, int L, int dg, int max_degree);
+bool tc_bwd_supported(int K, int L, int dg, int max_degree);
+int64_t tc_bwd_workspace_bytes(int64_t nv, int K, int L);
+int tc_bwd(const int64_t* edge_ptr, const int32_t* rev, const float4* geo, int64_t nv, int max_degree,
+           const float* X, const float* W, int K, int L, int dg, RbfParams rp, const float* Sbar, float* Xbar,
+           float* Wbar, float4* edge_grad, void* ws, int min_n, cudaStream_t st);
 int tc_fwd(const int64_t* edge_ptr, const int32_t* rev, const float4* geo, int64_t nv, int max_degree,
            const float* X, const float* W, int K, int L, int dg, RbfParams rp, float* S, int min_n,
            cudaStream_t st);
@@ -693,10 +698,13 @@ static int64_t generic_ws_bytes(int64_t num_nodes, int k_rbf, int l_sbf, int dg)
   return grid * k_rbf * l_sbf * dg * 4;
 }
 
+static int64_t fast_ws_bytes(int64_t num_nodes, int64_t num_edges, int k_rbf, int l_sbf, int dg) {
+  return fast_supported(k_rbf, l_sbf, dg) ? fast_bwd_workspace_bytes(num_nodes, num_edges, k_rbf, l_sbf, dg) : 0;
+}
+
 int64_t egn_triplet_bwd_workspace_bytes(int64_t num_nodes, int64_t num_edges, int k_rbf, int l_sbf, int dg) {
-  int64_t b = generic_ws_bytes(num_nodes, k_rbf, l_sbf, dg);
-  if (fast_supported(k_rbf, l_sbf, dg)) b += fast_bwd_workspace_bytes(num_nodes, num_edges, k_rbf, l_sbf, dg);
-  return b;
+  return generic_ws_bytes(num_nodes, k_rbf, l_sbf, dg) + fast_ws_bytes(num_nodes, num_edges, k_rbf, l_sbf, dg) +
+         tc_bwd_workspace_bytes(num_nodes, k_rbf, l_sbf);
 }
 
 int egn_triplet_bwd(const int64_t* edge_ptr, const int32_t* rev, const float* geo,
@@ -713,7 +721,8 @@ int egn_triplet_bwd(const int64_t* edge_ptr, const int32_t* rev, const float* ge
   const float4* g4 = reinterpret_cast<const float4*>(geo);
   float4* eg = reinterpret_cast<float4*>(edge_grad);
   int min_n = 0, accumulate = 0;
-  if (fast_supported(k_rbf, l_sbf, dg)) {
+  static const bool tc_all = [] { const char* e = std::getenv("EGN_TRIPLET_TC_ALL"); return e && e[0] == '1'; }();
+  if (fast_supported(k_rbf, l_sbf, dg) && !(tc_all && tc_bwd_supported(k_rbf, l_sbf, dg, max_degree))) {
     char* fws = reinterpret_cast<char*>(workspace) + generic_ws_bytes(num_nodes, k_rbf, l_sbf, dg);
     if (int rc = fast_bwd(edge_ptr, rev, g4, num_nodes, num_edges, X, W, k_rbf, l_sbf, dg, rp, S_bar, X_bar,
                           W_bar, eg, fws, st))
@@ -721,6 +730,14 @@ int egn_triplet_bwd(const int64_t* edge_ptr, const int32_t* rev, const float* ge
     if (max_degree >= 0 && max_degree <= kFastMaxDeg) return 0;
     min_n = kFastMaxDeg;
     accumulate = 1;
+  }
+  // centres above the small-degree kernel's range: tensor-core backward (triplet_tc_bwd.cu)
+  if (tc_bwd_supported(k_rbf, l_sbf, dg, max_degree)) {
+    if (!accumulate) cudaMemsetAsync(W_bar, 0, sizeof(float) * k_rbf * l_sbf * dg, st);
+    char* tws = reinterpret_cast<char*>(workspace) + generic_ws_bytes(num_nodes, k_rbf, l_sbf, dg) +
+                fast_ws_bytes(num_nodes, num_edges, k_rbf, l_sbf, dg);
+    return tc_bwd(edge_ptr, rev, g4, num_nodes, max_degree, X, W, k_rbf, l_sbf, dg, rp, S_bar, X_bar, W_bar, eg,
+                  tws, min_n, st);
   }
 #define EGN_BWD(CW, GC, R) \
   return launch_bwd<CW, GC, R>(edge_ptr, rev, g4, num_nodes, X, W, k_rbf, l_sbf, dg, max_degree, rp, S_bar, X_bar, \
