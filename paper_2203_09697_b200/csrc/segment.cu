@@ -219,15 +219,6 @@ __global__ void force_bwd_kernel(const int32_t* __restrict__ recv, const float4*
   }
 }
 
-__global__ void reduce_rows_kernel(const float* __restrict__ part, int nparts, int64_t len,
-                                   float* __restrict__ out) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < len;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    float s = 0.f;
-    for (int p = 0; p < nparts; ++p) s += part[p * len + i];
-    out[i] = s;
-  }
-}
 
 // ---------------------------------------------------------------- K <= 8 linears of the basis
 // out[e, n] = sum_k rbf[e, k] W[n, k] (+ b[n]): edge_init (engine.py:109-111) and the
@@ -501,7 +492,7 @@ int egn_force_head_bwd(const int32_t* recv, const float* geo, int64_t num_edges,
                                            scale, f_bar, m_bar, part, reinterpret_cast<float4*>(edge_grad));
     if (check_launch("force_head_bwd")) return 1;
   }
-  reduce_rows_kernel<<<grid_for(d, 128), 128, 0, st>>>(part, grid * 8, d, w_bar);
+  reduce_parts_kernel<<<(d + 31) / 32, 256, 0, st>>>(part, grid * 8, d, d, w_bar, nullptr);
   return check_launch("force_head_bwd_reduce");
 }
 
@@ -520,7 +511,7 @@ int egn_rbf_linear(const float* rbf, int64_t num_edges, int k, const float* w, c
 
 static int rbf_linear_bwd_grid(int64_t num_edges) {
   const int64_t tiles = (num_edges + kRlTile - 1) / kRlTile;
-  return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(tiles, kNumSMs)));
+  return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(tiles, kNumSMs * 4)));
 }
 
 int64_t egn_rbf_linear_bwd_workspace_bytes(int64_t num_edges, int k, int n) {
@@ -582,7 +573,7 @@ int egn_column_sum(const float* x, int64_t rows, int d, int64_t ld, float* out, 
   const int threads = d >= 256 ? 256 : ((d + 31) / 32) * 32;
   column_sum_partial_kernel<<<chunks, threads, 0, st>>>(x, rows, d, ld, part);
   if (check_launch("column_sum_partial")) return 1;
-  reduce_rows_kernel<<<grid_for(d, 128), 128, 0, st>>>(part, chunks, d, out);
+  reduce_parts_kernel<<<(d + 31) / 32, 256, 0, st>>>(part, chunks, d, d, out, nullptr);
   return check_launch("column_sum_reduce");
 }
 
