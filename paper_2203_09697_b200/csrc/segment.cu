@@ -472,7 +472,7 @@ int egn_force_head_fwd(const int64_t* edge_ptr, const int32_t* rev, const float*
 }
 
 int64_t egn_force_head_bwd_workspace_bytes(int64_t num_edges, int d) {
-  int grid = grid_for(num_edges * 32, 256, 148 * 2);
+  int grid = grid_for(num_edges * 32, 256, 148 * 6);
   return static_cast<int64_t>(grid) * 8 * d * 4;
 }
 
@@ -485,7 +485,7 @@ int egn_force_head_bwd(const int32_t* recv, const float* geo, int64_t num_edges,
     cudaMemsetAsync(w_bar, 0, sizeof(float) * d, st);
     return check_launch("force_head_bwd_empty");
   }
-  int grid = grid_for(num_edges * 32, 256, 148 * 2);
+  int grid = grid_for(num_edges * 32, 256, 148 * 6);
   float* part = reinterpret_cast<float*>(workspace);
   for (int c0 = 0; c0 < d; c0 += 512) {
     force_bwd_kernel<<<grid, 256, 0, st>>>(recv, reinterpret_cast<const float4*>(geo), num_edges, m, d, c0, w,

@@ -210,7 +210,8 @@ class Engine:
                 # sym (engine.py:195-200): m = m2 + m2[rev] Wsym^T
                 wg(m_bar, st["m2r"], gr[p + "sym.w"])
                 t = L(m_bar, w[p + "sym.w"], w_mn=True)
-                m2_bar = ops.gather_rows(bg.rev, t, out=m_bar.clone(), accumulate=True)
+                # m_bar is dead after this point of the block: accumulate in place
+                m2_bar = ops.gather_rows(bg.rev, t, out=m_bar, accumulate=True)
                 # EU2 (engine.py:180-192)
                 wg(m2_bar, st["a2"], gr[p + "eu2.w2"], gr[p + "eu2.b2"])
                 h2_bar = L(m2_bar, w[p + "eu2.w2"], w_mn=True, aux=st["h2"], flags=ops.EPI_DSILU_AUX)
@@ -218,10 +219,10 @@ class Engine:
                 wg(h2_bar, st["m_new"], gr[p + "eu2.w1"][:, :de], gr[p + "eu2.b1"])
                 pv_bar = ops.aggregate_in_edges(bg.edge_ptr, bg.rev, h2_bar)
                 wg(pv_bar, st["v"], gr[p + "eu2.w1"][:, de:])
-                v_bar = L(pv_bar, w1[:, de:].contiguous(), w_mn=True, resid=v_bar)
-                m_new_bar = L(h2_bar, w1[:, :de].contiguous(), w_mn=True, resid=m2_bar)
+                v_bar = L(pv_bar, w1[:, de:], w_mn=True, resid=v_bar)
+                m_new_bar = L(h2_bar, w1[:, :de], w_mn=True, resid=m2_bar)
             else:
-                m_new_bar = m_bar.clone()
+                m_new_bar = m_bar  # dead after this point of the block
             # EA + NU (engine.py:166-177)
             wg(v_bar, st["av"], gr[p + "nu.w2"], gr[p + "nu.b2"])
             hv_bar = L(v_bar, w[p + "nu.w2"], w_mn=True, aux=st["hv"], flags=ops.EPI_DSILU_AUX)
@@ -234,17 +235,18 @@ class Engine:
             w1 = w[p + "eu.w1"]
             wg(h_bar, st["m"], gr[p + "eu.w1"][:, :de], gr[p + "eu.b1"])
             wg(h_bar, st["ta"], gr[p + "eu.w1"][:, de:])
-            m_in_bar = L(h_bar, w1[:, :de].contiguous(), w_mn=True, resid=m_new_bar)
-            ta_bar = L(h_bar, w1[:, de:].contiguous(), w_mn=True)
+            m_in_bar = L(h_bar, w1[:, :de], w_mn=True, resid=m_new_bar)
+            ta_bar = L(h_bar, w1[:, de:], w_mn=True)
             # TU (engine.py:118-149)
             wg(ta_bar, st["Y"], gr[p + "tu.up"])
-            Y_bar = L(ta_bar, w[p + "tu.up"], w_mn=True)
             if gem:
-                Z_bar = Y_bar * st["g"]
+                # Z_bar = Y_bar * g fused into the GEMM epilogue (second output Y_bar)
+                Z_bar, Y_bar = L(ta_bar, w[p + "tu.up"], w_mn=True, aux=st["g"], flags=ops.EPI_MUL_AUX)
                 g_bar = Y_bar * st["Z"]
                 wg(Z_bar, st["S"], gr[p + "tu.bilinear_proj"])
                 S_bar = L(Z_bar, w[p + "tu.bilinear_proj"], w_mn=True)
             else:
+                Y_bar = L(ta_bar, w[p + "tu.up"], w_mn=True)
                 S_bar = Y_bar * st["g"]
                 g_bar = Y_bar * st["S"]
             ops.rbf_linear_bwd(fw.rbf, w[p + "tu.rbf_gate"], g_bar, rbf_bar, gr[p + "tu.rbf_gate"])
