@@ -302,7 +302,7 @@ def run_ours(args, wl):
         # graph-aligned centre partition: no halo, one gradient all-reduce per step
         comm = DistComm()
         tr = Trainer(params, None, e_t, f_t, 1.0, wl["w_forces"], graph=bg, comm=comm,
-                     global_graphs=graphs * world, cuda_graph=use_graph and backend == "nccl")
+                     global_graphs=graphs * world, cuda_graph=use_graph)
         parallelism = f"gp{world} (graph-aligned centre partition: no halo, gradient all-reduce, {backend})"
     else:
         comm = DistComm()

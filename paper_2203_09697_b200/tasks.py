@@ -115,7 +115,10 @@ class Trainer:
         return loss
 
     def _step_eager(self, lr: float) -> torch.Tensor:
-        loss = self.loss_and_grads()
+        return self._finish(self.loss_and_grads(), lr)
+
+    def _finish(self, loss: torch.Tensor, lr: float) -> torch.Tensor:
+        """Gradient/loss all-reduce (graph-aligned ranks) and the SGD update."""
         if self.comm is not None:
             self.comm.all_reduce_(self.weights.grad_flat, phase="backward", block=-1, stage="params",
                                   level="global")
@@ -127,12 +130,15 @@ class Trainer:
     def step(self, lr: float) -> torch.Tensor:
         if not self.cuda_graph:
             return self._step_eager(lr)
-        key = (id(self.bg), id(self.e_target), id(self.f_target), float(lr))
+        # The forward + backward (~420 kernels) is captured once per batch and replayed;
+        # the collectives and the SGD kernel run eagerly after it, so no communicator
+        # is ever captured.
+        key = (id(self.bg), id(self.e_target), id(self.f_target))
         if self._graph is not None and self._graph_key == key:
             self._graph.replay()
-            return self._graph_loss
-        # this call's update runs eagerly (it also sizes every workspace); the same
-        # step is then captured, not executed, and replayed from the next call on
+            return self._finish(self._graph_loss, lr)
+        # this call runs eagerly (it also sizes every workspace); the same forward +
+        # backward is then captured, not executed, and replayed from the next call on
         from . import _lib
 
         loss = self._step_eager(lr)
@@ -143,8 +149,8 @@ class Trainer:
         try:
             with torch.cuda.stream(side):
                 with torch.cuda.graph(graph, stream=side):
-                    self._graph_loss = self._step_eager(lr)
-        except Exception as exc:  # e.g. a collective backend that cannot be captured
+                    self._graph_loss = self.loss_and_grads()
+        except Exception as exc:
             import sys
 
             torch.cuda.synchronize()
@@ -153,7 +159,7 @@ class Trainer:
             self.cuda_graph = False
             return loss
         torch.cuda.current_stream().wait_stream(side)
-        self.kernels_per_step = _lib.LAUNCH_COUNTER["kernels"] - before
+        self.kernels_per_step = _lib.LAUNCH_COUNTER["kernels"] - before + 1  # + the SGD kernel
         self._graph, self._graph_key = graph, key
         return loss
 
