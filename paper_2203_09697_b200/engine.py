@@ -8,7 +8,7 @@ reproduces the reference's per-graph loop (tasks.py:158-183).
 
 Schedule per block (engine.py:118-217), with the algebraic reorder that is
 exact in real arithmetic:
-  X  = m W_down^T [A^T]                    (gather id3_kj commutes with linear)
+  X  = m W_down^T [A^T] (GemNet: m (A W_down)^T, one GEMM; gather id3_kj commutes with linear)
   S  = triplet_fwd(X)                      (centre-tile kernel, triplet.cu)
   ta = ((S [P^T]) * (rbf W_rbf^T)) W_up^T  (up/P/rbf-gate commute with segment_sum)
   EU, EA+NU, [EU2 + sym], GU               (dense MLPs; EA = in-edge gather-sum)
@@ -129,8 +129,15 @@ class Engine:
         for b in range(c.blocks):
             p = f"block{b}."
             st = {"m": m}
-            down = L(m, w[p + "tu.down"])
-            X = L(down, w[p + "tu.bilinear_a"]) if gem else down
+            if gem:
+                # X = (m W_down^T) A^T = m (A W_down)^T: one edge-sized GEMM with the
+                # folded [d_bil, d_e] weight (the [E, d_t] intermediate is never formed)
+                Wda = w[p + "tu.bilinear_a"] @ w[p + "tu.down"]
+                X = L(m, Wda)
+                down = None
+                st["Wda"] = Wda
+            else:
+                down = X = L(m, w[p + "tu.down"])
             Wk = self._sbf_weight(b)
             S = ops.triplet_fwd(bg.edge_ptr, bg.rev, bg.geo, X, Wk, c.cutoff, max_degree=bg.max_deg)
             g = ops.rbf_linear(rbf, w[p + "tu.rbf_gate"])  # K = k_rbf (6)
@@ -256,8 +263,12 @@ class Engine:
             if gem:
                 torch.mm(wp_bar, w[p + "tu.sbf_gate"].t(), out=gr[p + "tu.bilinear_b"])
                 torch.mm(w[p + "tu.bilinear_b"].t(), wp_bar, out=gr[p + "tu.sbf_gate"])
-                wg(X_bar, st["down"], gr[p + "tu.bilinear_a"])
-                down_bar = L(X_bar, w[p + "tu.bilinear_a"], w_mn=True)
+                # T = X_bar^T m; A_bar = T W_down^T, W_down_bar = A^T T (weight-sized products)
+                T = wg(X_bar, st["m"], torch.empty((X_bar.shape[1], de), dtype=torch.float32, device=bg.device))
+                torch.mm(T, w[p + "tu.down"].t(), out=gr[p + "tu.bilinear_a"])
+                torch.mm(w[p + "tu.bilinear_a"].t(), T, out=gr[p + "tu.down"])
+                m_bar = L(X_bar, st["Wda"], w_mn=True, resid=m_in_bar)
+                continue
             else:
                 gr[p + "tu.sbf_gate"].copy_(wp_bar)
                 down_bar = X_bar
