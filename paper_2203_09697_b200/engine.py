@@ -10,7 +10,8 @@ Schedule per block (engine.py:118-217), with the algebraic reorder that is
 exact in real arithmetic:
   X  = m W_down^T [A^T] (GemNet: m (A W_down)^T, one GEMM; gather id3_kj commutes with linear)
   S  = triplet_fwd(X)                      (centre-tile kernel, triplet.cu)
-  ta = ((S [P^T]) * (rbf W_rbf^T)) W_up^T  (up/P/rbf-gate commute with segment_sum)
+  ta = ((S [P^T]) * (rbf W_rbf^T)) W_up^T  (up/P/rbf-gate commute with segment_sum;
+                                           W_up is folded into the EU weight, ta is never formed)
   EU, EA+NU, [EU2 + sym], GU               (dense MLPs; EA = in-edge gather-sum)
 The backward is written out explicitly (no autograd), mirroring the
 reference's reverse walk; geometry adjoints accumulate into one per-edge
@@ -146,12 +147,13 @@ class Engine:
                 st["Z"] = Z
             else:
                 Y = S * g
-            ta = L(Y, w[p + "tu.up"])
             w1 = w[p + "eu.w1"]
-            # h = [m, ta] W1^T + b1 without materialising the concat; a1 = silu(h)
-            h, a1 = L(m, w1[:, :de], a2=ta, w2=w1[:, de:], bias=w[p + "eu.b1"], flags=ops.EPI_SILU_OUT2)
+            # h = [m, ta] W1^T + b1 with ta = Y W_up^T folded into the second segment:
+            # h = m W1a^T + Y (W1b W_up)^T + b1 (no concat, no [E, d_e] ta); a1 = silu(h)
+            W1u = w1[:, de:] @ w[p + "tu.up"]
+            h, a1 = L(m, w1[:, :de], a2=Y, w2=W1u, bias=w[p + "eu.b1"], flags=ops.EPI_SILU_OUT2)
             m_new = L(a1, w[p + "eu.w2"], bias=w[p + "eu.b2"], resid=m)
-            st.update(down=down, X=X, Wk=Wk, S=S, g=g, Y=Y, ta=ta, h=h, a1=a1, m_new=m_new)
+            st.update(down=down, X=X, Wk=Wk, S=S, g=g, Y=Y, W1u=W1u, h=h, a1=a1, m_new=m_new)
             agg = ops.aggregate_in_edges(bg.edge_ptr, bg.rev, m_new)
             hv, av = L(agg, w[p + "nu.w1"], bias=w[p + "nu.b1"], flags=ops.EPI_SILU_OUT2)
             v = L(av, w[p + "nu.w2"], bias=w[p + "nu.b2"])
@@ -241,19 +243,21 @@ class Engine:
             h_bar = L(m_new_bar, w[p + "eu.w2"], w_mn=True, aux=st["h"], flags=ops.EPI_DSILU_AUX)
             w1 = w[p + "eu.w1"]
             wg(h_bar, st["m"], gr[p + "eu.w1"][:, :de], gr[p + "eu.b1"])
-            wg(h_bar, st["ta"], gr[p + "eu.w1"][:, de:])
+            # ta = Y W_up^T was folded into W1u = W1b W_up: both weight gradients come from
+            # T2 = h_bar^T Y  (W1b_bar = T2 W_up^T, W_up_bar = W1b^T T2)
+            T2 = wg(h_bar, st["Y"], torch.empty((de, st["Y"].shape[1]), dtype=torch.float32, device=bg.device))
+            gr[p + "eu.w1"][:, de:].copy_(T2 @ w[p + "tu.up"].t())
+            torch.mm(w1[:, de:].t(), T2, out=gr[p + "tu.up"])
             m_in_bar = L(h_bar, w1[:, :de], w_mn=True, resid=m_new_bar)
-            ta_bar = L(h_bar, w1[:, de:], w_mn=True)
-            # TU (engine.py:118-149)
-            wg(ta_bar, st["Y"], gr[p + "tu.up"])
+            # TU (engine.py:118-149): Y_bar = ta_bar W_up = h_bar W1u
             if gem:
                 # Z_bar = Y_bar * g fused into the GEMM epilogue (second output Y_bar)
-                Z_bar, Y_bar = L(ta_bar, w[p + "tu.up"], w_mn=True, aux=st["g"], flags=ops.EPI_MUL_AUX)
+                Z_bar, Y_bar = L(h_bar, st["W1u"], w_mn=True, aux=st["g"], flags=ops.EPI_MUL_AUX)
                 g_bar = Y_bar * st["Z"]
                 wg(Z_bar, st["S"], gr[p + "tu.bilinear_proj"])
                 S_bar = L(Z_bar, w[p + "tu.bilinear_proj"], w_mn=True)
             else:
-                Y_bar = L(ta_bar, w[p + "tu.up"], w_mn=True)
+                Y_bar = L(h_bar, st["W1u"], w_mn=True)
                 S_bar = Y_bar * st["g"]
                 g_bar = Y_bar * st["S"]
             ops.rbf_linear_bwd(fw.rbf, w[p + "tu.rbf_gate"], g_bar, rbf_bar, gr[p + "tu.rbf_gate"])
