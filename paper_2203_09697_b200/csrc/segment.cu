@@ -282,9 +282,16 @@ __global__ void __launch_bounds__(256) rbf_linear_bwd_kernel(const float* __rest
     if (tid < kRlTile * K) {
       const int e = tid / K, k = tid - (tid / K) * K;
       if (e < te) {
-        float sacc = 0.f;
-        for (int n = 0; n < N; ++n) sacc = fmaf(gs[e][n], ws[n * K + k], sacc);
-        rbf_bar[(e0 + e) * K + k] += sacc;
+        float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+        int n = 0;
+        for (; n + 4 <= N; n += 4) {
+          s0 = fmaf(gs[e][n], ws[n * K + k], s0);
+          s1 = fmaf(gs[e][n + 1], ws[(n + 1) * K + k], s1);
+          s2 = fmaf(gs[e][n + 2], ws[(n + 2) * K + k], s2);
+          s3 = fmaf(gs[e][n + 3], ws[(n + 3) * K + k], s3);
+        }
+        for (; n < N; ++n) s0 = fmaf(gs[e][n], ws[n * K + k], s0);
+        rbf_bar[(e0 + e) * K + k] += (s0 + s1) + (s2 + s3);
       }
     }
 #pragma unroll
@@ -292,14 +299,22 @@ __global__ void __launch_bounds__(256) rbf_linear_bwd_kernel(const float* __rest
       const int slot = tid + 256 * r;
       if (slot < N * K) {
         const int n = slot / K, k = slot - (slot / K) * K;
-        float a = acc[r];
-        for (int e = 0; e < kRlTile; ++e) a = fmaf(gs[e][n], rs[e][k], a);
-        acc[r] = a;
+        float a0 = 0.f, a1 = 0.f;
+#pragma unroll 8
+        for (int e = 0; e < kRlTile; e += 2) {
+          a0 = fmaf(gs[e][n], rs[e][k], a0);
+          a1 = fmaf(gs[e + 1][n], rs[e + 1][k], a1);
+        }
+        acc[r] += a0 + a1;
       } else if (slot < len) {
         const int n = slot - N * K;
-        float a = acc[r];
-        for (int e = 0; e < kRlTile; ++e) a += gs[e][n];
-        acc[r] = a;
+        float a0 = 0.f, a1 = 0.f;
+#pragma unroll 8
+        for (int e = 0; e < kRlTile; e += 2) {
+          a0 += gs[e][n];
+          a1 += gs[e + 1][n];
+        }
+        acc[r] += a0 + a1;
       }
     }
   }

@@ -301,7 +301,7 @@ bw2_kernel(const int64_t* __restrict__ edge_ptr, const int32_t* __restrict__ rev
            const float4* __restrict__ geo, int64_t nv, const float* __restrict__ X,
            const float* __restrict__ W, int dg, RbfParams rp, const float* __restrict__ Sbar,
            float* __restrict__ Xbar, float* __restrict__ wbar_part, float* __restrict__ dd_part,
-           int64_t num_edges) {
+           int64_t num_edges, float4* __restrict__ edge_grad) {
   static_assert(L <= 8, "L <= 8");
   extern __shared__ __align__(16) float dsm[];
   float4* Us = reinterpret_cast<float4*>(dsm);      // [64]
@@ -326,7 +326,7 @@ bw2_kernel(const int64_t* __restrict__ edge_ptr, const int32_t* __restrict__ rev
       const int64_t r0 = rev[off];
       for (int c = tid; c < kCB; c += kT)
         if (c0 + c < dg) Xbar[r0 * dg + c0 + c] = 0.f;
-      if (tid == 0) dd_part[blockIdx.y * num_edges + off] = 0.f;
+      if (tid == 0 && gridDim.y > 1) dd_part[blockIdx.y * num_edges + off] = 0.f;
       continue;
     }
     __syncthreads();
@@ -422,7 +422,10 @@ bw2_kernel(const int64_t* __restrict__ edge_ptr, const int32_t* __restrict__ rev
           const int c = c0 + chan(cg, i);
           if (c < dg) Xbar[rq * dg + c] = xb[i];
         }
-        if (cg == 0) dd_part[blockIdx.y * num_edges + off + q] = dd;
+        if (cg == 0) {
+          if (gridDim.y == 1) edge_grad[off + q].w += dd;  // single channel block: final value
+          else dd_part[blockIdx.y * num_edges + off + q] = dd;
+        }
       }
       __syncthreads();
       // W_bar[k,l,c] += sum_{rows} rbf_k(q) R_bar[q,l,c]; thread-owned (l, c) entries
@@ -447,17 +450,28 @@ bw2_kernel(const int64_t* __restrict__ edge_ptr, const int32_t* __restrict__ rev
   for (int i = tid; i < K * L * kCB; i += kT) dst[i] = Wb[i];
 }
 
-// W_bar[k,l,c] = sum over x-CTAs of the partials of channel block c / 64
+// W_bar[k,l,c] = sum over x-CTAs of the partials of channel block c / 64; 32 outputs per
+// block, 8 warps split the partials, fixed-order combine
 __global__ void reduce_wbar_kernel(const float* __restrict__ part, int gx, int K, int L, int dg,
                                    float* __restrict__ out) {
+  __shared__ float red[8][33];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int total = K * L * dg;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+  const int i = blockIdx.x * 32 + lane;
+  float s = 0.f;
+  if (i < total) {
     const int kl = i / dg, c = i - kl * dg;
     const int cb = c / kCB, cc = c - cb * kCB;
     const float* src = part + static_cast<int64_t>(cb) * gx * (K * L * kCB) + kl * kCB + cc;
-    float s = 0.f;
-    for (int x = 0; x < gx; ++x) s += src[static_cast<int64_t>(x) * (K * L * kCB)];
-    out[i] = s;
+    for (int x = w; x < gx; x += 8) s += src[static_cast<int64_t>(x) * (K * L * kCB)];
+  }
+  red[w][lane] = s;
+  __syncthreads();
+  if (w == 0 && i < total) {
+    float t = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) t += red[k][lane];
+    out[i] = t;
   }
 }
 
@@ -518,11 +532,13 @@ int fast_bwd(const int64_t* edge_ptr, const int32_t* rev, const float4* geo, int
     cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     k2_configured = true;
   }
-  k2<<<dim3(gx, ncb), fast::kT, smem, st>>>(edge_ptr, rev, geo, nv, X, W, dg, rp, Sbar, Xbar, wpart, ddpart, ne);
+  k2<<<dim3(gx, ncb), fast::kT, smem, st>>>(edge_ptr, rev, geo, nv, X, W, dg, rp, Sbar, Xbar, wpart, ddpart, ne,
+                                            edge_grad);
   if (check_launch("triplet_bw2_fast")) return 1;
-  fast::reduce_wbar_kernel<<<grid_for(static_cast<int64_t>(K) * L * dg, 256), 256, 0, st>>>(wpart, gx, K, L, dg,
-                                                                                          Wbar);
+  fast::reduce_wbar_kernel<<<static_cast<int>((static_cast<int64_t>(K) * L * dg + 31) / 32), 256, 0, st>>>(
+      wpart, gx, K, L, dg, Wbar);
   if (check_launch("triplet_bw2_reduce")) return 1;
+  if (ncb == 1) return 0;  // bw2 added dE/dd directly
   fast::add_dd_kernel<<<grid_for(nv, 128), 128, 0, st>>>(edge_ptr, nv, ddpart, ncb, ne, edge_grad);
   return check_launch("triplet_bw_dd");
 }
