@@ -332,10 +332,18 @@ __global__ void reduce_parts_kernel(const float* __restrict__ part, int nparts, 
   __shared__ float red[8][33];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int i = blockIdx.x * 32 + lane;
-  float s = 0.f;
-  if (i < len)
-    for (int p = w; p < nparts; p += 8) s += part[static_cast<int64_t>(p) * len + i];
-  red[w][lane] = s;
+  float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+  if (i < len) {
+    int p = w;
+    for (; p + 24 < nparts; p += 32) {  // four independent loads in flight per thread
+      s0 += part[static_cast<int64_t>(p) * len + i];
+      s1 += part[static_cast<int64_t>(p + 8) * len + i];
+      s2 += part[static_cast<int64_t>(p + 16) * len + i];
+      s3 += part[static_cast<int64_t>(p + 24) * len + i];
+    }
+    for (; p < nparts; p += 8) s0 += part[static_cast<int64_t>(p) * len + i];
+  }
+  red[w][lane] = (s0 + s1) + (s2 + s3);
   __syncthreads();
   if (w == 0 && i < len) {
     float t = 0.f;
@@ -487,7 +495,7 @@ int egn_force_head_fwd(const int64_t* edge_ptr, const int32_t* rev, const float*
 }
 
 int64_t egn_force_head_bwd_workspace_bytes(int64_t num_edges, int d) {
-  int grid = grid_for(num_edges * 32, 256, 148 * 6);
+  int grid = grid_for(num_edges * 32, 256, 148 * 2);
   return static_cast<int64_t>(grid) * 8 * d * 4;
 }
 
@@ -500,7 +508,7 @@ int egn_force_head_bwd(const int32_t* recv, const float* geo, int64_t num_edges,
     cudaMemsetAsync(w_bar, 0, sizeof(float) * d, st);
     return check_launch("force_head_bwd_empty");
   }
-  int grid = grid_for(num_edges * 32, 256, 148 * 6);
+  int grid = grid_for(num_edges * 32, 256, 148 * 2);
   float* part = reinterpret_cast<float*>(workspace);
   for (int c0 = 0; c0 < d; c0 += 512) {
     force_bwd_kernel<<<grid, 256, 0, st>>>(recv, reinterpret_cast<const float4*>(geo), num_edges, m, d, c0, w,
