@@ -48,8 +48,9 @@ __device__ __forceinline__ void load_center(float4* Us, float* Rb, const float4*
   }
 }
 
-// Q chunk: rows (t, l) for t < nq, natural channel order; thread (cq = tid & 63, half = tid >> 6)
-template <int K, int L>
+// Q chunk: rows (t, l) for t < nq (row stride RS floats), natural channel order; thread
+// (cq = tid & 63, half = tid >> 6)
+template <int K, int L, int RS = kCB>
 __device__ __forceinline__ void build_q(float* Qs, const float (&wreg)[K][L], const float* Rb,
                                         const int32_t* __restrict__ rev, const float* __restrict__ X,
                                         int64_t off, int q0, int nq, int dg, int c0) {
@@ -76,7 +77,7 @@ __device__ __forceinline__ void build_q(float* Qs, const float (&wreg)[K][L], co
       float s = 0.f;
 #pragma unroll
       for (int k = 0; k < K; ++k) s = fmaf(r[k], wreg[k][l], s);
-      Qs[(t * L + l) * kCB + cq] = xv * s;
+      Qs[(t * L + l) * RS + cq] = xv * s;
     }
   }
 }
@@ -199,72 +200,103 @@ fwd_kernel(const int64_t* __restrict__ edge_ptr, const int32_t* __restrict__ rev
 }
 
 // ---------------------------------------------------------------------------
-// bw1: xbar(p,q) -> dE/dv (rows p and columns q), edge_grad.xyz += F / d
+// bw1: xbar(p, q) = sum_l T_l'(x_pq) Z[(q,l), p],  Z[(q,l), p] = sum_c Q[(q,l), c] Sbar[p, c]
+// Per (centre, 8-in-edge chunk, 64-channel block), Z is a small GEMM whose thread tile is one
+// in-edge q x all l x PP rows p (rows interleaved over the threads so shared-memory rows
+// of Sbar spread over the banks); xbar accumulates in shared memory, one owner per (p, q).
+// Then the row / column pass turns xbar into dE/dv (edge_grad.xyz += F / d).
+constexpr int kSbStride = kCB + 4;  // padded Sbar / Q rows (bank spread for 16-byte loads)
+
+template <int K, int L, int PP>
+__device__ __forceinline__ void bw1_tile(const float* Qs, const float* Sb, const float4* Us, float* XB, int n, int q0,
+                                         int nq, int G) {
+  const int tid = threadIdx.x;
+  const int t = tid / G, pg = tid - t * G;
+  if (t >= nq) return;
+  float acc[L][PP];
+#pragma unroll
+  for (int l = 0; l < L; ++l)
+#pragma unroll
+    for (int i = 0; i < PP; ++i) acc[l][i] = 0.f;
+  const float* qrow = Qs + (t * L) * kSbStride;
+#pragma unroll 4
+  for (int c = 0; c < kCB; c += 4) {
+    float4 sv[PP];
+#pragma unroll
+    for (int i = 0; i < PP; ++i) sv[i] = *reinterpret_cast<const float4*>(Sb + (pg + G * i) * kSbStride + c);
+#pragma unroll
+    for (int l = 0; l < L; ++l) {
+      const float4 qv = *reinterpret_cast<const float4*>(qrow + l * kSbStride + c);
+#pragma unroll
+      for (int i = 0; i < PP; ++i) {
+        acc[l][i] = fmaf(qv.x, sv[i].x, acc[l][i]);
+        acc[l][i] = fmaf(qv.y, sv[i].y, acc[l][i]);
+        acc[l][i] = fmaf(qv.z, sv[i].z, acc[l][i]);
+        acc[l][i] = fmaf(qv.w, sv[i].w, acc[l][i]);
+      }
+    }
+  }
+  const int q = q0 + t;
+  const float4 uq = Us[q];
+#pragma unroll
+  for (int i = 0; i < PP; ++i) {
+    const int p = pg + G * i;
+    if (p >= n || p == q) continue;
+    const float4 up = Us[p];
+    const float x = up.x * uq.x + up.y * uq.y + up.z * uq.z;
+    // sum_l T_l'(x) Z_l with T_l' = l U_{l-1}
+    float um = 0.f, uc = 1.f, v = 0.f;
+#pragma unroll
+    for (int l = 1; l < L; ++l) {
+      v = fmaf(static_cast<float>(l) * uc, acc[l][i], v);
+      const float un = fmaf(2.f * x, uc, -um);
+      um = uc;
+      uc = un;
+    }
+    XB[p * (kN + 1) + q] += v;  // single owner per (p, q), ordered over channel blocks
+  }
+}
+
 template <int K, int L>
 __global__ void __launch_bounds__(kT, 4)
 bw1_kernel(const int64_t* __restrict__ edge_ptr, const int32_t* __restrict__ rev,
            const float4* __restrict__ geo, int64_t nv, const float* __restrict__ X,
            const float* __restrict__ W, int dg, RbfParams rp, const float* __restrict__ Sbar,
            float4* __restrict__ edge_grad) {
-  __shared__ float4 Us[kN];
-  __shared__ float Rb[kN * K];
-  __shared__ __align__(16) float Dt[kQC * L * kCB];  // T' chunk
-  __shared__ __align__(16) float Qs[kQC * L * kCB];
-  __shared__ float XB[kN * (kN + 1)];                // xbar(p, q), padded rows
-  const int tid = threadIdx.x, cg = tid & 7, rg = tid >> 3;
+  extern __shared__ __align__(16) float bsm[];
+  float4* Us = reinterpret_cast<float4*>(bsm);             // [kN]
+  float* Rb = bsm + 4 * kN;                                 // [kN * K]
+  float* Qs = Rb + ((kN * K + 3) & ~3);                     // [kQC * L][kSbStride]
+  float* Sb = Qs + kQC * L * kSbStride;                     // [kN][kSbStride]
+  float* XB = Sb + kN * kSbStride;                          // [kN][kN + 1]
+  const int tid = threadIdx.x;
   for (int64_t j = blockIdx.x; j < nv; j += gridDim.x) {
     const int64_t off = edge_ptr[j];
     const int n = static_cast<int>(edge_ptr[j + 1] - off);
     if (n < 2 || n > kN) continue;
-    const int tmr = (n + 15) >> 4;
-    const int rows = tmr * 16;
     __syncthreads();
     load_center<K>(Us, Rb, geo, off, n, rp);
     for (int i = tid; i < n * (kN + 1); i += kT) XB[i] = 0.f;
+    // thread tile: PP rows p; G row groups per in-edge (G * nq <= kT)
+    const int PP = n <= 16 ? 1 : (n <= 32 ? 2 : 4);
+    const int G = (n + PP - 1) / PP;
     for (int c0 = 0; c0 < dg; c0 += kCB) {
       float wreg[K][L];
       load_wreg<K, L>(wreg, W, dg, c0 + (tid & 63));
-      float sb[4][8];
-#pragma unroll
-      for (int r = 0; r < 4; ++r) {
-        const int p = rg + 16 * r;
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const int c = c0 + chan(cg, i);
-          sb[r][i] = (r < tmr && p < n && c < dg) ? Sbar[(off + p) * dg + c] : 0.f;
-        }
+      __syncthreads();
+      for (int i = tid; i < n * kCB; i += kT) {
+        const int p = i >> 6, c = i & 63;
+        Sb[p * kSbStride + c] = c0 + c < dg ? Sbar[(off + p) * dg + c0 + c] : 0.f;
       }
       for (int q0 = 0; q0 < n; q0 += kQC) {
         const int nq = min(kQC, n - q0);
         __syncthreads();
-        build_q<K, L>(Qs, wreg, Rb, rev, X, off, q0, nq, dg, c0);
-        build_c<L, true>(Dt, Us, n, rows, q0, nq);
+        build_q<K, L, kSbStride>(Qs, wreg, Rb, rev, X, off, q0, nq, dg, c0);
         __syncthreads();
-        for (int t = 0; t < nq; ++t) {
-          float acc[4][8];
-#pragma unroll
-          for (int r = 0; r < 4; ++r)
-#pragma unroll
-            for (int i = 0; i < 8; ++i) acc[r][i] = 0.f;
-          switch (tmr) {
-            case 1: micro<1>(Dt + t * L * kCB, Qs + t * L * kCB, L, rg, cg, acc); break;
-            case 2: micro<2>(Dt + t * L * kCB, Qs + t * L * kCB, L, rg, cg, acc); break;
-            case 3: micro<3>(Dt + t * L * kCB, Qs + t * L * kCB, L, rg, cg, acc); break;
-            default: micro<4>(Dt + t * L * kCB, Qs + t * L * kCB, L, rg, cg, acc); break;
-          }
-#pragma unroll
-          for (int r = 0; r < 4; ++r) {
-            if (r < tmr) {
-              float v = 0.f;
-#pragma unroll
-              for (int i = 0; i < 8; ++i) v = fmaf(sb[r][i], acc[r][i], v);
-              v += __shfl_xor_sync(0xffffffffu, v, 1);
-              v += __shfl_xor_sync(0xffffffffu, v, 2);
-              v += __shfl_xor_sync(0xffffffffu, v, 4);
-              const int p = rg + 16 * r;
-              if (cg == 0 && p < n) XB[p * (kN + 1) + q0 + t] += v;  // row owner, ordered over c0
-            }
-          }
+        switch (PP) {
+          case 1: bw1_tile<K, L, 1>(Qs, Sb, Us, XB, n, q0, nq, G); break;
+          case 2: bw1_tile<K, L, 2>(Qs, Sb, Us, XB, n, q0, nq, G); break;
+          default: bw1_tile<K, L, 4>(Qs, Sb, Us, XB, n, q0, nq, G); break;
         }
       }
     }
@@ -518,7 +550,15 @@ int fast_bwd(const int64_t* edge_ptr, const int32_t* rev, const float4* geo, int
   {
     auto kern = fast::bw1_kernel<6, 7>;
     const int grid = static_cast<int>(std::min<int64_t>(nv, 1 << 30));
-    kern<<<grid, fast::kT, 0, st>>>(edge_ptr, rev, geo, nv, X, W, dg, rp, Sbar, edge_grad);
+    const size_t smem1 = (4 * fast::kN + ((fast::kN * 6 + 3) & ~3) + fast::kQC * 7 * fast::kSbStride +
+                          fast::kN * fast::kSbStride + fast::kN * (fast::kN + 1)) *
+                         sizeof(float);
+    static bool k1_configured = false;
+    if (!k1_configured) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem1));
+      k1_configured = true;
+    }
+    kern<<<grid, fast::kT, smem1, st>>>(edge_ptr, rev, geo, nv, X, W, dg, rp, Sbar, edge_grad);
     if (check_launch("triplet_bw1_fast")) return 1;
   }
   const int gx = static_cast<int>(std::min<int64_t>(nv, static_cast<int64_t>(kNumSMs) * 3));
