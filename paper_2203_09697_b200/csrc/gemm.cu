@@ -66,6 +66,7 @@ struct Params {
   int flush_steps;         // k-steps (of 8) per TMEM->register flush (0 = whole tile)
   int tma_out;             // single-output epilogues store through mapOut (TMA)
   float* gsum_part;        // wgrad: per-split column sums of g (rows of A), [splits][M], or null
+  int mcast;               // 1: CTA pairs (cluster of 2) share each A k-block by TMA multicast
   int64_t split_stride;    // split-K: elements between partial outputs
   long long* trace;        // debug timeline (EGN_GEMM_TRACE), CTA 0 only
 };
@@ -95,6 +96,27 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
       "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];"
       ::"r"(smem_u32(dst)), "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
       : "memory");
+}
+__device__ __forceinline__ void tma_load_2d_mc(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
+                                               uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+      " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "h"(mask)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_remote(uint64_t* bar, uint32_t cta) {
+  uint32_t remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(bar)), "r"(cta));
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.aligned;\n\tbarrier.cluster.wait.aligned;" ::: "memory");
 }
 __device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, const void* src, int c0, int c1, int c2) {
   asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(map), "r"(c0),
@@ -277,10 +299,12 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_const
     P.trace[1024 + 4 * blockIdx.x] = g;
   }
 
+  const uint32_t crank = P.mcast ? cluster_rank() : 0;
   if (tid == 0) {
     for (int s = 0; s < kTmaRing; ++s) {
       mbar_init(&tma_full[s], 1);
-      mbar_init(&tma_empty[s], 1);
+      // the multicast leader reuses slot s only after both CTAs' split warps released it
+      mbar_init(&tma_empty[s], (P.mcast && crank == 0) ? 2 : 1);
     }
     for (int s = 0; s < kOpRing; ++s) {
       mbar_init(&op_full[s], 1);
@@ -302,6 +326,7 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_const
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
+  if (P.mcast) cluster_sync();  // the peer's barriers exist before any multicast / remote arrive
   const uint32_t tmem = tmem_base;
 
   auto item_coords = [&](int item, int64_t& m0, int& n0, int& kbeg, int& nk) {
@@ -337,8 +362,11 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_const
           const CUtensorMap* mb = first ? &mapB0 : &mapB1;
           if (AMN) {
             tma_load_2d(st, ma, &tma_full[s], static_cast<int>(m0), kk);  // [32 k][128 m], unswizzled
-          } else {
+          } else if (!P.mcast) {
             tma_load_2d(st, ma, &tma_full[s], kk, static_cast<int>(m0));  // [128 m][32 k], SW128
+          } else if (crank == 0) {
+            // both CTAs of the pair work on this m-tile: one L2 read, delivered to both
+            tma_load_2d_mc(st, ma, &tma_full[s], kk, static_cast<int>(m0), 0x3);
           }
           if (BMN) {
 #pragma unroll
@@ -473,6 +501,7 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_const
         if (ct == 0) {
           EGN_TRACE(3, it);
           mbar_arrive(&tma_empty[s]);
+          if (P.mcast && crank == 1) mbar_arrive_remote(&tma_empty[s], 0);
           mbar_arrive(&op_full[o]);
         }
       }
@@ -672,6 +701,7 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_const
   if (warp == 1) {
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
   }
+  if (P.mcast) cluster_sync();  // no CTA leaves while its peer may still signal it
   if (P.trace && tid == 32) {
     long long g;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
@@ -759,7 +789,50 @@ static int launch(const CUtensorMap& a0, const CUtensorMap& b0, const CUtensorMa
   const int tiles_m = static_cast<int>((P.M + BM - 1) / BM);
   const int tiles_n = (P.N + BN - 1) / BN;
   const int total = tiles_m * tiles_n * splits;
-  const int grid = std::min(total, kNumSMs);
+  int grid = std::min(total, kNumSMs);
+  // CTA pairs over the two 64-column halves of a 128-column product share A by multicast
+  // Opt-in (EGN_GEMM_MCAST=1): measured slower at C2 shapes (the pair runs in lockstep and the
+  // loader is latency-, not L2-bandwidth-bound), kept for the wider XL products.
+  static const bool mc_enabled = [] { const char* e = std::getenv("EGN_GEMM_MCAST"); return e && e[0] == '1'; }();
+  if (!AMN && mc_enabled && tiles_n == 2 && splits == 1 && total >= 2) {
+    static int max_clusters = -1;
+    if (max_clusters < 0) {
+      cudaLaunchConfig_t qc = {};
+      cudaLaunchAttribute qa[1];
+      qa[0].id = cudaLaunchAttributeClusterDimension;
+      qa[0].val.clusterDim.x = 2;
+      qa[0].val.clusterDim.y = 1;
+      qa[0].val.clusterDim.z = 1;
+      qc.gridDim = dim3(kNumSMs, 1, 1);
+      qc.blockDim = dim3(kGemmThreads, 1, 1);
+      qc.dynamicSmemBytes = smem;
+      qc.attrs = qa;
+      qc.numAttrs = 1;
+      if (cudaOccupancyMaxActiveClusters(&max_clusters, kern, &qc) != cudaSuccess) {
+        cudaGetLastError();
+        max_clusters = 0;
+      }
+    }
+    if (max_clusters > 0) {
+      Params Q = P;
+      Q.mcast = 1;
+      grid = std::min(total, 2 * max_clusters) & ~1;
+      cudaLaunchConfig_t cfg = {};
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = 2;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      cfg.gridDim = dim3(grid, 1, 1);
+      cfg.blockDim = dim3(kGemmThreads, 1, 1);
+      cfg.dynamicSmemBytes = smem;
+      cfg.stream = st;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      cudaLaunchKernelEx(&cfg, kern, a0, b0, a1, b1, mo, Q, tiles_n, splits, total);
+      return check_launch("gemm_tf32x3_mc");
+    }
+  }
   if (getenv("EGN_GEMM_TRACE")) {  // debug timeline of CTA 0 (SM cycles since its first event)
     Params Q = P;
     long long* d = nullptr;
@@ -915,7 +988,7 @@ extern "C" int egn_gemm_wgrad(int64_t krows, int M, int N, const float* g, int64
   wgrad_split(krows, M, N, &splits, &kbps);
   float* part = reinterpret_cast<float*>(workspace);
   Params P{M, N, 1, static_cast<int>(krows), 0, nullptr, nullptr, 0, nullptr, nullptr, 0, nullptr, 0, 0,
-           part, N, nullptr, 0, kbps, flush_window(true), 0, nullptr, static_cast<int64_t>(M) * N};
+           part, N, nullptr, 0, kbps, flush_window(true), 0, nullptr, 0, static_cast<int64_t>(M) * N};
   CUtensorMap ma, mb;
   // A = g^T: g is [krows, M] with M contiguous (MN-major); B = x^T likewise
   if (int rc = make_map(&ma, g, krows, M, ldg, BK, kMapPlain)) return rc;
