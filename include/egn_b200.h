@@ -234,6 +234,19 @@ int egn_gemm_wgrad(int64_t krows, int M, int N, const float* g, int64_t ldg, con
                    int64_t ldx, float* out, int64_t ldo, float* g_colsum, int accumulate,
                    void* workspace, egn_stream_t stream);
 
+/* Batched small products C = op(A) op(B) (op = transpose if the flag is set; C stored
+ * transposed if trans_c): the weight-sized products of the folded projections
+ * (A W_down, W1b W_up, B W_sbf) and their adjoints, all in one launch.  fp32. */
+typedef struct {
+  const float* a;
+  const float* b;
+  float* c;
+  int m, n, k;
+  int lda, ldb, ldc;
+  int trans_a, trans_b, trans_c;
+} egn_small_gemm_t;
+int egn_small_gemm_batched(const egn_small_gemm_t* problems, int count, egn_stream_t stream);
+
 /* ------------------------------------------------------------------ */
 /* Optimizer: train_simple SGD update (tasks.py:207-208)               */
 /* ------------------------------------------------------------------ */

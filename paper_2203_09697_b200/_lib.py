@@ -23,6 +23,13 @@ _i64 = ctypes.c_int64
 _f32 = ctypes.c_float
 _f64 = ctypes.c_double
 
+class SmallGemm(ctypes.Structure):
+    """egn_small_gemm_t (include/egn_b200.h)."""
+
+    _fields_ = [("a", _p), ("b", _p), ("c", _p), ("m", _i32), ("n", _i32), ("k", _i32), ("lda", _i32),
+                ("ldb", _i32), ("ldc", _i32), ("trans_a", _i32), ("trans_b", _i32), ("trans_c", _i32)]
+
+
 # name -> (restype, argtypes); mirrors include/egn_b200.h
 SIGNATURES: dict[str, tuple] = {
     "egn_last_error": (ctypes.c_char_p, []),
@@ -59,6 +66,7 @@ SIGNATURES: dict[str, tuple] = {
                         _p, _i64, _p, _i64, _i32, _p, _i64, _p, _i64, _i32, _p]),
     "egn_gemm_wgrad_workspace_bytes": (_i64, [_i64, _i32, _i32]),
     "egn_gemm_wgrad": (_i32, [_i64, _i32, _i32, _p, _i64, _p, _i64, _p, _i64, _p, _i32, _p, _p]),
+    "egn_small_gemm_batched": (_i32, [_p, _i32, _p]),
     "egn_sgd": (_i32, [_p, _p, _i64, _f32, _p]),
 }
 

@@ -607,3 +607,78 @@ int egn_sgd(float* w, const float* g, int64_t n, float lr, egn_stream_t stream) 
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------- batched weight-sized products
+// C = op(A) op(B) for up to kMaxSmall independent small problems in one launch (the weight
+// folds A W_down, W1b W_up, B W_sbf and their adjoints): one 32 x 32 output tile per CTA,
+// fp32 FFMA, shared-memory K tiles.
+namespace egn {
+constexpr int kMaxSmall = 32;
+struct SmallBatch {
+  egn_small_gemm_t g[kMaxSmall];
+  int tile0[kMaxSmall + 1];
+  int count;
+};
+
+__global__ void __launch_bounds__(256) small_gemm_kernel(const __grid_constant__ SmallBatch b) {
+  __shared__ float As[32][33];
+  __shared__ float Bs[32][33];
+  int pi = 0;
+  while (pi + 1 < b.count && static_cast<int>(blockIdx.x) >= b.tile0[pi + 1]) ++pi;
+  const egn_small_gemm_t& g = b.g[pi];
+  const int t = blockIdx.x - b.tile0[pi];
+  const int tn = (g.n + 31) / 32;
+  const int m0 = (t / tn) * 32, n0 = (t % tn) * 32;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 8 row groups x 32 columns
+  float acc[4] = {0.f, 0.f, 0.f, 0.f};
+  for (int k0 = 0; k0 < g.k; k0 += 32) {
+    for (int i = threadIdx.x; i < 32 * 32; i += 256) {
+      const int r = i >> 5, c = i & 31;
+      const int m = m0 + r, k = k0 + c;
+      As[r][c] = (m < g.m && k < g.k) ? (g.trans_a ? g.a[static_cast<int64_t>(k) * g.lda + m]
+                                                    : g.a[static_cast<int64_t>(m) * g.lda + k])
+                                       : 0.f;
+      const int kk = k0 + r, n = n0 + c;
+      Bs[r][c] = (kk < g.k && n < g.n) ? (g.trans_b ? g.b[static_cast<int64_t>(n) * g.ldb + kk]
+                                                     : g.b[static_cast<int64_t>(kk) * g.ldb + n])
+                                        : 0.f;
+    }
+    __syncthreads();
+#pragma unroll 8
+    for (int kk = 0; kk < 32; ++kk) {
+      const float bv = Bs[kk][tx];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) acc[i] = fmaf(As[ty + 8 * i][kk], bv, acc[i]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int m = m0 + ty + 8 * i, n = n0 + tx;
+    if (m < g.m && n < g.n) {
+      if (g.trans_c) g.c[static_cast<int64_t>(n) * g.ldc + m] = acc[i];
+      else g.c[static_cast<int64_t>(m) * g.ldc + n] = acc[i];
+    }
+  }
+}
+}  // namespace egn
+
+extern "C" int egn_small_gemm_batched(const egn_small_gemm_t* problems, int count, egn_stream_t stream) {
+  using namespace egn;
+  cudaStream_t st = as_stream(stream);
+  for (int base = 0; base < count; base += kMaxSmall) {
+    SmallBatch b;
+    b.count = std::min(kMaxSmall, count - base);
+    b.tile0[0] = 0;
+    for (int i = 0; i < b.count; ++i) {
+      const egn_small_gemm_t& g = problems[base + i];
+      EGN_REQUIRE(g.m >= 0 && g.n >= 0 && g.k >= 0, "small_gemm: negative size");
+      b.g[i] = g;
+      b.tile0[i + 1] = b.tile0[i] + ((g.m + 31) / 32) * ((g.n + 31) / 32);
+    }
+    if (b.tile0[b.count] == 0) continue;
+    small_gemm_kernel<<<b.tile0[b.count], 256, 0, st>>>(b);
+    if (int rc = check_launch("small_gemm_batched")) return rc;
+  }
+  return 0;
+}

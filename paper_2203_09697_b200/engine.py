@@ -116,12 +116,39 @@ class Engine:
         dg = wp.shape[0]
         return wp.view(dg, c.k_rbf, c.l_sbf).permute(1, 2, 0).contiguous()
 
+    def _folded_weights(self) -> list:
+        """Per block: the folded weights of this step, all from one batched launch
+        (egn_small_gemm_batched): Wda = A W_down (GemNet), W1u = W1b W_up, and the
+        SBF weight W[k, l, c] = (B W_sbf)[c, k L + l] (GemNet; DimeNet: W_sbf permuted)."""
+        c, w = self.config, self.weights.w
+        gem = c.variant == GEMNET
+        de, dev = c.d_e, self.weights.flat.device
+        out, probs = [], []
+        for b in range(c.blocks):
+            p = f"block{b}."
+            f = {}
+            w1b = w[p + "eu.w1"][:, de:]
+            f["W1u"] = torch.empty((de, c.d_t), dtype=torch.float32, device=dev)
+            probs.append((w1b, w[p + "tu.up"], f["W1u"], 0, 0, 0))
+            if gem:
+                f["Wda"] = torch.empty((c.d_bil, de), dtype=torch.float32, device=dev)
+                probs.append((w[p + "tu.bilinear_a"], w[p + "tu.down"], f["Wda"], 0, 0, 0))
+                f["Wk"] = torch.empty((c.k_rbf, c.l_sbf, c.d_bil), dtype=torch.float32, device=dev)
+                probs.append((w[p + "tu.bilinear_b"], w[p + "tu.sbf_gate"],
+                              f["Wk"].view(c.k_rbf * c.l_sbf, c.d_bil), 0, 0, 1))
+            else:
+                f["Wk"] = self._sbf_weight(b)
+            out.append(f)
+        ops.small_gemms(probs)
+        return out
+
     # -- forward -------------------------------------------------------------
     def forward(self, bg: BatchGraph) -> ForwardResult:
         c, w = self.config, self.weights.w
         gem = c.variant == GEMNET
         de = c.d_e
         L = ops.linear
+        folded = self._folded_weights()
         rbf = ops.rbf(bg.geo, c.k_rbf, c.cutoff)
         m = ops.rbf_linear(rbf, w["edge_init.w"], w["edge_init.b"])  # K = k_rbf (6)
         u = torch.zeros((bg.num_graphs, c.d_u), dtype=torch.float32, device=bg.device)
@@ -133,13 +160,13 @@ class Engine:
             if gem:
                 # X = (m W_down^T) A^T = m (A W_down)^T: one edge-sized GEMM with the
                 # folded [d_bil, d_e] weight (the [E, d_t] intermediate is never formed)
-                Wda = w[p + "tu.bilinear_a"] @ w[p + "tu.down"]
+                Wda = folded[b]["Wda"]
                 X = L(m, Wda)
                 down = None
                 st["Wda"] = Wda
             else:
                 down = X = L(m, w[p + "tu.down"])
-            Wk = self._sbf_weight(b)
+            Wk = folded[b]["Wk"]
             S = ops.triplet_fwd(bg.edge_ptr, bg.rev, bg.geo, X, Wk, c.cutoff, max_degree=bg.max_deg)
             g = ops.rbf_linear(rbf, w[p + "tu.rbf_gate"])  # K = k_rbf (6)
             if gem:
@@ -150,7 +177,7 @@ class Engine:
             w1 = w[p + "eu.w1"]
             # h = [m, ta] W1^T + b1 with ta = Y W_up^T folded into the second segment:
             # h = m W1a^T + Y (W1b W_up)^T + b1 (no concat, no [E, d_e] ta); a1 = silu(h)
-            W1u = w1[:, de:] @ w[p + "tu.up"]
+            W1u = folded[b]["W1u"]
             h, a1 = L(m, w1[:, :de], a2=Y, w2=W1u, bias=w[p + "eu.b1"], flags=ops.EPI_SILU_OUT2)
             m_new = L(a1, w[p + "eu.w2"], bias=w[p + "eu.b2"], resid=m)
             st.update(down=down, X=X, Wk=Wk, S=S, g=g, Y=Y, W1u=W1u, h=h, a1=a1, m_new=m_new)
@@ -204,6 +231,7 @@ class Engine:
                                d_forces.to(torch.float32).contiguous(), m_bar, eg,
                                w_bar=gr["force_head.w"].view(-1))
         rbf_bar = torch.zeros_like(fw.rbf)
+        post = []  # weight-sized gradient products, batched after the block loop
         for b in range(c.blocks - 1, -1, -1):
             p = f"block{b}."
             st = fw.blocks[b]
@@ -246,8 +274,8 @@ class Engine:
             # ta = Y W_up^T was folded into W1u = W1b W_up: both weight gradients come from
             # T2 = h_bar^T Y  (W1b_bar = T2 W_up^T, W_up_bar = W1b^T T2)
             T2 = wg(h_bar, st["Y"], torch.empty((de, st["Y"].shape[1]), dtype=torch.float32, device=bg.device))
-            gr[p + "eu.w1"][:, de:].copy_(T2 @ w[p + "tu.up"].t())
-            torch.mm(w1[:, de:].t(), T2, out=gr[p + "tu.up"])
+            post.append((T2, w[p + "tu.up"], gr[p + "eu.w1"][:, de:], 0, 1, 0))  # W1b_bar = T2 W_up^T
+            post.append((w1[:, de:], T2, gr[p + "tu.up"], 1, 0, 0))  # W_up_bar = W1b^T T2
             m_in_bar = L(h_bar, w1[:, :de], w_mn=True, resid=m_new_bar)
             # TU (engine.py:118-149): Y_bar = ta_bar W_up = h_bar W1u
             if gem:
@@ -263,22 +291,24 @@ class Engine:
             ops.rbf_linear_bwd(fw.rbf, w[p + "tu.rbf_gate"], g_bar, rbf_bar, gr[p + "tu.rbf_gate"])
             X_bar, Wk_bar = ops.triplet_bwd(bg.edge_ptr, bg.rev, bg.geo, st["X"], st["Wk"], c.cutoff,
                                             S_bar, eg, max_degree=bg.max_deg)
-            wp_bar = Wk_bar.permute(2, 0, 1).reshape(Wk_bar.shape[2], -1)  # [dg, K*L]
             if gem:
-                torch.mm(wp_bar, w[p + "tu.sbf_gate"].t(), out=gr[p + "tu.bilinear_b"])
-                torch.mm(w[p + "tu.bilinear_b"].t(), wp_bar, out=gr[p + "tu.sbf_gate"])
+                # wp_bar[c, kl] = Wk_bar[kl, c]: read transposed in place
+                wkb = Wk_bar.view(-1, Wk_bar.shape[2])
+                post.append((wkb, w[p + "tu.sbf_gate"], gr[p + "tu.bilinear_b"], 1, 1, 0))
+                post.append((w[p + "tu.bilinear_b"], wkb, gr[p + "tu.sbf_gate"], 1, 1, 0))
                 # T = X_bar^T m; A_bar = T W_down^T, W_down_bar = A^T T (weight-sized products)
                 T = wg(X_bar, st["m"], torch.empty((X_bar.shape[1], de), dtype=torch.float32, device=bg.device))
-                torch.mm(T, w[p + "tu.down"].t(), out=gr[p + "tu.bilinear_a"])
-                torch.mm(w[p + "tu.bilinear_a"].t(), T, out=gr[p + "tu.down"])
+                post.append((T, w[p + "tu.down"], gr[p + "tu.bilinear_a"], 0, 1, 0))
+                post.append((w[p + "tu.bilinear_a"], T, gr[p + "tu.down"], 1, 0, 0))
                 m_bar = L(X_bar, st["Wda"], w_mn=True, resid=m_in_bar)
                 continue
             else:
-                gr[p + "tu.sbf_gate"].copy_(wp_bar)
+                gr[p + "tu.sbf_gate"].copy_(Wk_bar.permute(2, 0, 1).reshape(Wk_bar.shape[2], -1))  # [dg, K*L]
                 down_bar = X_bar
             wg(down_bar, st["m"], gr[p + "tu.down"])
             m_bar = L(down_bar, w[p + "tu.down"], w_mn=True, resid=m_in_bar)
-        # edge init (engine.py:109-111), K = k_rbf: cuBLAS
+        ops.small_gemms(post)  # every deferred weight-sized gradient product, one launch
+        # edge init (engine.py:109-111), K = k_rbf
         ops.rbf_linear_bwd(fw.rbf, w["edge_init.w"], m_bar, rbf_bar, gr["edge_init.w"], gr["edge_init.b"])
         ops.rbf_bwd(bg.geo, rbf_bar, c.cutoff, eg)
         return ops.positions_bwd(bg.edge_ptr, bg.rev, bg.geo, eg)

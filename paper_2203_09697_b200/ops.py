@@ -8,6 +8,7 @@ tensors of the documented dtype; there is no CPU path.
 
 from __future__ import annotations
 
+import ctypes
 import threading
 
 import torch
@@ -428,6 +429,31 @@ def linear_wgrad(g, x, out, bias_out=None):
     if bias_out is not None:
         column_sum(g, out=bias_out)
     return out
+
+
+def small_gemms(problems):
+    """One launch for many weight-sized products C = op(A) op(B) (egn_small_gemm_batched).
+
+    problems: (A, B, C, trans_a, trans_b, trans_c) with 2-D tensors whose rows are
+    contiguous; op(A) is [m, k] (A is [k, m] when trans_a), op(B) is [k, n] (B is [n, k]
+    when trans_b), C is [m, n] ([n, m] when trans_c)."""
+    from ._lib import SmallGemm
+
+    if not problems:
+        return
+    arr = (SmallGemm * len(problems))()
+    for i, (A, B, C, ta, tb, tc) in enumerate(problems):
+        for t in (A, B, C):
+            if t.dtype != torch.float32 or t.dim() != 2 or t.stride(1) != 1:
+                raise ValueError("small_gemms takes fp32 2-D tensors with contiguous rows")
+        m, k = (A.shape[1], A.shape[0]) if ta else (A.shape[0], A.shape[1])
+        kb, n = (B.shape[1], B.shape[0]) if tb else (B.shape[0], B.shape[1])
+        cm, cn = (C.shape[1], C.shape[0]) if tc else (C.shape[0], C.shape[1])
+        if kb != k or cm != m or cn != n:
+            raise ValueError(f"small_gemms: shape mismatch {tuple(A.shape)} {tuple(B.shape)} {tuple(C.shape)}")
+        arr[i] = SmallGemm(ptr(A), ptr(B), ptr(C), m, n, k, A.stride(0), B.stride(0), C.stride(0), int(ta), int(tb),
+                           int(tc))
+    call("egn_small_gemm_batched", ctypes.addressof(arr), len(problems), stream())
 
 
 def sgd_(w, g, lr):
