@@ -56,7 +56,7 @@ WORKLOADS = {
 def _args():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="gemnet-t-oc20")
@@ -87,53 +87,75 @@ def _systems(wl, graphs, rank=0):
 # clocks sampled during the timed region
 # ---------------------------------------------------------------------------
 class ClockSampler:
-    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    """SM clock and clock-event reasons polled through NVML every ~10 ms while the
+    timed region runs (nvidia-smi's own -lms loop starts too slowly for a region of
+    well under a second); falls back to one nvidia-smi query per poll."""
 
-    def __init__(self, index: int):
-        self.index = index
-        self.proc = None
-        self.lines = []
+    NAMES = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+
+    def __init__(self, index: int, period_s: float = 0.01):
+        self.period = period_s
+        self.sm, self.smax, self.reasons, self.err = [], None, set(), None
+        self._stop = threading.Event()
+        self._t = None
+        self.h = None
+        try:
+            import pynvml as N
+            import torch
+
+            N.nvmlInit()
+            p = torch.cuda.get_device_properties(index)
+            bus = f"{p.pci_domain_id:08x}:{p.pci_bus_id:02x}:{p.pci_device_id:02x}.0"
+            self.h = N.nvmlDeviceGetHandleByPciBusId(bus)
+            self.N = N
+            self.bits = {"hw_slowdown": N.nvmlClocksEventReasonHwSlowdown,
+                         "hw_thermal_slowdown": N.nvmlClocksEventReasonHwThermalSlowdown,
+                         "sw_thermal_slowdown": N.nvmlClocksEventReasonSwThermalSlowdown,
+                         "sw_power_cap": N.nvmlClocksEventReasonSwPowerCap}
+            self.smax = float(N.nvmlDeviceGetMaxClockInfo(self.h, N.NVML_CLOCK_SM))
+        except Exception as e:  # noqa: BLE001 - report, never fail the bench on telemetry
+            self.h, self.err = None, f"nvml: {e}"
+            self.index = index
+
+    def _poll_once(self):
+        if self.h is not None:
+            N = self.N
+            self.sm.append(float(N.nvmlDeviceGetClockInfo(self.h, N.NVML_CLOCK_SM)))
+            r = N.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+            for nm, bit in self.bits.items():
+                if r & bit:
+                    self.reasons.add(nm)
+            return
+        out = subprocess.run(["nvidia-smi", f"--id={self.index}", "--query-gpu=clocks.sm,clocks.max.sm",
+                              "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=10).stdout
+        parts = [p.strip() for p in out.split(",")]
+        if len(parts) >= 2:
+            self.sm.append(float(parts[0]))
+            self.smax = float(parts[1])
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self._poll_once()
+            except Exception as e:  # noqa: BLE001
+                self.err = str(e)
+                return
+            self._stop.wait(self.period)
 
     def start(self):
-        try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self._t = threading.Thread(target=self._read, daemon=True)
-            self._t.start()
-        except OSError:
-            self.proc = None
-
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
 
     def stop(self):
-        if self.proc is None:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        self.proc.terminate()
-        try:
-            self.proc.wait(timeout=5)
-        except subprocess.TimeoutExpired:
-            self.proc.kill()
-        sm, smax, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            parts = [p.strip() for p in ln.split(",")]
-            if len(parts) < 8:
-                continue
-            try:
-                sm.append(float(parts[0]))
-                smax = float(parts[1])
-            except ValueError:
-                continue
-            for nm, val in zip(names, parts[4:8]):
-                if val.lower() == "active":
-                    reasons.add(nm)
-        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": smax,
-                "reasons": sorted(reasons), "samples": len(sm)}
+        self._stop.set()
+        if self._t is not None:
+            self._t.join(timeout=15)
+        out = {"sm_mhz": float(np.median(self.sm)) if self.sm else None, "sm_max_mhz": self.smax,
+               "reasons": sorted(self.reasons), "samples": len(self.sm),
+               "source": "nvml" if self.h is not None else "nvidia-smi"}
+        if self.err:
+            out["error"] = self.err
+        return out
 
 
 # ---------------------------------------------------------------------------
@@ -326,7 +348,6 @@ def run_ours(args, wl):
     clocks = ClockSampler(torch.cuda.current_device()) if rank == 0 else None
     if clocks:
         clocks.start()
-        time.sleep(0.3)
     _lib.LAUNCH_COUNTER.update(calls=0, kernels=0)
     st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()

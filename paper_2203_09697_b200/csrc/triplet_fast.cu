@@ -326,7 +326,54 @@ bw1_kernel(const int64_t* __restrict__ edge_ptr, const int32_t* __restrict__ rev
 
 // ---------------------------------------------------------------------------
 // bw2: Qbar = C^T Sbar per (centre, 64-channel block); X_bar, W_bar partials, dd partials.
-// grid = (centre CTAs, channel blocks).  Thread (rg, cg): q = q0 + rg, all L, 8 channels.
+// grid = (centre CTAs, channel blocks).  The in-edges q of a centre go in batches of TQ = 16
+// (or 8 for a short tail).  Main loop: thread (rg, cg) owns row q = qb0 + rg, all L and
+// TQ/2 channels, Qbar accumulated over the out-edges p.  The batch's Qbar is staged in shared
+// memory; the epilogue then runs one thread per channel (two halves splitting the rows), so
+// the gate weights W[:, :, c] sit in registers and the chain rule folds through
+// v_k = sum_l Qbar_l W[k, l, c]:
+//   X_bar = sum_k rbf_k v_k,  dd = sum_c X sum_k rbf_k' v_k,  W_bar[k, l, c] += rbf_k X Qbar_l
+// W_bar accumulates in registers for the CTA's whole life (one partial per CTA).
+template <int L, int TQ>
+__device__ __forceinline__ void bw2_main(const float* Cb, const float* Sb, int n, float* QB) {
+  constexpr int CG = kT / TQ;           // channel groups: 8 (TQ 16) or 16 (TQ 8)
+  constexpr int CPT = kCB / CG;         // channels per thread: 8 or 4
+  const int tid = threadIdx.x, cg = tid % CG, rg = tid / CG;
+  float acc[L][CPT];
+#pragma unroll
+  for (int l = 0; l < L; ++l)
+#pragma unroll
+    for (int i = 0; i < CPT; ++i) acc[l][i] = 0.f;
+#pragma unroll 2
+  for (int p = 0; p < n; ++p) {
+    const float4 a0 = *reinterpret_cast<const float4*>(Cb + (p * TQ + rg) * 8);
+    const float4 a1 = *reinterpret_cast<const float4*>(Cb + (p * TQ + rg) * 8 + 4);
+    const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+    float bv[CPT];
+    {
+      const float4 b0 = *reinterpret_cast<const float4*>(Sb + p * kCB + cg * 4);
+      bv[0] = b0.x; bv[1] = b0.y; bv[2] = b0.z; bv[3] = b0.w;
+    }
+    if (CPT == 8) {
+      const float4 b1 = *reinterpret_cast<const float4*>(Sb + p * kCB + 32 + cg * 4);
+      bv[4 % CPT] = b1.x; bv[5 % CPT] = b1.y; bv[6 % CPT] = b1.z; bv[7 % CPT] = b1.w;
+    }
+#pragma unroll
+    for (int l = 0; l < L; ++l)
+#pragma unroll
+      for (int i = 0; i < CPT; ++i) acc[l][i] = fmaf(av[l], bv[i], acc[l][i]);
+  }
+  __syncthreads();  // every Cb read done: QB aliases it
+#pragma unroll
+  for (int l = 0; l < L; ++l) {
+    float* row = QB + (rg * L + l) * kCB;
+    *reinterpret_cast<float4*>(row + cg * 4) = make_float4(acc[l][0], acc[l][1], acc[l][2], acc[l][3]);
+    if (CPT == 8)
+      *reinterpret_cast<float4*>(row + 32 + cg * 4) =
+          make_float4(acc[l][4 % CPT], acc[l][5 % CPT], acc[l][6 % CPT], acc[l][7 % CPT]);
+  }
+}
+
 template <int K, int L>
 __global__ void __launch_bounds__(kT, 3)
 bw2_kernel(const int64_t* __restrict__ edge_ptr, const int32_t* __restrict__ rev,
@@ -338,148 +385,145 @@ bw2_kernel(const int64_t* __restrict__ edge_ptr, const int32_t* __restrict__ rev
   extern __shared__ __align__(16) float dsm[];
   float4* Us = reinterpret_cast<float4*>(dsm);      // [64]
   float* Rb = dsm + 4 * kN;                          // [64 * K]
-  float* Cb = Rb + ((kN * K + 3) & ~3);              // [p][rg*8 + l]  (one q per row group)
+  float* Cb = Rb + ((kN * K + 3) & ~3);              // [p][TQ q][8 l]; QB [TQ][L][64] aliases it
   float* Sb = Cb + kN * 16 * 8;                      // Sbar rows of the centre, this channel block
-  float* Wsm = Sb + kN * kCB;
-  float* Wb = Wsm + K * L * kCB;
-  float* Rst = Cb;                                   // R_bar staging [16][L][64] aliases Cb
-  const int tid = threadIdx.x, cg = tid & 7, rg = tid >> 3;
-  const int c0 = blockIdx.y * kCB;
+  float* Wsm = Sb + kN * kCB;                        // W[k, l, c0 + c]
+  float* DD = Wsm + K * L * kCB;                     // [16][2] dd partial per row and warp
+  const int tid = threadIdx.x;
+  const int c = tid & (kCB - 1), h = tid >> 6;       // epilogue: channel, row half
+  const int64_t c0 = static_cast<int64_t>(blockIdx.y) * kCB;
+  const bool cok = c0 + c < dg;
   for (int i = tid; i < K * L * kCB; i += kT) {
-    const int kl = i / kCB, c = i - kl * kCB;
-    Wsm[i] = c0 + c < dg ? W[kl * dg + c0 + c] : 0.f;
-    Wb[i] = 0.f;
+    const int kl = i / kCB, cc = i - kl * kCB;
+    Wsm[i] = c0 + cc < dg ? W[kl * dg + c0 + cc] : 0.f;
   }
+  float wb[K][L];
+#pragma unroll
+  for (int k = 0; k < K; ++k)
+#pragma unroll
+    for (int l = 0; l < L; ++l) wb[k][l] = 0.f;
   for (int64_t j = blockIdx.x; j < nv; j += gridDim.x) {
     const int64_t off = edge_ptr[j];
     const int n = static_cast<int>(edge_ptr[j + 1] - off);
     if (n > kN || n == 0) continue;
     if (n == 1) {
       const int64_t r0 = rev[off];
-      for (int c = tid; c < kCB; c += kT)
-        if (c0 + c < dg) Xbar[r0 * dg + c0 + c] = 0.f;
+      if (tid < kCB && cok) Xbar[r0 * dg + c0 + tid] = 0.f;
       if (tid == 0 && gridDim.y > 1) dd_part[blockIdx.y * num_edges + off] = 0.f;
       continue;
     }
     __syncthreads();
     load_center<K>(Us, Rb, geo, off, n, rp);
     for (int i = tid; i < n * kCB; i += kT) {
-      const int p = i >> 6, c = i & 63;
-      Sb[i] = c0 + c < dg ? Sbar[(off + p) * dg + c0 + c] : 0.f;
+      const int p = i >> 6, cc = i & 63;
+      Sb[i] = c0 + cc < dg ? Sbar[(off + p) * dg + c0 + cc] : 0.f;
     }
     for (int qb0 = 0; qb0 < n; qb0 += 16) {
+      const int nr = min(16, n - qb0);
+      const int TQ = nr <= 8 ? 8 : 16;
+      // X rows of this thread's epilogue rows, fetched before the main loop
+      float xo[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int r = h + 2 * i;
+        xo[i] = (r < nr && cok) ? __ldg(X + static_cast<int64_t>(rev[off + qb0 + r]) * dg + c0 + c) : 0.f;
+      }
       __syncthreads();
-      // Cb[p][rg*8 + l] = T_l(x_{p, qb0+rg}) (masked)
-      for (int i = tid; i < n * 16; i += kT) {
-        const int p = i >> 4, g = i & 15;
+      // Cb[p][g][l] = T_l(x_{p, qb0+g}) (masked on p == q and q >= n)
+      for (int i = tid; i < n * TQ; i += kT) {
+        const int p = i / TQ, g = i - p * TQ;
         const int q = qb0 + g;
         const bool ok = q < n && p != q;
         const float4 a = Us[p];
         const float4 b = ok ? Us[q] : a;
         const float x = a.x * b.x + a.y * b.y + a.z * b.z;
         const float m = ok ? 1.f : 0.f;
-        float* dst = Cb + p * 128 + g * 8;
+        float t[8];
         float tp = m * x, tc = m;
 #pragma unroll
         for (int l = 0; l < 8; ++l) {
-          dst[l] = l < L ? tc : 0.f;
+          t[l] = l < L ? tc : 0.f;
           const float tn = fmaf(2.f * x, tc, -tp);
           tp = tc;
           tc = tn;
         }
+        float4* dst = reinterpret_cast<float4*>(Cb + (p * TQ + g) * 8);
+        dst[0] = make_float4(t[0], t[1], t[2], t[3]);
+        dst[1] = make_float4(t[4], t[5], t[6], t[7]);
       }
       __syncthreads();
-      float qb[8][8];
+      if (TQ == 8) bw2_main<L, 8>(Cb, Sb, n, Cb);
+      else bw2_main<L, 16>(Cb, Sb, n, Cb);
+      __syncthreads();
+      // epilogue: thread (c, h) takes rows h, h + 2, ... of the batch
+      float wr[K][L];
 #pragma unroll
-      for (int l = 0; l < 8; ++l)
+      for (int k = 0; k < K; ++k)
 #pragma unroll
-        for (int i = 0; i < 8; ++i) qb[l][i] = 0.f;
-#pragma unroll 2
-      for (int p = 0; p < n; ++p) {
-        const float4 a0 = *reinterpret_cast<const float4*>(Cb + p * 128 + rg * 8);
-        const float4 a1 = *reinterpret_cast<const float4*>(Cb + p * 128 + rg * 8 + 4);
-        const float4 b0 = *reinterpret_cast<const float4*>(Sb + p * kCB + cg * 4);
-        const float4 b1 = *reinterpret_cast<const float4*>(Sb + p * kCB + 32 + cg * 4);
-        const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
-        const float bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
-#pragma unroll
-        for (int l = 0; l < L; ++l)
-#pragma unroll
-          for (int i = 0; i < 8; ++i) qb[l][i] = fmaf(av[l], bv[i], qb[l][i]);
-      }
-      // epilogue for row q
-      const int q = qb0 + rg;
-      const bool valid = q < n;
-      const float4 uq = valid ? Us[q] : make_float4(0.f, 0.f, 0.f, 1.f);
-      const int64_t rq = valid ? static_cast<int64_t>(rev[off + q]) : 0;
-      float rbo[K], rdo[K];
-#pragma unroll
-      for (int k = 0; k < K; ++k) {
-        rbo[k] = valid ? Rb[q * K + k] : 0.f;
-        rdo[k] = -2.f * rp.gamma * (uq.w - rp.step * k) * rbo[k];
-      }
-      float xo[8], xb[8];
+        for (int l = 0; l < L; ++l) wr[k][l] = Wsm[(k * L + l) * kCB + c];
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
-        const int c = c0 + chan(cg, i);
-        xo[i] = (valid && c < dg) ? X[rq * dg + c] : 0.f;
-        xb[i] = 0.f;
-      }
-      float dd = 0.f;
-      __syncthreads();  // Cb reads done: Rst may overwrite it
+        const int r = h + 2 * i;
+        if (r >= nr) break;
+        const int q = qb0 + r;
+        const float d = Us[q].w;
+        float rb[K], v[K];
 #pragma unroll
-      for (int l = 0; l < L; ++l) {
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const int c = chan(cg, i);
-          float rw = 0.f, rwd = 0.f;
-#pragma unroll
-          for (int k = 0; k < K; ++k) {
-            const float w = Wsm[(k * L + l) * kCB + c];
-            rw = fmaf(rbo[k], w, rw);
-            rwd = fmaf(rdo[k], w, rwd);
-          }
-          xb[i] = fmaf(qb[l][i], rw, xb[i]);
-          const float rbar = qb[l][i] * xo[i];
-          dd = fmaf(rbar, rwd, dd);
-          Rst[(rg * L + l) * kCB + c] = rbar;  // zero for invalid rows (xo == 0)
+        for (int k = 0; k < K; ++k) {
+          rb[k] = Rb[q * K + k];
+          v[k] = 0.f;
         }
-      }
-      dd += __shfl_xor_sync(0xffffffffu, dd, 1);
-      dd += __shfl_xor_sync(0xffffffffu, dd, 2);
-      dd += __shfl_xor_sync(0xffffffffu, dd, 4);
-      if (valid) {
+        float qv[L];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const int c = c0 + chan(cg, i);
-          if (c < dg) Xbar[rq * dg + c] = xb[i];
+        for (int l = 0; l < L; ++l) qv[l] = Cb[(r * L + l) * kCB + c];
+#pragma unroll
+        for (int k = 0; k < K; ++k)
+#pragma unroll
+          for (int l = 0; l < L; ++l) v[k] = fmaf(qv[l], wr[k][l], v[k]);
+        float xb = 0.f, ds = 0.f;
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+          xb = fmaf(rb[k], v[k], xb);
+          ds = fmaf(-2.f * rp.gamma * (d - rp.step * k) * rb[k], v[k], ds);
         }
-        if (cg == 0) {
-          if (gridDim.y == 1) edge_grad[off + q].w += dd;  // single channel block: final value
-          else dd_part[blockIdx.y * num_edges + off + q] = dd;
+        if (cok) Xbar[static_cast<int64_t>(rev[off + q]) * dg + c0 + c] = xb;
+        const float x = xo[i];
+#pragma unroll
+        for (int l = 0; l < L; ++l) {
+          const float rbar = qv[l] * x;
+#pragma unroll
+          for (int k = 0; k < K; ++k) wb[k][l] = fmaf(rb[k], rbar, wb[k][l]);
         }
+        float dd = ds * x;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) dd += __shfl_xor_sync(0xffffffffu, dd, o);
+        if ((tid & 31) == 0) DD[r * 2 + ((tid >> 5) & 1)] = dd;
       }
       __syncthreads();
-      // W_bar[k,l,c] += sum_{rows} rbf_k(q) R_bar[q,l,c]; thread-owned (l, c) entries
-      const int nrow = min(16, n - qb0);
-      for (int idx = tid; idx < L * kCB; idx += kT) {
-        float s[K];
-#pragma unroll
-        for (int k = 0; k < K; ++k) s[k] = Wb[k * L * kCB + idx];
-        for (int r = 0; r < nrow; ++r) {
-          const float rv = Rst[r * L * kCB + idx];
-#pragma unroll
-          for (int k = 0; k < K; ++k) s[k] = fmaf(Rb[(qb0 + r) * K + k], rv, s[k]);
-        }
-#pragma unroll
-        for (int k = 0; k < K; ++k) Wb[k * L * kCB + idx] = s[k];
+      if (tid < nr) {
+        const float dd = DD[tid * 2] + DD[tid * 2 + 1];
+        if (gridDim.y == 1) edge_grad[off + qb0 + tid].w += dd;  // single channel block: final value
+        else dd_part[blockIdx.y * num_edges + off + qb0 + tid] = dd;
       }
     }
   }
+  // combine the two row halves (fixed order), one partial per CTA:
+  // layout [gridDim.y][gridDim.x][K*L*64]
   __syncthreads();
-  // partial layout [gridDim.y][gridDim.x][K*L*64]
-  float* dst = wbar_part + (static_cast<int64_t>(blockIdx.y) * gridDim.x + blockIdx.x) * (K * L * kCB);
-  for (int i = tid; i < K * L * kCB; i += kT) dst[i] = Wb[i];
+  if (h == 1) {
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+#pragma unroll
+      for (int l = 0; l < L; ++l) Cb[(k * L + l) * kCB + c] = wb[k][l];
+  }
+  __syncthreads();
+  if (h == 0) {
+    float* dst = wbar_part + (static_cast<int64_t>(blockIdx.y) * gridDim.x + blockIdx.x) * (K * L * kCB);
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+#pragma unroll
+      for (int l = 0; l < L; ++l) dst[(k * L + l) * kCB + c] = wb[k][l] + Cb[(k * L + l) * kCB + c];
+  }
 }
 
 // W_bar[k,l,c] = sum over x-CTAs of the partials of channel block c / 64; 32 outputs per
@@ -565,7 +609,7 @@ int fast_bwd(const int64_t* edge_ptr, const int32_t* rev, const float4* geo, int
   float* wpart = reinterpret_cast<float*>(ws);
   float* ddpart = wpart + static_cast<int64_t>(ncb) * gx * K * L * fast::kCB;
   const size_t smem = (4 * fast::kN + ((fast::kN * 6 + 3) & ~3) + fast::kN * 128 + fast::kN * fast::kCB +
-                       2 * 6 * 7 * fast::kCB) * sizeof(float);
+                       6 * 7 * fast::kCB + 32) * sizeof(float);
   auto k2 = fast::bw2_kernel<6, 7>;
   static bool k2_configured = false;
   if (!k2_configured) {
