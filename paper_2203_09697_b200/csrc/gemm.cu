@@ -69,6 +69,9 @@ struct Params {
   int mcast;               // 1: CTA pairs (cluster of 2) share each A k-block by TMA multicast
   int64_t split_stride;    // split-K: elements between partial outputs
   long long* trace;        // debug timeline (EGN_GEMM_TRACE), CTA 0 only
+  int dbg;                 // EGN_GEMM_DBG experiments: 1 no MMA, 2 no split math, 4 no TMEM reads
+  int op_tma;              // (with store_warp) residual / aux rows arrive by TMA through mapOp
+  int store_warp;          // (with tma_out) a dedicated warp issues the TMA stores
 };
 
 // ---------------------------------------------------------------- PTX helpers
@@ -86,9 +89,15 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "WAIT_%=:\n\t"
+#ifdef EGN_WAIT_HINT
       "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
       "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
-      "r"(parity), "r"(1000000)
+      "r"(parity), "r"(EGN_WAIT_HINT)
+#else
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+#endif
       : "memory");
 }
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
@@ -223,22 +232,34 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
 // so shared-memory traffic per k-step is the B operand only.
 // Accuracy: the tensor core accumulates with truncation, a bias that grows with
 // the number of k-steps summed in TMEM.  All three products of a k-step go to a
-// TMEM tile (double buffered per group) that is restarted every P.flush_steps
+// TMEM tile (kAccBufs buffers per group) that is restarted every P.flush_steps
 // k-steps; the group adds each finished window into fp32 registers (round to
 // nearest).
-// TMEM columns: [0, 256) accumulators (group, buffer) x 64; [256, 256 + 64 kOpRing)
+// TMEM columns: [0, 384) accumulators (group, buffer of kAccBufs) x 64; [384, 384 + 64 kOpRing)
 // A operand slots (hi at +0, lo at +32).
 // Epilogue: each warp owns a [2 chunks][32 rows][32 cols] fp32 buffer (16-byte
 // granules XOR-swizzled by row), prefetched with the operand rows (residual /
 // gathered rows / aux) during the main loop; thread = row combines in place,
 // then lanes = columns copy out coalesced.
-constexpr int BN = 64;
-constexpr int kTmaRing = 5;
-constexpr int kOpRing = 2;
-constexpr int kTmaSlot = BM * BK * 4 + BN * BK * 4;  // 24 KB raw A + raw B
-constexpr int kOpSlot = 2 * BN * BK * 4;            // 16 KB B hi + lo
-constexpr int kEpiWarp = 2 * 32 * 32 * 4;           // 8 KB per accumulator warp
-constexpr size_t kGemmSmem = static_cast<size_t>(kTmaRing) * kTmaSlot + kOpRing * kOpSlot + 8 * kEpiWarp + 1024;
+constexpr int kEpiWarp = 2 * 32 * 32 * 4;  // 8 KB per accumulator warp
+constexpr int EW = 64;                     // output columns per accumulator warp
+// Per-tile-width configuration.  BN = 64: two accumulator groups of 4 warps (tile
+// parity), each warp 32 rows x 64 columns.  BN = 128 (N % 128 == 0): one group of 8
+// warps, warp = (row quarter, column half); one A k-block feeds N = 128 MMAs, which
+// run at twice the N = 64 rate per output column.
+template <int BN>
+struct Cfg {
+  static constexpr int kTmaRing = BN == 64 ? 5 : 3;
+  static constexpr int kOpRing = 2;
+  static constexpr int kAccBufs = BN == 64 ? 2 : 3;  // TMEM window buffers per group
+  static constexpr int kGroups = BN == 64 ? 2 : 1;
+  static constexpr int kTmaSlot = BM * BK * 4 + BN * BK * 4;  // raw A + raw B k-block
+  static constexpr int kOpSlot = 2 * BN * BK * 4;             // B hi + lo
+  static constexpr size_t kSmem =
+      static_cast<size_t>(kTmaRing) * kTmaSlot + kOpRing * kOpSlot + 8 * kEpiWarp + 1024;
+  static_assert(kGroups * kAccBufs * BN + 64 * kOpRing <= 512, "TMEM columns");
+  static_assert(kSmem <= 232448, "shared memory");
+};
 
 __device__ __forceinline__ void mma_tf32_ta(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc,
                                             uint32_t accumulate) {
@@ -271,22 +292,29 @@ __device__ __forceinline__ float dsilu(float o) {
 // element (r, c) of a [32][32] epilogue chunk (granule swizzled by row)
 __device__ __forceinline__ int epi_idx(int r, int c) { return r * 32 + ((((c >> 2) ^ (r & 7))) << 2) + (c & 3); }
 
-template <bool AMN, bool BMN>
-__global__ void __launch_bounds__(448, 1)
+template <bool AMN, bool BMN, int BN>
+__global__ void __launch_bounds__(480, 1)
 gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_constant__ CUtensorMap mapB0,
                    const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ CUtensorMap mapB1,
-                   const __grid_constant__ CUtensorMap mapOut, Params P, int tiles_n, int splits, int total_items) {
+                   const __grid_constant__ CUtensorMap mapOut, const __grid_constant__ CUtensorMap mapOp, Params P,
+                   int tiles_n, int splits, int total_items) {
   constexpr int A_BYTES = BM * BK * 4;  // 16 KB raw A k-block
-  constexpr int B_BYTES = BN * BK * 4;  // 8 KB
+  using C = Cfg<BN>;
+  constexpr int kTmaRing = C::kTmaRing, kOpRing = C::kOpRing, kAccBufs = C::kAccBufs, kGroups = C::kGroups;
+  constexpr int kTmaSlot = C::kTmaSlot, kOpSlot = C::kOpSlot;
+  constexpr int B_BYTES = BN * BK * 4;  // 8 / 16 KB
   constexpr uint32_t TMEM_COLS = 512;
-  constexpr uint32_t A_TMEM = 256;
+  constexpr uint32_t A_TMEM = kGroups * kAccBufs * BN;  // 384
   extern __shared__ __align__(16) uint8_t smem_raw[];
   // 1024-byte alignment for SWIZZLE_128B by offsetting the __shared__ array itself
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* opring = smem + kTmaRing * kTmaSlot;
   float* epi_all = reinterpret_cast<float*>(opring + kOpRing * kOpSlot);
   __shared__ __align__(8) uint64_t tma_full[kTmaRing], tma_empty[kTmaRing], op_full[kOpRing], op_empty[kOpRing];
-  __shared__ __align__(8) uint64_t accf_bar[2][2], acce_bar[2][2];
+  __shared__ __align__(8) uint64_t accf_bar[kGroups][kAccBufs], acce_bar[kGroups][kAccBufs];
+  // store warp hand-off per group: results staged (epi_full), staging read by the TMA store
+  // (buf_free), next tile's operand rows landed in the staging buffers (op_bar)
+  __shared__ __align__(8) uint64_t epi_full[kGroups], buf_free[kGroups], op_bar[kGroups];
   __shared__ uint32_t tmem_base;
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -301,6 +329,13 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_const
 
   const uint32_t crank = P.mcast ? cluster_rank() : 0;
   if (tid == 0) {
+    // descriptor fetches off the critical path (the output map is first used at the end of a tile)
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&mapA0) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&mapB0) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&mapA1) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&mapB1) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&mapOut) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&mapOp) : "memory");
     for (int s = 0; s < kTmaRing; ++s) {
       mbar_init(&tma_full[s], 1);
       // the multicast leader reuses slot s only after both CTAs' split warps released it
@@ -310,11 +345,14 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_const
       mbar_init(&op_full[s], 1);
       mbar_init(&op_empty[s], 1);
     }
-    for (int gr = 0; gr < 2; ++gr) {
-      for (int b = 0; b < 2; ++b) {
+    for (int gr = 0; gr < kGroups; ++gr) {
+      for (int b = 0; b < kAccBufs; ++b) {
         mbar_init(&accf_bar[gr][b], 1);
-        mbar_init(&acce_bar[gr][b], 4);
+        mbar_init(&acce_bar[gr][b], 8 / kGroups);  // every warp of the group drains
       }
+      mbar_init(&epi_full[gr], 8 / kGroups);
+      mbar_init(&buf_free[gr], 1);
+      mbar_init(&op_bar[gr], 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -354,13 +392,16 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_const
         EGN_TRACE(0, it);
         if (elect_one()) {
           uint8_t* st = smem + s * kTmaSlot;
-          mbar_expect_tx(&tma_full[s], A_BYTES + B_BYTES);
+          const bool skip_b = P.dbg & 16, skip_a = (P.dbg & 32) && (n0 != 0);
+          if (skip_a && skip_b) mbar_arrive(&tma_full[s]);
+          else mbar_expect_tx(&tma_full[s], (skip_a ? 0 : A_BYTES) + (skip_b ? 0 : B_BYTES));
           const int kb = kbeg + kbl;
           const bool first = kb < nk0;
           const int kk = (first ? kb : kb - nk0) * BK;
           const CUtensorMap* ma = first ? &mapA0 : &mapA1;
           const CUtensorMap* mb = first ? &mapB0 : &mapB1;
-          if (AMN) {
+          if (skip_a) {
+          } else if (AMN) {
             tma_load_2d(st, ma, &tma_full[s], static_cast<int>(m0), kk);  // [32 k][128 m], unswizzled
           } else if (!P.mcast) {
             tma_load_2d(st, ma, &tma_full[s], kk, static_cast<int>(m0));  // [128 m][32 k], SW128
@@ -368,7 +409,8 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_const
             // both CTAs of the pair work on this m-tile: one L2 read, delivered to both
             tma_load_2d_mc(st, ma, &tma_full[s], kk, static_cast<int>(m0), 0x3);
           }
-          if (BMN) {
+          if (skip_b) {
+          } else if (BMN) {
 #pragma unroll
             for (int i = 0; i < BN / 32; ++i) tma_load_2d(st + A_BYTES + i * 4096, mb, &tma_full[s], n0 + 32 * i, kk);
           } else {
@@ -384,13 +426,14 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_const
                            (static_cast<uint32_t>(BN >> 3) << 17) | (static_cast<uint32_t>(BM >> 4) << 24);
     uint32_t it = 0, t = 0;
     uint32_t fc0 = 0, fc1 = 0;  // window counters per accumulator group
+    uint32_t wtr = 0;           // (trace) windows started
     for (int item = blockIdx.x; item < total_items; item += gridDim.x, ++t) {
       int64_t m0;
       int n0, kbeg, nk;
       item_coords(item, m0, n0, kbeg, nk);
-      const int gr = t & 1;
+      const int gr = kGroups == 2 ? static_cast<int>(t & 1) : 0;
       uint32_t& fc = gr ? fc1 : fc0;
-      const uint32_t tg = tmem + gr * (2 * BN);
+      const uint32_t tg = tmem + gr * (kAccBufs * BN);
       uint32_t tacc = tg, bsel = 0;
       const int nsteps = nk * (BK / 8);
       const int win = P.flush_steps > 0 ? P.flush_steps : nsteps;
@@ -407,14 +450,16 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_const
         for (int k = 0; k < BK / 8; ++k) {
           const bool fstart = wpos == 0;
           if (fstart) {
-            bsel = fc & 1;
-            mbar_wait(&acce_bar[gr][bsel], ((fc >> 1) & 1) ^ 1);
+            bsel = fc % kAccBufs;
+            mbar_wait(&acce_bar[gr][bsel], ((fc / kAccBufs) & 1) ^ 1);
+            EGN_TRACE(12, wtr);
+            ++wtr;
             asm volatile("tcgen05.fence::after_thread_sync;");
             tacc = tg + bsel * BN;
           }
           ++j;
           const bool fend = (++wpos == win) || (j == nsteps);
-          if (elect_one()) {
+          if (elect_one() && !(P.dbg & 1)) {
             const uint32_t ob = BMN ? k * 1024 : k * 32;
             const uint64_t dbh = BMN ? sw128_mnmajor_desc_u(bhi + ob) : sw128_kmajor_desc_u(bhi + ob);
             const uint64_t dbl = BMN ? sw128_mnmajor_desc_u(blo + ob) : sw128_kmajor_desc_u(blo + ob);
@@ -422,8 +467,8 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_const
             mma_tf32_ta(tacc, ta + 32 + k * 8, dbh, idesc, fstart ? 0u : 1u);
             mma_tf32_ta(tacc, ta + k * 8, dbl, idesc, 1u);
             mma_tf32_ta(tacc, ta + k * 8, dbh, idesc, 1u);
-            if (fend) mma_commit(&accf_bar[gr][bsel]);
           }
+          if (fend && elect_one()) mma_commit(&accf_bar[gr][bsel]);  // same elected lane as the MMAs
           __syncwarp();
           if (fend) {
             ++fc;
@@ -453,9 +498,11 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_const
         mbar_wait(&tma_full[s], (it / kTmaRing) & 1);
         if (ct == 0) EGN_TRACE(2, it);
         mbar_wait(&op_empty[o], ((it / kOpRing) & 1) ^ 1);
+        if (ct == 0) EGN_TRACE(11, it);
         asm volatile("tcgen05.fence::after_thread_sync;");
         const uint8_t* st = smem + s * kTmaSlot;
         const uint32_t ta = tmem + lane_off + A_TMEM + o * 64;
+        if (!(P.dbg & 2)) {
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           float hi[16], lo[16];
@@ -494,6 +541,7 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_const
           bhi[i] = h;
           blo[i] = make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w);
         }
+        }
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         asm volatile("tcgen05.fence::before_thread_sync;");
@@ -507,29 +555,41 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_const
       }
       if (AMN && P.gsum_part != nullptr && n0 == 0 && m0 + r < P.M) P.gsum_part[z * P.M + m0 + r] = gs;
     }
-  } else {
+  } else if (warp < 14) {
     // ---------------- accumulator groups + epilogue (thread = tile row)
-    const int gr = (warp - 6) >> 2;
+    const int gr = kGroups == 2 ? (warp - 6) >> 2 : 0;
+    const int chalf = kGroups == 2 ? 0 : (warp - 6) >> 2;  // this warp's 64-column half of the tile
     const int q = warp & 3;  // TMEM lane quarter == this warp's 32 tile rows
     const uint32_t lane_off = static_cast<uint32_t>(q * 32) << 16;
-    const uint32_t tg = tmem + gr * (2 * BN) + lane_off;
+    const uint32_t tg = tmem + gr * (kAccBufs * BN) + lane_off + chalf * EW;
     float* ebuf = epi_all + (warp - 6) * (2 * 32 * 32);
     const int opkind = (P.flags & EPI_RESID) ? 1 : ((P.flags & EPI_GATHER) ? 2 : ((P.flags & (EPI_DSILU_AUX | EPI_MUL_AUX)) ? 3 : 0));
     uint32_t fcount = 0;
     uint32_t t = 0;
     for (int item = blockIdx.x; item < total_items; item += gridDim.x, ++t) {
-      if ((t & 1) != static_cast<uint32_t>(gr)) continue;
-      if (q == 0 && gr == 0) EGN_TRACE(7, t);
+      if (kGroups == 2 && (t & 1) != static_cast<uint32_t>(gr)) continue;
+      if (q == 0 && gr == 0 && chalf == 0) EGN_TRACE(7, t);
       int64_t m0;
       int n0, kbeg, nk;
       const int z = item_coords(item, m0, n0, kbeg, nk);
+      n0 += chalf * EW;  // this warp's columns
       const int64_t rbase = m0 + q * 32;
       const int nrows = P.M - rbase < 32 ? static_cast<int>(P.M - rbase) : 32;
-      if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-      __syncwarp();  // previous tile's copy-out / TMA store done with the buffer
+      const uint32_t u = t / kGroups;  // this group's tile count
+      // with TMA stores the staging buffer is free once the store warp saw the previous
+      // store read it; operand rows by TMA are loaded by the store warp itself
+      const bool sw = P.tma_out && P.store_warp;
+      const bool op_async = opkind && !(sw && P.op_tma);
+      if (sw) {
+        if (op_async) mbar_wait(&buf_free[gr], (u & 1) ^ 1);
+      } else if (lane == 0) {
+        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // own previous store
+      }
+      __syncwarp();
+      if (q == 0 && gr == 0 && chalf == 0) EGN_TRACE(15, t);
       // prefetch this warp's operand rows into the swizzled buffer (16 B cp.async,
       // two rows per instruction), overlapped with the main loop
-      if (opkind) {
+      if (op_async) {
         int32_t gi = 0;
         if (opkind == 2 && lane < nrows) gi = P.gidx[rbase + lane];
         const int half = lane >> 4, gcol = lane & 15;  // 16 granules = 64 columns per row
@@ -548,20 +608,21 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_const
         }
         asm volatile("cp.async.commit_group;" ::: "memory");
       }
-      float acc[BN];
+      float acc[EW];
 #pragma unroll
-      for (int i = 0; i < BN; ++i) acc[i] = 0.f;
+      for (int i = 0; i < EW; ++i) acc[i] = 0.f;
       const int nsteps = nk * (BK / 8);
       const int win = P.flush_steps > 0 ? P.flush_steps : nsteps;
       const int nflush = nsteps > 0 ? (nsteps + win - 1) / win : 0;
       for (int j = 0; j < nflush; ++j, ++fcount) {
-        const uint32_t b = fcount & 1;
-        mbar_wait(&accf_bar[gr][b], (fcount >> 1) & 1);
-        if (q == 0 && gr == 0) EGN_TRACE(5, fcount);
+        const uint32_t b = fcount % kAccBufs;
+        mbar_wait(&accf_bar[gr][b], (fcount / kAccBufs) & 1);
+        if (q == 0 && gr == 0 && chalf == 0) EGN_TRACE(5, fcount);
         asm volatile("tcgen05.fence::after_thread_sync;");
         const uint32_t base = tg + b * BN;
 #pragma unroll
-        for (int c = 0; c < BN; c += 16) {
+        for (int c = 0; c < EW; c += 16) {
+          if (P.dbg & 4) break;
           float v[16];
           tmem_ld16<16>(base + c, v);
 #pragma unroll
@@ -572,10 +633,13 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_const
         __syncwarp();
         if (lane == 0) mbar_arrive(&acce_bar[gr][b]);
       }
-      if (q == 0 && gr == 0) EGN_TRACE(6, t);
-      if (opkind) asm volatile("cp.async.wait_all;" ::: "memory");
+      if (q == 0 && gr == 0 && chalf == 0) EGN_TRACE(6, t);
+      if (P.tma_out && lane == 0) asm volatile("prefetch.tensormap [%0];" ::"l"(&mapOut) : "memory");
+      if (op_async) asm volatile("cp.async.wait_all;" ::: "memory");
+      else if (opkind) mbar_wait(&op_bar[gr], u & 1);
+      else if (sw) mbar_wait(&buf_free[gr], (u & 1) ^ 1);
       __syncwarp();
-      if (q == 0 && gr == 0) EGN_TRACE(8, t);
+      if (q == 0 && gr == 0 && chalf == 0) EGN_TRACE(8, t);
       // thread = row: combine with the operand in place.  Variant loops are
       // hoisted so each unrolled body is branch-free; an additive bias is applied
       // in the copy-out (lane = column), a bias under a product here.
@@ -585,11 +649,11 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_const
 #define EGN_SLOT(c4) reinterpret_cast<float4*>(ebuf + ((c4) >> 3) * 1024 + epi_idx(lane, ((c4) & 7) * 4))
 #define EGN_ACC4(c4) make_float4(acc[(c4) * 4], acc[(c4) * 4 + 1], acc[(c4) * 4 + 2], acc[(c4) * 4 + 3])
       const bool silu2 = fl & EPI_SILU_OUT2;
-      const bool tma_store = P.tma_out && variant <= 1 && !silu2;
-      if (tma_store && has_bias) {
+      const bool tma_store = P.tma_out;  // host: never with SILU_OUT2 / MUL_AUX
+      if (tma_store && has_bias && variant <= 1) {
         // bias here (the TMA store has no lane = column pass); broadcast loads
 #pragma unroll
-        for (int c4 = 0; c4 < BN / 4; ++c4) {
+        for (int c4 = 0; c4 < EW / 4; ++c4) {
           const int col = min(n0 + c4 * 4, P.N - 4);
           const float4 bv = make_float4(__ldg(P.bias + col), __ldg(P.bias + col + 1), __ldg(P.bias + col + 2),
                                         __ldg(P.bias + col + 3));
@@ -602,10 +666,10 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_const
         }
       } else if (variant == 0) {
 #pragma unroll
-        for (int c4 = 0; c4 < BN / 4; ++c4) *EGN_SLOT(c4) = EGN_ACC4(c4);
+        for (int c4 = 0; c4 < EW / 4; ++c4) *EGN_SLOT(c4) = EGN_ACC4(c4);
       } else if (variant == 1) {
 #pragma unroll
-        for (int c4 = 0; c4 < BN / 4; ++c4) {
+        for (int c4 = 0; c4 < EW / 4; ++c4) {
           const float4 o = *EGN_SLOT(c4);
           const float4 a = EGN_ACC4(c4);
           *EGN_SLOT(c4) = make_float4(a.x + o.x, a.y + o.y, a.z + o.z, a.w + o.w);
@@ -613,7 +677,7 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_const
       } else {
         const bool dsl = variant == 2;
 #pragma unroll
-        for (int c4 = 0; c4 < BN / 4; ++c4) {
+        for (int c4 = 0; c4 < EW / 4; ++c4) {
           const float4 o = *EGN_SLOT(c4);
           float4 a = EGN_ACC4(c4);
           const int col = n0 + c4 * 4;
@@ -626,19 +690,25 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_const
         }
       }
       if (tma_store) {
+        if (q == 0 && gr == 0 && chalf == 0) EGN_TRACE(13, t);
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
+        if (q == 0 && gr == 0 && chalf == 0) EGN_TRACE(14, t);
         if (lane == 0) {
-          // [split][M][N] output map: rows >= M clip per split
-          tma_store_3d(&mapOut, ebuf, n0, static_cast<int>(rbase), z);
-          if (n0 + 32 < P.N) tma_store_3d(&mapOut, ebuf + 1024, n0 + 32, static_cast<int>(rbase), z);
-          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+          if (sw) {
+            mbar_arrive(&epi_full[gr]);  // the store warp takes it from here
+          } else {
+            // [split][M][N] output map: rows >= M clip per split
+            tma_store_3d(&mapOut, ebuf, n0, static_cast<int>(rbase), z);
+            if (n0 + 32 < P.N) tma_store_3d(&mapOut, ebuf + 1024, n0 + 32, static_cast<int>(rbase), z);
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+          }
         }
-        if (q == 0 && gr == 0) EGN_TRACE(9, t);
+        if (q == 0 && gr == 0 && chalf == 0) EGN_TRACE(9, t);
         continue;
       }
       __syncwarp();
-      if (q == 0 && gr == 0) EGN_TRACE(9, t);
+      if (q == 0 && gr == 0 && chalf == 0) EGN_TRACE(9, t);
       float* out_base = P.out + static_cast<int64_t>(z) * P.split_stride;
       const int64_t ldo = P.ldo, ldo2 = P.ldo2;
 #pragma unroll
@@ -662,12 +732,12 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_const
           }
         }
       }
-      if (q == 0 && gr == 0) EGN_TRACE(10, t);
+      if (q == 0 && gr == 0 && chalf == 0) EGN_TRACE(10, t);
       if (variant == 3) {
         // out2 = the pre-gate value acc + bias: second pass through the buffer
         __syncwarp();
 #pragma unroll
-        for (int c4 = 0; c4 < BN / 4; ++c4) *EGN_SLOT(c4) = EGN_ACC4(c4);
+        for (int c4 = 0; c4 < EW / 4; ++c4) *EGN_SLOT(c4) = EGN_ACC4(c4);
         __syncwarp();
 #pragma unroll
         for (int ch = 0; ch < 2; ++ch) {
@@ -685,6 +755,69 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_const
 #undef EGN_ACC4
     }
     if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  } else if (P.tma_out && P.store_warp) {
+    // ---------------- store warp: TMA-stores each finished tile from the staging
+    // buffers, then refills them with the operand rows of the group's next tile
+    const int opkind = (P.flags & EPI_RESID) ? 1 : ((P.flags & (EPI_DSILU_AUX | EPI_MUL_AUX)) ? 3 : 0);
+    const bool op_tma = P.op_tma && opkind && !(P.flags & EPI_GATHER);
+    constexpr int kWarps = 8 / kGroups;
+    // staging buffer (g, w) belongs to epilogue warp 6 + g * kWarps + w: rows of its TMEM
+    // lane quarter (warp % 4), columns of its half (one-group layout)
+    auto warp_box = [&](int item, int g, int w, int64_t& rb, int& nn, int& z) {
+      int64_t m0;
+      int n0, kbeg, nk;
+      z = item_coords(item, m0, n0, kbeg, nk);
+      const int ew = g * kWarps + w;
+      rb = m0 + ((6 + ew) & 3) * 32;
+      nn = n0 + (kGroups == 2 ? 0 : (ew >> 2) * EW);
+    };
+    auto prefetch = [&](int item, int g) {
+      if (!op_tma || item >= total_items) return;
+      if (elect_one()) {
+        uint32_t bytes = 0;
+        for (int w = 0; w < kWarps; ++w) {
+          int64_t rb;
+          int nn, z;
+          warp_box(item, g, w, rb, nn, z);
+          bytes += (nn + 32 < P.N ? 2u : 1u) * 4096u;
+        }
+        mbar_expect_tx(&op_bar[g], bytes);
+        for (int w = 0; w < kWarps; ++w) {
+          int64_t rb;
+          int nn, z;
+          warp_box(item, g, w, rb, nn, z);
+          float* eb = epi_all + (g * kWarps + w) * (2 * 32 * 32);
+          tma_load_2d(eb, &mapOp, &op_bar[g], nn, static_cast<int>(rb));
+          if (nn + 32 < P.N) tma_load_2d(eb + 1024, &mapOp, &op_bar[g], nn + 32, static_cast<int>(rb));
+        }
+      }
+      __syncwarp();
+    };
+    for (int g = 0; g < kGroups; ++g) prefetch(blockIdx.x + g * gridDim.x, g);
+    uint32_t t = 0;
+    for (int item = blockIdx.x; item < total_items; item += gridDim.x, ++t) {
+      const int g = kGroups == 2 ? static_cast<int>(t & 1) : 0;
+      const uint32_t u = t / kGroups;
+      mbar_wait(&epi_full[g], u & 1);
+      if (elect_one()) {
+        for (int w = 0; w < kWarps; ++w) {
+          int64_t rb;
+          int nn, z;
+          warp_box(item, g, w, rb, nn, z);
+          const float* eb = epi_all + (g * kWarps + w) * (2 * 32 * 32);
+          // [split][M][N] output map: rows >= M clip per split
+          tma_store_3d(&mapOut, eb, nn, static_cast<int>(rb), z);
+          if (nn + 32 < P.N) tma_store_3d(&mapOut, eb + 1024, nn + 32, static_cast<int>(rb), z);
+        }
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        mbar_arrive(&buf_free[g]);
+      }
+      __syncwarp();
+      prefetch(item + kGroups * gridDim.x, g);
+    }
+    if (elect_one()) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    __syncwarp();
   }
   if (P.trace && tid == 32) {
     long long g;
@@ -753,7 +886,7 @@ static int make_map(CUtensorMap* map, const float* ptr, int64_t outer, int64_t i
   return 0;
 }
 
-constexpr int kGemmThreads = 448;
+constexpr int kGemmThreads = 480;  // 14 role warps + the store warp
 
 // Output map [splits][M][N] (row stride ld, split stride M * ld), box 32 x 32 x 1,
 // SWIZZLE_128B: the epilogue buffer layout (16-byte granules XOR row % 8).
@@ -776,11 +909,11 @@ static bool out_map_ok(const float* out, int64_t ldo) {
   return (reinterpret_cast<uintptr_t>(out) & 15) == 0 && (ldo * 4) % 16 == 0;
 }
 
-template <bool AMN, bool BMN>
+template <bool AMN, bool BMN, int BN>
 static int launch(const CUtensorMap& a0, const CUtensorMap& b0, const CUtensorMap& a1, const CUtensorMap& b1,
-                  const CUtensorMap& mo, const Params& P, int splits, cudaStream_t st) {
-  const size_t smem = kGemmSmem;
-  auto kern = gemm_tf32x3_kernel<AMN, BMN>;
+                  const CUtensorMap& mo, const CUtensorMap& mop, const Params& P, int splits, cudaStream_t st) {
+  const size_t smem = Cfg<BN>::kSmem;
+  auto kern = gemm_tf32x3_kernel<AMN, BMN, BN>;
   static bool configured = false;
   if (!configured) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
@@ -829,7 +962,7 @@ static int launch(const CUtensorMap& a0, const CUtensorMap& b0, const CUtensorMa
       cfg.stream = st;
       cfg.attrs = at;
       cfg.numAttrs = 1;
-      cudaLaunchKernelEx(&cfg, kern, a0, b0, a1, b1, mo, Q, tiles_n, splits, total);
+      cudaLaunchKernelEx(&cfg, kern, a0, b0, a1, b1, mo, mop, Q, tiles_n, splits, total);
       return check_launch("gemm_tf32x3_mc");
     }
   }
@@ -838,8 +971,9 @@ static int launch(const CUtensorMap& a0, const CUtensorMap& b0, const CUtensorMa
     long long* d = nullptr;
     cudaMalloc(&d, (1024 + 4 * kNumSMs) * sizeof(long long));
     cudaMemset(d, 0, (1024 + 4 * kNumSMs) * sizeof(long long));
+    static_assert(16 * 64 <= 1024, "trace rows");
     Q.trace = d;
-    kern<<<grid, kGemmThreads, smem, st>>>(a0, b0, a1, b1, mo, Q, tiles_n, splits, total);
+    kern<<<grid, kGemmThreads, smem, st>>>(a0, b0, a1, b1, mo, mop, Q, tiles_n, splits, total);
     long long h[1024 + 4 * kNumSMs];
     cudaStreamSynchronize(st);
     cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
@@ -856,9 +990,10 @@ static int launch(const CUtensorMap& a0, const CUtensorMap& b0, const CUtensorMa
     }
     cudaFree(d);
     long long t0 = h[0];
-    const char* names[11] = {"prod_issue", "mma_conv_ok", "conv_full_ok", "conv_done", "mma_issued", "acc0_flush",
-                             "epi0_start", "tile0_begin", "epi0_opwait", "epi0_rows", "epi0_out"};
-    for (int r = 0; r < 11; ++r) {
+    const char* names[16] = {"prod_issue", "mma_conv_ok", "conv_full_ok", "conv_done", "mma_issued", "acc0_flush",
+                             "epi0_start", "tile0_begin", "epi0_opwait", "epi0_rows", "epi0_out", "conv_op_ok",
+                             "mma_win_ok", "epi_combined", "epi_fenced", "epi_bufok"};
+    for (int r = 0; r < 16; ++r) {
       printf("%-14s", names[r]);
       for (int i = 0; i < 30; ++i) printf(" %6lld", h[r * 64 + i] ? (h[r * 64 + i] - t0) / 100 : -1);
       printf("\n");
@@ -866,7 +1001,14 @@ static int launch(const CUtensorMap& a0, const CUtensorMap& b0, const CUtensorMa
     fflush(stdout);
     return check_launch("gemm_tf32x3");
   }
-  kern<<<grid, kGemmThreads, smem, st>>>(a0, b0, a1, b1, mo, P, tiles_n, splits, total);
+  static const int dbg = [] { const char* e = std::getenv("EGN_GEMM_DBG"); return e ? std::atoi(e) : 0; }();
+  if (dbg) {
+    Params Q = P;
+    Q.dbg = dbg;
+    kern<<<grid, kGemmThreads, smem, st>>>(a0, b0, a1, b1, mo, mop, Q, tiles_n, splits, total);
+    return check_launch("gemm_tf32x3");
+  }
+  kern<<<grid, kGemmThreads, smem, st>>>(a0, b0, a1, b1, mo, mop, P, tiles_n, splits, total);
   return check_launch("gemm_tf32x3");
 }
 
@@ -907,7 +1049,16 @@ __global__ void reduce_splits_kernel(const float* __restrict__ part, int splits,
   }
 }
 
+// Tile width: 128 columns (N = 128 MMAs, one A k-block per 128 x 128 tile, store warp)
+// when N allows and there is at least a wave of such tiles; else 64 (two accumulator
+// groups, more CTAs for small products).
+static int tile_n(int64_t M, int N) { return (N % 128 == 0 && M >= static_cast<int64_t>(kNumSMs) * BM) ? 128 : 64; }
+static int wgrad_tile_n(int64_t krows, int N) {
+  return (N % 128 == 0 && krows >= static_cast<int64_t>(kNumSMs) * 8 * BK) ? 128 : 64;
+}
+
 static void wgrad_split(int64_t krows, int M, int N, int* splits, int* kbps) {
+  const int BN = wgrad_tile_n(krows, N);
   const int tiles = static_cast<int>(((M + BM - 1) / BM) * ((N + BN - 1) / BN));
   const int nk = static_cast<int>((krows + BK - 1) / BK);
   int want = std::max(1, kNumSMs / tiles);      // one wave of CTAs
@@ -944,6 +1095,8 @@ extern "C" int egn_gemm(int64_t M, int N, int nseg, const float* a0, int64_t lda
            ldo2, 0, 0};
   P.flush_steps = (k0 + (nseg > 1 ? k1 : 0)) > 512 ? flush_window(true) : flush_window(false);
   CUtensorMap ma0, mb0, ma1, mb1;
+  const int BN = tile_n(M, N);
+  P.store_warp = BN == 128;
   // A: K-major [M, K]; B: K-major [N, K] (weights (out, in)) or MN-major [K, N] (b_mn)
   if (int rc = make_map(&ma0, a0, M, k0, lda0, BM, kMapK)) return rc;
   if (int rc = b_mn ? make_map(&mb0, b0, k0, N, ldb0, BK, kMapMN) : make_map(&mb0, b0, N, k0, ldb0, BN, kMapK)) return rc;
@@ -955,13 +1108,27 @@ extern "C" int egn_gemm(int64_t M, int N, int nseg, const float* a0, int64_t lda
     mb1 = mb0;
   }
   CUtensorMap mo = ma0;
-  if (out_map_ok(out, ldo) && !(flags & (EPI_SILU_OUT2 | EPI_MUL_AUX))) {
+  static const bool no_tma_out = std::getenv("EGN_GEMM_NO_TMA_OUT") != nullptr;
+  if (!no_tma_out && out_map_ok(out, ldo) && !(flags & (EPI_SILU_OUT2 | EPI_MUL_AUX))) {
     if (int rc = make_out_map(&mo, out, M, N, ldo, 1)) return rc;
     P.tma_out = 1;
   }
+  // residual / aux rows by TMA into the staging buffers (the store warp loads them)
+  CUtensorMap mop = ma0;
+  const float* opnd = (flags & EPI_RESID) ? resid
+                      : ((flags & (EPI_DSILU_AUX | EPI_MUL_AUX)) && !(flags & EPI_GATHER)) ? aux : nullptr;
+  const int64_t ldop = (flags & EPI_RESID) ? ldr : ldaux;
+  if (P.tma_out && P.store_warp && opnd != nullptr && out_map_ok(opnd, ldop)) {
+    if (int rc = make_map(&mop, opnd, M, N, ldop, 32, kMapK)) return rc;
+    P.op_tma = 1;
+  }
   cudaStream_t st = as_stream(stream);
-  if (b_mn) return launch<false, true>(ma0, mb0, ma1, mb1, mo, P, 1, st);
-  return launch<false, false>(ma0, mb0, ma1, mb1, mo, P, 1, st);
+  if (BN == 128) {
+    if (b_mn) return launch<false, true, 128>(ma0, mb0, ma1, mb1, mo, mop, P, 1, st);
+    return launch<false, false, 128>(ma0, mb0, ma1, mb1, mo, mop, P, 1, st);
+  }
+  if (b_mn) return launch<false, true, 64>(ma0, mb0, ma1, mb1, mo, mop, P, 1, st);
+  return launch<false, false, 64>(ma0, mb0, ma1, mb1, mo, mop, P, 1, st);
 }
 
 extern "C" int64_t egn_gemm_wgrad_workspace_bytes(int64_t krows, int M, int N) {
@@ -1000,7 +1167,11 @@ extern "C" int egn_gemm_wgrad(int64_t krows, int M, int N, const float* g, int64
   }
   float* gpart = part + static_cast<int64_t>(splits) * M * N;
   P.gsum_part = g_colsum ? gpart : nullptr;
-  if (int rc = launch<true, true>(ma, mb, ma, mb, mo, P, splits, st)) return rc;
+  const bool wide = wgrad_tile_n(krows, N) == 128;
+  P.store_warp = wide;
+  const int rc = wide ? launch<true, true, 128>(ma, mb, ma, mb, mo, ma, P, splits, st)
+                      : launch<true, true, 64>(ma, mb, ma, mb, mo, ma, P, splits, st);
+  if (rc) return rc;
   const int64_t len = static_cast<int64_t>(M) * N;
   const int mg = g_colsum ? M : 0;
   reduce_splits_kernel<<<static_cast<int>(std::min<int64_t>((len + mg + 31) / 32, 4096)), 256, 0, st>>>(
