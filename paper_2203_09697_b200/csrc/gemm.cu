@@ -296,7 +296,8 @@ template <bool AMN, bool BMN, int BN>
 __global__ void __launch_bounds__(480, 1)
 gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_constant__ CUtensorMap mapB0,
                    const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ CUtensorMap mapB1,
-                   const __grid_constant__ CUtensorMap mapOut, const __grid_constant__ CUtensorMap mapOp, Params P,
+                   const __grid_constant__ CUtensorMap mapOut, const __grid_constant__ CUtensorMap mapOut2,
+                   const __grid_constant__ CUtensorMap mapOp, Params P,
                    int tiles_n, int splits, int total_items) {
   constexpr int A_BYTES = BM * BK * 4;  // 16 KB raw A k-block
   using C = Cfg<BN>;
@@ -336,6 +337,7 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_const
     asm volatile("prefetch.tensormap [%0];" ::"l"(&mapB1) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&mapOut) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&mapOp) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&mapOut2) : "memory");
     for (int s = 0; s < kTmaRing; ++s) {
       mbar_init(&tma_full[s], 1);
       // the multicast leader reuses slot s only after both CTAs' split warps released it
@@ -580,8 +582,10 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_const
       // store read it; operand rows by TMA are loaded by the store warp itself
       const bool sw = P.tma_out && P.store_warp;
       const bool op_async = opkind && !(sw && P.op_tma);
+      // staged outputs per tile (out, out2) = store-warp hand-offs per tile
+      const uint32_t nout = (P.flags & (EPI_SILU_OUT2 | EPI_MUL_AUX)) ? 2u : 1u;
       if (sw) {
-        if (op_async) mbar_wait(&buf_free[gr], (u & 1) ^ 1);
+        if (op_async) mbar_wait(&buf_free[gr], ((u * nout) & 1) ^ 1);
       } else if (lane == 0) {
         asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // own previous store
       }
@@ -637,7 +641,7 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_const
       if (P.tma_out && lane == 0) asm volatile("prefetch.tensormap [%0];" ::"l"(&mapOut) : "memory");
       if (op_async) asm volatile("cp.async.wait_all;" ::: "memory");
       else if (opkind) mbar_wait(&op_bar[gr], u & 1);
-      else if (sw) mbar_wait(&buf_free[gr], (u & 1) ^ 1);
+      else if (sw) mbar_wait(&buf_free[gr], ((u * nout) & 1) ^ 1);
       __syncwarp();
       if (q == 0 && gr == 0 && chalf == 0) EGN_TRACE(8, t);
       // thread = row: combine with the operand in place.  Variant loops are
@@ -649,14 +653,17 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_const
 #define EGN_SLOT(c4) reinterpret_cast<float4*>(ebuf + ((c4) >> 3) * 1024 + epi_idx(lane, ((c4) & 7) * 4))
 #define EGN_ACC4(c4) make_float4(acc[(c4) * 4], acc[(c4) * 4 + 1], acc[(c4) * 4 + 2], acc[(c4) * 4 + 3])
       const bool silu2 = fl & EPI_SILU_OUT2;
-      const bool tma_store = P.tma_out;  // host: never with SILU_OUT2 / MUL_AUX
+      const bool tma_store = P.tma_out;  // two outputs only with the store warp
       if (tma_store && has_bias && variant <= 1) {
-        // bias here (the TMA store has no lane = column pass); broadcast loads
+        // bias here (the TMA store has no lane = column pass); broadcast loads, 16 B
+        // when the bias vector is aligned
+        const bool b16 = (reinterpret_cast<uintptr_t>(P.bias) & 15) == 0;
 #pragma unroll
         for (int c4 = 0; c4 < EW / 4; ++c4) {
           const int col = min(n0 + c4 * 4, P.N - 4);
-          const float4 bv = make_float4(__ldg(P.bias + col), __ldg(P.bias + col + 1), __ldg(P.bias + col + 2),
-                                        __ldg(P.bias + col + 3));
+          const float4 bv = b16 ? __ldg(reinterpret_cast<const float4*>(P.bias + col))
+                                : make_float4(__ldg(P.bias + col), __ldg(P.bias + col + 1), __ldg(P.bias + col + 2),
+                                              __ldg(P.bias + col + 3));
           float4 a = EGN_ACC4(c4);
           if (variant == 1) {
             const float4 o = *EGN_SLOT(c4);
@@ -697,12 +704,39 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_const
         if (lane == 0) {
           if (sw) {
             mbar_arrive(&epi_full[gr]);  // the store warp takes it from here
-          } else {
+          } else {  // (single output only)
             // [split][M][N] output map: rows >= M clip per split
             tma_store_3d(&mapOut, ebuf, n0, static_cast<int>(rbase), z);
             if (n0 + 32 < P.N) tma_store_3d(&mapOut, ebuf + 1024, n0 + 32, static_cast<int>(rbase), z);
             asm volatile("cp.async.bulk.commit_group;" ::: "memory");
           }
+        }
+        if (sw && nout == 2) {
+          // second output through the same staging buffer once the first store read it:
+          // silu(out) in place, or the pre-gate value
+          mbar_wait(&buf_free[gr], (u * 2) & 1);
+          if (silu2) {
+#pragma unroll
+            for (int c4 = 0; c4 < EW / 4; ++c4) {
+              const float4 v = *EGN_SLOT(c4);
+              *EGN_SLOT(c4) = make_float4(__fdividef(v.x, 1.f + __expf(-v.x)), __fdividef(v.y, 1.f + __expf(-v.y)),
+                                          __fdividef(v.z, 1.f + __expf(-v.z)), __fdividef(v.w, 1.f + __expf(-v.w)));
+            }
+          } else {
+#pragma unroll
+            for (int c4 = 0; c4 < EW / 4; ++c4) {
+              float4 a = EGN_ACC4(c4);
+              if (has_bias) {
+                const int col = min(n0 + c4 * 4, P.N - 4);
+                a.x += __ldg(P.bias + col); a.y += __ldg(P.bias + col + 1);
+                a.z += __ldg(P.bias + col + 2); a.w += __ldg(P.bias + col + 3);
+              }
+              *EGN_SLOT(c4) = a;
+            }
+          }
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&epi_full[gr]);
         }
         if (q == 0 && gr == 0 && chalf == 0) EGN_TRACE(9, t);
         continue;
@@ -760,6 +794,7 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_const
     // buffers, then refills them with the operand rows of the group's next tile
     const int opkind = (P.flags & EPI_RESID) ? 1 : ((P.flags & (EPI_DSILU_AUX | EPI_MUL_AUX)) ? 3 : 0);
     const bool op_tma = P.op_tma && opkind && !(P.flags & EPI_GATHER);
+    const uint32_t nout = (P.flags & (EPI_SILU_OUT2 | EPI_MUL_AUX)) ? 2u : 1u;
     constexpr int kWarps = 8 / kGroups;
     // staging buffer (g, w) belongs to epilogue warp 6 + g * kWarps + w: rows of its TMEM
     // lane quarter (warp % 4), columns of its half (one-group layout)
@@ -798,22 +833,25 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_const
     for (int item = blockIdx.x; item < total_items; item += gridDim.x, ++t) {
       const int g = kGroups == 2 ? static_cast<int>(t & 1) : 0;
       const uint32_t u = t / kGroups;
-      mbar_wait(&epi_full[g], u & 1);
-      if (elect_one()) {
-        for (int w = 0; w < kWarps; ++w) {
-          int64_t rb;
-          int nn, z;
-          warp_box(item, g, w, rb, nn, z);
-          const float* eb = epi_all + (g * kWarps + w) * (2 * 32 * 32);
-          // [split][M][N] output map: rows >= M clip per split
-          tma_store_3d(&mapOut, eb, nn, static_cast<int>(rb), z);
-          if (nn + 32 < P.N) tma_store_3d(&mapOut, eb + 1024, nn + 32, static_cast<int>(rb), z);
+      for (uint32_t pass = 0; pass < nout; ++pass) {
+        mbar_wait(&epi_full[g], (u * nout + pass) & 1);
+        const CUtensorMap* mo = pass ? &mapOut2 : &mapOut;
+        if (elect_one()) {
+          for (int w = 0; w < kWarps; ++w) {
+            int64_t rb;
+            int nn, z;
+            warp_box(item, g, w, rb, nn, z);
+            const float* eb = epi_all + (g * kWarps + w) * (2 * 32 * 32);
+            // [split][M][N] output map: rows >= M clip per split
+            tma_store_3d(mo, eb, nn, static_cast<int>(rb), z);
+            if (nn + 32 < P.N) tma_store_3d(mo, eb + 1024, nn + 32, static_cast<int>(rb), z);
+          }
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+          asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+          mbar_arrive(&buf_free[g]);
         }
-        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-        mbar_arrive(&buf_free[g]);
+        __syncwarp();
       }
-      __syncwarp();
       prefetch(item + kGroups * gridDim.x, g);
     }
     if (elect_one()) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
@@ -911,7 +949,8 @@ static bool out_map_ok(const float* out, int64_t ldo) {
 
 template <bool AMN, bool BMN, int BN>
 static int launch(const CUtensorMap& a0, const CUtensorMap& b0, const CUtensorMap& a1, const CUtensorMap& b1,
-                  const CUtensorMap& mo, const CUtensorMap& mop, const Params& P, int splits, cudaStream_t st) {
+                  const CUtensorMap& mo, const CUtensorMap& mo2, const CUtensorMap& mop, const Params& P, int splits,
+                  cudaStream_t st) {
   const size_t smem = Cfg<BN>::kSmem;
   auto kern = gemm_tf32x3_kernel<AMN, BMN, BN>;
   static bool configured = false;
@@ -962,7 +1001,7 @@ static int launch(const CUtensorMap& a0, const CUtensorMap& b0, const CUtensorMa
       cfg.stream = st;
       cfg.attrs = at;
       cfg.numAttrs = 1;
-      cudaLaunchKernelEx(&cfg, kern, a0, b0, a1, b1, mo, mop, Q, tiles_n, splits, total);
+      cudaLaunchKernelEx(&cfg, kern, a0, b0, a1, b1, mo, mo2, mop, Q, tiles_n, splits, total);
       return check_launch("gemm_tf32x3_mc");
     }
   }
@@ -973,7 +1012,7 @@ static int launch(const CUtensorMap& a0, const CUtensorMap& b0, const CUtensorMa
     cudaMemset(d, 0, (1024 + 4 * kNumSMs) * sizeof(long long));
     static_assert(16 * 64 <= 1024, "trace rows");
     Q.trace = d;
-    kern<<<grid, kGemmThreads, smem, st>>>(a0, b0, a1, b1, mo, mop, Q, tiles_n, splits, total);
+    kern<<<grid, kGemmThreads, smem, st>>>(a0, b0, a1, b1, mo, mo2, mop, Q, tiles_n, splits, total);
     long long h[1024 + 4 * kNumSMs];
     cudaStreamSynchronize(st);
     cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
@@ -1005,10 +1044,10 @@ static int launch(const CUtensorMap& a0, const CUtensorMap& b0, const CUtensorMa
   if (dbg) {
     Params Q = P;
     Q.dbg = dbg;
-    kern<<<grid, kGemmThreads, smem, st>>>(a0, b0, a1, b1, mo, mop, Q, tiles_n, splits, total);
+    kern<<<grid, kGemmThreads, smem, st>>>(a0, b0, a1, b1, mo, mo2, mop, Q, tiles_n, splits, total);
     return check_launch("gemm_tf32x3");
   }
-  kern<<<grid, kGemmThreads, smem, st>>>(a0, b0, a1, b1, mo, mop, P, tiles_n, splits, total);
+  kern<<<grid, kGemmThreads, smem, st>>>(a0, b0, a1, b1, mo, mo2, mop, P, tiles_n, splits, total);
   return check_launch("gemm_tf32x3");
 }
 
@@ -1109,8 +1148,14 @@ extern "C" int egn_gemm(int64_t M, int N, int nseg, const float* a0, int64_t lda
   }
   CUtensorMap mo = ma0;
   static const bool no_tma_out = std::getenv("EGN_GEMM_NO_TMA_OUT") != nullptr;
-  if (!no_tma_out && out_map_ok(out, ldo) && !(flags & (EPI_SILU_OUT2 | EPI_MUL_AUX))) {
+  CUtensorMap mo2 = ma0;
+  // two outputs (SiLU / gate) go through TMA only with the store warp (it sequences the
+  // two stores through one staging buffer)
+  const bool two_out = flags & (EPI_SILU_OUT2 | EPI_MUL_AUX);
+  if (!no_tma_out && out_map_ok(out, ldo) && (!two_out || (P.store_warp && out_map_ok(out2, ldo2)))) {
     if (int rc = make_out_map(&mo, out, M, N, ldo, 1)) return rc;
+    if (two_out)
+      if (int rc = make_out_map(&mo2, out2, M, N, ldo2, 1)) return rc;
     P.tma_out = 1;
   }
   // residual / aux rows by TMA into the staging buffers (the store warp loads them)
@@ -1124,11 +1169,11 @@ extern "C" int egn_gemm(int64_t M, int N, int nseg, const float* a0, int64_t lda
   }
   cudaStream_t st = as_stream(stream);
   if (BN == 128) {
-    if (b_mn) return launch<false, true, 128>(ma0, mb0, ma1, mb1, mo, mop, P, 1, st);
-    return launch<false, false, 128>(ma0, mb0, ma1, mb1, mo, mop, P, 1, st);
+    if (b_mn) return launch<false, true, 128>(ma0, mb0, ma1, mb1, mo, mo2, mop, P, 1, st);
+    return launch<false, false, 128>(ma0, mb0, ma1, mb1, mo, mo2, mop, P, 1, st);
   }
-  if (b_mn) return launch<false, true, 64>(ma0, mb0, ma1, mb1, mo, mop, P, 1, st);
-  return launch<false, false, 64>(ma0, mb0, ma1, mb1, mo, mop, P, 1, st);
+  if (b_mn) return launch<false, true, 64>(ma0, mb0, ma1, mb1, mo, mo2, mop, P, 1, st);
+  return launch<false, false, 64>(ma0, mb0, ma1, mb1, mo, mo2, mop, P, 1, st);
 }
 
 extern "C" int64_t egn_gemm_wgrad_workspace_bytes(int64_t krows, int M, int N) {
@@ -1169,8 +1214,8 @@ extern "C" int egn_gemm_wgrad(int64_t krows, int M, int N, const float* g, int64
   P.gsum_part = g_colsum ? gpart : nullptr;
   const bool wide = wgrad_tile_n(krows, N) == 128;
   P.store_warp = wide;
-  const int rc = wide ? launch<true, true, 128>(ma, mb, ma, mb, mo, ma, P, splits, st)
-                      : launch<true, true, 64>(ma, mb, ma, mb, mo, ma, P, splits, st);
+  const int rc = wide ? launch<true, true, 128>(ma, mb, ma, mb, mo, ma, ma, P, splits, st)
+                      : launch<true, true, 64>(ma, mb, ma, mb, mo, ma, ma, P, splits, st);
   if (rc) return rc;
   const int64_t len = static_cast<int64_t>(M) * N;
   const int mg = g_colsum ? M : 0;

@@ -25,7 +25,9 @@ for _ in range(3):
     ops.gemm(a, w, b_mn=True)
 torch.cuda.synchronize()
 os.environ["EGN_GEMM_TRACE"] = "1"
-for name, fn in (("dgrad (no operand)", lambda: ops.gemm(a, w, b_mn=True)),
+bias = torch.randn((128,), device="cuda")
+for name, fn in (("silu2 bias", lambda: ops.gemm(a, w, bias=bias, flags=ops.EPI_SILU_OUT2)),
+                 ("dgrad (no operand)", lambda: ops.gemm(a, w, b_mn=True)),
                  ("fwd resid", lambda: ops.gemm(a, w, resid=r)),
                  ("wgrad", lambda: ops.gemm_wgrad(g, a))):
     print("==", name, flush=True)
