@@ -448,6 +448,45 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_const
         const uint32_t bhi = smem_u32(opring + o * kOpSlot);
         const uint32_t blo = bhi + B_BYTES;
         const uint32_t ta = tmem + A_TMEM + o * 64;
+        if (win % (BK / 8) == 0) {
+          // windows of whole k-blocks: the 8 small products (lo x hi, hi x lo) of the
+          // k-block go first into the window tile, the 4 big ones last, so only the big
+          // terms accumulate at full magnitude (fewer truncations at large |acc|)
+          const bool fstart = wpos == 0;
+          if (fstart) {
+            bsel = fc % kAccBufs;
+            mbar_wait(&acce_bar[gr][bsel], ((fc / kAccBufs) & 1) ^ 1);
+            EGN_TRACE(12, wtr);
+            ++wtr;
+            asm volatile("tcgen05.fence::after_thread_sync;");
+            tacc = tg + bsel * BN;
+          }
+          j += BK / 8;
+          wpos += BK / 8;
+          const bool fend = (wpos == win) || (j == nsteps);
+          if (elect_one() && !(P.dbg & 1)) {
+#pragma unroll
+            for (int k = 0; k < BK / 8; ++k) {
+              const uint32_t ob = BMN ? k * 1024 : k * 32;
+              const uint64_t dbh = BMN ? sw128_mnmajor_desc_u(bhi + ob) : sw128_kmajor_desc_u(bhi + ob);
+              const uint64_t dbl = BMN ? sw128_mnmajor_desc_u(blo + ob) : sw128_kmajor_desc_u(blo + ob);
+              mma_tf32_ta(tacc, ta + 32 + k * 8, dbh, idesc, (fstart && k == 0) ? 0u : 1u);
+              mma_tf32_ta(tacc, ta + k * 8, dbl, idesc, 1u);
+            }
+#pragma unroll
+            for (int k = 0; k < BK / 8; ++k) {
+              const uint32_t ob = BMN ? k * 1024 : k * 32;
+              const uint64_t dbh = BMN ? sw128_mnmajor_desc_u(bhi + ob) : sw128_kmajor_desc_u(bhi + ob);
+              mma_tf32_ta(tacc, ta + k * 8, dbh, idesc, 1u);
+            }
+          }
+          if (fend && elect_one()) mma_commit(&accf_bar[gr][bsel]);
+          __syncwarp();
+          if (fend) {
+            ++fc;
+            wpos = 0;
+          }
+        } else
 #pragma unroll
         for (int k = 0; k < BK / 8; ++k) {
           const bool fstart = wpos == 0;
@@ -1106,12 +1145,12 @@ static void wgrad_split(int64_t krows, int M, int N, int* splits, int* kbps) {
   *splits = (nk + *kbps - 1) / *kbps;
 }
 
-// k-steps per TMEM->register flush: long-K products (weight gradients over edge
-// rows) flush every few steps, short-K products once per tile.  EGN_GEMM_FLUSH /
-// EGN_GEMM_FLUSH_SHORT override for precision experiments.
+// k-steps (of 8) per TMEM->register flush: one k-block (small products first, see the
+// MMA issuer).  EGN_GEMM_FLUSH (long K) / EGN_GEMM_FLUSH_SHORT override for precision
+// experiments (values that are not multiples of 4 use the per-k8 interleaved order).
 static int flush_window(bool long_k) {
   static const int lw = [] { const char* e = std::getenv("EGN_GEMM_FLUSH"); return e ? std::atoi(e) : 4; }();
-  static const int sw = [] { const char* e = std::getenv("EGN_GEMM_FLUSH_SHORT"); return e ? std::atoi(e) : 2; }();
+  static const int sw = [] { const char* e = std::getenv("EGN_GEMM_FLUSH_SHORT"); return e ? std::atoi(e) : 4; }();
   return long_k ? lw : sw;
 }
 
