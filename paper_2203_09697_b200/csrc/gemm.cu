@@ -1140,7 +1140,7 @@ static void wgrad_split(int64_t krows, int M, int N, int* splits, int* kbps) {
   const int tiles = static_cast<int>(((M + BM - 1) / BM) * ((N + BN - 1) / BN));
   const int nk = static_cast<int>((krows + BK - 1) / BK);
   int want = std::max(1, kNumSMs / tiles);      // one wave of CTAs
-  want = std::min(want, std::max(1, nk / 8));   // >= 8 k-blocks per CTA
+  want = std::min(want, std::max(1, nk / 4));   // >= 4 k-blocks per CTA
   *kbps = (nk + want - 1) / want;
   *splits = (nk + *kbps - 1) / *kbps;
 }
