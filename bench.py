@@ -233,7 +233,13 @@ def _time_kernel(fn, iters, flush):
 
 
 def _kernel_roofline(tr, bg, cfg):
-    """Triplet-interaction kernels on block-0 operands, L2 flushed between launches."""
+    """Roofline of the dominant kernel, measured live with the L2 flushed between launches.
+
+    The dominant kernel by share of the step is the tcgen05 GEMM (~55% of
+    the step over 128 calls); its representative launch is the E x 128 x 128 product with a
+    residual epilogue (the most frequent wide shape).  Algorithmic bytes = A + W + residual
+    read once + output written once.  The triplet-interaction kernels (SURVEY.md 8(d)
+    bytes per triplet / edge) are reported alongside under "triplet"."""
     import torch
 
     from paper_2203_09697_b200 import ops
@@ -256,25 +262,37 @@ def _kernel_roofline(tr, bg, cfg):
     peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
     hbm = peaks.get("hbm_gbs", 6650.0)
     fma = 2.0 * nt * cfg.l_sbf * dg
-    dominant = "triplet_bwd" if t_b >= t_f else "triplet_fwd"
-    ach = (b_bwd / t_b if dominant == "triplet_bwd" else b_fwd / t_f) / 1e9
-    # DRAM traffic of the same kernel from the committed ncu capture (same workload only)
+    fp32_peak = 148 * 128 * 2 * 1.965e9  # FFMA pipe
+    # dominant kernel: the E x d_e x d_e GEMM with residual epilogue
+    de = cfg.d_e
+    g = torch.Generator(device="cuda").manual_seed(0)
+    A = torch.randn((ne, de), device="cuda", generator=g)
+    W = torch.randn((de, de), device="cuda", generator=g) * de ** -0.5
+    R = torch.randn((ne, de), device="cuda", generator=g)
+    t_g = _time_kernel(lambda: ops.gemm(A, W, resid=R), 20, flush)
+    b_gemm = 4 * (3 * ne * de + de * de)
+    ach = b_gemm / t_g / 1e9
     traffic = None
     tpath = ROOT / "profiles" / "r1_traffic.json"
+    key = f"gemm_fwd_resid_{de}"
     if tpath.exists():
         tj = json.loads(tpath.read_text())
-        if tj.get("workload", {}).get("edges") == ne and tj.get("workload", {}).get("triplets") == nt:
-            rec = tj.get(dominant, {})
-            traffic = rec.get("dram_read", 0) + rec.get("dram_write", 0) or None
-    fp32_peak = 148 * 128 * 2 * 1.965e9  # FFMA pipe: the bound of this formulation
-    return {"bound": "hbm", "kernel": dominant, "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
-            "traffic": traffic, "traffic_source": "profiles/r1_traffic.json (ncu --set full)" if traffic else None,
-            "fp32_pipe_frac": (2 * fma / t_b if dominant == "triplet_bwd" else fma / t_f) / fp32_peak,
+        if tj.get("workload", {}).get("edges") == ne:
+            rec = tj.get(key, {})
+            traffic = (rec.get("dram_read", 0) + rec.get("dram_write", 0)) or None
+    tf32_peak = peaks.get("bf16_tflops", 1640.8) / 2  # TF32 = half the bf16 tensor rate
+    return {"bound": "hbm", "kernel": f"gemm_tf32x3 E x {de} x {de} (+residual), 3xTF32 on tcgen05",
+            "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
+            "traffic": traffic, "traffic_source": f"profiles/r1_traffic.json:{key} (ncu --set full)" if traffic else None,
             "peak_source": "MEASURED_PEAKS.json" if peaks else "fallback",
-            "triplet_fwd_us": t_f * 1e6, "triplet_bwd_us": t_b * 1e6,
-            "triplet_fwd_gtrip_s": nt / t_f / 1e9, "triplet_bwd_gtrip_s": nt / t_b / 1e9,
-            "triplet_fwd_fp32_tflops": fma / t_f / 1e12, "triplet_bwd_fp32_tflops": 2 * fma / t_b / 1e12,
-            "algorithmic_bytes": {"fwd": b_fwd, "bwd": b_bwd}}
+            "launch_us": t_g * 1e6, "algorithmic_bytes": b_gemm,
+            "tensor_frac": 3 * 2.0 * ne * de * de / t_g / 1e12 / tf32_peak,
+            "triplet": {"fwd_us": t_f * 1e6, "bwd_us": t_b * 1e6,
+                        "fwd_gbs": b_fwd / t_f / 1e9, "bwd_gbs": b_bwd / t_b / 1e9,
+                        "fwd_hbm_frac": b_fwd / t_f / 1e9 / hbm, "bwd_hbm_frac": b_bwd / t_b / 1e9 / hbm,
+                        "fwd_gtrip_s": nt / t_f / 1e9, "bwd_gtrip_s": nt / t_b / 1e9,
+                        "fwd_fp32_pipe_frac": fma / t_f / fp32_peak, "bwd_fp32_pipe_frac": 2 * fma / t_b / fp32_peak,
+                        "algorithmic_bytes": {"fwd": b_fwd, "bwd": b_bwd}}}
 
 
 def run_ours(args, wl):

@@ -5,8 +5,9 @@ python bench.py > gpurun_out/bench_full.json 2> gpurun_out/bench_full.err
 python bench.py --impl reference > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
 python tools/profile_step.py --plain --steps 1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv --log-file gpurun_out/r1_launches.csv python tools/profile_step.py --plain --steps 1 > gpurun_out/ncu_launch.log 2>&1
-ncu --set full --import-source on --clock-control none -k regex:gemm_tf32x3 -s 60 -c 1 -o gpurun_out/r1_gemm python tools/profile_step.py --plain --steps 1 > gpurun_out/ncu1.log 2>&1
-ncu --set full --import-source on --clock-control none --kernel-name-base demangled -k "regex:gemm_tf32x3_kernel<false, false>" -s 20 -c 1 -o gpurun_out/r1_gemm_fwd python tools/profile_step.py --plain --steps 1 > gpurun_out/ncu1b.log 2>&1
+# the roofline GEMM launch (E x 128 x 128 + residual) alone, then one wgrad
+ncu --set full --import-source on --clock-control none -k regex:gemm_tf32x3 -s 3 -c 1 -o gpurun_out/r1_gemm python tools/gemm_one_shape.py --reps 1 > gpurun_out/ncu1.log 2>&1
+ncu --set full --import-source on --clock-control none -k regex:gemm_tf32x3 -s 3 -c 1 -o gpurun_out/r1_gemm_wgrad python tools/gemm_one_shape.py --kind wgrad --reps 1 > gpurun_out/ncu1b.log 2>&1
 ncu --set full --import-source on --clock-control none -k regex:fwd_kernel -s 4 -c 1 -o gpurun_out/r1_tfwd python tools/profile_step.py --plain --steps 1 > gpurun_out/ncu2.log 2>&1
 ncu --set full --import-source on --clock-control none -k regex:bw1_kernel -s 4 -c 1 -o gpurun_out/r1_tbw1 python tools/profile_step.py --plain --steps 1 > gpurun_out/ncu3.log 2>&1
 ncu --set full --import-source on --clock-control none -k regex:bw2_kernel -s 4 -c 1 -o gpurun_out/r1_tbw2 python tools/profile_step.py --plain --steps 1 > gpurun_out/ncu4.log 2>&1
