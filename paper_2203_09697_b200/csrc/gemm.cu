@@ -1174,7 +1174,10 @@ extern "C" int egn_gemm(int64_t M, int N, int nseg, const float* a0, int64_t lda
   P.flush_steps = (k0 + (nseg > 1 ? k1 : 0)) > 512 ? flush_window(true) : flush_window(false);
   CUtensorMap ma0, mb0, ma1, mb1;
   const int BN = tile_n(M, N);
-  P.store_warp = BN == 128;
+  // store warp for every tile width (EGN_GEMM_SW64=0 keeps the BN = 64 accumulator groups
+  // issuing their own stores, for comparison)
+  static const bool sw64 = [] { const char* e = std::getenv("EGN_GEMM_SW64"); return !(e && e[0] == '0'); }();
+  P.store_warp = BN == 128 || sw64;
   // A: K-major [M, K]; B: K-major [N, K] (weights (out, in)) or MN-major [K, N] (b_mn)
   if (int rc = make_map(&ma0, a0, M, k0, lda0, BM, kMapK)) return rc;
   if (int rc = b_mn ? make_map(&mb0, b0, k0, N, ldb0, BK, kMapMN) : make_map(&mb0, b0, N, k0, ldb0, BN, kMapK)) return rc;
@@ -1252,7 +1255,7 @@ extern "C" int egn_gemm_wgrad(int64_t krows, int M, int N, const float* g, int64
   float* gpart = part + static_cast<int64_t>(splits) * M * N;
   P.gsum_part = g_colsum ? gpart : nullptr;
   const bool wide = wgrad_tile_n(krows, N) == 128;
-  P.store_warp = wide;
+  P.store_warp = 1;
   const int rc = wide ? launch<true, true, 128>(ma, mb, ma, mb, mo, ma, ma, P, splits, st)
                       : launch<true, true, 64>(ma, mb, ma, mb, mo, ma, ma, P, splits, st);
   if (rc) return rc;
