@@ -595,7 +595,7 @@ def backward(fw: Forward, P: dict, d_energy: float = 1.0, d_forces: np.ndarray |
 
 
 # ---------------------------------------------------------------------------
-# drivers (tasks.py:37-67, 131-209)
+# drivers (tasks.py:37-67, 79-128, 131-209)
 # ---------------------------------------------------------------------------
 
 
@@ -606,6 +606,44 @@ def predict(c: Config, P: dict, pos, z):
         return fw.energy, fw.forces
     _, d_pos = backward(fw, P, d_energy=1.0)
     return fw.energy, -d_pos
+
+
+def relax(c: Config, P: dict, pos, z, fmax_threshold: float, max_steps: int = 200, step_size: float = 0.05):
+    """Steepest-descent relaxation x <- x + eta F with the energy guard of energy-centric
+    models (reject and halve eta when the energy rises); tasks.py:79-128.  Returns
+    (trajectory, max_forces, energies, converged, steps)."""
+    if fmax_threshold <= 0:
+        raise ValueError("fmax_threshold must be positive")
+    if max_steps < 0:
+        raise ValueError("max_steps must be >= 0")
+    guard = c.variant == DIMENET  # energy_centric (config.py:46-47); the diagnostic model is not restated
+    eta = step_size
+    x = np.array(pos, dtype=np.float64)
+    trajectory = [x.copy()]
+    energies, max_forces = [], []
+    steps, converged = 0, False
+    energy, forces = predict(c, P, x, z)
+    while True:
+        if not (np.isfinite(energy) and np.all(np.isfinite(forces))):
+            raise RuntimeError(f"non-finite prediction at step {steps}")
+        fmax = float(np.sqrt((forces * forces).sum(axis=1)).max())
+        energies.append(energy)
+        max_forces.append(fmax)
+        if fmax < fmax_threshold:
+            converged = True
+            break
+        if steps >= max_steps:
+            break
+        proposal = x + eta * forces
+        steps += 1
+        new_energy, new_forces = predict(c, P, proposal, z)
+        if guard and new_energy > energy:
+            eta *= 0.5
+        else:
+            x = proposal
+            energy, forces = new_energy, new_forces
+        trajectory.append(x.copy())
+    return trajectory, max_forces, energies, converged, steps
 
 
 def loss_and_grads(c: Config, P: dict, dataset, w_energy=1.0, w_forces=0.0):

@@ -16,7 +16,7 @@ __all__ = [
     "DIMENET", "GEMNET", "ModelConfig", "ModelParams", "ParamSpec", "init_params", "load_params",
     "param_specs", "save_params", "zero_params", "CenterPartition", "CommModel", "CommVolume",
     "GraphPartition", "comm_volume", "partition_centers", "partition_graph", "split_range",
-    "AtomicSystem", "random_cloud", "build_graph", "build_batch", "EGNModel", "predict",
+    "AtomicSystem", "random_cloud", "build_graph", "build_batch", "EGNModel", "predict", "relax", "RelaxationResult",
     "loss_and_grads", "train_simple", "Trainer", "enumerate_triplets", "WorkerGroup", "ParallelRunResult",
     "GradientBundle", "CollectiveShapeError", "CollectiveTimeoutError", "WorkerGroupError",
 ]
@@ -31,7 +31,7 @@ def __getattr__(name):
     if name in ("EGNModel",):
         from .model import EGNModel
         return EGNModel
-    if name in ("predict", "loss_and_grads", "train_simple", "Trainer"):
+    if name in ("predict", "relax", "RelaxationResult", "loss_and_grads", "train_simple", "Trainer"):
         from . import tasks
         return getattr(tasks, name)
     if name in ("WorkerGroup", "ParallelRunResult", "GradientBundle", "CollectiveError", "CollectiveShapeError",

@@ -1,7 +1,7 @@
-"""Model-level drivers on the GPU: predict, loss_and_grads, train_simple.
+"""Model-level drivers on the GPU: predict, relax, loss_and_grads, train_simple.
 
-Same signatures and semantics as egn/tasks.py:37-67 (predict), :131-185
-(loss_and_grads) and :188-209 (train_simple); the per-sample loop of the
+Same signatures and semantics as egn/tasks.py:37-67 (predict), :79-128 (relax),
+:131-185 (loss_and_grads) and :188-209 (train_simple); the per-sample loop of the
 reference becomes one batched forward/backward over the disjoint union of
 all samples (per-graph energies and per-graph global state are kept
 separate, so the result equals the per-graph loop).  ``Trainer`` is the
@@ -10,6 +10,8 @@ weights stay in HBM between steps.
 """
 
 from __future__ import annotations
+
+from dataclasses import dataclass
 
 import numpy as np
 import torch
@@ -40,6 +42,88 @@ def predict(system, params: ModelParams, workers: int | None = None, device="cud
         return float(fw.energy[0]), fw.forces.double().cpu().numpy()
     pos_bar = eng.backward(bg, fw, torch.ones(1, device=bg.device))
     return float(fw.energy[0]), (-pos_bar).cpu().numpy()
+
+
+@dataclass
+class RelaxationResult:
+    """egn/tasks.py:70-76."""
+
+    trajectory: list  # positions after each iteration; entry 0 is the input
+    max_forces: list
+    energies: list
+    converged: bool
+    steps: int
+
+
+class _DeviceEvaluator:
+    """Energy, forces and max |F| of one system at device positions: graph rebuilt on the
+    GPU at every evaluation (neighbour list, triplets, geometry), weights resident."""
+
+    def __init__(self, params: ModelParams, n_atoms: int, device="cuda"):
+        self.config = params.config
+        self.engine = Engine(DeviceWeights.from_params(params, device))
+        self.sizes = [int(n_atoms)]
+
+    def __call__(self, pos: torch.Tensor):
+        c = self.config
+        bg = build_batch(None, c.cutoff, positions=pos, sizes=self.sizes)
+        fw = self.engine.forward(bg)
+        if c.variant == GEMNET:
+            forces = fw.forces.double()
+        else:
+            forces = -self.engine.backward(bg, fw, torch.ones(1, device=bg.device))
+        energy = fw.energy[0].double()
+        fmax = torch.sqrt((forces * forces).sum(dim=1)).max() if forces.shape[0] else forces.new_zeros(())
+        finite = torch.isfinite(energy) & torch.isfinite(forces).all()
+        # one small device->host read per evaluation: the loop branches on it
+        e, f, ok = torch.stack([energy, fmax, finite.double()]).cpu().tolist()
+        return e, forces, f, bool(ok)
+
+
+def relax(system, params: ModelParams, fmax_threshold: float, max_steps: int = 200, step_size: float = 0.05,
+          workers: int | None = None, device="cuda") -> RelaxationResult:
+    """Iterate x <- x + eta * F until max |F| < fmax_threshold or max_steps
+    (egn/tasks.py:79-128).  Energy-centric models reject a step that raises the energy
+    and halve eta, so the energy sequence is non-increasing.  Positions stay on the
+    device; the neighbour graph is rebuilt on the GPU at every evaluation."""
+    if fmax_threshold <= 0:
+        raise ValueError("fmax_threshold must be positive")
+    if max_steps < 0:
+        raise ValueError("max_steps must be >= 0")
+    config = params.config
+    _check_workers(config, workers)
+    if config.diagnostic:
+        raise ValueError("the diagnostic quadratic-well model is a test fixture, not part of this path")
+    guard = config.energy_centric
+    eta = float(step_size)
+    x = torch.as_tensor(np.asarray(system.positions, dtype=np.float64), device=device).clone()
+    evaluate = _DeviceEvaluator(params, x.shape[0], device)
+    trajectory = [x.cpu().numpy().copy()]
+    energies: list[float] = []
+    max_forces: list[float] = []
+    steps = 0
+    converged = False
+    energy, forces, fmax, ok = evaluate(x)
+    while True:
+        if not ok:
+            raise RuntimeError(f"non-finite prediction at step {steps}")
+        energies.append(energy)
+        max_forces.append(fmax)
+        if fmax < fmax_threshold:
+            converged = True
+            break
+        if steps >= max_steps:
+            break
+        proposal = x + eta * forces
+        steps += 1
+        new_energy, new_forces, new_fmax, new_ok = evaluate(proposal)
+        if guard and new_energy > energy:
+            eta *= 0.5
+        else:
+            x = proposal
+            energy, forces, fmax, ok = new_energy, new_forces, new_fmax, new_ok
+        trajectory.append(x.cpu().numpy().copy())
+    return RelaxationResult(trajectory, max_forces, energies, converged, steps)
 
 
 def _seeds(energy, forces, e_target, f_target, atom_count, w_energy, w_forces, n):

@@ -1,6 +1,6 @@
 """Generate golden fixtures by running the REFERENCE package (egn) in this container.
 
-    PYTHONPATH=/root/reference/pkg/src python tests/golden/make_golden.py
+    PYTHONPATH=/root/reference/pkg/src python tests/golden/make_golden.py [graphs models training relax]
 
 The reference is not available on the GPU box, so its outputs are frozen
 here as small .npz files.  Inputs (positions) are stored explicitly;
@@ -22,7 +22,7 @@ sys.path.insert(0, REF)
 
 from egn import ModelConfig, ModelTape, build_graph, init_params  # noqa: E402
 from egn.system import AtomicSystem, random_cloud  # noqa: E402
-from egn.tasks import loss_and_grads, train_simple  # noqa: E402
+from egn.tasks import loss_and_grads, relax, train_simple  # noqa: E402
 
 OUT = Path(__file__).resolve().parent
 
@@ -171,10 +171,40 @@ def make_training():
         print("train", variant, loss, hist)
 
 
+RELAX_CASES = {
+    # name: (config kwargs, (n atoms, density, seed), fmax_threshold, max_steps, step_size)
+    "dimenet": (dict(variant="dimenet-style", blocks=2, seed=7), (10, 0.9, 60), 1e-3, 8, 1.0),
+    "gemnet": (dict(variant="gemnet-style", blocks=2, seed=8), (10, 0.9, 61), 1e-3, 6, 0.05),
+}
+
+
+def make_relax():
+    """relax() trajectories (tasks.py:79-128): graph rebuilt per evaluation, energy guard
+    with step halving for the energy-centric variant."""
+    for name, (kw, (n, rho, seed), fmax, steps, eta) in RELAX_CASES.items():
+        cfg = ModelConfig(**kw)
+        params = init_params(cfg)
+        system = random_cloud(n, rho, np.random.default_rng(seed))
+        res = relax(system, params, fmax_threshold=fmax, max_steps=steps, step_size=eta)
+        out = {"config": np.array(cfg.to_json()), "pos": system.positions, "z": system.atomic_numbers,
+               "fmax_threshold": np.array(fmax), "max_steps": np.array(steps), "step_size": np.array(eta),
+               "trajectory": np.stack(res.trajectory), "energies": np.array(res.energies),
+               "max_forces": np.array(res.max_forces), "converged": np.array(res.converged),
+               "steps": np.array(res.steps), "numpy_version": np.array(np.__version__)}
+        np.savez_compressed(OUT / f"relax_{name}.npz", **out)
+        print(f"relax_{name}.npz steps", res.steps, "converged", res.converged, "energies", res.energies)
+
+
 if __name__ == "__main__":
-    make_graphs()
-    make_models()
-    make_training()
+    parts = sys.argv[1:] or ["graphs", "models", "training", "relax"]
+    if "graphs" in parts:
+        make_graphs()
+    if "models" in parts:
+        make_models()
+    if "training" in parts:
+        make_training()
+    if "relax" in parts:
+        make_relax()
     (OUT / "README.md").write_text(
         "Golden fixtures produced by `make_golden.py` from the reference package egn "
         "(/root/reference/pkg/src) with numpy " + np.__version__ + ".\n"

@@ -95,6 +95,28 @@ def test_loss_and_grads_matches_reference(variant):
     np.testing.assert_allclose(hist, gd["history"], rtol=1e-9)
 
 
+@pytest.mark.parametrize("variant", ["dimenet", "gemnet"])
+def test_relax_matches_reference(variant):
+    """relax (tasks.py:79-128): graph rebuilt per evaluation; the dimenet case rejects
+    five proposals (energy guard, eta halved), the gemnet case has no guard."""
+    gd = load_golden(f"relax_{variant}.npz")
+    cfg = _cfg(gd["config"])
+    P = O.init_params(cfg)
+    traj, fmax, energies, converged, steps = O.relax(cfg, P, gd["pos"], gd["z"], float(gd["fmax_threshold"]),
+                                                     int(gd["max_steps"]), float(gd["step_size"]))
+    assert steps == int(gd["steps"]) and converged == bool(gd["converged"])
+    assert max_rel(np.stack(traj), gd["trajectory"]) < 1e-10
+    assert max_rel(np.array(energies), gd["energies"]) < 1e-10
+    assert max_rel(np.array(fmax), gd["max_forces"]) < 1e-10
+    if variant == "dimenet":
+        assert np.sum(np.diff(energies) == 0) == 5
+        assert np.all(np.diff(energies) <= 0)
+    with pytest.raises(ValueError):
+        O.relax(cfg, P, gd["pos"], gd["z"], 0.0)
+    with pytest.raises(ValueError):
+        O.relax(cfg, P, gd["pos"], gd["z"], 1e-3, max_steps=-1)
+
+
 def test_oracle_fd_gradient_spot_check():
     """Independent of the fixtures: central differences of the oracle energy."""
     cfg = O.Config(variant=O.DIMENET, blocks=1)
