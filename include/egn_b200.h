@@ -81,6 +81,42 @@ int egn_triplet_angles(const double* pos, const int64_t* edge_ptr, const int32_t
                        egn_stream_t stream);
 
 /* ------------------------------------------------------------------ */
+/* Periodic cells (no counterpart in the reference,  */
+/* which is non-periodic: parity is pinned by an explicit supercell     */
+/* expansion through the reference build_graph, tests/golden/pbc.npz)   */
+/* ------------------------------------------------------------------ */
+/*
+ * Per graph g: cell[9g..9g+8] = lattice vectors c0, c1, c2 (rows, fp64) and
+ * nimg[3g..3g+2] = (na, nb, nc) images per axis (0 on a non-periodic axis).
+ * Image index img = ((i+na)(2nb+1) + (j+nb))(2nc+1) + (k+nc) for i in [-na, na] ...;
+ * shift s = (i c0 + j c1) + k c2 per component (fp64, round-to-nearest, no FMA).
+ * An edge (a, b, img) has the vector (x_b + s) - x_a and exists iff
+ * 0 < |v| <= cutoff (and not (b == a, s == 0)); each row is ordered by (b, img),
+ * so a row is sorted by (recv, img) and the reverse of (a, b, img) is
+ * (b, a, n_img - 1 - img).  Degrees/counts/triplets then follow the
+ * non-periodic CSR conventions above (triplet exclusion is by edge: the
+ * in-edge is never the reverse of the out-edge).
+ */
+int egn_neighbors_count_pbc(const double* pos, const int64_t* graph_ptr, const int32_t* node_graph,
+                            int64_t num_nodes, const double* cell, const int32_t* nimg, double cutoff, int32_t* deg,
+                            egn_stream_t stream);
+/* src/recv/img [E] and shift [E,3] (fp64) of every periodic edge, rows ordered by (recv, img). */
+int egn_neighbors_fill_pbc(const double* pos, const int64_t* graph_ptr, const int32_t* node_graph,
+                           int64_t num_nodes, const double* cell, const int32_t* nimg, double cutoff,
+                           const int64_t* edge_ptr, int32_t* src, int32_t* recv, int32_t* img, double* shift,
+                           egn_stream_t stream);
+/* rev[e] = index of (recv_e, src_e, mirrored image); *missing counts edges without one. */
+int egn_reverse_edges_pbc(const int64_t* edge_ptr, const int32_t* src, const int32_t* recv, const int32_t* img,
+                          const int32_t* node_graph, const int32_t* nimg, int64_t num_edges, int32_t* rev,
+                          int32_t* missing, egn_stream_t stream);
+/* egn_geometry / egn_triplet_angles on edge vectors (x_recv + shift) - x_src; shift NULL
+ * gives the non-periodic results bit for bit. */
+int egn_geometry_shift(const double* pos, const int32_t* src, const int32_t* recv, const double* shift,
+                       int64_t num_edges, float* geo, double* dist64, double* unit64, egn_stream_t stream);
+int egn_triplet_angles_shift(const double* pos, const int64_t* edge_ptr, const int32_t* recv, const double* shift,
+                             const int64_t* tri_ptr, int64_t num_nodes, double* angles, egn_stream_t stream);
+
+/* ------------------------------------------------------------------ */
 /* Basis: rbf_features / rbf_features_ddist (basis.py:35-51)           */
 /* ------------------------------------------------------------------ */
 

@@ -161,6 +161,10 @@ class Graph:
     units: np.ndarray
     angles: np.ndarray
     rev: np.ndarray = field(default=None)
+    # periodic graphs: edge vectors (x_recv + shift) - x_src and the
+    # image index per edge; None for the reference's non-periodic graphs
+    vec: np.ndarray = field(default=None)
+    img: np.ndarray = field(default=None)
 
 
 def neighbor_list(pos: np.ndarray, cutoff: float):
@@ -209,31 +213,34 @@ def reverse_edges(src: np.ndarray, recv: np.ndarray) -> np.ndarray:
     return rev
 
 
-def triplet_vectors(pos, src, recv, trip_in, trip_out):
-    """graph.py:153-159."""
+def triplet_vectors(pos, src, recv, trip_in, trip_out, vec=None, rev=None):
+    """graph.py:153-159.  Periodic graphs: v1 = vector of the out-edge j -> k' (the reverse of
+    the in-edge), v2 = vector of the out-edge j -> i', i.e. the images the edges connect."""
     k = src[trip_in]
     j = recv[trip_in]
     i = recv[trip_out]
+    if vec is not None:
+        return k, j, i, vec[rev[trip_in]], vec[trip_out]
     return k, j, i, pos[k] - pos[j], pos[i] - pos[j]
 
 
-def triplet_angles(pos, src, recv, trip_in, trip_out):
+def triplet_angles(pos, src, recv, trip_in, trip_out, vec=None, rev=None):
     """atan2(|v1 x v2|, v1.v2); graph.py:162-170."""
     if trip_in.size == 0:
         return np.empty(0, dtype=np.float64)
-    _, _, _, v1, v2 = triplet_vectors(pos, src, recv, trip_in, trip_out)
+    _, _, _, v1, v2 = triplet_vectors(pos, src, recv, trip_in, trip_out, vec, rev)
     cross = np.cross(v1, v2)
     s = np.sqrt((cross * cross).sum(axis=1))
     c = (v1 * v2).sum(axis=1)
     return np.arctan2(s, c)
 
 
-def angle_gradients(pos, src, recv, trip_in, trip_out):
+def angle_gradients(pos, src, recv, trip_in, trip_out, vec=None, rev=None):
     """Closed-form d(angle)/d(x_k, x_j, x_i), zero subgradient when collinear; graph.py:173-197."""
     if trip_in.size == 0:
         z = np.zeros((0, 3))
         return z, z, z
-    _, _, _, v1, v2 = triplet_vectors(pos, src, recv, trip_in, trip_out)
+    _, _, _, v1, v2 = triplet_vectors(pos, src, recv, trip_in, trip_out, vec, rev)
     cross = np.cross(v1, v2)
     s = np.sqrt((cross * cross).sum(axis=1))
     ok = s > COLLINEAR_EPS
@@ -262,6 +269,88 @@ def build_graph(pos: np.ndarray, cutoff: float) -> Graph:
     angles = triplet_angles(pos, src, recv, trip_in, trip_out)
     rev = reverse_edges(src, recv)
     return Graph(n, src, recv, trip_in, trip_out, dist, units, angles, rev)
+
+
+# ---------------------------------------------------------------------------
+# periodic cells (no reference counterpart -- pinned against the
+# reference build_graph on an explicit supercell, tests/golden/pbc.npz)
+# ---------------------------------------------------------------------------
+
+
+def image_ranges(cell, pbc, cutoff, pos=None):
+    """Images per periodic axis: max(ceil(r), floor(r + span)), r = cutoff / h_a with
+    h_a = |det C| / |c_b x c_c| and span the extent of the fractional coordinates along a
+    (< 1 for atoms inside one cell, where this is ceil(r))."""
+    cell = np.asarray(cell, dtype=np.float64)
+    vol = abs(np.linalg.det(cell))
+    span = np.zeros(3)
+    if pos is not None and len(pos):
+        frac = np.asarray(pos, dtype=np.float64) @ np.linalg.inv(cell)
+        span = frac.max(axis=0) - frac.min(axis=0)
+    out = np.zeros(3, dtype=np.int64)
+    for a in range(3):
+        if pbc[a]:
+            r = cutoff / (vol / np.linalg.norm(np.cross(cell[(a + 1) % 3], cell[(a + 2) % 3])))
+            out[a] = max(int(np.ceil(r)), int(np.floor(r + span[a])))
+    return out
+
+
+def image_shifts(cell, nimg):
+    """Shift of every image index img = ((i+na)(2nb+1) + (j+nb))(2nc+1) + (k+nc):
+    s = (i c0 + j c1) + k c2, evaluated left to right in fp64."""
+    cell = np.asarray(cell, dtype=np.float64)
+    na, nb, nc = (int(x) for x in nimg)
+    ijk = np.array([(i, j, k) for i in range(-na, na + 1) for j in range(-nb, nb + 1) for k in range(-nc, nc + 1)],
+                   dtype=np.float64)
+    return (ijk[:, 0:1] * cell[0] + ijk[:, 1:2] * cell[1]) + ijk[:, 2:3] * cell[2]
+
+
+def build_graph_pbc(pos, cell, pbc, cutoff) -> Graph:
+    """Periodic cutoff graph: edges (a, b, img) with 0 < |(x_b + s_img) - x_a| <= cutoff
+    (not b == a in the home image), rows ordered by (b, img); reverse = (b, a, mirrored
+    img); triplets of out-edge (j -> i') pair it with every in-edge (k -> j) that is not its
+    own reverse, in the order of the centre's out-edges (for a non-periodic cell this is
+    the reference's enumerate_triplets order)."""
+    if cutoff <= 0:
+        raise ValueError("cutoff must be positive")
+    pos = np.asarray(pos, dtype=np.float64)
+    n = pos.shape[0]
+    nimg = image_ranges(cell, pbc, cutoff, pos)
+    shifts = image_shifts(cell, nimg)
+    n_img = shifts.shape[0]
+    centre = n_img // 2
+    # candidate (a, b, img): vector (x_b + s) - x_a, same operation order as the kernels
+    shifted = pos[None, :, :] + shifts[:, None, :]  # [img, b, 3]
+    diff = shifted[None, :, :, :] - pos[:, None, None, :]  # [a, img, b, 3]
+    dist = np.sqrt((diff * diff).sum(axis=3))
+    mask = (dist > 0.0) & (dist <= cutoff)
+    mask[np.arange(n), centre, np.arange(n)] = False
+    mask = mask.transpose(0, 2, 1)  # [a, b, img]: row-major nonzero = (a, b, img) order
+    src, recv, img = (x.astype(np.int64) for x in np.nonzero(mask))
+    shift = shifts[img]
+    vec = (pos[recv] + shift) - pos[src]
+    d = np.sqrt((vec * vec).sum(axis=1))
+    units = vec / d[:, None] if src.size else np.zeros((0, 3))
+    key = {(int(a), int(b), int(m)): e for e, (a, b, m) in enumerate(zip(src, recv, img))}
+    rev = np.empty(src.size, dtype=np.int64)
+    for e in range(src.size):
+        pair = (int(recv[e]), int(src[e]), n_img - 1 - int(img[e]))
+        if pair not in key:
+            raise ValueError(f"edge {e} has no reverse edge {pair}")
+        rev[e] = key[pair]
+    ptr = np.searchsorted(src, np.arange(n + 1))
+    ins, outs = [], []
+    for j in range(n):
+        row = np.arange(ptr[j], ptr[j + 1])
+        for p in row:
+            q = row[row != p]
+            if q.size:
+                ins.append(rev[q])
+                outs.append(np.full(q.size, p, dtype=np.int64))
+    trip_in = np.concatenate(ins) if ins else np.empty(0, dtype=np.int64)
+    trip_out = np.concatenate(outs) if outs else np.empty(0, dtype=np.int64)
+    angles = triplet_angles(pos, src, recv, trip_in, trip_out, vec, rev)
+    return Graph(n, src, recv, trip_in, trip_out, d, units, angles, rev, vec, img)
 
 
 # ---------------------------------------------------------------------------
@@ -566,7 +655,7 @@ def backward(fw: Forward, P: dict, d_energy: float = 1.0, d_forces: np.ndarray |
         dd, da = sbf_partials(d_in, g.angles, c.k_rbf, c.l_sbf, c.cutoff)
         np.add.at(dist_bar, g.trip_in, (S_bar * dd).sum(axis=1))
         ang_bar = (S_bar * da).sum(axis=1)
-        g_k, g_j, g_i = angle_gradients(pos, g.src, g.recv, g.trip_in, g.trip_out)
+        g_k, g_j, g_i = angle_gradients(pos, g.src, g.recv, g.trip_in, g.trip_out, g.vec, g.rev)
         k = g.src[g.trip_in]
         j = g.recv[g.trip_in]
         i = g.recv[g.trip_out]
@@ -578,7 +667,7 @@ def backward(fw: Forward, P: dict, d_energy: float = 1.0, d_forces: np.ndarray |
     if n_e:
         dist_bar += (R_bar * rbf_ddist(g.dist, c.k_rbf, c.cutoff)).sum(axis=1)
         if gem:
-            diff = pos[g.recv] - pos[g.src]
+            diff = g.vec if g.vec is not None else pos[g.recv] - pos[g.src]
             unit = diff / g.dist[:, None]
             proj = (units_bar * unit).sum(axis=1, keepdims=True)
             contrib = (units_bar - proj * unit) / g.dist[:, None]

@@ -40,6 +40,11 @@ SIGNATURES: dict[str, tuple] = {
     "egn_reverse_edges": (_i32, [_p, _p, _p, _i64, _p, _p, _p]),
     "egn_triplets_fill": (_i32, [_p, _p, _p, _i64, _p, _p, _p]),
     "egn_geometry": (_i32, [_p, _p, _p, _i64, _p, _p, _p, _p]),
+    "egn_neighbors_count_pbc": (_i32, [_p, _p, _p, _i64, _p, _p, _f64, _p, _p]),
+    "egn_neighbors_fill_pbc": (_i32, [_p, _p, _p, _i64, _p, _p, _f64, _p, _p, _p, _p, _p, _p]),
+    "egn_reverse_edges_pbc": (_i32, [_p, _p, _p, _p, _p, _p, _i64, _p, _p, _p]),
+    "egn_geometry_shift": (_i32, [_p, _p, _p, _p, _i64, _p, _p, _p, _p]),
+    "egn_triplet_angles_shift": (_i32, [_p, _p, _p, _p, _p, _i64, _p, _p]),
     "egn_triplet_angles": (_i32, [_p, _p, _p, _p, _i64, _p, _p]),
     "egn_rbf": (_i32, [_p, _i64, _i32, _f64, _p, _p]),
     "egn_sbf": (_i32, [_p, _p, _p, _i64, _i32, _i32, _f64, _p, _p]),

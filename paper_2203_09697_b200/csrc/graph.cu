@@ -226,6 +226,185 @@ __global__ void triplet_angles_kernel(const double* __restrict__ pos,
   }
 }
 
+// ---------------------------------------------------------------------------
+// Periodic cells.  Per graph: cell rows c0, c1, c2 (lattice vectors)
+// and image ranges nimg = (na, nb, nc); image index img = ((i+na)(2nb+1) + (j+nb))(2nc+1)
+// + (k+nc) for the shift s = (i c0 + j c1) + k c2 (per component, round-to-nearest, no FMA).
+// An edge (a, b, img) is the vector (x_b + s) - x_a; candidates of a row are ordered by
+// (b, img), so rows are sorted by (recv, img) and the mirrored image of img is
+// n_img - 1 - img.
+struct Img {
+  int na, nb, nc, n;
+};
+__device__ __forceinline__ Img img_dims(const int32_t* __restrict__ nimg, int g) {
+  Img m;
+  m.na = nimg[3 * g];
+  m.nb = nimg[3 * g + 1];
+  m.nc = nimg[3 * g + 2];
+  m.n = (2 * m.na + 1) * (2 * m.nb + 1) * (2 * m.nc + 1);
+  return m;
+}
+__device__ __forceinline__ void img_shift(const double* __restrict__ cell, int g, const Img& m, int img,
+                                          double& sx, double& sy, double& sz) {
+  const int kc = img % (2 * m.nc + 1) - m.nc;
+  const int r = img / (2 * m.nc + 1);
+  const int jb = r % (2 * m.nb + 1) - m.nb;
+  const int ia = r / (2 * m.nb + 1) - m.na;
+  const double* c = cell + 9 * g;
+  const double fi = ia, fj = jb, fk = kc;
+  sx = __dadd_rn(__dadd_rn(__dmul_rn(fi, c[0]), __dmul_rn(fj, c[3])), __dmul_rn(fk, c[6]));
+  sy = __dadd_rn(__dadd_rn(__dmul_rn(fi, c[1]), __dmul_rn(fj, c[4])), __dmul_rn(fk, c[7]));
+  sz = __dadd_rn(__dadd_rn(__dmul_rn(fi, c[2]), __dmul_rn(fj, c[5])), __dmul_rn(fk, c[8]));
+}
+__device__ __forceinline__ double pair_dist_shift(const double* __restrict__ pos, int64_t a, int64_t b, double sx,
+                                                  double sy, double sz) {
+  const double bx = __dadd_rn(pos[3 * b + 0], sx), by = __dadd_rn(pos[3 * b + 1], sy),
+               bz = __dadd_rn(pos[3 * b + 2], sz);
+  const double dx = __dsub_rn(bx, pos[3 * a + 0]), dy = __dsub_rn(by, pos[3 * a + 1]),
+               dz = __dsub_rn(bz, pos[3 * a + 2]);
+  return __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz)));
+}
+
+// One warp per source atom; lanes sweep (b, img) candidates in (b, img) order.
+template <bool FILL>
+__global__ void neighbors_pbc_kernel(const double* __restrict__ pos, const int64_t* __restrict__ graph_ptr,
+                                     const int32_t* __restrict__ node_graph, int64_t n,
+                                     const double* __restrict__ cell, const int32_t* __restrict__ nimg,
+                                     double cutoff, int32_t* __restrict__ deg, const int64_t* __restrict__ edge_ptr,
+                                     int32_t* __restrict__ src, int32_t* __restrict__ recv,
+                                     int32_t* __restrict__ eimg, double* __restrict__ shift) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t a = warp; a < n; a += nwarps) {
+    const int g = node_graph[a];
+    const int64_t b0 = graph_ptr[g], b1 = graph_ptr[g + 1];
+    const Img m = img_dims(nimg, g);
+    const int centre = m.n / 2;
+    const int64_t ncand = (b1 - b0) * m.n;
+    int count = 0;
+    int64_t out = FILL ? edge_ptr[a] : 0;
+    for (int64_t base = 0; base < ncand; base += 32) {
+      const int64_t c = base + lane;
+      bool hit = false;
+      int64_t b = 0;
+      int img = 0;
+      double sx = 0.0, sy = 0.0, sz = 0.0;
+      if (c < ncand) {
+        b = b0 + c / m.n;
+        img = static_cast<int>(c % m.n);
+        img_shift(cell, g, m, img, sx, sy, sz);
+        const double d = pair_dist_shift(pos, a, b, sx, sy, sz);
+        hit = !(b == a && img == centre) && (d > 0.0) && (d <= cutoff);
+      }
+      if (!FILL) {
+        count += hit;
+      } else {
+        const unsigned mask = __ballot_sync(0xffffffffu, hit);
+        if (hit) {
+          const int64_t slot = out + __popc(mask & ((1u << lane) - 1u));
+          src[slot] = static_cast<int32_t>(a);
+          recv[slot] = static_cast<int32_t>(b);
+          eimg[slot] = img;
+          shift[3 * slot + 0] = sx;
+          shift[3 * slot + 1] = sy;
+          shift[3 * slot + 2] = sz;
+        }
+        out += __popc(mask);
+      }
+    }
+    if (!FILL) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) count += __shfl_xor_sync(0xffffffffu, count, o);
+      if (lane == 0) deg[a] = count;
+    }
+  }
+}
+
+// rev[e]: the edge (recv_e, src_e, mirrored image): binary search on (recv, img) in recv_e's row.
+__global__ void reverse_edges_pbc_kernel(const int64_t* __restrict__ edge_ptr, const int32_t* __restrict__ src,
+                                         const int32_t* __restrict__ recv, const int32_t* __restrict__ eimg,
+                                         const int32_t* __restrict__ node_graph, const int32_t* __restrict__ nimg,
+                                         int64_t ne, int32_t* __restrict__ rev, int32_t* __restrict__ missing) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < ne; e += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t a = src[e], b = recv[e];
+    const Img m = img_dims(nimg, node_graph[a]);
+    const int64_t key = static_cast<int64_t>(a) * m.n + (m.n - 1 - eimg[e]);
+    int64_t lo = edge_ptr[b], hi = edge_ptr[b + 1];
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (static_cast<int64_t>(recv[mid]) * m.n + eimg[mid] < key) lo = mid + 1;
+      else hi = mid;
+    }
+    if (lo < edge_ptr[b + 1] && static_cast<int64_t>(recv[lo]) * m.n + eimg[lo] == key) {
+      rev[e] = static_cast<int32_t>(lo);
+    } else {
+      rev[e] = -1;
+      atomicAdd(missing, 1);
+    }
+  }
+}
+
+// Edge geometry from (x_recv + shift) - x_src (shift NULL: the non-periodic form).
+__global__ void geometry_shift_kernel(const double* __restrict__ pos, const int32_t* __restrict__ src,
+                                      const int32_t* __restrict__ recv, const double* __restrict__ shift, int64_t ne,
+                                      float4* __restrict__ geo, double* __restrict__ dist64,
+                                      double* __restrict__ unit64) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < ne; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t a = src[e], b = recv[e];
+    const double bx = __dadd_rn(pos[3 * b + 0], shift[3 * e + 0]);
+    const double by = __dadd_rn(pos[3 * b + 1], shift[3 * e + 1]);
+    const double bz = __dadd_rn(pos[3 * b + 2], shift[3 * e + 2]);
+    const double dx = __dsub_rn(bx, pos[3 * a + 0]), dy = __dsub_rn(by, pos[3 * a + 1]),
+                 dz = __dsub_rn(bz, pos[3 * a + 2]);
+    const double d = __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz)));
+    const double ux = __ddiv_rn(dx, d), uy = __ddiv_rn(dy, d), uz = __ddiv_rn(dz, d);
+    geo[e] = make_float4(static_cast<float>(ux), static_cast<float>(uy), static_cast<float>(uz),
+                         static_cast<float>(d));
+    if (dist64) dist64[e] = d;
+    if (unit64) {
+      unit64[3 * e + 0] = ux;
+      unit64[3 * e + 1] = uy;
+      unit64[3 * e + 2] = uz;
+    }
+  }
+}
+
+// Triplet angles from edge vectors: v1 = -vec(rev-side in-edge) = vec(off+q), v2 = vec(off+p),
+// vec(e) = (x_recv + shift) - x_src, all per the centre's out-edges.
+__global__ void triplet_angles_shift_kernel(const double* __restrict__ pos, const int64_t* __restrict__ edge_ptr,
+                                            const int32_t* __restrict__ recv, const double* __restrict__ shift,
+                                            const int64_t* __restrict__ tri_ptr, int64_t nv,
+                                            double* __restrict__ angles) {
+  for (int64_t j = blockIdx.x; j < nv; j += gridDim.x) {
+    const int64_t off = edge_ptr[j];
+    const int64_t n = edge_ptr[j + 1] - off;
+    if (n < 2) continue;
+    const int64_t t0 = tri_ptr[j];
+    const int64_t cnt = n * (n - 1);
+    const double xj = pos[3 * j], yj = pos[3 * j + 1], zj = pos[3 * j + 2];
+    for (int64_t k = threadIdx.x; k < cnt; k += blockDim.x) {
+      const int64_t p = k / (n - 1);
+      const int64_t r = k - p * (n - 1);
+      const int64_t q = r < p ? r : r + 1;
+      const int64_t eq = off + q, ep = off + p;
+      const int64_t kk = recv[eq], ii = recv[ep];
+      const double v1x = __dsub_rn(__dadd_rn(pos[3 * kk], shift[3 * eq]), xj);
+      const double v1y = __dsub_rn(__dadd_rn(pos[3 * kk + 1], shift[3 * eq + 1]), yj);
+      const double v1z = __dsub_rn(__dadd_rn(pos[3 * kk + 2], shift[3 * eq + 2]), zj);
+      const double v2x = __dsub_rn(__dadd_rn(pos[3 * ii], shift[3 * ep]), xj);
+      const double v2y = __dsub_rn(__dadd_rn(pos[3 * ii + 1], shift[3 * ep + 1]), yj);
+      const double v2z = __dsub_rn(__dadd_rn(pos[3 * ii + 2], shift[3 * ep + 2]), zj);
+      const double cx = __dsub_rn(__dmul_rn(v1y, v2z), __dmul_rn(v1z, v2y));
+      const double cy = __dsub_rn(__dmul_rn(v1z, v2x), __dmul_rn(v1x, v2z));
+      const double cz = __dsub_rn(__dmul_rn(v1x, v2y), __dmul_rn(v1y, v2x));
+      const double s = __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(cx, cx), __dmul_rn(cy, cy)), __dmul_rn(cz, cz)));
+      const double c = __dadd_rn(__dadd_rn(__dmul_rn(v1x, v2x), __dmul_rn(v1y, v2y)), __dmul_rn(v1z, v2z));
+      angles[t0 + k] = atan2(s, c);
+    }
+  }
+}
+
 }  // namespace egn
 
 using namespace egn;
@@ -298,6 +477,54 @@ int egn_triplet_angles(const double* pos, const int64_t* edge_ptr, const int32_t
   triplet_angles_kernel<<<grid, 256, 0, as_stream(stream)>>>(pos, edge_ptr, recv, tri_ptr,
                                                              num_nodes, angles);
   return check_launch("triplet_angles");
+}
+
+int egn_neighbors_count_pbc(const double* pos, const int64_t* graph_ptr, const int32_t* node_graph,
+                            int64_t num_nodes, const double* cell, const int32_t* nimg, double cutoff, int32_t* deg,
+                            egn_stream_t stream) {
+  EGN_REQUIRE(cutoff > 0, "cutoff must be positive");
+  if (num_nodes == 0) return 0;
+  neighbors_pbc_kernel<false><<<grid_for(num_nodes * 32, 256), 256, 0, as_stream(stream)>>>(
+      pos, graph_ptr, node_graph, num_nodes, cell, nimg, cutoff, deg, nullptr, nullptr, nullptr, nullptr, nullptr);
+  return check_launch("neighbors_count_pbc");
+}
+
+int egn_neighbors_fill_pbc(const double* pos, const int64_t* graph_ptr, const int32_t* node_graph,
+                           int64_t num_nodes, const double* cell, const int32_t* nimg, double cutoff,
+                           const int64_t* edge_ptr, int32_t* src, int32_t* recv, int32_t* img, double* shift,
+                           egn_stream_t stream) {
+  if (num_nodes == 0) return 0;
+  neighbors_pbc_kernel<true><<<grid_for(num_nodes * 32, 256), 256, 0, as_stream(stream)>>>(
+      pos, graph_ptr, node_graph, num_nodes, cell, nimg, cutoff, nullptr, edge_ptr, src, recv, img, shift);
+  return check_launch("neighbors_fill_pbc");
+}
+
+int egn_reverse_edges_pbc(const int64_t* edge_ptr, const int32_t* src, const int32_t* recv, const int32_t* img,
+                          const int32_t* node_graph, const int32_t* nimg, int64_t num_edges, int32_t* rev,
+                          int32_t* missing, egn_stream_t stream) {
+  if (num_edges == 0) return 0;
+  reverse_edges_pbc_kernel<<<grid_for(num_edges, 256), 256, 0, as_stream(stream)>>>(
+      edge_ptr, src, recv, img, node_graph, nimg, num_edges, rev, missing);
+  return check_launch("reverse_edges_pbc");
+}
+
+int egn_geometry_shift(const double* pos, const int32_t* src, const int32_t* recv, const double* shift,
+                       int64_t num_edges, float* geo, double* dist64, double* unit64, egn_stream_t stream) {
+  if (num_edges == 0) return 0;
+  if (shift == nullptr) return egn_geometry(pos, src, recv, num_edges, geo, dist64, unit64, stream);
+  geometry_shift_kernel<<<grid_for(num_edges, 256), 256, 0, as_stream(stream)>>>(
+      pos, src, recv, shift, num_edges, reinterpret_cast<float4*>(geo), dist64, unit64);
+  return check_launch("geometry_shift");
+}
+
+int egn_triplet_angles_shift(const double* pos, const int64_t* edge_ptr, const int32_t* recv, const double* shift,
+                             const int64_t* tri_ptr, int64_t num_nodes, double* angles, egn_stream_t stream) {
+  if (num_nodes == 0) return 0;
+  if (shift == nullptr) return egn_triplet_angles(pos, edge_ptr, recv, tri_ptr, num_nodes, angles, stream);
+  const int grid = static_cast<int>(num_nodes < 65535 ? num_nodes : 65535);
+  triplet_angles_shift_kernel<<<grid, 256, 0, as_stream(stream)>>>(pos, edge_ptr, recv, shift, tri_ptr, num_nodes,
+                                                                   angles);
+  return check_launch("triplet_angles_shift");
 }
 
 }  // extern "C"

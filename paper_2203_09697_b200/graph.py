@@ -41,6 +41,12 @@ class BatchGraph:
     graph_sizes: list  # host: atoms per graph
     edge_counts: list | None = None  # host: edges per graph (lazily)
     max_deg: int = 0  # host: max out-degree (sizes the backward tile)
+    # periodic batches: per-edge image index and shift (x_recv + shift
+    # - x_src is the edge vector), per-graph cell / image ranges; None when non-periodic
+    img: torch.Tensor | None = None  # i32 [E]
+    shift: torch.Tensor | None = None  # f64 [E, 3]
+    cell: torch.Tensor | None = None  # f64 [G, 3, 3]
+    nimg: torch.Tensor | None = None  # i32 [G, 3]
 
     @property
     def device(self):
@@ -56,8 +62,12 @@ class BatchGraph:
         neighbour list is built once per batch and its buffers stay valid for a
         captured step."""
         self.pos.copy_(pos, non_blocking=True)
-        ops.call("egn_geometry", ops.ptr(self.pos), ops.ptr(self.src), ops.ptr(self.recv), self.num_edges,
-                 ops.ptr(self.geo), None, None, ops.stream())
+        if self.shift is None:
+            ops.call("egn_geometry", ops.ptr(self.pos), ops.ptr(self.src), ops.ptr(self.recv), self.num_edges,
+                     ops.ptr(self.geo), None, None, ops.stream())
+        else:
+            ops.call("egn_geometry_shift", ops.ptr(self.pos), ops.ptr(self.src), ops.ptr(self.recv),
+                     ops.ptr(self.shift), self.num_edges, ops.ptr(self.geo), None, None, ops.stream())
 
 
 def _as_positions(systems) -> tuple[np.ndarray, list[int]]:
@@ -67,11 +77,63 @@ def _as_positions(systems) -> tuple[np.ndarray, list[int]]:
     return (np.concatenate(pos, axis=0) if pos else np.zeros((0, 3))), [p.shape[0] for p in pos]
 
 
+def image_ranges(cell, pbc, cutoff: float, span=None) -> np.ndarray:
+    """Images per axis that can hold a neighbour within the cutoff: max(ceil(r), floor(r +
+    span_a)) with r = cutoff / h_a, h_a = |det C| / |c_b x c_c| the cell height normal to
+    face a and span_a the extent of the atoms' fractional coordinates along a (< 1 when
+    all atoms sit in one cell, where this is ceil(r)); 0 on non-periodic axes."""
+    cell = np.asarray(cell, dtype=np.float64)
+    vol = abs(np.linalg.det(cell))
+    span = np.zeros(3) if span is None else np.asarray(span, dtype=np.float64)
+    out = np.zeros(3, dtype=np.int32)
+    for a in range(3):
+        if pbc[a]:
+            r = cutoff / (vol / np.linalg.norm(np.cross(cell[(a + 1) % 3], cell[(a + 2) % 3])))
+            out[a] = max(int(np.ceil(r)), int(np.floor(r + span[a])))
+    return out
+
+
+def _frac_spans(pos: torch.Tensor, sizes, cells, pbc) -> np.ndarray:
+    """Extent of the fractional coordinates of every periodic graph ([G, 3], one sync)."""
+    g = len(sizes)
+    spans = []
+    off = 0
+    for i in range(g):
+        n = sizes[i]
+        if n and bool(np.any(pbc[i])):
+            inv = torch.from_numpy(np.linalg.inv(cells[i])).to(pos.device)
+            frac = pos[off:off + n] @ inv
+            spans.append(frac.max(dim=0).values - frac.min(dim=0).values)
+        else:
+            spans.append(torch.zeros(3, dtype=torch.float64, device=pos.device))
+        off += n
+    return torch.stack(spans).cpu().numpy() if spans else np.zeros((0, 3))
+
+
+def _periodic_info(systems, g):
+    """(cells [G,3,3], nimg-ready pbc [G,3]) when any system is periodic, else None."""
+    if systems is None:
+        return None
+    if hasattr(systems, "positions"):
+        systems = [systems]
+    if not isinstance(systems, (list, tuple)) or not any(getattr(s, "periodic", False) for s in systems):
+        return None
+    cells = np.zeros((g, 3, 3))
+    pbc = np.zeros((g, 3), dtype=bool)
+    for i, s in enumerate(systems):
+        if getattr(s, "periodic", False):
+            cells[i] = s.cell
+            pbc[i] = s.pbc
+    return cells, pbc
+
+
 def build_batch(systems, cutoff: float, device="cuda", positions: torch.Tensor | None = None,
-                sizes: list[int] | None = None) -> BatchGraph:
+                sizes: list[int] | None = None, cells=None, pbc=None) -> BatchGraph:
     """Build the batched device graph.  ``systems``: an AtomicSystem, a list of
     them, or raw (n,3) position arrays; alternatively pass device ``positions``
-    (f64 [V,3]) and ``sizes`` directly (no host->device copy of positions)."""
+    (f64 [V,3]) and ``sizes`` directly (no host->device copy of positions).
+    Periodic systems (AtomicSystem.cell / pbc, or ``cells`` [G,3,3] with ``pbc`` [G,3])
+    get edges to every periodic image within the cutoff."""
     if cutoff <= 0:
         raise ValueError("cutoff must be positive")
     if positions is None:
@@ -87,17 +149,39 @@ def build_batch(systems, cutoff: float, device="cuda", positions: torch.Tensor |
     gp[1:] = np.cumsum(sizes)
     graph_ptr = torch.from_numpy(gp).to(dev)
     node_graph = torch.from_numpy(np.repeat(np.arange(g, dtype=np.int32), sizes)).to(dev)
-    deg = ops.neighbors_count(pos, graph_ptr, node_graph, cutoff)
+    per = None
+    if cells is not None:
+        per = (np.broadcast_to(np.asarray(cells, dtype=np.float64), (g, 3, 3)),
+               np.broadcast_to(np.asarray(pbc if pbc is not None else True, dtype=bool), (g, 3)))
+    else:
+        per = _periodic_info(systems, g)
+    if per is not None:
+        cells_np, pbc_np = per
+        spans = _frac_spans(pos, sizes, cells_np, pbc_np)
+        nimg_np = np.stack([image_ranges(cells_np[i], pbc_np[i], cutoff, spans[i]) for i in range(g)]).astype(np.int32)
+        cell_t = torch.from_numpy(np.ascontiguousarray(cells_np)).to(dev)
+        nimg_t = torch.from_numpy(nimg_np).to(dev)
+        deg = ops.neighbors_count_pbc(pos, graph_ptr, node_graph, cell_t, nimg_t, cutoff)
+    else:
+        deg = ops.neighbors_count(pos, graph_ptr, node_graph, cutoff)
     edge_ptr = ops.scan_counts(deg)
     tri_ptr = ops.scan_counts(deg, square_minus_one=True)
     dmax = deg.max().to(torch.int64) if pos.shape[0] else edge_ptr[-1]
     counts = torch.stack([edge_ptr[-1], tri_ptr[-1], dmax]).cpu()  # the one host sync
     ne, nt, max_deg = int(counts[0]), int(counts[1]), int(counts[2])
-    src, recv = ops.neighbors_fill(pos, graph_ptr, node_graph, cutoff, edge_ptr, ne)
-    rev, missing = ops.reverse_edges(edge_ptr, src, recv)
-    geo, _, _ = ops.geometry(pos, src, recv)
+    img = shift = cell_keep = nimg_keep = None
+    if per is not None:
+        src, recv, img, shift = ops.neighbors_fill_pbc(pos, graph_ptr, node_graph, cell_t, nimg_t, cutoff, edge_ptr,
+                                                       ne)
+        rev, missing = ops.reverse_edges_pbc(edge_ptr, src, recv, img, node_graph, nimg_t)
+        cell_keep, nimg_keep = cell_t, nimg_t
+    else:
+        src, recv = ops.neighbors_fill(pos, graph_ptr, node_graph, cutoff, edge_ptr, ne)
+        rev, missing = ops.reverse_edges(edge_ptr, src, recv)
+    geo, _, _ = ops.geometry(pos, src, recv, shift=shift)
     return BatchGraph(g, int(pos.shape[0]), ne, nt, float(cutoff), pos, graph_ptr, node_graph, deg,
-                      edge_ptr, src, recv, rev, tri_ptr, geo, list(sizes), max_deg=max_deg)
+                      edge_ptr, src, recv, rev, tri_ptr, geo, list(sizes), max_deg=max_deg, img=img, shift=shift,
+                      cell=cell_keep, nimg=nimg_keep)
 
 
 # ---------------------------------------------------------------------------
@@ -172,8 +256,8 @@ def topology_of(bg: BatchGraph) -> GraphTopology:
 
 
 def geometry_of(bg: BatchGraph) -> Geometry:
-    _, d64, u64 = ops.geometry(bg.pos, bg.src, bg.recv, want_fp64=True)
-    ang = ops.triplet_angles(bg.pos, bg.edge_ptr, bg.recv, bg.tri_ptr, bg.num_triplets)
+    _, d64, u64 = ops.geometry(bg.pos, bg.src, bg.recv, want_fp64=True, shift=bg.shift)
+    ang = ops.triplet_angles(bg.pos, bg.edge_ptr, bg.recv, bg.tri_ptr, bg.num_triplets, shift=bg.shift)
     return Geometry(d64, u64, ang)
 
 

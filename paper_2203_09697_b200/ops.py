@@ -59,20 +59,57 @@ def triplets_fill(edge_ptr, rev, tri_ptr, num_triplets):
     return kj, ji
 
 
-def geometry(pos, src, recv, want_fp64=False):
+def neighbors_count_pbc(pos, graph_ptr, node_graph, cell, nimg, cutoff):
+    n = pos.shape[0]
+    deg = torch.empty(n, dtype=torch.int32, device=pos.device)
+    call("egn_neighbors_count_pbc", ptr(pos), ptr(graph_ptr), ptr(node_graph), n, ptr(cell), ptr(nimg),
+         float(cutoff), ptr(deg), stream())
+    return deg
+
+
+def neighbors_fill_pbc(pos, graph_ptr, node_graph, cell, nimg, cutoff, edge_ptr, num_edges):
+    dev = pos.device
+    src = torch.empty(num_edges, dtype=torch.int32, device=dev)
+    recv = torch.empty(num_edges, dtype=torch.int32, device=dev)
+    img = torch.empty(num_edges, dtype=torch.int32, device=dev)
+    shift = torch.empty((num_edges, 3), dtype=torch.float64, device=dev)
+    call("egn_neighbors_fill_pbc", ptr(pos), ptr(graph_ptr), ptr(node_graph), pos.shape[0], ptr(cell), ptr(nimg),
+         float(cutoff), ptr(edge_ptr), ptr(src), ptr(recv), ptr(img), ptr(shift), stream())
+    return src, recv, img, shift
+
+
+def reverse_edges_pbc(edge_ptr, src, recv, img, node_graph, nimg):
+    rev = torch.empty_like(src)
+    missing = torch.zeros(1, dtype=torch.int32, device=src.device)
+    call("egn_reverse_edges_pbc", ptr(edge_ptr), ptr(src), ptr(recv), ptr(img), ptr(node_graph), ptr(nimg),
+         src.shape[0], ptr(rev), ptr(missing), stream())
+    return rev, missing
+
+
+def geometry(pos, src, recv, want_fp64=False, shift=None):
+    """Packed fp32 (u, d) per edge (+ fp64 d and u); edge vector (x_recv + shift) - x_src."""
     e = src.shape[0]
     geo = torch.empty((e, 4), dtype=torch.float32, device=pos.device)
     d64 = u64 = None
     if want_fp64:
         d64 = torch.empty(e, dtype=torch.float64, device=pos.device)
         u64 = torch.empty((e, 3), dtype=torch.float64, device=pos.device)
-    call("egn_geometry", ptr(pos), ptr(src), ptr(recv), e, ptr(geo), ptr(d64), ptr(u64), stream())
+    if shift is None:
+        call("egn_geometry", ptr(pos), ptr(src), ptr(recv), e, ptr(geo), ptr(d64), ptr(u64), stream())
+    else:
+        call("egn_geometry_shift", ptr(pos), ptr(src), ptr(recv), ptr(shift), e, ptr(geo), ptr(d64), ptr(u64),
+             stream())
     return geo, d64, u64
 
 
-def triplet_angles(pos, edge_ptr, recv, tri_ptr, num_triplets):
+def triplet_angles(pos, edge_ptr, recv, tri_ptr, num_triplets, shift=None):
     out = torch.empty(num_triplets, dtype=torch.float64, device=pos.device)
-    call("egn_triplet_angles", ptr(pos), ptr(edge_ptr), ptr(recv), ptr(tri_ptr), pos.shape[0], ptr(out), stream())
+    if shift is None:
+        call("egn_triplet_angles", ptr(pos), ptr(edge_ptr), ptr(recv), ptr(tri_ptr), pos.shape[0], ptr(out),
+             stream())
+    else:
+        call("egn_triplet_angles_shift", ptr(pos), ptr(edge_ptr), ptr(recv), ptr(shift), ptr(tri_ptr),
+             pos.shape[0], ptr(out), stream())
     return out
 
 

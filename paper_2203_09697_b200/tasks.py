@@ -59,14 +59,17 @@ class _DeviceEvaluator:
     """Energy, forces and max |F| of one system at device positions: graph rebuilt on the
     GPU at every evaluation (neighbour list, triplets, geometry), weights resident."""
 
-    def __init__(self, params: ModelParams, n_atoms: int, device="cuda"):
+    def __init__(self, params: ModelParams, system, device="cuda"):
         self.config = params.config
         self.engine = Engine(DeviceWeights.from_params(params, device))
-        self.sizes = [int(n_atoms)]
+        self.sizes = [int(system.positions.shape[0])]
+        periodic = getattr(system, "periodic", False)
+        self.cells = [system.cell] if periodic else None
+        self.pbc = [system.pbc] if periodic else None
 
     def __call__(self, pos: torch.Tensor):
         c = self.config
-        bg = build_batch(None, c.cutoff, positions=pos, sizes=self.sizes)
+        bg = build_batch(None, c.cutoff, positions=pos, sizes=self.sizes, cells=self.cells, pbc=self.pbc)
         fw = self.engine.forward(bg)
         if c.variant == GEMNET:
             forces = fw.forces.double()
@@ -97,7 +100,7 @@ def relax(system, params: ModelParams, fmax_threshold: float, max_steps: int = 2
     guard = config.energy_centric
     eta = float(step_size)
     x = torch.as_tensor(np.asarray(system.positions, dtype=np.float64), device=device).clone()
-    evaluate = _DeviceEvaluator(params, x.shape[0], device)
+    evaluate = _DeviceEvaluator(params, system, device)
     trajectory = [x.cpu().numpy().copy()]
     energies: list[float] = []
     max_forces: list[float] = []

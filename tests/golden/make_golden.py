@@ -195,8 +195,74 @@ def make_relax():
         print(f"relax_{name}.npz steps", res.steps, "converged", res.converged, "energies", res.energies)
 
 
+PBC_CASES = {
+    # name: (n atoms, box-fill seed, cell rows, pbc, cutoff)
+    "cubic4": (4, 70, [[3.0, 0, 0], [0, 3.0, 0], [0, 0, 3.0]], (True, True, True), 2.5),
+    "triclinic5": (5, 71, [[3.2, 0, 0], [0.8, 2.9, 0], [0.5, 0.6, 3.1]], (True, True, True), 2.8),
+    "slab6": (6, 72, [[3.5, 0, 0], [0, 3.5, 0], [0, 0, 20.0]], (True, True, False), 3.0),
+    "self_image1": (1, 73, [[1.6, 0, 0], [0, 1.7, 0], [0, 0, 1.8]], (True, True, True), 2.0),
+    # atoms spread over three cells along c0 (unwrapped coordinates): wider image range
+    "unwrapped5": (5, 74, [[3.0, 0, 0], [0.4, 3.1, 0], [0, 0.5, 3.3]], (True, True, True), 2.6),
+}
+
+
+def _image_shifts(cell, pbc, cutoff, pos):
+    """Image ranges max(ceil(r), floor(r + span)) (r = cutoff / cell height, span = extent of
+    the fractional coordinates) and shifts (i c0 + j c1) + k c2 in image-index order
+    ((i, j, k) lexicographic) -- the convention of include/egn_b200.h."""
+    cell = np.asarray(cell, dtype=np.float64)
+    vol = abs(np.linalg.det(cell))
+    frac = pos @ np.linalg.inv(cell)
+    span = frac.max(axis=0) - frac.min(axis=0)
+    nimg = []
+    for a in range(3):
+        r = cutoff / (vol / np.linalg.norm(np.cross(cell[(a + 1) % 3], cell[(a + 2) % 3])))
+        nimg.append(max(int(np.ceil(r)), int(np.floor(r + span[a]))) if pbc[a] else 0)
+    ijk = np.array([(i, j, k) for i in range(-nimg[0], nimg[0] + 1) for j in range(-nimg[1], nimg[1] + 1)
+                    for k in range(-nimg[2], nimg[2] + 1)], dtype=np.float64)
+    return np.array(nimg), (ijk[:, 0:1] * cell[0] + ijk[:, 1:2] * cell[1]) + ijk[:, 2:3] * cell[2]
+
+
+def make_pbc():
+    """Periodic neighbour lists from the REFERENCE build_graph on an explicit supercell: every
+    image within range is materialised as atoms x_b + s_img; the neighbours of the home-image
+    atoms are the periodic edges (a, b, img) with their distances."""
+    out = {}
+    for name, (n, seed, cell, pbc, cutoff) in PBC_CASES.items():
+        cell = np.asarray(cell, dtype=np.float64)
+        frac = np.random.default_rng(seed).uniform(0.0, 1.0, (n, 3))
+        if name == "unwrapped5":
+            frac[:, 0] += np.array([0.0, 1.0, -1.0, 2.0, 0.0])
+        pos = frac @ cell
+        nimg, shifts = _image_shifts(cell, pbc, cutoff, pos)
+        n_img = shifts.shape[0]
+        centre = n_img // 2
+        sc = (pos[None, :, :] + shifts[:, None, :]).reshape(-1, 3)  # supercell atom img * n + b
+        topo, geom = build_graph(AtomicSystem(sc, np.full(sc.shape[0], 6)), cutoff)
+        home = (topo.edge_src >= centre * n) & (topo.edge_src < (centre + 1) * n)
+        a = topo.edge_src[home] - centre * n
+        b = topo.edge_recv[home] % n
+        img = topo.edge_recv[home] // n
+        d = geom.distances[home]
+        order = np.lexsort((img, b, a))  # rows ordered by (a, b, img)
+        out[f"{name}/pos"] = pos
+        out[f"{name}/cell"] = cell
+        out[f"{name}/pbc"] = np.array(pbc)
+        out[f"{name}/cutoff"] = np.array(cutoff)
+        out[f"{name}/nimg"] = nimg
+        out[f"{name}/src"] = a[order]
+        out[f"{name}/recv"] = b[order]
+        out[f"{name}/img"] = img[order]
+        out[f"{name}/dist"] = d[order]
+        print(name, "edges", len(order), "images", nimg.tolist())
+    out["numpy_version"] = np.array(np.__version__)
+    np.savez_compressed(OUT / "pbc.npz", **out)
+
+
 if __name__ == "__main__":
-    parts = sys.argv[1:] or ["graphs", "models", "training", "relax"]
+    parts = sys.argv[1:] or ["graphs", "models", "training", "relax", "pbc"]
+    if "pbc" in parts:
+        make_pbc()
     if "graphs" in parts:
         make_graphs()
     if "models" in parts:

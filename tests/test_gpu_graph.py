@@ -103,3 +103,46 @@ def test_large_graph_neighbor_counts():
     deg = np.bincount(ref_src, minlength=1000)
     assert topo.num_triplets == int((deg * (deg - 1)).sum())
     assert max_rel(geom.distances.cpu().numpy(), np.sqrt(((pos[ref_recv] - pos[ref_src]) ** 2).sum(1))) == 0.0
+
+
+@pytest.mark.parametrize("name", ["cubic4", "triclinic5", "slab6", "self_image1", "unwrapped5"])
+def test_periodic_graph_bit_exact(name):
+    """GPU periodic neighbour list / reverse edges / triplets / geometry vs the oracle
+    restatement (itself pinned to the reference on an explicit supercell)."""
+    from conftest import load_golden
+    from paper_2203_09697_b200 import AtomicSystem
+    from paper_2203_09697_b200.graph import build_batch, geometry_of, topology_of
+
+    gd = load_golden("pbc.npz")
+    pos, cell, pbc, cutoff = gd[f"{name}/pos"], gd[f"{name}/cell"], gd[f"{name}/pbc"], float(gd[f"{name}/cutoff"])
+    ref = O.build_graph_pbc(pos, cell, pbc, cutoff)
+    bg = build_batch(AtomicSystem(pos, np.full(pos.shape[0], 6), cell=cell, pbc=tuple(pbc)), cutoff)
+    topo, geom = topology_of(bg), geometry_of(bg)
+    np.testing.assert_array_equal(bg.img.cpu().numpy(), ref.img)
+    for key, val in (("src", topo.edge_src), ("recv", topo.edge_recv), ("trip_in", topo.trip_in),
+                     ("trip_out", topo.trip_out), ("rev", topo.reverse_edges())):
+        np.testing.assert_array_equal(val.cpu().numpy(), getattr(ref, key), err_msg=key)
+    np.testing.assert_array_equal(geom.distances.cpu().numpy(), ref.dist)
+    np.testing.assert_array_equal(geom.unit_vectors.cpu().numpy(), ref.units)
+    np.testing.assert_allclose(geom.angles.cpu().numpy(), ref.angles, rtol=0, atol=1e-12)
+
+
+def test_periodic_batch_mixes_periodic_and_open_graphs():
+    from paper_2203_09697_b200 import AtomicSystem
+    from paper_2203_09697_b200.graph import build_batch, topology_of
+
+    rng = np.random.default_rng(3)
+    cell = np.array([[4.0, 0, 0], [0.5, 3.8, 0], [0, 0.3, 4.2]])
+    p1 = rng.uniform(0, 1, (7, 3)) @ cell
+    p2, _ = O.random_cloud(12, 0.2, rng)
+    systems = [AtomicSystem(p1, np.full(7, 6), cell=cell, pbc=(True, True, True)), AtomicSystem(p2, np.full(12, 6))]
+    bg = build_batch(systems, 3.0)
+    t = topology_of(bg)
+    r1 = O.build_graph_pbc(p1, cell, (True, True, True), 3.0)
+    r2 = O.build_graph(p2, 3.0)
+    e1 = r1.src.size
+    np.testing.assert_array_equal(t.edge_src.cpu().numpy()[:e1], r1.src)
+    np.testing.assert_array_equal(t.edge_recv.cpu().numpy()[:e1], r1.recv)
+    np.testing.assert_array_equal(t.edge_src.cpu().numpy()[e1:], r2.src + 7)
+    np.testing.assert_array_equal(t.edge_recv.cpu().numpy()[e1:], r2.recv + 7)
+    np.testing.assert_array_equal(bg.geo[:, 3].cpu().numpy(), np.concatenate([r1.dist, r2.dist]).astype(np.float32))

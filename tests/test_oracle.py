@@ -117,6 +117,35 @@ def test_relax_matches_reference(variant):
         O.relax(cfg, P, gd["pos"], gd["z"], 1e-3, max_steps=-1)
 
 
+PBC_NAMES = ["cubic4", "triclinic5", "slab6", "self_image1", "unwrapped5"]
+
+
+@pytest.mark.parametrize("name", PBC_NAMES)
+def test_periodic_graph_matches_reference_supercell(name):
+    """Periodic neighbour list vs the reference build_graph on an explicit
+    supercell (tests/golden/pbc.npz): same (a, b, image) edges, bit-identical distances."""
+    gd = load_golden("pbc.npz")
+    g = O.build_graph_pbc(gd[f"{name}/pos"], gd[f"{name}/cell"], gd[f"{name}/pbc"], float(gd[f"{name}/cutoff"]))
+    np.testing.assert_array_equal(O.image_ranges(gd[f"{name}/cell"], gd[f"{name}/pbc"], float(gd[f"{name}/cutoff"]),
+                                                 gd[f"{name}/pos"]), gd[f"{name}/nimg"])
+    for key, val in (("src", g.src), ("recv", g.recv), ("img", g.img), ("dist", g.dist)):
+        np.testing.assert_array_equal(val, gd[f"{name}/{key}"], err_msg=f"{name}/{key}")
+    # reverse edges mirror the image; triplets never pair an edge with its own reverse
+    n_img = int(np.prod(2 * gd[f"{name}/nimg"] + 1))
+    assert np.array_equal(g.src[g.rev], g.recv) and np.array_equal(g.img[g.rev], n_img - 1 - g.img)
+    assert not np.any(g.rev[g.trip_out] == g.trip_in)
+    assert np.array_equal(g.recv[g.trip_in], g.src[g.trip_out])
+
+
+def test_periodic_graph_without_images_is_the_reference_graph():
+    rng = np.random.default_rng(5)
+    pos, _ = O.random_cloud(30, 0.2, rng)
+    a = O.build_graph(pos, 3.0)
+    b = O.build_graph_pbc(pos, np.eye(3) * 1e3, (True, True, True), 3.0)
+    for key in ("src", "recv", "trip_in", "trip_out", "rev", "dist", "units", "angles"):
+        np.testing.assert_array_equal(getattr(a, key), getattr(b, key), err_msg=key)
+
+
 def test_oracle_fd_gradient_spot_check():
     """Independent of the fixtures: central differences of the oracle energy."""
     cfg = O.Config(variant=O.DIMENET, blocks=1)
