@@ -325,6 +325,110 @@ __global__ void __launch_bounds__(256) rbf_linear_bwd_kernel(const float* __rest
   }
 }
 
+// Lane group per edge: LPE = N / 4 lanes hold float4 slices of g's row (32 / LPE edges per
+// warp instruction) and the matching W rows in registers.  rbf_bar[e, k] = sum_n g[e, n] W[n, k]
+// is an 8-value transpose reduction inside the lane group; W_bar[n, k] += g[e, n] rbf[e, k] and
+// b_bar[n] += g[e, n] accumulate in registers, then a fixed-order sum over the CTA's warps (and
+// the lane groups) gives one partial row per CTA (reduced by reduce_parts_kernel).
+template <int LPE, int KT>
+__global__ void __launch_bounds__(256) rbf_linear_bwd_group_kernel(const float* __restrict__ rbf, int64_t ne,
+                                                                   int K, const float* __restrict__ W, int N,
+                                                                   const float* __restrict__ g, int64_t ldg,
+                                                                   float* __restrict__ rbf_bar,
+                                                                   float* __restrict__ part) {
+  constexpr int EPW = 32 / LPE;  // edges per warp instruction
+  static_assert(LPE >= 8 && LPE <= 32, "lane group of 8..32");
+  __shared__ float red[8 * EPW][36 * LPE];  // per slot: N K weights + N biases, N = 4 LPE, K <= 8
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int grp = lane / LPE, gl = lane % LPE;  // lane group (edge slot) and lane inside it
+  const int len = N * K + N;
+  const int kk_n = KT == 8 ? K : KT;
+  float wr[4][8], wacc[4][8], bacc[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    bacc[i] = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      wr[i][k] = k < kk_n ? W[(gl * 4 + i) * kk_n + k] : 0.f;
+      wacc[i][k] = 0.f;
+    }
+  }
+  // bits of the lane-group index that pick the reduced column (levels LPE/2, LPE/4, LPE/8)
+  const int b4 = (gl / (LPE / 2)) & 1, b3 = (gl / (LPE / 4)) & 1, b2 = (gl / (LPE / 8)) & 1;
+  const int kk = b4 * 4 + b3 * 2 + b2;
+  const bool writer = (gl % (LPE / 8)) == 0 && kk < kk_n;
+  const int64_t slots = static_cast<int64_t>(gridDim.x) * 8 * EPW;  // edge slots in flight
+  const int64_t my = (static_cast<int64_t>(blockIdx.x) * 8 + warp) * EPW + grp;
+  for (int64_t e0 = my; e0 - grp < ne; e0 += 2 * slots) {
+    float gv[2][4], r[2][8], old[2];
+    bool ok[2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int64_t e = e0 + u * slots;
+      ok[u] = e < ne;
+      const int64_t ec = ok[u] ? e : 0;
+      const float4 v = ok[u] ? __ldg(reinterpret_cast<const float4*>(g + ec * ldg + gl * 4)) : make_float4(0.f, 0.f, 0.f, 0.f);
+      gv[u][0] = v.x; gv[u][1] = v.y; gv[u][2] = v.z; gv[u][3] = v.w;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) r[u][k] = (k < kk_n && ok[u]) ? __ldg(rbf + ec * kk_n + k) : 0.f;
+      old[u] = (writer && ok[u]) ? rbf_bar[ec * kk_n + kk] : 0.f;
+    }
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      float sv[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        float t = 0.f;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) t = fmaf(gv[u][i], wr[i][k], t);
+        sv[k] = k < kk_n ? t : 0.f;
+      }
+      float w4[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float mine = b4 ? sv[4 + j] : sv[j];
+        const float other = b4 ? sv[j] : sv[4 + j];
+        w4[j] = mine + __shfl_xor_sync(0xffffffffu, other, LPE / 2);
+      }
+      float w2[2];
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const float mine = b3 ? w4[2 + j] : w4[j];
+        const float other = b3 ? w4[j] : w4[2 + j];
+        w2[j] = mine + __shfl_xor_sync(0xffffffffu, other, LPE / 4);
+      }
+      float x = (b2 ? w2[1] : w2[0]) + __shfl_xor_sync(0xffffffffu, b2 ? w2[0] : w2[1], LPE / 8);
+#pragma unroll
+      for (int o = LPE / 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+      if (!ok[u]) continue;
+      if (writer) rbf_bar[(e0 + u * slots) * kk_n + kk] = old[u] + x;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        bacc[i] += gv[u][i];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) wacc[i][k] = fmaf(gv[u][i], r[u][k], wacc[i][k]);
+      }
+    }
+  }
+  // fixed-order reduction over the CTA's (warp, lane group) slots
+  float* mine = red[warp * EPW + grp];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int n = gl * 4 + i;
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      if (k < kk_n) mine[n * kk_n + k] = wacc[i][k];
+    mine[N * kk_n + n] = bacc[i];
+  }
+  __syncthreads();
+  for (int slot = threadIdx.x; slot < len; slot += 256) {
+    float t = 0.f;
+#pragma unroll
+    for (int w = 0; w < 8 * EPW; ++w) t += red[w][slot];
+    part[blockIdx.x * static_cast<int64_t>(len) + slot] = t;
+  }
+}
+
 // out1[i] = sum_p part[p][i] for i < split, out2[i - split] for i >= split (out2 may be
 // null): 8 warps split the parts, fixed-order combine (32 outputs per block).
 __global__ void reduce_parts_kernel(const float* __restrict__ part, int nparts, int len, int split,
@@ -551,9 +655,24 @@ int egn_rbf_linear_bwd(const float* rbf, int64_t num_edges, int k, const float* 
     if (b_bar) cudaMemsetAsync(b_bar, 0, sizeof(float) * n, st);
     return check_launch("rbf_linear_bwd_empty");
   }
-  const int grid = rbf_linear_bwd_grid(num_edges);
+  int grid = rbf_linear_bwd_grid(num_edges);
   float* part = reinterpret_cast<float*>(workspace);
-  rbf_linear_bwd_kernel<<<grid, 256, 0, st>>>(rbf, num_edges, k, w, n, g, ldg, rbf_bar, part);
+  const int lpe = n / 4;
+  const bool group_path = n % 4 == 0 && (lpe == 8 || lpe == 16 || lpe == 32) && ldg % 4 == 0 &&
+                          (reinterpret_cast<uintptr_t>(g) & 15) == 0;
+  if (group_path) {
+    // lane group per edge; grid sized to one wave (the workspace holds rbf_linear_bwd_grid rows)
+    grid = std::min(grid, k == 6 ? kNumSMs * 2 : kNumSMs);  // 98 / 136 registers per thread
+#define EGN_RLB(L)                                                                                      \
+    (k == 6 ? rbf_linear_bwd_group_kernel<L, 6><<<grid, 256, 0, st>>>(rbf, num_edges, k, w, n, g, ldg, rbf_bar, part) \
+            : rbf_linear_bwd_group_kernel<L, 8><<<grid, 256, 0, st>>>(rbf, num_edges, k, w, n, g, ldg, rbf_bar, part))
+    if (lpe == 32) EGN_RLB(32);
+    else if (lpe == 16) EGN_RLB(16);
+    else EGN_RLB(8);
+#undef EGN_RLB
+  } else {
+    rbf_linear_bwd_kernel<<<grid, 256, 0, st>>>(rbf, num_edges, k, w, n, g, ldg, rbf_bar, part);
+  }
   if (check_launch("rbf_linear_bwd")) return 1;
   // part rows are [n*k weights | n biases]
   const int len = n * k + n;
