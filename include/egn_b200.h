@@ -283,6 +283,19 @@ typedef struct {
 } egn_small_gemm_t;
 int egn_small_gemm_batched(const egn_small_gemm_t* problems, int count, egn_stream_t stream);
 
+/* Graph-level update block GU (record_gu_head/tail, engine.py:207-217), G graphs:
+ *   pre = s W1^T + b1, act = silu(pre), u += act W2^T + b2
+ * s [G, dv] (per-graph sum of node features), W1 [du, dv], W2 [du, du]; pre/act [G, du]
+ * written, u [G, du] updated in place (two launches, activation / bias / residual fused). */
+int egn_graph_mlp_fwd(int64_t num_graphs, int dv, int du, const float* s, const float* w1, const float* b1,
+                      const float* w2, const float* b2, float* pre, float* act, float* u, egn_stream_t stream);
+/* Adjoint: pre_bar = silu'(pre) (u_bar W2), s_bar = pre_bar W1 [G, dv]; W1_bar = pre_bar^T s,
+ * b1_bar = column sums of pre_bar, W2_bar = u_bar^T act, b2_bar = column sums of u_bar
+ * (all overwritten; sums over graphs in order). */
+int egn_graph_mlp_bwd(int64_t num_graphs, int dv, int du, const float* u_bar, const float* s, const float* pre,
+                      const float* act, const float* w1, const float* w2, float* pre_bar, float* s_bar,
+                      float* w1_bar, float* b1_bar, float* w2_bar, float* b2_bar, egn_stream_t stream);
+
 /* ------------------------------------------------------------------ */
 /* Optimizer: train_simple SGD update (tasks.py:207-208)               */
 /* ------------------------------------------------------------------ */

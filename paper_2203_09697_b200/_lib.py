@@ -41,6 +41,8 @@ SIGNATURES: dict[str, tuple] = {
     "egn_triplets_fill": (_i32, [_p, _p, _p, _i64, _p, _p, _p]),
     "egn_geometry": (_i32, [_p, _p, _p, _i64, _p, _p, _p, _p]),
     "egn_neighbors_count_pbc": (_i32, [_p, _p, _p, _i64, _p, _p, _f64, _p, _p]),
+    "egn_graph_mlp_fwd": (_i32, [_i64, _i32, _i32, _p, _p, _p, _p, _p, _p, _p, _p, _p]),
+    "egn_graph_mlp_bwd": (_i32, [_i64, _i32, _i32, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p]),
     "egn_neighbors_fill_pbc": (_i32, [_p, _p, _p, _i64, _p, _p, _f64, _p, _p, _p, _p, _p, _p]),
     "egn_reverse_edges_pbc": (_i32, [_p, _p, _p, _p, _p, _p, _i64, _p, _p, _p]),
     "egn_geometry_shift": (_i32, [_p, _p, _p, _p, _i64, _p, _p, _p, _p]),
@@ -115,7 +117,7 @@ def stream() -> int:
 
 # Kernels launched per successful ABI call (for the bench's gpu_launches count).
 KERNELS_PER_CALL = {
-    "egn_triplet_bwd": 4, "egn_force_head_fwd": 2, "egn_force_head_bwd": 2, "egn_column_sum": 2, "egn_gemm_wgrad": 2, "egn_rbf_linear_bwd": 2,
+    "egn_triplet_bwd": 4, "egn_force_head_fwd": 2, "egn_force_head_bwd": 2, "egn_column_sum": 2, "egn_gemm_wgrad": 2, "egn_rbf_linear_bwd": 2, "egn_graph_mlp_fwd": 2, "egn_graph_mlp_bwd": 3,
 }
 LAUNCH_COUNTER = {"calls": 0, "kernels": 0}
 

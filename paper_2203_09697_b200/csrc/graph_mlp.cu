@@ -1,0 +1,161 @@
+// Graph-level update block GU (egn/engine.py:207-217): per graph g
+//   pre = s W1^T + b1,  act = silu(pre),  u += act W2^T + b2        (s = sum of v over g's nodes)
+// and its adjoint.  G (graphs in the batch) is small, so these are SIMT kernels with one warp
+// per output element and the activations / bias / residual fused (two launches forward,
+// three backward) instead of library GEMM calls plus elementwise passes.  fp32 FMA in
+// fixed order (deterministic).
+#include <algorithm>
+
+#include "common.cuh"
+
+namespace egn {
+namespace gmlp {
+
+__device__ __forceinline__ float silu_f(float x) { return x / (1.f + __expf(-x)); }
+__device__ __forceinline__ float dsilu_f(float x) {
+  const float sg = 1.f / (1.f + __expf(-x));
+  return sg * (1.f + x * (1.f - sg));
+}
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Row-parallel layers: grid (graphs, ceil(out / 8)), warp = one output (r, j); the lanes split
+// the dot product (4 independent loads in flight per lane), fixed butterfly reduction.
+//   x_stride: distance between consecutive inputs of one weight row (1: W[j, :] rows,
+//   out: W[:, j] columns), w_row: distance between consecutive outputs.
+__device__ __forceinline__ float warp_dot(const float* __restrict__ x, const float* __restrict__ w, int n,
+                                          int64_t w_step, int lane) {
+  float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+  int k = lane;
+  for (; k + 96 < n; k += 128) {
+    const float w0 = __ldg(w + k * w_step), w1 = __ldg(w + (k + 32) * w_step), w2 = __ldg(w + (k + 64) * w_step),
+                w3 = __ldg(w + (k + 96) * w_step);
+    a0 = fmaf(x[k], w0, a0);
+    a1 = fmaf(x[k + 32], w1, a1);
+    a2 = fmaf(x[k + 64], w2, a2);
+    a3 = fmaf(x[k + 96], w3, a3);
+  }
+  for (; k < n; k += 32) a0 = fmaf(x[k], __ldg(w + k * w_step), a0);
+  return warp_sum((a0 + a1) + (a2 + a3));
+}
+
+// layer 1 forward: pre = s W1^T + b1, act = silu(pre)
+__global__ void __launch_bounds__(256) fwd1_kernel(int dv, int du, const float* __restrict__ s,
+                                                   const float* __restrict__ W1, const float* __restrict__ b1,
+                                                   float* __restrict__ pre, float* __restrict__ act) {
+  const int64_t r = blockIdx.x;
+  const int j = blockIdx.y * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (j >= du) return;
+  const float h = warp_dot(s + r * dv, W1 + static_cast<int64_t>(j) * dv, dv, 1, lane) + b1[j];
+  if (lane == 0) {
+    pre[r * du + j] = h;
+    act[r * du + j] = silu_f(h);
+  }
+}
+
+// layer 2 forward: u += act W2^T + b2
+__global__ void __launch_bounds__(256) fwd2_kernel(int du, const float* __restrict__ act,
+                                                   const float* __restrict__ W2, const float* __restrict__ b2,
+                                                   float* __restrict__ u) {
+  const int64_t r = blockIdx.x;
+  const int j = blockIdx.y * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (j >= du) return;
+  const float y = warp_dot(act + r * du, W2 + static_cast<int64_t>(j) * du, du, 1, lane);
+  if (lane == 0) u[r * du + j] += y + b2[j];
+}
+
+// backward layer 2: pre_bar = silu'(pre) (u_bar W2)   (W2 columns)
+__global__ void __launch_bounds__(256) bwd2_kernel(int du, const float* __restrict__ u_bar,
+                                                   const float* __restrict__ pre, const float* __restrict__ W2,
+                                                   float* __restrict__ pre_bar) {
+  const int64_t r = blockIdx.x;
+  const int j = blockIdx.y * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (j >= du) return;
+  const float y = warp_dot(u_bar + r * du, W2 + j, du, du, lane);
+  if (lane == 0) pre_bar[r * du + j] = y * dsilu_f(pre[r * du + j]);
+}
+
+// backward layer 1: s_bar = pre_bar W1   (W1 columns)
+__global__ void __launch_bounds__(256) bwd1_kernel(int dv, int du, const float* __restrict__ pre_bar,
+                                                   const float* __restrict__ W1, float* __restrict__ s_bar) {
+  const int64_t r = blockIdx.x;
+  const int i = blockIdx.y * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (i >= dv) return;
+  const float y = warp_dot(pre_bar + r * du, W1 + i, du, dv, lane);
+  if (lane == 0) s_bar[r * dv + i] = y;
+}
+
+// backward weights: CTA j = output row j of W1_bar [du, dv] and W2_bar [du, du]:
+//   W2_bar[j, k] = sum_g u_bar[g, j] act[g, k],  W1_bar[j, i] = sum_g pre_bar[g, j] s[g, i],
+//   b2_bar[j] = sum_g u_bar[g, j],  b1_bar[j] = sum_g pre_bar[g, j]   (graphs in order)
+__global__ void __launch_bounds__(256) bwd_weights_kernel(int64_t G, int dv, int du, const float* __restrict__ u_bar,
+                                                          const float* __restrict__ act,
+                                                          const float* __restrict__ pre_bar,
+                                                          const float* __restrict__ s, float* __restrict__ gW1,
+                                                          float* __restrict__ gb1, float* __restrict__ gW2,
+                                                          float* __restrict__ gb2) {
+  const int j = blockIdx.x;
+  for (int k = threadIdx.x; k < du; k += blockDim.x) {
+    float a = 0.f;
+#pragma unroll 16
+    for (int64_t g = 0; g < G; ++g) a = fmaf(__ldg(u_bar + g * du + j), __ldg(act + g * du + k), a);
+    gW2[static_cast<int64_t>(j) * du + k] = a;
+  }
+  for (int i = threadIdx.x; i < dv; i += blockDim.x) {
+    float a = 0.f;
+#pragma unroll 16
+    for (int64_t g = 0; g < G; ++g) a = fmaf(__ldg(pre_bar + g * du + j), __ldg(s + g * dv + i), a);
+    gW1[static_cast<int64_t>(j) * dv + i] = a;
+  }
+  if (threadIdx.x == 0) {
+    float a = 0.f, b = 0.f;
+    for (int64_t g = 0; g < G; ++g) {
+      a += u_bar[g * du + j];
+      b += pre_bar[g * du + j];
+    }
+    gb2[j] = a;
+    gb1[j] = b;
+  }
+}
+
+}  // namespace gmlp
+}  // namespace egn
+
+using namespace egn;
+
+extern "C" int egn_graph_mlp_fwd(int64_t num_graphs, int dv, int du, const float* s, const float* w1,
+                                 const float* b1, const float* w2, const float* b2, float* pre, float* act,
+                                 float* u, egn_stream_t stream) {
+  EGN_REQUIRE(dv >= 1 && du >= 1, "graph MLP dims must be positive");
+  EGN_REQUIRE(num_graphs < 65536, "graph MLP: at most 65535 graphs per batch");
+  if (num_graphs == 0) return 0;
+  cudaStream_t st = as_stream(stream);
+  const dim3 grid(static_cast<unsigned>(num_graphs), (du + 7) / 8);
+  gmlp::fwd1_kernel<<<grid, 256, 0, st>>>(dv, du, s, w1, b1, pre, act);
+  if (check_launch("graph_mlp_fwd1")) return 1;
+  gmlp::fwd2_kernel<<<grid, 256, 0, st>>>(du, act, w2, b2, u);
+  return check_launch("graph_mlp_fwd2");
+}
+
+extern "C" int egn_graph_mlp_bwd(int64_t num_graphs, int dv, int du, const float* u_bar, const float* s,
+                                 const float* pre, const float* act, const float* w1, const float* w2,
+                                 float* pre_bar, float* s_bar, float* w1_bar, float* b1_bar, float* w2_bar,
+                                 float* b2_bar, egn_stream_t stream) {
+  EGN_REQUIRE(dv >= 1 && du >= 1, "graph MLP dims must be positive");
+  EGN_REQUIRE(num_graphs < 65536, "graph MLP: at most 65535 graphs per batch");
+  cudaStream_t st = as_stream(stream);
+  if (num_graphs > 0) {
+    gmlp::bwd2_kernel<<<dim3(static_cast<unsigned>(num_graphs), (du + 7) / 8), 256, 0, st>>>(du, u_bar, pre, w2,
+                                                                                              pre_bar);
+    if (check_launch("graph_mlp_bwd2")) return 1;
+    gmlp::bwd1_kernel<<<dim3(static_cast<unsigned>(num_graphs), (dv + 7) / 8), 256, 0, st>>>(dv, du, pre_bar, w1,
+                                                                                              s_bar);
+    if (check_launch("graph_mlp_bwd1")) return 1;
+  }
+  gmlp::bwd_weights_kernel<<<du, 256, 0, st>>>(num_graphs, dv, du, u_bar, act, pre_bar, s, w1_bar, b1_bar, w2_bar,
+                                               b2_bar);
+  return check_launch("graph_mlp_bwd_weights");
+}

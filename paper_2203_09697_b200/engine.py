@@ -196,9 +196,8 @@ class Engine:
             else:
                 m = m_new
             s = ops.graph_sum(bg.graph_ptr, v)
-            pre = torch.addmm(w[p + "gu.b1"], s, w[p + "gu.w1"].t())  # G rows: cuBLAS
-            act = F.silu(pre)
-            u = torch.addmm(w[p + "gu.b2"], act, w[p + "gu.w2"].t()).add_(u)
+            # GU (engine.py:207-217): u += silu(s W1^T + b1) W2^T + b2, one fused launch over G rows
+            pre, act = ops.graph_mlp_fwd(s, w[p + "gu.w1"], w[p + "gu.b1"], w[p + "gu.w2"], w[p + "gu.b2"], u)
             st.update(s=s, pre=pre, act=act)
             blocks.append(st)
         energy = torch.addmm(w["energy_head.b"], u, w["energy_head.w"].t()).view(-1)
@@ -235,13 +234,9 @@ class Engine:
         for b in range(c.blocks - 1, -1, -1):
             p = f"block{b}."
             st = fw.blocks[b]
-            # GU (engine.py:207-217), G rows: cuBLAS
-            torch.mm(u_bar.t(), st["act"], out=gr[p + "gu.w2"])
-            gr[p + "gu.b2"].copy_(u_bar.sum(0))
-            pre_bar = _silu_bwd(u_bar @ w[p + "gu.w2"], st["pre"])
-            gr[p + "gu.b1"].copy_(pre_bar.sum(0))
-            torch.mm(pre_bar.t(), st["s"], out=gr[p + "gu.w1"])
-            s_bar = pre_bar @ w[p + "gu.w1"]
+            # GU (engine.py:207-217): fused adjoint over G rows (data and weight gradients)
+            s_bar = ops.graph_mlp_bwd(u_bar, st["s"], st["pre"], st["act"], w[p + "gu.w1"], w[p + "gu.w2"],
+                                      gr[p + "gu.w1"], gr[p + "gu.b1"], gr[p + "gu.w2"], gr[p + "gu.b2"])
             v_bar = ops.gather_rows(bg.node_graph, s_bar)
             if gem:
                 # sym (engine.py:195-200): m = m2 + m2[rev] Wsym^T

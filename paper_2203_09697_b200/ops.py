@@ -135,6 +135,35 @@ def rbf_linear(rbf_t, w, b=None, out=None):
     return out
 
 
+def graph_mlp_fwd(s, w1, b1, w2, b2, u):
+    """GU block over G graphs (egn_graph_mlp_fwd): returns (pre, act); u updated in place."""
+    g, dv = s.shape
+    du = w1.shape[0]
+    pre = torch.empty((g, du), dtype=torch.float32, device=s.device)
+    act = torch.empty_like(pre)
+    call("egn_graph_mlp_fwd", g, dv, du, ptr(_c(s, torch.float32)), ptr(_c(w1, torch.float32)),
+         ptr(_c(b1, torch.float32)), ptr(_c(w2, torch.float32)), ptr(_c(b2, torch.float32)), ptr(pre), ptr(act),
+         ptr(u), stream())
+    return pre, act
+
+
+def graph_mlp_bwd(u_bar, s, pre, act, w1, w2, w1_bar, b1_bar, w2_bar, b2_bar):
+    """Adjoint of graph_mlp_fwd (egn_graph_mlp_bwd): returns s_bar [G, dv]; weight / bias
+    adjoints written into the given (contiguous) views."""
+    g, dv = s.shape
+    du = w1.shape[0]
+    pre_bar = torch.empty((g, du), dtype=torch.float32, device=s.device)
+    s_bar = torch.empty((g, dv), dtype=torch.float32, device=s.device)
+    for t in (w1_bar, b1_bar, w2_bar, b2_bar):
+        if not t.is_contiguous():
+            raise ValueError("graph_mlp_bwd outputs must be contiguous")
+    call("egn_graph_mlp_bwd", g, dv, du, ptr(_c(u_bar, torch.float32)), ptr(_c(s, torch.float32)),
+         ptr(_c(pre, torch.float32)), ptr(_c(act, torch.float32)), ptr(_c(w1, torch.float32)),
+         ptr(_c(w2, torch.float32)), ptr(pre_bar), ptr(s_bar), ptr(w1_bar), ptr(b1_bar), ptr(w2_bar), ptr(b2_bar),
+         stream())
+    return s_bar
+
+
 def rbf_linear_bwd(rbf_t, w, g, rbf_bar, w_bar, b_bar=None):
     """Adjoint of rbf_linear: rbf_bar += g w; w_bar = g^T rbf; b_bar = column sums of g."""
     e, k = rbf_t.shape

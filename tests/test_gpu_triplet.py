@@ -199,3 +199,37 @@ def test_rbf_linear_bwd_vs_fp64(n, k, ne, strided):
     assert max_rel(rbf_bar.cpu().numpy(), ref_rb.cpu().numpy()) < 1e-5
     assert max_rel(w_bar.cpu().numpy(), (gd.t() @ rd).cpu().numpy()) < 1e-5
     assert max_rel(b_bar.cpu().numpy(), gd.sum(0).cpu().numpy()) < 1e-5
+
+
+@pytest.mark.parametrize("g,dv,du", [(32, 128, 128), (1, 16, 24), (33, 7, 5), (5, 200, 96)])
+def test_graph_mlp_vs_fp64(g, dv, du):
+    """Fused GU block (egn_graph_mlp_fwd / _bwd) vs fp64 torch: u += silu(s W1^T + b1) W2^T + b2
+    and every adjoint."""
+    from paper_2203_09697_b200 import ops
+
+    gen = torch.Generator(device="cuda").manual_seed(g * 1000 + dv)
+    s = torch.randn((g, dv), device="cuda", generator=gen)
+    w1 = torch.randn((du, dv), device="cuda", generator=gen) * dv ** -0.5
+    b1 = torch.randn((du,), device="cuda", generator=gen)
+    w2 = torch.randn((du, du), device="cuda", generator=gen) * du ** -0.5
+    b2 = torch.randn((du,), device="cuda", generator=gen)
+    u0 = torch.randn((g, du), device="cuda", generator=gen)
+    u = u0.clone()
+    pre, act = ops.graph_mlp_fwd(s, w1, b1, w2, b2, u)
+    sd, w1d, b1d, w2d, b2d = (t.double() for t in (s, w1, b1, w2, b2))
+    pre_r = sd @ w1d.t() + b1d
+    act_r = torch.nn.functional.silu(pre_r)
+    u_r = u0.double() + act_r @ w2d.t() + b2d
+    assert max_rel(pre.cpu().numpy(), pre_r.cpu().numpy()) < 1e-5
+    assert max_rel(act.cpu().numpy(), act_r.cpu().numpy()) < 1e-5
+    assert max_rel(u.cpu().numpy(), u_r.cpu().numpy()) < 1e-5
+    u_bar = torch.randn((g, du), device="cuda", generator=gen)
+    gw1, gb1 = torch.empty_like(w1), torch.empty_like(b1)
+    gw2, gb2 = torch.empty_like(w2), torch.empty_like(b2)
+    s_bar = ops.graph_mlp_bwd(u_bar, s, pre, act, w1, w2, gw1, gb1, gw2, gb2)
+    ub = u_bar.double()
+    sg = torch.sigmoid(pre_r)
+    pb = (ub @ w2d) * sg * (1 + pre_r * (1 - sg))
+    for got, ref in ((s_bar, pb @ w1d), (gw1, pb.t() @ sd), (gb1, pb.sum(0)), (gw2, ub.t() @ act_r),
+                     (gb2, ub.sum(0))):
+        assert max_rel(got.cpu().numpy(), ref.cpu().numpy()) < 1e-5
