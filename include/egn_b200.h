@@ -216,9 +216,11 @@ int egn_rbf_linear(const float* rbf, int64_t num_edges, int k, const float* w, c
                    int64_t ldo, egn_stream_t stream);
 /* Adjoint (linear VJP, tape.py:104-119) for N <= 128: rbf_bar[e,k] += sum_n g[e,n] w[n,k];
  * w_bar = g^T rbf (overwritten), b_bar = column sums of g (overwritten; NULL to skip);
- * deterministic (fixed-order partial reduction). */
+ * deterministic (fixed-order partial reduction).  g2 (NULL to skip, same row stride ldg):
+ * the adjoint of a gate product, g := g * g2 elementwise (engine.py:138/146 mul VJP). */
 int64_t egn_rbf_linear_bwd_workspace_bytes(int64_t num_edges, int k, int n);
 int egn_rbf_linear_bwd(const float* rbf, int64_t num_edges, int k, const float* w, int n, const float* g,
+                       const float* g2,
                        int64_t ldg, float* rbf_bar, float* w_bar, float* b_bar, void* workspace,
                        egn_stream_t stream);
 

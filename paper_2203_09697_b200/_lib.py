@@ -64,7 +64,7 @@ SIGNATURES: dict[str, tuple] = {
     "egn_force_head_bwd": (_i32, [_p, _p, _i64, _p, _i32, _p, _p, _p, _p, _p, _p, _p, _p]),
     "egn_rbf_linear": (_i32, [_p, _i64, _i32, _p, _p, _i32, _p, _i64, _p]),
     "egn_rbf_linear_bwd_workspace_bytes": (_i64, [_i64, _i32, _i32]),
-    "egn_rbf_linear_bwd": (_i32, [_p, _i64, _i32, _p, _i32, _p, _i64, _p, _p, _p, _p, _p]),
+    "egn_rbf_linear_bwd": (_i32, [_p, _i64, _i32, _p, _i32, _p, _p, _i64, _p, _p, _p, _p, _p]),
     "egn_rbf_bwd": (_i32, [_p, _p, _i64, _i32, _f64, _p, _p]),
     "egn_positions_bwd": (_i32, [_p, _p, _p, _i64, _p, _p, _p]),
     "egn_column_sum_workspace_bytes": (_i64, [_i64, _i32]),

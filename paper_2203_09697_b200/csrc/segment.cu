@@ -298,7 +298,8 @@ __global__ void rbf_linear_kernel(const float* __restrict__ rbf, int64_t ne, int
 constexpr int kRlTile = 32;
 __global__ void __launch_bounds__(256) rbf_linear_bwd_kernel(const float* __restrict__ rbf, int64_t ne, int K,
                                                              const float* __restrict__ W, int N,
-                                                             const float* __restrict__ g, int64_t ldg,
+                                                             const float* __restrict__ g,
+                                                             const float* __restrict__ g2, int64_t ldg,
                                                              float* __restrict__ rbf_bar, float* __restrict__ part) {
   __shared__ float ws[128 * 8];
   __shared__ float gs[kRlTile][129];
@@ -316,7 +317,7 @@ __global__ void __launch_bounds__(256) rbf_linear_bwd_kernel(const float* __rest
     __syncthreads();
     for (int i = tid; i < kRlTile * N; i += 256) {
       const int e = i / N, n = i - (i / N) * N;
-      gs[e][n] = e < te ? g[(e0 + e) * ldg + n] : 0.f;
+      gs[e][n] = e < te ? (g2 ? g[(e0 + e) * ldg + n] * g2[(e0 + e) * ldg + n] : g[(e0 + e) * ldg + n]) : 0.f;
     }
     for (int i = tid; i < kRlTile * K; i += 256) {
       const int e = i / K, k = i - (i / K) * K;
@@ -377,7 +378,8 @@ __global__ void __launch_bounds__(256) rbf_linear_bwd_kernel(const float* __rest
 template <int LPE, int KT>
 __global__ void __launch_bounds__(256) rbf_linear_bwd_group_kernel(const float* __restrict__ rbf, int64_t ne,
                                                                    int K, const float* __restrict__ W, int N,
-                                                                   const float* __restrict__ g, int64_t ldg,
+                                                                   const float* __restrict__ g,
+                                                                   const float* __restrict__ g2, int64_t ldg,
                                                                    float* __restrict__ rbf_bar,
                                                                    float* __restrict__ part) {
   constexpr int EPW = 32 / LPE;  // edges per warp instruction
@@ -411,7 +413,11 @@ __global__ void __launch_bounds__(256) rbf_linear_bwd_group_kernel(const float* 
       const int64_t e = e0 + u * slots;
       ok[u] = e < ne;
       const int64_t ec = ok[u] ? e : 0;
-      const float4 v = ok[u] ? __ldg(reinterpret_cast<const float4*>(g + ec * ldg + gl * 4)) : make_float4(0.f, 0.f, 0.f, 0.f);
+      float4 v = ok[u] ? __ldg(reinterpret_cast<const float4*>(g + ec * ldg + gl * 4)) : make_float4(0.f, 0.f, 0.f, 0.f);
+      if (g2 != nullptr && ok[u]) {  // g = g * g2 (fused elementwise product)
+        const float4 v2 = __ldg(reinterpret_cast<const float4*>(g2 + ec * ldg + gl * 4));
+        v.x *= v2.x; v.y *= v2.y; v.z *= v2.z; v.w *= v2.w;
+      }
       gv[u][0] = v.x; gv[u][1] = v.y; gv[u][2] = v.z; gv[u][3] = v.w;
 #pragma unroll
       for (int k = 0; k < 8; ++k) r[u][k] = (k < kk_n && ok[u]) ? __ldg(rbf + ec * kk_n + k) : 0.f;
@@ -696,7 +702,7 @@ int64_t egn_rbf_linear_bwd_workspace_bytes(int64_t num_edges, int k, int n) {
 }
 
 int egn_rbf_linear_bwd(const float* rbf, int64_t num_edges, int k, const float* w, int n, const float* g,
-                       int64_t ldg, float* rbf_bar, float* w_bar, float* b_bar, void* workspace,
+                       const float* g2, int64_t ldg, float* rbf_bar, float* w_bar, float* b_bar, void* workspace,
                        egn_stream_t stream) {
   EGN_REQUIRE(k >= 1 && k <= 8 && n >= 1 && n <= 128, "rbf_linear_bwd needs K <= 8, N <= 128");
   cudaStream_t st = as_stream(stream);
@@ -709,19 +715,19 @@ int egn_rbf_linear_bwd(const float* rbf, int64_t num_edges, int k, const float* 
   float* part = reinterpret_cast<float*>(workspace);
   const int lpe = n / 4;
   const bool group_path = n % 4 == 0 && (lpe == 8 || lpe == 16 || lpe == 32) && ldg % 4 == 0 &&
-                          (reinterpret_cast<uintptr_t>(g) & 15) == 0;
+                          (reinterpret_cast<uintptr_t>(g) & 15) == 0 && (reinterpret_cast<uintptr_t>(g2) & 15) == 0;
   if (group_path) {
     // lane group per edge; grid sized to one wave (the workspace holds rbf_linear_bwd_grid rows)
     grid = std::min(grid, k == 6 ? kNumSMs * 2 : kNumSMs);  // 98 / 136 registers per thread
 #define EGN_RLB(L)                                                                                      \
-    (k == 6 ? rbf_linear_bwd_group_kernel<L, 6><<<grid, 256, 0, st>>>(rbf, num_edges, k, w, n, g, ldg, rbf_bar, part) \
-            : rbf_linear_bwd_group_kernel<L, 8><<<grid, 256, 0, st>>>(rbf, num_edges, k, w, n, g, ldg, rbf_bar, part))
+    (k == 6 ? rbf_linear_bwd_group_kernel<L, 6><<<grid, 256, 0, st>>>(rbf, num_edges, k, w, n, g, g2, ldg, rbf_bar, part) \
+            : rbf_linear_bwd_group_kernel<L, 8><<<grid, 256, 0, st>>>(rbf, num_edges, k, w, n, g, g2, ldg, rbf_bar, part))
     if (lpe == 32) EGN_RLB(32);
     else if (lpe == 16) EGN_RLB(16);
     else EGN_RLB(8);
 #undef EGN_RLB
   } else {
-    rbf_linear_bwd_kernel<<<grid, 256, 0, st>>>(rbf, num_edges, k, w, n, g, ldg, rbf_bar, part);
+    rbf_linear_bwd_kernel<<<grid, 256, 0, st>>>(rbf, num_edges, k, w, n, g, g2, ldg, rbf_bar, part);
   }
   if (check_launch("rbf_linear_bwd")) return 1;
   // part rows are [n*k weights | n biases]

@@ -276,14 +276,14 @@ class Engine:
             if gem:
                 # Z_bar = Y_bar * g fused into the GEMM epilogue (second output Y_bar)
                 Z_bar, Y_bar = L(h_bar, st["W1u"], w_mn=True, aux=st["g"], flags=ops.EPI_MUL_AUX)
-                g_bar = Y_bar * st["Z"]
+                g_prod = (Y_bar, st["Z"])  # g_bar = Y_bar * Z, formed inside the adjoint kernel
                 wg(Z_bar, st["S"], gr[p + "tu.bilinear_proj"])
                 S_bar = L(Z_bar, w[p + "tu.bilinear_proj"], w_mn=True)
             else:
                 Y_bar = L(h_bar, st["W1u"], w_mn=True)
                 S_bar = Y_bar * st["g"]
-                g_bar = Y_bar * st["S"]
-            ops.rbf_linear_bwd(fw.rbf, w[p + "tu.rbf_gate"], g_bar, rbf_bar, gr[p + "tu.rbf_gate"])
+                g_prod = (Y_bar, st["S"])  # g_bar = Y_bar * S
+            ops.rbf_linear_bwd(fw.rbf, w[p + "tu.rbf_gate"], g_prod[0], rbf_bar, gr[p + "tu.rbf_gate"], g2=g_prod[1])
             X_bar, Wk_bar = ops.triplet_bwd(bg.edge_ptr, bg.rev, bg.geo, st["X"], st["Wk"], c.cutoff,
                                             S_bar, eg, max_degree=bg.max_deg)
             if gem:

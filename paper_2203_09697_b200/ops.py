@@ -164,13 +164,18 @@ def graph_mlp_bwd(u_bar, s, pre, act, w1, w2, w1_bar, b1_bar, w2_bar, b2_bar):
     return s_bar
 
 
-def rbf_linear_bwd(rbf_t, w, g, rbf_bar, w_bar, b_bar=None):
-    """Adjoint of rbf_linear: rbf_bar += g w; w_bar = g^T rbf; b_bar = column sums of g."""
+def rbf_linear_bwd(rbf_t, w, g, rbf_bar, w_bar, b_bar=None, g2=None):
+    """Adjoint of rbf_linear: rbf_bar += g w; w_bar = g^T rbf; b_bar = column sums of g.
+    g2 (same shape): the adjoint arrives as a product g * g2 (a gate's VJP), fused."""
     e, k = rbf_t.shape
     n = w.shape[0]
     if g.stride(1) != 1:
         g = g.contiguous()
+    if g2 is not None and (g2.stride(1) != 1 or g2.stride(0) != g.stride(0)):
+        g, g2 = (g * g2).contiguous(), None
     if k > 8 or n > 128:
+        if g2 is not None:
+            g = g * g2
         rbf_bar.addmm_(g, w)
         wgrad(g, rbf_t, out=w_bar)
         if b_bar is not None:
@@ -178,8 +183,9 @@ def rbf_linear_bwd(rbf_t, w, g, rbf_bar, w_bar, b_bar=None):
         return
     nbytes = call("egn_rbf_linear_bwd_workspace_bytes", e, k, n)
     ws = _workspace_named("rbflin", nbytes, g.device)
-    call("egn_rbf_linear_bwd", ptr(_c(rbf_t, torch.float32)), e, k, ptr(_c(w, torch.float32)), n, ptr(g), g.stride(0),
-         ptr(rbf_bar), ptr(w_bar), ptr(b_bar) if b_bar is not None else None, ptr(ws), stream())
+    call("egn_rbf_linear_bwd", ptr(_c(rbf_t, torch.float32)), e, k, ptr(_c(w, torch.float32)), n, ptr(g),
+         ptr(g2) if g2 is not None else None, g.stride(0), ptr(rbf_bar), ptr(w_bar),
+         ptr(b_bar) if b_bar is not None else None, ptr(ws), stream())
 
 
 def sbf(geo, edge_ptr, tri_ptr, num_triplets, k_rbf, l_sbf, cutoff):

@@ -177,9 +177,11 @@ def test_triplet_dimension_errors():
     assert torch.equal(S3[:, :256], S_lo)
 
 
-@pytest.mark.parametrize("n,k,ne,strided", [(128, 6, 5000, False), (64, 6, 3001, True), (32, 8, 777, False),
-                                            (48, 3, 1000, False), (8, 6, 513, False), (128, 1, 2, False)])
-def test_rbf_linear_bwd_vs_fp64(n, k, ne, strided):
+@pytest.mark.parametrize("n,k,ne,strided,prod", [(128, 6, 5000, False, False), (64, 6, 3001, True, False),
+                                                 (32, 8, 777, False, False), (48, 3, 1000, False, True),
+                                                 (8, 6, 513, False, False), (128, 1, 2, False, False),
+                                                 (64, 6, 4000, False, True)])
+def test_rbf_linear_bwd_vs_fp64(n, k, ne, strided, prod):
     """Basis-linear adjoint (warp-per-edge path for N = 32, 64, 128; tiled path otherwise):
     rbf_bar += g W, W_bar = g^T rbf, b_bar = column sums of g, vs fp64 torch."""
     from paper_2203_09697_b200 import ops
@@ -193,8 +195,11 @@ def test_rbf_linear_bwd_vs_fp64(n, k, ne, strided):
     rbf_bar = rbf_bar0.clone()
     w_bar = torch.empty((n, k), device="cuda")
     b_bar = torch.empty((n,), device="cuda")
-    ops.rbf_linear_bwd(rbf_t, w, g, rbf_bar, w_bar, b_bar)
+    g2 = torch.randn_like(g) if prod else None
+    ops.rbf_linear_bwd(rbf_t, w, g, rbf_bar, w_bar, b_bar, g2=g2)
     gd, rd, wd = g.double(), rbf_t.double(), w.double()
+    if prod:
+        gd = gd * g2.double()
     ref_rb = rbf_bar0.double() + gd @ wd
     assert max_rel(rbf_bar.cpu().numpy(), ref_rb.cpu().numpy()) < 1e-5
     assert max_rel(w_bar.cpu().numpy(), (gd.t() @ rd).cpu().numpy()) < 1e-5
