@@ -14,4 +14,10 @@ ncu --set full --import-source on --clock-control none -k regex:bw2_kernel -s 4 
 # tensor-core triplet kernels on the C5 deg-500, d_g 64 graph
 ncu --set full --import-source on --clock-control none -k regex:fwd_kernel -s 1 -c 1 -o gpurun_out/r1_tc_fwd python tools/c5_sweep.py --degrees 500 --dg 64 --iters 1 > gpurun_out/ncu5.log 2>&1
 ncu --set full --import-source on --clock-control none -k "regex:^(y_kernel|a_kernel)$" -c 2 -o gpurun_out/r1_tc_bwd python tools/c5_sweep.py --degrees 500 --dg 64 --iters 1 > gpurun_out/ncu6.log 2>&1
+
+# every GEMM call of one step (cold L2), relaxation driver timing
+python tools/gemm_census.py --out gpurun_out/gemm_census.txt > /dev/null 2>&1
+python tools/relax_bench.py > gpurun_out/relax.json 2>/dev/null
+python tools/relax_bench.py --variant dimenet-style >> gpurun_out/relax.json 2>/dev/null
+python tools/profile_step.py --out gpurun_out/step_kernels.txt > gpurun_out/prof.log 2>&1
 ls -la gpurun_out/
