@@ -247,14 +247,16 @@ constexpr int EW = 64;                     // output columns per accumulator war
 // parity), each warp 32 rows x 64 columns.  BN = 128 (N % 128 == 0): one group of 8
 // warps, warp = (row quarter, column half); one A k-block feeds N = 128 MMAs, which
 // run at twice the N = 64 rate per output column.
-template <int BN>
+// TRUNC (activation x weight products): the operand slot holds B_lo only (the raw tiles are
+// the hi parts), which leaves room for a deeper TMA ring.
+template <int BN, bool TRUNC = false>
 struct Cfg {
-  static constexpr int kTmaRing = BN == 64 ? 5 : 3;
+  static constexpr int kTmaRing = TRUNC ? (BN == 64 ? 6 : 4) : (BN == 64 ? 5 : 3);
   static constexpr int kOpRing = 2;
   static constexpr int kAccBufs = BN == 64 ? 2 : 3;  // TMEM window buffers per group
   static constexpr int kGroups = BN == 64 ? 2 : 1;
   static constexpr int kTmaSlot = BM * BK * 4 + BN * BK * 4;  // raw A + raw B k-block
-  static constexpr int kOpSlot = 2 * BN * BK * 4;             // B hi + lo
+  static constexpr int kOpSlot = (TRUNC ? 1 : 2) * BN * BK * 4;  // B lo (+ B hi)
   static constexpr size_t kSmem =
       static_cast<size_t>(kTmaRing) * kTmaSlot + kOpRing * kOpSlot + 8 * kEpiWarp + 1024;
   static_assert(kGroups * kAccBufs * BN + 64 * kOpRing <= 512, "TMEM columns");
@@ -300,7 +302,7 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_const
                    const __grid_constant__ CUtensorMap mapOp, Params P,
                    int tiles_n, int splits, int total_items) {
   constexpr int A_BYTES = BM * BK * 4;  // 16 KB raw A k-block
-  using C = Cfg<BN>;
+  using C = Cfg<BN, !AMN>;
   constexpr int kTmaRing = C::kTmaRing, kOpRing = C::kOpRing, kAccBufs = C::kAccBufs, kGroups = C::kGroups;
   constexpr int kTmaSlot = C::kTmaSlot, kOpSlot = C::kOpSlot;
   constexpr int B_BYTES = BN * BK * 4;  // 8 / 16 KB
@@ -329,6 +331,13 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_const
   }
 
   const uint32_t crank = P.mcast ? cluster_rank() : 0;
+  // Truncation split (activation x weight products, K-major A): the tensor core reads fp32
+  // operands as tf32 by truncation (tools/tf32_trunc_probe.cu), so the raw TMA tiles serve as
+  // the hi parts (A_hi B_hi and A_hi B_lo read A from shared memory); the split warps only
+  // form lo = x - trunc(x) (A_lo to TMEM, B_lo to shared memory) and the TMA slot stays until
+  // the k-block's MMAs complete.  Weight gradients (MN-major A read by the split warps) keep
+  // the rna hi / lo split.
+  constexpr bool trunc = !AMN;
   if (tid == 0) {
     // descriptor fetches off the critical path (the output map is first used at the end of a tile)
     asm volatile("prefetch.tensormap [%0];" ::"l"(&mapA0) : "memory");
@@ -448,7 +457,49 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_const
         const uint32_t bhi = smem_u32(opring + o * kOpSlot);
         const uint32_t blo = bhi + B_BYTES;
         const uint32_t ta = tmem + A_TMEM + o * 64;
-        if (win % (BK / 8) == 0) {
+        if (trunc) {
+          // raw A / B in the TMA slot are the hi parts; B_lo at the operand slot, A_lo in TMEM
+          const int s = it % kTmaRing;
+          const uint32_t araw = smem_u32(smem + s * kTmaSlot);
+          const uint32_t braw = araw + A_BYTES;
+          const uint32_t bl = bhi;  // B_lo
+          const bool fstart = wpos == 0;
+          if (fstart) {
+            bsel = fc % kAccBufs;
+            mbar_wait(&acce_bar[gr][bsel], ((fc / kAccBufs) & 1) ^ 1);
+            EGN_TRACE(12, wtr);
+            ++wtr;
+            asm volatile("tcgen05.fence::after_thread_sync;");
+            tacc = tg + bsel * BN;
+          }
+          j += BK / 8;
+          wpos += BK / 8;
+          const bool fend = (wpos >= win) || (j == nsteps);
+          if (elect_one()) {
+#pragma unroll
+            for (int k = 0; k < BK / 8; ++k) {  // small terms first
+              const uint32_t ob = BMN ? k * 1024 : k * 32;
+              const uint64_t db = BMN ? sw128_mnmajor_desc_u(braw + ob) : sw128_kmajor_desc_u(braw + ob);
+              const uint64_t dl = BMN ? sw128_mnmajor_desc_u(bl + ob) : sw128_kmajor_desc_u(bl + ob);
+              const uint64_t da = sw128_kmajor_desc_u(araw + k * 32);
+              mma_tf32_ta(tacc, ta + k * 8, db, idesc, (fstart && k == 0) ? 0u : 1u);  // A_lo B_hi
+              mma_tf32(tacc, da, dl, idesc, 1u);                                     // A_hi B_lo
+            }
+#pragma unroll
+            for (int k = 0; k < BK / 8; ++k) {
+              const uint32_t ob = BMN ? k * 1024 : k * 32;
+              const uint64_t db = BMN ? sw128_mnmajor_desc_u(braw + ob) : sw128_kmajor_desc_u(braw + ob);
+              mma_tf32(tacc, sw128_kmajor_desc_u(araw + k * 32), db, idesc, 1u);  // A_hi B_hi
+            }
+            if (fend) mma_commit(&accf_bar[gr][bsel]);
+            mma_commit(&tma_empty[s]);  // the raw tiles are free once these MMAs completed
+          }
+          __syncwarp();
+          if (fend) {
+            ++fc;
+            wpos = 0;
+          }
+        } else if (win % (BK / 8) == 0) {
           // windows of whole k-blocks: the 8 small products (lo x hi, hi x lo) of the
           // k-block go first into the window tile, the 4 big ones last, so only the big
           // terms accumulate at full magnitude (fewer truncations at large |acc|)
@@ -543,7 +594,33 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_const
         asm volatile("tcgen05.fence::after_thread_sync;");
         const uint8_t* st = smem + s * kTmaSlot;
         const uint32_t ta = tmem + lane_off + A_TMEM + o * 64;
-        if (!(P.dbg & 2)) {
+        if (trunc) {
+          // lo = x - trunc_tf32(x) only (the raw tiles are the hi parts)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            float lo[16];
+#pragma unroll
+            for (int g = 0; g < 4; ++g) {
+              const int gran = h * 4 + g;
+              const float4 v = *reinterpret_cast<const float4*>(st + r * 128 + ((gran ^ (r & 7)) << 4));
+              lo[g * 4 + 0] = v.x - __uint_as_float(__float_as_uint(v.x) & 0xffffe000u);
+              lo[g * 4 + 1] = v.y - __uint_as_float(__float_as_uint(v.y) & 0xffffe000u);
+              lo[g * 4 + 2] = v.z - __uint_as_float(__float_as_uint(v.z) & 0xffffe000u);
+              lo[g * 4 + 3] = v.w - __uint_as_float(__float_as_uint(v.w) & 0xffffe000u);
+            }
+            tmem_st16(ta + h * 16, lo);
+          }
+          const float4* braw = reinterpret_cast<const float4*>(st + A_BYTES);
+          float4* bl = reinterpret_cast<float4*>(opring + o * kOpSlot);
+#pragma unroll
+          for (int i = ct; i < B_BYTES / 16; i += 128) {
+            const float4 v = braw[i];
+            bl[i] = make_float4(v.x - __uint_as_float(__float_as_uint(v.x) & 0xffffe000u),
+                                v.y - __uint_as_float(__float_as_uint(v.y) & 0xffffe000u),
+                                v.z - __uint_as_float(__float_as_uint(v.z) & 0xffffe000u),
+                                v.w - __uint_as_float(__float_as_uint(v.w) & 0xffffe000u));
+          }
+        } else if (!(P.dbg & 2)) {
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           float hi[16], lo[16];
@@ -589,8 +666,10 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_const
         named_bar_sync(1, 128);
         if (ct == 0) {
           EGN_TRACE(3, it);
-          mbar_arrive(&tma_empty[s]);
-          if (P.mcast && crank == 1) mbar_arrive_remote(&tma_empty[s], 0);
+          if (!trunc) {  // (truncation split: the MMA commit releases the raw tiles)
+            mbar_arrive(&tma_empty[s]);
+            if (P.mcast && crank == 1) mbar_arrive_remote(&tma_empty[s], 0);
+          }
           mbar_arrive(&op_full[o]);
         }
       }
@@ -990,7 +1069,7 @@ template <bool AMN, bool BMN, int BN>
 static int launch(const CUtensorMap& a0, const CUtensorMap& b0, const CUtensorMap& a1, const CUtensorMap& b1,
                   const CUtensorMap& mo, const CUtensorMap& mo2, const CUtensorMap& mop, const Params& P, int splits,
                   cudaStream_t st) {
-  const size_t smem = Cfg<BN>::kSmem;
+  const size_t smem = Cfg<BN, !AMN>::kSmem;
   auto kern = gemm_tf32x3_kernel<AMN, BMN, BN>;
   static bool configured = false;
   if (!configured) {
@@ -1005,7 +1084,7 @@ static int launch(const CUtensorMap& a0, const CUtensorMap& b0, const CUtensorMa
   // Opt-in (EGN_GEMM_MCAST=1): measured slower at C2 shapes (the pair runs in lockstep and the
   // loader is latency-, not L2-bandwidth-bound), kept for the wider XL products.
   static const bool mc_enabled = [] { const char* e = std::getenv("EGN_GEMM_MCAST"); return e && e[0] == '1'; }();
-  if (!AMN && mc_enabled && tiles_n == 2 && splits == 1 && total >= 2) {
+  if (AMN && mc_enabled && tiles_n == 2 && splits == 1 && total >= 2) {  // (A multicast: split-K only)
     static int max_clusters = -1;
     if (max_clusters < 0) {
       cudaLaunchConfig_t qc = {};
