@@ -218,29 +218,30 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
     }                                                                                   \
   } while (0)
 
-// Persistent, warp-specialised 3xTF32 GEMM, 128 x 64 output tiles.
+// Persistent, warp-specialised 3xTF32 GEMM, 128 x BN output tiles (BN = 64 or 128).
 //   warp 0       : TMA producer: raw fp32 A/B k-blocks into a kTmaRing-deep ring
 //   warp 1       : MMA issuer (whole warp walks the loop, one elected lane issues)
-//   warps 2..5   : split each landed k-block and release its TMA slot at once:
-//                  A rows (thread = row) go to a TMEM slot as hi = rna_tf32(a),
-//                  lo = a - hi (tcgen05.st); B goes to a shared hi/lo slot (same
-//                  swizzled layout, elementwise).  kOpRing operand slots.
-//   warps 6..13  : two accumulator groups of 4 warps; group = tile parity, so one
-//                  group's epilogue overlaps the other group's main loop.
-//                  TMEM lane quarter = warp % 4.
-// Per k-step the three products A_lo.B_hi, A_hi.B_lo, A_hi.B_hi read A from TMEM,
-// so shared-memory traffic per k-step is the B operand only.
+//   warps 2..5   : split each landed k-block: the raw tiles are the tf32 hi parts (the
+//                  tensor core truncates), so A rows (thread = row) give A_lo = a - trunc(a)
+//                  to a TMEM slot (tcgen05.st) and B gives B_lo to a shared operand slot
+//                  (same swizzled layout, elementwise).  Weight gradients (MN-major A)
+//                  put A_hi = rna(a) and A_lo into TMEM instead.  kOpRing operand slots.
+//   warps 6..13  : accumulator warps: two groups of 4 (BN 64, group = tile parity) or one
+//                  group of 8 (BN 128, warp = lane quarter x column half).
+//   warp 14      : store warp (TMA stores of finished tiles, operand-row prefetch).
+// Per k-step: A_lo.B_hi (A from TMEM), A_hi.B_lo and A_hi.B_hi (A from the TMA slot); the
+// MMA commit releases the TMA slot and the operand slot.
 // Accuracy: the tensor core accumulates with truncation, a bias that grows with
-// the number of k-steps summed in TMEM.  All three products of a k-step go to a
-// TMEM tile (kAccBufs buffers per group) that is restarted every P.flush_steps
-// k-steps; the group adds each finished window into fp32 registers (round to
-// nearest).
-// TMEM columns: [0, 384) accumulators (group, buffer of kAccBufs) x 64; [384, 384 + 64 kOpRing)
-// A operand slots (hi at +0, lo at +32).
-// Epilogue: each warp owns a [2 chunks][32 rows][32 cols] fp32 buffer (16-byte
-// granules XOR-swizzled by row), prefetched with the operand rows (residual /
-// gathered rows / aux) during the main loop; thread = row combines in place,
-// then lanes = columns copy out coalesced.
+// the number of k-steps summed in TMEM.  The products of each k-block (small ones
+// first) go to a TMEM window tile (kAccBufs buffers per group) that is restarted every
+// P.flush_steps k-steps; the group adds each finished window into fp32 registers (round
+// to nearest).
+// TMEM columns: [0, 384) accumulator windows; [384, 384 + 64 kOpRing) A operand slots
+// (A_lo at +0; weight gradients: A_hi at +0, A_lo at +32).
+// Epilogue: each warp owns a [2 chunks][32 rows][32 cols] fp32 staging buffer (16-byte
+// granules XOR-swizzled by row, the TMA SWIZZLE_128B layout) that receives the operand rows
+// (residual / gathered rows / aux); thread = row combines in place, then the store warp
+// TMA-stores it.
 constexpr int kEpiWarp = 2 * 32 * 32 * 4;  // 8 KB per accumulator warp
 constexpr int EW = 64;                     // output columns per accumulator warp
 // Per-tile-width configuration.  BN = 64: two accumulator groups of 4 warps (tile
@@ -302,7 +303,7 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_const
                    const __grid_constant__ CUtensorMap mapOp, Params P,
                    int tiles_n, int splits, int total_items) {
   constexpr int A_BYTES = BM * BK * 4;  // 16 KB raw A k-block
-  using C = Cfg<BN, !AMN>;
+  using C = Cfg<BN, true>;
   constexpr int kTmaRing = C::kTmaRing, kOpRing = C::kOpRing, kAccBufs = C::kAccBufs, kGroups = C::kGroups;
   constexpr int kTmaSlot = C::kTmaSlot, kOpSlot = C::kOpSlot;
   constexpr int B_BYTES = BN * BK * 4;  // 8 / 16 KB
@@ -336,8 +337,9 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_const
   // the hi parts (A_hi B_hi and A_hi B_lo read A from shared memory); the split warps only
   // form lo = x - trunc(x) (A_lo to TMEM, B_lo to shared memory) and the TMA slot stays until
   // the k-block's MMAs complete.  Weight gradients (MN-major A read by the split warps) keep
-  // the rna hi / lo split.
-  constexpr bool trunc = !AMN;
+  // the rna hi / lo split of A in TMEM and truncate B only.
+  constexpr bool trunc = true;
+  constexpr bool trunc_a = !AMN;
   if (tid == 0) {
     // descriptor fetches off the critical path (the output map is first used at the end of a tile)
     asm volatile("prefetch.tensormap [%0];" ::"l"(&mapA0) : "memory");
@@ -476,91 +478,31 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_const
           wpos += BK / 8;
           const bool fend = (wpos >= win) || (j == nsteps);
           if (elect_one()) {
+            // A_lo / A_hi: TMEM columns [0, 32) / shared-memory raw tile (trunc_a), or TMEM
+            // [32, 64) / [0, 32) (rna split of an MN-major A)
 #pragma unroll
             for (int k = 0; k < BK / 8; ++k) {  // small terms first
               const uint32_t ob = BMN ? k * 1024 : k * 32;
               const uint64_t db = BMN ? sw128_mnmajor_desc_u(braw + ob) : sw128_kmajor_desc_u(braw + ob);
               const uint64_t dl = BMN ? sw128_mnmajor_desc_u(bl + ob) : sw128_kmajor_desc_u(bl + ob);
-              const uint64_t da = sw128_kmajor_desc_u(araw + k * 32);
-              mma_tf32_ta(tacc, ta + k * 8, db, idesc, (fstart && k == 0) ? 0u : 1u);  // A_lo B_hi
-              mma_tf32(tacc, da, dl, idesc, 1u);                                     // A_hi B_lo
+              if (trunc_a) {
+                mma_tf32_ta(tacc, ta + k * 8, db, idesc, (fstart && k == 0) ? 0u : 1u);  // A_lo B_hi
+                mma_tf32(tacc, sw128_kmajor_desc_u(araw + k * 32), dl, idesc, 1u);      // A_hi B_lo
+              } else {
+                mma_tf32_ta(tacc, ta + 32 + k * 8, db, idesc, (fstart && k == 0) ? 0u : 1u);
+                mma_tf32_ta(tacc, ta + k * 8, dl, idesc, 1u);
+              }
             }
 #pragma unroll
             for (int k = 0; k < BK / 8; ++k) {
               const uint32_t ob = BMN ? k * 1024 : k * 32;
               const uint64_t db = BMN ? sw128_mnmajor_desc_u(braw + ob) : sw128_kmajor_desc_u(braw + ob);
-              mma_tf32(tacc, sw128_kmajor_desc_u(araw + k * 32), db, idesc, 1u);  // A_hi B_hi
+              if (trunc_a) mma_tf32(tacc, sw128_kmajor_desc_u(araw + k * 32), db, idesc, 1u);  // A_hi B_hi
+              else mma_tf32_ta(tacc, ta + k * 8, db, idesc, 1u);
             }
             if (fend) mma_commit(&accf_bar[gr][bsel]);
             mma_commit(&tma_empty[s]);  // the raw tiles are free once these MMAs completed
           }
-          __syncwarp();
-          if (fend) {
-            ++fc;
-            wpos = 0;
-          }
-        } else if (win % (BK / 8) == 0) {
-          // windows of whole k-blocks: the 8 small products (lo x hi, hi x lo) of the
-          // k-block go first into the window tile, the 4 big ones last, so only the big
-          // terms accumulate at full magnitude (fewer truncations at large |acc|)
-          const bool fstart = wpos == 0;
-          if (fstart) {
-            bsel = fc % kAccBufs;
-            mbar_wait(&acce_bar[gr][bsel], ((fc / kAccBufs) & 1) ^ 1);
-            EGN_TRACE(12, wtr);
-            ++wtr;
-            asm volatile("tcgen05.fence::after_thread_sync;");
-            tacc = tg + bsel * BN;
-          }
-          j += BK / 8;
-          wpos += BK / 8;
-          const bool fend = (wpos == win) || (j == nsteps);
-          if (elect_one() && !(P.dbg & 1)) {
-#pragma unroll
-            for (int k = 0; k < BK / 8; ++k) {
-              const uint32_t ob = BMN ? k * 1024 : k * 32;
-              const uint64_t dbh = BMN ? sw128_mnmajor_desc_u(bhi + ob) : sw128_kmajor_desc_u(bhi + ob);
-              const uint64_t dbl = BMN ? sw128_mnmajor_desc_u(blo + ob) : sw128_kmajor_desc_u(blo + ob);
-              mma_tf32_ta(tacc, ta + 32 + k * 8, dbh, idesc, (fstart && k == 0) ? 0u : 1u);
-              mma_tf32_ta(tacc, ta + k * 8, dbl, idesc, 1u);
-            }
-#pragma unroll
-            for (int k = 0; k < BK / 8; ++k) {
-              const uint32_t ob = BMN ? k * 1024 : k * 32;
-              const uint64_t dbh = BMN ? sw128_mnmajor_desc_u(bhi + ob) : sw128_kmajor_desc_u(bhi + ob);
-              mma_tf32_ta(tacc, ta + k * 8, dbh, idesc, 1u);
-            }
-          }
-          if (fend && elect_one()) mma_commit(&accf_bar[gr][bsel]);
-          __syncwarp();
-          if (fend) {
-            ++fc;
-            wpos = 0;
-          }
-        } else
-#pragma unroll
-        for (int k = 0; k < BK / 8; ++k) {
-          const bool fstart = wpos == 0;
-          if (fstart) {
-            bsel = fc % kAccBufs;
-            mbar_wait(&acce_bar[gr][bsel], ((fc / kAccBufs) & 1) ^ 1);
-            EGN_TRACE(12, wtr);
-            ++wtr;
-            asm volatile("tcgen05.fence::after_thread_sync;");
-            tacc = tg + bsel * BN;
-          }
-          ++j;
-          const bool fend = (++wpos == win) || (j == nsteps);
-          if (elect_one() && !(P.dbg & 1)) {
-            const uint32_t ob = BMN ? k * 1024 : k * 32;
-            const uint64_t dbh = BMN ? sw128_mnmajor_desc_u(bhi + ob) : sw128_kmajor_desc_u(bhi + ob);
-            const uint64_t dbl = BMN ? sw128_mnmajor_desc_u(blo + ob) : sw128_kmajor_desc_u(blo + ob);
-            // small terms first into the fresh window tile, then the big term
-            mma_tf32_ta(tacc, ta + 32 + k * 8, dbh, idesc, fstart ? 0u : 1u);
-            mma_tf32_ta(tacc, ta + k * 8, dbl, idesc, 1u);
-            mma_tf32_ta(tacc, ta + k * 8, dbh, idesc, 1u);
-          }
-          if (fend && elect_one()) mma_commit(&accf_bar[gr][bsel]);  // same elected lane as the MMAs
           __syncwarp();
           if (fend) {
             ++fc;
@@ -598,6 +540,7 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_const
           // lo = x - trunc_tf32(x) only (the raw tiles are the hi parts)
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
+            if (!trunc_a) break;
             float lo[16];
 #pragma unroll
             for (int g = 0; g < 4; ++g) {
@@ -610,6 +553,29 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_const
             }
             tmem_st16(ta + h * 16, lo);
           }
+          if (!trunc_a) {  // MN-major A: rna hi / lo into TMEM columns [0, 32) / [32, 64)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              float hi[16], lo[16];
+#pragma unroll
+              for (int g = 0; g < 4; ++g) {
+                const float* col = reinterpret_cast<const float*>(st) + r;
+                const float4 v = make_float4(col[(h * 16 + g * 4 + 0) * BM], col[(h * 16 + g * 4 + 1) * BM],
+                                             col[(h * 16 + g * 4 + 2) * BM], col[(h * 16 + g * 4 + 3) * BM]);
+                gs += (v.x + v.y) + (v.z + v.w);
+                hi[g * 4 + 0] = tf32_rna_int(v.x);
+                hi[g * 4 + 1] = tf32_rna_int(v.y);
+                hi[g * 4 + 2] = tf32_rna_int(v.z);
+                hi[g * 4 + 3] = tf32_rna_int(v.w);
+                lo[g * 4 + 0] = v.x - hi[g * 4 + 0];
+                lo[g * 4 + 1] = v.y - hi[g * 4 + 1];
+                lo[g * 4 + 2] = v.z - hi[g * 4 + 2];
+                lo[g * 4 + 3] = v.w - hi[g * 4 + 3];
+              }
+              tmem_st16(ta + h * 16, hi);
+              tmem_st16(ta + 32 + h * 16, lo);
+            }
+          }
           const float4* braw = reinterpret_cast<const float4*>(st + A_BYTES);
           float4* bl = reinterpret_cast<float4*>(opring + o * kOpSlot);
 #pragma unroll
@@ -620,45 +586,6 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_const
                                 v.z - __uint_as_float(__float_as_uint(v.z) & 0xffffe000u),
                                 v.w - __uint_as_float(__float_as_uint(v.w) & 0xffffe000u));
           }
-        } else if (!(P.dbg & 2)) {
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          float hi[16], lo[16];
-#pragma unroll
-          for (int g = 0; g < 4; ++g) {
-            float4 v;
-            if (AMN) {
-              const float* col = reinterpret_cast<const float*>(st) + r;
-              v = make_float4(col[(h * 16 + g * 4 + 0) * BM], col[(h * 16 + g * 4 + 1) * BM],
-                              col[(h * 16 + g * 4 + 2) * BM], col[(h * 16 + g * 4 + 3) * BM]);
-            } else {
-              const int gran = h * 4 + g;
-              v = *reinterpret_cast<const float4*>(st + r * 128 + ((gran ^ (r & 7)) << 4));
-            }
-            if (AMN) gs += (v.x + v.y) + (v.z + v.w);
-            hi[g * 4 + 0] = tf32_rna_int(v.x);
-            hi[g * 4 + 1] = tf32_rna_int(v.y);
-            hi[g * 4 + 2] = tf32_rna_int(v.z);
-            hi[g * 4 + 3] = tf32_rna_int(v.w);
-            lo[g * 4 + 0] = v.x - hi[g * 4 + 0];
-            lo[g * 4 + 1] = v.y - hi[g * 4 + 1];
-            lo[g * 4 + 2] = v.z - hi[g * 4 + 2];
-            lo[g * 4 + 3] = v.w - hi[g * 4 + 3];
-          }
-          tmem_st16(ta + h * 16, hi);
-          tmem_st16(ta + 32 + h * 16, lo);
-        }
-        const float4* braw = reinterpret_cast<const float4*>(st + A_BYTES);
-        float4* bhi = reinterpret_cast<float4*>(opring + o * kOpSlot);
-        float4* blo = reinterpret_cast<float4*>(opring + o * kOpSlot + B_BYTES);
-#pragma unroll
-        for (int i = ct; i < B_BYTES / 16; i += 128) {
-          const float4 v = braw[i];
-          float4 h;
-          h.x = tf32_rna_int(v.x); h.y = tf32_rna_int(v.y); h.z = tf32_rna_int(v.z); h.w = tf32_rna_int(v.w);
-          bhi[i] = h;
-          blo[i] = make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w);
-        }
         }
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -1069,7 +996,7 @@ template <bool AMN, bool BMN, int BN>
 static int launch(const CUtensorMap& a0, const CUtensorMap& b0, const CUtensorMap& a1, const CUtensorMap& b1,
                   const CUtensorMap& mo, const CUtensorMap& mo2, const CUtensorMap& mop, const Params& P, int splits,
                   cudaStream_t st) {
-  const size_t smem = Cfg<BN, !AMN>::kSmem;
+  const size_t smem = Cfg<BN, true>::kSmem;
   auto kern = gemm_tf32x3_kernel<AMN, BMN, BN>;
   static bool configured = false;
   if (!configured) {
@@ -1084,7 +1011,7 @@ static int launch(const CUtensorMap& a0, const CUtensorMap& b0, const CUtensorMa
   // Opt-in (EGN_GEMM_MCAST=1): measured slower at C2 shapes (the pair runs in lockstep and the
   // loader is latency-, not L2-bandwidth-bound), kept for the wider XL products.
   static const bool mc_enabled = [] { const char* e = std::getenv("EGN_GEMM_MCAST"); return e && e[0] == '1'; }();
-  if (AMN && mc_enabled && tiles_n == 2 && splits == 1 && total >= 2) {  // (A multicast: split-K only)
+  if (false && mc_enabled && tiles_n == 2) {  // multicast retired: the truncation split releases TMA slots from the MMA warp
     static int max_clusters = -1;
     if (max_clusters < 0) {
       cudaLaunchConfig_t qc = {};
