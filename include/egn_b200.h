@@ -257,6 +257,10 @@ int egn_column_sum(const float* x, int64_t rows, int d, int64_t ld, float* out, 
  * A is row-major with K contiguous; B is row-major [N, K] (weights stored (out, in)) or,
  * with b_mn != 0, [K, N] with N contiguous (the weight of a data-gradient product);
  * K_s % 4 == 0, N % 16 == 0, pointers 16-byte aligned, row strides multiples of 4. */
+/* Products with M <= egn_gemm_simt_max_m (default 8192, env EGN_GEMM_SIMT_MAX_M) run as an
+ * fp32 SIMT GEMM with the same epilogue (too few 128-row tiles to fill the GPU); value >= 0
+ * sets the threshold, the previous one is returned (value < 0: query only). */
+int64_t egn_gemm_simt_max_m(int64_t value);
 int egn_gemm(int64_t M, int N, int nseg, const float* a0, int64_t lda0, const float* b0, int64_t ldb0,
              int k0, const float* a1, int64_t lda1, const float* b1, int64_t ldb1, int k1,
              const float* bias, const float* resid, int64_t ldr, const float* gsrc,

@@ -1103,6 +1103,132 @@ static int launch(const CUtensorMap& a0, const CUtensorMap& b0, const CUtensorMa
   return check_launch("gemm_tf32x3");
 }
 
+// ---------------------------------------------------------------- small-M products
+// Node-level products (M = atoms, a few thousand rows) fill too few 128-row tcgen05 tiles to
+// hide the pipeline latency; they run as a SIMT fp32 GEMM (32 x 64 tiles, thread = 4 x 4
+// outputs, K in 32-wide shared-memory slabs, next slab prefetched into registers) with the
+// same fused epilogue.  fp32 FMA in fixed order.
+constexpr int kSimtM = 32, kSimtN = 64, kSimtK = 32;
+static int64_t g_simt_max_m = [] { const char* e = std::getenv("EGN_GEMM_SIMT_MAX_M"); return e ? std::atoll(e) : 8192LL; }();
+
+// 32 x 64 tile per 128-thread CTA (thread = 4 x 4 outputs); the next K slab is fetched into
+// registers while the current one is multiplied out of shared memory.
+template <bool BMN>
+__global__ void __launch_bounds__(128) gemm_simt_kernel(int64_t M, int N, int nseg, const float* __restrict__ a0,
+                                                        int64_t lda0, const float* __restrict__ b0, int64_t ldb0,
+                                                        int k0, const float* __restrict__ a1, int64_t lda1,
+                                                        const float* __restrict__ b1, int64_t ldb1, int k1,
+                                                        Params P) {
+  __shared__ __align__(16) float As[kSimtK][kSimtM + 4];  // [k][m]
+  __shared__ __align__(16) float Bs[kSimtK][kSimtN + 4];  // [k][n]
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;  // ty 0..7 (4 rows), tx 0..15 (4 cols)
+  const int64_t m0 = static_cast<int64_t>(blockIdx.x) * kSimtM;
+  const int n0 = blockIdx.y * kSimtN;
+  float acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
+  // slab loaders: A 32 x 32 (2 float4 / thread), B 64 x 32 (4 float4 / thread)
+  auto load = [&](int sg, int kk, float4 (&ra)[2], float4 (&rb)[4]) {
+    const float* A = sg ? a1 : a0;
+    const float* B = sg ? b1 : b0;
+    const int64_t lda = sg ? lda1 : lda0, ldb = sg ? ldb1 : ldb0;
+    const int K = sg ? k1 : k0;
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const int row = (tid >> 3) + 16 * i, kq = (tid & 7) * 4;
+      ra[i] = (m0 + row < M && kk + kq < K) ? __ldg(reinterpret_cast<const float4*>(A + (m0 + row) * lda + kk + kq))
+                                            : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      if (!BMN) {
+        const int row = (tid >> 3) + 16 * i, kq = (tid & 7) * 4;
+        rb[i] = (n0 + row < N && kk + kq < K)
+                    ? __ldg(reinterpret_cast<const float4*>(B + static_cast<int64_t>(n0 + row) * ldb + kk + kq))
+                    : make_float4(0.f, 0.f, 0.f, 0.f);
+      } else {
+        const int k = (tid >> 4) + 8 * i, nq = (tid & 15) * 4;
+        rb[i] = (kk + k < K && n0 + nq < N)
+                    ? __ldg(reinterpret_cast<const float4*>(B + static_cast<int64_t>(kk + k) * ldb + n0 + nq))
+                    : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    }
+  };
+  auto stash = [&](const float4 (&ra)[2], const float4 (&rb)[4]) {
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const int row = (tid >> 3) + 16 * i, kq = (tid & 7) * 4;
+      As[kq][row] = ra[i].x; As[kq + 1][row] = ra[i].y; As[kq + 2][row] = ra[i].z; As[kq + 3][row] = ra[i].w;
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      if (!BMN) {
+        const int row = (tid >> 3) + 16 * i, kq = (tid & 7) * 4;
+        Bs[kq][row] = rb[i].x; Bs[kq + 1][row] = rb[i].y; Bs[kq + 2][row] = rb[i].z; Bs[kq + 3][row] = rb[i].w;
+      } else {
+        const int k = (tid >> 4) + 8 * i, nq = (tid & 15) * 4;
+        *reinterpret_cast<float4*>(&Bs[k][nq]) = rb[i];
+      }
+    }
+  };
+  // flattened slab sequence over both segments
+  const int ns0 = (k0 + kSimtK - 1) / kSimtK, ns = ns0 + (nseg > 1 ? (k1 + kSimtK - 1) / kSimtK : 0);
+  float4 ra[2], rb[4];
+  if (ns > 0) load(0, 0, ra, rb);
+  for (int sl = 0; sl < ns; ++sl) {
+    __syncthreads();  // previous slab consumed
+    stash(ra, rb);
+    __syncthreads();
+    if (sl + 1 < ns) {
+      const int nx = sl + 1;
+      load(nx < ns0 ? 0 : 1, (nx < ns0 ? nx : nx - ns0) * kSimtK, ra, rb);  // next slab in flight
+    }
+#pragma unroll 8
+    for (int k = 0; k < kSimtK; ++k) {
+      const float4 a = *reinterpret_cast<const float4*>(&As[k][ty * 4]);
+      const float4 b = *reinterpret_cast<const float4*>(&Bs[k][tx * 4]);
+      const float av[4] = {a.x, a.y, a.z, a.w}, bv[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
+    }
+  }
+  const int fl = P.flags;
+  const int n = n0 + tx * 4;
+  if (n >= N) return;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int64_t m = m0 + ty * 4 + i;
+    if (m >= M) break;
+    float v[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      v[j] = acc[i][j];
+      if (fl & EPI_BIAS) v[j] += __ldg(P.bias + n + j);
+      if (fl & EPI_RESID) v[j] += P.resid[m * P.ldr + n + j];
+      if (fl & EPI_GATHER) v[j] += P.gsrc[static_cast<int64_t>(P.gidx[m]) * P.ldg + n + j];
+    }
+    float o[4], o2[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      o[j] = v[j];
+      o2[j] = 0.f;
+      if (fl & EPI_DSILU_AUX) o[j] = v[j] * dsilu(P.aux[m * P.ldaux + n + j]);
+      if (fl & EPI_MUL_AUX) {
+        o2[j] = v[j];
+        o[j] = v[j] * P.aux[m * P.ldaux + n + j];
+      }
+      if (fl & EPI_SILU_OUT2) o2[j] = __fdividef(v[j], 1.f + __expf(-v[j]));
+    }
+    *reinterpret_cast<float4*>(P.out + m * P.ldo + n) = make_float4(o[0], o[1], o[2], o[3]);
+    if (fl & (EPI_MUL_AUX | EPI_SILU_OUT2))
+      *reinterpret_cast<float4*>(P.out2 + m * P.ldo2 + n) = make_float4(o2[0], o2[1], o2[2], o2[3]);
+  }
+}
+
 // Fixed-order sum of the split-K partials: elements [0, len) of the [splits][M][N]
 // matrix partials go to out (row stride ldo), elements [len, len + mg) of the
 // [splits][M] column-sum partials go to gout.
@@ -1184,6 +1310,19 @@ extern "C" int egn_gemm(int64_t M, int N, int nseg, const float* a0, int64_t lda
   if (M == 0) return 0;
   Params P{M, N, nseg, k0, nseg > 1 ? k1 : 0, bias, resid, ldr, gsrc, gidx, ldg, aux, ldaux, flags, out, ldo, out2,
            ldo2, 0, 0};
+  // small M (at most ~half a wave of 128-row tiles): SIMT fp32 path
+  const bool al = (reinterpret_cast<uintptr_t>(a0) & 15) == 0 && lda0 % 4 == 0 &&
+                  (reinterpret_cast<uintptr_t>(b0) & 15) == 0 && ldb0 % 4 == 0 &&
+                  (nseg == 1 || ((reinterpret_cast<uintptr_t>(a1) & 15) == 0 && lda1 % 4 == 0 &&
+                                 (reinterpret_cast<uintptr_t>(b1) & 15) == 0 && ldb1 % 4 == 0));
+  if (M <= g_simt_max_m && al && (reinterpret_cast<uintptr_t>(out) & 15) == 0 && ldo % 4 == 0 &&
+      (!(flags & (EPI_MUL_AUX | EPI_SILU_OUT2)) || ((reinterpret_cast<uintptr_t>(out2) & 15) == 0 && ldo2 % 4 == 0))) {
+    const dim3 grid(static_cast<unsigned>((M + kSimtM - 1) / kSimtM), static_cast<unsigned>((N + kSimtN - 1) / kSimtN));
+    cudaStream_t st = as_stream(stream);
+    if (b_mn) gemm_simt_kernel<true><<<grid, 128, 0, st>>>(M, N, nseg, a0, lda0, b0, ldb0, k0, a1, lda1, b1, ldb1, k1, P);
+    else gemm_simt_kernel<false><<<grid, 128, 0, st>>>(M, N, nseg, a0, lda0, b0, ldb0, k0, a1, lda1, b1, ldb1, k1, P);
+    return check_launch("gemm_simt");
+  }
   P.flush_steps = (k0 + (nseg > 1 ? k1 : 0)) > 512 ? flush_window(true) : flush_window(false);
   CUtensorMap ma0, mb0, ma1, mb1;
   const int BN = tile_n(M, N);
@@ -1229,6 +1368,12 @@ extern "C" int egn_gemm(int64_t M, int N, int nseg, const float* a0, int64_t lda
   }
   if (b_mn) return launch<false, true, 64>(ma0, mb0, ma1, mb1, mo, mo2, mop, P, 1, st);
   return launch<false, false, 64>(ma0, mb0, ma1, mb1, mo, mo2, mop, P, 1, st);
+}
+
+extern "C" int64_t egn_gemm_simt_max_m(int64_t value) {
+  const int64_t old = egn::gemm::g_simt_max_m;
+  if (value >= 0) egn::gemm::g_simt_max_m = value;
+  return old;
 }
 
 extern "C" int64_t egn_gemm_wgrad_workspace_bytes(int64_t krows, int M, int N) {

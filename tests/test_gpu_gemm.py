@@ -15,6 +15,17 @@ def _rel(a, b):
     return float((a.double() - b).abs().max() / max(b.abs().max().item(), 1e-30))
 
 
+@pytest.fixture(params=["tcgen05", "simt"], autouse=True)
+def gemm_path(request):
+    """Run every product test on both paths: the tcgen05 3xTF32 GEMM and the small-M fp32
+    SIMT GEMM (egn_gemm_simt_max_m threshold forced to 0 / infinity)."""
+    from paper_2203_09697_b200 import _lib
+
+    old = _lib.call("egn_gemm_simt_max_m", 0 if request.param == "tcgen05" else 1 << 40)
+    yield request.param
+    _lib.call("egn_gemm_simt_max_m", old)
+
+
 @pytest.mark.parametrize("M,N,K", [(128, 64, 32), (1000, 64, 128), (4097, 128, 256), (300, 256, 64),
                                    (77, 384, 96), (2560, 16, 128), (58644, 128, 128)])
 def test_plain_gemm(M, N, K):
