@@ -1229,6 +1229,76 @@ __global__ void __launch_bounds__(128) gemm_simt_kernel(int64_t M, int N, int ns
   }
 }
 
+// Weight gradient over few rows (node rows): out[z][m][n] = sum_{r in split z} g[r][m] x[r][n]
+// as an fp32 SIMT product (32 x 64 output tile per 128-thread CTA, 32-row slabs, next slab
+// prefetched into registers), plus the split's column sums of g (n-block 0 only); the
+// partials are summed by reduce_splits_kernel in fixed order.
+__global__ void __launch_bounds__(128) wgrad_simt_kernel(int64_t R, int M, int N, const float* __restrict__ g,
+                                                         int64_t ldg, const float* __restrict__ x, int64_t ldx,
+                                                         int rows_per_split, float* __restrict__ part,
+                                                         float* __restrict__ gpart) {
+  __shared__ __align__(16) float As[kSimtK][kSimtM + 4];  // [r][m]
+  __shared__ __align__(16) float Bs[kSimtK][kSimtN + 4];  // [r][n]
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  const int tiles_m = (M + kSimtM - 1) / kSimtM;
+  const int m0 = (blockIdx.x % tiles_m) * kSimtM;
+  const int n0 = (blockIdx.x / tiles_m) * kSimtN;
+  const int z = blockIdx.y;
+  const int64_t r_beg = static_cast<int64_t>(z) * rows_per_split;
+  const int64_t r_end = r_beg + rows_per_split < R ? r_beg + rows_per_split : R;
+  float acc[4][4], cs[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
+  auto load = [&](int64_t r0, float4 (&ra)[2], float4 (&rb)[4]) {
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {  // g slab [32 r][32 m]
+      const int r = (tid >> 3) + 16 * i, mq = (tid & 7) * 4;
+      ra[i] = (r0 + r < r_end && m0 + mq < M) ? __ldg(reinterpret_cast<const float4*>(g + (r0 + r) * ldg + m0 + mq))
+                                              : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {  // x slab [32 r][64 n]
+      const int r = (tid >> 4) + 8 * i, nq = (tid & 15) * 4;
+      rb[i] = (r0 + r < r_end && n0 + nq < N) ? __ldg(reinterpret_cast<const float4*>(x + (r0 + r) * ldx + n0 + nq))
+                                              : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  };
+  float4 ra[2], rb[4];
+  if (r_beg < r_end) load(r_beg, ra, rb);
+  for (int64_t r0 = r_beg; r0 < r_end; r0 += kSimtK) {
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < 2; ++i) *reinterpret_cast<float4*>(&As[(tid >> 3) + 16 * i][(tid & 7) * 4]) = ra[i];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) *reinterpret_cast<float4*>(&Bs[(tid >> 4) + 8 * i][(tid & 15) * 4]) = rb[i];
+    __syncthreads();
+    if (r0 + kSimtK < r_end) load(r0 + kSimtK, ra, rb);
+#pragma unroll 8
+    for (int k = 0; k < kSimtK; ++k) {
+      const float4 a = *reinterpret_cast<const float4*>(&As[k][ty * 4]);
+      const float4 b = *reinterpret_cast<const float4*>(&Bs[k][tx * 4]);
+      const float av[4] = {a.x, a.y, a.z, a.w}, bv[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        cs[i] += av[i];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
+      }
+    }
+  }
+  float* out = part + static_cast<int64_t>(z) * M * N;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int m = m0 + ty * 4 + i;
+    const int n = n0 + tx * 4;
+    if (m < M && n < N) *reinterpret_cast<float4*>(out + static_cast<int64_t>(m) * N + n) =
+        make_float4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
+    if (gpart != nullptr && n0 == 0 && tx == 0 && m < M) gpart[static_cast<int64_t>(z) * M + m] = cs[i];
+  }
+}
+
 // Fixed-order sum of the split-K partials: elements [0, len) of the [splits][M][N]
 // matrix partials go to out (row stride ldo), elements [len, len + mg) of the
 // [splits][M] column-sum partials go to gout.
@@ -1399,6 +1469,21 @@ extern "C" int egn_gemm_wgrad(int64_t krows, int M, int N, const float* g, int64
   int splits, kbps;
   wgrad_split(krows, M, N, &splits, &kbps);
   float* part = reinterpret_cast<float*>(workspace);
+  if (krows <= g_simt_max_m && (reinterpret_cast<uintptr_t>(g) & 15) == 0 && ldg % 4 == 0 &&
+      (reinterpret_cast<uintptr_t>(x) & 15) == 0 && ldx % 4 == 0 && M % 4 == 0) {
+    // few rows: SIMT fp32 partials over the same split plan (workspace sized by wgrad_split)
+    const int rps = static_cast<int>((krows + splits - 1) / splits);
+    float* gpart_s = part + static_cast<int64_t>(splits) * M * N;
+    const dim3 grid(static_cast<unsigned>(((M + kSimtM - 1) / kSimtM) * ((N + kSimtN - 1) / kSimtN)),
+                    static_cast<unsigned>(splits));
+    wgrad_simt_kernel<<<grid, 128, 0, st>>>(krows, M, N, g, ldg, x, ldx, rps, part, g_colsum ? gpart_s : nullptr);
+    if (check_launch("gemm_wgrad_simt")) return 1;
+    const int64_t len = static_cast<int64_t>(M) * N;
+    const int mg = g_colsum ? M : 0;
+    reduce_splits_kernel<<<static_cast<int>(std::min<int64_t>((len + mg + 31) / 32, 4096)), 256, 0, st>>>(
+        part, splits, len, N, out, ldo, gpart_s, mg, g_colsum, accumulate);
+    return check_launch("gemm_wgrad_reduce");
+  }
   Params P{M, N, 1, static_cast<int>(krows), 0, nullptr, nullptr, 0, nullptr, nullptr, 0, nullptr, 0, 0,
            part, N, nullptr, 0, kbps, flush_window(true), 0, nullptr, 0, static_cast<int64_t>(M) * N};
   CUtensorMap ma, mb;
