@@ -88,7 +88,8 @@ __global__ void __launch_bounds__(256) bwd1_kernel(int dv, int du, const float* 
   if (lane == 0) s_bar[r * dv + i] = y;
 }
 
-// backward weights: CTA j = output row j of W1_bar [du, dv] and W2_bar [du, du]:
+// backward weights: CTA (j, layer): row j of W2_bar [du, du] (layer 0) or W1_bar [du, dv]
+// (layer 1) and the bias entry j:
 //   W2_bar[j, k] = sum_g u_bar[g, j] act[g, k],  W1_bar[j, i] = sum_g pre_bar[g, j] s[g, i],
 //   b2_bar[j] = sum_g u_bar[g, j],  b1_bar[j] = sum_g pre_bar[g, j]   (graphs in order)
 __global__ void __launch_bounds__(256) bwd_weights_kernel(int64_t G, int dv, int du, const float* __restrict__ u_bar,
@@ -98,26 +99,36 @@ __global__ void __launch_bounds__(256) bwd_weights_kernel(int64_t G, int dv, int
                                                           float* __restrict__ gb1, float* __restrict__ gW2,
                                                           float* __restrict__ gb2) {
   const int j = blockIdx.x;
-  for (int k = threadIdx.x; k < du; k += blockDim.x) {
-    float a = 0.f;
-#pragma unroll 16
-    for (int64_t g = 0; g < G; ++g) a = fmaf(__ldg(u_bar + g * du + j), __ldg(act + g * du + k), a);
-    gW2[static_cast<int64_t>(j) * du + k] = a;
-  }
-  for (int i = threadIdx.x; i < dv; i += blockDim.x) {
-    float a = 0.f;
-#pragma unroll 16
-    for (int64_t g = 0; g < G; ++g) a = fmaf(__ldg(pre_bar + g * du + j), __ldg(s + g * dv + i), a);
-    gW1[static_cast<int64_t>(j) * dv + i] = a;
-  }
-  if (threadIdx.x == 0) {
-    float a = 0.f, b = 0.f;
-    for (int64_t g = 0; g < G; ++g) {
-      a += u_bar[g * du + j];
-      b += pre_bar[g * du + j];
+  const bool l2 = blockIdx.y == 0;
+  const float* lhs = l2 ? u_bar : pre_bar;  // [G, du], column j
+  const float* rhs = l2 ? act : s;          // [G, width]
+  const int width = l2 ? du : dv;
+  float* gw = l2 ? gW2 : gW1;
+  // graphs in chunks of 8 with every load of a chunk issued before its FMAs (explicit ILP:
+  // the sequential accumulation chain alone serialises the loads)
+  for (int k = threadIdx.x; k < width; k += blockDim.x) {
+    float a = 0.f, bsum = 0.f;
+    int g = 0;
+    for (; g + 8 <= G; g += 8) {
+      float l[8], r[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        l[u] = __ldg(lhs + static_cast<int64_t>(g + u) * du + j);
+        r[u] = __ldg(rhs + static_cast<int64_t>(g + u) * width + k);
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        a = fmaf(l[u], r[u], a);
+        bsum += l[u];
+      }
     }
-    gb2[j] = a;
-    gb1[j] = b;
+    for (; g < G; ++g) {
+      const float l = __ldg(lhs + static_cast<int64_t>(g) * du + j);
+      a = fmaf(l, __ldg(rhs + static_cast<int64_t>(g) * width + k), a);
+      bsum += l;
+    }
+    gw[static_cast<int64_t>(j) * width + k] = a;
+    if (k == 0) (l2 ? gb2 : gb1)[j] = bsum;
   }
 }
 
@@ -155,7 +166,7 @@ extern "C" int egn_graph_mlp_bwd(int64_t num_graphs, int dv, int du, const float
                                                                                               s_bar);
     if (check_launch("graph_mlp_bwd1")) return 1;
   }
-  gmlp::bwd_weights_kernel<<<du, 256, 0, st>>>(num_graphs, dv, du, u_bar, act, pre_bar, s, w1_bar, b1_bar, w2_bar,
-                                               b2_bar);
+  gmlp::bwd_weights_kernel<<<dim3(du, 2), 256, 0, st>>>(num_graphs, dv, du, u_bar, act, pre_bar, s, w1_bar, b1_bar,
+                                                         w2_bar, b2_bar);
   return check_launch("graph_mlp_bwd_weights");
 }

@@ -192,25 +192,104 @@ __global__ void edge_dot_kernel(const float* __restrict__ m, int64_t ne, int d,
   }
 }
 
-// forces[v] = sum over in-edges e of v of scale[e] u_e
-__global__ void force_gather_kernel(const int64_t* __restrict__ edge_ptr,
-                                    const int32_t* __restrict__ rev,
-                                    const float4* __restrict__ geo, int64_t nv,
-                                    const float* __restrict__ scale, float* __restrict__ forces) {
-  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nv;
-       v += (int64_t)gridDim.x * blockDim.x) {
+// forces[v] = sum over in-edges e of v of scale[e] u_e: warp per node, lanes over the in-edges
+// (32 at a time), fixed butterfly reduction
+__global__ void force_gather_warp_kernel(const int64_t* __restrict__ edge_ptr, const int32_t* __restrict__ rev,
+                                         const float4* __restrict__ geo, int64_t nv, const float* __restrict__ scale,
+                                         float* __restrict__ forces) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t v = warp; v < nv; v += nwarps) {
     float fx = 0.f, fy = 0.f, fz = 0.f;
-    for (int64_t e = edge_ptr[v]; e < edge_ptr[v + 1]; ++e) {
-      int64_t ie = rev[e];
-      float s = scale[ie];
-      float4 g = geo[ie];
-      fx += s * g.x;
-      fy += s * g.y;
-      fz += s * g.z;
+    for (int64_t e = edge_ptr[v] + lane; e < edge_ptr[v + 1]; e += 32) {
+      const int64_t ie = rev[e];
+      const float sc = scale[ie];
+      const float4 g = geo[ie];
+      fx = fmaf(sc, g.x, fx);
+      fy = fmaf(sc, g.y, fy);
+      fz = fmaf(sc, g.z, fz);
     }
-    forces[3 * v + 0] = fx;
-    forces[3 * v + 1] = fy;
-    forces[3 * v + 2] = fz;
+    fx = warp_sum(fx);
+    fy = warp_sum(fy);
+    fz = warp_sum(fz);
+    if (lane == 0) {
+      forces[3 * v + 0] = fx;
+      forces[3 * v + 1] = fy;
+      forces[3 * v + 2] = fz;
+    }
+  }
+}
+
+// Adjoint of the force head, lane group per edge (LPE = d / 4 lanes, float4 columns), two
+// edges in flight: m_bar += sbar w, edge_grad += unit-vector adjoint, w_bar partial per CTA
+// (fixed-order sum over the CTA's lane groups).  sbar = f_bar[recv] . u.
+template <int LPE>
+__global__ void __launch_bounds__(256) force_bwd_group_kernel(const int32_t* __restrict__ recv,
+                                                              const float4* __restrict__ geo, int64_t ne,
+                                                              const float* __restrict__ m, int d,
+                                                              const float* __restrict__ w,
+                                                              const float* __restrict__ scale,
+                                                              const float* __restrict__ fbar,
+                                                              float* __restrict__ mbar, float* __restrict__ wpart,
+                                                              float4* __restrict__ edge_grad) {
+  constexpr int EPW = 32 / LPE;
+  __shared__ float red[8 * EPW][4 * LPE];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int grp = lane / LPE, gl = lane % LPE;
+  const float4 wv = make_float4(__ldg(w + gl * 4), __ldg(w + gl * 4 + 1), __ldg(w + gl * 4 + 2), __ldg(w + gl * 4 + 3));
+  float4 wacc = make_float4(0.f, 0.f, 0.f, 0.f);
+  const int64_t slots = static_cast<int64_t>(gridDim.x) * 8 * EPW;
+  const int64_t my = (static_cast<int64_t>(blockIdx.x) * 8 + warp) * EPW + grp;
+  for (int64_t e0 = my; e0 - grp < ne; e0 += 2 * slots) {
+    float4 g[2], mv[2], mb[2];
+    float sb[2];
+    bool ok[2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int64_t e = e0 + u * slots;
+      ok[u] = e < ne;
+      const int64_t ec = ok[u] ? e : 0;
+      g[u] = geo[ec];
+      const int64_t v = recv[ec];
+      sb[u] = ok[u] ? (fbar[3 * v] * g[u].x + fbar[3 * v + 1] * g[u].y + fbar[3 * v + 2] * g[u].z) : 0.f;
+      mv[u] = ok[u] ? __ldg(reinterpret_cast<const float4*>(m + ec * d) + gl) : make_float4(0.f, 0.f, 0.f, 0.f);
+      mb[u] = ok[u] ? reinterpret_cast<const float4*>(mbar + ec * d)[gl] : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      if (!ok[u]) continue;
+      const int64_t e = e0 + u * slots;
+      const float s = sb[u];
+      reinterpret_cast<float4*>(mbar + e * d)[gl] =
+          make_float4(fmaf(s, wv.x, mb[u].x), fmaf(s, wv.y, mb[u].y), fmaf(s, wv.z, mb[u].z), fmaf(s, wv.w, mb[u].w));
+      wacc.x = fmaf(s, mv[u].x, wacc.x);
+      wacc.y = fmaf(s, mv[u].y, wacc.y);
+      wacc.z = fmaf(s, mv[u].z, wacc.z);
+      wacc.w = fmaf(s, mv[u].w, wacc.w);
+      if (gl == 0) {
+        const int64_t v = recv[e];
+        const float bx = fbar[3 * v], by = fbar[3 * v + 1], bz = fbar[3 * v + 2];
+        const float sc = scale[e];
+        // units_bar = scale * fbar; d(unit)/d(v) adjoint: (ub - (ub.u) u) / d
+        const float ux = sc * bx, uy = sc * by, uz = sc * bz;
+        const float pr = ux * g[u].x + uy * g[u].y + uz * g[u].z;
+        const float inv = 1.f / g[u].w;
+        float4 eg = edge_grad[e];
+        eg.x += (ux - pr * g[u].x) * inv;
+        eg.y += (uy - pr * g[u].y) * inv;
+        eg.z += (uz - pr * g[u].z) * inv;
+        edge_grad[e] = eg;
+      }
+    }
+  }
+  *reinterpret_cast<float4*>(&red[warp * EPW + grp][gl * 4]) = wacc;
+  __syncthreads();
+  for (int c = threadIdx.x; c < d; c += 256) {
+    float t = 0.f;
+#pragma unroll
+    for (int r = 0; r < 8 * EPW; ++r) t += red[r][c];
+    wpart[blockIdx.x * static_cast<int64_t>(d) + c] = t;
   }
 }
 
@@ -524,25 +603,35 @@ __global__ void rbf_bwd_kernel(const float4* __restrict__ geo, const float* __re
   }
 }
 
-// pos_bar[a] = sum_{e in out(a)} (g_{rev e} - g_e), g_e = grad_v(e) + dd_e * u_e.
-__global__ void positions_bwd_kernel(const int64_t* __restrict__ edge_ptr,
-                                     const int32_t* __restrict__ rev,
-                                     const float4* __restrict__ geo, int64_t nv,
-                                     const float4* __restrict__ eg, double* __restrict__ pos_bar) {
-  for (int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a < nv;
-       a += (int64_t)gridDim.x * blockDim.x) {
+// pos_bar[a] = sum_{e in out(a)} (g_{rev e} - g_e), g_e = grad_v(e) + dd_e * u_e: warp per
+// atom, lanes over the out-edges, fp64 partials, fixed butterfly reduction
+__global__ void positions_bwd_warp_kernel(const int64_t* __restrict__ edge_ptr, const int32_t* __restrict__ rev,
+                                          const float4* __restrict__ geo, int64_t nv, const float4* __restrict__ eg,
+                                          double* __restrict__ pos_bar) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t a = warp; a < nv; a += nwarps) {
     double sx = 0.0, sy = 0.0, sz = 0.0;
-    for (int64_t e = edge_ptr[a]; e < edge_ptr[a + 1]; ++e) {
-      int64_t ie = rev[e];
-      float4 gi = eg[ie], ui = geo[ie];
-      float4 go = eg[e], uo = geo[e];
+    for (int64_t e = edge_ptr[a] + lane; e < edge_ptr[a + 1]; e += 32) {
+      const int64_t ie = rev[e];
+      const float4 gi = eg[ie], ui = geo[ie];
+      const float4 go = eg[e], uo = geo[e];
       sx += (double)fmaf(gi.w, ui.x, gi.x) - (double)fmaf(go.w, uo.x, go.x);
       sy += (double)fmaf(gi.w, ui.y, gi.y) - (double)fmaf(go.w, uo.y, go.y);
       sz += (double)fmaf(gi.w, ui.z, gi.z) - (double)fmaf(go.w, uo.z, go.z);
     }
-    pos_bar[3 * a + 0] = sx;
-    pos_bar[3 * a + 1] = sy;
-    pos_bar[3 * a + 2] = sz;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      sx += __shfl_xor_sync(0xffffffffu, sx, o);
+      sy += __shfl_xor_sync(0xffffffffu, sy, o);
+      sz += __shfl_xor_sync(0xffffffffu, sz, o);
+    }
+    if (lane == 0) {
+      pos_bar[3 * a + 0] = sx;
+      pos_bar[3 * a + 1] = sy;
+      pos_bar[3 * a + 2] = sz;
+    }
   }
 }
 
@@ -649,7 +738,7 @@ int egn_force_head_fwd(const int64_t* edge_ptr, const int32_t* rev, const float*
     edge_dot_kernel<<<grid_for(num_edges * 32, 256), 256, 0, st>>>(m, num_edges, d, w, scale);
     if (check_launch("force_head_dot")) return 1;
   }
-  force_gather_kernel<<<grid_for(num_nodes, 128), 128, 0, st>>>(
+  force_gather_warp_kernel<<<grid_for(num_nodes * 32, 256), 256, 0, st>>>(
       edge_ptr, rev, reinterpret_cast<const float4*>(geo), num_nodes, scale, forces);
   return check_launch("force_head_gather");
 }
@@ -670,6 +759,19 @@ int egn_force_head_bwd(const int32_t* recv, const float* geo, int64_t num_edges,
   }
   int grid = grid_for(num_edges * 32, 256, 148 * 2);
   float* part = reinterpret_cast<float*>(workspace);
+  const int lpe = d / 4;
+  if (d % 4 == 0 && (lpe == 8 || lpe == 16 || lpe == 32) && (reinterpret_cast<uintptr_t>(m) & 15) == 0 &&
+      (reinterpret_cast<uintptr_t>(m_bar) & 15) == 0) {
+    // lane group per edge; one partial row per CTA (the workspace holds grid * 8 rows)
+    const auto* g4 = reinterpret_cast<const float4*>(geo);
+    auto* eg4 = reinterpret_cast<float4*>(edge_grad);
+    if (lpe == 32) force_bwd_group_kernel<32><<<grid, 256, 0, st>>>(recv, g4, num_edges, m, d, w, scale, f_bar, m_bar, part, eg4);
+    else if (lpe == 16) force_bwd_group_kernel<16><<<grid, 256, 0, st>>>(recv, g4, num_edges, m, d, w, scale, f_bar, m_bar, part, eg4);
+    else force_bwd_group_kernel<8><<<grid, 256, 0, st>>>(recv, g4, num_edges, m, d, w, scale, f_bar, m_bar, part, eg4);
+    if (check_launch("force_head_bwd")) return 1;
+    reduce_parts_kernel<<<(d + 31) / 32, 256, 0, st>>>(part, grid, d, d, w_bar, nullptr);
+    return check_launch("force_head_bwd_reduce");
+  }
   for (int c0 = 0; c0 < d; c0 += 512) {
     force_bwd_kernel<<<grid, 256, 0, st>>>(recv, reinterpret_cast<const float4*>(geo), num_edges, m, d, c0, w,
                                            scale, f_bar, m_bar, part, reinterpret_cast<float4*>(edge_grad));
@@ -749,7 +851,7 @@ int egn_positions_bwd(const int64_t* edge_ptr, const int32_t* rev, const float* 
                       int64_t num_nodes, const float* edge_grad, double* pos_bar,
                       egn_stream_t stream) {
   if (num_nodes == 0) return 0;
-  positions_bwd_kernel<<<grid_for(num_nodes, 128), 128, 0, as_stream(stream)>>>(
+  positions_bwd_warp_kernel<<<grid_for(num_nodes * 32, 256), 256, 0, as_stream(stream)>>>(
       edge_ptr, rev, reinterpret_cast<const float4*>(geo), num_nodes,
       reinterpret_cast<const float4*>(edge_grad), pos_bar);
   return check_launch("positions_bwd");
