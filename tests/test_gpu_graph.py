@@ -165,3 +165,18 @@ def test_aggregate_in_edges_vs_numpy(d):
     ref = np.stack([xe[rev[ptr[v]:ptr[v + 1]]].sum(axis=0) if ptr[v + 1] > ptr[v] else np.zeros(d)
                     for v in range(bg.num_nodes)])
     assert max_rel(out, ref) < 1e-5
+
+
+@pytest.mark.parametrize("d,rows,acc", [(128, 1001, False), (128, 1000, True), (64, 7, True), (6, 33, False)])
+def test_gather_rows_vs_torch(d, rows, acc):
+    """out[r] (+)= x[idx[r]] (16-byte path for d % 4 == 0, odd row counts, accumulate)."""
+    from paper_2203_09697_b200 import ops
+
+    g = torch.Generator(device="cuda").manual_seed(d + rows)
+    x = torch.randn((500, d), device="cuda", generator=g)
+    idx = torch.randint(0, 500, (rows,), device="cuda", generator=g, dtype=torch.int32)
+    base = torch.randn((rows, d), device="cuda", generator=g)
+    out = base.clone()
+    ops.gather_rows(idx, x, out=out, accumulate=acc)
+    ref = (base if acc else 0) + x[idx.long()]
+    assert torch.equal(out, ref)
