@@ -306,6 +306,11 @@ int egn_graph_mlp_bwd(int64_t num_graphs, int dv, int du, const float* u_bar, co
 /* Optimizer: train_simple SGD update (tasks.py:207-208)               */
 /* ------------------------------------------------------------------ */
 int egn_sgd(float* w, const float* g, int64_t n, float lr, egn_stream_t stream);
+/* AdamW step t >= 1 over a flat parameter buffer (the
+ * reference documents it only): decoupled weight decay, bias-corrected first / second moments
+ * m, v (caller-owned, zero before step 1), torch.optim.AdamW's update order. */
+int egn_adamw(float* w, const float* g, float* m, float* v, int64_t n, float lr, float beta1, float beta2,
+              float eps, float weight_decay, int64_t step, egn_stream_t stream);
 
 #ifdef __cplusplus
 }

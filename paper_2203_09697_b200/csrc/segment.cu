@@ -3,6 +3,7 @@
 // atomics), so results are deterministic and match the reference's
 // ascending-edge accumulation order (receiver_plan, engine.py:78-90).
 #include <algorithm>
+#include <cmath>
 
 #include "common.cuh"
 
@@ -658,6 +659,24 @@ __global__ void column_sum_partial_kernel(const float* __restrict__ x, int64_t r
   }
 }
 
+// AdamW (decoupled weight decay; torch.optim.AdamW's update order):
+//   w *= 1 - lr wd;  m += (1 - b1)(g - m);  v = b2 v + (1 - b2) g^2;
+//   w -= (lr / bc1) m / (sqrt(v) / sqrt(bc2) + eps),  bc = 1 - beta^t
+__global__ void adamw_kernel(float* __restrict__ w, const float* __restrict__ g, float* __restrict__ m,
+                             float* __restrict__ v, int64_t n, float lr, float b1, float b2, float eps, float wd,
+                             float step_size, float bc2_sqrt) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const float gi = g[i];
+    float p = w[i] * (1.f - lr * wd);
+    const float mi = m[i] + (1.f - b1) * (gi - m[i]);
+    const float vi = v[i] * b2 + (1.f - b2) * gi * gi;
+    m[i] = mi;
+    v[i] = vi;
+    p -= step_size * (mi / (sqrtf(vi) / bc2_sqrt + eps));
+    w[i] = p;
+  }
+}
+
 __global__ void sgd_kernel(float* __restrict__ w, const float* __restrict__ g, int64_t n, float lr) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
@@ -875,6 +894,18 @@ int egn_column_sum(const float* x, int64_t rows, int d, int64_t ld, float* out, 
   if (check_launch("column_sum_partial")) return 1;
   reduce_parts_kernel<<<(d + 31) / 32, 256, 0, st>>>(part, chunks, d, d, out, nullptr);
   return check_launch("column_sum_reduce");
+}
+
+int egn_adamw(float* w, const float* g, float* m, float* v, int64_t n, float lr, float beta1, float beta2,
+              float eps, float weight_decay, int64_t step, egn_stream_t stream) {
+  EGN_REQUIRE(step >= 1, "adamw step count starts at 1");
+  if (n == 0) return 0;
+  const double bc1 = 1.0 - std::pow(static_cast<double>(beta1), static_cast<double>(step));
+  const double bc2 = 1.0 - std::pow(static_cast<double>(beta2), static_cast<double>(step));
+  adamw_kernel<<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(w, g, m, v, n, lr, beta1, beta2, eps, weight_decay,
+                                                                static_cast<float>(lr / bc1),
+                                                                static_cast<float>(std::sqrt(bc2)));
+  return check_launch("adamw");
 }
 
 int egn_sgd(float* w, const float* g, int64_t n, float lr, egn_stream_t stream) {

@@ -85,6 +85,15 @@ class DeviceWeights:
         """w -= lr * g (tasks.py:207-208)."""
         ops.sgd_(self.flat, self.grad_flat, lr)
 
+    def adamw_(self, lr: float, betas=(0.9, 0.999), eps: float = 1e-8, weight_decay: float = 1e-2) -> None:
+        """One AdamW step over the flat buffer (moments allocated on first use)."""
+        if not hasattr(self, "_adam_m"):
+            self._adam_m = torch.zeros_like(self.flat)
+            self._adam_v = torch.zeros_like(self.flat)
+            self._adam_t = 0
+        self._adam_t += 1
+        ops.adamw_(self.flat, self.grad_flat, self._adam_m, self._adam_v, lr, self._adam_t, betas, eps, weight_decay)
+
 
 @dataclass
 class ForwardResult:

@@ -530,3 +530,9 @@ def small_gemms(problems):
 
 def sgd_(w, g, lr):
     call("egn_sgd", ptr(w), ptr(g), w.numel(), float(lr), stream())
+
+
+def adamw_(w, g, m, v, lr, step, betas=(0.9, 0.999), eps=1e-8, weight_decay=1e-2):
+    """In-place AdamW step `step` (>= 1) on flat fp32 buffers (egn_adamw)."""
+    call("egn_adamw", ptr(w), ptr(g), ptr(m), ptr(v), w.numel(), float(lr), float(betas[0]), float(betas[1]),
+         float(eps), float(weight_decay), int(step), stream())

@@ -147,7 +147,8 @@ class Trainer:
 
     def __init__(self, params: ModelParams, systems, e_target, f_target=None, w_energy=1.0,
                  w_forces=0.0, device="cuda", graph: BatchGraph | None = None, comm=None,
-                 global_graphs: int | None = None, cuda_graph: bool = False):
+                 global_graphs: int | None = None, cuda_graph: bool = False, optimizer: str = "sgd",
+                 adamw: dict | None = None):
         """comm / global_graphs: graph-aligned graph parallelism.  Every rank owns
         whole graphs (its own BatchGraph), so no edge or node crosses a rank; the
         loss is normalised over the global batch (egn/tasks.py:158-185) and the
@@ -156,6 +157,13 @@ class Trainer:
         if w_forces != 0.0 and c.variant != GEMNET:
             raise ValueError("force-loss gradients require the force-centric variant; "
                              "set w_forces=0 for energy-centric training")
+        if optimizer not in ("sgd", "adamw"):
+            raise ValueError(f"optimizer must be 'sgd' or 'adamw', got {optimizer!r}")
+        # sgd: the reference update (tasks.py:207-208); adamw: SURVEY 8(f) f4 (betas, eps,
+        # weight_decay in `adamw`, torch.optim.AdamW defaults otherwise)
+        self.optimizer = optimizer
+        self.adamw = {"betas": (0.9, 0.999), "eps": 1e-8, "weight_decay": 1e-2}
+        self.adamw.update(adamw or {})
         self.config = c
         self.weights = DeviceWeights.from_params(params, device)
         self.engine = Engine(self.weights)
@@ -211,7 +219,10 @@ class Trainer:
                                   level="global")
             self.comm.all_reduce_(loss, phase="backward", block=-1, stage="loss", level="global")
         if lr != 0.0:
-            self.weights.sgd_(lr)
+            if self.optimizer == "adamw":
+                self.weights.adamw_(lr, **self.adamw)
+            else:
+                self.weights.sgd_(lr)
         return loss
 
     def step(self, lr: float) -> torch.Tensor:

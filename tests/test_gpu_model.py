@@ -349,3 +349,47 @@ def test_periodic_lattice_translation_invariance():
     e1, f1 = predict(AtomicSystem(moved, np.full(7, 6), cell=cell, pbc=(True, True, True)), params)
     assert abs(e1 - e0) <= 1e-5 * max(abs(e0), 1.0)
     assert max_rel(f1, f0) < 1e-4
+
+
+def test_adamw_step_matches_torch_and_numpy():
+    """egn_adamw vs torch.optim.AdamW (fp32) and an fp64 numpy restatement over 5 steps."""
+    from paper_2203_09697_b200 import ops
+
+    g0 = torch.Generator(device="cuda").manual_seed(5)
+    n = 100_003
+    w = torch.randn(n, device="cuda", generator=g0)
+    w_ref = w.clone().requires_grad_(True)
+    m = torch.zeros_like(w)
+    v = torch.zeros_like(w)
+    opt = torch.optim.AdamW([w_ref], lr=3e-3, betas=(0.9, 0.99), eps=1e-7, weight_decay=0.05)
+    wn = w.double().cpu().numpy()
+    mn = np.zeros(n)
+    vn = np.zeros(n)
+    for t in range(1, 6):
+        grad = torch.randn(n, device="cuda", generator=g0)
+        ops.adamw_(w, grad, m, v, 3e-3, t, (0.9, 0.99), 1e-7, 0.05)
+        w_ref.grad = grad.clone()
+        opt.step()
+        gn = grad.double().cpu().numpy()
+        wn = wn * (1 - 3e-3 * 0.05)
+        mn = 0.9 * mn + 0.1 * gn
+        vn = 0.99 * vn + 0.01 * gn * gn
+        wn = wn - 3e-3 / (1 - 0.9 ** t) * mn / (np.sqrt(vn) / np.sqrt(1 - 0.99 ** t) + 1e-7)
+    assert max_rel(w.cpu().numpy(), w_ref.detach().cpu().numpy()) < 1e-6
+    assert max_rel(w.cpu().numpy(), wn) < 1e-5
+
+
+def test_trainer_adamw_reduces_loss():
+    from paper_2203_09697_b200 import ModelConfig, init_params
+    from paper_2203_09697_b200.tasks import Trainer
+
+    gd = load_golden("train_gemnet.npz")
+    cfg = ModelConfig.from_json(str(gd["config"]))
+    systems = [gd[f"pos{i}"] for i in range(3)]
+    e_t = [float(gd[f"e{i}"]) for i in range(3)]
+    f_t = np.concatenate([gd[f"f{i}"] for i in range(3)])
+    tr = Trainer(init_params(cfg), systems, e_t, f_t, 1.0, 0.5, optimizer="adamw", adamw={"weight_decay": 0.0})
+    losses = [float(tr.step(1e-3)) for _ in range(8)]
+    assert losses[-1] < losses[0]
+    with pytest.raises(ValueError):
+        Trainer(init_params(cfg), systems, e_t, f_t, 1.0, 0.5, optimizer="lamb")
