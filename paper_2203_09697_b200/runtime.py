@@ -43,7 +43,7 @@ from .engine import DeviceWeights, ForwardResult, _silu_bwd
 from .graph import BatchGraph
 from .partition import CenterPartition, partition_centers
 
-ALLOWED_LEVELS = frozenset({"edge", "node", "global", "position", "param"})
+ALLOWED_LEVELS = frozenset({"edge", "node", "global", "position", "param", "replica"})
 
 
 class CollectiveError(RuntimeError):
@@ -147,8 +147,39 @@ class LocalComm(Comm):
         return full[int(bounds[0]):int(bounds[1])]
 
 
+def gp_dp_layout(world: int, gp: int) -> tuple[list, list]:
+    """GP x DP composition (pkg/README.md "Scaling notes"): `world` ranks
+    as world / gp data-parallel replicas of `gp` graph-parallel workers.  Replica k owns ranks
+    [k gp, (k + 1) gp); the DP group of worker index i is {i, i + gp, i + 2 gp, ...}.
+    Returns (gp_groups, dp_groups) as rank lists."""
+    if gp < 1 or world % gp:
+        raise ValueError(f"world size {world} is not a multiple of the graph-parallel size {gp}")
+    gp_groups = [list(range(k * gp, (k + 1) * gp)) for k in range(world // gp)]
+    dp_groups = [list(range(i, world, gp)) for i in range(gp)]
+    return gp_groups, dp_groups
+
+
 class DistComm(Comm):
     """torch.distributed process group (NCCL on GPUs, gloo on CPU)."""
+
+    @classmethod
+    def gp_dp(cls, gp: int, log=None) -> tuple["DistComm", "DistComm"]:
+        """This rank's (graph-parallel, data-parallel) communicators of gp_dp_layout; every rank
+        must call it (torch.distributed.new_group is collective)."""
+        import torch.distributed as dist
+
+        rank, world = dist.get_rank(), dist.get_world_size()
+        gp_groups, dp_groups = gp_dp_layout(world, gp)
+        mine_gp = mine_dp = None
+        for ranks in gp_groups:
+            g = dist.new_group(ranks)
+            if rank in ranks:
+                mine_gp = g
+        for ranks in dp_groups:
+            g = dist.new_group(ranks)
+            if rank in ranks:
+                mine_dp = g
+        return cls(mine_gp, log), cls(mine_dp, log)
 
     def __init__(self, group=None, log=None):
         import torch.distributed as dist
@@ -576,12 +607,16 @@ class GPTrainer:
     the loss value is all-reduced for reporting."""
 
     def __init__(self, params, bg: BatchGraph, e_target, f_target, w_energy: float, w_forces: float, comm: Comm,
-                 part: CenterPartition, device="cuda"):
+                 part: CenterPartition, device="cuda", dp_comm: Comm | None = None, global_graphs: int | None = None):
+        """dp_comm / global_graphs: GP x DP composition -- this replica's graphs are part of a
+        global batch of `global_graphs`; after the graph-parallel backward the parameter
+        gradient and the loss are all-reduced across the replicas (gp_dp_layout)."""
         self.config = params.config
         self.bg, self.comm, self.part = bg, comm, part
+        self.dp_comm = dp_comm
         self.weights = DeviceWeights.from_params(params, device)
         self.engine = GraphParallelEngine(self.weights, comm, part)
-        self.n = bg.num_graphs
+        self.n = bg.num_graphs if global_graphs is None else int(global_graphs)
         self.e_target = torch.as_tensor(np.asarray(e_target), dtype=torch.float64, device=bg.device)
         n0, n1 = self.engine.n0, self.engine.n1
         self.f_target = (torch.as_tensor(np.asarray(f_target), dtype=torch.float64, device=bg.device)[n0:n1]
@@ -604,6 +639,10 @@ class GPTrainer:
             d_f = 2.0 * self.w_forces * delta / (self.n * self.atom_count[:, None])
         self.engine.backward(self.bg, fw, d_e, d_f)
         self.comm.all_reduce_(loss, phase="backward", block=-1, stage="loss", level="global")
+        if self.dp_comm is not None:
+            self.dp_comm.all_reduce_(self.weights.grad_flat, phase="backward", block=-1, stage="params",
+                                     level="replica")
+            self.dp_comm.all_reduce_(loss, phase="backward", block=-1, stage="loss", level="replica")
         if lr != 0.0:
             self.weights.sgd_(lr)
         return loss

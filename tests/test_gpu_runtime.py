@@ -172,3 +172,67 @@ def test_graph_aligned_trainer_equals_union_batch():
         loss, g = out[r]
         assert abs(loss - loss_ref) <= 1e-5 * abs(loss_ref)
         assert max_rel(g, g_ref) < 1e-5
+
+
+def test_gp_dp_composition_equals_union_batch():
+    """GP x DP: 2 data-parallel replicas x 2 graph-parallel workers (threads
+    on one GPU, ThreadComm per GP group and per DP group).  Each replica runs its own graphs
+    through the graph-parallel engine; the replica gradients are all-reduced -- one step
+    must equal the single-device step over the union batch."""
+    import threading
+
+    from paper_2203_09697_b200 import ModelConfig, init_params
+    from paper_2203_09697_b200.graph import build_batch
+    from paper_2203_09697_b200.partition import partition_centers
+    from paper_2203_09697_b200.runtime import CommLog, GPTrainer, ThreadComm, _ThreadShared, gp_dp_layout
+    from paper_2203_09697_b200.tasks import Trainer
+
+    cfg = ModelConfig(variant="gemnet-style", blocks=2, d_u=16, d_v=16, d_e=32, d_t=32, d_bil=32, k_rbf=6,
+                      l_sbf=7, cutoff=6.0, seed=4)
+    params = init_params(cfg)
+    rng = np.random.default_rng(12)
+    systems = [O.random_cloud(n, 0.06, rng)[0] for n in (21, 27, 24, 19)]
+    e_t = rng.standard_normal(4)
+    f_t = [rng.standard_normal((s.shape[0], 3)) for s in systems]
+    ref = Trainer(params, None, e_t, np.concatenate(f_t), 1.0, 0.5, graph=build_batch(systems, cfg.cutoff))
+    loss_ref = float(ref.step(0.0))
+    g_ref = ref.weights.grad_flat.double().cpu().numpy()
+
+    world, gp = 4, 2
+    gp_groups, dp_groups = gp_dp_layout(world, gp)
+    log = CommLog()
+    gp_shared = [_ThreadShared(gp, 60.0, None) for _ in gp_groups]
+    dp_shared = [_ThreadShared(len(dp_groups[0]), 60.0, None) for _ in dp_groups]
+    per = len(systems) // len(gp_groups)
+    bgs = [build_batch(systems[k * per:(k + 1) * per], cfg.cutoff) for k in range(len(gp_groups))]
+    parts = [partition_centers(bg.deg.cpu().numpy(), gp) for bg in bgs]
+    out, errs = {}, []
+    stream = torch.cuda.current_stream()
+
+    def body(rank):
+        try:
+            with torch.cuda.stream(stream):
+                k, i = rank // gp, rank % gp  # replica, worker index
+                sl = slice(k * per, (k + 1) * per)
+                tr = GPTrainer(params, bgs[k], e_t[sl], np.concatenate(f_t[sl]), 1.0, 0.5,
+                               ThreadComm(i, gp_shared[k], log), parts[k],
+                               dp_comm=ThreadComm(k, dp_shared[i], log), global_graphs=len(systems))
+                loss = float(tr.step(0.0))
+                torch.cuda.synchronize()
+                out[rank] = (loss, tr.weights.grad_flat.double().cpu().numpy())
+        except BaseException as exc:  # noqa: BLE001
+            errs.append(exc)
+            for sh in gp_shared + dp_shared:
+                sh.abort()
+
+    ts = [threading.Thread(target=body, args=(r,)) for r in range(world)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errs, errs
+    for r in range(world):
+        loss, g = out[r]
+        assert abs(loss - loss_ref) <= 1e-5 * abs(loss_ref)
+        assert max_rel(g, g_ref) < 1e-4
+    assert "replica" in log.levels()

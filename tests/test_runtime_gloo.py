@@ -133,3 +133,52 @@ def test_thread_comm_timeout():
     sh = _ThreadShared(2, timeout=0.5, fault=None)
     with pytest.raises(CollectiveTimeoutError):
         ThreadComm(0, sh, CommLog()).all_reduce_(torch.zeros(1), level="global")
+
+
+def test_gp_dp_layout():
+    from paper_2203_09697_b200.runtime import gp_dp_layout
+
+    gp, dp = gp_dp_layout(8, 2)
+    assert gp == [[0, 1], [2, 3], [4, 5], [6, 7]]
+    assert dp == [[0, 2, 4, 6], [1, 3, 5, 7]]
+    gp, dp = gp_dp_layout(6, 3)
+    assert gp == [[0, 1, 2], [3, 4, 5]] and dp == [[0, 3], [1, 4], [2, 5]]
+    with pytest.raises(ValueError):
+        gp_dp_layout(6, 4)
+
+
+def _gp_dp_worker(rank, world, port, q):
+    try:
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        from paper_2203_09697_b200.runtime import DistComm
+
+        gp_comm, dp_comm = DistComm.gp_dp(2)
+        t = torch.tensor([float(rank)])
+        gp_comm.all_reduce_(t.clone(), level="param")
+        a = gp_comm.all_reduce_(torch.tensor([float(rank)]), level="param")
+        b = dp_comm.all_reduce_(torch.tensor([float(rank)]), level="replica")
+        k, i = rank // 2, rank % 2
+        assert float(a) == float(2 * k + 2 * k + 1), (rank, float(a))  # ranks 2k, 2k+1
+        assert float(b) == float(i + (i + 2)), (rank, float(b))        # ranks i, i+2
+        assert gp_comm.rank == i and dp_comm.rank == k and gp_comm.world == 2 and dp_comm.world == 2
+        dist.barrier()
+        dist.destroy_process_group()
+        q.put((rank, "ok"))
+    except BaseException as exc:  # noqa: BLE001
+        q.put((rank, repr(exc)))
+
+
+def test_gp_dp_groups_gloo():
+    """GP x DP communicators (world 4 = 2 replicas x 2 graph-parallel workers) on gloo."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    world = 4
+    procs = [ctx.Process(target=_gp_dp_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    results = [q.get(timeout=180) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+    assert sorted(results) == [(r, "ok") for r in range(world)], results
