@@ -109,6 +109,19 @@ int egn_neighbors_fill_pbc(const double* pos, const int64_t* graph_ptr, const in
 int egn_reverse_edges_pbc(const int64_t* edge_ptr, const int32_t* src, const int32_t* recv, const int32_t* img,
                           const int32_t* node_graph, const int32_t* nimg, int64_t num_edges, int32_t* rev,
                           int32_t* missing, egn_stream_t stream);
+/* Neighbour cap (OC20 max-neighbours; reference-free, pinned to the
+ * oracle restatement): keep1[e] = e is among the max_neighbors nearest out-edges of its
+ * source (fp64 distance, then edge index); keep[e] = keep1[e] && keep1[rev[e]] (mutual, so the
+ * graph stays symmetric); deg[v] = kept out-degree. */
+int egn_cap_keep(const int64_t* edge_ptr, const double* dist, const int32_t* rev, int64_t num_nodes, int max_neighbors,
+                 int32_t* keep1, int32_t* keep, int32_t* deg, egn_stream_t stream);
+/* Compact the kept edges in row order into new_ptr (egn_scan_counts of the kept degrees):
+ * new_id[e] (-1 if dropped), src/recv (+ img / shift of periodic graphs, NULL otherwise) and the
+ * remapped reverse edges nrev. */
+int egn_cap_compact(const int64_t* edge_ptr, const int64_t* new_ptr, int64_t num_nodes, int64_t num_edges,
+                    const int32_t* keep, const int32_t* src, const int32_t* recv, const int32_t* img,
+                    const double* shift, const int32_t* rev, int32_t* new_id, int32_t* nsrc, int32_t* nrecv,
+                    int32_t* nimg, double* nshift, int32_t* nrev, egn_stream_t stream);
 /* egn_geometry / egn_triplet_angles on edge vectors (x_recv + shift) - x_src; shift NULL
  * gives the non-periodic results bit for bit. */
 int egn_geometry_shift(const double* pos, const int32_t* src, const int32_t* recv, const double* shift,

@@ -353,6 +353,42 @@ def build_graph_pbc(pos, cell, pbc, cutoff) -> Graph:
     return Graph(n, src, recv, trip_in, trip_out, d, units, angles, rev, vec, img)
 
 
+def cap_graph(g: Graph, pos, max_nb: int) -> Graph:
+    """Neighbour cap (no reference counterpart): an out-edge survives when it
+    is among the max_nb nearest of its source (fp64 distance, ties by edge index) and so is its
+    reverse at the other end; survivors keep their row order; triplets and angles follow from
+    the capped graph as in build_graph_pbc."""
+    n = g.n
+    ptr = np.searchsorted(g.src, np.arange(n + 1))
+    keep1 = np.zeros(g.src.size, dtype=bool)
+    for v in range(n):
+        row = np.arange(ptr[v], ptr[v + 1])
+        order = row[np.argsort(g.dist[row], kind="stable")]
+        keep1[order[:max_nb]] = True
+    keep = keep1 & keep1[g.rev]
+    new_id = np.full(g.src.size, -1, dtype=np.int64)
+    new_id[keep] = np.arange(int(keep.sum()))
+    src, recv = g.src[keep], g.recv[keep]
+    rev = new_id[g.rev[keep]]
+    vec = (g.vec[keep] if g.vec is not None else np.asarray(pos)[recv] - np.asarray(pos)[src])
+    img = g.img[keep] if g.img is not None else None
+    d = g.dist[keep]
+    units = g.units[keep]
+    nptr = np.searchsorted(src, np.arange(n + 1))
+    ins, outs = [], []
+    for j in range(n):
+        row = np.arange(nptr[j], nptr[j + 1])
+        for p in row:
+            q = row[row != p]
+            if q.size:
+                ins.append(rev[q])
+                outs.append(np.full(q.size, p, dtype=np.int64))
+    trip_in = np.concatenate(ins) if ins else np.empty(0, dtype=np.int64)
+    trip_out = np.concatenate(outs) if outs else np.empty(0, dtype=np.int64)
+    angles = triplet_angles(pos, src, recv, trip_in, trip_out, vec, rev)
+    return Graph(n, src, recv, trip_in, trip_out, d, units, angles, rev, vec, img)
+
+
 # ---------------------------------------------------------------------------
 # basis (basis.py:23-93)
 # ---------------------------------------------------------------------------

@@ -43,6 +43,8 @@ SIGNATURES: dict[str, tuple] = {
     "egn_neighbors_count_pbc": (_i32, [_p, _p, _p, _i64, _p, _p, _f64, _p, _p]),
     "egn_gemm_simt_max_m": (_i64, [_i64]),
     "egn_adamw": (_i32, [_p, _p, _p, _p, _i64, _f32, _f32, _f32, _f32, _f32, _i64, _p]),
+    "egn_cap_keep": (_i32, [_p, _p, _p, _i64, _i32, _p, _p, _p, _p]),
+    "egn_cap_compact": (_i32, [_p, _p, _i64, _i64, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p]),
     "egn_graph_mlp_fwd": (_i32, [_i64, _i32, _i32, _p, _p, _p, _p, _p, _p, _p, _p, _p]),
     "egn_graph_mlp_bwd": (_i32, [_i64, _i32, _i32, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p]),
     "egn_neighbors_fill_pbc": (_i32, [_p, _p, _p, _i64, _p, _p, _f64, _p, _p, _p, _p, _p, _p]),
@@ -119,7 +121,7 @@ def stream() -> int:
 
 # Kernels launched per successful ABI call (for the bench's gpu_launches count).
 KERNELS_PER_CALL = {
-    "egn_triplet_bwd": 4, "egn_force_head_fwd": 2, "egn_force_head_bwd": 2, "egn_column_sum": 2, "egn_gemm_wgrad": 2, "egn_rbf_linear_bwd": 2, "egn_graph_mlp_fwd": 2, "egn_graph_mlp_bwd": 3,
+    "egn_triplet_bwd": 4, "egn_force_head_fwd": 2, "egn_force_head_bwd": 2, "egn_column_sum": 2, "egn_gemm_wgrad": 2, "egn_rbf_linear_bwd": 2, "egn_graph_mlp_fwd": 2, "egn_graph_mlp_bwd": 3, "egn_cap_keep": 2, "egn_cap_compact": 2,
 }
 LAUNCH_COUNTER = {"calls": 0, "kernels": 0}
 

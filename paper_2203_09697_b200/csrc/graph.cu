@@ -405,6 +405,95 @@ __global__ void triplet_angles_shift_kernel(const double* __restrict__ pos, cons
   }
 }
 
+// ---------------------------------------------------------------------------
+// Neighbour cap (SURVEY.md 8(f) f1, OC20's max-neighbours): an out-edge survives when it is
+// among the max_nb nearest of its source (distance, then edge index, in fp64) and its
+// reverse survives the same test at the other end (mutual, so the graph stays symmetric
+// for the reverse-edge algebra).  Then the kept edges are compacted in row order.
+__global__ void cap_rank_kernel(const int64_t* __restrict__ edge_ptr, const double* __restrict__ dist, int64_t nv,
+                                int max_nb, int32_t* __restrict__ keep) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t v = warp; v < nv; v += nwarps) {
+    const int64_t e0 = edge_ptr[v], e1 = edge_ptr[v + 1];
+    for (int64_t e = e0 + lane; e < e1; e += 32) {
+      const double d = dist[e];
+      int64_t rank = 0;
+      for (int64_t f = e0; f < e1; ++f) {
+        const double df = dist[f];
+        rank += (df < d) || (df == d && f < e);
+      }
+      keep[e] = rank < max_nb;
+    }
+  }
+}
+
+__global__ void cap_mutual_kernel(const int64_t* __restrict__ edge_ptr, const int32_t* __restrict__ rev, int64_t nv,
+                                  const int32_t* __restrict__ keep1, int32_t* __restrict__ keep,
+                                  int32_t* __restrict__ deg) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t v = warp; v < nv; v += nwarps) {
+    int count = 0;
+    for (int64_t e = edge_ptr[v] + lane; e < edge_ptr[v + 1]; e += 32) {
+      const int32_t k = keep1[e] && keep1[rev[e]];
+      keep[e] = k;
+      count += k;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) count += __shfl_xor_sync(0xffffffffu, count, o);
+    if (lane == 0) deg[v] = count;
+  }
+}
+
+// kept edges of each row compacted in order: new_id[e] (or -1), and the per-edge payload
+__global__ void cap_compact_kernel(const int64_t* __restrict__ edge_ptr, const int64_t* __restrict__ new_ptr,
+                                   int64_t nv, const int32_t* __restrict__ keep, const int32_t* __restrict__ src,
+                                   const int32_t* __restrict__ recv, const int32_t* __restrict__ img,
+                                   const double* __restrict__ shift, int32_t* __restrict__ new_id,
+                                   int32_t* __restrict__ nsrc, int32_t* __restrict__ nrecv, int32_t* __restrict__ nimg,
+                                   double* __restrict__ nshift) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t v = warp; v < nv; v += nwarps) {
+    const int64_t e1 = edge_ptr[v + 1];
+    int64_t out = new_ptr[v];
+    for (int64_t base = edge_ptr[v]; base < e1; base += 32) {
+      const int64_t e = base + lane;
+      const bool k = e < e1 && keep[e];
+      const unsigned mask = __ballot_sync(0xffffffffu, k);
+      if (e < e1) {
+        if (k) {
+          const int64_t slot = out + __popc(mask & ((1u << lane) - 1u));
+          new_id[e] = static_cast<int32_t>(slot);
+          nsrc[slot] = src[e];
+          nrecv[slot] = recv[e];
+          if (img) nimg[slot] = img[e];
+          if (shift) {
+            nshift[3 * slot] = shift[3 * e];
+            nshift[3 * slot + 1] = shift[3 * e + 1];
+            nshift[3 * slot + 2] = shift[3 * e + 2];
+          }
+        } else {
+          new_id[e] = -1;
+        }
+      }
+      out += __popc(mask);
+    }
+  }
+}
+
+__global__ void cap_rev_kernel(int64_t ne, const int32_t* __restrict__ rev, const int32_t* __restrict__ new_id,
+                               int32_t* __restrict__ nrev) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < ne; e += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t n = new_id[e];
+    if (n >= 0) nrev[n] = new_id[rev[e]];
+  }
+}
+
 }  // namespace egn
 
 using namespace egn;
@@ -506,6 +595,30 @@ int egn_reverse_edges_pbc(const int64_t* edge_ptr, const int32_t* src, const int
   reverse_edges_pbc_kernel<<<grid_for(num_edges, 256), 256, 0, as_stream(stream)>>>(
       edge_ptr, src, recv, img, node_graph, nimg, num_edges, rev, missing);
   return check_launch("reverse_edges_pbc");
+}
+
+int egn_cap_keep(const int64_t* edge_ptr, const double* dist, const int32_t* rev, int64_t num_nodes, int max_neighbors,
+                 int32_t* keep1, int32_t* keep, int32_t* deg, egn_stream_t stream) {
+  EGN_REQUIRE(max_neighbors >= 0, "max_neighbors must be >= 0");
+  if (num_nodes == 0) return 0;
+  cudaStream_t st = as_stream(stream);
+  cap_rank_kernel<<<grid_for(num_nodes * 32, 256), 256, 0, st>>>(edge_ptr, dist, num_nodes, max_neighbors, keep1);
+  if (check_launch("cap_rank")) return 1;
+  cap_mutual_kernel<<<grid_for(num_nodes * 32, 256), 256, 0, st>>>(edge_ptr, rev, num_nodes, keep1, keep, deg);
+  return check_launch("cap_mutual");
+}
+
+int egn_cap_compact(const int64_t* edge_ptr, const int64_t* new_ptr, int64_t num_nodes, int64_t num_edges,
+                    const int32_t* keep, const int32_t* src, const int32_t* recv, const int32_t* img,
+                    const double* shift, const int32_t* rev, int32_t* new_id, int32_t* nsrc, int32_t* nrecv,
+                    int32_t* nimg, double* nshift, int32_t* nrev, egn_stream_t stream) {
+  if (num_nodes == 0 || num_edges == 0) return 0;
+  cudaStream_t st = as_stream(stream);
+  cap_compact_kernel<<<grid_for(num_nodes * 32, 256), 256, 0, st>>>(edge_ptr, new_ptr, num_nodes, keep, src, recv,
+                                                                    img, shift, new_id, nsrc, nrecv, nimg, nshift);
+  if (check_launch("cap_compact")) return 1;
+  cap_rev_kernel<<<grid_for(num_edges, 256), 256, 0, st>>>(num_edges, rev, new_id, nrev);
+  return check_launch("cap_rev");
 }
 
 int egn_geometry_shift(const double* pos, const int32_t* src, const int32_t* recv, const double* shift,

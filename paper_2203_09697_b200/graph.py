@@ -127,13 +127,42 @@ def _periodic_info(systems, g):
     return cells, pbc
 
 
+def _cap(pos, graph_ptr, node_graph, deg, edge_ptr, src, recv, rev, img, shift, max_neighbors):
+    """Keep the mutual max_neighbors-nearest edges (egn_cap_keep / egn_cap_compact)."""
+    nv, ne = pos.shape[0], src.shape[0]
+    dev = pos.device
+    _, d64, _ = ops.geometry(pos, src, recv, want_fp64=True, shift=shift)
+    keep1 = torch.empty(ne, dtype=torch.int32, device=dev)
+    keep = torch.empty(ne, dtype=torch.int32, device=dev)
+    ndeg = torch.empty(nv, dtype=torch.int32, device=dev)
+    ops.call("egn_cap_keep", ops.ptr(edge_ptr), ops.ptr(d64), ops.ptr(rev), nv, int(max_neighbors), ops.ptr(keep1),
+             ops.ptr(keep), ops.ptr(ndeg), ops.stream())
+    nptr = ops.scan_counts(ndeg)
+    ntri = ops.scan_counts(ndeg, square_minus_one=True)
+    dmax = ndeg.max().to(torch.int64) if nv else nptr[-1]
+    counts = torch.stack([nptr[-1], ntri[-1], dmax]).cpu()
+    nne, nnt, nmax = int(counts[0]), int(counts[1]), int(counts[2])
+    new_id = torch.empty(ne, dtype=torch.int32, device=dev)
+    nsrc = torch.empty(nne, dtype=torch.int32, device=dev)
+    nrecv = torch.empty(nne, dtype=torch.int32, device=dev)
+    nimg = torch.empty(nne, dtype=torch.int32, device=dev) if img is not None else None
+    nshift = torch.empty((nne, 3), dtype=torch.float64, device=dev) if shift is not None else None
+    nrev = torch.empty(nne, dtype=torch.int32, device=dev)
+    ops.call("egn_cap_compact", ops.ptr(edge_ptr), ops.ptr(nptr), nv, ne, ops.ptr(keep), ops.ptr(src), ops.ptr(recv),
+             ops.ptr(img), ops.ptr(shift), ops.ptr(rev), ops.ptr(new_id), ops.ptr(nsrc), ops.ptr(nrecv),
+             ops.ptr(nimg), ops.ptr(nshift), ops.ptr(nrev), ops.stream())
+    return ndeg, nptr, ntri, nne, nnt, nmax, nsrc, nrecv, nrev, nimg, nshift
+
+
 def build_batch(systems, cutoff: float, device="cuda", positions: torch.Tensor | None = None,
-                sizes: list[int] | None = None, cells=None, pbc=None) -> BatchGraph:
+                sizes: list[int] | None = None, cells=None, pbc=None, max_neighbors: int | None = None) -> BatchGraph:
     """Build the batched device graph.  ``systems``: an AtomicSystem, a list of
     them, or raw (n,3) position arrays; alternatively pass device ``positions``
     (f64 [V,3]) and ``sizes`` directly (no host->device copy of positions).
     Periodic systems (AtomicSystem.cell / pbc, or ``cells`` [G,3,3] with ``pbc`` [G,3])
-    get edges to every periodic image within the cutoff."""
+    get edges to every periodic image within the cutoff.  max_neighbors:
+    keep an edge only if it is among the max_neighbors nearest of its source and its reverse
+    is among those of its receiver (OC20-style cap, kept symmetric; ties by edge order)."""
     if cutoff <= 0:
         raise ValueError("cutoff must be positive")
     if positions is None:
@@ -178,6 +207,12 @@ def build_batch(systems, cutoff: float, device="cuda", positions: torch.Tensor |
     else:
         src, recv = ops.neighbors_fill(pos, graph_ptr, node_graph, cutoff, edge_ptr, ne)
         rev, missing = ops.reverse_edges(edge_ptr, src, recv)
+    if max_neighbors is not None:
+        if max_neighbors < 0:
+            raise ValueError("max_neighbors must be >= 0")
+        if max_deg > max_neighbors:
+            deg, edge_ptr, tri_ptr, ne, nt, max_deg, src, recv, rev, img, shift = _cap(
+                pos, graph_ptr, node_graph, deg, edge_ptr, src, recv, rev, img, shift, max_neighbors)
     geo, _, _ = ops.geometry(pos, src, recv, shift=shift)
     return BatchGraph(g, int(pos.shape[0]), ne, nt, float(cutoff), pos, graph_ptr, node_graph, deg,
                       edge_ptr, src, recv, rev, tri_ptr, geo, list(sizes), max_deg=max_deg, img=img, shift=shift,

@@ -180,3 +180,36 @@ def test_gather_rows_vs_torch(d, rows, acc):
     ops.gather_rows(idx, x, out=out, accumulate=acc)
     ref = (base if acc else 0) + x[idx.long()]
     assert torch.equal(out, ref)
+
+
+@pytest.mark.parametrize("seed,k", [(0, 4), (1, 8), (2, 12), (3, 1000)])
+def test_neighbour_cap_bit_exact(seed, k):
+    """GPU max_neighbors cap vs the oracle restatement: edges, reverse edges, triplets, geometry."""
+    from paper_2203_09697_b200.graph import build_batch, geometry_of, topology_of
+
+    rng = np.random.default_rng(700 + seed)
+    pos, _ = O.random_cloud(int(rng.integers(20, 70)), 0.2, rng)
+    ref = O.cap_graph(O.build_graph(pos, 4.5), pos, k)
+    bg = build_batch(pos, 4.5, max_neighbors=k)
+    topo, geom = topology_of(bg), geometry_of(bg)
+    for key, val in (("src", topo.edge_src), ("recv", topo.edge_recv), ("trip_in", topo.trip_in),
+                     ("trip_out", topo.trip_out), ("rev", topo.reverse_edges())):
+        np.testing.assert_array_equal(val.cpu().numpy(), getattr(ref, key), err_msg=key)
+    np.testing.assert_array_equal(geom.distances.cpu().numpy(), ref.dist)
+    assert bg.max_deg <= k
+
+
+def test_neighbour_cap_periodic():
+    from conftest import load_golden
+    from paper_2203_09697_b200 import AtomicSystem
+    from paper_2203_09697_b200.graph import build_batch, topology_of
+
+    gd = load_golden("pbc.npz")
+    pos, cell, cutoff = gd["triclinic5/pos"], gd["triclinic5/cell"], float(gd["triclinic5/cutoff"])
+    ref = O.cap_graph(O.build_graph_pbc(pos, cell, (True, True, True), cutoff), pos, 6)
+    bg = build_batch(AtomicSystem(pos, np.full(5, 6), cell=cell, pbc=(True, True, True)), cutoff, max_neighbors=6)
+    t = topology_of(bg)
+    np.testing.assert_array_equal(t.edge_src.cpu().numpy(), ref.src)
+    np.testing.assert_array_equal(t.edge_recv.cpu().numpy(), ref.recv)
+    np.testing.assert_array_equal(bg.img.cpu().numpy(), ref.img)
+    np.testing.assert_array_equal(t.reverse_edges().cpu().numpy(), ref.rev)

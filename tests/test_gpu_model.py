@@ -393,3 +393,30 @@ def test_trainer_adamw_reduces_loss():
     assert losses[-1] < losses[0]
     with pytest.raises(ValueError):
         Trainer(init_params(cfg), systems, e_t, f_t, 1.0, 0.5, optimizer="lamb")
+
+
+def test_capped_graph_model_vs_oracle():
+    """Model on a max_neighbors-capped graph vs the fp64 oracle on the same capped graph."""
+    from paper_2203_09697_b200 import ModelConfig, init_params
+    from paper_2203_09697_b200.engine import DeviceWeights, Engine
+    from paper_2203_09697_b200.graph import build_batch
+
+    cfg = ModelConfig(variant="gemnet-style", blocks=2, d_u=16, d_v=16, d_e=32, d_t=16, d_bil=16, k_rbf=6, l_sbf=7,
+                      cutoff=4.5, seed=6)
+    params = init_params(cfg)
+    oc = O.Config(**{k: getattr(cfg, k) for k in O.Config.__dataclass_fields__})
+    pos, z = O.random_cloud(30, 0.2, np.random.default_rng(17))
+    g = O.cap_graph(O.build_graph(pos, cfg.cutoff), pos, 6)
+    f = O.forward(oc, params.arrays, pos, z, graph=g)
+    df = np.random.default_rng(1).standard_normal((30, 3))
+    G, dp = O.backward(f, params.arrays, 0.7, df)
+    eng = Engine(DeviceWeights.from_params(params))
+    bg = build_batch(pos, cfg.cutoff, max_neighbors=6)
+    fw = eng.forward(bg)
+    pos_bar = eng.backward(bg, fw, torch.tensor([0.7], device="cuda"), torch.tensor(df, device="cuda"))
+    grads = eng.weights.to_numpy(grads=True)
+    assert abs(float(fw.energy[0]) - f.energy) <= TOL * max(abs(f.energy), 1e-8)
+    assert max_rel(fw.forces.cpu().numpy(), f.forces) < TOL
+    assert max_rel(pos_bar.cpu().numpy(), dp) < TOL
+    for k in G:
+        assert max_rel(grads[k], G[k]) < TOL, k

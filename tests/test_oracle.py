@@ -166,3 +166,22 @@ def test_oracle_fd_gradient_spot_check():
         a[i] = orig
         fd = (ep - em) / (2 * h)
         assert abs(fd - G[name].ravel()[i]) < 1e-6 * max(1.0, abs(fd))
+
+
+def test_neighbour_cap_restatement():
+    """Cap rule: mutual k-nearest edges; symmetric, degree <= k, identity when
+    k >= max degree, and every kept edge is within both endpoints' k nearest."""
+    rng = np.random.default_rng(3)
+    pos, _ = O.random_cloud(40, 0.2, rng)
+    g = O.build_graph(pos, 4.0)
+    for k in (1, 5, 8, 20):
+        c = O.cap_graph(g, pos, k)
+        assert np.array_equal(c.src[c.rev], c.recv) and np.array_equal(c.recv[c.rev], c.src)
+        assert np.bincount(c.src, minlength=40).max() <= k
+        for a, b, d in zip(c.src, c.recv, c.dist):
+            for x, y in ((a, b), (b, a)):
+                row = g.dist[g.src == x]
+                assert np.sum(row < d) < k  # (ties resolved by edge order)
+    full = O.cap_graph(g, pos, 1000)
+    for key in ("src", "recv", "trip_in", "trip_out", "rev", "dist", "angles"):
+        assert np.array_equal(getattr(full, key), getattr(g, key)), key
