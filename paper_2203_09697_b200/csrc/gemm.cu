@@ -1229,6 +1229,168 @@ __global__ void __launch_bounds__(128) gemm_simt_kernel(int64_t M, int N, int ns
   }
 }
 
+// Whole-panel variant for K <= kPanelMaxK (the node products: K = 64 / 128 / 128 + 64).  The
+// slab kernel above waits one L2/DRAM latency per 32-wide K slab with one warp per SM
+// sub-partition; here every 16 B chunk of the CTA's A panel [32 x K] and B panel [64 x K]
+// (or [K x 64]) is put in flight at once with cp.async (zero-filled past M / N), the
+// epilogue operands are loaded into registers behind them, and 256 threads split K in two
+// halves (fixed-order combine through shared memory).  (One bulk copy per row through the
+// TMA engine measured slower: ~80 small copies per CTA serialise in the copy engine.)
+constexpr int kPanelMaxK = 256;
+__device__ __forceinline__ void cp16_zfill(void* dst, const void* src, bool valid) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src), "r"(valid ? 16 : 0)
+               : "memory");
+}
+// Shared-memory row pitch (floats) for K-contiguous panels: pitch / 4 odd, so the eight
+// 16 B reads of a quarter warp (eight consecutive rows) hit eight distinct bank quads.
+__host__ __device__ __forceinline__ int panel_pitch(int K) { return ((K / 4) & 1) ? K + 8 : K + 4; }
+static size_t panel_smem(int K, bool b_mn) {
+  const int kp = panel_pitch(K);
+  const size_t panels = static_cast<size_t>(kSimtM) * kp + (b_mn ? static_cast<size_t>(K) * (kSimtN + 4)
+                                                                 : static_cast<size_t>(kSimtN) * kp);
+  return sizeof(float) * std::max<size_t>(panels, 2 * 2 * 4 * 128);  // >= the half-combine exchange
+}
+
+// CTA tile 32 x 64: thread (ty, tx) of each K half owns rows ty + 8 i (i < 4) and columns
+// tx + 16 j (tx * 4 + j when BMN).
+template <bool BMN>
+__global__ void __launch_bounds__(256) gemm_simt_panel_kernel(int64_t M, int N, int nseg, const float* __restrict__ a0,
+                                                              int64_t lda0, const float* __restrict__ b0,
+                                                              int64_t ldb0, int k0, const float* __restrict__ a1,
+                                                              int64_t lda1, const float* __restrict__ b1,
+                                                              int64_t ldb1, int k1, Params P) {
+  extern __shared__ __align__(16) float psm[];
+  const int K = k0 + (nseg > 1 ? k1 : 0);
+  const int kp = panel_pitch(K);
+  float* As = psm;                // [32][kp]     (m, k)
+  float* Bs = psm + kSimtM * kp;  // [64][kp] (n, k)  or  [K][68] (k, n) when BMN
+  const int tid = threadIdx.x, h = tid >> 7, t = tid & 127, tx = t & 15, ty = t >> 4;
+  const int64_t m0 = static_cast<int64_t>(blockIdx.x) * kSimtM;
+  const int n0 = blockIdx.y * kSimtN;
+  const int kq = K / 4;  // 16 B chunks per K row
+  // ---- issue the panels
+  for (int c = tid; c < kSimtM * kq; c += 256) {
+    const int r = c / kq, k = (c - r * kq) * 4;
+    const bool ok = m0 + r < M;
+    const float* src = k < k0 ? a0 + (ok ? (m0 + r) * lda0 : 0) + k : a1 + (ok ? (m0 + r) * lda1 : 0) + (k - k0);
+    cp16_zfill(As + r * kp + k, src, ok);
+  }
+  if (!BMN) {
+    for (int c = tid; c < kSimtN * kq; c += 256) {
+      const int r = c / kq, k = (c - r * kq) * 4;
+      const bool ok = n0 + r < N;
+      const int64_t n = ok ? n0 + r : 0;
+      const float* src = k < k0 ? b0 + n * ldb0 + k : b1 + n * ldb1 + (k - k0);
+      cp16_zfill(Bs + r * kp + k, src, ok);
+    }
+  } else {
+    for (int c = tid; c < K * (kSimtN / 4); c += 256) {
+      const int k = c >> 4, nq = (c & 15) * 4;
+      const bool ok = n0 + nq < N;
+      const float* src = k < k0 ? b0 + static_cast<int64_t>(k) * ldb0 + (ok ? n0 + nq : 0)
+                                : b1 + static_cast<int64_t>(k - k0) * ldb1 + (ok ? n0 + nq : 0);
+      cp16_zfill(Bs + k * (kSimtN + 4) + nq, src, ok);
+    }
+  }
+  asm volatile("cp.async.commit_group;" ::: "memory");
+  // ---- epilogue operands of this thread's 8 outputs (rows ty + 8 i, i = 2 h + ii) behind them
+  const int fl = P.flags;
+  auto ncol = [&](int j) { return BMN ? n0 + tx * 4 + j : n0 + tx + 16 * j; };
+  float add[2][4], aux[2][4];
+#pragma unroll
+  for (int ii = 0; ii < 2; ++ii) {
+    const int64_t m = m0 + ty + 8 * (2 * h + ii);
+    const bool okm = m < M;
+    const int64_t gr = (okm && (fl & EPI_GATHER)) ? static_cast<int64_t>(P.gidx[m]) : 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int n = ncol(j);
+      const bool ok = okm && n < N;
+      float v = 0.f;
+      if (ok && (fl & EPI_BIAS)) v += __ldg(P.bias + n);
+      if (ok && (fl & EPI_RESID)) v += P.resid[m * P.ldr + n];
+      if (ok && (fl & EPI_GATHER)) v += P.gsrc[gr * P.ldg + n];
+      add[ii][j] = v;
+      aux[ii][j] = (ok && (fl & (EPI_DSILU_AUX | EPI_MUL_AUX))) ? P.aux[m * P.ldaux + n] : 0.f;
+    }
+  }
+  asm volatile("cp.async.wait_all;" ::: "memory");
+  __syncthreads();
+  // ---- this half's share of K (multiples of 4)
+  const int kh = (K / 8) * 4;
+  const int kb = h ? kh : 0, ke = h ? K : kh;
+  float acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
+#pragma unroll 2
+  for (int k = kb; k < ke; k += 4) {
+    float4 a[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) a[i] = *reinterpret_cast<const float4*>(As + (ty + 8 * i) * kp + k);
+    if (!BMN) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float4 b = *reinterpret_cast<const float4*>(Bs + (tx + 16 * j) * kp + k);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          acc[i][j] = fmaf(a[i].x, b.x, acc[i][j]);
+          acc[i][j] = fmaf(a[i].y, b.y, acc[i][j]);
+          acc[i][j] = fmaf(a[i].z, b.z, acc[i][j]);
+          acc[i][j] = fmaf(a[i].w, b.w, acc[i][j]);
+        }
+      }
+    } else {
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) {
+        const float4 b = *reinterpret_cast<const float4*>(Bs + (k + kk) * (kSimtN + 4) + tx * 4);
+        const float bv[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const float av = kk == 0 ? a[i].x : kk == 1 ? a[i].y : kk == 2 ? a[i].z : a[i].w;
+#pragma unroll
+          for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(av, bv[j], acc[i][j]);
+        }
+      }
+    }
+  }
+  // ---- combine the halves: each half hands the other the rows it finishes
+  __syncthreads();  // panels consumed
+  float* xch = psm;  // [2 halves][2 rows][4][128 threads]
+#pragma unroll
+  for (int ii = 0; ii < 2; ++ii)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) xch[((h * 2 + ii) * 4 + j) * 128 + t] = h ? acc[ii][j] : acc[2 + ii][j];
+  __syncthreads();
+#pragma unroll
+  for (int ii = 0; ii < 2; ++ii) {
+    const int64_t m = m0 + ty + 8 * (2 * h + ii);
+    if (m >= M) continue;
+    float v[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      // low-K half first, the same order for every element
+      const float other = xch[(((1 - h) * 2 + ii) * 4 + j) * 128 + t];
+      v[j] = (h ? other + acc[2 + ii][j] : acc[ii][j] + other) + add[ii][j];
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int n = ncol(j);
+      if (n >= N) continue;
+      float o = v[j], o2 = 0.f;
+      if (fl & EPI_DSILU_AUX) o = v[j] * dsilu(aux[ii][j]);
+      if (fl & EPI_MUL_AUX) {
+        o2 = v[j];
+        o = v[j] * aux[ii][j];
+      }
+      if (fl & EPI_SILU_OUT2) o2 = __fdividef(v[j], 1.f + __expf(-v[j]));
+      P.out[m * P.ldo + n] = o;
+      if (fl & (EPI_MUL_AUX | EPI_SILU_OUT2)) P.out2[m * P.ldo2 + n] = o2;
+    }
+  }
+}
+
 // Weight gradient over few rows (node rows): out[z][m][n] = sum_{r in split z} g[r][m] x[r][n]
 // as an fp32 SIMT product (32 x 64 output tile per 128-thread CTA, 32-row slabs, next slab
 // prefetched into registers), plus the split's column sums of g (n-block 0 only); the
@@ -1296,6 +1458,84 @@ __global__ void __launch_bounds__(128) wgrad_simt_kernel(int64_t R, int M, int N
     if (m < M && n < N) *reinterpret_cast<float4*>(out + static_cast<int64_t>(m) * N + n) =
         make_float4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
     if (gpart != nullptr && n0 == 0 && tx == 0 && m < M) gpart[static_cast<int64_t>(z) * M + m] = cs[i];
+  }
+}
+
+// Whole-panel variant of wgrad_simt_kernel for splits of at most kPanelMaxRows rows: the
+// split's g [rows x 32] and x [rows x 64] panels are put in flight at once (cp.async), and
+// 256 threads take half the rows each, combined low rows first.
+constexpr int kPanelMaxRows = 128;
+__global__ void __launch_bounds__(256) wgrad_simt_panel_kernel(int64_t R, int M, int N, const float* __restrict__ g,
+                                                               int64_t ldg, const float* __restrict__ x, int64_t ldx,
+                                                               int rows_per_split, float* __restrict__ part,
+                                                               float* __restrict__ gpart) {
+  extern __shared__ __align__(16) float psm[];
+  float(*Gs)[kSimtM + 4] = reinterpret_cast<float(*)[kSimtM + 4]>(psm);                                  // [r][m]
+  float(*Xs)[kSimtN + 4] = reinterpret_cast<float(*)[kSimtN + 4]>(psm + kPanelMaxRows * (kSimtM + 4));  // [r][n]
+  const int tid = threadIdx.x, h = tid >> 7, t = tid & 127, tx = t & 15, ty = t >> 4;
+  const int tiles_m = (M + kSimtM - 1) / kSimtM;
+  const int m0 = (blockIdx.x % tiles_m) * kSimtM;
+  const int n0 = (blockIdx.x / tiles_m) * kSimtN;
+  const int z = blockIdx.y;
+  const int64_t r_beg = static_cast<int64_t>(z) * rows_per_split;
+  const int64_t r_end = r_beg + rows_per_split < R ? r_beg + rows_per_split : R;
+  const int rows = r_end > r_beg ? static_cast<int>(r_end - r_beg) : 0;
+  for (int c = tid; c < rows * (kSimtM / 4); c += 256) {
+    const int r = c >> 3, mq = (c & 7) * 4;
+    const bool ok = m0 + mq < M;
+    cp16_zfill(&Gs[r][mq], g + (r_beg + r) * ldg + (ok ? m0 + mq : 0), ok);
+  }
+  for (int c = tid; c < rows * (kSimtN / 4); c += 256) {
+    const int r = c >> 4, nq = (c & 15) * 4;
+    const bool ok = n0 + nq < N;
+    cp16_zfill(&Xs[r][nq], x + (r_beg + r) * ldx + (ok ? n0 + nq : 0), ok);
+  }
+  asm volatile("cp.async.commit_group;" ::: "memory");
+  asm volatile("cp.async.wait_all;" ::: "memory");
+  __syncthreads();
+  const int rh = rows / 2;
+  const int rb = h ? rh : 0, re = h ? rows : rh;
+  float acc[4][4], cs[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
+#pragma unroll 4
+  for (int r = rb; r < re; ++r) {
+    const float4 a = *reinterpret_cast<const float4*>(&Gs[r][ty * 4]);
+    const float4 b = *reinterpret_cast<const float4*>(&Xs[r][tx * 4]);
+    const float av[4] = {a.x, a.y, a.z, a.w}, bv[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      cs[i] += av[i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
+    }
+  }
+  __syncthreads();  // panels consumed
+  float* xch = &Gs[0][0];  // [2 halves][2 rows][5][128 threads] (4 products + column sum)
+#pragma unroll
+  for (int ii = 0; ii < 2; ++ii) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) xch[((h * 2 + ii) * 5 + j) * 128 + t] = h ? acc[ii][j] : acc[2 + ii][j];
+    xch[((h * 2 + ii) * 5 + 4) * 128 + t] = h ? cs[ii] : cs[2 + ii];
+  }
+  __syncthreads();
+  float* out = part + static_cast<int64_t>(z) * M * N;
+#pragma unroll
+  for (int ii = 0; ii < 2; ++ii) {
+    const int i = 2 * h + ii;
+    const int m = m0 + ty * 4 + i;
+    const int n = n0 + tx * 4;
+    const float* o = xch + (((1 - h) * 2 + ii) * 5) * 128 + t;
+    float v[5];
+#pragma unroll
+    for (int j = 0; j < 5; ++j) {
+      const float mine = j < 4 ? (h ? acc[2 + ii][j] : acc[ii][j]) : (h ? cs[2 + ii] : cs[ii]);
+      v[j] = h ? o[j * 128] + mine : mine + o[j * 128];
+    }
+    if (m < M && n < N) *reinterpret_cast<float4*>(out + static_cast<int64_t>(m) * N + n) = make_float4(v[0], v[1], v[2], v[3]);
+    if (gpart != nullptr && n0 == 0 && tx == 0 && m < M) gpart[static_cast<int64_t>(z) * M + m] = v[4];
   }
 }
 
@@ -1389,6 +1629,22 @@ extern "C" int egn_gemm(int64_t M, int N, int nseg, const float* a0, int64_t lda
       (!(flags & (EPI_MUL_AUX | EPI_SILU_OUT2)) || ((reinterpret_cast<uintptr_t>(out2) & 15) == 0 && ldo2 % 4 == 0))) {
     const dim3 grid(static_cast<unsigned>((M + kSimtM - 1) / kSimtM), static_cast<unsigned>((N + kSimtN - 1) / kSimtN));
     cudaStream_t st = as_stream(stream);
+    const int K = k0 + (nseg > 1 ? k1 : 0);
+    // EGN_GEMM_PANEL=0 keeps the slab kernel (for comparison)
+    static const bool panel = [] { const char* e = std::getenv("EGN_GEMM_PANEL"); return !(e && e[0] == '0'); }();
+    if (panel && K <= kPanelMaxK) {
+      static const bool attr = [] {
+        const int mx = static_cast<int>(std::max(panel_smem(kPanelMaxK, false), panel_smem(kPanelMaxK, true)));
+        cudaFuncSetAttribute(gemm_simt_panel_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        cudaFuncSetAttribute(gemm_simt_panel_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        return true;
+      }();
+      (void)attr;
+      const size_t sm = panel_smem(K, b_mn);
+      if (b_mn) gemm_simt_panel_kernel<true><<<grid, 256, sm, st>>>(M, N, nseg, a0, lda0, b0, ldb0, k0, a1, lda1, b1, ldb1, k1, P);
+      else gemm_simt_panel_kernel<false><<<grid, 256, sm, st>>>(M, N, nseg, a0, lda0, b0, ldb0, k0, a1, lda1, b1, ldb1, k1, P);
+      return check_launch("gemm_simt_panel");
+    }
     if (b_mn) gemm_simt_kernel<true><<<grid, 128, 0, st>>>(M, N, nseg, a0, lda0, b0, ldb0, k0, a1, lda1, b1, ldb1, k1, P);
     else gemm_simt_kernel<false><<<grid, 128, 0, st>>>(M, N, nseg, a0, lda0, b0, ldb0, k0, a1, lda1, b1, ldb1, k1, P);
     return check_launch("gemm_simt");
@@ -1476,7 +1732,19 @@ extern "C" int egn_gemm_wgrad(int64_t krows, int M, int N, const float* g, int64
     float* gpart_s = part + static_cast<int64_t>(splits) * M * N;
     const dim3 grid(static_cast<unsigned>(((M + kSimtM - 1) / kSimtM) * ((N + kSimtN - 1) / kSimtN)),
                     static_cast<unsigned>(splits));
-    wgrad_simt_kernel<<<grid, 128, 0, st>>>(krows, M, N, g, ldg, x, ldx, rps, part, g_colsum ? gpart_s : nullptr);
+    static const bool panel = [] { const char* e = std::getenv("EGN_GEMM_PANEL"); return !(e && e[0] == '0'); }();
+    if (panel && rps <= kPanelMaxRows) {
+      constexpr int sm = kPanelMaxRows * (kSimtM + 4 + kSimtN + 4) * static_cast<int>(sizeof(float));
+      static const bool attr = [] {
+        cudaFuncSetAttribute(wgrad_simt_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+        return true;
+      }();
+      (void)attr;
+      wgrad_simt_panel_kernel<<<grid, 256, sm, st>>>(krows, M, N, g, ldg, x, ldx, rps, part,
+                                                     g_colsum ? gpart_s : nullptr);
+    } else {
+      wgrad_simt_kernel<<<grid, 128, 0, st>>>(krows, M, N, g, ldg, x, ldx, rps, part, g_colsum ? gpart_s : nullptr);
+    }
     if (check_launch("gemm_wgrad_simt")) return 1;
     const int64_t len = static_cast<int64_t>(M) * N;
     const int mg = g_colsum ? M : 0;
