@@ -318,6 +318,13 @@ int egn_graph_mlp_bwd(int64_t num_graphs, int dv, int du, const float* u_bar, co
 /* ------------------------------------------------------------------ */
 /* Optimizer: train_simple SGD update (tasks.py:207-208)               */
 /* ------------------------------------------------------------------ */
+/* Loss of one step and its seeds (reference egn/tasks.py:166-176, per sample, fp64):
+ * d_energy[g] = 2 w_e (E_g - E*_g) / n, d_forces[v] = 2 w_f (F_v - F*_v) / (n count_v),
+ * loss[0] = (sum_g w_e (E_g - E*_g)^2 + w_f sum_v |F_v - F*_v|^2 / count_v) / n.
+ * forces == NULL: energy terms only.  One launch; seeds are written as fp32. */
+int egn_loss_seeds(const float* energy, const double* e_target, int64_t num_graphs, const float* forces,
+                   const double* f_target, const double* atom_count, int64_t num_nodes, double w_energy,
+                   double w_forces, double n, double* loss, float* d_energy, float* d_forces, egn_stream_t stream);
 int egn_sgd(float* w, const float* g, int64_t n, float lr, egn_stream_t stream);
 /* AdamW step t >= 1 over a flat parameter buffer (the
  * reference documents it only): decoupled weight decay, bias-corrected first / second moments

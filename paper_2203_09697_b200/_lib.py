@@ -43,6 +43,7 @@ SIGNATURES: dict[str, tuple] = {
     "egn_neighbors_count_pbc": (_i32, [_p, _p, _p, _i64, _p, _p, _f64, _p, _p]),
     "egn_gemm_simt_max_m": (_i64, [_i64]),
     "egn_adamw": (_i32, [_p, _p, _p, _p, _i64, _f32, _f32, _f32, _f32, _f32, _i64, _p]),
+    "egn_loss_seeds": (_i32, [_p, _p, _i64, _p, _p, _p, _i64, _f64, _f64, _f64, _p, _p, _p, _p]),
     "egn_cap_keep": (_i32, [_p, _p, _p, _i64, _i32, _p, _p, _p, _p]),
     "egn_cap_compact": (_i32, [_p, _p, _i64, _i64, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p]),
     "egn_graph_mlp_fwd": (_i32, [_i64, _i32, _i32, _p, _p, _p, _p, _p, _p, _p, _p, _p]),

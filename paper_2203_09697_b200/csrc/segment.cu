@@ -896,6 +896,70 @@ int egn_column_sum(const float* x, int64_t rows, int d, int64_t ld, float* out, 
   return check_launch("column_sum_reduce");
 }
 
+// Loss and its seeds in one CTA (tasks.py:166-176 per sample; fp64 like the reference):
+// res = E - E*, d_energy = 2 w_e res / n, delta = F - F*, d_forces = 2 w_f delta / (n count),
+// loss = (sum w_e res^2 + w_f sum_v |delta_v|^2 / count_v) / n.  Seeds are cast to fp32 (the
+// precision the backward consumes); the loss sums run in a fixed order.
+__global__ void __launch_bounds__(1024) loss_seeds_kernel(const float* __restrict__ energy,
+                                                          const double* __restrict__ e_target, int64_t G,
+                                                          const float* __restrict__ forces,
+                                                          const double* __restrict__ f_target,
+                                                          const double* __restrict__ count, int64_t V, double w_e,
+                                                          double w_f, double n, double* __restrict__ loss,
+                                                          float* __restrict__ d_energy,
+                                                          float* __restrict__ d_forces) {
+  __shared__ double red[2][32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  double le = 0.0, lf = 0.0;
+  for (int64_t g = tid; g < G; g += blockDim.x) {
+    const double r = static_cast<double>(energy[g]) - e_target[g];
+    d_energy[g] = static_cast<float>(2.0 * w_e * r / n);
+    le += w_e * r * r;
+  }
+  if (forces != nullptr) {
+    for (int64_t v = tid; v < V; v += blockDim.x) {
+      const double cnt = count[v];
+      double s = 0.0;
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const double d = static_cast<double>(forces[3 * v + c]) - f_target[3 * v + c];
+        d_forces[3 * v + c] = static_cast<float>(2.0 * w_f * d / (n * cnt));
+        s += d * d;
+      }
+      lf += s / cnt;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    le += __shfl_xor_sync(0xffffffffu, le, o);
+    lf += __shfl_xor_sync(0xffffffffu, lf, o);
+  }
+  if (lane == 0) {
+    red[0][warp] = le;
+    red[1][warp] = lf;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double a = 0.0, b = 0.0;
+    for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) {
+      a += red[0][w];
+      b += red[1][w];
+    }
+    loss[0] = a / n + w_f * b / n;
+  }
+}
+
+int egn_loss_seeds(const float* energy, const double* e_target, int64_t num_graphs, const float* forces,
+                   const double* f_target, const double* atom_count, int64_t num_nodes, double w_energy,
+                   double w_forces, double n, double* loss, float* d_energy, float* d_forces, egn_stream_t stream) {
+  EGN_REQUIRE(n > 0.0, "loss normaliser must be positive");
+  EGN_REQUIRE(forces == nullptr || (f_target != nullptr && atom_count != nullptr && d_forces != nullptr),
+              "force terms need targets, atom counts and a seed buffer");
+  loss_seeds_kernel<<<1, 1024, 0, as_stream(stream)>>>(energy, e_target, num_graphs, forces, f_target, atom_count,
+                                                        num_nodes, w_energy, w_forces, n, loss, d_energy, d_forces);
+  return check_launch("loss_seeds");
+}
+
 int egn_adamw(float* w, const float* g, float* m, float* v, int64_t n, float lr, float beta1, float beta2,
               float eps, float weight_decay, int64_t step, egn_stream_t stream) {
   EGN_REQUIRE(step >= 1, "adamw step count starts at 1");

@@ -532,6 +532,26 @@ def sgd_(w, g, lr):
     call("egn_sgd", ptr(w), ptr(g), w.numel(), float(lr), stream())
 
 
+def loss_seeds(energy, e_target, forces, f_target, atom_count, w_energy, w_forces, n):
+    """(loss f64 [], d_energy f32 [G], d_forces f32 [V, 3] or None) in one launch
+    (egn_loss_seeds; egn/tasks.py:166-176).  forces=None: energy terms only."""
+    G = energy.shape[0]
+    dev = energy.device
+    loss = torch.empty((), dtype=torch.float64, device=dev)
+    d_e = torch.empty(G, dtype=torch.float32, device=dev)
+    d_f = None
+    V = 0
+    if forces is not None:
+        forces, f_target = _c(forces, torch.float32), _c(f_target, torch.float64)
+        V = forces.shape[0]
+        d_f = torch.empty((V, 3), dtype=torch.float32, device=dev)
+    call("egn_loss_seeds", ptr(_c(energy, torch.float32)), ptr(_c(e_target, torch.float64)), G,
+         ptr(forces) if forces is not None else None, ptr(f_target) if forces is not None else None,
+         ptr(_c(atom_count, torch.float64)) if forces is not None else None, V, float(w_energy),
+         float(w_forces), float(n), ptr(loss), ptr(d_e), ptr(d_f) if d_f is not None else None, stream())
+    return loss, d_e, d_f
+
+
 def adamw_(w, g, m, v, lr, step, betas=(0.9, 0.999), eps=1e-8, weight_decay=1e-2):
     """In-place AdamW step `step` (>= 1) on flat fp32 buffers (egn_adamw)."""
     call("egn_adamw", ptr(w), ptr(g), ptr(m), ptr(v), w.numel(), float(lr), float(betas[0]), float(betas[1]),

@@ -16,6 +16,7 @@ from dataclasses import dataclass
 import numpy as np
 import torch
 
+from . import ops
 from .config import GEMNET
 from .engine import DeviceWeights, Engine
 from .graph import BatchGraph, build_batch
@@ -130,16 +131,13 @@ def relax(system, params: ModelParams, fmax_threshold: float, max_steps: int = 2
 
 
 def _seeds(energy, forces, e_target, f_target, atom_count, w_energy, w_forces, n):
-    """Loss and its seeds, per sample as tasks.py:166-176 computes them."""
-    res = energy.double() - e_target
-    loss = (w_energy * res * res).sum() / n
-    d_energy = 2.0 * w_energy * res / n
-    d_forces = None
-    if w_forces != 0.0:
-        delta = forces.double() - f_target
-        loss = loss + w_forces * ((delta * delta).sum(dim=1) / atom_count).sum() / n
-        d_forces = 2.0 * w_forces * delta / (n * atom_count[:, None])
-    return loss, d_energy, d_forces
+    """Loss and its seeds, per sample as tasks.py:166-176 computes them, in one native launch
+    (egn_loss_seeds: fp64 residuals, fp32 seeds):
+    loss = sum(w_e res^2) / n + w_f sum_v(|delta_v|^2 / count_v) / n,
+    d_energy = 2 w_e res / n, d_forces = 2 w_f delta / (n count)."""
+    use_f = w_forces != 0.0
+    return ops.loss_seeds(energy, e_target, forces if use_f else None, f_target if use_f else None,
+                          atom_count, w_energy, w_forces, n)
 
 
 class Trainer:

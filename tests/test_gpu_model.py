@@ -420,3 +420,34 @@ def test_capped_graph_model_vs_oracle():
     assert max_rel(pos_bar.cpu().numpy(), dp) < TOL
     for k in G:
         assert max_rel(grads[k], G[k]) < TOL, k
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("with_forces", [False, True])
+def test_loss_seeds_match_reference_formula(with_forces):
+    """egn_loss_seeds against egn/tasks.py:166-176 evaluated in numpy fp64."""
+    from paper_2203_09697_b200 import ops
+
+    rng = np.random.default_rng(5)
+    sizes = [7, 12, 3, 30]
+    G, V = len(sizes), sum(sizes)
+    e = rng.standard_normal(G).astype(np.float32)
+    e_t = rng.standard_normal(G)
+    f = rng.standard_normal((V, 3)).astype(np.float32)
+    f_t = rng.standard_normal((V, 3))
+    cnt = np.repeat(np.asarray(sizes, dtype=np.float64), sizes)
+    w_e, w_f, n = 0.7, (1.3 if with_forces else 0.0), 6.0
+    dev = "cuda"
+    loss, d_e, d_f = ops.loss_seeds(torch.tensor(e, device=dev), torch.tensor(e_t, device=dev),
+                                    torch.tensor(f, device=dev) if with_forces else None,
+                                    torch.tensor(f_t, device=dev), torch.tensor(cnt, device=dev), w_e, w_f, n)
+    res = e.astype(np.float64) - e_t
+    ref_loss = (w_e * res * res).sum() / n
+    np.testing.assert_array_equal(d_e.cpu().numpy(), (2.0 * w_e * res / n).astype(np.float32))
+    if with_forces:
+        delta = f.astype(np.float64) - f_t
+        ref_loss += w_f * ((delta * delta).sum(1) / cnt).sum() / n
+        np.testing.assert_array_equal(d_f.cpu().numpy(), (2.0 * w_f * delta / (n * cnt[:, None])).astype(np.float32))
+    else:
+        assert d_f is None
+    assert abs(float(loss) - ref_loss) <= 1e-12 * abs(ref_loss)
