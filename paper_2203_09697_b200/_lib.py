@@ -15,7 +15,7 @@ from pathlib import Path
 import torch
 
 _HERE = Path(__file__).resolve().parent
-LIB_PATH = _HERE / "libegn_b200.so"
+LIB_PATH = Path(os.environ.get("EGN_LIB", _HERE / "libegn_b200.so"))  # EGN_LIB: same-box A/B builds
 
 _p = ctypes.c_void_p
 _i32 = ctypes.c_int
