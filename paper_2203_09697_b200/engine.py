@@ -29,6 +29,9 @@ from __future__ import annotations
 
 from dataclasses import dataclass, field
 
+import os
+import threading
+
 import numpy as np
 import torch
 import torch.nn.functional as F
@@ -113,6 +116,16 @@ class Engine:
     def __init__(self, weights: DeviceWeights):
         self.weights = weights
         self.config = weights.config
+        self._side = {}  # per host thread: the stream weight gradients run on (backward)
+
+    def _side_stream(self, device):
+        """Side stream for the weight-gradient products of backward(), or None (EGN_WGRAD_STREAM=0)."""
+        if device.type != "cuda" or os.environ.get("EGN_WGRAD_STREAM", "1") == "0":
+            return None
+        key = threading.get_ident()
+        if key not in self._side:
+            self._side[key] = torch.cuda.Stream(device=device)
+        return self._side[key]
 
     # -- helpers -----------------------------------------------------------
     def _sbf_weight(self, b: int) -> torch.Tensor:
@@ -226,7 +239,30 @@ class Engine:
         if d_forces is not None and not gem:
             raise ValueError("force seed given but this variant has no force head")
         de = c.d_e
-        L, wg, cs = ops.linear, ops.linear_wgrad, ops.column_sum
+        L, cs = ops.linear, ops.column_sum
+        # Weight gradients (g^T x) depend on nothing the data gradients produce later in the
+        # block, so they run on a side stream and overlap the data-gradient products and
+        # gathers of the main stream (each fills the other's wave tail and launch latency).
+        # Same kernels, same order per stream: results are unchanged.  Their operands stay
+        # referenced until the join at the next block, so no buffer is recycled under them.
+        main = torch.cuda.current_stream() if bg.device.type == "cuda" else None
+        side = self._side_stream(bg.device)
+        pending = []
+
+        def wg(g, x, out, bias_out=None):
+            if side is None or not (ops._tc_ok(4, x.shape[1], g, x) and out.stride(1) == 1):
+                return ops.linear_wgrad(g, x, out, bias_out)
+            side.wait_stream(main)
+            with torch.cuda.stream(side):
+                ops.gemm_wgrad(g, x, out=out, colsum=bias_out)
+            pending.append((g, x, out, bias_out))
+            return out
+
+        def join():
+            if side is not None and pending:
+                main.wait_stream(side)
+                pending.clear()
+
         self.weights.grad_flat.zero_()
         eg = torch.zeros((bg.num_edges, 4), dtype=torch.float32, device=bg.device)
         dE = d_energy.to(torch.float32).view(-1, 1)
@@ -241,6 +277,7 @@ class Engine:
         rbf_bar = torch.zeros_like(fw.rbf)
         post = []  # weight-sized gradient products, batched after the block loop
         for b in range(c.blocks - 1, -1, -1):
+            join()
             p = f"block{b}."
             st = fw.blocks[b]
             # GU (engine.py:207-217): fused adjoint over G rows (data and weight gradients)
@@ -251,7 +288,9 @@ class Engine:
                 # sym (engine.py:195-200): m = m2 + m2[rev] Wsym^T
                 wg(m_bar, st["m2r"], gr[p + "sym.w"])
                 t = L(m_bar, w[p + "sym.w"], w_mn=True)
-                # m_bar is dead after this point of the block: accumulate in place
+                # m_bar is dead after this point of the block: accumulate in place (once the
+                # side-stream weight gradient above has read it)
+                join()
                 m2_bar = ops.gather_rows(bg.rev, t, out=m_bar, accumulate=True)
                 # EU2 (engine.py:180-192)
                 wg(m2_bar, st["a2"], gr[p + "eu2.w2"], gr[p + "eu2.b2"])
@@ -311,6 +350,7 @@ class Engine:
                 down_bar = X_bar
             wg(down_bar, st["m"], gr[p + "tu.down"])
             m_bar = L(down_bar, w[p + "tu.down"], w_mn=True, resid=m_in_bar)
+        join()
         ops.small_gemms(post)  # every deferred weight-sized gradient product, one launch
         # edge init (engine.py:109-111), K = k_rbf
         ops.rbf_linear_bwd(fw.rbf, w["edge_init.w"], m_bar, rbf_bar, gr["edge_init.w"], gr["edge_init.b"])
