@@ -29,6 +29,7 @@ from __future__ import annotations
 
 from dataclasses import dataclass, field
 
+import contextlib
 import os
 import threading
 
@@ -171,6 +172,7 @@ class Engine:
         de = c.d_e
         L = ops.linear
         folded = self._folded_weights()
+        side = self._side_stream(bg.device)
         rbf = ops.rbf(bg.geo, c.k_rbf, c.cutoff)
         m = ops.rbf_linear(rbf, w["edge_init.w"], w["edge_init.b"])  # K = k_rbf (6)
         u = torch.zeros((bg.num_graphs, c.d_u), dtype=torch.float32, device=bg.device)
@@ -217,11 +219,18 @@ class Engine:
                 st.update(h2=h2, a2=a2, m2r=m2r)
             else:
                 m = m_new
-            s = ops.graph_sum(bg.graph_ptr, v)
-            # GU (engine.py:207-217): u += silu(s W1^T + b1) W2^T + b2, one fused launch over G rows
-            pre, act = ops.graph_mlp_fwd(s, w[p + "gu.w1"], w[p + "gu.b1"], w[p + "gu.w2"], w[p + "gu.b2"], u)
+            # GU (engine.py:207-217): u += silu(s W1^T + b1) W2^T + b2, one fused launch over G rows.
+            # Only the energy head reads u, so the graph update runs on the side stream,
+            # overlapping the next block's edge work (joined before the energy head).
+            if side is not None:
+                side.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(side) if side is not None else contextlib.nullcontext():
+                s = ops.graph_sum(bg.graph_ptr, v)
+                pre, act = ops.graph_mlp_fwd(s, w[p + "gu.w1"], w[p + "gu.b1"], w[p + "gu.w2"], w[p + "gu.b2"], u)
             st.update(s=s, pre=pre, act=act)
             blocks.append(st)
+        if side is not None:
+            torch.cuda.current_stream().wait_stream(side)
         energy = torch.addmm(w["energy_head.b"], u, w["energy_head.w"].t()).view(-1)
         forces = scale = None
         if gem:
@@ -281,9 +290,19 @@ class Engine:
             p = f"block{b}."
             st = fw.blocks[b]
             # GU (engine.py:207-217): fused adjoint over G rows (data and weight gradients)
-            s_bar = ops.graph_mlp_bwd(u_bar, st["s"], st["pre"], st["act"], w[p + "gu.w1"], w[p + "gu.w2"],
-                                      gr[p + "gu.w1"], gr[p + "gu.b1"], gr[p + "gu.w2"], gr[p + "gu.b2"])
-            v_bar = ops.gather_rows(bg.node_graph, s_bar)
+            # (node-level: on the side stream, overlapping the edge-level adjoints below; the
+            # main stream waits for v_ready before its first use of v_bar)
+            v_ready = None
+            if side is not None:
+                side.wait_stream(main)
+            with torch.cuda.stream(side) if side is not None else contextlib.nullcontext():
+                s_bar = ops.graph_mlp_bwd(u_bar, st["s"], st["pre"], st["act"], w[p + "gu.w1"], w[p + "gu.w2"],
+                                          gr[p + "gu.w1"], gr[p + "gu.b1"], gr[p + "gu.w2"], gr[p + "gu.b2"])
+                v_bar = ops.gather_rows(bg.node_graph, s_bar)
+            if side is not None:
+                v_ready = torch.cuda.Event()
+                v_ready.record(side)
+                pending.append((s_bar, v_bar))
             if gem:
                 # sym (engine.py:195-200): m = m2 + m2[rev] Wsym^T
                 wg(m_bar, st["m2r"], gr[p + "sym.w"])
@@ -299,12 +318,16 @@ class Engine:
                 wg(h2_bar, st["m_new"], gr[p + "eu2.w1"][:, :de], gr[p + "eu2.b1"])
                 pv_bar = ops.aggregate_in_edges(bg.edge_ptr, bg.rev, h2_bar)
                 wg(pv_bar, st["v"], gr[p + "eu2.w1"][:, de:])
+                if v_ready is not None:
+                    main.wait_event(v_ready)
                 v_bar = L(pv_bar, w1[:, de:], w_mn=True, resid=v_bar)
                 m_new_bar = L(h2_bar, w1[:, :de], w_mn=True, resid=m2_bar)
             else:
                 m_new_bar = m_bar  # dead after this point of the block
             # EA + NU (engine.py:166-177)
             wg(v_bar, st["av"], gr[p + "nu.w2"], gr[p + "nu.b2"])
+            if v_ready is not None:
+                main.wait_event(v_ready)
             hv_bar = L(v_bar, w[p + "nu.w2"], w_mn=True, aux=st["hv"], flags=ops.EPI_DSILU_AUX)
             wg(hv_bar, st["agg"], gr[p + "nu.w1"], gr[p + "nu.b1"])
             agg_bar = L(hv_bar, w[p + "nu.w1"], w_mn=True)
