@@ -178,6 +178,16 @@ class Engine:
         u = torch.zeros((bg.num_graphs, c.d_u), dtype=torch.float32, device=bg.device)
         v = None
         blocks = []
+        # the rbf gates of every block (K = k_rbf (6)) depend on the geometry only: side stream,
+        # overlapping block 0's down-projection and triplet interaction
+        gates_ready = None
+        if side is not None:
+            side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side) if side is not None else contextlib.nullcontext():
+            gates = [ops.rbf_linear(rbf, w[f"block{b}.tu.rbf_gate"]) for b in range(c.blocks)]
+        if side is not None:
+            gates_ready = torch.cuda.Event()
+            gates_ready.record(side)
         for b in range(c.blocks):
             p = f"block{b}."
             st = {"m": m}
@@ -192,7 +202,10 @@ class Engine:
                 down = X = L(m, w[p + "tu.down"])
             Wk = folded[b]["Wk"]
             S = ops.triplet_fwd(bg.edge_ptr, bg.rev, bg.geo, X, Wk, c.cutoff, max_degree=bg.max_deg)
-            g = ops.rbf_linear(rbf, w[p + "tu.rbf_gate"])  # K = k_rbf (6)
+            g = gates[b]
+            if gates_ready is not None:
+                torch.cuda.current_stream().wait_event(gates_ready)
+                gates_ready = None
             if gem:
                 Y, Z = L(S, w[p + "tu.bilinear_proj"], aux=g, flags=ops.EPI_MUL_AUX)  # Y = (S P^T) * g
                 st["Z"] = Z
@@ -354,7 +367,14 @@ class Engine:
                 Y_bar = L(h_bar, st["W1u"], w_mn=True)
                 S_bar = Y_bar * st["g"]
                 g_prod = (Y_bar, st["S"])  # g_bar = Y_bar * S
-            ops.rbf_linear_bwd(fw.rbf, w[p + "tu.rbf_gate"], g_prod[0], rbf_bar, gr[p + "tu.rbf_gate"], g2=g_prod[1])
+            # rbf_bar is read only after the block loop: the gate adjoint runs on the side stream
+            if side is not None:
+                side.wait_stream(main)
+            with torch.cuda.stream(side) if side is not None else contextlib.nullcontext():
+                ops.rbf_linear_bwd(fw.rbf, w[p + "tu.rbf_gate"], g_prod[0], rbf_bar, gr[p + "tu.rbf_gate"],
+                                   g2=g_prod[1])
+            if side is not None:
+                pending.append(g_prod)
             X_bar, Wk_bar = ops.triplet_bwd(bg.edge_ptr, bg.rev, bg.geo, st["X"], st["Wk"], c.cutoff,
                                             S_bar, eg, max_degree=bg.max_deg)
             if gem:
