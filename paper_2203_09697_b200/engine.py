@@ -119,11 +119,12 @@ class Engine:
         self.config = weights.config
         self._side = {}  # per host thread: the stream weight gradients run on (backward)
 
-    def _side_stream(self, device):
-        """Side stream for the weight-gradient products of backward(), or None (EGN_WGRAD_STREAM=0)."""
+    def _side_stream(self, device, index: int = 0):
+        """Side stream `index` of this host thread (0: weight gradients and graph-level work,
+        1: the node-level adjoint chain), or None (EGN_WGRAD_STREAM=0: one stream)."""
         if device.type != "cuda" or os.environ.get("EGN_WGRAD_STREAM", "1") == "0":
             return None
-        key = threading.get_ident()
+        key = (threading.get_ident(), index)
         if key not in self._side:
             self._side[key] = torch.cuda.Stream(device=device)
         return self._side[key]
@@ -269,6 +270,7 @@ class Engine:
         # referenced until the join at the next block, so no buffer is recycled under them.
         main = torch.cuda.current_stream() if bg.device.type == "cuda" else None
         side = self._side_stream(bg.device)
+        side2 = self._side_stream(bg.device, 1)
         pending = []
 
         def wg(g, x, out, bias_out=None):
@@ -329,22 +331,40 @@ class Engine:
                 h2_bar = L(m2_bar, w[p + "eu2.w2"], w_mn=True, aux=st["h2"], flags=ops.EPI_DSILU_AUX)
                 w1 = w[p + "eu2.w1"]
                 wg(h2_bar, st["m_new"], gr[p + "eu2.w1"][:, :de], gr[p + "eu2.b1"])
-                pv_bar = ops.aggregate_in_edges(bg.edge_ptr, bg.rev, h2_bar)
-                wg(pv_bar, st["v"], gr[p + "eu2.w1"][:, de:])
-                if v_ready is not None:
-                    main.wait_event(v_ready)
-                v_bar = L(pv_bar, w1[:, de:], w_mn=True, resid=v_bar)
+                # The node-level chain (EA + NU adjoints, engine.py:166-177: pv_bar -> v_bar ->
+                # hv_bar -> agg_bar) runs on a second side stream, overlapping the edge-sized
+                # m_new_bar product; the main stream joins it before the gather into m_new_bar.
+                if side2 is not None:
+                    side2.wait_stream(main)
+                with torch.cuda.stream(side2) if side2 is not None else contextlib.nullcontext():
+                    pv_bar = ops.aggregate_in_edges(bg.edge_ptr, bg.rev, h2_bar)
+                    if v_ready is not None:
+                        side2.wait_event(v_ready)
+                    v_bar = L(pv_bar, w1[:, de:], w_mn=True, resid=v_bar)
+                    hv_bar = L(v_bar, w[p + "nu.w2"], w_mn=True, aux=st["hv"], flags=ops.EPI_DSILU_AUX)
+                    agg_bar = L(hv_bar, w[p + "nu.w1"], w_mn=True)
+                node_ready = None
+                if side2 is not None:
+                    node_ready = torch.cuda.Event()
+                    node_ready.record(side2)
+                    pending.append((h2_bar, pv_bar, v_bar, hv_bar, agg_bar))
                 m_new_bar = L(h2_bar, w1[:, :de], w_mn=True, resid=m2_bar)
+                if node_ready is not None:
+                    main.wait_event(node_ready)
+                wg(pv_bar, st["v"], gr[p + "eu2.w1"][:, de:])
+                wg(v_bar, st["av"], gr[p + "nu.w2"], gr[p + "nu.b2"])
+                wg(hv_bar, st["agg"], gr[p + "nu.w1"], gr[p + "nu.b1"])
+                ops.gather_rows(bg.recv, agg_bar, out=m_new_bar, accumulate=True)
             else:
                 m_new_bar = m_bar  # dead after this point of the block
-            # EA + NU (engine.py:166-177)
-            wg(v_bar, st["av"], gr[p + "nu.w2"], gr[p + "nu.b2"])
-            if v_ready is not None:
-                main.wait_event(v_ready)
-            hv_bar = L(v_bar, w[p + "nu.w2"], w_mn=True, aux=st["hv"], flags=ops.EPI_DSILU_AUX)
-            wg(hv_bar, st["agg"], gr[p + "nu.w1"], gr[p + "nu.b1"])
-            agg_bar = L(hv_bar, w[p + "nu.w1"], w_mn=True)
-            ops.gather_rows(bg.recv, agg_bar, out=m_new_bar, accumulate=True)
+                # EA + NU (engine.py:166-177)
+                wg(v_bar, st["av"], gr[p + "nu.w2"], gr[p + "nu.b2"])
+                if v_ready is not None:
+                    main.wait_event(v_ready)
+                hv_bar = L(v_bar, w[p + "nu.w2"], w_mn=True, aux=st["hv"], flags=ops.EPI_DSILU_AUX)
+                wg(hv_bar, st["agg"], gr[p + "nu.w1"], gr[p + "nu.b1"])
+                agg_bar = L(hv_bar, w[p + "nu.w1"], w_mn=True)
+                ops.gather_rows(bg.recv, agg_bar, out=m_new_bar, accumulate=True)
             # EU (engine.py:152-158)
             wg(m_new_bar, st["a1"], gr[p + "eu.w2"], gr[p + "eu.b2"])
             h_bar = L(m_new_bar, w[p + "eu.w2"], w_mn=True, aux=st["h"], flags=ops.EPI_DSILU_AUX)
