@@ -119,10 +119,15 @@ class Engine:
         self.config = weights.config
         self._side = {}  # per host thread: the stream weight gradients run on (backward)
 
-    def _side_stream(self, device, index: int = 0):
+    def _side_stream(self, bg, index: int = 0):
         """Side stream `index` of this host thread (0: weight gradients and graph-level work,
-        1: the node-level adjoint chain), or None (EGN_WGRAD_STREAM=0: one stream)."""
+        1: the node-level adjoint chain), or None: EGN_WGRAD_STREAM=0, or a batch below
+        EGN_SIDE_MIN_EDGES edges (default 16384), whose kernels are too short for the
+        fork / join to pay in an eagerly launched step (relaxation of one small system)."""
+        device = bg.device
         if device.type != "cuda" or os.environ.get("EGN_WGRAD_STREAM", "1") == "0":
+            return None
+        if bg.num_edges < int(os.environ.get("EGN_SIDE_MIN_EDGES", "16384")):
             return None
         key = (threading.get_ident(), index)
         if key not in self._side:
@@ -173,7 +178,7 @@ class Engine:
         de = c.d_e
         L = ops.linear
         folded = self._folded_weights()
-        side = self._side_stream(bg.device)
+        side = self._side_stream(bg)
         rbf = ops.rbf(bg.geo, c.k_rbf, c.cutoff)
         m = ops.rbf_linear(rbf, w["edge_init.w"], w["edge_init.b"])  # K = k_rbf (6)
         u = torch.zeros((bg.num_graphs, c.d_u), dtype=torch.float32, device=bg.device)
@@ -269,8 +274,8 @@ class Engine:
         # Same kernels, same order per stream: results are unchanged.  Their operands stay
         # referenced until the join at the next block, so no buffer is recycled under them.
         main = torch.cuda.current_stream() if bg.device.type == "cuda" else None
-        side = self._side_stream(bg.device)
-        side2 = self._side_stream(bg.device, 1)
+        side = self._side_stream(bg)
+        side2 = self._side_stream(bg, 1)
         pending = []
 
         def wg(g, x, out, bias_out=None):
