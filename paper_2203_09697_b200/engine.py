@@ -419,11 +419,19 @@ class Engine:
             wg(down_bar, st["m"], gr[p + "tu.down"])
             m_bar = L(down_bar, w[p + "tu.down"], w_mn=True, resid=m_in_bar)
         join()
-        ops.small_gemms(post)  # every deferred weight-sized gradient product, one launch
+        # every deferred weight-sized gradient product in one launch, on the side stream next to
+        # the edge-init / geometry adjoints
+        if side is not None:
+            side.wait_stream(main)
+        with torch.cuda.stream(side) if side is not None else contextlib.nullcontext():
+            ops.small_gemms(post)
         # edge init (engine.py:109-111), K = k_rbf
         ops.rbf_linear_bwd(fw.rbf, w["edge_init.w"], m_bar, rbf_bar, gr["edge_init.w"], gr["edge_init.b"])
         ops.rbf_bwd(bg.geo, rbf_bar, c.cutoff, eg)
-        return ops.positions_bwd(bg.edge_ptr, bg.rev, bg.geo, eg)
+        pos_bar = ops.positions_bwd(bg.edge_ptr, bg.rev, bg.geo, eg)
+        if side is not None:
+            main.wait_stream(side)
+        return pos_bar
 
     # -- debug / parity ------------------------------------------------------
     def triplet_features(self, bg: BatchGraph, fw: ForwardResult, block: int) -> torch.Tensor:
