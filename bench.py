@@ -218,18 +218,39 @@ def run_reference(args, wl):
 # GPU path
 # ---------------------------------------------------------------------------
 def _time_kernel(fn, iters, flush):
+    """Device time of one launch of fn with a cold L2: `iters` (256 MB flush, fn) pairs captured
+    in one CUDA graph, minus a graph of the flushes alone, timed with CUDA events on the
+    capturing stream.  No host launch gap enters the interval."""
     import torch
 
-    times = []
-    for _ in range(iters):
-        flush.zero_()
-        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        s.record()
-        fn()
-        e.record()
+    fn()
+    torch.cuda.synchronize()
+    st = torch.cuda.Stream()
+    st.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(st):
+        g_run, g_flush = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g_run, stream=st):
+            for _ in range(iters):
+                flush.zero_()
+                fn()
+        with torch.cuda.graph(g_flush, stream=st):
+            for _ in range(iters):
+                flush.zero_()
+    torch.cuda.current_stream().wait_stream(st)
+
+    def replay(g):
+        with torch.cuda.stream(st):
+            g.replay()
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record(st)
+            g.replay()
+            e.record(st)
         torch.cuda.synchronize()
-        times.append(s.elapsed_time(e) / 1000.0)
-    return float(np.median(times))
+        return s.elapsed_time(e) / 1000.0
+
+    t = (replay(g_run) - replay(g_flush)) / iters
+    del g_run, g_flush
+    return float(t)
 
 
 def _kernel_roofline(tr, bg, cfg):
