@@ -90,7 +90,8 @@ int egn_triplet_angles(const double* pos, const int64_t* edge_ptr, const int32_t
  * nimg[3g..3g+2] = (na, nb, nc) images per axis (0 on a non-periodic axis).
  * Image index img = ((i+na)(2nb+1) + (j+nb))(2nc+1) + (k+nc) for i in [-na, na] ...;
  * shift s = (i c0 + j c1) + k c2 per component (fp64, round-to-nearest, no FMA).
- * An edge (a, b, img) has the vector (x_b + s) - x_a and exists iff
+ * An edge (a, b, img) has the vector (x_b - x_a) + s (exactly antisymmetric, so
+ * every edge has its reverse) and exists iff
  * 0 < |v| <= cutoff (and not (b == a, s == 0)); each row is ordered by (b, img),
  * so a row is sorted by (recv, img) and the reverse of (a, b, img) is
  * (b, a, n_img - 1 - img).  Degrees/counts/triplets then follow the
@@ -122,7 +123,7 @@ int egn_cap_compact(const int64_t* edge_ptr, const int64_t* new_ptr, int64_t num
                     const int32_t* keep, const int32_t* src, const int32_t* recv, const int32_t* img,
                     const double* shift, const int32_t* rev, int32_t* new_id, int32_t* nsrc, int32_t* nrecv,
                     int32_t* nimg, double* nshift, int32_t* nrev, egn_stream_t stream);
-/* egn_geometry / egn_triplet_angles on edge vectors (x_recv + shift) - x_src; shift NULL
+/* egn_geometry / egn_triplet_angles on edge vectors (x_recv - x_src) + shift; shift NULL
  * gives the non-periodic results bit for bit. */
 int egn_geometry_shift(const double* pos, const int32_t* src, const int32_t* recv, const double* shift,
                        int64_t num_edges, float* geo, double* dist64, double* unit64, egn_stream_t stream);

@@ -161,7 +161,7 @@ class Graph:
     units: np.ndarray
     angles: np.ndarray
     rev: np.ndarray = field(default=None)
-    # periodic graphs: edge vectors (x_recv + shift) - x_src and the
+    # periodic graphs: edge vectors (x_recv - x_src) + shift and the
     # image index per edge; None for the reference's non-periodic graphs
     vec: np.ndarray = field(default=None)
     img: np.ndarray = field(default=None)
@@ -306,7 +306,7 @@ def image_shifts(cell, nimg):
 
 
 def build_graph_pbc(pos, cell, pbc, cutoff) -> Graph:
-    """Periodic cutoff graph: edges (a, b, img) with 0 < |(x_b + s_img) - x_a| <= cutoff
+    """Periodic cutoff graph: edges (a, b, img) with 0 < |(x_b - x_a) + s_img| <= cutoff
     (not b == a in the home image), rows ordered by (b, img); reverse = (b, a, mirrored
     img); triplets of out-edge (j -> i') pair it with every in-edge (k -> j) that is not its
     own reverse, in the order of the centre's out-edges (for a non-periodic cell this is
@@ -319,16 +319,17 @@ def build_graph_pbc(pos, cell, pbc, cutoff) -> Graph:
     shifts = image_shifts(cell, nimg)
     n_img = shifts.shape[0]
     centre = n_img // 2
-    # candidate (a, b, img): vector (x_b + s) - x_a, same operation order as the kernels
-    shifted = pos[None, :, :] + shifts[:, None, :]  # [img, b, 3]
-    diff = shifted[None, :, :, :] - pos[:, None, None, :]  # [a, img, b, 3]
+    # candidate (a, b, img): vector (x_b - x_a) + s, same operation order as the kernels.  This
+    # form is exactly antisymmetric under (a, b, s) -> (b, a, -s), so every edge has its
+    # reverse; it equals the supercell reference's (x_b + s) - x_a to within an ulp
+    diff = (pos[None, None, :, :] - pos[:, None, None, :]) + shifts[None, :, None, :]  # [a, img, b, 3]
     dist = np.sqrt((diff * diff).sum(axis=3))
     mask = (dist > 0.0) & (dist <= cutoff)
     mask[np.arange(n), centre, np.arange(n)] = False
     mask = mask.transpose(0, 2, 1)  # [a, b, img]: row-major nonzero = (a, b, img) order
     src, recv, img = (x.astype(np.int64) for x in np.nonzero(mask))
     shift = shifts[img]
-    vec = (pos[recv] + shift) - pos[src]
+    vec = (pos[recv] - pos[src]) + shift
     d = np.sqrt((vec * vec).sum(axis=1))
     units = vec / d[:, None] if src.size else np.zeros((0, 3))
     key = {(int(a), int(b), int(m)): e for e, (a, b, m) in enumerate(zip(src, recv, img))}

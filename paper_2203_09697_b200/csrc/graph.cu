@@ -230,7 +230,7 @@ __global__ void triplet_angles_kernel(const double* __restrict__ pos,
 // Periodic cells.  Per graph: cell rows c0, c1, c2 (lattice vectors)
 // and image ranges nimg = (na, nb, nc); image index img = ((i+na)(2nb+1) + (j+nb))(2nc+1)
 // + (k+nc) for the shift s = (i c0 + j c1) + k c2 (per component, round-to-nearest, no FMA).
-// An edge (a, b, img) is the vector (x_b + s) - x_a; candidates of a row are ordered by
+// An edge (a, b, img) is the vector (x_b - x_a) + s; candidates of a row are ordered by
 // (b, img), so rows are sorted by (recv, img) and the mirrored image of img is
 // n_img - 1 - img.
 struct Img {
@@ -258,10 +258,11 @@ __device__ __forceinline__ void img_shift(const double* __restrict__ cell, int g
 }
 __device__ __forceinline__ double pair_dist_shift(const double* __restrict__ pos, int64_t a, int64_t b, double sx,
                                                   double sy, double sz) {
-  const double bx = __dadd_rn(pos[3 * b + 0], sx), by = __dadd_rn(pos[3 * b + 1], sy),
-               bz = __dadd_rn(pos[3 * b + 2], sz);
-  const double dx = __dsub_rn(bx, pos[3 * a + 0]), dy = __dsub_rn(by, pos[3 * a + 1]),
-               dz = __dsub_rn(bz, pos[3 * a + 2]);
+  // (x_b - x_a) + s: exactly antisymmetric under (a, b, s) -> (b, a, -s), so an edge and its
+  // reverse always pass or fail the cutoff together (s = 0: the reference's x_b - x_a)
+  const double dx = __dadd_rn(__dsub_rn(pos[3 * b + 0], pos[3 * a + 0]), sx);
+  const double dy = __dadd_rn(__dsub_rn(pos[3 * b + 1], pos[3 * a + 1]), sy);
+  const double dz = __dadd_rn(__dsub_rn(pos[3 * b + 2], pos[3 * a + 2]), sz);
   return __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz)));
 }
 
@@ -345,18 +346,16 @@ __global__ void reverse_edges_pbc_kernel(const int64_t* __restrict__ edge_ptr, c
   }
 }
 
-// Edge geometry from (x_recv + shift) - x_src (shift NULL: the non-periodic form).
+// Edge geometry from (x_recv - x_src) + shift (shift NULL: the non-periodic form).
 __global__ void geometry_shift_kernel(const double* __restrict__ pos, const int32_t* __restrict__ src,
                                       const int32_t* __restrict__ recv, const double* __restrict__ shift, int64_t ne,
                                       float4* __restrict__ geo, double* __restrict__ dist64,
                                       double* __restrict__ unit64) {
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < ne; e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t a = src[e], b = recv[e];
-    const double bx = __dadd_rn(pos[3 * b + 0], shift[3 * e + 0]);
-    const double by = __dadd_rn(pos[3 * b + 1], shift[3 * e + 1]);
-    const double bz = __dadd_rn(pos[3 * b + 2], shift[3 * e + 2]);
-    const double dx = __dsub_rn(bx, pos[3 * a + 0]), dy = __dsub_rn(by, pos[3 * a + 1]),
-                 dz = __dsub_rn(bz, pos[3 * a + 2]);
+    const double dx = __dadd_rn(__dsub_rn(pos[3 * b + 0], pos[3 * a + 0]), shift[3 * e + 0]);
+    const double dy = __dadd_rn(__dsub_rn(pos[3 * b + 1], pos[3 * a + 1]), shift[3 * e + 1]);
+    const double dz = __dadd_rn(__dsub_rn(pos[3 * b + 2], pos[3 * a + 2]), shift[3 * e + 2]);
     const double d = __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz)));
     const double ux = __ddiv_rn(dx, d), uy = __ddiv_rn(dy, d), uz = __ddiv_rn(dz, d);
     geo[e] = make_float4(static_cast<float>(ux), static_cast<float>(uy), static_cast<float>(uz),
@@ -371,7 +370,7 @@ __global__ void geometry_shift_kernel(const double* __restrict__ pos, const int3
 }
 
 // Triplet angles from edge vectors: v1 = -vec(rev-side in-edge) = vec(off+q), v2 = vec(off+p),
-// vec(e) = (x_recv + shift) - x_src, all per the centre's out-edges.
+// vec(e) = (x_recv - x_src) + shift, all per the centre's out-edges.
 __global__ void triplet_angles_shift_kernel(const double* __restrict__ pos, const int64_t* __restrict__ edge_ptr,
                                             const int32_t* __restrict__ recv, const double* __restrict__ shift,
                                             const int64_t* __restrict__ tri_ptr, int64_t nv,
@@ -389,12 +388,12 @@ __global__ void triplet_angles_shift_kernel(const double* __restrict__ pos, cons
       const int64_t q = r < p ? r : r + 1;
       const int64_t eq = off + q, ep = off + p;
       const int64_t kk = recv[eq], ii = recv[ep];
-      const double v1x = __dsub_rn(__dadd_rn(pos[3 * kk], shift[3 * eq]), xj);
-      const double v1y = __dsub_rn(__dadd_rn(pos[3 * kk + 1], shift[3 * eq + 1]), yj);
-      const double v1z = __dsub_rn(__dadd_rn(pos[3 * kk + 2], shift[3 * eq + 2]), zj);
-      const double v2x = __dsub_rn(__dadd_rn(pos[3 * ii], shift[3 * ep]), xj);
-      const double v2y = __dsub_rn(__dadd_rn(pos[3 * ii + 1], shift[3 * ep + 1]), yj);
-      const double v2z = __dsub_rn(__dadd_rn(pos[3 * ii + 2], shift[3 * ep + 2]), zj);
+      const double v1x = __dadd_rn(__dsub_rn(pos[3 * kk], xj), shift[3 * eq]);
+      const double v1y = __dadd_rn(__dsub_rn(pos[3 * kk + 1], yj), shift[3 * eq + 1]);
+      const double v1z = __dadd_rn(__dsub_rn(pos[3 * kk + 2], zj), shift[3 * eq + 2]);
+      const double v2x = __dadd_rn(__dsub_rn(pos[3 * ii], xj), shift[3 * ep]);
+      const double v2y = __dadd_rn(__dsub_rn(pos[3 * ii + 1], yj), shift[3 * ep + 1]);
+      const double v2z = __dadd_rn(__dsub_rn(pos[3 * ii + 2], zj), shift[3 * ep + 2]);
       const double cx = __dsub_rn(__dmul_rn(v1y, v2z), __dmul_rn(v1z, v2y));
       const double cy = __dsub_rn(__dmul_rn(v1z, v2x), __dmul_rn(v1x, v2z));
       const double cz = __dsub_rn(__dmul_rn(v1x, v2y), __dmul_rn(v1y, v2x));

@@ -41,8 +41,8 @@ class BatchGraph:
     graph_sizes: list  # host: atoms per graph
     edge_counts: list | None = None  # host: edges per graph (lazily)
     max_deg: int = 0  # host: max out-degree (sizes the backward tile)
-    # periodic batches: per-edge image index and shift (x_recv + shift
-    # - x_src is the edge vector), per-graph cell / image ranges; None when non-periodic
+    # periodic batches: per-edge image index and shift ((x_recv - x_src)
+    # + shift is the edge vector), per-graph cell / image ranges; None when non-periodic
     img: torch.Tensor | None = None  # i32 [E]
     shift: torch.Tensor | None = None  # f64 [E, 3]
     cell: torch.Tensor | None = None  # f64 [G, 3, 3]
@@ -196,7 +196,7 @@ def build_batch(systems, cutoff: float, device="cuda", positions: torch.Tensor |
     edge_ptr = ops.scan_counts(deg)
     tri_ptr = ops.scan_counts(deg, square_minus_one=True)
     dmax = deg.max().to(torch.int64) if pos.shape[0] else edge_ptr[-1]
-    counts = torch.stack([edge_ptr[-1], tri_ptr[-1], dmax]).cpu()  # the one host sync
+    counts = torch.stack([edge_ptr[-1], tri_ptr[-1], dmax]).cpu()  # host sync 1: sizes
     ne, nt, max_deg = int(counts[0]), int(counts[1]), int(counts[2])
     img = shift = cell_keep = nimg_keep = None
     if per is not None:
@@ -207,6 +207,11 @@ def build_batch(systems, cutoff: float, device="cuda", positions: torch.Tensor |
     else:
         src, recv = ops.neighbors_fill(pos, graph_ptr, node_graph, cutoff, edge_ptr, ne)
         rev, missing = ops.reverse_edges(edge_ptr, src, recv)
+    # host sync 2: every edge must have its reverse (egn/graph.py:52-53 raises otherwise);
+    # rev = -1 would index row -1 in every gather / scatter downstream
+    if ne and int(missing.item()):
+        bad = int(torch.nonzero(rev < 0)[0].item())
+        raise ValueError(f"edge {bad} ({int(src[bad])} -> {int(recv[bad])}) has no reverse edge")
     if max_neighbors is not None:
         if max_neighbors < 0:
             raise ValueError("max_neighbors must be >= 0")

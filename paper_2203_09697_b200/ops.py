@@ -87,7 +87,7 @@ def reverse_edges_pbc(edge_ptr, src, recv, img, node_graph, nimg):
 
 
 def geometry(pos, src, recv, want_fp64=False, shift=None):
-    """Packed fp32 (u, d) per edge (+ fp64 d and u); edge vector (x_recv + shift) - x_src."""
+    """Packed fp32 (u, d) per edge (+ fp64 d and u); edge vector (x_recv - x_src) + shift."""
     e = src.shape[0]
     geo = torch.empty((e, 4), dtype=torch.float32, device=pos.device)
     d64 = u64 = None
@@ -224,16 +224,26 @@ def triplet_fwd(edge_ptr, rev, geo, X, Wk, cutoff, max_degree=-1):
 
 
 _WS: dict = {}
+# Workspaces that were outgrown are retired, never freed: a captured CUDA graph (Trainer.step)
+# holds raw pointers into the buffer that was current at capture time, and its replays must
+# keep writing valid memory even after a later, larger call replaced that buffer.
+_WS_RETIRED: list = []
+
+
+def _workspace_named(name: str, nbytes: int, device, minimum: int = 1 << 16) -> torch.Tensor:
+    # per thread: in-process graph-parallel ranks (runtime.ThreadComm) share a stream
+    key = (str(device), name, threading.get_ident())
+    buf = _WS.get(key)
+    if buf is None or buf.numel() < nbytes:
+        if buf is not None:
+            _WS_RETIRED.append(buf)
+        buf = torch.empty(max(nbytes, minimum), dtype=torch.uint8, device=device)
+        _WS[key] = buf
+    return buf
 
 
 def _workspace(nbytes: int, device) -> torch.Tensor:
-    # per thread: in-process graph-parallel ranks (runtime.ThreadComm) share a stream
-    key = (str(device), "ws", threading.get_ident())
-    buf = _WS.get(key)
-    if buf is None or buf.numel() < nbytes:
-        buf = torch.empty(max(nbytes, 1 << 20), dtype=torch.uint8, device=device)
-        _WS[key] = buf
-    return buf
+    return _workspace_named("ws", nbytes, device, 1 << 20)
 
 
 def triplet_bwd(edge_ptr, rev, geo, X, Wk, cutoff, S_bar, edge_grad, X_bar=None, W_bar=None, max_degree=None):
@@ -349,15 +359,6 @@ def column_sum(x, out=None):
     ws = _workspace_named("colsum", nbytes, x.device)
     call("egn_column_sum", ptr(x), rows, d, x.stride(0), ptr(out), ptr(ws), stream())
     return out
-
-
-def _workspace_named(name: str, nbytes: int, device) -> torch.Tensor:
-    key = (str(device), name, threading.get_ident())
-    buf = _WS.get(key)
-    if buf is None or buf.numel() < nbytes:
-        buf = torch.empty(max(nbytes, 1 << 16), dtype=torch.uint8, device=device)
-        _WS[key] = buf
-    return buf
 
 
 def wgrad(g: torch.Tensor, x: torch.Tensor, out: torch.Tensor | None = None, splits: int = 64) -> torch.Tensor:

@@ -127,6 +127,25 @@ def test_periodic_graph_bit_exact(name):
     np.testing.assert_allclose(geom.angles.cpu().numpy(), ref.angles, rtol=0, atol=1e-12)
 
 
+def test_periodic_graph_symmetric_at_cutoff_boundary():
+    """Own +-2-cell images exactly at the cutoff (cell 3, cutoff 6): every edge has its reverse
+    (no rev = -1 reaches the model), and the GPU graph equals the oracle bit for bit."""
+    from paper_2203_09697_b200 import AtomicSystem
+    from paper_2203_09697_b200.graph import build_batch
+
+    rng = np.random.default_rng(7)
+    cell = np.eye(3) * 3.0
+    for _ in range(20):
+        pos = rng.uniform(0.0, 3.0, size=(2, 3))
+        ref = O.build_graph_pbc(pos, cell, (True, True, True), 6.0)
+        bg = build_batch(AtomicSystem(pos, np.full(2, 6), cell=cell, pbc=(True, True, True)), 6.0)
+        rev = bg.rev.cpu().numpy()
+        assert rev.min() >= 0
+        np.testing.assert_array_equal(rev, ref.rev)
+        np.testing.assert_array_equal(bg.src.cpu().numpy(), ref.src)
+        np.testing.assert_array_equal(bg.img.cpu().numpy(), ref.img)
+
+
 def test_periodic_batch_mixes_periodic_and_open_graphs():
     from paper_2203_09697_b200 import AtomicSystem
     from paper_2203_09697_b200.graph import build_batch, topology_of

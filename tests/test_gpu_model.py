@@ -15,6 +15,25 @@ from oracle import egn_oracle as O
 
 pytestmark = pytest.mark.gpu
 
+
+@pytest.fixture(params=["default", "tcgen05"], autouse=True)
+def gemm_path(request, monkeypatch):
+    """Every model test runs twice: the default dispatch (node-row and small products on the
+    SIMT GEMM, one stream below EGN_SIDE_MIN_EDGES edges) and with every product forced onto
+    the tcgen05 3xTF32 GEMM (egn_gemm_simt_max_m = 0) and the three-stream schedule forced on
+    (EGN_SIDE_MIN_EDGES = 0) -- the code path the bench step runs at M = 58,644."""
+    from paper_2203_09697_b200 import _lib
+
+    if request.param == "default":
+        yield request.param
+        return
+    monkeypatch.setenv("EGN_SIDE_MIN_EDGES", "0")
+    old = _lib.call("egn_gemm_simt_max_m", 0)
+    try:
+        yield request.param
+    finally:
+        _lib.call("egn_gemm_simt_max_m", old)
+
 SMALL = ["model_dimenet_small.npz", "model_gemnet_small.npz", "model_gemnet_odd.npz", "model_dimenet_chain.npz"]
 LARGE = ["model_dimenet_c1dims.npz", "model_gemnet_c2dims.npz"]
 

@@ -123,18 +123,37 @@ PBC_NAMES = ["cubic4", "triclinic5", "slab6", "self_image1", "unwrapped5"]
 @pytest.mark.parametrize("name", PBC_NAMES)
 def test_periodic_graph_matches_reference_supercell(name):
     """Periodic neighbour list vs the reference build_graph on an explicit
-    supercell (tests/golden/pbc.npz): same (a, b, image) edges, bit-identical distances."""
+    supercell (tests/golden/pbc.npz): same (a, b, image) edges; distances within a few ulp of the coordinates (the
+    supercell materialises x_b + s before subtracting x_a, the kernels form (x_b - x_a) + s,
+    which is exactly antisymmetric so every edge has its reverse)."""
     gd = load_golden("pbc.npz")
     g = O.build_graph_pbc(gd[f"{name}/pos"], gd[f"{name}/cell"], gd[f"{name}/pbc"], float(gd[f"{name}/cutoff"]))
     np.testing.assert_array_equal(O.image_ranges(gd[f"{name}/cell"], gd[f"{name}/pbc"], float(gd[f"{name}/cutoff"]),
                                                  gd[f"{name}/pos"]), gd[f"{name}/nimg"])
-    for key, val in (("src", g.src), ("recv", g.recv), ("img", g.img), ("dist", g.dist)):
+    for key, val in (("src", g.src), ("recv", g.recv), ("img", g.img)):
         np.testing.assert_array_equal(val, gd[f"{name}/{key}"], err_msg=f"{name}/{key}")
+    # the two operation orders round differently at the scale of the coordinates (unwrapped
+    # inputs sit several cells out): a few ulp of max |x|
+    ref_d = gd[f"{name}/dist"]
+    scale = max(float(np.abs(gd[f"{name}/pos"]).max()) + float(np.abs(gd[f"{name}/cell"]).sum(0).max()), 1.0)
+    assert np.abs(g.dist - ref_d).max(initial=0.0) <= 8 * np.finfo(np.float64).eps * scale, name
     # reverse edges mirror the image; triplets never pair an edge with its own reverse
     n_img = int(np.prod(2 * gd[f"{name}/nimg"] + 1))
     assert np.array_equal(g.src[g.rev], g.recv) and np.array_equal(g.img[g.rev], n_img - 1 - g.img)
     assert not np.any(g.rev[g.trip_out] == g.trip_in)
     assert np.array_equal(g.recv[g.trip_in], g.src[g.trip_out])
+
+
+def test_periodic_graph_symmetric_at_cutoff_boundary():
+    """An atom's own +-2-cell images sit exactly at the cutoff (cell 3, cutoff 6): with the
+    antisymmetric edge vector (x_b - x_a) + s both directions pass or fail together, so the
+    graph always has every reverse edge (the oracle raises ValueError otherwise)."""
+    rng = np.random.default_rng(7)
+    for trial in range(40):
+        pos = rng.uniform(0.0, 3.0, size=(2, 3))
+        g = O.build_graph_pbc(pos, np.eye(3) * 3.0, (True, True, True), 6.0)
+        assert np.array_equal(g.src[g.rev], g.recv) and np.array_equal(g.rev[g.rev], np.arange(g.src.size))
+        assert np.array_equal(g.dist[g.rev], g.dist)
 
 
 def test_periodic_graph_without_images_is_the_reference_graph():
