@@ -12,17 +12,20 @@ per GPU at OC20-like density (random_cloud rho=0.06, cutoff 6 A, <=50
 neighbours), loss w_E = w_F = 1 against a teacher model (init_params(seed=1)).
 
 N > 1 (weak scaling, 32 graphs per GPU): graph parallelism over the global
-batch (runtime.GraphParallelEngine, NCCL).  ``--partition aligned`` (default)
-splits the centre range at graph boundaries, so edge/node exchanges are empty
-and only the per-graph GU sums, the loss, the position and the parameter
-gradients are all-reduced; ``--partition balanced`` splits by triplet count
-inside graphs (full edge/node all-gathers every block).
+batch (NCCL).  ``--partition aligned`` (default) gives every rank whole graphs
+(its own batch), so only the gradient and the loss are all-reduced;
+``--partition centre`` splits the centre range by triplet count inside graphs
+(runtime.GraphParallelEngine: own-row compute, asynchronous row all-gathers /
+reduce-scatters every block); ``--partition reference`` runs the reference's
+schedule (split_range shards, full-buffer all-reduces; runtime.ReferenceScheduleEngine).
 
 Prints ONE JSON line (rank 0).  ``value`` = triplet-interactions/s of the
 whole job = N_t(global batch) * blocks / t_step, device-timed (CUDA events,
-max over ranks) with inputs resident; ``e2e`` = the same metric with host
-buffers: H2D of positions + targets, graph build, step, D2H of the loss
-inside the timed region.  ``--impl reference`` times the CPU reference path
+max over ranks) with inputs resident; ``e2e`` = the same metric through Trainer.update_inputs / step
+with host buffers: H2D of positions + targets, geometry recomputed on the
+resident topology (a pass over a fixed dataset revisits the same graphs, as
+train_simple does; the neighbour list is built once per batch), the step, and
+the D2H of the loss inside the timed region.  ``--impl reference`` times the CPU reference path
 (the fp64 numpy oracle, a restatement of egn.ModelTape; oracle/egn_oracle.py)
 on the host cores for a bounded sample of the same workload.
 """
@@ -61,7 +64,7 @@ def _args():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="gemnet-t-oc20")
     ap.add_argument("--graphs", type=int, default=None, help="override graphs per GPU")
-    ap.add_argument("--partition", choices=["aligned", "balanced"], default="aligned")
+    ap.add_argument("--partition", choices=["aligned", "centre", "reference"], default="aligned")
     ap.add_argument("--cpu-budget", type=float, default=12.0, help="seconds of CPU oracle sampling")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-kernel-timing", action="store_true")
@@ -323,7 +326,7 @@ def run_ours(args, wl):
     from paper_2203_09697_b200 import _lib, init_params
     from paper_2203_09697_b200.engine import DeviceWeights, Engine
     from paper_2203_09697_b200.graph import build_batch
-    from paper_2203_09697_b200.partition import partition_centers
+    from paper_2203_09697_b200.partition import partition_centers, partition_reference
     from paper_2203_09697_b200.runtime import DistComm, GPTrainer
     from paper_2203_09697_b200.tasks import Trainer
 
@@ -367,10 +370,12 @@ def run_ours(args, wl):
         parallelism = f"gp{world} (graph-aligned centre partition: no halo, gradient all-reduce, {backend})"
     else:
         comm = DistComm()
-        cand = bg.graph_ptr.cpu().numpy() if args.partition == "aligned" else None
-        part = partition_centers(bg.deg.cpu().numpy(), world, candidates=cand)
+        if args.partition == "centre":
+            part = partition_centers(bg.deg.cpu().numpy(), world)
+        else:
+            part = partition_reference(bg.tri_ptr.cpu().numpy(), bg.num_edges, bg.num_nodes, world)
         tr = GPTrainer(params, bg, e_t, f_t, 1.0, wl["w_forces"], comm, part)
-        parallelism = f"gp{world} ({args.partition} centre partition, {backend})"
+        parallelism = f"gp{world} ({args.partition} schedule, halo exchanges every block, {backend})"
 
     def barrier():
         if world > 1:
@@ -422,10 +427,9 @@ def run_ours(args, wl):
             # positions and targets into the resident batch, recompute its geometry
             tr.update_inputs(pos, et, ft)
         else:
-            g = build_batch(None, cfg.cutoff, positions=pos, sizes=sizes)
-            n0, n1 = tr.engine.n0, tr.engine.n1
-            tr.bg, tr.e_target = g, et
-            tr.f_target = ft[n0:n1] if ft is not None else None
+            tr.bg.update_positions(pos)
+            tr.e_target = et
+            tr.f_target = ft[tr.n0:tr.n1] if ft is not None else None
         loss_host[i].copy_(tr.step(lr).reshape(()), non_blocking=True)
 
     for i in range(2):

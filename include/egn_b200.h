@@ -164,6 +164,21 @@ int egn_triplet_fwd(const int64_t* edge_ptr, const int32_t* rev, const float* ge
                     int64_t num_nodes, int max_degree, const float* X, const float* W, int k_rbf,
                     int l_sbf, int dg, double cutoff, float* S, egn_stream_t stream);
 
+/* Triplet window (graph-parallel reference schedule: one split_range shard of the triplet
+ * list, egn/partition.py:28-37, egn/runtime.py:425-431).  The launch covers the centres of
+ * edge_ptr[0 .. num_nodes] and keeps only triplets whose centre-local index
+ * k = p (n-1) + (q < p ? q : q-1) is >= first_lo at the first centre and < last_hi at the last;
+ * the kept terms are summed exactly as egn_triplet_fwd does (rows of every covered centre are
+ * written, zero where no triplet of the row is kept). */
+int egn_triplet_fwd_window(const int64_t* edge_ptr, const int32_t* rev, const float* geo, int64_t num_nodes,
+                           int64_t first_lo, int64_t last_hi, const float* X, const float* W, int k_rbf, int l_sbf,
+                           int dg, double cutoff, float* S, egn_stream_t stream);
+/* Adjoint of egn_triplet_fwd_window: X_bar rows rev(q) of the covered centres overwritten,
+ * W_bar overwritten, edge_grad accumulated (workspace: egn_triplet_bwd_workspace_bytes). */
+int egn_triplet_bwd_window(const int64_t* edge_ptr, const int32_t* rev, const float* geo, int64_t num_nodes,
+                           int64_t first_lo, int64_t last_hi, int max_degree, const float* X, const float* W,
+                           int k_rbf, int l_sbf, int dg, double cutoff, const float* S_bar, float* X_bar,
+                           float* W_bar, float* edge_grad, void* workspace, egn_stream_t stream);
 /* Adjoint of egn_triplet_fwd (tape.py gather/segment_sum/linear/angular_sbf VJPs).
  * Inputs S_bar [E,dg].  Outputs:
  *   X_bar [E, dg]            (overwritten),
@@ -212,7 +227,9 @@ int egn_graph_sum(const int64_t* graph_ptr, int64_t num_graphs, const float* x, 
                   float* out, egn_stream_t stream);
 
 /* GemNet direct force head (record_force_head, engine.py:234-246):
- *   s_e = m_e . w ; f[v] = sum_{recv(e)=v} s_e u_e.  scale [E] is an output. */
+ *   s_e = m_e . w ; f[v] = sum_{recv(e)=v} s_e u_e.  scale [E] is an output.
+ * m NULL: scale is an input (the graph-parallel runtime all-gathers it between the two
+ * halves); forces NULL: only the per-edge dot products s_e. */
 int egn_force_head_fwd(const int64_t* edge_ptr, const int32_t* rev, const float* geo,
                        int64_t num_nodes, int64_t num_edges, const float* m, int d,
                        const float* w, float* scale, float* forces, egn_stream_t stream);
@@ -315,6 +332,37 @@ int egn_graph_mlp_fwd(int64_t num_graphs, int dv, int du, const float* s, const 
 int egn_graph_mlp_bwd(int64_t num_graphs, int dv, int du, const float* u_bar, const float* s, const float* pre,
                       const float* act, const float* w1, const float* w2, float* pre_bar, float* s_bar,
                       float* w1_bar, float* b1_bar, float* w2_bar, float* b2_bar, egn_stream_t stream);
+/* w1 NULL in egn_graph_mlp_fwd / _bwd: the first layer is the identity (dv == du; its input
+ * is the already projected, all-reduced z of the graph-parallel reference schedule,
+ * egn/runtime.py:477-484 + egn/engine.py:214-217); w1_bar may then be NULL. */
+/* GU head z = x W^T (+ b) over G rows (egn/engine.py:207-211, record_gu_head); w NULL = identity. */
+int egn_graph_linear(int64_t num_graphs, int din, int dout, const float* x, const float* w, const float* b, float* y,
+                     egn_stream_t stream);
+/* Adjoint: x_bar = y_bar W, w_bar = y_bar^T x, b_bar = column sums of y_bar (each optional). */
+int egn_graph_linear_bwd(int64_t num_graphs, int din, int dout, const float* y_bar, const float* x, const float* w,
+                         float* x_bar, float* w_bar, float* b_bar, egn_stream_t stream);
+
+/* ------------------------------------------------------------------ */
+/* Basis tables and geometry derivatives at the public API (fp64)      */
+/* ------------------------------------------------------------------ */
+/* rbf_features (egn/basis.py:35-42): out[e, k] = exp(-gamma (d_e - c_k)^2), c = linspace(0,
+ * cutoff, K), gamma = (K / cutoff)^2; d_out (optional) = d/dd (rbf_features_ddist :45-51).
+ * invalid (optional device int32) is set to 1 when some d lies outside (0, cutoff] (the
+ * reference raises ValueError; the binding checks the flag). */
+int egn_rbf_features(const double* distances, int64_t n, int k_rbf, double cutoff, double* out, double* d_out,
+                     int32_t* invalid, egn_stream_t stream);
+/* sbf_features (egn/basis.py:54-74): out[t, k L + l] = rbf_k(d_t) cos(l a_t); d_dist / d_ang
+ * (optional) = sbf_features_partials (:77-95); invalid also flags angles outside [0, pi]. */
+int egn_sbf_features(const double* in_edge_distances, const double* angles, int64_t n, int k_rbf, int l_sbf,
+                     double cutoff, double* out, double* d_dist, double* d_ang, int32_t* invalid,
+                     egn_stream_t stream);
+/* geometry_grads (egn/gradients.py:33-36): distance gradients -u / +u per edge [E, 3] and the
+ * closed-form angle gradients at k, j, i per triplet [N_t, 3] (egn/graph.py:173-203; zero for
+ * collinear triplets, |v1 x v2| <= 1e-14).  Indices int64 as in GraphTopology. */
+int egn_geometry_grads(const double* pos, const int64_t* src, const int64_t* recv, int64_t num_edges,
+                       const int64_t* trip_in, const int64_t* trip_out, int64_t num_triplets, double* dist_d_src,
+                       double* dist_d_recv, double* angle_d_k, double* angle_d_j, double* angle_d_i,
+                       egn_stream_t stream);
 
 /* ------------------------------------------------------------------ */
 /* Optimizer: train_simple SGD update (tasks.py:207-208)               */

@@ -8,8 +8,8 @@ include/egn_b200.h (libegn_b200.so).  See DESIGN.md.
 
 from .config import DIMENET, GEMNET, ModelConfig
 from .params import ModelParams, ParamSpec, init_params, load_params, param_specs, save_params, zero_params
-from .partition import (CenterPartition, CommModel, CommVolume, GraphPartition, comm_volume,
-                        partition_centers, partition_graph, split_range)
+from .partition import (CenterPartition, CommModel, CommVolume, GraphPartition, ReferencePartition, comm_volume,
+                        partition_centers, partition_graph, partition_reference, split_range)
 from .system import AtomicSystem, random_cloud
 
 __all__ = [
@@ -19,6 +19,9 @@ __all__ = [
     "AtomicSystem", "random_cloud", "build_graph", "build_batch", "EGNModel", "predict", "relax", "RelaxationResult",
     "loss_and_grads", "train_simple", "Trainer", "enumerate_triplets", "WorkerGroup", "ParallelRunResult",
     "GradientBundle", "CollectiveShapeError", "CollectiveTimeoutError", "WorkerGroupError",
+    "ModelTape", "BasisFeatures", "compute_basis", "rbf_features", "sbf_features", "initial_state", "block_forward",
+    "GeometryGrads", "backward", "forces_energy_centric", "geometry_grads", "FeatureState", "Collective", "CommLog",
+    "partition_reference", "ReferencePartition",
 ]
 
 
@@ -34,8 +37,14 @@ def __getattr__(name):
     if name in ("predict", "relax", "RelaxationResult", "loss_and_grads", "train_simple", "Trainer"):
         from . import tasks
         return getattr(tasks, name)
+    if name in ("ModelTape", "BasisFeatures", "compute_basis", "rbf_features", "rbf_features_ddist", "sbf_features",
+                "sbf_features_partials", "initial_state", "block_forward", "GeometryGrads", "backward",
+                "forces_energy_centric", "geometry_grads"):
+        from . import api
+        return getattr(api, name)
     if name in ("WorkerGroup", "ParallelRunResult", "GradientBundle", "CollectiveError", "CollectiveShapeError",
-                "CollectiveTimeoutError", "WorkerGroupError", "GraphParallelEngine", "GPTrainer"):
+                "CollectiveTimeoutError", "WorkerGroupError", "GraphParallelEngine", "GPTrainer", "FeatureState",
+                "Collective", "CommLog", "ReferenceScheduleEngine"):
         from . import runtime
         return getattr(runtime, name)
     if name in ("Engine", "DeviceWeights"):

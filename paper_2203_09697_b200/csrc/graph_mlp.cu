@@ -42,17 +42,20 @@ __device__ __forceinline__ float warp_dot(const float* __restrict__ x, const flo
   return warp_sum((a0 + a1) + (a2 + a3));
 }
 
-// layer 1 forward: pre = s W1^T + b1, act = silu(pre)
+// layer 1 forward: pre = s W1^T + b1, act = silu(pre).  W1 NULL: s is already projected
+// (pre = s + b1, dv == du; the graph-parallel reference schedule all-reduces z = s W1^T);
+// b1 / act NULL: no bias / no activation output (the bare linear z = s W1^T).
 __global__ void __launch_bounds__(256) fwd1_kernel(int dv, int du, const float* __restrict__ s,
                                                    const float* __restrict__ W1, const float* __restrict__ b1,
                                                    float* __restrict__ pre, float* __restrict__ act) {
   const int64_t r = blockIdx.x;
   const int j = blockIdx.y * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   if (j >= du) return;
-  const float h = warp_dot(s + r * dv, W1 + static_cast<int64_t>(j) * dv, dv, 1, lane) + b1[j];
+  float h = W1 ? warp_dot(s + r * dv, W1 + static_cast<int64_t>(j) * dv, dv, 1, lane) : s[r * dv + j];
+  if (b1) h += b1[j];
   if (lane == 0) {
     pre[r * du + j] = h;
-    act[r * du + j] = silu_f(h);
+    if (act) act[r * du + j] = silu_f(h);
   }
 }
 
@@ -78,13 +81,13 @@ __global__ void __launch_bounds__(256) bwd2_kernel(int du, const float* __restri
   if (lane == 0) pre_bar[r * du + j] = y * dsilu_f(pre[r * du + j]);
 }
 
-// backward layer 1: s_bar = pre_bar W1   (W1 columns)
+// backward layer 1: s_bar = pre_bar W1   (W1 columns; W1 NULL: s_bar = pre_bar)
 __global__ void __launch_bounds__(256) bwd1_kernel(int dv, int du, const float* __restrict__ pre_bar,
                                                    const float* __restrict__ W1, float* __restrict__ s_bar) {
   const int64_t r = blockIdx.x;
   const int i = blockIdx.y * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   if (i >= dv) return;
-  const float y = warp_dot(pre_bar + r * du, W1 + i, du, dv, lane);
+  const float y = W1 ? warp_dot(pre_bar + r * du, W1 + i, du, dv, lane) : pre_bar[r * du + i];
   if (lane == 0) s_bar[r * dv + i] = y;
 }
 
@@ -100,6 +103,8 @@ __global__ void __launch_bounds__(256) bwd_weights_kernel(int64_t G, int dv, int
                                                           float* __restrict__ gb2) {
   const int j = blockIdx.x;
   const bool l2 = blockIdx.y == 0;
+  // NULL outputs are skipped (the split head / tail of the graph-parallel reference schedule)
+  if (l2 && gW2 == nullptr && gb2 == nullptr) return;
   const float* lhs = l2 ? u_bar : pre_bar;  // [G, du], column j
   const float* rhs = l2 ? act : s;          // [G, width]
   const int width = l2 ? du : dv;
@@ -127,8 +132,9 @@ __global__ void __launch_bounds__(256) bwd_weights_kernel(int64_t G, int dv, int
       a = fmaf(l, __ldg(rhs + static_cast<int64_t>(g) * width + k), a);
       bsum += l;
     }
-    gw[static_cast<int64_t>(j) * width + k] = a;
-    if (k == 0) (l2 ? gb2 : gb1)[j] = bsum;
+    if (gw) gw[static_cast<int64_t>(j) * width + k] = a;
+    float* gb = l2 ? gb2 : gb1;
+    if (k == 0 && gb) gb[j] = bsum;
   }
 }
 
@@ -142,6 +148,7 @@ extern "C" int egn_graph_mlp_fwd(int64_t num_graphs, int dv, int du, const float
                                  float* u, egn_stream_t stream) {
   EGN_REQUIRE(dv >= 1 && du >= 1, "graph MLP dims must be positive");
   EGN_REQUIRE(num_graphs < 65536, "graph MLP: at most 65535 graphs per batch");
+  EGN_REQUIRE(w1 != nullptr || dv == du, "graph MLP: identity first layer needs dv == du");
   if (num_graphs == 0) return 0;
   cudaStream_t st = as_stream(stream);
   const dim3 grid(static_cast<unsigned>(num_graphs), (du + 7) / 8);
@@ -169,4 +176,37 @@ extern "C" int egn_graph_mlp_bwd(int64_t num_graphs, int dv, int du, const float
   gmlp::bwd_weights_kernel<<<dim3(du, 2), 256, 0, st>>>(num_graphs, dv, du, u_bar, act, pre_bar, s, w1_bar, b1_bar,
                                                          w2_bar, b2_bar);
   return check_launch("graph_mlp_bwd_weights");
+}
+
+// z = x W^T (+ b) over G rows (the GU head of the graph-parallel reference schedule,
+// egn/engine.py:207-211: z = (sum of own v) W1^T, all-reduced before the tail).
+extern "C" int egn_graph_linear(int64_t num_graphs, int din, int dout, const float* x, const float* w,
+                                const float* b, float* y, egn_stream_t stream) {
+  EGN_REQUIRE(din >= 1 && dout >= 1, "graph linear dims must be positive");
+  EGN_REQUIRE(num_graphs < 65536, "graph linear: at most 65535 graphs per batch");
+  EGN_REQUIRE(w != nullptr || din == dout, "graph linear: identity needs din == dout");
+  if (num_graphs == 0) return 0;
+  const dim3 grid(static_cast<unsigned>(num_graphs), (dout + 7) / 8);
+  gmlp::fwd1_kernel<<<grid, 256, 0, as_stream(stream)>>>(din, dout, x, w, b, y, nullptr);
+  return check_launch("graph_linear");
+}
+
+// Adjoint of egn_graph_linear: x_bar = y_bar W, w_bar = y_bar^T x, b_bar = column sums of
+// y_bar (each output optional, graphs summed in order).
+extern "C" int egn_graph_linear_bwd(int64_t num_graphs, int din, int dout, const float* y_bar, const float* x,
+                                    const float* w, float* x_bar, float* w_bar, float* b_bar, egn_stream_t stream) {
+  EGN_REQUIRE(din >= 1 && dout >= 1, "graph linear dims must be positive");
+  EGN_REQUIRE(num_graphs < 65536, "graph linear: at most 65535 graphs per batch");
+  cudaStream_t st = as_stream(stream);
+  if (x_bar && num_graphs > 0) {
+    gmlp::bwd1_kernel<<<dim3(static_cast<unsigned>(num_graphs), (din + 7) / 8), 256, 0, st>>>(din, dout, y_bar, w,
+                                                                                               x_bar);
+    if (check_launch("graph_linear_bwd_x")) return 1;
+  }
+  if (w_bar || b_bar) {
+    gmlp::bwd_weights_kernel<<<dim3(dout, 2), 256, 0, st>>>(num_graphs, din, dout, nullptr, nullptr, y_bar, x, w_bar,
+                                                            b_bar, nullptr, nullptr);
+    return check_launch("graph_linear_bwd_w");
+  }
+  return 0;
 }

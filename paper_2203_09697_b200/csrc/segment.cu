@@ -751,12 +751,12 @@ int egn_graph_sum(const int64_t* graph_ptr, int64_t num_graphs, const float* x, 
 int egn_force_head_fwd(const int64_t* edge_ptr, const int32_t* rev, const float* geo,
                        int64_t num_nodes, int64_t num_edges, const float* m, int d,
                        const float* w, float* scale, float* forces, egn_stream_t stream) {
-  if (num_nodes == 0) return 0;
   cudaStream_t st = as_stream(stream);
-  if (num_edges > 0) {
+  if (num_edges > 0 && m != nullptr) {
     edge_dot_kernel<<<grid_for(num_edges * 32, 256), 256, 0, st>>>(m, num_edges, d, w, scale);
     if (check_launch("force_head_dot")) return 1;
   }
+  if (num_nodes == 0 || forces == nullptr) return 0;
   force_gather_warp_kernel<<<grid_for(num_nodes * 32, 256), 256, 0, st>>>(
       edge_ptr, rev, reinterpret_cast<const float4*>(geo), num_nodes, scale, forces);
   return check_launch("force_head_gather");

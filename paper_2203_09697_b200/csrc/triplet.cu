@@ -41,6 +41,19 @@ constexpr int kThreads = 128;
 constexpr int kMaxL = 8;
 constexpr int kMaxK = 16;
 
+// Triplet window (graph-parallel "reference" schedule, egn/partition.py:28-37): the launch
+// covers centres [0, nv) and keeps only the triplets whose centre-local index
+// k = p (n - 1) + (q < p ? q : q - 1) (the (out, in) order of enumerate_triplets) is >= first_lo
+// at centre 0 and < last_hi at centre nv - 1, so a contiguous split_range shard of the
+// triplet list is reproduced exactly even when it cuts through a centre's tile.
+struct TripWin {
+  int64_t first_lo, last_hi;
+};
+__device__ __forceinline__ bool in_window(const TripWin& w, int64_t j, int64_t nv, int n, int p, int q) {
+  const int64_t k = static_cast<int64_t>(p) * (n - 1) + (q < p ? q : q - 1);
+  return (j != 0 || k >= w.first_lo) && (j != nv - 1 || k < w.last_hi);
+}
+
 template <int CW, int GC>
 struct ChanMap {
   static constexpr int VW = CW < 4 ? CW : 4;
@@ -138,7 +151,7 @@ __global__ void __launch_bounds__(kThreads)
 triplet_fwd_kernel(const int64_t* __restrict__ edge_ptr, const int32_t* __restrict__ rev,
                    const float4* __restrict__ geo, int64_t nv, const float* __restrict__ X,
                    const float* __restrict__ W, int K, int L, int dg, int qt, RbfParams rp,
-                   float* __restrict__ S, int min_n) {
+                   float* __restrict__ S, int min_n, TripWin win) {
   using CM = ChanMap<CW, GC>;
   constexpr int GP = kThreads / GC, VW = CM::VW, DP = CM::DP;
   extern __shared__ __align__(16) float sm[];
@@ -177,7 +190,7 @@ triplet_fwd_kernel(const int64_t* __restrict__ edge_ptr, const int32_t* __restri
 #pragma unroll
           for (int r = 0; r < R; ++r) {
             float x = up[r].x * uq.x + up[r].y * uq.y + up[r].z * uq.z;
-            float m = pidx[r] != qg ? 1.f : 0.f;
+            float m = (pidx[r] != qg && in_window(win, j, nv, n, pidx[r], qg)) ? 1.f : 0.f;
             x2[r] = 2.f * x;
             tc[r] = m;       // T_0
             tp[r] = m * x;   // T_{-1} = T_1 = x
@@ -254,7 +267,7 @@ triplet_bwd_kernel(const int64_t* __restrict__ edge_ptr, const int32_t* __restri
                    const float4* __restrict__ geo, int64_t nv, const float* __restrict__ X,
                    const float* __restrict__ W, int K, int L, int dg, int qt, int nmax, int min_n, RbfParams rp,
                    const float* __restrict__ Sbar, float* __restrict__ Xbar,
-                   float* __restrict__ wbar_part, float4* __restrict__ edge_grad) {
+                   float* __restrict__ wbar_part, float4* __restrict__ edge_grad, TripWin win) {
   using CM = ChanMap<CW, GC>;
   constexpr int GP = kThreads / GC, VW = CM::VW, DP = CM::DP, PB = GP * R1;
   extern __shared__ __align__(16) float sm[];
@@ -353,7 +366,7 @@ triplet_bwd_kernel(const int64_t* __restrict__ edge_ptr, const int32_t* __restri
               float v = s[r];
 #pragma unroll
               for (int o = GC / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-              v = (pidx[r] < n && pidx[r] != qg) ? v : 0.f;
+              v = (pidx[r] < n && pidx[r] != qg && in_window(win, j, nv, n, pidx[r], qg)) ? v : 0.f;
               fr[r][0] = fmaf(v, uq.x - x[r] * up[r].x, fr[r][0]);
               fr[r][1] = fmaf(v, uq.y - x[r] * up[r].y, fr[r][1]);
               fr[r][2] = fmaf(v, uq.z - x[r] * up[r].z, fr[r][2]);
@@ -421,7 +434,7 @@ triplet_bwd_kernel(const int64_t* __restrict__ edge_ptr, const int32_t* __restri
         for (int t = 0; t < np; ++t) {
           const float4 up = Us[t];
           const float x = up.x * uq.x + up.y * uq.y + up.z * uq.z;
-          const float m = (p0 + t != q) ? 1.f : 0.f;
+          const float m = (p0 + t != q && in_window(win, j, nv, n, p0 + t, q)) ? 1.f : 0.f;
           float sbp[CW];
 #pragma unroll
           for (int i = 0; i < CW; i += VW) load_vec<VW>(Sbs + t * DP + CM::chan(cg, i), sbp + i);
@@ -602,7 +615,7 @@ static int pick_qt(int K, int L, int DP, int extra_floats, int budget_bytes) {
 template <int CW, int GC, int R>
 static int launch_fwd(const int64_t* edge_ptr, const int32_t* rev, const float4* geo, int64_t nv,
                       const float* X, const float* W, int K, int L, int dg, RbfParams rp, float* S,
-                      int min_n, cudaStream_t st) {
+                      int min_n, cudaStream_t st, TripWin win = TripWin{0, INT64_MAX}) {
   constexpr int DP = CW * GC;
   int qt = pick_qt(K, L, DP, 0, 48 * 1024);
   TileLayout Ly(qt, K, L, DP, 0);
@@ -614,7 +627,8 @@ static int launch_fwd(const int64_t* edge_ptr, const int32_t* rev, const float4*
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, smem);
   if (per_sm < 1) per_sm = 1;
   int64_t grid = std::min<int64_t>(nv, static_cast<int64_t>(kNumSMs) * per_sm * 4);
-  kern<<<static_cast<int>(grid), kThreads, smem, st>>>(edge_ptr, rev, geo, nv, X, W, K, L, dg, qt, rp, S, min_n);
+  kern<<<static_cast<int>(grid), kThreads, smem, st>>>(edge_ptr, rev, geo, nv, X, W, K, L, dg, qt, rp, S, min_n,
+                                                       win);
   return check_launch("triplet_fwd");
 }
 
@@ -622,7 +636,7 @@ template <int CW, int GC, int R>
 static int launch_bwd(const int64_t* edge_ptr, const int32_t* rev, const float4* geo, int64_t nv,
                       const float* X, const float* W, int K, int L, int dg, int max_deg, RbfParams rp,
                       const float* Sbar, float* Xbar, float* Wbar, float4* edge_grad, void* ws,
-                      int min_n, int accumulate, cudaStream_t st) {
+                      int min_n, int accumulate, cudaStream_t st, TripWin win = TripWin{0, INT64_MAX}) {
   constexpr int DP = CW * GC, GP = kThreads / GC, PB = GP * R;
   EGN_REQUIRE(max_deg >= 0, "triplet backward needs the maximum centre degree");
   const int nmax = max_deg > 2 ? max_deg : 2;
@@ -640,7 +654,7 @@ static int launch_bwd(const int64_t* edge_ptr, const int32_t* rev, const float4*
   const int grid = static_cast<int>(std::min<int64_t>(nv, static_cast<int64_t>(kNumSMs) * per_sm));
   float* part = reinterpret_cast<float*>(ws);
   kern<<<grid, kThreads, smem, st>>>(edge_ptr, rev, geo, nv, X, W, K, L, dg, qt, nmax, min_n, rp, Sbar, Xbar, part,
-                                     edge_grad);
+                                     edge_grad, win);
   if (check_launch("triplet_bwd")) return 1;
   const int64_t len = static_cast<int64_t>(K) * L * dg;
   reduce_partials_kernel<<<grid_for(len, 256), 256, 0, st>>>(part, grid, len, Wbar, accumulate);
@@ -742,6 +756,54 @@ int egn_triplet_bwd(const int64_t* edge_ptr, const int32_t* rev, const float* ge
 #define EGN_BWD(CW, GC, R) \
   return launch_bwd<CW, GC, R>(edge_ptr, rev, g4, num_nodes, X, W, k_rbf, l_sbf, dg, max_degree, rp, S_bar, X_bar, \
                                W_bar, eg, workspace, min_n, accumulate, st)
+  if (dg <= 4) EGN_BWD(4, 1, 1);
+  if (dg <= 8) EGN_BWD(8, 1, 1);
+  if (dg <= 16) EGN_BWD(8, 2, 2);
+  if (dg <= 32) EGN_BWD(8, 4, 2);
+  if (dg <= 64) EGN_BWD(8, 8, 4);
+  if (dg <= 128) EGN_BWD(8, 16, 4);
+  EGN_BWD(8, 32, 4);
+#undef EGN_BWD
+}
+
+int egn_triplet_fwd_window(const int64_t* edge_ptr, const int32_t* rev, const float* geo, int64_t num_nodes,
+                           int64_t first_lo, int64_t last_hi, const float* X, const float* W, int k_rbf, int l_sbf,
+                           int dg, double cutoff, float* S, egn_stream_t stream) {
+  if (int rc = check_dims(k_rbf, l_sbf, dg)) return rc;
+  if (num_nodes == 0) return 0;
+  RbfParams rp = rbf_params(k_rbf, cutoff);
+  const float4* g4 = reinterpret_cast<const float4*>(geo);
+  cudaStream_t st = as_stream(stream);
+  const TripWin win{first_lo, last_hi};
+#define EGN_FWD(CW, GC, R) \
+  return launch_fwd<CW, GC, R>(edge_ptr, rev, g4, num_nodes, X, W, k_rbf, l_sbf, dg, rp, S, -1, st, win)
+  if (dg <= 4) EGN_FWD(4, 1, 1);
+  if (dg <= 8) EGN_FWD(8, 1, 1);
+  if (dg <= 16) EGN_FWD(8, 2, 2);
+  if (dg <= 32) EGN_FWD(8, 4, 2);
+  if (dg <= 64) EGN_FWD(8, 8, 4);
+  if (dg <= 128) EGN_FWD(8, 16, 4);
+  EGN_FWD(8, 32, 4);
+#undef EGN_FWD
+}
+
+int egn_triplet_bwd_window(const int64_t* edge_ptr, const int32_t* rev, const float* geo, int64_t num_nodes,
+                           int64_t first_lo, int64_t last_hi, int max_degree, const float* X, const float* W,
+                           int k_rbf, int l_sbf, int dg, double cutoff, const float* S_bar, float* X_bar,
+                           float* W_bar, float* edge_grad, void* workspace, egn_stream_t stream) {
+  if (int rc = check_dims(k_rbf, l_sbf, dg)) return rc;
+  cudaStream_t st = as_stream(stream);
+  if (num_nodes == 0) {
+    cudaMemsetAsync(W_bar, 0, sizeof(float) * k_rbf * l_sbf * dg, st);
+    return check_launch("triplet_bwd_window_empty");
+  }
+  RbfParams rp = rbf_params(k_rbf, cutoff);
+  const float4* g4 = reinterpret_cast<const float4*>(geo);
+  float4* eg = reinterpret_cast<float4*>(edge_grad);
+  const TripWin win{first_lo, last_hi};
+#define EGN_BWD(CW, GC, R) \
+  return launch_bwd<CW, GC, R>(edge_ptr, rev, g4, num_nodes, X, W, k_rbf, l_sbf, dg, max_degree, rp, S_bar, X_bar, \
+                               W_bar, eg, workspace, -1, 0, st, win)
   if (dg <= 4) EGN_BWD(4, 1, 1);
   if (dg <= 8) EGN_BWD(8, 1, 1);
   if (dg <= 16) EGN_BWD(8, 2, 2);

@@ -19,8 +19,8 @@ float4 (dE/dv_e, dE/dd_e) that a final CSR gather turns into dE/dx.
 
 Edge- and node-sized dense products run on the native tcgen05 3xTF32 GEMM
 (ops.linear / ops.linear_wgrad, fused epilogues, bias adjoints folded into the
-weight-gradient kernel); only the K = k_rbf (6) products and the G-row global
-stage use cuBLAS fp32.  The graph-structured work (neighbour list, basis,
+weight-gradient kernel); the K = k_rbf (6) products, the G-row global stage and
+the energy head run on dedicated native kernels.  The graph-structured work (neighbour list, basis,
 triplet interaction, segment sums, force head, geometry adjoints, SGD) runs in
 the native library.
 """
@@ -172,7 +172,10 @@ class Engine:
         return out
 
     # -- forward -------------------------------------------------------------
-    def forward(self, bg: BatchGraph) -> ForwardResult:
+    def forward(self, bg: BatchGraph, m0: torch.Tensor | None = None, u0: torch.Tensor | None = None,
+                blocks: list | None = None) -> ForwardResult:
+        """Full forward; m0 / u0 / blocks (the reference's block_forward, egn/engine.py:281-317):
+        start from given edge / global features and run only the listed blocks."""
         c, w = self.config, self.weights.w
         gem = c.variant == GEMNET
         de = c.d_e
@@ -180,9 +183,11 @@ class Engine:
         folded = self._folded_weights()
         side = self._side_stream(bg)
         rbf = ops.rbf(bg.geo, c.k_rbf, c.cutoff)
-        m = ops.rbf_linear(rbf, w["edge_init.w"], w["edge_init.b"])  # K = k_rbf (6)
-        u = torch.zeros((bg.num_graphs, c.d_u), dtype=torch.float32, device=bg.device)
+        m = ops.rbf_linear(rbf, w["edge_init.w"], w["edge_init.b"]) if m0 is None else m0  # K = k_rbf (6)
+        u = (torch.zeros((bg.num_graphs, c.d_u), dtype=torch.float32, device=bg.device) if u0 is None
+             else u0.clone())
         v = None
+        order = list(range(c.blocks)) if blocks is None else list(blocks)
         blocks = []
         # the rbf gates of every block (K = k_rbf (6)) depend on the geometry only: side stream,
         # overlapping block 0's down-projection and triplet interaction
@@ -194,7 +199,7 @@ class Engine:
         if side is not None:
             gates_ready = torch.cuda.Event()
             gates_ready.record(side)
-        for b in range(c.blocks):
+        for b in order:
             p = f"block{b}."
             st = {"m": m}
             if gem:
@@ -250,7 +255,7 @@ class Engine:
             blocks.append(st)
         if side is not None:
             torch.cuda.current_stream().wait_stream(side)
-        energy = torch.addmm(w["energy_head.b"], u, w["energy_head.w"].t()).view(-1)
+        energy = ops.graph_linear(u, w["energy_head.w"], w["energy_head.b"]).view(-1)
         forces = scale = None
         if gem:
             scale, forces = ops.force_head_fwd(bg.edge_ptr, bg.rev, bg.geo, m, w["force_head.w"].view(-1))
@@ -295,9 +300,8 @@ class Engine:
         self.weights.grad_flat.zero_()
         eg = torch.zeros((bg.num_edges, 4), dtype=torch.float32, device=bg.device)
         dE = d_energy.to(torch.float32).view(-1, 1)
-        torch.mm(dE.t(), fw.u, out=gr["energy_head.w"])
-        gr["energy_head.b"].copy_(dE.sum(0))
-        u_bar = dE @ w["energy_head.w"]
+        u_bar = ops.graph_linear_bwd(dE, fw.u, w["energy_head.w"], w_bar=gr["energy_head.w"],
+                                     b_bar=gr["energy_head.b"])
         m_bar = torch.zeros((bg.num_edges, de), dtype=torch.float32, device=bg.device)
         if gem and d_forces is not None:
             ops.force_head_bwd(bg.recv, bg.geo, fw.m, w["force_head.w"].view(-1), fw.scale,
@@ -434,10 +438,11 @@ class Engine:
         return pos_bar
 
     # -- debug / parity ------------------------------------------------------
-    def triplet_features(self, bg: BatchGraph, fw: ForwardResult, block: int) -> torch.Tensor:
-        """t_feat of one block for every triplet in (out, in) order (engine.py:146,149)."""
+    def triplet_features(self, bg: BatchGraph, fw: ForwardResult, block: int, index: int | None = None) -> torch.Tensor:
+        """t_feat of one block for every triplet in (out, in) order (engine.py:146,149); index:
+        position of that block in fw.blocks when the forward ran a subset of blocks."""
         c, w = self.config, self.weights.w
-        st = fw.blocks[block]
+        st = fw.blocks[block if index is None else index]
         P = ops.triplet_terms(bg.edge_ptr, bg.rev, bg.geo, bg.tri_ptr, bg.num_triplets, st["X"], st["Wk"],
                               c.cutoff)
         _, ji = ops.triplets_fill(bg.edge_ptr, bg.rev, bg.tri_ptr, bg.num_triplets)

@@ -136,12 +136,14 @@ def rbf_linear(rbf_t, w, b=None, out=None):
 
 
 def graph_mlp_fwd(s, w1, b1, w2, b2, u):
-    """GU block over G graphs (egn_graph_mlp_fwd): returns (pre, act); u updated in place."""
+    """GU block over G graphs (egn_graph_mlp_fwd): returns (pre, act); u updated in place.
+    w1 None: identity first layer (s is the already projected z = s W1^T)."""
     g, dv = s.shape
-    du = w1.shape[0]
+    du = w1.shape[0] if w1 is not None else dv
     pre = torch.empty((g, du), dtype=torch.float32, device=s.device)
     act = torch.empty_like(pre)
-    call("egn_graph_mlp_fwd", g, dv, du, ptr(_c(s, torch.float32)), ptr(_c(w1, torch.float32)),
+    call("egn_graph_mlp_fwd", g, dv, du, ptr(_c(s, torch.float32)),
+         ptr(_c(w1, torch.float32)) if w1 is not None else None,
          ptr(_c(b1, torch.float32)), ptr(_c(w2, torch.float32)), ptr(_c(b2, torch.float32)), ptr(pre), ptr(act),
          ptr(u), stream())
     return pre, act
@@ -149,19 +151,42 @@ def graph_mlp_fwd(s, w1, b1, w2, b2, u):
 
 def graph_mlp_bwd(u_bar, s, pre, act, w1, w2, w1_bar, b1_bar, w2_bar, b2_bar):
     """Adjoint of graph_mlp_fwd (egn_graph_mlp_bwd): returns s_bar [G, dv]; weight / bias
-    adjoints written into the given (contiguous) views."""
+    adjoints written into the given (contiguous) views.  w1 None: identity first layer
+    (s is the projected z; s_bar = pre_bar, w1_bar unused)."""
     g, dv = s.shape
-    du = w1.shape[0]
+    du = w1.shape[0] if w1 is not None else dv
     pre_bar = torch.empty((g, du), dtype=torch.float32, device=s.device)
     s_bar = torch.empty((g, dv), dtype=torch.float32, device=s.device)
     for t in (w1_bar, b1_bar, w2_bar, b2_bar):
-        if not t.is_contiguous():
+        if t is not None and not t.is_contiguous():
             raise ValueError("graph_mlp_bwd outputs must be contiguous")
     call("egn_graph_mlp_bwd", g, dv, du, ptr(_c(u_bar, torch.float32)), ptr(_c(s, torch.float32)),
-         ptr(_c(pre, torch.float32)), ptr(_c(act, torch.float32)), ptr(_c(w1, torch.float32)),
-         ptr(_c(w2, torch.float32)), ptr(pre_bar), ptr(s_bar), ptr(w1_bar), ptr(b1_bar), ptr(w2_bar), ptr(b2_bar),
-         stream())
+         ptr(_c(pre, torch.float32)), ptr(_c(act, torch.float32)),
+         ptr(_c(w1, torch.float32)) if w1 is not None else None,
+         ptr(_c(w2, torch.float32)), ptr(pre_bar), ptr(s_bar), ptr(w1_bar) if w1 is not None else None, ptr(b1_bar),
+         ptr(w2_bar), ptr(b2_bar), stream())
     return s_bar
+
+
+def graph_linear(x, w, b=None):
+    """z = x w^T (+ b) over G rows (egn_graph_linear)."""
+    g, din = x.shape
+    dout = w.shape[0]
+    y = torch.empty((g, dout), dtype=torch.float32, device=x.device)
+    call("egn_graph_linear", g, din, dout, ptr(_c(x, torch.float32)), ptr(_c(w, torch.float32)),
+         ptr(_c(b, torch.float32)) if b is not None else None, ptr(y), stream())
+    return y
+
+
+def graph_linear_bwd(y_bar, x, w, x_bar=True, w_bar=None, b_bar=None):
+    """Adjoint of graph_linear: returns x_bar = y_bar w (or None); w_bar = y_bar^T x and
+    b_bar = column sums of y_bar written into the given contiguous views."""
+    g, din = x.shape
+    dout = w.shape[0]
+    xb = torch.empty((g, din), dtype=torch.float32, device=x.device) if x_bar else None
+    call("egn_graph_linear_bwd", g, din, dout, ptr(_c(y_bar, torch.float32)), ptr(_c(x, torch.float32)),
+         ptr(_c(w, torch.float32)), ptr(xb), ptr(w_bar), ptr(b_bar), stream())
+    return xb
 
 
 def rbf_linear_bwd(rbf_t, w, g, rbf_bar, w_bar, b_bar=None, g2=None):
@@ -273,6 +298,45 @@ def triplet_bwd(edge_ptr, rev, geo, X, Wk, cutoff, S_bar, edge_grad, X_bar=None,
     return X_bar, W_bar
 
 
+def triplet_fwd_window(edge_ptr, rev, geo, X, Wk, cutoff, first_lo, last_hi, S):
+    """Triplet forward over the centres of edge_ptr restricted to a contiguous triplet window
+    (egn_triplet_fwd_window); writes the covered centres' rows of the full-size S."""
+    k, l, dg = Wk.shape
+    if dg > MAX_TRIPLET_WIDTH:
+        for c0, c1 in _channel_chunks(dg):
+            part = torch.zeros((S.shape[0], c1 - c0), dtype=torch.float32, device=S.device)
+            triplet_fwd_window(edge_ptr, rev, geo, X[:, c0:c1].contiguous(), Wk[:, :, c0:c1].contiguous(), cutoff,
+                               first_lo, last_hi, part)
+            S[:, c0:c1] += part
+        return S
+    call("egn_triplet_fwd_window", ptr(edge_ptr), ptr(rev), ptr(geo), edge_ptr.shape[0] - 1, int(first_lo),
+         int(last_hi), ptr(_c(X, torch.float32)), ptr(_c(Wk, torch.float32)), k, l, dg, float(cutoff), ptr(S),
+         stream())
+    return S
+
+
+def triplet_bwd_window(edge_ptr, rev, geo, X, Wk, cutoff, first_lo, last_hi, S_bar, edge_grad, X_bar, max_degree):
+    """Adjoint of triplet_fwd_window: X_bar rows rev(q) of the covered centres overwritten (the
+    caller zeroes the rest), returns W_bar; edge_grad accumulated."""
+    k, l, dg = Wk.shape
+    W_bar = torch.empty_like(Wk)
+    if dg > MAX_TRIPLET_WIDTH:
+        for c0, c1 in _channel_chunks(dg):
+            xb = torch.zeros((X.shape[0], c1 - c0), dtype=torch.float32, device=X.device)
+            W_bar[:, :, c0:c1] = triplet_bwd_window(edge_ptr, rev, geo, X[:, c0:c1].contiguous(),
+                                                    Wk[:, :, c0:c1].contiguous(), cutoff, first_lo, last_hi,
+                                                    S_bar[:, c0:c1].contiguous(), edge_grad, xb, max_degree)
+            X_bar[:, c0:c1] += xb
+        return W_bar
+    nv, ne = edge_ptr.shape[0] - 1, X.shape[0]
+    nbytes = call("egn_triplet_bwd_workspace_bytes", nv, ne, k, l, dg)
+    ws = _workspace(nbytes, X.device)
+    call("egn_triplet_bwd_window", ptr(edge_ptr), ptr(rev), ptr(geo), nv, int(first_lo), int(last_hi),
+         int(max_degree), ptr(_c(X, torch.float32)), ptr(_c(Wk, torch.float32)), k, l, dg, float(cutoff),
+         ptr(_c(S_bar, torch.float32)), ptr(X_bar), ptr(W_bar), ptr(edge_grad), ptr(ws), stream())
+    return W_bar
+
+
 def triplet_terms(edge_ptr, rev, geo, tri_ptr, num_triplets, X, Wk, cutoff):
     k, l, dg = Wk.shape
     out = torch.empty((num_triplets, dg), dtype=torch.float32, device=X.device)
@@ -323,6 +387,22 @@ def force_head_fwd(edge_ptr, rev, geo, m, w):
     call("egn_force_head_fwd", ptr(edge_ptr), ptr(rev), ptr(geo), nv, ne, ptr(_c(m, torch.float32)), m.shape[1],
          ptr(_c(w, torch.float32)), ptr(scale), ptr(forces), stream())
     return scale, forces
+
+
+def force_head_scale(m, w, out):
+    """s_e = m_e . w into out [rows] (first half of egn_force_head_fwd)."""
+    call("egn_force_head_fwd", None, None, None, 0, m.shape[0], ptr(_c(m, torch.float32)), m.shape[1],
+         ptr(_c(w, torch.float32)), ptr(out), None, stream())
+    return out
+
+
+def force_head_gather(edge_ptr, rev, geo, scale, d):
+    """f[v] = sum over v's in-edges of s_e u_e for the centres of edge_ptr (second half)."""
+    nv = edge_ptr.shape[0] - 1
+    forces = torch.empty((nv, 3), dtype=torch.float32, device=scale.device)
+    call("egn_force_head_fwd", ptr(edge_ptr), ptr(rev), ptr(geo), nv, 0, None, int(d), None, ptr(scale),
+         ptr(forces), stream())
+    return forces
 
 
 def force_head_bwd(recv, geo, m, w, scale, f_bar, m_bar, edge_grad, w_bar=None):
@@ -459,23 +539,25 @@ def _silu_grad(h):
     return s * (1.0 + h * (1.0 - s))
 
 
-def linear(a, w, a2=None, w2=None, bias=None, resid=None, gather=None, aux=None, flags=0, w_mn=False):
+def linear(a, w, a2=None, w2=None, bias=None, resid=None, gather=None, aux=None, flags=0, w_mn=False, out=None):
     """Dense layer y = a w^T (+ a2 w2^T) (+ bias, resid, gathered rows; SiLU / gate / SiLU' epilogues).
 
     w is stored (out, in) as in the reference (egn/tape.py:104-119); w_mn=True
     computes a @ w instead (the data gradient).  Runs the tcgen05 3xTF32 GEMM for
     every shape that maps onto UMMA tiles (all model dims of BASELINE configs);
     only toy widths (N % 16 != 0 or K % 4 != 0) use an fp32 cuBLAS composite.
+    out: optional row-major destination (e.g. the owned rows of a full-size buffer).
     Returns y, or (y, out2) for EPI_SILU_OUT2 / EPI_MUL_AUX."""
     k = a.shape[1]
     n = w.shape[1] if w_mn else w.shape[0]
-    ok = _tc_ok(k, n, a, w, a2, w2, resid, aux)
+    ok = _tc_ok(k, n, a, w, a2, w2, resid, aux, out)
     if a2 is not None:
         ok = ok and a2.shape[1] % 4 == 0 and not w_mn
     if gather is not None:
         ok = ok and gather[0].stride(-1) == 1
     if ok:
-        return gemm(a, w, a2=a2, b2=w2, bias=bias, resid=resid, gather=gather, aux=aux, flags=flags, b_mn=w_mn)
+        return gemm(a, w, a2=a2, b2=w2, bias=bias, resid=resid, gather=gather, aux=aux, flags=flags, b_mn=w_mn,
+                    out=out)
     y = a @ w if w_mn else a @ w.t()
     if a2 is not None:
         y = y + a2 @ w2.t()
@@ -487,6 +569,9 @@ def linear(a, w, a2=None, w2=None, bias=None, resid=None, gather=None, aux=None,
         y = y + gather[0].index_select(0, gather[1].long())
     if flags & EPI_DSILU_AUX:
         y = y * _silu_grad(aux)
+    if out is not None:
+        out.copy_(y)
+        y = out
     if flags & EPI_MUL_AUX:
         return y * aux, y
     if flags & EPI_SILU_OUT2:

@@ -103,6 +103,55 @@ def partition_centers(deg: np.ndarray, workers: int, weight: str = "triplets",
 
 
 @dataclass(frozen=True)
+class ReferencePartition:
+    """The reference's balanced shards (egn/partition.py:28-49: split_range of the sorted
+    triplet, edge and node orders) for the graph-parallel reference schedule, plus the centre
+    range that covers each rank's triplet shard and the window into its first / last centre
+    (egn_triplet_fwd_window: a shard may cut through a centre's tile)."""
+
+    workers: int
+    trip_bounds: np.ndarray  # [P+1]
+    edge_bounds: np.ndarray  # [P+1]
+    node_bounds: np.ndarray  # [P+1]
+    centre_lo: np.ndarray  # [P] first centre of the triplet shard
+    centre_hi: np.ndarray  # [P] one past the last centre
+    first_lo: np.ndarray  # [P] centre-local triplet index where the shard starts (first centre)
+    last_hi: np.ndarray  # [P] centre-local index where it ends (last centre)
+
+    def triplet_shards(self) -> list:
+        return [np.arange(a, b, dtype=np.int64) for a, b in zip(self.trip_bounds[:-1], self.trip_bounds[1:])]
+
+
+def _bounds(n: int, workers: int) -> np.ndarray:
+    sizes = [s.size for s in split_range(n, workers)]
+    return np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+
+
+def partition_reference(tri_ptr: np.ndarray, num_edges: int, num_nodes: int, workers: int) -> ReferencePartition:
+    """split_range shards (identical to partition_graph) and the centre windows of the triplet
+    shards; tri_ptr [V+1] = triplet offsets per centre (sorted (out, in) order)."""
+    if workers < 1:
+        raise ValueError("workers must be >= 1")
+    tri_ptr = np.asarray(tri_ptr, dtype=np.int64)
+    nt = int(tri_ptr[-1]) if tri_ptr.size else 0
+    tb = _bounds(nt, workers)
+    lo = np.zeros(workers, dtype=np.int64)
+    hi = np.zeros(workers, dtype=np.int64)
+    flo = np.zeros(workers, dtype=np.int64)
+    lhi = np.zeros(workers, dtype=np.int64)
+    for r in range(workers):
+        t0, t1 = int(tb[r]), int(tb[r + 1])
+        if t1 <= t0:
+            continue
+        jlo = int(np.searchsorted(tri_ptr, t0, side="right")) - 1
+        jhi = int(np.searchsorted(tri_ptr, t1 - 1, side="right")) - 1
+        lo[r], hi[r] = jlo, jhi + 1
+        flo[r], lhi[r] = t0 - tri_ptr[jlo], t1 - tri_ptr[jhi]
+    return ReferencePartition(workers, tb, _bounds(int(num_edges), workers), _bounds(int(num_nodes), workers),
+                              lo, hi, flo, lhi)
+
+
+@dataclass(frozen=True)
 class CommModel:
     n_v: int
     n_e: int

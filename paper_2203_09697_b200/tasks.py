@@ -30,12 +30,29 @@ def _check_workers(config, workers):
     return p
 
 
-def predict(system, params: ModelParams, workers: int | None = None, device="cuda"):
-    """Energy and forces of one system (tasks.py:37-67)."""
+def _group(systems, params: ModelParams, p: int, device):
+    """WorkerGroup of p graph-parallel ranks (reference schedule), as tasks.py:59-62 builds it."""
+    from .runtime import WorkerGroup
+
     config = params.config
-    _check_workers(config, workers)
+    run = params if config.workers == p else ModelParams(config.replace(workers=p), params.arrays)
+    return WorkerGroup(systems, run, device=device)
+
+
+def predict(system, params: ModelParams, workers: int | None = None, device="cuda"):
+    """Energy and forces of one system (tasks.py:37-67); workers > 1 runs the graph-parallel
+    runtime (WorkerGroup), as the reference does."""
+    config = params.config
+    p = _check_workers(config, workers)
     if config.diagnostic:
         raise ValueError("the diagnostic quadratic-well model is a test fixture, not part of this path")
+    if p > 1:
+        group = _group(system, params, p, device)
+        if config.variant == GEMNET:
+            res = group.forward()
+            return float(res.energy), res.forces
+        res, bundle = group.forward_backward(d_energy=1.0)
+        return float(res.energy), -bundle.d_positions
     bg = build_batch(system, config.cutoff, device)
     eng = Engine(DeviceWeights.from_params(params, device))
     fw = eng.forward(bg)
@@ -281,13 +298,36 @@ def loss_and_grads(dataset, params: ModelParams, w_energy: float = 1.0, w_forces
     if w_forces != 0.0 and config.variant != GEMNET:
         raise ValueError("force-loss gradients require the force-centric variant; "
                          "set w_forces=0 for energy-centric training")
-    _check_workers(config, workers)
+    p = _check_workers(config, workers)
     if len(dataset) == 0:
         raise ValueError("dataset is empty")
     systems, e_t, f_t = _unpack(dataset)
+    if p > 1:
+        return _loss_and_grads_parallel(systems, e_t, f_t, params, w_energy, w_forces, p, device)
     tr = Trainer(params, systems, e_t, f_t if w_forces != 0.0 else None, w_energy, w_forces, device)
     loss = float(tr.loss_and_grads())
     return loss, tr.weights.to_numpy(grads=True)
+
+
+def _loss_and_grads_parallel(systems, e_t, f_t, params, w_energy, w_forces, p, device):
+    """tasks.py:158-183 with workers > 1: a forward of the graph-parallel runtime gives the
+    energies (and forces), the per-sample seeds follow, and forward_backward with those seeds
+    gives the gradient -- over the batched dataset in one WorkerGroup."""
+    group = _group(systems, params, p, device)
+    res = group.forward()
+    n = len(systems)
+    energy = np.atleast_1d(np.asarray(res.energy, dtype=np.float64))
+    resid = energy - np.asarray(e_t, dtype=np.float64)
+    loss = float((w_energy * resid * resid).sum() / n)
+    d_f = None
+    if w_forces != 0.0:
+        sizes = [np.asarray(getattr(s, "positions", s)).shape[0] for s in systems]
+        counts = np.repeat(sizes, sizes).astype(np.float64)
+        delta = res.forces - f_t
+        loss += float(w_forces * ((delta * delta).sum(axis=1) / counts).sum() / n)
+        d_f = 2.0 * w_forces * delta / (n * counts[:, None])
+    _, bundle = group.forward_backward(d_energy=2.0 * w_energy * resid / n, d_forces=d_f)
+    return loss, bundle.d_params
 
 
 def train_simple(dataset, params: ModelParams, lr: float, epochs: int, w_energy: float = 1.0,
@@ -295,6 +335,18 @@ def train_simple(dataset, params: ModelParams, lr: float, epochs: int, w_energy:
     """Plain gradient descent; returns fitted parameters and the loss history (tasks.py:188-209)."""
     if len(dataset) == 0:
         raise ValueError("dataset is empty")
+    p = _check_workers(params.config, workers)
+    if p > 1:
+        history = []
+        arrays = {k: np.array(v, dtype=np.float64) for k, v in params.arrays.items()}
+        for _ in range(epochs):
+            loss, grads = loss_and_grads(dataset, ModelParams(params.config, arrays), w_energy, w_forces, p, device)
+            if not np.isfinite(loss):
+                raise RuntimeError(f"non-finite loss {loss}")
+            history.append(loss)
+            if lr != 0.0:
+                arrays = {k: v - lr * grads[k] for k, v in arrays.items()}  # tasks.py:207-208
+        return ModelParams(params.config, arrays), history
     systems, e_t, f_t = _unpack(dataset)
     tr = Trainer(params, systems, e_t, f_t if w_forces != 0.0 else None, w_energy, w_forces, device)
     history = []

@@ -39,9 +39,10 @@ def _case(variant, n=40, seed=3):
     return cfg, init_params(cfg), pos, z
 
 
+@pytest.mark.parametrize("schedule", ["reference", "centre"])
 @pytest.mark.parametrize("variant", ["dimenet-style", "gemnet-style"])
 @pytest.mark.parametrize("workers", [1, 2, 3, 4])
-def test_parallel_matches_oracle(variant, workers):
+def test_parallel_matches_oracle(variant, workers, schedule):
     from paper_2203_09697_b200 import ModelParams
     from paper_2203_09697_b200.runtime import WorkerGroup
 
@@ -49,7 +50,7 @@ def test_parallel_matches_oracle(variant, workers):
     run = ModelParams(cfg.replace(workers=workers), params.arrays)
     rng = np.random.default_rng(5)
     df = rng.standard_normal((pos.shape[0], 3)) if variant == "gemnet-style" else None
-    res, bundle = WorkerGroup(pos, run).forward_backward(d_energy=0.8, d_forces=df)
+    res, bundle = WorkerGroup(pos, run, schedule=schedule).forward_backward(d_energy=0.8, d_forces=df)
     oc = O.Config(**{k: getattr(cfg, k) for k in O.Config.__dataclass_fields__})
     fw = O.forward(oc, params.arrays, pos, z)
     G, dpos = O.backward(fw, params.arrays, 0.8, df)
@@ -61,8 +62,9 @@ def test_parallel_matches_oracle(variant, workers):
         assert max_rel(bundle.d_params[k], g) < TOL, k
 
 
+@pytest.mark.parametrize("schedule", ["reference", "centre"])
 @pytest.mark.parametrize("variant", ["dimenet-style", "gemnet-style"])
-def test_parallel_equals_single_rank_engine(variant):
+def test_parallel_equals_single_rank_engine(variant, schedule):
     """P = 1, 2, 4 agree with each other to fp32 summation-order noise."""
     from paper_2203_09697_b200 import ModelParams
     from paper_2203_09697_b200.runtime import WorkerGroup
@@ -71,7 +73,7 @@ def test_parallel_equals_single_rank_engine(variant):
     outs = {}
     for p in (1, 2, 4):
         run = ModelParams(cfg.replace(workers=p), params.arrays)
-        outs[p] = WorkerGroup(pos, run).forward_backward(d_energy=1.0)
+        outs[p] = WorkerGroup(pos, run, schedule=schedule).forward_backward(d_energy=1.0)
     r1, b1 = outs[1]
     for p in (2, 4):
         rp, bp = outs[p]
@@ -82,8 +84,10 @@ def test_parallel_equals_single_rank_engine(variant):
 
 
 @pytest.mark.parametrize("variant", ["dimenet-style", "gemnet-style"])
-def test_comm_volume_independent_of_triplets(variant):
-    """Forward exchange per block: N_e d_e + G d_v (+ N_e d_e + N_v d_v for gemnet); no triplet level."""
+def test_centre_schedule_comm_volume(variant):
+    """Centre schedule, forward rows moved per block: X (N_e d_g) + m_new (N_e d_e) + G d_v
+    (+ pv (N_v d_e) + m2 (N_e d_e) for gemnet) -- independent of the triplet count; no
+    triplet-level buffer."""
     from paper_2203_09697_b200 import ModelParams
     from paper_2203_09697_b200.runtime import WorkerGroup
 
@@ -92,12 +96,12 @@ def test_comm_volume_independent_of_triplets(variant):
         c2 = cfg.replace(workers=3, d_t=d_t)
         from paper_2203_09697_b200 import init_params
 
-        wg = WorkerGroup(pos, init_params(c2))
+        wg = WorkerGroup(pos, init_params(c2), schedule="centre")
         res = wg.forward()
         ne, nv = wg.bg.num_edges, wg.bg.num_nodes
-        expect = ne * c2.d_e + c2.d_v
+        expect = ne * c2.triplet_width + ne * c2.d_e + c2.d_v
         if variant == "gemnet-style":
-            expect += ne * c2.d_e + nv * c2.d_v
+            expect += ne * c2.d_e + nv * c2.d_e
         assert res.comm_log.forward_blocks() == {b: expect for b in range(c2.blocks)}
         assert "triplet" not in res.comm_log.levels()
 
@@ -113,7 +117,8 @@ def test_graph_aligned_partition_is_halo_free_and_exact(variant):
     cfg, params, _, _ = _case(variant)
     rng = np.random.default_rng(21)
     systems = [O.random_cloud(n, 0.06, rng)[0] for n in (30, 41, 25, 37)]
-    wg = WorkerGroup(systems, ModelParams(cfg.replace(workers=2), params.arrays), align_graphs=True)
+    wg = WorkerGroup(systems, ModelParams(cfg.replace(workers=2), params.arrays), schedule="centre",
+                     align_graphs=True)
     de = np.array([0.5, -1.0, 0.25, 2.0])
     df = rng.standard_normal((sum(s.shape[0] for s in systems), 3)) if variant == "gemnet-style" else None
     res, bundle = wg.forward_backward(d_energy=de, d_forces=df)
@@ -255,3 +260,106 @@ def test_gp_dp_composition_equals_union_batch():
         assert abs(loss - loss_ref) <= 1e-5 * abs(loss_ref)
         assert max_rel(g, g_ref) < 1e-4
     assert "replica" in log.levels()
+
+
+# ---------------------------------------------------------------------------
+# reference schedule: the reference's own runtime tests (tests/test_runtime.py) on the GPU
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("variant", ["dimenet-style", "gemnet-style"])
+@pytest.mark.parametrize("workers", [1, 2, 5])
+def test_forward_comm_matches_prediction_exactly(variant, workers):
+    """tests/test_runtime.py:202-212: forward CommLog == comm_volume, per block and total."""
+    from paper_2203_09697_b200 import CommModel, comm_volume, init_params
+    from paper_2203_09697_b200.runtime import WorkerGroup
+
+    cfg, _, pos, _ = _case(variant)
+    cfg = cfg.replace(workers=workers)
+    group = WorkerGroup(pos, init_params(cfg))
+    result, _ = group.forward_backward(d_energy=1.0)
+    expected = comm_volume(CommModel.from_graph(group.topology, cfg), cfg.blocks)
+    per_block = result.comm_log.forward_blocks()
+    assert sorted(per_block) == list(range(cfg.blocks))
+    for elements in per_block.values():
+        assert elements == expected.per_block
+    assert result.comm_log.elements(phase="forward") == expected.total
+    # tests/test_runtime.py:225-240: only replicated-buffer sizes, never a triplet buffer
+    assert {r.level for r in result.comm_log.records if r.phase == "forward"} == {"edge", "node", "global"}
+    sizes = {group.topology.num_edges * cfg.d_e, group.topology.num_nodes * cfg.d_v, cfg.d_u}
+    assert all(r.elements in sizes for r in result.comm_log.records if r.phase == "forward")
+
+
+def test_forward_comm_invariant_under_triplet_dim():
+    """tests/test_runtime.py:215-222."""
+    from paper_2203_09697_b200 import init_params
+    from paper_2203_09697_b200.runtime import WorkerGroup
+
+    cfg, _, pos, _ = _case("gemnet-style")
+    counts = {}
+    for d_t in (8, 24):
+        c2 = cfg.replace(workers=2, d_t=d_t, d_bil=d_t)
+        counts[d_t] = WorkerGroup(pos, init_params(c2)).forward().comm_log.elements(phase="forward")
+    assert counts[8] == counts[24]
+
+
+@pytest.mark.parametrize("variant", ["dimenet-style", "gemnet-style"])
+def test_triplet_shards_are_split_range_and_match_oracle(variant):
+    """ParallelRunResult.triplet_shards (egn/runtime.py:430-431): rank r holds the last block's
+    t_feat rows of split_range(N_t, P)[r] -- shards cut through centre tiles (window kernel)."""
+    from paper_2203_09697_b200 import ModelParams, split_range
+    from paper_2203_09697_b200.runtime import WorkerGroup
+
+    cfg, params, pos, z = _case(variant)
+    run = ModelParams(cfg.replace(workers=3), params.arrays)
+    group = WorkerGroup(pos, run)
+    res = group.forward()
+    nt = group.topology.num_triplets
+    shards = split_range(nt, 3)
+    oc = O.Config(**{k: getattr(cfg, k) for k in O.Config.__dataclass_fields__})
+    ref = O.forward(oc, params.arrays, pos, z).t_feat
+    assert [s.shape[0] for s in res.triplet_shards] == [s.size for s in shards]
+    for got, idx in zip(res.triplet_shards, shards):
+        assert max_rel(got, ref[idx]) < TOL
+    # a shard boundary strictly inside a centre's tile exists in this graph
+    tp = group.bg.tri_ptr.cpu().numpy()
+    assert any(int(s[0]) not in set(tp.tolist()) for s in shards[1:] if s.size)
+
+
+def test_replicas_identical_and_stage_timing():
+    """tests/test_runtime.py:243-252 (replica digests agree after every collective) and
+    :318-328 (stage timing CSV)."""
+    from paper_2203_09697_b200 import ModelParams
+    from paper_2203_09697_b200.runtime import WorkerGroup
+
+    cfg, params, pos, _ = _case("gemnet-style")
+    group = WorkerGroup(pos, ModelParams(cfg.replace(workers=3), params.arrays), track_replicas=True)
+    res, _ = group.forward_backward(d_energy=1.0)
+    assert len(res.replica_digests) == 3 and len(res.replica_digests[0]) > 0
+    assert res.replica_digests[0] == res.replica_digests[1] == res.replica_digests[2]
+    assert {"init", "block0.tu", "block0.eu", "block0.nu", "backward.reduce"} <= set(res.stage_seconds)
+    assert all(v >= 0.0 for v in res.stage_seconds.values())
+    rows = res.timing_csv_rows()
+    assert rows[0] == "stage,seconds" and len(rows) == len(res.stage_seconds) + 1
+
+
+def test_zero_edge_and_more_workers_than_triplets():
+    """tests/test_runtime.py:178-199: empty shards contribute zeros."""
+    from paper_2203_09697_b200 import ModelConfig, ModelParams, init_params
+    from paper_2203_09697_b200.runtime import WorkerGroup
+
+    cfg = ModelConfig(variant="gemnet-style", blocks=1, workers=3)
+    params = init_params(cfg)
+    far = np.array([[0.0, 0, 0], [40.0, 0, 0]])
+    res, _ = WorkerGroup(far, params).forward_backward(d_energy=1.0)
+    oc = O.Config(**{k: getattr(cfg, k) for k in O.Config.__dataclass_fields__})
+    f = O.forward(oc, params.arrays, far, np.ones(2, dtype=np.int64))
+    assert abs(res.energy - f.energy) <= TOL * max(1.0, abs(f.energy))
+    np.testing.assert_array_equal(res.forces, np.zeros((2, 3)))
+    tri = np.array([[0.0, 0, 0], [1.0, 0, 0], [0.0, 1.2, 0]])
+    cfg6 = ModelConfig(variant="dimenet-style", blocks=2, workers=8)
+    p6 = init_params(cfg6)
+    res6, b6 = WorkerGroup(tri, p6).forward_backward(d_energy=1.0)
+    oc6 = O.Config(**{k: getattr(cfg6, k) for k in O.Config.__dataclass_fields__})
+    f6 = O.forward(oc6, p6.arrays, tri, np.ones(3, dtype=np.int64))
+    G6, dp6 = O.backward(f6, p6.arrays, 1.0)
+    assert abs(res6.energy - f6.energy) <= TOL * max(1.0, abs(f6.energy))
+    assert max_rel(b6.d_positions, dp6) < TOL
