@@ -185,6 +185,28 @@ def cpu_reference(wl, systems, budget_s, min_graphs=1):
     return {"triplets_per_s": trip / secs, "graphs": done, "seconds": secs, "sec_per_graph": secs / done}
 
 
+def host_info() -> dict:
+    """CPU model, core count and the BLAS threads the numpy oracle runs with."""
+    model = None
+    try:
+        for ln in Path("/proc/cpuinfo").read_text().splitlines():
+            if ln.startswith("model name"):
+                model = ln.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    blas = None
+    try:
+        from threadpoolctl import threadpool_info
+
+        blas = [{"api": i.get("internal_api"), "threads": i.get("num_threads"), "version": i.get("version")}
+                for i in threadpool_info() if i.get("user_api") == "blas"]
+    except Exception:  # noqa: BLE001 - informational only
+        pass
+    return {"cpu_model": model, "os_cpu_count": os.cpu_count(),
+            "OPENBLAS_NUM_THREADS": os.environ.get("OPENBLAS_NUM_THREADS", "unset (all cores)"), "blas": blas}
+
+
 def run_reference(args, wl):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -204,13 +226,18 @@ def run_reference(args, wl):
     line = {
         "impl": "reference", "metric": "triplet-interactions/s (train step, fwd+bwd+SGD)", "value": value,
         "unit": "triplets/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": ms_graph * graphs * args.gpus, "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": ms_graph * graphs * args.gpus, "ms_per_step_kind": "extrapolated: ms per graph x graphs",
+        "timed": "forward + backward per graph (the fp64 oracle port of egn.ModelTape + backward); the SGD update "
+                 "(one axpy over the parameters) and the graph build are outside the timed region, as in "
+                 "egn/bench.py:294-296",
+        "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": args.workload, "variant": wl["variant"], "graphs_per_gpu": graphs,
                    "atoms_per_graph": wl["atoms"], "cutoff": wl["cutoff"],
                    "sample": "one graph of the batch per step (fwd+bwd), host cores"},
         "cpu_baseline": {"value": value, "unit": "triplets/s", "cores": cores, "kind": "port",
-                         "sample": f"{args.steps} graphs x fwd+bwd of the {graphs}-graph batch, fp64 numpy oracle"},
+                         "sample": f"{args.steps} graphs x fwd+bwd of the {graphs}-graph batch, fp64 numpy oracle",
+                         "host": host_info()},
         "e2e": {"value": value, "unit": "triplets/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "steps_per_s": 1000.0 / (ms_graph * graphs * args.gpus),
     }
@@ -466,7 +493,8 @@ def run_ours(args, wl):
     if rank == 0 and not args.no_cpu_baseline:
         r = cpu_reference(wl, systems[:graphs], args.cpu_budget)
         cpu = {"value": r["triplets_per_s"], "unit": "triplets/s", "cores": os.cpu_count(), "kind": "port",
-               "sample": f"{r['graphs']} graph(s) of the batch, fwd+bwd, fp64 numpy oracle, {r['seconds']:.1f}s"}
+               "sample": f"{r['graphs']} graph(s) of the batch, fwd+bwd, fp64 numpy oracle, {r['seconds']:.1f}s",
+               "host": host_info()}
     if rank == 0:
         line = {
             "metric": "triplet-interactions/s (train step, fwd+bwd+SGD)", "value": value, "unit": "triplets/s",

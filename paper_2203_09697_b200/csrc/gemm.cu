@@ -1588,6 +1588,10 @@ static void wgrad_split(int64_t krows, int M, int N, int* splits, int* kbps) {
   const int BN = wgrad_tile_n(krows, N);
   const int tiles = static_cast<int>(((M + BM - 1) / BM) * ((N + BN - 1) / BN));
   const int nk = static_cast<int>((krows + BK - 1) / BK);
+  if (nk == 0) {  // no rows: nothing to split (the entry point zero-fills the output)
+    *kbps = *splits = 1;
+    return;
+  }
   int want = std::max(1, kNumSMs / tiles);      // one wave of CTAs
   want = std::min(want, std::max(1, nk / 4));   // >= 4 k-blocks per CTA
   *kbps = (nk + want - 1) / want;

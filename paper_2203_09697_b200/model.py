@@ -3,8 +3,9 @@
 Parameters are registered under the reference's weight names
 (egn/params.py:30-70, e.g. ``block0.tu.down``), so ``state_dict()`` keys
 equal ``param_specs`` names; they are views into one flat fp32 device
-buffer.  The forward/backward run the native engine (engine.py); the
-autograd Function only routes gradients, it never records torch ops.
+buffer.  The forward/backward run the native engine (engine.py) behind the custom op
+``torch.ops.egn.energy_forces`` (torch_ops.py) and its registered autograd formula, so
+the model is visible to the dispatcher, FakeTensor tracing and torch.compile.
 """
 
 from __future__ import annotations
@@ -15,34 +16,6 @@ from .config import GEMNET, ModelConfig
 from .engine import DeviceWeights, Engine
 from .graph import BatchGraph, build_batch
 from .params import ModelParams, init_params
-
-
-class _EGNFunction(torch.autograd.Function):
-    @staticmethod
-    def forward(ctx, engine: Engine, bg: BatchGraph, *params):
-        fw = engine.forward(bg)
-        if engine.config.variant == GEMNET:
-            forces = fw.forces
-        else:
-            # energy-centric forces F = -dE/dx at fixed topology (tasks.py:57-59)
-            ones = torch.ones(bg.num_graphs, device=bg.device)
-            forces = (-engine.backward(bg, fw, ones)).to(torch.float32)
-        ctx.engine, ctx.bg, ctx.fw = engine, bg, fw
-        ctx.mark_non_differentiable(forces) if engine.config.variant != GEMNET else None
-        return fw.energy.clone(), forces
-
-    @staticmethod
-    def backward(ctx, g_energy, g_forces):
-        engine, bg, fw = ctx.engine, ctx.bg, ctx.fw
-        gem = engine.config.variant == GEMNET
-        if g_energy is None:
-            g_energy = torch.zeros(bg.num_graphs, device=bg.device)
-        if not gem:
-            g_forces = None  # non-differentiable output (tasks.py:147-151)
-        engine.backward(bg, fw, g_energy, g_forces)
-        w = engine.weights
-        grads = tuple(w.g[s.name].clone() for s in w.specs)
-        return (None, None) + grads
 
 
 class EGNModel(torch.nn.Module):
@@ -70,10 +43,27 @@ class EGNModel(torch.nn.Module):
     def batch(self, systems) -> BatchGraph:
         return build_batch(systems, self.config.cutoff, device=self.weights.flat.device)
 
+    def _key(self, bg: BatchGraph) -> int:
+        """Registry key of (engine, batch) for egn::energy_forces; the last few batches stay
+        registered (the graph topology is built outside the traced region)."""
+        from .torch_ops import register_model, release_model
+
+        keys = self.__dict__.setdefault("_op_keys", {})
+        ent = keys.get(id(bg))
+        if ent is None or ent[1] is not bg:
+            while len(keys) >= 4:
+                old = next(iter(keys))
+                release_model(keys.pop(old)[0])
+            ent = (register_model(self.engine, bg), bg)
+            keys[id(bg)] = ent
+        return ent[0]
+
     def forward(self, batch):
         """batch: BatchGraph, AtomicSystem or list of systems -> (energy [G], forces [V, 3])."""
+        from . import torch_ops  # noqa: F401  (registers torch.ops.egn.*)
+
         bg = batch if isinstance(batch, BatchGraph) else self.batch(batch)
-        return _EGNFunction.apply(self.engine, bg, *self.parameters_in_order())
+        return torch.ops.egn.energy_forces(self.parameters_in_order(), bg.pos, self._key(bg))
 
     def to_params(self) -> ModelParams:
         return ModelParams(self.config, self.weights.to_numpy())

@@ -967,7 +967,7 @@ class ReferenceScheduleEngine:
                     mb = m_bar[e0:e1]
                     _wg(mb, st["m2r"][e0:e1], gr[p + "sym.w"])
                     t = L(mb, w[p + "sym.w"], w_mn=True)
-                    ops.gather_rows(ident, mb, out=m2_bar[e0:e1])
+                    ops.gather_rows(ident[: e1 - e0], mb, out=m2_bar[e0:e1])
                     ops.scatter_rows(bg.rev[e0:e1], ident[: e1 - e0], t, m2_bar)
                 cm.all_reduce_(m2_bar, phase="backward", block=b, stage="sym", level="edge")
                 self.clock.mark(f"backward.block{b}.eu2")

@@ -130,7 +130,8 @@ def test_model_tape_matches_oracle(variant):
 
 
 def test_block_forward_equals_second_block():
-    cfg = egn.ModelConfig(variant="gemnet-style", blocks=2, d_u=16, d_v=16, d_e=32, d_t=16, d_bil=16, seed=1)
+    cfg = egn.ModelConfig(variant="gemnet-style", blocks=2, d_u=16, d_v=16, d_e=32, d_t=16, d_bil=16, cutoff=6.0,
+                          seed=1)
     params = egn.init_params(cfg)
     pos, z = O.random_cloud(14, 0.06, np.random.default_rng(3))
     tape = egn.ModelTape(egn.AtomicSystem(pos, z), params)
@@ -146,7 +147,7 @@ def test_block_forward_equals_second_block():
 # -- egn/tasks.py with workers > 1 -------------------------------------------------------
 @pytest.mark.parametrize("variant", ["dimenet-style", "gemnet-style"])
 def test_predict_and_loss_with_workers(variant):
-    cfg = egn.ModelConfig(variant=variant, blocks=2, d_u=16, d_v=16, d_e=32, d_t=16, d_bil=16, seed=3)
+    cfg = egn.ModelConfig(variant=variant, blocks=2, d_u=16, d_v=16, d_e=32, d_t=16, d_bil=16, cutoff=6.0, seed=3)
     params = egn.init_params(cfg)
     rng = np.random.default_rng(6)
     systems = [O.random_cloud(n, 0.06, rng) for n in (16, 21)]

@@ -107,7 +107,8 @@ def test_two_process_gp_step_equals_single_process(schedule):
         assert status == "ok", status
         assert abs(loss - loss_ref) <= 1e-5 * abs(loss_ref), (rank, loss, loss_ref)
         assert max_rel(g, g_ref) < 1e-5, rank
-        assert "edge" in levels and "node" in levels  # real halo exchanges happened
+        if rank == 0:  # rank 0 keeps the CommLog
+            assert "edge" in levels and "node" in levels  # real halo exchanges happened
 
 
 def test_bench_multi_rank_path_runs():

@@ -112,3 +112,33 @@ def test_product_path_does_not_import_oracle():
         text = f.read_text()
         assert not re.search(r"^\s*(from|import)\s+oracle", text, re.M), f
         assert "egn_oracle" not in text, f
+
+
+def test_torch_custom_ops_registered_with_fake_kernels():
+    """torch.ops.egn.* exist and their fake (meta) implementations give shapes without a GPU
+    (FakeTensor tracing / torch.compile see them as opaque graph nodes)."""
+    import torch
+    from torch._subclasses.fake_tensor import FakeTensorMode
+
+    import paper_2203_09697_b200.torch_ops as T
+
+    names = {"rbf", "rbf_linear", "linear", "triplet_fwd", "triplet_bwd", "aggregate_in_edges", "gather_rows",
+             "graph_sum", "force_head", "positions_bwd", "energy_forces", "energy_forces_backward"}
+    assert names <= set(dir(torch.ops.egn))
+    with FakeTensorMode():
+        E, V, dg = 50, 7, 16
+        geo = torch.empty((E, 4))
+        X = torch.empty((E, dg))
+        Wk = torch.empty((6, 7, dg))
+        ep = torch.empty(V + 1, dtype=torch.int64)
+        rev = torch.empty(E, dtype=torch.int32)
+        assert torch.ops.egn.rbf(geo, 6, 6.0).shape == (E, 6)
+        assert torch.ops.egn.triplet_fwd(ep, rev, geo, X, Wk, 6.0, 10).shape == (E, dg)
+        xb, wb = torch.ops.egn.triplet_bwd(ep, rev, geo, X, Wk, 6.0, X, torch.empty((E, 4)), 10)
+        assert xb.shape == X.shape and wb.shape == Wk.shape
+        assert torch.ops.egn.linear(X, torch.empty((32, dg))).shape == (E, 32)
+        assert torch.ops.egn.linear(X, torch.empty((dg, 8)), w_mn=True).shape == (E, 8)
+        assert torch.ops.egn.aggregate_in_edges(ep, rev, X).shape == (V, dg)
+        assert torch.ops.egn.positions_bwd(ep, rev, geo, torch.empty((E, 4))).dtype == torch.float64
+        s, f = torch.ops.egn.force_head(ep, rev, geo, X, torch.empty(dg))
+        assert s.shape == (E,) and f.shape == (V, 3)
