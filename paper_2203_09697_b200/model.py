@@ -63,7 +63,7 @@ class EGNModel(torch.nn.Module):
         from . import torch_ops  # noqa: F401  (registers torch.ops.egn.*)
 
         bg = batch if isinstance(batch, BatchGraph) else self.batch(batch)
-        return torch.ops.egn.energy_forces(self.parameters_in_order(), bg.pos, self._key(bg))
+        return torch.ops.egn.energy_forces(self.parameters_in_order(), bg.pos, bg.graph_ptr, self._key(bg))
 
     def to_params(self) -> ModelParams:
         return ModelParams(self.config, self.weights.to_numpy())

@@ -8,7 +8,7 @@ Two levels:
 * kernel ops -- ``egn::rbf``, ``egn::rbf_linear``, ``egn::linear``, ``egn::triplet_fwd``,
   ``egn::triplet_bwd`` (mutates edge_grad), ``egn::aggregate_in_edges``, ``egn::gather_rows``,
   ``egn::graph_sum``, ``egn::force_head``, ``egn::positions_bwd``;
-* the model op ``egn::energy_forces(params, positions, key)`` -> (energy [G], forces [V, 3])
+* the model op ``egn::energy_forces(params, positions, graph_ptr, key)`` -> (energy [G], forces [V, 3])
   with its autograd formula ``egn::energy_forces_backward`` (the explicit adjoint of
   engine.Engine), which EGNModel calls.  `key` names a registered (Engine, BatchGraph) pair:
   graph topology is data-dependent, so it is built outside the traced region and looked up
@@ -157,15 +157,12 @@ def _(edge_ptr, rev, geo, edge_grad):
 # ---------------------------------------------------------------------------
 # model op with its autograd formula
 # ---------------------------------------------------------------------------
-def _sizes(key):
-    ent = _MODELS[key]
-    return ent["bg"].num_graphs, ent["bg"].num_nodes
-
-
 @torch.library.custom_op("egn::energy_forces", mutates_args=())
-def energy_forces(params: list[Tensor], positions: Tensor, key: int) -> tuple[Tensor, Tensor]:
+def energy_forces(params: list[Tensor], positions: Tensor, graph_ptr: Tensor, key: int) -> tuple[Tensor, Tensor]:
     """Energies [G] and forces [V, 3] of the registered batch (egn/engine.py:320-438); params
-    are the views of the engine's flat weight buffer (state_dict order).  Energy-centric
+    are the views of the engine's flat weight buffer (state_dict order); positions [V, 3] and
+    graph_ptr [G+1] give the output shapes (the fake implementation never reads `key`, which
+    torch.compile may turn symbolic).  Energy-centric
     variants return F = -dE/dx at fixed topology (egn/tasks.py:54-59)."""
     ent = _MODELS[key]
     eng, bg = ent["engine"], ent["bg"]
@@ -180,8 +177,8 @@ def energy_forces(params: list[Tensor], positions: Tensor, key: int) -> tuple[Te
 
 
 @energy_forces.register_fake
-def _(params, positions, key):
-    g, v = _sizes(key)
+def _(params, positions, graph_ptr, key):
+    g, v = graph_ptr.shape[0] - 1, positions.shape[0]
     return positions.new_empty((g,), dtype=torch.float32), positions.new_empty((v, 3), dtype=torch.float32)
 
 
@@ -204,22 +201,22 @@ def _(params, g_energy, g_forces, key):
 
 
 def _setup(ctx, inputs, output):
-    params, positions, key = inputs
+    params, positions, graph_ptr, key = inputs
     ctx.key = key
-    ctx.n = len(params)
+    ctx.g, ctx.v = graph_ptr.shape[0] - 1, positions.shape[0]
     ctx.save_for_backward(*params)
 
 
 def _backward(ctx, g_energy, g_forces):
     params = list(ctx.saved_tensors)
-    g, v = _sizes(ctx.key)
+    g, v = ctx.g, ctx.v
     dev = params[0].device
     if g_energy is None:
         g_energy = torch.zeros(g, device=dev)
     if g_forces is None:
         g_forces = torch.zeros((v, 3), device=dev)
     grads = torch.ops.egn.energy_forces_backward(params, g_energy.contiguous(), g_forces.contiguous(), ctx.key)
-    return list(grads), None, None
+    return list(grads), None, None, None
 
 
 energy_forces.register_autograd(_backward, setup_context=_setup)
