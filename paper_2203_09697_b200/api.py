@@ -241,10 +241,11 @@ class ModelTape:
     @property
     def state(self) -> FeatureState:
         fw, c = self._fw, self.config
+        dw = self.engine.weights
+        h = lambda x, dim: dw.unpad_rows(x, dim).double().cpu().numpy()  # noqa: E731
         t = self.engine.triplet_features(self.bg, fw, c.blocks - 1) if c.blocks else None
-        return FeatureState(fw.u.double().cpu().numpy(), fw.v.double().cpu().numpy(), fw.m.double().cpu().numpy(),
-                            t.double().cpu().numpy() if t is not None else None, self.topology, self.geometry,
-                            self.basis)
+        return FeatureState(h(fw.u, "d_u"), h(fw.v, "d_v"), h(fw.m, "d_e"), h(t, "d_t") if t is not None else None,
+                            self.topology, self.geometry, self.basis)
 
     def backward(self, d_energy: float = 1.0, d_forces=None, check_replay: bool = False) -> GradientBundle:
         if d_forces is not None and self.config.variant != GEMNET:
@@ -301,9 +302,16 @@ def block_forward(state: FeatureState, params, block: int, positions=None) -> Fe
         raise ValueError("block_forward needs the positions of the state's system")
     bg = batch_from_topology(topo, positions, c.cutoff)
     eng = Engine(DeviceWeights.from_params(params, dev))
-    m0 = torch.as_tensor(np.asarray(state.edge_features, dtype=np.float32), device=dev).contiguous()
-    u0 = torch.as_tensor(np.asarray(state.global_features, dtype=np.float32), device=dev).reshape(1, -1).contiguous()
+    pc = eng.config  # padded widths (zero channels beyond the reference ones)
+    m_np = np.asarray(state.edge_features, dtype=np.float32)
+    u_np = np.asarray(state.global_features, dtype=np.float32).reshape(1, -1)
+    m0 = torch.zeros((m_np.shape[0], pc.d_e), dtype=torch.float32, device=dev)
+    m0[:, : m_np.shape[1]] = torch.as_tensor(m_np, device=dev)
+    u0 = torch.zeros((1, pc.d_u), dtype=torch.float32, device=dev)
+    u0[:, : u_np.shape[1]] = torch.as_tensor(u_np, device=dev)
     fw = eng.forward(bg, m0=m0, u0=u0, blocks=[block])
     t = eng.triplet_features(bg, fw, block, index=0)
-    return FeatureState(fw.u.double().cpu().numpy(), fw.v.double().cpu().numpy(), fw.m.double().cpu().numpy(),
-                        t.double().cpu().numpy(), topo, state.geometry, state.basis)
+    dw = eng.weights
+    h = lambda x, dim: dw.unpad_rows(x, dim).double().cpu().numpy()  # noqa: E731
+    return FeatureState(h(fw.u, "d_u"), h(fw.v, "d_v"), h(fw.m, "d_e"), h(t, "d_t"), topo, state.geometry,
+                        state.basis)

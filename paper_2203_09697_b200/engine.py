@@ -35,7 +35,6 @@ import threading
 
 import numpy as np
 import torch
-import torch.nn.functional as F
 
 from . import ops
 from .config import GEMNET, ModelConfig
@@ -46,18 +45,51 @@ torch.backends.cuda.matmul.allow_tf32 = False
 torch.backends.cudnn.allow_tf32 = False
 
 
-def _silu_bwd(g: torch.Tensor, h: torch.Tensor) -> torch.Tensor:
-    s = torch.sigmoid(h)
-    return g * s * (1.0 + h * (1.0 - s))
+def _segments(name: str, c: ModelConfig) -> tuple[list, list]:
+    """Row and column segments (widths) of a weight of config c.  A concatenated input
+    ([m, ta] for eu.w1, [m_new, v] for eu2.w1) has one segment per operand, each padded on
+    its own, so the operands keep their own zero-padded layouts."""
+    leaf = name.split(".", 1)[1] if name.startswith("block") else name
+    K, KL = c.k_rbf, c.k_rbf * c.l_sbf
+    table = {
+        "atom_embedding": ([118], [c.d_v]), "edge_init.w": ([c.d_e], [K]), "edge_init.b": ([c.d_e], []),
+        "tu.down": ([c.d_t], [c.d_e]), "tu.rbf_gate": ([c.d_t], [K]), "tu.sbf_gate": ([c.d_t], [KL]),
+        "tu.bilinear_a": ([c.d_bil], [c.d_t]), "tu.bilinear_b": ([c.d_bil], [c.d_t]),
+        "tu.bilinear_proj": ([c.d_t], [c.d_bil]), "tu.up": ([c.d_e], [c.d_t]),
+        "eu.w1": ([c.d_e], [c.d_e, c.d_e]), "eu.b1": ([c.d_e], []), "eu.w2": ([c.d_e], [c.d_e]),
+        "eu.b2": ([c.d_e], []), "nu.w1": ([c.d_v], [c.d_e]), "nu.b1": ([c.d_v], []), "nu.w2": ([c.d_v], [c.d_v]),
+        "nu.b2": ([c.d_v], []), "eu2.w1": ([c.d_e], [c.d_e, c.d_v]), "eu2.b1": ([c.d_e], []),
+        "eu2.w2": ([c.d_e], [c.d_e]), "eu2.b2": ([c.d_e], []), "sym.w": ([c.d_e], [c.d_e]),
+        "gu.w1": ([c.d_u], [c.d_v]), "gu.b1": ([c.d_u], []), "gu.w2": ([c.d_u], [c.d_u]), "gu.b2": ([c.d_u], []),
+        "energy_head.w": ([1], [c.d_u]), "energy_head.b": ([1], []), "force_head.w": ([1], [c.d_e]),
+    }
+    return table[leaf]
+
+
+def _seg_index(real: list, padded: list) -> np.ndarray:
+    """Positions of the real entries of a segmented axis inside its padded layout."""
+    out, off = [], 0
+    for r, p in zip(real, padded):
+        out.append(np.arange(off, off + r))
+        off += p
+    return np.concatenate(out) if out else np.zeros(0, dtype=np.int64)
 
 
 class DeviceWeights:
     """fp32 device copy of ModelParams in one flat buffer (+ a grad buffer of
-    the same layout), so the SGD update is a single native kernel."""
+    the same layout), so the SGD update is a single native kernel.
 
-    def __init__(self, config: ModelConfig, device="cuda"):
-        self.config = config
-        self.specs = param_specs(config)
+    Feature widths that do not map onto the tcgen05 GEMM tiling (e.g. GemNet-XL d_e = 1302)
+    are zero-padded to a multiple of 16 (ModelConfig.padded): ``config`` is the padded
+    config the engine runs, ``ref_config`` the reference one; load() / to_numpy() convert
+    between the reference layout and the padded device layout (exact: see padded())."""
+
+    def __init__(self, config: ModelConfig, device="cuda", pad: int | None = 16):
+        self.ref_config = config
+        self.config = config.padded(pad) if pad else config
+        self.is_padded = self.config != config
+        self.ref_specs = param_specs(config)
+        self.specs = param_specs(self.config)
         sizes = [int(np.prod(s.shape)) for s in self.specs]
         self.offsets = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
         total = int(self.offsets[-1])
@@ -68,6 +100,12 @@ class DeviceWeights:
         for s, a, b in zip(self.specs, self.offsets[:-1], self.offsets[1:]):
             self.w[s.name] = self.flat[a:b].view(s.shape)
             self.g[s.name] = self.grad_flat[a:b].view(s.shape)
+        self._index = {}
+        if self.is_padded:
+            for s in self.specs:
+                rr, rc = _segments(s.name, config)
+                pr, pc = _segments(s.name, self.config)
+                self._index[s.name] = (_seg_index(rr, pr), _seg_index(rc, pc) if rc else None)
 
     @classmethod
     def from_params(cls, params: ModelParams, device="cuda") -> "DeviceWeights":
@@ -75,15 +113,41 @@ class DeviceWeights:
         dw.load(params)
         return dw
 
+    def _pad(self, name: str, a: np.ndarray, shape) -> np.ndarray:
+        if not self.is_padded:
+            return a
+        out = np.zeros(shape, dtype=np.float64)
+        ri, ci = self._index[name]
+        if ci is None:
+            out[ri] = a
+        else:
+            out[np.ix_(ri, ci)] = a
+        return out
+
+    def _unpad(self, name: str, a: np.ndarray) -> np.ndarray:
+        if not self.is_padded:
+            return a
+        ri, ci = self._index[name]
+        return a[ri] if ci is None else a[np.ix_(ri, ci)]
+
     def load(self, params: ModelParams) -> None:
-        host = np.concatenate([np.asarray(params.arrays[s.name], dtype=np.float64).ravel()
+        host = np.concatenate([self._pad(s.name, np.asarray(params.arrays[s.name], dtype=np.float64), s.shape).ravel()
                                for s in self.specs])
         self.flat.copy_(torch.from_numpy(host.astype(np.float32)))
 
     def to_numpy(self, grads: bool = False) -> dict:
+        """Reference-layout host arrays (padding removed)."""
         src = (self.grad_flat if grads else self.flat).detach().double().cpu().numpy()
-        return {s.name: src[a:b].reshape(s.shape).copy()
+        return {s.name: self._unpad(s.name, src[a:b].reshape(s.shape)).copy()
                 for s, a, b in zip(self.specs, self.offsets[:-1], self.offsets[1:])}
+
+    def unpad(self, name: str, a: np.ndarray) -> np.ndarray:
+        """Reference-layout view of a padded parameter-shaped host array."""
+        return self._unpad(name, a)
+
+    def unpad_rows(self, x: torch.Tensor, dim: str) -> torch.Tensor:
+        """Reference channels of a padded activation (columns [0, d) of [rows, d_padded])."""
+        return x[:, : getattr(self.ref_config, dim)]
 
     def sgd_(self, lr: float) -> None:
         """w -= lr * g (tasks.py:207-208)."""

@@ -126,10 +126,8 @@ def rbf_linear(rbf_t, w, b=None, out=None):
     if out is None:
         out = torch.empty((e, n), dtype=torch.float32, device=rbf_t.device)
     if k > 8 or n % 4 or out.stride(0) % 4 or out.stride(1) != 1 or out.data_ptr() % 16:
-        # widths outside the native kernel's tiling (e.g. GemNet-XL d_e = 1302): fp32 cuBLAS
-        if b is not None:
-            return torch.addmm(b, rbf_t, w.t(), out=out)
-        return torch.mm(rbf_t, w.t(), out=out)
+        raise ValueError(f"rbf_linear: K = {k} <= 8, N = {n} % 4 == 0 and 16-byte aligned rows required "
+                         "(the engine pads feature widths to multiples of 16)")
     call("egn_rbf_linear", ptr(_c(rbf_t, torch.float32)), e, k, ptr(_c(w, torch.float32)),
          ptr(_c(b, torch.float32)) if b is not None else None, n, ptr(out), out.stride(0), stream())
     return out
@@ -198,13 +196,16 @@ def rbf_linear_bwd(rbf_t, w, g, rbf_bar, w_bar, b_bar=None, g2=None):
         g = g.contiguous()
     if g2 is not None and (g2.stride(1) != 1 or g2.stride(0) != g.stride(0)):
         g, g2 = (g * g2).contiguous(), None
-    if k > 8 or n > 128:
-        if g2 is not None:
-            g = g * g2
-        rbf_bar.addmm_(g, w)
-        wgrad(g, rbf_t, out=w_bar)
-        if b_bar is not None:
-            column_sum(g, out=b_bar)
+    if k > 8:
+        raise ValueError(f"rbf_linear_bwd: k_rbf = {k} > 8 is outside the native kernel")
+    if n > 128:
+        # wide outputs (XL edge_init d_e = 2048, C3 rbf gate d_t = 256): 128-column chunks of the
+        # same kernel; rbf_bar accumulates over chunks, W_bar / b_bar rows per chunk
+        for c0 in range(0, n, 128):
+            c1 = min(n, c0 + 128)
+            rbf_linear_bwd(rbf_t, w[c0:c1], g[:, c0:c1], rbf_bar, w_bar[c0:c1],
+                           b_bar[c0:c1] if b_bar is not None else None,
+                           g2[:, c0:c1] if g2 is not None else None)
         return
     nbytes = call("egn_rbf_linear_bwd_workspace_bytes", e, k, n)
     ws = _workspace_named("rbflin", nbytes, g.device)
@@ -441,28 +442,6 @@ def column_sum(x, out=None):
     return out
 
 
-def wgrad(g: torch.Tensor, x: torch.Tensor, out: torch.Tensor | None = None, splits: int = 64) -> torch.Tensor:
-    """g^T x for tall-skinny operands (rows >> cols): split-K batched GEMM + ordered sum.
-
-    cuBLAS runs a [a, b] = [E, a]^T [E, b] product with only (a/64)(b/64)
-    CTAs; splitting the E dimension into `splits` batches fills the GPU."""
-    rows = g.shape[0]
-    chunk = rows // splits
-    if chunk < 256:
-        res = g.t() @ x
-    else:
-        n = chunk * splits
-        gb = g[:n].reshape(splits, chunk, g.shape[1])
-        xb = x[:n].reshape(splits, chunk, x.shape[1])
-        res = torch.bmm(gb.transpose(1, 2), xb).sum(0)
-        if n < rows:
-            res = res.addmm_(g[n:].t(), x[n:])
-    if out is not None:
-        out.copy_(res)
-        return out
-    return res
-
-
 EPI_BIAS, EPI_RESID, EPI_GATHER, EPI_SILU_OUT2, EPI_MUL_AUX, EPI_DSILU_AUX = 1, 2, 4, 8, 16, 32
 
 
@@ -534,18 +513,14 @@ def _tc_ok(k, n, *ts):
     return True
 
 
-def _silu_grad(h):
-    s = torch.sigmoid(h)
-    return s * (1.0 + h * (1.0 - s))
-
-
 def linear(a, w, a2=None, w2=None, bias=None, resid=None, gather=None, aux=None, flags=0, w_mn=False, out=None):
     """Dense layer y = a w^T (+ a2 w2^T) (+ bias, resid, gathered rows; SiLU / gate / SiLU' epilogues).
 
     w is stored (out, in) as in the reference (egn/tape.py:104-119); w_mn=True
-    computes a @ w instead (the data gradient).  Runs the tcgen05 3xTF32 GEMM for
-    every shape that maps onto UMMA tiles (all model dims of BASELINE configs);
-    only toy widths (N % 16 != 0 or K % 4 != 0) use an fp32 cuBLAS composite.
+    computes a @ w instead (the data gradient).  Always the tcgen05 3xTF32 GEMM (or its
+    small-M SIMT sibling inside egn_gemm): shapes must map onto the UMMA tiling (N % 16 == 0,
+    K % 4 == 0, 16-byte aligned rows) -- the engine pads every feature width to a multiple
+    of 16 (DeviceWeights / ModelConfig.padded), so no model product ever needs a fallback.
     out: optional row-major destination (e.g. the owned rows of a full-size buffer).
     Returns y, or (y, out2) for EPI_SILU_OUT2 / EPI_MUL_AUX."""
     k = a.shape[1]
@@ -555,38 +530,17 @@ def linear(a, w, a2=None, w2=None, bias=None, resid=None, gather=None, aux=None,
         ok = ok and a2.shape[1] % 4 == 0 and not w_mn
     if gather is not None:
         ok = ok and gather[0].stride(-1) == 1
-    if ok:
-        return gemm(a, w, a2=a2, b2=w2, bias=bias, resid=resid, gather=gather, aux=aux, flags=flags, b_mn=w_mn,
-                    out=out)
-    y = a @ w if w_mn else a @ w.t()
-    if a2 is not None:
-        y = y + a2 @ w2.t()
-    if bias is not None:
-        y = y + bias
-    if resid is not None:
-        y = y + resid
-    if gather is not None:
-        y = y + gather[0].index_select(0, gather[1].long())
-    if flags & EPI_DSILU_AUX:
-        y = y * _silu_grad(aux)
-    if out is not None:
-        out.copy_(y)
-        y = out
-    if flags & EPI_MUL_AUX:
-        return y * aux, y
-    if flags & EPI_SILU_OUT2:
-        return y, torch.nn.functional.silu(y)
-    return y
+    if not ok:
+        raise ValueError(f"linear: [{a.shape[0]} x {k}] x [{k} x {n}] does not map onto the tcgen05 tiling "
+                         "(N % 16, K % 4, 16-byte aligned rows)")
+    return gemm(a, w, a2=a2, b2=w2, bias=bias, resid=resid, gather=gather, aux=aux, flags=flags, b_mn=w_mn, out=out)
 
 
 def linear_wgrad(g, x, out, bias_out=None):
     """out = g^T x (weight gradient over all rows); bias_out = column sums of g."""
-    if _tc_ok(4, x.shape[1], g, x) and out.stride(1) == 1:
-        return gemm_wgrad(g, x, out=out, colsum=bias_out)
-    out.copy_(g.t() @ x)
-    if bias_out is not None:
-        column_sum(g, out=bias_out)
-    return out
+    if not (_tc_ok(4, x.shape[1], g, x) and out.stride(1) == 1):
+        raise ValueError(f"linear_wgrad: N = {x.shape[1]} does not map onto the tcgen05 tiling")
+    return gemm_wgrad(g, x, out=out, colsum=bias_out)
 
 
 def small_gemms(problems):

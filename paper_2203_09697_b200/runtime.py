@@ -154,13 +154,22 @@ class Comm:
         self.track = track  # replica digests (egn/runtime.py:397-401, track_replicas)
         self.digests: list = []
 
-    def _tag(self, t: torch.Tensor, op: str, phase="forward", block=-1, stage="", level="edge", rows=None):
+    def _tag(self, t: torch.Tensor, op: str, phase="forward", block=-1, stage="", level="edge", rows=None,
+             width=None, elements=None):
+        """CommLog record.  Row collectives count the rows they move (a chunked all-gather logs
+        each chunk).  width / elements: the reference-layout size when the device buffer has
+        zero-padded feature columns (DeviceWeights padding), so the log stays comparable with
+        comm_volume()."""
         if level not in ALLOWED_LEVELS:
             raise ValueError(f"buffers of level {level!r} must never enter a collective")
         if self.rank == 0:
-            # row collectives count the rows they move (a chunked all-gather logs each chunk)
-            n = int(t.numel()) if rows is None else int(rows) * int(np.prod(t.shape[1:]))
-            self.log.records.append(CommRecord(phase, block, stage, level, n, op))
+            if elements is None and rows is None and width is None:
+                elements = int(t.numel())
+            elif elements is None:
+                r = t.shape[0] if rows is None else int(rows)
+                w = int(np.prod(t.shape[1:])) if width is None else int(width)
+                elements = r * w
+            self.log.records.append(CommRecord(phase, block, stage, level, int(elements), op))
 
     def _digest(self, t: torch.Tensor) -> torch.Tensor:
         if self.track:
@@ -482,6 +491,8 @@ class GraphParallelEngine:
         self.config = weights.config
         self._helper = Engine(weights)  # folded weights (one batched launch per step)
         self.n0, self.n1, self.e0, self.e1, self.t0, self.t1 = part.rank(comm.rank)
+        self.R = weights.ref_config  # CommLog widths in the reference layout
+        self.nparam = sum(int(np.prod(s.shape)) for s in weights.ref_specs)
         self.chunks = max(1, int(chunks))
         self.clock = clock or _NO_CLOCK
         self._cache: dict = {}
@@ -565,7 +576,7 @@ class GraphParallelEngine:
             X = torch.empty((E, dg), dtype=f32, device=dev)
             mm = m
             self._produce(d, X, d["eb"], lambda a, z, out: L(mm[a:z], Wx, out=out),
-                          phase="forward", block=b, stage="X", level="edge")
+                          phase="forward", block=b, stage="X", level="edge", width=self.R.triplet_width)
             Wk = folded[b]["Wk"]
             S = ops.triplet_fwd(d["ep_own"], bg.rev, bg.geo, X, Wk, c.cutoff, max_degree=bg.max_deg)
             S_o, g = S[e0:e1], gates[b]
@@ -581,7 +592,7 @@ class GraphParallelEngine:
             m_new_full = torch.empty((E, de), dtype=f32, device=dev)
             self._produce(d, m_new_full, d["eb"],
                           lambda a, z, out: L(a1[a:z], w[p + "eu.w2"], bias=w[p + "eu.b2"], resid=mm[a:z], out=out),
-                          phase="forward", block=b, stage="m_new", level="edge")
+                          phase="forward", block=b, stage="m_new", level="edge", width=self.R.d_e)
             m_new = m_new_full[e0:e1]
             self.clock.mark(f"block{b}.nu")
             agg = ops.aggregate_in_edges(d["ep_own"], bg.rev, m_new_full)
@@ -594,14 +605,14 @@ class GraphParallelEngine:
                 pv = torch.empty((V, de), dtype=f32, device=dev)
                 vv = v
                 self._produce(d, pv, d["nb"], lambda a, z, out: L(vv[a:z], w1[:, de:], out=out),
-                              phase="forward", block=b, stage="pv", level="node")
+                              phase="forward", block=b, stage="pv", level="node", width=self.R.d_e)
                 h2, a2 = L(m_new, w1[:, :de], bias=w[p + "eu2.b1"], gather=(pv, d["recv_own"]),
                            flags=ops.EPI_SILU_OUT2)
                 m2_full = torch.empty((E, de), dtype=f32, device=dev)
                 self._produce(d, m2_full, d["eb"],
                               lambda a, z, out: L(a2[a:z], w[p + "eu2.w2"], bias=w[p + "eu2.b2"],
                                                   resid=m_new[a:z], out=out),
-                              phase="forward", block=b, stage="m2", level="edge")
+                              phase="forward", block=b, stage="m2", level="edge", width=self.R.d_e)
                 self.clock.mark(f"block{b}.sym")
                 m2r = ops.gather_rows(d["rev_own"], m2_full)
                 m = L(m2r, w[p + "sym.w"], resid=m2_full[e0:e1])
@@ -611,7 +622,7 @@ class GraphParallelEngine:
             # GU head: per-graph sums of own nodes, all-reduced under the next blocks' edge work
             s = ops.graph_sum(d["gp_own"], v) if n1 > n0 else torch.zeros((G, c.d_v), dtype=f32, device=dev)
             pending.append((b, s, cm.all_reduce_(s, async_op=True, phase="forward", block=b, stage="gu",
-                                                 level="global")))
+                                                 level="global", width=self.R.d_v)))
             blocks.append(st)
         self.clock.mark("readout")
         for b, s, hnd in pending:
@@ -681,7 +692,7 @@ class GraphParallelEngine:
                     part = torch.zeros((E, de), dtype=f32, device=dev)
                     ops.scatter_rows(d["rev_own"], ident[: e1 - e0], t, part)
                     hnd = cm.reduce_scatter_rows(part, d["eb"], async_op=True, phase="backward", block=b,
-                                                 stage="m2", level="edge")
+                                                 stage="m2", level="edge", width=self.R.d_e)
                     _wg(m_bar, st["m2r"], gr[p + "sym.w"])  # under the reduce-scatter
                     m2_bar = _rows_add(hnd.wait(), m_bar, ident)
                 # EU2
@@ -696,7 +707,7 @@ class GraphParallelEngine:
                 else:
                     pv_part = ops.aggregate_in_edges(bg.edge_ptr, bg.rev, h2_full)
                     hnd = cm.reduce_scatter_rows(pv_part, d["nb"], async_op=True, phase="backward", block=b,
-                                                 stage="pv", level="node")
+                                                 stage="pv", level="node", width=self.R.d_e)
                 _wg(h2_bar, st["m_new"], gr[p + "eu2.w1"][:, :de], gr[p + "eu2.b1"])
                 m_new_bar = L(h2_bar, w1[:, :de], w_mn=True, resid=m2_bar)
                 if not hf:
@@ -717,7 +728,7 @@ class GraphParallelEngine:
                 part = torch.zeros((E, de), dtype=f32, device=dev)
                 ops.scatter_rows(d["rev_own"], d["src_local"], agg_bar, part)
                 hnd = cm.reduce_scatter_rows(part, d["eb"], async_op=True, phase="backward", block=b,
-                                             stage="m_new", level="edge")
+                                             stage="m_new", level="edge", width=self.R.d_e)
                 _wg(v_bar, st["av"], gr[p + "nu.w2"], gr[p + "nu.b2"])
                 _wg(hv_bar, st["agg"], gr[p + "nu.w1"], gr[p + "nu.b1"])
                 m_new_bar = _rows_add(hnd.wait(), m_new_bar, ident)
@@ -748,7 +759,7 @@ class GraphParallelEngine:
                                                  X_bar=X_bar_full, max_degree=bg.max_deg)
             if not hf:
                 hnd = cm.reduce_scatter_rows(X_bar_full, d["eb"], async_op=True, phase="backward", block=b,
-                                             stage="X", level="edge")
+                                             stage="X", level="edge", width=self.R.triplet_width)
             ops.rbf_linear_bwd(fw.rbf, w[p + "tu.rbf_gate"], g_prod[0], rbf_bar, gr[p + "tu.rbf_gate"], g2=g_prod[1])
             X_bar = X_bar_full[e0:e1] if hf else hnd.wait()
             if gem:
@@ -771,7 +782,8 @@ class GraphParallelEngine:
         pos_bar = ops.positions_bwd(bg.edge_ptr, bg.rev, bg.geo, eg)
         self.clock.mark("backward.reduce")
         cm.all_reduce_(pos_bar, phase="backward", block=-1, stage="positions", level="position")
-        cm.all_reduce_(self.weights.grad_flat, phase="backward", block=-1, stage="params", level="param")
+        cm.all_reduce_(self.weights.grad_flat, phase="backward", block=-1, stage="params", level="param",
+                       elements=self.nparam)
         return pos_bar
 
 
@@ -795,6 +807,8 @@ class ReferenceScheduleEngine:
         self.n0, self.n1 = int(part.node_bounds[r]), int(part.node_bounds[r + 1])
         self.j0, self.j1 = int(part.centre_lo[r]), int(part.centre_hi[r])
         self.flo, self.lhi = int(part.first_lo[r]), int(part.last_hi[r])
+        self.R = weights.ref_config  # CommLog widths in the reference layout
+        self.nparam = sum(int(np.prod(s.shape)) for s in weights.ref_specs)
         self.clock = clock or _NO_CLOCK
         self._cache: dict = {}
         self._prep_key = None
@@ -848,7 +862,7 @@ class ReferenceScheduleEngine:
                 else:
                     Y = S[ra:rb] * g
                 L(Y, w[p + "tu.up"], out=ta[ra:rb])
-            cm.all_reduce_(ta, phase="forward", block=b, stage="ta", level="edge")
+            cm.all_reduce_(ta, phase="forward", block=b, stage="ta", level="edge", width=self.R.d_e)
             self.clock.mark(f"block{b}.eu")
             w1 = w[p + "eu.w1"]
             h, a1 = L(m, w1[:, :de], a2=ta, w2=w1[:, de:], bias=w[p + "eu.b1"], flags=ops.EPI_SILU_OUT2)
@@ -860,7 +874,7 @@ class ReferenceScheduleEngine:
                 agg = ops.aggregate_in_edges(d["ep_n"], bg.rev, m_new)
                 hv, av = L(agg, w[p + "nu.w1"], bias=w[p + "nu.b1"], flags=ops.EPI_SILU_OUT2)
                 L(av, w[p + "nu.w2"], bias=w[p + "nu.b2"], out=v_part[n0:n1])
-            v = cm.all_reduce_(v_part, phase="forward", block=b, stage="nu", level="node")
+            v = cm.all_reduce_(v_part, phase="forward", block=b, stage="nu", level="node", width=self.R.d_v)
             st.update(X=X, Wx=Wx, Wk=Wk, S=S, g=g, Y=Y, Z=Z, ta=ta, h=h, a1=a1, m_new=m_new, agg=agg, hv=hv, av=av, v=v)
             if gem:
                 self.clock.mark(f"block{b}.eu2")
@@ -872,7 +886,7 @@ class ReferenceScheduleEngine:
                     h2, a2 = L(m_new[e0:e1], w1[:, :de], bias=w[p + "eu2.b1"], gather=(pv, bg.recv[e0:e1]),
                                flags=ops.EPI_SILU_OUT2)
                     L(a2, w[p + "eu2.w2"], bias=w[p + "eu2.b2"], resid=m_new[e0:e1], out=m2[e0:e1])
-                cm.all_reduce_(m2, phase="forward", block=b, stage="eu2", level="edge")
+                cm.all_reduce_(m2, phase="forward", block=b, stage="eu2", level="edge", width=self.R.d_e)
                 self.clock.mark(f"block{b}.sym")
                 m2r = ops.gather_rows(bg.rev, m2)
                 m = L(m2r, w[p + "sym.w"], resid=m2)
@@ -883,7 +897,7 @@ class ReferenceScheduleEngine:
             s = (ops.graph_sum(d["gp_own"], v[n0:n1]) if n1 > n0
                  else torch.zeros((G, c.d_v), dtype=f32, device=dev))
             z = ops.graph_linear(s, w[p + "gu.w1"])
-            cm.all_reduce_(z, phase="forward", block=b, stage="gu", level="global")
+            cm.all_reduce_(z, phase="forward", block=b, stage="gu", level="global", width=self.R.d_u)
             pre, act = ops.graph_mlp_fwd(z, None, w[p + "gu.b1"], w[p + "gu.w2"], w[p + "gu.b2"], u)
             st.update(s=s, z=z, pre=pre, act=act)
             blocks.append(st)
@@ -938,14 +952,14 @@ class ReferenceScheduleEngine:
                                          b_bar=gr["energy_head.b"])
         else:
             u_bar = torch.zeros((G, c.d_u), dtype=f32, device=dev)
-        cm.all_reduce_(u_bar, phase="backward", block=-1, stage="energy", level="global")
+        cm.all_reduce_(u_bar, phase="backward", block=-1, stage="energy", level="global", width=self.R.d_u)
         m_bar = torch.zeros((E, de), dtype=f32, device=dev)
         if gem and d_forces is not None:
             f_part = torch.zeros((V, 3), dtype=f32, device=dev)
             f_part[n0:n1] = d_forces.to(f32)[n0:n1]
             ops.force_head_bwd(bg.recv, bg.geo, fw.m, w["force_head.w"].view(-1), fw.scale, f_part, m_bar, eg,
                                w_bar=gr["force_head.w"].view(-1))
-            cm.all_reduce_(m_bar, phase="backward", block=-1, stage="force", level="edge")
+            cm.all_reduce_(m_bar, phase="backward", block=-1, stage="force", level="edge", width=self.R.d_e)
         post = []
         for b in range(c.blocks - 1, -1, -1):
             p, st = f"block{b}.", fw.blocks[b]
@@ -955,7 +969,7 @@ class ReferenceScheduleEngine:
                                           gr[p + "gu.b1"], gr[p + "gu.w2"], gr[p + "gu.b2"])
             else:
                 z_bar = torch.zeros((G, c.d_u), dtype=f32, device=dev)
-            cm.all_reduce_(z_bar, phase="backward", block=b, stage="gu", level="global")
+            cm.all_reduce_(z_bar, phase="backward", block=b, stage="gu", level="global", width=self.R.d_u)
             s_bar = ops.graph_linear_bwd(z_bar, st["s"], w[p + "gu.w1"], w_bar=gr[p + "gu.w1"])
             v_bar = torch.zeros((V, c.d_v), dtype=f32, device=dev)
             if n1 > n0:
@@ -969,7 +983,7 @@ class ReferenceScheduleEngine:
                     t = L(mb, w[p + "sym.w"], w_mn=True)
                     ops.gather_rows(ident[: e1 - e0], mb, out=m2_bar[e0:e1])
                     ops.scatter_rows(bg.rev[e0:e1], ident[: e1 - e0], t, m2_bar)
-                cm.all_reduce_(m2_bar, phase="backward", block=b, stage="sym", level="edge")
+                cm.all_reduce_(m2_bar, phase="backward", block=b, stage="sym", level="edge", width=self.R.d_e)
                 self.clock.mark(f"backward.block{b}.eu2")
                 mn_bar = torch.zeros((E, de), dtype=f32, device=dev)
                 if e1 > e0:
@@ -987,7 +1001,7 @@ class ReferenceScheduleEngine:
             else:
                 mn_bar = torch.zeros((E, de), dtype=f32, device=dev)
             self.clock.mark(f"backward.block{b}.nu")
-            cm.all_reduce_(v_bar, phase="backward", block=b, stage="nu", level="node")
+            cm.all_reduce_(v_bar, phase="backward", block=b, stage="nu", level="node", width=self.R.d_v)
             if n1 > n0:
                 vb = v_bar[n0:n1]
                 _wg(vb, st["av"], gr[p + "nu.w2"], gr[p + "nu.b2"])
@@ -995,7 +1009,7 @@ class ReferenceScheduleEngine:
                 _wg(hv_bar, st["agg"], gr[p + "nu.w1"], gr[p + "nu.b1"])
                 agg_bar = L(hv_bar, w[p + "nu.w1"], w_mn=True)
                 ops.scatter_rows(bg.rev[d["na"]:d["nb"]], d["src_local"], agg_bar, mn_bar)
-            cm.all_reduce_(mn_bar, phase="backward", block=b, stage="m_new", level="edge")
+            cm.all_reduce_(mn_bar, phase="backward", block=b, stage="m_new", level="edge", width=self.R.d_e)
             if not gem:
                 _rows_add(mn_bar, m_bar, ident)
             m_new_bar = mn_bar
@@ -1011,7 +1025,7 @@ class ReferenceScheduleEngine:
                 _wg(h_bar, st["ta"][e0:e1], gr[p + "eu.w1"][:, de:])
                 L(h_bar, w1[:, :de], w_mn=True, resid=g1, out=m_in[e0:e1])
                 L(h_bar, w1[:, de:], w_mn=True, out=ta_bar[e0:e1])
-            cm.all_reduce_(ta_bar, phase="backward", block=b, stage="ta", level="edge")
+            cm.all_reduce_(ta_bar, phase="backward", block=b, stage="ta", level="edge", width=self.R.d_e)
             self.clock.mark(f"backward.block{b}.tu")
             if has_t:
                 tb = ta_bar[ra:rb]
@@ -1043,7 +1057,7 @@ class ReferenceScheduleEngine:
                     gr[p + "tu.sbf_gate"].copy_(Wk_bar.permute(2, 0, 1).reshape(Wk_bar.shape[2], -1))
                     _wg(X_bar, st["m"], gr[p + "tu.down"])
                     m_in = L(X_bar, w[p + "tu.down"], w_mn=True, resid=m_in)
-            m_bar = cm.all_reduce_(m_in, phase="backward", block=b, stage="m_in", level="edge")
+            m_bar = cm.all_reduce_(m_in, phase="backward", block=b, stage="m_in", level="edge", width=self.R.d_e)
         self.clock.mark("backward.init")
         ops.small_gemms(post)
         if e1 > e0:
@@ -1054,7 +1068,8 @@ class ReferenceScheduleEngine:
         pos_bar = ops.positions_bwd(bg.edge_ptr, bg.rev, bg.geo, eg)
         self.clock.mark("backward.reduce")
         cm.all_reduce_(pos_bar, phase="backward", block=-1, stage="positions", level="position")
-        cm.all_reduce_(self.weights.grad_flat, phase="backward", block=-1, stage="params", level="param")
+        cm.all_reduce_(self.weights.grad_flat, phase="backward", block=-1, stage="params", level="param",
+                       elements=self.nparam)
         return pos_bar
 
 
@@ -1276,17 +1291,19 @@ class WorkerGroup:
             raise WorkerGroupError("finalize", 0, AssertionError("worker outputs diverged"))
         fw0 = outs[0][0]
         to_np = lambda t: t.double().cpu().numpy()  # noqa: E731
+        dw = outs[0][1].weights
+        un = lambda t, dim: to_np(dw.unpad_rows(t, dim))  # noqa: E731
         if self.schedule == "reference":
-            m, v = to_np(fw0.m), to_np(fw0.v)
+            m, v = un(fw0.m, "d_e"), un(fw0.v, "d_v")
             forces = to_np(fw0.forces) if fw0.forces is not None else None
         else:
-            m = np.concatenate([to_np(o[0].m) for o in outs], axis=0)
-            v = np.concatenate([to_np(o[0].v) for o in outs], axis=0)
+            m = np.concatenate([un(o[0].m, "d_e") for o in outs], axis=0)
+            v = np.concatenate([un(o[0].v, "d_v") for o in outs], axis=0)
             forces = (np.concatenate([to_np(o[0].forces) for o in outs], axis=0)
                       if self.config.variant == GEMNET else None)
         energy = float(fw0.energy[0]) if fw0.energy.numel() == 1 else to_np(fw0.energy)
-        state = FeatureState(to_np(fw0.u), v, m, None, self.topology, self.geometry)
-        shards = [to_np(o[3]) for o in outs] if self.schedule == "reference" else []
+        state = FeatureState(un(fw0.u, "d_u"), v, m, None, self.topology, self.geometry)
+        shards = [un(o[3], "d_t") for o in outs] if self.schedule == "reference" else []
         result = ParallelRunResult(energy, forces, state, shards, log, [c.digests for c in comms],
                                    clocks[0].seconds(), self.partition)
         bundle = None

@@ -61,13 +61,14 @@ def test_model_matches_reference_golden(fname):
     grads = eng.weights.to_numpy(grads=True)
     e_ref = float(gd["energy"])
     assert abs(float(fw.energy[0]) - e_ref) <= TOL * max(abs(e_ref), 1e-8)
-    assert max_rel(fw.m.cpu().numpy(), gd["m"]) < TOL
-    assert max_rel(fw.v.cpu().numpy(), gd["v"]) < TOL
-    assert max_rel(fw.u.cpu().numpy(), gd["u"]) < TOL
+    dw = eng.weights  # padded widths (non-tile dims) -> reference channels
+    assert max_rel(dw.unpad_rows(fw.m, "d_e").cpu().numpy(), gd["m"]) < TOL
+    assert max_rel(dw.unpad_rows(fw.v, "d_v").cpu().numpy(), gd["v"]) < TOL
+    assert max_rel(dw.unpad_rows(fw.u, "d_u").cpu().numpy(), gd["u"]) < TOL
     assert max_rel(pos_bar.cpu().numpy(), gd["d_positions"]) < TOL
     if cfg.variant == "gemnet-style":
         assert max_rel(fw.forces.cpu().numpy(), gd["forces"]) < TOL
-    t_feat = eng.triplet_features(bg, fw, cfg.blocks - 1).cpu().numpy()
+    t_feat = dw.unpad_rows(eng.triplet_features(bg, fw, cfg.blocks - 1), "d_t").cpu().numpy()
     assert max_rel(t_feat, gd["t_feat"]) < TOL
     for name in gd["param_names"]:
         name = str(name)
@@ -137,7 +138,7 @@ def test_nn_module_autograd_path():
     loss.backward()
     G, _ = O.backward(f, params.arrays, 0.5, w.double().cpu().numpy())
     for name, p in model.named_parameters():
-        assert max_rel(p.grad.double().cpu().numpy(), G[name]) < TOL, name
+        assert max_rel(model.weights.unpad(name, p.grad.double().cpu().numpy()), G[name]) < TOL, name
 
 
 def test_dimenet_predict_forces_and_force_loss_error():
@@ -196,11 +197,52 @@ def test_rigid_motion_invariance():
 
 XL = {
     # C3 DimeNet++-XL (d_e 2048, d_v = d_u 1536, d_t 256) and C4 GemNet-XL
-    # (d_v = d_u 2320, d_e 1302, d_t 512, d_bil 288 > 256: channel-chunked triplet
-    # kernels, non-tile-aligned dims on the cuBLAS composite), 2 blocks, small graph
+    # (d_v = d_u 2320, d_e 1302 -> zero-padded to 1312 for the tcgen05 tiling, d_t 512,
+    # d_bil 288 > 256: channel-chunked triplet kernels), 2 blocks, small graph
     "c3-dimenet-xl": dict(variant="dimenet-style", blocks=2, d_u=1536, d_v=1536, d_e=2048, d_t=256, d_bil=64),
     "c4-gemnet-xl": dict(variant="gemnet-style", blocks=2, d_u=2320, d_v=2320, d_e=1302, d_t=512, d_bil=288),
 }
+
+
+@pytest.mark.parametrize("name", sorted(XL))
+def test_xl_dims_batch_over_8k_edges(name):
+    """C3/C4 widths on a batch above the SIMT threshold (> 8192 edges: every edge product on
+    the tcgen05 GEMM, d_e = 1302 padded), one block, vs the fp64 oracle per graph."""
+    from paper_2203_09697_b200 import ModelConfig, init_params
+    from paper_2203_09697_b200.engine import DeviceWeights, Engine
+    from paper_2203_09697_b200.graph import build_batch
+
+    cfg = ModelConfig(k_rbf=6, l_sbf=7, cutoff=6.0, seed=9, **{**XL[name], "blocks": 1})
+    params = init_params(cfg)
+    rng = np.random.default_rng(31)
+    systems = [O.random_cloud(80, 0.06, rng) for _ in range(6)]
+    eng = Engine(DeviceWeights.from_params(params))
+    assert eng.weights.config.d_e % 16 == 0
+    bg = build_batch([s[0] for s in systems], cfg.cutoff)
+    assert bg.num_edges > 8192
+    fw = eng.forward(bg)
+    gem = cfg.variant == "gemnet-style"
+    de = rng.standard_normal(len(systems))
+    dfs = [rng.standard_normal(s[0].shape) for s in systems] if gem else None
+    pos_bar = eng.backward(bg, fw, torch.tensor(de, device="cuda"),
+                           torch.tensor(np.concatenate(dfs), device="cuda") if gem else None).cpu().numpy()
+    grads = eng.weights.to_numpy(grads=True)
+    oc = O.Config(**{k: getattr(cfg, k) for k in O.Config.__dataclass_fields__})
+    ref_g = {k: np.zeros_like(v) for k, v in params.arrays.items()}
+    off = 0
+    for i, (pos, z) in enumerate(systems):
+        f = O.forward(oc, params.arrays, pos, z)
+        G, dp = O.backward(f, params.arrays, float(de[i]), dfs[i] if gem else None)
+        n = pos.shape[0]
+        assert abs(float(fw.energy[i]) - f.energy) <= TOL * max(abs(f.energy), 1e-8)
+        assert max_rel(pos_bar[off:off + n], dp) < TOL
+        if gem:
+            assert max_rel(fw.forces[off:off + n].double().cpu().numpy(), f.forces) < TOL
+        for k in ref_g:
+            ref_g[k] += G[k]
+        off += n
+    for k, g in ref_g.items():
+        assert max_rel(grads[k], g) < TOL, k
 
 
 @pytest.mark.parametrize("name", sorted(XL))
@@ -549,4 +591,4 @@ def test_egn_model_custom_op_under_torch_compile(variant):
     G, _ = O.backward(fr, params.arrays, 0.5, w.double().cpu().numpy() if variant == "gemnet-style" else None)
     assert abs(float(e0[0]) - fr.energy) <= TOL * max(1.0, abs(fr.energy))
     for n, g in G.items():
-        assert max_rel(g0[n].double().cpu().numpy(), g) < TOL, n
+        assert max_rel(model.weights.unpad(n, g0[n].double().cpu().numpy()), g) < TOL, n
