@@ -53,6 +53,12 @@ WORKLOADS = {
     # BASELINE configs[0] (the reference's own CPU-runnable case)
     "dimenet-pp-small": dict(variant="dimenet-style", blocks=4, d_u=128, d_v=128, d_e=128, d_t=64, d_bil=64,
                              k_rbf=6, l_sbf=7, cutoff=6.0, atoms=64, density=0.06, graphs=4, w_forces=0.0),
+    # BASELINE configs[2] / [3] on one GPU: DimeNet++-XL and
+    # GemNet-XL (d_e = 1302 zero-padded to 1312 for the tcgen05 tiling)
+    "dimenet-pp-xl": dict(variant="dimenet-style", blocks=4, d_u=1536, d_v=1536, d_e=2048, d_t=256, d_bil=64,
+                          k_rbf=6, l_sbf=7, cutoff=6.0, atoms=80, density=0.06, graphs=8, w_forces=0.0),
+    "gemnet-xl": dict(variant="gemnet-style", blocks=8, d_u=2320, d_v=2320, d_e=1302, d_t=512, d_bil=288,
+                      k_rbf=6, l_sbf=7, cutoff=6.0, atoms=80, density=0.06, graphs=8, w_forces=1.0),
 }
 
 
@@ -296,6 +302,7 @@ def _kernel_roofline(tr, bg, cfg):
     from paper_2203_09697_b200 import ops
 
     eng = tr.engine
+    cfg = eng.config  # padded widths (what the kernels run)
     fw = eng.forward(bg)
     st0 = fw.blocks[0]
     dg = cfg.triplet_width
@@ -331,19 +338,43 @@ def _kernel_roofline(tr, bg, cfg):
         if tj.get("workload", {}).get("edges") == ne:
             rec = tj.get(key, {})
             traffic = (rec.get("dram_read", 0) + rec.get("dram_write", 0)) or None
-    tf32_peak = peaks.get("bf16_tflops", 1640.8) / 2  # TF32 = half the bf16 tensor rate
-    return {"bound": "hbm", "kernel": f"gemm_tf32x3 E x {de} x {de} (+residual), 3xTF32 on tcgen05",
-            "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
+    bf16 = peaks.get("bf16_tflops", 1640.8)
+    tf32_peak = bf16 / 2  # TF32 = half the bf16 tensor rate
+    flops = 2.0 * ne * de * de
+    # fp32-accurate products cost 3 TF32 MMAs: the attainable rate is tf32_peak / 3; the kernel is
+    # tensor-bound when its intensity (fp32 FLOP per algorithmic byte) exceeds that rate / HBM
+    tensor_bound = flops / b_gemm > (tf32_peak / 3) * 1e12 / (hbm * 1e9)
+    base = {"kernel": f"gemm_tf32x3 E x {de} x {de} (+residual), 3xTF32 on tcgen05",
             "traffic": traffic, "traffic_source": f"profiles/r1_traffic.json:{key} (ncu --set full)" if traffic else None,
             "peak_source": "MEASURED_PEAKS.json" if peaks else "fallback",
-            "launch_us": t_g * 1e6, "algorithmic_bytes": b_gemm,
-            "tensor_frac": 3 * 2.0 * ne * de * de / t_g / 1e12 / tf32_peak,
+            "launch_us": t_g * 1e6, "algorithmic_bytes": b_gemm, "algorithmic_flops": flops,
+            "tensor_frac": 3 * flops / t_g / 1e12 / tf32_peak, "hbm_frac": ach / hbm}
+    if tensor_bound:
+        base.update(bound="tensor", achieved=flops / t_g / 1e12, unit="TFLOP/s", peak=tf32_peak / 3,
+                    frac=flops / t_g / 1e12 / (tf32_peak / 3),
+                    peak_derivation=f"measured dense bf16 {bf16:.0f} TF/s / 2 (TF32) / 3 (3xTF32 per fp32 product)")
+    else:
+        base.update(bound="hbm", achieved=ach, peak=hbm, unit="GB/s", frac=ach / hbm)
+    return {**base,
             "triplet": {"fwd_us": t_f * 1e6, "bwd_us": t_b * 1e6,
                         "fwd_gbs": b_fwd / t_f / 1e9, "bwd_gbs": b_bwd / t_b / 1e9,
                         "fwd_hbm_frac": b_fwd / t_f / 1e9 / hbm, "bwd_hbm_frac": b_bwd / t_b / 1e9 / hbm,
                         "fwd_gtrip_s": nt / t_f / 1e9, "bwd_gtrip_s": nt / t_b / 1e9,
                         "fwd_fp32_pipe_frac": fma / t_f / fp32_peak, "bwd_fp32_pipe_frac": 2 * fma / t_b / fp32_peak,
                         "algorithmic_bytes": {"fwd": b_fwd, "bwd": b_bwd}}}
+
+
+def dense_flops_per_step(cfg, ne, nv):
+    """SURVEY.md 8(d) dense algorithmic FLOPs (after the reorder) of one training step:
+    forward per block 2[N_e(d_e d_t + K d_t + K L d_t + d_t d_e + 3 d_e^2) + N_v(d_e d_v + d_v^2)]
+    (+ GemNet 2 N_e(d_t d_bil + K L d_bil + d_bil d_t + (d_e + d_v) d_e + 2 d_e^2)); backward ~2x."""
+    c = cfg
+    K, KL = c.k_rbf, c.k_rbf * c.l_sbf
+    f = 2 * (ne * (c.d_e * c.d_t + K * c.d_t + KL * c.d_t + c.d_t * c.d_e + 3 * c.d_e ** 2)
+             + nv * (c.d_e * c.d_v + c.d_v ** 2))
+    if c.variant == "gemnet-style":
+        f += 2 * ne * (c.d_t * c.d_bil + KL * c.d_bil + c.d_bil * c.d_t + (c.d_e + c.d_v) * c.d_e + 2 * c.d_e ** 2)
+    return 3.0 * f * c.blocks
 
 
 def run_ours(args, wl):
@@ -507,6 +538,11 @@ def run_ours(args, wl):
                        "triplets_total": int(nt[0]), "parallelism": parallelism,
                        "l2": "step working set > L2 (126 MB); kernel timings flush L2 with a 256 MB write"},
             "steps_per_s": 1.0 / t_dev,
+            "dense": {"tflop_per_step": dense_flops_per_step(cfg, int(nt[1]), sum(len(s.positions) for s in systems)
+                                                             * (world if aligned else 1)) / 1e12,
+                      "achieved_tflops": dense_flops_per_step(cfg, int(nt[1]), sum(len(s.positions) for s in systems)
+                                                              * (world if aligned else 1)) / t_dev / 1e12,
+                      "source": "SURVEY.md 8(d) formula, reference widths, fwd + 2x bwd"},
             "e2e": {"value": total_trip / t_e2e, "unit": "triplets/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": 8, "ms_per_step": t_e2e * 1e3},
             "gpu_launches": launches,

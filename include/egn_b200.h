@@ -158,12 +158,21 @@ int egn_sbf(const float* geo, const int64_t* edge_ptr, const int64_t* tri_ptr, i
  * The gate by rbf(d_ji) and the up projection are applied by the caller on
  * the per-edge result, which is exact because both are constant or linear
  * inside a triplet segment (engine.py:138,147-148).
- * max_degree: max deg(j) if known (selects the deg<=64 fast path alone), -1 if not.
+ * max_degree: max deg(j) if known (selects the deg<=64 fast path alone, and sizes the
+ * spherical-harmonic path's per-chunk moments), -1 if not.
+ * workspace: egn_triplet_fwd_workspace_bytes(...) bytes (NULL: the spherical-harmonic path is
+ * not used).
  */
+int64_t egn_triplet_fwd_workspace_bytes(int64_t num_nodes, int max_degree, int k_rbf, int l_sbf, int dg);
 int egn_triplet_fwd(const int64_t* edge_ptr, const int32_t* rev, const float* geo,
                     int64_t num_nodes, int max_degree, const float* X, const float* W, int k_rbf,
-                    int l_sbf, int dg, double cutoff, float* S, egn_stream_t stream);
+                    int l_sbf, int dg, double cutoff, float* S, void* workspace, egn_stream_t stream);
 
+/* Triplet kernel selection (returns the previous mode; -1 queries): 0 = auto (deg <= 64:
+ * pairwise centre tiles; larger centres: linear-in-degree spherical-harmonic kernels, the
+ * angular sum factorised by the addition theorem -- triplet_sh.cu), 1 = spherical-harmonic
+ * kernels for every centre, 2 = pairwise kernels only (tensor-core kernels above deg 64). */
+int egn_triplet_path(int mode);
 /* Triplet window (graph-parallel reference schedule: one split_range shard of the triplet
  * list, egn/partition.py:28-37, egn/runtime.py:425-431).  The launch covers the centres of
  * edge_ptr[0 .. num_nodes] and keeps only triplets whose centre-local index
@@ -188,8 +197,8 @@ int egn_triplet_bwd_window(const int64_t* edge_ptr, const int32_t* rev, const fl
  *                              in-edge distance of the basis.
  * max_degree bounds deg(j) over all centres (sizes shared memory).
  * workspace: egn_triplet_bwd_workspace_bytes(...) bytes of device memory. */
-int64_t egn_triplet_bwd_workspace_bytes(int64_t num_nodes, int64_t num_edges, int k_rbf, int l_sbf,
-                                        int dg);
+int64_t egn_triplet_bwd_workspace_bytes(int64_t num_nodes, int64_t num_edges, int max_degree, int k_rbf,
+                                        int l_sbf, int dg);
 int egn_triplet_bwd(const int64_t* edge_ptr, const int32_t* rev, const float* geo,
                     int64_t num_nodes, int64_t num_edges, int max_degree, const float* X,
                     const float* W, int k_rbf, int l_sbf, int dg, double cutoff, const float* S_bar,

@@ -55,10 +55,12 @@ SIGNATURES: dict[str, tuple] = {
     "egn_triplet_angles": (_i32, [_p, _p, _p, _p, _i64, _p, _p]),
     "egn_rbf": (_i32, [_p, _i64, _i32, _f64, _p, _p]),
     "egn_sbf": (_i32, [_p, _p, _p, _i64, _i32, _i32, _f64, _p, _p]),
-    "egn_triplet_fwd": (_i32, [_p, _p, _p, _i64, _i32, _p, _p, _i32, _i32, _i32, _f64, _p, _p]),
-    "egn_triplet_bwd_workspace_bytes": (_i64, [_i64, _i64, _i32, _i32, _i32]),
+    "egn_triplet_fwd_workspace_bytes": (_i64, [_i64, _i32, _i32, _i32, _i32]),
+    "egn_triplet_fwd": (_i32, [_p, _p, _p, _i64, _i32, _p, _p, _i32, _i32, _i32, _f64, _p, _p, _p]),
+    "egn_triplet_bwd_workspace_bytes": (_i64, [_i64, _i64, _i32, _i32, _i32, _i32]),
     "egn_triplet_bwd": (_i32, [_p, _p, _p, _i64, _i64, _i32, _p, _p, _i32, _i32, _i32, _f64, _p, _p, _p, _p, _p,
                                _p]),
+    "egn_triplet_path": (_i32, [_i32]),
     "egn_triplet_fwd_window": (_i32, [_p, _p, _p, _i64, _i64, _i64, _p, _p, _i32, _i32, _i32, _f64, _p, _p]),
     "egn_triplet_bwd_window": (_i32, [_p, _p, _p, _i64, _i64, _i64, _i32, _p, _p, _i32, _i32, _i32, _f64, _p, _p,
                                       _p, _p, _p, _p]),
@@ -130,19 +132,20 @@ def stream() -> int:
 
 # Kernels launched per successful ABI call (for the bench's gpu_launches count).
 KERNELS_PER_CALL = {
-    "egn_triplet_bwd": 4, "egn_triplet_bwd_window": 2, "egn_graph_linear_bwd": 2, "egn_geometry_grads": 2, "egn_force_head_fwd": 2, "egn_force_head_bwd": 2, "egn_column_sum": 2, "egn_gemm_wgrad": 2, "egn_rbf_linear_bwd": 2, "egn_graph_mlp_fwd": 2, "egn_graph_mlp_bwd": 3, "egn_cap_keep": 2, "egn_cap_compact": 2,
+    "egn_triplet_bwd": 4, "egn_triplet_fwd": 2, "egn_triplet_bwd_window": 2, "egn_graph_linear_bwd": 2, "egn_geometry_grads": 2, "egn_force_head_fwd": 2, "egn_force_head_bwd": 2, "egn_column_sum": 2, "egn_gemm_wgrad": 2, "egn_rbf_linear_bwd": 2, "egn_graph_mlp_fwd": 2, "egn_graph_mlp_bwd": 3, "egn_cap_keep": 2, "egn_cap_compact": 2,
 }
 LAUNCH_COUNTER = {"calls": 0, "kernels": 0}
+_NOT_LAUNCHES = {"egn_triplet_path", "egn_abi_version"}
 
 
 def call(name: str, *args) -> int:
     """Invoke an ABI function; raise EgnNativeError with the library message on failure."""
     fn = getattr(lib(), name)
     rc = fn(*args)
-    if SIGNATURES[name][0] is _i32 and not name.endswith("_bytes"):
+    if SIGNATURES[name][0] is _i32 and not name.endswith("_bytes") and name not in _NOT_LAUNCHES:
         LAUNCH_COUNTER["calls"] += 1
         LAUNCH_COUNTER["kernels"] += KERNELS_PER_CALL.get(name, 1)
-    if SIGNATURES[name][0] is _i32 and rc != 0:
+    if SIGNATURES[name][0] is _i32 and rc != 0 and name not in _NOT_LAUNCHES:
         msg = lib().egn_last_error().decode(errors="replace")
         if rc == 2:
             raise ValueError(f"{name}: {msg}")

@@ -500,7 +500,7 @@ using namespace egn;
 extern "C" {
 
 const char* egn_last_error(void) { return g_err; }
-int egn_abi_version(void) { return 2; }
+int egn_abi_version(void) { return 3; }
 
 int egn_neighbors_count(const double* pos, const int64_t* graph_ptr, const int32_t* node_graph,
                         int64_t num_nodes, double cutoff, int32_t* deg, egn_stream_t stream) {

@@ -32,6 +32,7 @@
 #include <algorithm>
 
 #include <cstdlib>
+#include <string>
 
 #include "common.cuh"
 
@@ -554,6 +555,26 @@ int fast_bwd(const int64_t* edge_ptr, const int32_t* rev, const float4* geo, int
              const float* X, const float* W, int K, int L, int dg, RbfParams rp, const float* Sbar, float* Xbar,
              float* Wbar, float4* edge_grad, void* ws, cudaStream_t st);
 constexpr int kFastMaxDeg = 64;
+// spherical-harmonic factorised path (triplet_sh.cu): O(deg) per edge
+bool sh_supported(int K, int L, int dg);
+int64_t sh_fwd_workspace_bytes(int64_t nv, int max_degree, int K, int L, int dg);
+int sh_fwd(const int64_t* edge_ptr, const int32_t* rev, const float4* geo, int64_t nv, int max_degree, const float* X,
+           const float* W, int K, int L, int dg, RbfParams rp, float* S, void* ws, int min_n, cudaStream_t st);
+int64_t sh_bwd_workspace_bytes(int64_t nv, int64_t ne, int max_degree, int K, int L, int dg);
+int sh_bwd(const int64_t* edge_ptr, const int32_t* rev, const float4* geo, int64_t nv, int64_t ne, int max_degree,
+           const float* X, const float* W, int K, int L, int dg, RbfParams rp, const float* Sbar, float* Xbar,
+           float* Wbar, float4* edge_grad, void* ws, int min_n, int accumulate, cudaStream_t st);
+
+// Path selection (egn_triplet_path): 0 = auto (deg <= 64: pairwise centre tiles; larger centres:
+// the linear-in-degree spherical-harmonic kernels), 1 = spherical-harmonic kernels for every
+// centre, 2 = pairwise only (centre tiles + tensor-core kernels for deg > 64).  EGN_TRIPLET_PATH
+// (auto / sh / pairwise) sets the initial value; EGN_TRIPLET_TC_ALL=1 forces the tensor path.
+static int g_triplet_path = [] {
+  const char* e = std::getenv("EGN_TRIPLET_PATH");
+  if (!e) return 0;
+  const std::string v(e);
+  return v == "sh" ? 1 : (v == "pairwise" ? 2 : 0);
+}();
 bool tc_fwd_supported(int K, int L, int dg, int max_degree);
 bool tc_bwd_supported(int K, int L, int dg, int max_degree);
 int64_t tc_bwd_workspace_bytes(int64_t nv, int K, int L);
@@ -675,9 +696,16 @@ static int check_dims(int K, int L, int dg) {
 
 extern "C" {
 
+int64_t egn_triplet_fwd_workspace_bytes(int64_t num_nodes, int max_degree, int k_rbf, int l_sbf, int dg) {
+  // only the spherical-harmonic path needs one (its per-chunk moments)
+  const bool fast_covers = g_triplet_path == 0 && fast_supported(k_rbf, l_sbf, dg) && max_degree <= kFastMaxDeg;
+  if (!sh_supported(k_rbf, l_sbf, dg) || max_degree < 0 || g_triplet_path == 2 || fast_covers) return 0;
+  return sh_fwd_workspace_bytes(num_nodes, max_degree, k_rbf, l_sbf, dg);
+}
+
 int egn_triplet_fwd(const int64_t* edge_ptr, const int32_t* rev, const float* geo,
                     int64_t num_nodes, int max_degree, const float* X, const float* W, int k_rbf,
-                    int l_sbf, int dg, double cutoff, float* S, egn_stream_t stream) {
+                    int l_sbf, int dg, double cutoff, float* S, void* workspace, egn_stream_t stream) {
   if (int rc = check_dims(k_rbf, l_sbf, dg)) return rc;
   if (num_nodes == 0) return 0;
   RbfParams rp = rbf_params(k_rbf, cutoff);
@@ -688,11 +716,16 @@ int egn_triplet_fwd(const int64_t* edge_ptr, const int32_t* rev, const float* ge
   // the generic CUDA-core kernel
   int min_n = 0;
   static const bool tc_all = [] { const char* e = std::getenv("EGN_TRIPLET_TC_ALL"); return e && e[0] == '1'; }();
-  if (fast_supported(k_rbf, l_sbf, dg) && !(tc_all && tc_fwd_supported(k_rbf, l_sbf, dg, max_degree))) {
+  const bool use_sh = !tc_all && g_triplet_path != 2 && sh_supported(k_rbf, l_sbf, dg) && max_degree >= 0 &&
+                      workspace != nullptr;
+  if (fast_supported(k_rbf, l_sbf, dg) && !(tc_all && tc_fwd_supported(k_rbf, l_sbf, dg, max_degree)) &&
+      !(use_sh && g_triplet_path == 1)) {
     if (int rc = fast_fwd(edge_ptr, rev, g4, num_nodes, X, W, k_rbf, l_sbf, dg, rp, S, st)) return rc;
     if (max_degree >= 0 && max_degree <= kFastMaxDeg) return 0;
     min_n = kFastMaxDeg;
   }
+  if (use_sh)
+    return sh_fwd(edge_ptr, rev, g4, num_nodes, max_degree, X, W, k_rbf, l_sbf, dg, rp, S, workspace, min_n, st);
   if (tc_fwd_supported(k_rbf, l_sbf, dg, max_degree))
     return tc_fwd(edge_ptr, rev, g4, num_nodes, max_degree, X, W, k_rbf, l_sbf, dg, rp, S, min_n, st);
 #define EGN_FWD(CW, GC, R) \
@@ -716,9 +749,13 @@ static int64_t fast_ws_bytes(int64_t num_nodes, int64_t num_edges, int k_rbf, in
   return fast_supported(k_rbf, l_sbf, dg) ? fast_bwd_workspace_bytes(num_nodes, num_edges, k_rbf, l_sbf, dg) : 0;
 }
 
-int64_t egn_triplet_bwd_workspace_bytes(int64_t num_nodes, int64_t num_edges, int k_rbf, int l_sbf, int dg) {
+int64_t egn_triplet_bwd_workspace_bytes(int64_t num_nodes, int64_t num_edges, int max_degree, int k_rbf, int l_sbf,
+                                        int dg) {
   return generic_ws_bytes(num_nodes, k_rbf, l_sbf, dg) + fast_ws_bytes(num_nodes, num_edges, k_rbf, l_sbf, dg) +
-         tc_bwd_workspace_bytes(num_nodes, k_rbf, l_sbf);
+         tc_bwd_workspace_bytes(num_nodes, k_rbf, l_sbf) +
+         (sh_supported(k_rbf, l_sbf, dg) && max_degree >= 0
+              ? sh_bwd_workspace_bytes(num_nodes, num_edges, max_degree, k_rbf, l_sbf, dg)
+              : 0);
 }
 
 int egn_triplet_bwd(const int64_t* edge_ptr, const int32_t* rev, const float* geo,
@@ -736,7 +773,9 @@ int egn_triplet_bwd(const int64_t* edge_ptr, const int32_t* rev, const float* ge
   float4* eg = reinterpret_cast<float4*>(edge_grad);
   int min_n = 0, accumulate = 0;
   static const bool tc_all = [] { const char* e = std::getenv("EGN_TRIPLET_TC_ALL"); return e && e[0] == '1'; }();
-  if (fast_supported(k_rbf, l_sbf, dg) && !(tc_all && tc_bwd_supported(k_rbf, l_sbf, dg, max_degree))) {
+  const bool use_sh = !tc_all && g_triplet_path != 2 && sh_supported(k_rbf, l_sbf, dg) && max_degree >= 0;
+  if (fast_supported(k_rbf, l_sbf, dg) && !(tc_all && tc_bwd_supported(k_rbf, l_sbf, dg, max_degree)) &&
+      !(use_sh && g_triplet_path == 1)) {
     char* fws = reinterpret_cast<char*>(workspace) + generic_ws_bytes(num_nodes, k_rbf, l_sbf, dg);
     if (int rc = fast_bwd(edge_ptr, rev, g4, num_nodes, num_edges, X, W, k_rbf, l_sbf, dg, rp, S_bar, X_bar,
                           W_bar, eg, fws, st))
@@ -744,6 +783,12 @@ int egn_triplet_bwd(const int64_t* edge_ptr, const int32_t* rev, const float* ge
     if (max_degree >= 0 && max_degree <= kFastMaxDeg) return 0;
     min_n = kFastMaxDeg;
     accumulate = 1;
+  }
+  if (use_sh) {
+    char* sws = reinterpret_cast<char*>(workspace) + generic_ws_bytes(num_nodes, k_rbf, l_sbf, dg) +
+                fast_ws_bytes(num_nodes, num_edges, k_rbf, l_sbf, dg) + tc_bwd_workspace_bytes(num_nodes, k_rbf, l_sbf);
+    return sh_bwd(edge_ptr, rev, g4, num_nodes, num_edges, max_degree, X, W, k_rbf, l_sbf, dg, rp, S_bar, X_bar,
+                  W_bar, eg, sws, min_n, accumulate, st);
   }
   // centres above the small-degree kernel's range: tensor-core backward (triplet_tc_bwd.cu)
   if (tc_bwd_supported(k_rbf, l_sbf, dg, max_degree)) {
@@ -764,6 +809,12 @@ int egn_triplet_bwd(const int64_t* edge_ptr, const int32_t* rev, const float* ge
   if (dg <= 128) EGN_BWD(8, 16, 4);
   EGN_BWD(8, 32, 4);
 #undef EGN_BWD
+}
+
+int egn_triplet_path(int mode) {
+  const int old = g_triplet_path;
+  if (mode >= 0 && mode <= 2) g_triplet_path = mode;
+  return old;
 }
 
 int egn_triplet_fwd_window(const int64_t* edge_ptr, const int32_t* rev, const float* geo, int64_t num_nodes,

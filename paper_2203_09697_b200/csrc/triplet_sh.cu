@@ -1,0 +1,1006 @@
+// Linear-in-degree triplet interaction: the angular sum factorised with the spherical-harmonic
+// addition theorem (checked in fp64 by tools/sh_triplet_check.py).
+//
+// Per centre j with out-edges p, q (unit vectors u, distances d) the reference's triplet sum
+// (egn/engine.py:136-148 with cos(l alpha) = T_l(u_p . u_q), the same algebra as triplet.cu)
+//     S[p, c] = sum_{q != p} sum_l T_l(u_p . u_q) Q[q, l, c],   Q[q, l, c] = X[rq, c] sum_k rbf_k(d_q) W[k, l, c]
+// costs O(n^2 L) per centre.  With T_l = sum_j a_lj P_j (Chebyshev in the Legendre basis, exact
+// rationals below) and P_j(u_p . u_q) = 4 pi / (2j+1) sum_m Y_jm(u_p) Y_jm(u_q):
+//     W'[k, j, c]  = sum_l W[k, l, c] A[l][j],          A[l][j] = a_lj 4 pi / (2j+1)
+//     Q'[q, j, c]  = X[rq, c] sum_k rbf_k(d_q) W'[k, j, c]
+//     M[jm, c]     = sum_q Y_jm(u_q) Q'[q, j, c]                       (L^2 = 49 moments)
+//     S[p, c]      = sum_jm Y_jm(u_p) M[jm, c] - sum_j s_j Q'[p, j, c],  s_j = (2j+1) / (4 pi)
+// (the last term removes q = p, where T_l(1) = 1): O(n L^2) per centre.  At deg 500 (C5) that is
+// ~36x fewer FMAs than the pairwise form, and the kernels become bound by the X gather.
+//
+// Backward (S_bar given), per centre:
+//     Mbar[jm, c]   = sum_p Y_jm(u_p) S_bar[p, c]
+//     Q'bar[e, j, c] = sum_m Y_jm(u_e) Mbar[jm, c] - s_j S_bar[e, c]
+//     X_bar[re, c]  = sum_j Q'bar R'_j,  R'bar = Q'bar X[re, c] -> W'_bar, dE/dd_e (rbf')
+//     dE/du_e       = sum_jm grad Y_jm(u_e) P[e, jm],  P[e, jm] = sum_c (S_bar[e, c] M[jm, c] + Mbar[jm, c] Q'[e, j, c])
+// and dE/dv_e = (I - u u^T) dE/du_e / d_e.  W_bar[k, l, c] = sum_j A[l][j] W'_bar[k, j, c].
+//
+// Mapping: one warp per (centre, 32-channel block), lane = channel; 4 independent warps per CTA
+// (no block-level barriers).  Edges go in tiles of 32: lane t evaluates Y(u_t) (49 values)
+// into the warp's shared tile, then every lane sweeps the tile (broadcast reads).  Sums over
+// channels (P, dE/dd) are warp butterflies.  Everything is fixed-order: deterministic.
+#include <algorithm>
+
+#include "common.cuh"
+
+namespace egn {
+namespace sh {
+
+constexpr int kW = 4;     // warps per CTA
+constexpr int kTile = 32;  // edges per tile
+constexpr float kPi = 3.14159265358979323846f;
+
+// a_lj: T_l = sum_j a_lj P_j (l, j < 8), exact rationals
+__host__ __device__ constexpr double cheb_leg(int l, int j) {
+  constexpr double a[8][8] = {
+      {1, 0, 0, 0, 0, 0, 0, 0},
+      {0, 1, 0, 0, 0, 0, 0, 0},
+      {-1.0 / 3, 0, 4.0 / 3, 0, 0, 0, 0, 0},
+      {0, -3.0 / 5, 0, 8.0 / 5, 0, 0, 0, 0},
+      {-1.0 / 15, 0, -16.0 / 21, 0, 64.0 / 35, 0, 0, 0},
+      {0, -1.0 / 7, 0, -8.0 / 9, 0, 128.0 / 63, 0, 0},
+      {-1.0 / 35, 0, -4.0 / 21, 0, -384.0 / 385, 0, 512.0 / 231, 0},
+      {0, -1.0 / 15, 0, -112.0 / 495, 0, -128.0 / 117, 0, 1024.0 / 429}};
+  return a[l][j];
+}
+
+__host__ __device__ constexpr double factd(int n) { return n <= 1 ? 1.0 : n * factd(n - 1); }
+__host__ __device__ constexpr double dfact(int n) { return n <= 1 ? 1.0 : n * dfact(n - 2); }  // (2m-1)!!
+__host__ __device__ constexpr double csqrt(double x) {
+  double g = x > 1 ? x : 1.0;
+  for (int i = 0; i < 60; ++i) g = 0.5 * (g + x / g);
+  return x <= 0 ? 0.0 : g;
+}
+
+// Every constant the kernels need, evaluated by the compiler and placed in constant memory
+// (indices are compile-time after unrolling, so they become constant-bank operands).
+struct ShTables {
+  float norm[8][8];  // orthonormal real-harmonic normalisation (sqrt 2 for m > 0)
+  float qmm[8];      // Q_m^m = (2m-1)!!
+  float A[8][8];     // A[l][j] = a_lj 4 pi / (2j+1): W' = W A
+  float s[8];        // (2j+1) / (4 pi): the q = p (self) term
+};
+constexpr ShTables make_tables() {
+  ShTables t{};
+  const double pi = 3.14159265358979323846;
+  for (int j = 0; j < 8; ++j) {
+    for (int m = 0; m < 8; ++m)
+      t.norm[j][m] = m > j ? 0.f
+                           : static_cast<float>(csqrt((2 * j + 1) / (4 * pi) * factd(j - m) / factd(j + m)) *
+                                                (m > 0 ? 1.4142135623730950488 : 1.0));
+    t.qmm[j] = static_cast<float>(dfact(2 * j - 1));
+    t.s[j] = static_cast<float>((2 * j + 1) / (4 * pi));
+    for (int l = 0; l < 8; ++l) t.A[l][j] = static_cast<float>(cheb_leg(l, j) * 4 * pi / (2 * j + 1));
+  }
+  return t;
+}
+__constant__ ShTables c_tab = make_tables();
+
+// Y_jm(u) for j < L at index j*j + j + m (m in [-j, j]), written with stride `st`.
+// Recurrences: C_m + i S_m = (x + i y)^m; Q_j^m(z) = associated Legendre without (1-z^2)^(m/2).
+template <int L>
+__device__ __forceinline__ void sh_eval(float x, float y, float z, float* out, int st) {
+  float C[L], S[L];
+  C[0] = 1.f;
+  S[0] = 0.f;
+#pragma unroll
+  for (int m = 1; m < L; ++m) {
+    C[m] = x * C[m - 1] - y * S[m - 1];
+    S[m] = x * S[m - 1] + y * C[m - 1];
+  }
+#pragma unroll
+  for (int m = 0; m < L; ++m) {
+    float q2 = 0.f, q1 = c_tab.qmm[m];
+#pragma unroll
+    for (int j = m; j < L; ++j) {
+      float q;
+      if (j == m) {
+        q = q1;
+      } else if (j == m + 1) {
+        q = static_cast<float>(2 * m + 1) * z * q1;
+        q2 = q1;
+        q1 = q;
+      } else {
+        q = (static_cast<float>(2 * j - 1) * z * q1 - static_cast<float>(j + m - 1) * q2) *
+            static_cast<float>(1.0 / (j - m));
+        q2 = q1;
+        q1 = q;
+      }
+      const float nq = c_tab.norm[j][m] * q;
+      if (m == 0) {
+        out[(j * j + j) * st] = nq;
+      } else {
+        out[(j * j + j + m) * st] = nq * C[m];
+        out[(j * j + j - m) * st] = nq * S[m];
+      }
+    }
+  }
+}
+
+// g = sum_jm P[jm] grad Y_jm(u) (Cartesian gradient of the recurrence polynomials; only its
+// tangential part is used, where it equals the spherical gradient).
+template <int L>
+__device__ __forceinline__ float3 sh_grad(float x, float y, float z, const float* P, int st) {
+  float C[L], S[L];
+  C[0] = 1.f;
+  S[0] = 0.f;
+#pragma unroll
+  for (int m = 1; m < L; ++m) {
+    C[m] = x * C[m - 1] - y * S[m - 1];
+    S[m] = x * S[m - 1] + y * C[m - 1];
+  }
+  float gx = 0.f, gy = 0.f, gz = 0.f;
+#pragma unroll
+  for (int m = 0; m < L; ++m) {
+    float q2 = 0.f, q1 = c_tab.qmm[m], d2 = 0.f, d1 = 0.f;
+#pragma unroll
+    for (int j = m; j < L; ++j) {
+      float q, dq;
+      if (j == m) {
+        q = q1;
+        dq = 0.f;
+      } else if (j == m + 1) {
+        q = static_cast<float>(2 * m + 1) * z * q1;
+        dq = static_cast<float>(2 * m + 1) * (q1 + z * d1);
+        q2 = q1;
+        q1 = q;
+        d2 = d1;
+        d1 = dq;
+      } else {
+        const float inv = static_cast<float>(1.0 / (j - m));
+        q = (static_cast<float>(2 * j - 1) * z * q1 - static_cast<float>(j + m - 1) * q2) * inv;
+        dq = (static_cast<float>(2 * j - 1) * (q1 + z * d1) - static_cast<float>(j + m - 1) * d2) * inv;
+        q2 = q1;
+        q1 = q;
+        d2 = d1;
+        d1 = dq;
+      }
+      const float nrm = c_tab.norm[j][m];
+      if (m == 0) {
+        gz = fmaf(P[(j * j + j) * st], nrm * dq, gz);
+      } else {
+        const float pc = P[(j * j + j + m) * st] * nrm, ps = P[(j * j + j - m) * st] * nrm;
+        const float fm = static_cast<float>(m);
+        // d/dx (x+iy)^m = m (x+iy)^(m-1), d/dy = i m (x+iy)^(m-1)
+        gx = fmaf(pc, q * fm * C[m - 1], fmaf(ps, q * fm * S[m - 1], gx));
+        gy = fmaf(pc, -q * fm * S[m - 1], fmaf(ps, q * fm * C[m - 1], gy));
+        gz = fmaf(pc, dq * C[m], fmaf(ps, dq * S[m], gz));
+      }
+    }
+  }
+  return make_float3(gx, gy, gz);
+}
+
+// grad Y_jm(u) (Cartesian gradient of the recurrence polynomials) for j < L, written as
+// out[3 (j*j + j + m) + d], d = x, y, z
+template <int L>
+__device__ __forceinline__ void sh_grad_table(float x, float y, float z, float* out) {
+  float C[L], S[L];
+  C[0] = 1.f;
+  S[0] = 0.f;
+#pragma unroll
+  for (int m = 1; m < L; ++m) {
+    C[m] = x * C[m - 1] - y * S[m - 1];
+    S[m] = x * S[m - 1] + y * C[m - 1];
+  }
+#pragma unroll
+  for (int m = 0; m < L; ++m) {
+    float q2 = 0.f, q1 = c_tab.qmm[m], d2 = 0.f, d1 = 0.f;
+#pragma unroll
+    for (int j = m; j < L; ++j) {
+      float q, dq;
+      if (j == m) {
+        q = q1;
+        dq = 0.f;
+      } else if (j == m + 1) {
+        q = static_cast<float>(2 * m + 1) * z * q1;
+        dq = static_cast<float>(2 * m + 1) * (q1 + z * d1);
+        q2 = q1;
+        q1 = q;
+        d2 = d1;
+        d1 = dq;
+      } else {
+        const float inv = static_cast<float>(1.0 / (j - m));
+        q = (static_cast<float>(2 * j - 1) * z * q1 - static_cast<float>(j + m - 1) * q2) * inv;
+        dq = (static_cast<float>(2 * j - 1) * (q1 + z * d1) - static_cast<float>(j + m - 1) * d2) * inv;
+        q2 = q1;
+        q1 = q;
+        d2 = d1;
+        d1 = dq;
+      }
+      const float nrm = c_tab.norm[j][m];
+      if (m == 0) {
+        float* o = out + 3 * (j * j + j);
+        o[0] = 0.f;
+        o[1] = 0.f;
+        o[2] = nrm * dq;
+      } else {
+        const float fm = static_cast<float>(m), nq = nrm * q * fm;
+        float* oc = out + 3 * (j * j + j + m);
+        oc[0] = nq * C[m - 1];
+        oc[1] = -nq * S[m - 1];
+        oc[2] = nrm * dq * C[m];
+        float* os = out + 3 * (j * j + j - m);
+        os[0] = nq * S[m - 1];
+        os[1] = nq * C[m - 1];
+        os[2] = nrm * dq * S[m];
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ float rbf1(float d, int k, RbfParams rp) {
+  const float dd = d - rp.step * k;
+  return __expf(-rp.gamma * dd * dd);
+}
+
+// W'[k][j] = sum_l W[k, l, c] A[l][j] for this lane's channel
+template <int K, int L>
+__device__ __forceinline__ void load_wprime(float (&wp)[K][L], const float* __restrict__ W, int dg, int c, bool cok) {
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    float w[L];
+#pragma unroll
+    for (int l = 0; l < L; ++l) w[l] = cok ? __ldg(W + (k * L + l) * dg + c) : 0.f;
+#pragma unroll
+    for (int j = 0; j < L; ++j) {
+      float s = 0.f;
+#pragma unroll
+      for (int l = j; l < L; l += 2) s = fmaf(w[l], c_tab.A[l][j], s);  // a_lj = 0 unless l >= j, l - j even
+      wp[k][j] = s;
+    }
+  }
+}
+
+template <int L>
+__device__ __forceinline__ constexpr int jof(int jm) {
+  int j = 0;
+  while ((j + 1) * (j + 1) <= jm) ++j;
+  return j;
+}
+
+// warp shared-memory carve-up (floats).  The Y tile is edge-major with a 16-byte aligned row
+// (52 floats), so a lane reads four harmonics of one edge with one broadcast LDS.128.
+constexpr int kYS = 52;
+template <int K, int L, int T = kTile>
+struct WarpSmem {
+  static constexpr int J = L * L;
+  static_assert(J <= kYS, "L <= 7 for the 52-float Y rows");
+  static constexpr int ys = 0;                        // Y tile [T][kYS]
+  static constexpr int rs = ys + T * kYS;             // rbf tile [T][8]
+  static constexpr int us = rs + T * 8;               // float4 (u, d) [T]
+  static constexpr int rq = us + 4 * T;               // int rq [T]
+  static constexpr int xs = rq + T;                   // X[rq_t, c] of the tile [T t][32 lanes]
+  static constexpr int sbs = xs + T * 32;             // S_bar[e_t, c] of the tile (backward)
+  static constexpr int ms = sbs + T * 32;             // M [J][32] (backward, lane columns)
+  static constexpr int pt = ms + J * 32;              // P tile [J + 1][T] (backward)
+  static constexpr int fwd_total = ms;
+  static constexpr int bwd_total = pt + (J + 1) * T;
+};
+
+// stage the tile [t0, t0 + 32) of the centre's out-edges: Y, rbf, (u, d), rev, and this lane's
+// channel of the gathered X rows (and of S_bar for the backward): all 32 row loads of the tile
+// are issued back to back, so the sweep over the tile never waits on a dependent global load.
+template <int K, int L, int T = kTile>
+__device__ __forceinline__ void stage_tile(float* wsm, const float4* __restrict__ geo, const int32_t* __restrict__ rev,
+                                           int64_t off, int t0, int n, RbfParams rp, int lane,
+                                           const float* __restrict__ X = nullptr, const float* __restrict__ Sbar = nullptr,
+                                           int dg = 0, int c = 0, bool cok = false) {
+  using SM = WarpSmem<K, L, T>;
+  const int e = t0 + lane;
+  int32_t rq = 0;
+  if (lane < T && e < n) {
+    const float4 g = geo[off + e];
+    rq = rev[off + e];
+    reinterpret_cast<float4*>(wsm + SM::us)[lane] = g;
+    reinterpret_cast<int32_t*>(wsm + SM::rq)[lane] = rq;
+    sh_eval<L>(g.x, g.y, g.z, wsm + SM::ys + lane * kYS, 1);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) wsm[SM::rs + lane * 8 + k] = k < K ? rbf1(g.w, k, rp) : 0.f;
+  }
+  const int nt = min(T, n - t0);
+  if (X) {
+    float xv[T];
+#pragma unroll
+    for (int t = 0; t < T; ++t) {
+      const int64_t r = __shfl_sync(0xffffffffu, rq, t);
+      xv[t] = (t < nt && cok) ? __ldg(X + r * dg + c) : 0.f;
+    }
+#pragma unroll
+    for (int t = 0; t < T; ++t) wsm[SM::xs + t * 32 + lane] = xv[t];
+  }
+  if (Sbar) {
+    float sv[T];
+#pragma unroll
+    for (int t = 0; t < T; ++t) sv[t] = (t < nt && cok) ? __ldg(Sbar + (off + t0 + t) * dg + c) : 0.f;
+#pragma unroll
+    for (int t = 0; t < T; ++t) wsm[SM::sbs + t * 32 + lane] = sv[t];
+  }
+  __syncwarp();
+}
+
+// the harmonics / radial values of tile edge t as registers (broadcast vector loads)
+template <int J>
+__device__ __forceinline__ void load_y(const float* ys_row, float (&y)[J]) {
+#pragma unroll
+  for (int i = 0; i < J; i += 4) {
+    const float4 v = *reinterpret_cast<const float4*>(ys_row + i);
+    y[i] = v.x;
+    if (i + 1 < J) y[i + 1] = v.y;
+    if (i + 2 < J) y[i + 2] = v.z;
+    if (i + 3 < J) y[i + 3] = v.w;
+  }
+}
+template <int K>
+__device__ __forceinline__ void load_rb(const float* rs_row, float (&rb)[K]) {
+  const float4 a = *reinterpret_cast<const float4*>(rs_row);
+  const float4 b = *reinterpret_cast<const float4*>(rs_row + 4);
+  const float v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+#pragma unroll
+  for (int k = 0; k < K; ++k) rb[k] = v[k];
+}
+
+// R'_j = sum_k rbf_k W'[k, j]
+template <int K, int L>
+__device__ __forceinline__ void rprime(const float (&rb)[K], const float (&wp)[K][L], float (&r)[L]) {
+#pragma unroll
+  for (int jj = 0; jj < L; ++jj) {
+    float s = 0.f;
+#pragma unroll
+    for (int k = 0; k < K; ++k) s = fmaf(rb[k], wp[k][jj], s);
+    r[jj] = s;
+  }
+}
+
+template <int L>
+__device__ __forceinline__ float self_w(int j) {
+  return c_tab.s[j];
+}
+
+// ---------------------------------------------------------------------------
+// work items: (centre j, chunk of kChunk out-edges, 32-channel block).  A centre of degree n
+// has ceil(n / kChunk) chunks; items run over nv x nch x ncb (nch from the max degree), so a
+// deg-500 centre is spread over 4 warps per channel block instead of one.  The moments of a
+// centre are the fixed-order sum of its chunks' partial moments (global, [nv][nch][J][dg]).
+// ---------------------------------------------------------------------------
+constexpr int kChunk = 4 * kTile;
+
+struct Item {
+  int64_t j, off;
+  int n, ch, e0, e1, c;
+  bool cok, live;
+};
+__device__ __forceinline__ Item decode(int64_t it, int nch, int ncb, const int64_t* __restrict__ edge_ptr, int dg,
+                                       int min_n, int lane) {
+  Item x;
+  const int64_t jc = it / ncb;
+  x.c = static_cast<int>(it - jc * ncb) * 32 + lane;
+  x.j = jc / nch;
+  x.ch = static_cast<int>(jc - x.j * nch);
+  x.off = edge_ptr[x.j];
+  x.n = static_cast<int>(edge_ptr[x.j + 1] - x.off);
+  x.e0 = x.ch * kChunk;
+  x.e1 = min(x.n, x.e0 + kChunk);
+  x.cok = x.c < dg;
+  x.live = x.n >= 2 && x.n > min_n && x.e0 < x.n;
+  return x;
+}
+
+// ---------------------------------------------------------------------------
+// forward
+// ---------------------------------------------------------------------------
+// K1: partial moments of the chunk, and S = -self for its edges
+template <int K, int L>
+__global__ void __launch_bounds__(kW * 32, 3)
+fwd_moments_kernel(const int64_t* __restrict__ edge_ptr, const int32_t* __restrict__ rev,
+                   const float4* __restrict__ geo, int64_t nv, int nch, const float* __restrict__ X,
+                   const float* __restrict__ W, int dg, RbfParams rp, float* __restrict__ S,
+                   float* __restrict__ Mpart, int min_n) {
+  using SM = WarpSmem<K, L>;
+  constexpr int J = L * L;
+  extern __shared__ __align__(16) float smem[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  float* wsm = smem + warp * SM::fwd_total;
+  const float* Ys = wsm + SM::ys;
+  const float* Rs = wsm + SM::rs;
+  const float* Xs = wsm + SM::xs;
+  const int ncb = (dg + 31) / 32;
+  const int64_t items = nv * nch * ncb;
+  for (int64_t it = static_cast<int64_t>(blockIdx.x) * kW + warp; it < items;
+       it += static_cast<int64_t>(gridDim.x) * kW) {
+    const Item q = decode(it, nch, ncb, edge_ptr, dg, min_n, lane);
+    if (!q.live) {
+      if (q.n == 1 && q.ch == 0 && q.n > min_n && q.cok) S[q.off * dg + q.c] = 0.f;
+      continue;
+    }
+    float wp[K][L];
+    load_wprime<K, L>(wp, W, dg, q.c, q.cok);
+    float M[J];
+#pragma unroll
+    for (int i = 0; i < J; ++i) M[i] = 0.f;
+    for (int t0 = q.e0; t0 < q.e1; t0 += kTile) {
+      __syncwarp();
+      stage_tile<K, L>(wsm, geo, rev, q.off, t0, q.e1, rp, lane, X, nullptr, dg, q.c, q.cok);
+      const int nt = min(kTile, q.e1 - t0);
+#pragma unroll 1
+      for (int t = 0; t < nt; ++t) {
+        const float x = Xs[t * 32 + lane];
+        float rb[K], r[L], y[J];
+        load_rb<K>(Rs + t * 8, rb);
+        rprime<K, L>(rb, wp, r);
+        load_y<J>(Ys + t * kYS, y);
+        float self = 0.f;
+#pragma unroll
+        for (int jj = 0; jj < L; ++jj) {
+          r[jj] *= x;  // Q'_j
+          self = fmaf(self_w<L>(jj), r[jj], self);
+        }
+#pragma unroll
+        for (int i = 0; i < J; ++i) M[i] = fmaf(y[i], r[jof<L>(i)], M[i]);
+        if (q.cok) S[(q.off + t0 + t) * dg + q.c] = -self;
+      }
+    }
+    if (q.cok) {
+      float* dst = Mpart + ((q.j * nch + q.ch) * J) * static_cast<int64_t>(dg) + q.c;
+#pragma unroll
+      for (int i = 0; i < J; ++i) dst[static_cast<int64_t>(i) * dg] = M[i];
+    }
+  }
+}
+
+// moments of centre j for this lane's channel: the fixed-order sum of its chunks' partials
+template <int J>
+__device__ __forceinline__ void gather_moments(const float* __restrict__ Mpart, int64_t j, int nch, int nchunks,
+                                               int dg, int c, float (&M)[J]) {
+#pragma unroll
+  for (int i = 0; i < J; ++i) M[i] = 0.f;
+  for (int ch = 0; ch < nchunks; ++ch) {
+    const float* src = Mpart + ((j * nch + ch) * J) * static_cast<int64_t>(dg) + c;
+#pragma unroll
+    for (int i = 0; i < J; ++i) M[i] += __ldg(src + static_cast<int64_t>(i) * dg);
+  }
+}
+
+// K2: S = -self + sum_jm Y_jm(u_p) M[jm] for the chunk's edges
+template <int K, int L>
+__global__ void __launch_bounds__(kW * 32, 3)
+fwd_apply_kernel(const int64_t* __restrict__ edge_ptr, const int32_t* __restrict__ rev,
+                 const float4* __restrict__ geo, int64_t nv, int nch, int dg, RbfParams rp, float* __restrict__ S,
+                 const float* __restrict__ Mpart, int min_n) {
+  using SM = WarpSmem<K, L>;
+  constexpr int J = L * L;
+  extern __shared__ __align__(16) float smem[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  float* wsm = smem + warp * SM::fwd_total;
+  const float* Ys = wsm + SM::ys;
+  const float* Ss = wsm + SM::sbs;
+  const int ncb = (dg + 31) / 32;
+  const int64_t items = nv * nch * ncb;
+  for (int64_t it = static_cast<int64_t>(blockIdx.x) * kW + warp; it < items;
+       it += static_cast<int64_t>(gridDim.x) * kW) {
+    const Item q = decode(it, nch, ncb, edge_ptr, dg, min_n, lane);
+    if (!q.live) continue;
+    float M[J];
+    gather_moments<J>(Mpart, q.j, nch, (q.n + kChunk - 1) / kChunk, dg, q.cok ? q.c : 0, M);
+    for (int t0 = q.e0; t0 < q.e1; t0 += kTile) {
+      __syncwarp();
+      stage_tile<K, L>(wsm, geo, rev, q.off, t0, q.e1, rp, lane, nullptr, S, dg, q.c, q.cok);
+      const int nt = min(kTile, q.e1 - t0);
+#pragma unroll 1
+      for (int t = 0; t < nt; ++t) {
+        float y[J];
+        load_y<J>(Ys + t * kYS, y);
+        float a = Ss[t * 32 + lane];
+#pragma unroll
+        for (int i = 0; i < J; ++i) a = fmaf(y[i], M[i], a);
+        if (q.cok) S[(q.off + t0 + t) * dg + q.c] = a;
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// backward
+// ---------------------------------------------------------------------------
+// Sum of v over the 32 lanes for 16 values at once (reduce-scatter butterfly, 16 shuffles):
+// afterwards lane pairs (lane, lane ^ 1) hold the total of value index idx16(lane).
+__device__ __forceinline__ float reduce16(float (&v)[16], int lane) {
+  float a[8];
+  {
+    const bool hi = lane & 16;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const float send = hi ? v[i] : v[i + 8];
+      const float keep = hi ? v[i + 8] : v[i];
+      a[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+    }
+  }
+  float b[4];
+  {
+    const bool hi = lane & 8;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float send = hi ? a[i] : a[i + 4];
+      const float keep = hi ? a[i + 4] : a[i];
+      b[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+    }
+  }
+  float cc[2];
+  {
+    const bool hi = lane & 4;
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const float send = hi ? b[i] : b[i + 2];
+      const float keep = hi ? b[i + 2] : b[i];
+      cc[i] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+    }
+  }
+  float d;
+  {
+    const bool hi = lane & 2;
+    const float send = hi ? cc[0] : cc[1];
+    const float keep = hi ? cc[1] : cc[0];
+    d = keep + __shfl_xor_sync(0xffffffffu, send, 2);
+  }
+  return d + __shfl_xor_sync(0xffffffffu, d, 1);
+}
+__device__ __forceinline__ int idx16(int lane) {
+  return ((lane & 16) ? 8 : 0) + ((lane & 8) ? 4 : 0) + ((lane & 4) ? 2 : 0) + ((lane & 2) ? 1 : 0);
+}
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// K1: partial moments M (forward) and Mbar = sum_p Y(u_p) S_bar[p] of the chunk
+template <int K, int L>
+__global__ void __launch_bounds__(kW * 32, 3)
+bwd_moments_kernel(const int64_t* __restrict__ edge_ptr, const int32_t* __restrict__ rev,
+                   const float4* __restrict__ geo, int64_t nv, int nch, const float* __restrict__ X,
+                   const float* __restrict__ W, int dg, RbfParams rp, const float* __restrict__ Sbar,
+                   float* __restrict__ Mpart, float* __restrict__ Mbpart, int min_n) {
+  using SM = WarpSmem<K, L>;
+  constexpr int J = L * L;
+  extern __shared__ __align__(16) float smem[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  float* wsm = smem + warp * SM::fwd_total;
+  const float* Ys = wsm + SM::ys;
+  const float* Rs = wsm + SM::rs;
+  const float* Xs = wsm + SM::xs;
+  const float* Sbs = wsm + SM::sbs;
+  const int ncb = (dg + 31) / 32;
+  const int64_t items = nv * nch * ncb;
+  for (int64_t it = static_cast<int64_t>(blockIdx.x) * kW + warp; it < items;
+       it += static_cast<int64_t>(gridDim.x) * kW) {
+    const Item q = decode(it, nch, ncb, edge_ptr, dg, min_n, lane);
+    if (!q.live) continue;
+    const int64_t base = ((q.j * nch + q.ch) * J) * static_cast<int64_t>(dg) + q.c;
+    {
+      float wp[K][L];
+      load_wprime<K, L>(wp, W, dg, q.c, q.cok);
+      float M[J];
+#pragma unroll
+      for (int i = 0; i < J; ++i) M[i] = 0.f;
+      for (int t0 = q.e0; t0 < q.e1; t0 += kTile) {
+        __syncwarp();
+        // a single-tile chunk stages S_bar too and keeps the tile for the Mbar sweep
+        stage_tile<K, L>(wsm, geo, rev, q.off, t0, q.e1, rp, lane, X, q.e1 - q.e0 > kTile ? nullptr : Sbar, dg, q.c,
+                         q.cok);
+        const int nt = min(kTile, q.e1 - t0);
+#pragma unroll 1
+        for (int t = 0; t < nt; ++t) {
+          const float x = Xs[t * 32 + lane];
+          float rb[K], r[L], y[J];
+          load_rb<K>(Rs + t * 8, rb);
+          rprime<K, L>(rb, wp, r);
+          load_y<J>(Ys + t * kYS, y);
+#pragma unroll
+          for (int jj = 0; jj < L; ++jj) r[jj] *= x;
+#pragma unroll
+          for (int i = 0; i < J; ++i) M[i] = fmaf(y[i], r[jof<L>(i)], M[i]);
+        }
+      }
+      if (q.cok) {
+#pragma unroll
+        for (int i = 0; i < J; ++i) Mpart[base + static_cast<int64_t>(i) * dg] = M[i];
+      }
+    }
+    float Mb[J];
+#pragma unroll
+    for (int i = 0; i < J; ++i) Mb[i] = 0.f;
+    for (int t0 = q.e0; t0 < q.e1; t0 += kTile) {
+      if (q.e1 - q.e0 > kTile) {  // else the tile is still staged
+        __syncwarp();
+        stage_tile<K, L>(wsm, geo, rev, q.off, t0, q.e1, rp, lane, nullptr, Sbar, dg, q.c, q.cok);
+      }
+      const int nt = min(kTile, q.e1 - t0);
+#pragma unroll 1
+      for (int t = 0; t < nt; ++t) {
+        const float sb = Sbs[t * 32 + lane];
+        float y[J];
+        load_y<J>(Ys + t * kYS, y);
+#pragma unroll
+        for (int i = 0; i < J; ++i) Mb[i] = fmaf(y[i], sb, Mb[i]);
+      }
+    }
+    if (q.cok) {
+#pragma unroll
+      for (int i = 0; i < J; ++i) Mbpart[base + static_cast<int64_t>(i) * dg] = Mb[i];
+    }
+  }
+}
+
+// K2 per chunk, one pass per tile: M -> shared (lane columns), Mbar -> registers; per edge
+//   Q'bar -> X_bar, W'_bar (flushed per tile into this warp's partial), dE/dd,
+//   g_c = sum_jm grad Y_jm(u_e) (S_bar[e, c] M[jm, c] + Mbar[jm, c] Q'[e, j, c])
+// and (g, dE/dd) summed over the 32 channel lanes with one 4-value butterfly (6 shuffles).
+// Persistent warps with a fixed channel block (W'_bar partial per warp).
+constexpr int kBT = 8;  // backward tile: 8 edges (shared memory for 3 CTAs per SM)
+constexpr int kGS = 148;  // grad-Y row: 147 floats, 16-byte aligned
+template <int K, int L>
+struct BwdSmem {
+  static constexpr int J = L * L;
+  static constexpr int ys = 0;                  // Y [kBT][kYS]
+  static constexpr int gs = ys + kBT * kYS;     // grad Y [kBT][kGS]
+  static constexpr int rs = gs + kBT * kGS;     // rbf [kBT][8]
+  static constexpr int us = rs + kBT * 8;       // (u, d) [kBT]
+  static constexpr int rq = us + 4 * kBT;       // rev [kBT]
+  static constexpr int xs = rq + kBT;           // X tile [kBT][32]
+  static constexpr int sbs = xs + kBT * 32;     // S_bar tile [kBT][32]
+  static constexpr int ms = sbs + kBT * 32;     // M [J][32]
+  static constexpr int total = ms + J * 32;
+};
+
+template <int K, int L>
+__global__ void __launch_bounds__(kW * 32, 3)
+bwd_apply_kernel(const int64_t* __restrict__ edge_ptr, const int32_t* __restrict__ rev,
+                 const float4* __restrict__ geo, int64_t nv, int64_t ne, int nch, const float* __restrict__ X,
+                 const float* __restrict__ W, int dg, RbfParams rp, const float* __restrict__ Sbar,
+                 const float* __restrict__ Mpart, const float* __restrict__ Mbpart, float* __restrict__ Xbar,
+                 float* __restrict__ wbar_part, float4* __restrict__ eg_part, float4* __restrict__ edge_grad,
+                 int min_n) {
+  using SM = BwdSmem<K, L>;
+  constexpr int J = L * L;
+  extern __shared__ __align__(16) float smem[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  float* wsm = smem + warp * SM::total;
+  const float* Ys = wsm + SM::ys;
+  const float* Gs = wsm + SM::gs;
+  const float* Rs = wsm + SM::rs;
+  const float4* Us = reinterpret_cast<const float4*>(wsm + SM::us);
+  const int32_t* Rq = reinterpret_cast<const int32_t*>(wsm + SM::rq);
+  const float* Xs = wsm + SM::xs;
+  const float* Sbs = wsm + SM::sbs;
+  float* Ms = wsm + SM::ms;
+  const int ncb = (dg + 31) / 32;
+  const int64_t gw = static_cast<int64_t>(blockIdx.x) * kW + warp;
+  const int64_t nw = static_cast<int64_t>(gridDim.x) * kW;  // multiple of ncb (host)
+  const int cb = static_cast<int>(gw % ncb);
+  float* wpart = wbar_part + gw * (K * L * 32) + lane;
+#pragma unroll
+  for (int i = 0; i < K * L; ++i) wpart[i * 32] = 0.f;
+  for (int64_t jc = gw / ncb; jc < nv * nch; jc += nw / ncb) {
+    const Item q = decode(jc * ncb + cb, nch, ncb, edge_ptr, dg, min_n, lane);
+    if (!q.live) {
+      if (q.n == 1 && q.ch == 0 && q.n > min_n && q.cok) Xbar[static_cast<int64_t>(rev[q.off]) * dg + q.c] = 0.f;
+      continue;
+    }
+    const int nchunks = (q.n + kChunk - 1) / kChunk;
+    {
+      float M[J];
+      gather_moments<J>(Mpart, q.j, nch, nchunks, dg, q.cok ? q.c : 0, M);
+      __syncwarp();
+#pragma unroll
+      for (int i = 0; i < J; ++i) Ms[i * 32 + lane] = M[i];
+    }
+    float Mb[J];
+    gather_moments<J>(Mbpart, q.j, nch, nchunks, dg, q.cok ? q.c : 0, Mb);
+    float wp[K][L];
+    load_wprime<K, L>(wp, W, dg, q.c, q.cok);
+    for (int t0 = q.e0; t0 < q.e1; t0 += kBT) {
+      __syncwarp();
+      // stage: Y, grad Y, rbf, (u, d), rev; X and S_bar tiles
+      {
+        const int e = t0 + lane;
+        int32_t rq = 0;
+        if (lane < kBT && e < q.e1) {
+          const float4 g = geo[q.off + e];
+          rq = rev[q.off + e];
+          reinterpret_cast<float4*>(wsm + SM::us)[lane] = g;
+          reinterpret_cast<int32_t*>(wsm + SM::rq)[lane] = rq;
+          sh_eval<L>(g.x, g.y, g.z, wsm + SM::ys + lane * kYS, 1);
+          sh_grad_table<L>(g.x, g.y, g.z, wsm + SM::gs + lane * kGS);
+#pragma unroll
+          for (int k = 0; k < 8; ++k) wsm[SM::rs + lane * 8 + k] = k < K ? rbf1(g.w, k, rp) : 0.f;
+        }
+        const int nt = min(kBT, q.e1 - t0);
+        float xv[kBT], sv[kBT];
+#pragma unroll
+        for (int t = 0; t < kBT; ++t) {
+          const int64_t r = __shfl_sync(0xffffffffu, rq, t);
+          xv[t] = (t < nt && q.cok) ? __ldg(X + r * dg + q.c) : 0.f;
+          sv[t] = (t < nt && q.cok) ? __ldg(Sbar + (q.off + t0 + t) * dg + q.c) : 0.f;
+        }
+#pragma unroll
+        for (int t = 0; t < kBT; ++t) {
+          wsm[SM::xs + t * 32 + lane] = xv[t];
+          wsm[SM::sbs + t * 32 + lane] = sv[t];
+        }
+        __syncwarp();
+      }
+      const int nt = min(kBT, q.e1 - t0);
+      float wpb[K][L];
+#pragma unroll
+      for (int k = 0; k < K; ++k)
+#pragma unroll
+        for (int jj = 0; jj < L; ++jj) wpb[k][jj] = 0.f;
+#pragma unroll 1
+      for (int t = 0; t < nt; ++t) {
+        const int64_t rq = Rq[t];
+        const float sb = Sbs[t * 32 + lane];
+        const float x = Xs[t * 32 + lane];
+        const float d = Us[t].w;
+        float rb[K], drb[K], r[L], qb[L];
+        load_rb<K>(Rs + t * 8, rb);
+#pragma unroll
+        for (int k = 0; k < K; ++k) drb[k] = -2.f * rp.gamma * (d - rp.step * k) * rb[k];
+        rprime<K, L>(rb, wp, r);
+#pragma unroll
+        for (int jj = 0; jj < L; ++jj) qb[jj] = -self_w<L>(jj) * sb;
+        const float* yrow = Ys + t * kYS;
+#pragma unroll
+        for (int i = 0; i < J; i += 4) {
+          const float4 v = *reinterpret_cast<const float4*>(yrow + i);
+          const float yy[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (i + u < J) qb[jof<L>(i + u)] = fmaf(yy[u], Mb[i + u], qb[jof<L>(i + u)]);
+        }
+        float xb = 0.f, dd = 0.f;
+#pragma unroll
+        for (int jj = 0; jj < L; ++jj) {
+          xb = fmaf(qb[jj], r[jj], xb);
+          const float rbar = qb[jj] * x;
+          float sdr = 0.f;
+#pragma unroll
+          for (int k = 0; k < K; ++k) {
+            wpb[k][jj] = fmaf(rb[k], rbar, wpb[k][jj]);
+            sdr = fmaf(drb[k], wp[k][jj], sdr);
+          }
+          dd = fmaf(rbar, sdr, dd);
+          r[jj] *= x;  // Q'_j
+        }
+        if (q.cok) Xbar[rq * dg + q.c] = xb;
+        // g_c = sum_jm grad Y_jm (sb M[jm] + Mbar[jm] Q'_j)
+        float gx = 0.f, gy = 0.f, gz = 0.f;
+        const float* grow = Gs + t * kGS;
+#pragma unroll
+        for (int i = 0; i < J; i += 4) {
+          // 4 harmonics = 12 gradient components = 3 float4 loads
+          const float4 a = *reinterpret_cast<const float4*>(grow + 3 * i);
+          const float4 b = *reinterpret_cast<const float4*>(grow + 3 * i + 4);
+          const float4 cc = *reinterpret_cast<const float4*>(grow + 3 * i + 8);
+          const float gv[12] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w, cc.x, cc.y, cc.z, cc.w};
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int jm = i + u;
+            if (jm < J) {
+              const float pv = fmaf(sb, Ms[jm * 32 + lane], Mb[jm] * r[jof<L>(jm < J ? jm : 0)]);
+              gx = fmaf(gv[3 * u], pv, gx);
+              gy = fmaf(gv[3 * u + 1], pv, gy);
+              gz = fmaf(gv[3 * u + 2], pv, gz);
+            }
+          }
+        }
+        // (gx, gy, gz, dd) summed over the lanes: halve twice, then a 3-step butterfly
+        {
+          const bool h16 = lane & 16;
+          const float s0 = h16 ? gx : gz, s1 = h16 ? gy : dd;
+          const float k0 = h16 ? gz : gx, k1 = h16 ? dd : gy;
+          const float a0 = k0 + __shfl_xor_sync(0xffffffffu, s0, 16);
+          const float a1 = k1 + __shfl_xor_sync(0xffffffffu, s1, 16);
+          const bool h8 = lane & 8;
+          float v = (h8 ? a1 : a0) + __shfl_xor_sync(0xffffffffu, h8 ? a0 : a1, 8);
+          v += __shfl_xor_sync(0xffffffffu, v, 4);
+          v += __shfl_xor_sync(0xffffffffu, v, 2);
+          v += __shfl_xor_sync(0xffffffffu, v, 1);
+          // lane (h16, h8) holds component 2 h16 + h8 of (gx, gy, gz, dd)
+          if ((lane & 7) == 0) wsm[SM::xs + t * 32 + ((lane >> 3) & 3)] = v;  // X tile row t is consumed
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < K; ++k)
+#pragma unroll
+        for (int jj = 0; jj < L; ++jj) wpart[(k * L + jj) * 32] += wpb[k][jj];
+      __syncwarp();
+      if (lane < nt) {
+        const float4 u = Us[lane];
+        const float* gr = wsm + SM::xs + lane * 32;
+        const float gxx = gr[0], gyy = gr[1], gzz = gr[2], ddd = gr[3];
+        const float gu = gxx * u.x + gyy * u.y + gzz * u.z;
+        const float inv = 1.f / u.w;
+        const float4 add = make_float4((gxx - gu * u.x) * inv, (gyy - gu * u.y) * inv, (gzz - gu * u.z) * inv, ddd);
+        const int64_t e = q.off + t0 + lane;
+        if (eg_part) {
+          eg_part[static_cast<int64_t>(cb) * ne + e] = add;
+        } else {
+          float4 gg = edge_grad[e];
+          gg.x += add.x;
+          gg.y += add.y;
+          gg.z += add.z;
+          gg.w += add.w;
+          edge_grad[e] = gg;
+        }
+      }
+    }
+  }
+}
+
+// W_bar[k, l, c] = sum_j A[l][j] sum_{warps w of block cb} W'_bar_w[k, j, c]: one CTA per (k, cb),
+// 32 warps split the warp partials (strided), then a fixed-order combine: deterministic.
+template <int K, int L>
+__global__ void __launch_bounds__(1024) reduce_wbar_kernel(const float* __restrict__ part, int64_t nw, int ncb, int dg,
+                                                            float* __restrict__ out, int accumulate) {
+  __shared__ float red[32][L][33];
+  const int k = blockIdx.x / ncb, cb = blockIdx.x - (blockIdx.x / ncb) * ncb;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  float acc[L];
+#pragma unroll
+  for (int jj = 0; jj < L; ++jj) acc[jj] = 0.f;
+  for (int64_t w = cb + static_cast<int64_t>(wid) * ncb; w < nw; w += static_cast<int64_t>(32) * ncb) {
+    const float* src = part + w * (K * L * 32) + (k * L) * 32 + lane;
+#pragma unroll
+    for (int jj = 0; jj < L; ++jj) acc[jj] += __ldg(src + jj * 32);
+  }
+#pragma unroll
+  for (int jj = 0; jj < L; ++jj) red[wid][jj][lane] = acc[jj];
+  __syncthreads();
+  if (wid == 0) {
+    float wpb[L];
+#pragma unroll
+    for (int jj = 0; jj < L; ++jj) {
+      float t = 0.f;
+      for (int u = 0; u < 32; ++u) t += red[u][jj][lane];
+      wpb[jj] = t;
+    }
+    const int c = cb * 32 + lane;
+    if (c < dg) {
+#pragma unroll
+      for (int l = 0; l < L; ++l) {
+        float s = 0.f;
+#pragma unroll
+        for (int jj = 0; jj <= l && jj < L; ++jj)
+          if (((l - jj) & 1) == 0) s = fmaf(wpb[jj], c_tab.A[l][jj], s);
+        float* o = out + (static_cast<int64_t>(k) * L + l) * dg + c;
+        *o = accumulate ? *o + s : s;
+      }
+    }
+  }
+}
+
+// edge_grad[e] += sum over channel blocks (fixed order) for the centres handled here
+__global__ void add_eg_kernel(const int64_t* __restrict__ edge_ptr, int64_t nv, const float4* __restrict__ part,
+                              int ncb, int64_t ne, int min_n, float4* __restrict__ edge_grad) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nv; v += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e0 = edge_ptr[v], e1 = edge_ptr[v + 1];
+    if (e1 - e0 < 2 || e1 - e0 <= min_n) continue;
+    for (int64_t e = e0; e < e1; ++e) {
+      float4 g = edge_grad[e];
+      for (int b = 0; b < ncb; ++b) {
+        const float4 p = part[b * ne + e];
+        g.x += p.x;
+        g.y += p.y;
+        g.z += p.z;
+        g.w += p.w;
+      }
+      edge_grad[e] = g;
+    }
+  }
+}
+
+}  // namespace sh
+
+// ---------------------------------------------------------------------------
+// host side (called from triplet.cu's ABI functions)
+// ---------------------------------------------------------------------------
+bool sh_supported(int K, int L, int dg) { return K == 6 && L == 7 && dg >= 1; }
+
+static int sh_nch(int max_degree) { return std::max(1, (std::max(max_degree, 1) + sh::kChunk - 1) / sh::kChunk); }
+
+static int sh_grid(int64_t items) {
+  return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((items + sh::kW - 1) / sh::kW, kNumSMs * 24)));
+}
+
+int64_t sh_fwd_workspace_bytes(int64_t nv, int max_degree, int K, int L, int dg) {
+  return std::max<int64_t>(nv, 1) * sh_nch(max_degree) * L * L * static_cast<int64_t>(dg) * 4;
+}
+
+template <typename F>
+static void set_smem(F kern, size_t smem, bool& configured) {
+  if (!configured) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    configured = true;
+  }
+}
+
+int sh_fwd(const int64_t* edge_ptr, const int32_t* rev, const float4* geo, int64_t nv, int max_degree, const float* X,
+           const float* W, int K, int L, int dg, RbfParams rp, float* S, void* ws, int min_n, cudaStream_t st) {
+  using SM = sh::WarpSmem<6, 7>;
+  const int nch = sh_nch(max_degree);
+  const int ncb = (dg + 31) / 32;
+  const size_t smem = sizeof(float) * SM::fwd_total * sh::kW;
+  float* Mpart = reinterpret_cast<float*>(ws);
+  static bool c1 = false, c2 = false;
+  auto k1 = sh::fwd_moments_kernel<6, 7>;
+  auto k2 = sh::fwd_apply_kernel<6, 7>;
+  set_smem(k1, smem, c1);
+  set_smem(k2, smem, c2);
+  const int grid = sh_grid(nv * nch * ncb);
+  k1<<<grid, sh::kW * 32, smem, st>>>(edge_ptr, rev, geo, nv, nch, X, W, dg, rp, S, Mpart, min_n);
+  if (check_launch("triplet_fwd_sh_moments")) return 1;
+  k2<<<grid, sh::kW * 32, smem, st>>>(edge_ptr, rev, geo, nv, nch, dg, rp, S, Mpart, min_n);
+  return check_launch("triplet_fwd_sh_apply");
+}
+
+static int64_t sh_bwd_warps(int64_t nv, int nch, int dg, int* grid_out) {
+  const int ncb = (dg + 31) / 32;
+  // persistent warps: up to ~12 per SM, a multiple of ncb and of the CTA width
+  int64_t want = std::min<int64_t>(nv * nch * ncb, static_cast<int64_t>(kNumSMs) * 12);
+  const int64_t unit = static_cast<int64_t>(ncb) * sh::kW / std::__gcd(ncb, sh::kW);
+  want = std::max<int64_t>(unit, (want + unit - 1) / unit * unit);
+  *grid_out = static_cast<int>(want / sh::kW);
+  return want;
+}
+
+int64_t sh_bwd_workspace_bytes(int64_t nv, int64_t ne, int max_degree, int K, int L, int dg) {
+  int grid;
+  const int nch = sh_nch(max_degree);
+  const int64_t nw = sh_bwd_warps(std::max<int64_t>(nv, 1), nch, dg, &grid);
+  const int ncb = (dg + 31) / 32;
+  return nw * K * L * 32 * 4 + 2 * sh_fwd_workspace_bytes(nv, max_degree, K, L, dg) +
+         (ncb > 1 ? static_cast<int64_t>(ncb) * std::max<int64_t>(ne, 1) * 16 : 0) + 256;
+}
+
+int sh_bwd(const int64_t* edge_ptr, const int32_t* rev, const float4* geo, int64_t nv, int64_t ne, int max_degree,
+           const float* X, const float* W, int K, int L, int dg, RbfParams rp, const float* Sbar, float* Xbar,
+           float* Wbar, float4* edge_grad, void* ws, int min_n, int accumulate, cudaStream_t st) {
+  using SM = sh::WarpSmem<6, 7>;
+  const int nch = sh_nch(max_degree);
+  int grid;
+  const int64_t nw = sh_bwd_warps(std::max<int64_t>(nv, 1), nch, dg, &grid);
+  const int ncb = (dg + 31) / 32;
+  float* wpart = reinterpret_cast<float*>(ws);
+  float* Mpart = wpart + nw * K * L * 32;
+  float* Mbpart = Mpart + sh_fwd_workspace_bytes(nv, max_degree, K, L, dg) / 4;
+  float4* egp = nullptr;
+  if (ncb > 1) {
+    const uintptr_t p = reinterpret_cast<uintptr_t>(Mbpart + sh_fwd_workspace_bytes(nv, max_degree, K, L, dg) / 4);
+    egp = reinterpret_cast<float4*>((p + 15) & ~static_cast<uintptr_t>(15));
+  }
+  static bool c1 = false, c2 = false;
+  auto k1 = sh::bwd_moments_kernel<6, 7>;
+  auto k2 = sh::bwd_apply_kernel<6, 7>;
+  const size_t smem1 = sizeof(float) * SM::fwd_total * sh::kW;
+  const size_t smem2 = sizeof(float) * sh::BwdSmem<6, 7>::total * sh::kW;
+  set_smem(k1, smem1, c1);
+  set_smem(k2, smem2, c2);
+  k1<<<sh_grid(nv * nch * ncb), sh::kW * 32, smem1, st>>>(edge_ptr, rev, geo, nv, nch, X, W, dg, rp, Sbar, Mpart,
+                                                         Mbpart, min_n);
+  if (check_launch("triplet_bwd_sh_moments")) return 1;
+  k2<<<grid, sh::kW * 32, smem2, st>>>(edge_ptr, rev, geo, nv, ne, nch, X, W, dg, rp, Sbar, Mpart, Mbpart, Xbar,
+                                       wpart, egp, edge_grad, min_n);
+  if (check_launch("triplet_bwd_sh_apply")) return 1;
+  sh::reduce_wbar_kernel<6, 7><<<K * ncb, 1024, 0, st>>>(wpart, nw, ncb, dg, Wbar, accumulate);
+  if (check_launch("triplet_bwd_sh_reduce")) return 1;
+  if (ncb == 1) return 0;
+  sh::add_eg_kernel<<<grid_for(nv, 128), 128, 0, st>>>(edge_ptr, nv, egp, ncb, ne, min_n, edge_grad);
+  return check_launch("triplet_bwd_sh_eg");
+}
+
+}  // namespace egn

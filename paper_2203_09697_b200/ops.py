@@ -244,8 +244,11 @@ def triplet_fwd(edge_ptr, rev, geo, X, Wk, cutoff, max_degree=-1):
                                       cutoff, max_degree)
         return S
     S = torch.empty_like(X)
-    call("egn_triplet_fwd", ptr(edge_ptr), ptr(rev), ptr(geo), edge_ptr.shape[0] - 1, int(max_degree), ptr(X),
-         ptr(Wk), k, l, dg, float(cutoff), ptr(S), stream())
+    nv = edge_ptr.shape[0] - 1
+    nbytes = call("egn_triplet_fwd_workspace_bytes", nv, int(max_degree), k, l, dg)
+    ws = _workspace_named("tfwd", nbytes, X.device) if nbytes > 0 else None
+    call("egn_triplet_fwd", ptr(edge_ptr), ptr(rev), ptr(geo), nv, int(max_degree), ptr(X),
+         ptr(Wk), k, l, dg, float(cutoff), ptr(S), ptr(ws), stream())
     return S
 
 
@@ -292,7 +295,7 @@ def triplet_bwd(edge_ptr, rev, geo, X, Wk, cutoff, S_bar, edge_grad, X_bar=None,
             W_bar[:, :, c0:c1] = wb
         return X_bar, W_bar
     ne = X.shape[0]
-    nbytes = call("egn_triplet_bwd_workspace_bytes", nv, ne, k, l, dg)
+    nbytes = call("egn_triplet_bwd_workspace_bytes", nv, ne, int(max_degree), k, l, dg)
     ws = _workspace(nbytes, X.device)
     call("egn_triplet_bwd", ptr(edge_ptr), ptr(rev), ptr(geo), nv, ne, int(max_degree), ptr(X), ptr(Wk), k, l, dg,
          float(cutoff), ptr(S_bar), ptr(X_bar), ptr(W_bar), ptr(edge_grad), ptr(ws), stream())
@@ -330,7 +333,7 @@ def triplet_bwd_window(edge_ptr, rev, geo, X, Wk, cutoff, first_lo, last_hi, S_b
             X_bar[:, c0:c1] += xb
         return W_bar
     nv, ne = edge_ptr.shape[0] - 1, X.shape[0]
-    nbytes = call("egn_triplet_bwd_workspace_bytes", nv, ne, k, l, dg)
+    nbytes = call("egn_triplet_bwd_workspace_bytes", nv, ne, int(max_degree), k, l, dg)
     ws = _workspace(nbytes, X.device)
     call("egn_triplet_bwd_window", ptr(edge_ptr), ptr(rev), ptr(geo), nv, int(first_lo), int(last_hi),
          int(max_degree), ptr(_c(X, torch.float32)), ptr(_c(Wk, torch.float32)), k, l, dg, float(cutoff),

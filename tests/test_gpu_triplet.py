@@ -88,8 +88,26 @@ CASES = [
 ]
 
 
+@pytest.fixture(params=["auto", "sh", "pairwise"])
+def triplet_path(request):
+    """Every kernel test on each path: auto (pairwise centre tiles up to deg 64, the
+    spherical-harmonic factorised kernels above), spherical-harmonic kernels for every
+    centre, pairwise only (tensor-core kernels above deg 64)."""
+    from paper_2203_09697_b200 import _lib
+
+    old = _lib.call("egn_triplet_path", {"auto": 0, "sh": 1, "pairwise": 2}[request.param])
+    yield request.param
+    _lib.call("egn_triplet_path", old)
+
+
+CASES += [
+    (120, 0.8, 6.0, 6, 7, 64),   # near-complete graph, degree ~ 119: four 32-edge tiles per centre
+    (200, 0.6, 6.0, 6, 7, 96),   # channel blocks 32 + 32 + 32
+]
+
+
 @pytest.mark.parametrize("case", CASES)
-def test_triplet_fwd_bwd_matches_reference(case):
+def test_triplet_fwd_bwd_matches_reference(case, triplet_path):
     n, rho, cutoff, K, L, dg = case
     pos, _ = O.random_cloud(n, rho, np.random.default_rng(n + dg))
     (S, Sr), (Xb, Xbr), (Wb, Wbr), (pb, pbr), g = _run(pos, cutoff, K, L, dg)
@@ -168,7 +186,7 @@ def test_triplet_dimension_errors():
         X3, W3 = torch.zeros((bg.num_edges, 300), device="cuda"), torch.zeros((6, 4, 300), device="cuda")
         S3 = torch.empty_like(X3)
         call("egn_triplet_fwd", ptr(bg.edge_ptr), ptr(bg.rev), ptr(bg.geo), bg.num_nodes, -1, ptr(X3), ptr(W3), 6, 4,
-             300, 1.5, ptr(S3), stream())
+             300, 1.5, ptr(S3), None, stream())
     # ... and ops.triplet_fwd chunks wider embeddings exactly (per-channel independence)
     X3 = torch.randn((bg.num_edges, 300), device="cuda")
     W3 = torch.randn((6, 4, 300), device="cuda")

@@ -100,10 +100,10 @@ def test_native_library_loads_and_exports_all_symbols():
     lib = _lib.lib()
     for name in _lib.header_symbols():
         assert hasattr(lib, name), name
-    assert lib.egn_abi_version() == 2
+    assert lib.egn_abi_version() == 3
     assert isinstance(lib.egn_last_error(), bytes)
     # pure host entry point: workspace sizing
-    assert lib.egn_triplet_bwd_workspace_bytes(1000, 20000, 6, 7, 64) > 0
+    assert lib.egn_triplet_bwd_workspace_bytes(1000, 20000, 40, 6, 7, 64) > 0
 
 
 def test_product_path_does_not_import_oracle():

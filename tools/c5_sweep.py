@@ -56,10 +56,12 @@ def main():
     ap.add_argument("--atoms", type=int, default=1000)
     ap.add_argument("--iters", type=int, default=5)
     ap.add_argument("--out", default=None)
+    ap.add_argument("--path", default="auto", choices=["auto", "sh", "pairwise"],
+                    help="triplet kernels: auto (pairwise <= deg 64, spherical-harmonic above), sh, pairwise")
     args = ap.parse_args()
     import torch.distributed as dist
 
-    from paper_2203_09697_b200 import ops
+    from paper_2203_09697_b200 import _lib, ops
     from paper_2203_09697_b200.graph import build_batch
     from paper_2203_09697_b200.partition import partition_centers
 
@@ -72,6 +74,7 @@ def main():
     hbm = peaks["hbm_gbs"] * 1e9
     fp32 = 148 * 128 * 2 * 1.965e9
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
+    _lib.call("egn_triplet_path", {"auto": 0, "sh": 1, "pairwise": 2}[args.path])
     cutoff, K, L = 6.0, 6, 7
     rows = []
     for deg in [int(x) for x in args.degrees.split(",")]:
@@ -107,8 +110,12 @@ def main():
             b_f = 12 * nt + (8 * dg + 4) * ne
             b_b = 16 * nt + (12 * dg + 8) * ne
             flops = 2.0 * nt * L * dg
-            row = {"target_deg": deg, "mean_deg": ne / args.atoms, "max_deg": md, "edges": ne, "triplets": nt,
-                   "dg": dg, "gpus": world, "fwd_us": t_f * 1e6, "bwd_us": t_b * 1e6,
+            # bytes the implicit-triplet kernels must move: X rows gathered + S written (+ geometry)
+            b_impl_f = (8 * dg + 20) * ne
+            b_impl_b = (16 * dg + 36) * ne  # S_bar, X read; X_bar written; geometry, edge_grad
+            row = {"path": args.path, "target_deg": deg, "mean_deg": ne / args.atoms, "max_deg": md, "edges": ne,
+                   "triplets": nt, "dg": dg, "gpus": world, "fwd_us": t_f * 1e6, "bwd_us": t_b * 1e6,
+                   "fwd_hbm_frac_implicit": b_impl_f / t_f / hbm, "bwd_hbm_frac_implicit": b_impl_b / t_b / hbm,
                    "fwd_gtrip_s": nt / t_f / 1e9, "bwd_gtrip_s": nt / t_b / 1e9,
                    "fwd_fp32_frac": flops / t_f / fp32, "bwd_fp32_frac": 2 * flops / t_b / fp32,
                    "fwd_hbm_frac": b_f / t_f / hbm, "bwd_hbm_frac": b_b / t_b / hbm}
