@@ -168,6 +168,25 @@ int egn_triplet_fwd(const int64_t* edge_ptr, const int32_t* rev, const float* ge
                     int64_t num_nodes, int max_degree, const float* X, const float* W, int k_rbf,
                     int l_sbf, int dg, double cutoff, float* S, void* workspace, egn_stream_t stream);
 
+/* DimeNet++ / GemNet bases (no reference counterpart): basis 0 = the
+ * reference's Gaussian rbf x cos(l angle) (= egn_triplet_fwd / _bwd), 1 = GemNet CBF (radial
+ * Bessel basis e_k(d_kj) x Y_l0(angle)), 2 = DimeNet SBF (sqrt(2/c^3) / |j_{l+1}(z_lk)|
+ * u(d_kj/c) j_l(z_lk d_kj / c) x Y_l0(angle)); the radial Bessel basis is
+ * e_k(d) = sqrt(2/c) u(d/c) sin((k+1) pi d/c) with the polynomial envelope u (p = 6).  Bases 1
+ * and 2 run the spherical-harmonic kernels (k_rbf = 6, l_sbf = 7) and need max_degree and the
+ * workspace of egn_triplet_fwd_basis_workspace_bytes / egn_triplet_bwd_workspace_bytes. */
+int64_t egn_triplet_fwd_basis_workspace_bytes(int64_t num_nodes, int max_degree, int k_rbf, int l_sbf, int dg);
+int egn_triplet_fwd_basis(const int64_t* edge_ptr, const int32_t* rev, const float* geo, int64_t num_nodes,
+                          int max_degree, const float* X, const float* W, int k_rbf, int l_sbf, int dg, double cutoff,
+                          int basis, float* S, void* workspace, egn_stream_t stream);
+int egn_triplet_bwd_basis(const int64_t* edge_ptr, const int32_t* rev, const float* geo, int64_t num_nodes,
+                          int64_t num_edges, int max_degree, const float* X, const float* W, int k_rbf, int l_sbf,
+                          int dg, double cutoff, int basis, const float* S_bar, float* X_bar, float* W_bar,
+                          float* edge_grad, void* workspace, egn_stream_t stream);
+/* Edge radial Bessel basis [E, K] of the packed geometry and its adjoint (edge_grad.w +=). */
+int egn_rbf_bessel(const float* geo, int64_t num_edges, int k_rbf, double cutoff, float* rbf, egn_stream_t stream);
+int egn_rbf_bessel_bwd(const float* geo, const float* rbf_bar, int64_t num_edges, int k_rbf, double cutoff,
+                       float* edge_grad, egn_stream_t stream);
 /* Triplet kernel selection (returns the previous mode; -1 queries): 0 = auto (deg <= 64:
  * pairwise centre tiles; larger centres: linear-in-degree spherical-harmonic kernels, the
  * angular sum factorised by the addition theorem -- triplet_sh.cu), 1 = spherical-harmonic

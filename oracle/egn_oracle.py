@@ -50,6 +50,10 @@ class Config:
     l_sbf: int = 4
     cutoff: float = 1.5
     seed: int = 0
+    # "gaussian": the reference's surrogate bases (egn/basis.py); "bessel": the DimeNet++ / GemNet
+    # bases (no reference counterpart -- restated below from the published
+    # definitions with scipy.special, independent of the CUDA kernels)
+    basis: str = "gaussian"
 
 
 def param_specs(c: Config) -> list[tuple[str, tuple[int, ...], int]]:
@@ -440,6 +444,140 @@ def sbf_partials(d_in, ang, k, l, cutoff):
 
 
 # ---------------------------------------------------------------------------
+# DimeNet++ / GemNet bases.  No reference counterpart: restated from the
+# published definitions (DimeNet, Klicpera et al. 2020, eqs. 7-8 and the polynomial envelope;
+# GemNet, Gasteiger et al. 2021, the radial Bessel basis and the circular basis Y_l0), with
+# scipy.special for the spherical Bessel functions and Legendre polynomials.  Parity unpinned
+# (no reference output exists); checked by finite differences (tests/test_oracle.py).
+# ---------------------------------------------------------------------------
+ENVELOPE_P = 6  # DimeNet's envelope exponent 5 -> p = exponent + 1
+
+
+def envelope(x, p: int = ENVELOPE_P):
+    """u(x) = 1/x + a x^(p-1) + b x^p + c x^(p+1) on (0, 1), 0 beyond (DimeNet Envelope)."""
+    a, b, c = -(p + 1) * (p + 2) / 2.0, p * (p + 2.0), -p * (p + 1) / 2.0
+    x = np.asarray(x, dtype=np.float64)
+    u = 1.0 / x + a * x ** (p - 1) + b * x ** p + c * x ** (p + 1)
+    return np.where(x < 1.0, u, 0.0)
+
+
+def envelope_dx(x, p: int = ENVELOPE_P):
+    a, b, c = -(p + 1) * (p + 2) / 2.0, p * (p + 2.0), -p * (p + 1) / 2.0
+    x = np.asarray(x, dtype=np.float64)
+    du = -1.0 / x ** 2 + a * (p - 1) * x ** (p - 2) + b * p * x ** (p - 1) + c * (p + 1) * x ** p
+    return np.where(x < 1.0, du, 0.0)
+
+
+def bessel_rbf(d, k: int, cutoff: float):
+    """e_n(d) = sqrt(2/c) u(d/c) sin(n pi d/c), n = 1..k (GemNet / DimeNet radial basis)."""
+    d = np.asarray(d, dtype=np.float64)
+    if d.size and (np.any(d <= 0.0) or np.any(d > cutoff)):
+        raise ValueError("distances must lie in (0, cutoff]")
+    x = d[:, None] / cutoff
+    n = np.arange(1, k + 1, dtype=np.float64)[None, :]
+    return np.sqrt(2.0 / cutoff) * envelope(x) * np.sin(n * np.pi * x)
+
+
+def bessel_rbf_ddist(d, k: int, cutoff: float):
+    x = np.asarray(d, dtype=np.float64)[:, None] / cutoff
+    n = np.arange(1, k + 1, dtype=np.float64)[None, :]
+    return np.sqrt(2.0 / cutoff) * (envelope_dx(x) * np.sin(n * np.pi * x)
+                                     + envelope(x) * n * np.pi * np.cos(n * np.pi * x)) / cutoff
+
+
+def spherical_bessel_zeros(l_max: int, k: int) -> np.ndarray:
+    """z[l, n]: the first k positive zeros of j_l, l < l_max (scipy, bracket + brentq)."""
+    from scipy.optimize import brentq
+    from scipy.special import spherical_jn
+
+    z = np.zeros((l_max, k))
+    xs = np.linspace(0.1, 20.0 + 4.0 * (k + l_max), 40000)
+    for l in range(l_max):
+        f = spherical_jn(l, xs)
+        roots = []
+        for i in range(xs.size - 1):
+            if f[i] * f[i + 1] < 0:
+                roots.append(brentq(lambda t: spherical_jn(l, t), xs[i], xs[i + 1], xtol=1e-15))
+                if len(roots) == k:
+                    break
+        z[l] = roots
+    return z
+
+
+def _y_l0(ang, l_max):
+    """Y_l0(angle) = sqrt((2l+1)/(4 pi)) P_l(cos angle) and its derivative w.r.t. the angle."""
+    from scipy.special import eval_legendre
+
+    x = np.cos(np.asarray(ang, dtype=np.float64))
+    s = np.sin(np.asarray(ang, dtype=np.float64))
+    out = np.zeros((x.size, l_max))
+    dout = np.zeros((x.size, l_max))
+    for l in range(l_max):
+        nrm = np.sqrt((2 * l + 1) / (4 * np.pi))
+        out[:, l] = nrm * eval_legendre(l, x)
+        # P_l'(x) = l (x P_l - P_{l-1}) / (x^2 - 1);  d/dangle = -sin(angle) P_l'(cos angle)
+        dp = np.polynomial.legendre.legval(x, np.polynomial.legendre.legder(np.eye(l_max)[l]))
+        dout[:, l] = -nrm * s * dp
+    return out, dout
+
+
+def _sbf_bessel_parts(d_in, ang, k, l, cutoff, variant):
+    """Radial [n, k, l] and its d-derivative, angular [n, l] and its angle derivative."""
+    from scipy.special import spherical_jn
+
+    d = np.asarray(d_in, dtype=np.float64)
+    if d.size and (np.any(d <= 0.0) or np.any(d > cutoff)):
+        raise ValueError("distances must lie in (0, cutoff]")
+    ang_v, ang_d = _y_l0(ang, l)
+    if variant == GEMNET:  # GemNet: radial Bessel basis of d_kj times the circular basis Y_l0
+        rad = np.repeat(bessel_rbf(d, k, cutoff)[:, :, None], l, axis=2)
+        drad = np.repeat(bessel_rbf_ddist(d, k, cutoff)[:, :, None], l, axis=2)
+        return rad, drad, ang_v, ang_d
+    # DimeNet: sqrt(2/c^3) / |j_{l+1}(z_ln)| u(d/c) j_l(z_ln d/c)
+    z = spherical_bessel_zeros(l, k)  # [l, k]
+    x = d[:, None, None] / cutoff
+    zz = z.T[None, :, :]  # [1, k, l]
+    orders = np.arange(l)[None, None, :]
+    norm = np.sqrt(2.0 / cutoff ** 3) / np.abs(spherical_jn(orders + 1, zz))
+    j = spherical_jn(orders, zz * x)
+    dj = spherical_jn(orders, zz * x, derivative=True) * zz / cutoff
+    u, du = envelope(x), envelope_dx(x) / cutoff
+    return norm * u * j, norm * (du * j + u * dj), ang_v, ang_d
+
+
+def sbf_bessel(d_in, ang, k, l, cutoff, variant):
+    """(t, k*L + l) = radial_{k,l}(d_kj) * Y_l0(angle)."""
+    rad, _, ang_v, _ = _sbf_bessel_parts(d_in, ang, k, l, cutoff, variant)
+    return (rad * ang_v[:, None, :]).reshape(ang_v.shape[0], k * l)
+
+
+def sbf_bessel_partials(d_in, ang, k, l, cutoff, variant):
+    rad, drad, ang_v, ang_d = _sbf_bessel_parts(d_in, ang, k, l, cutoff, variant)
+    n = ang_v.shape[0]
+    return (drad * ang_v[:, None, :]).reshape(n, k * l), (rad * ang_d[:, None, :]).reshape(n, k * l)
+
+
+def edge_basis(c, d):
+    return bessel_rbf(d, c.k_rbf, c.cutoff) if c.basis == "bessel" else rbf(d, c.k_rbf, c.cutoff)
+
+
+def edge_basis_ddist(c, d):
+    return bessel_rbf_ddist(d, c.k_rbf, c.cutoff) if c.basis == "bessel" else rbf_ddist(d, c.k_rbf, c.cutoff)
+
+
+def triplet_basis(c, d_in, ang):
+    if c.basis == "bessel":
+        return sbf_bessel(d_in, ang, c.k_rbf, c.l_sbf, c.cutoff, c.variant)
+    return sbf(d_in, ang, c.k_rbf, c.l_sbf, c.cutoff)
+
+
+def triplet_basis_partials(c, d_in, ang):
+    if c.basis == "bessel":
+        return sbf_bessel_partials(d_in, ang, c.k_rbf, c.l_sbf, c.cutoff, c.variant)
+    return sbf_partials(d_in, ang, c.k_rbf, c.l_sbf, c.cutoff)
+
+
+# ---------------------------------------------------------------------------
 # primitives (tape.py:27-154)
 # ---------------------------------------------------------------------------
 
@@ -527,8 +665,8 @@ def forward(c: Config, P: dict, pos: np.ndarray, z: np.ndarray, graph: Graph | N
     g = graph if graph is not None else build_graph(pos, c.cutoff)
     n_e, n_v = g.src.size, g.n
     gem = c.variant == GEMNET
-    R = rbf(g.dist, c.k_rbf, c.cutoff) if n_e else np.zeros((0, c.k_rbf))
-    S = sbf(g.dist[g.trip_in], g.angles, c.k_rbf, c.l_sbf, c.cutoff) if g.trip_in.size else np.zeros((0, c.k_rbf * c.l_sbf))
+    R = edge_basis(c, g.dist) if n_e else np.zeros((0, c.k_rbf))
+    S = triplet_basis(c, g.dist[g.trip_in], g.angles) if g.trip_in.size else np.zeros((0, c.k_rbf * c.l_sbf))
     sel, seg = receiver_plan(g.recv, n_v)
 
     m = R @ P["edge_init.w"].T + P["edge_init.b"]
@@ -689,7 +827,7 @@ def backward(fw: Forward, P: dict, d_energy: float = 1.0, d_forces: np.ndarray |
     pos_bar = np.zeros_like(pos)
     if n_t:
         d_in = g.dist[g.trip_in]
-        dd, da = sbf_partials(d_in, g.angles, c.k_rbf, c.l_sbf, c.cutoff)
+        dd, da = triplet_basis_partials(c, d_in, g.angles)
         np.add.at(dist_bar, g.trip_in, (S_bar * dd).sum(axis=1))
         ang_bar = (S_bar * da).sum(axis=1)
         g_k, g_j, g_i = angle_gradients(pos, g.src, g.recv, g.trip_in, g.trip_out, g.vec, g.rev)
@@ -702,7 +840,7 @@ def backward(fw: Forward, P: dict, d_energy: float = 1.0, d_forces: np.ndarray |
         np.add.at(buf, j, ang_bar[:, None] * g_j)
         pos_bar = pos_bar + buf
     if n_e:
-        dist_bar += (R_bar * rbf_ddist(g.dist, c.k_rbf, c.cutoff)).sum(axis=1)
+        dist_bar += (R_bar * edge_basis_ddist(c, g.dist)).sum(axis=1)
         if gem:
             diff = g.vec if g.vec is not None else pos[g.recv] - pos[g.src]
             unit = diff / g.dist[:, None]

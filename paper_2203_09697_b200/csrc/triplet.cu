@@ -559,11 +559,13 @@ constexpr int kFastMaxDeg = 64;
 bool sh_supported(int K, int L, int dg);
 int64_t sh_fwd_workspace_bytes(int64_t nv, int max_degree, int K, int L, int dg);
 int sh_fwd(const int64_t* edge_ptr, const int32_t* rev, const float4* geo, int64_t nv, int max_degree, const float* X,
-           const float* W, int K, int L, int dg, RbfParams rp, float* S, void* ws, int min_n, cudaStream_t st);
+           const float* W, int K, int L, int dg, RbfParams rp, float cutoff, int mode, float* S, void* ws, int min_n,
+           cudaStream_t st);
 int64_t sh_bwd_workspace_bytes(int64_t nv, int64_t ne, int max_degree, int K, int L, int dg);
 int sh_bwd(const int64_t* edge_ptr, const int32_t* rev, const float4* geo, int64_t nv, int64_t ne, int max_degree,
-           const float* X, const float* W, int K, int L, int dg, RbfParams rp, const float* Sbar, float* Xbar,
-           float* Wbar, float4* edge_grad, void* ws, int min_n, int accumulate, cudaStream_t st);
+           const float* X, const float* W, int K, int L, int dg, RbfParams rp, float cutoff, int mode,
+           const float* Sbar, float* Xbar, float* Wbar, float4* edge_grad, void* ws, int min_n, int accumulate,
+           cudaStream_t st);
 
 // Path selection (egn_triplet_path): 0 = auto (deg <= 64: pairwise centre tiles; larger centres:
 // the linear-in-degree spherical-harmonic kernels), 1 = spherical-harmonic kernels for every
@@ -696,6 +698,11 @@ static int check_dims(int K, int L, int dg) {
 
 extern "C" {
 
+int64_t egn_triplet_fwd_basis_workspace_bytes(int64_t num_nodes, int max_degree, int k_rbf, int l_sbf, int dg) {
+  return sh_supported(k_rbf, l_sbf, dg) && max_degree >= 0 ? sh_fwd_workspace_bytes(num_nodes, max_degree, k_rbf, l_sbf, dg)
+                                                           : 0;
+}
+
 int64_t egn_triplet_fwd_workspace_bytes(int64_t num_nodes, int max_degree, int k_rbf, int l_sbf, int dg) {
   // only the spherical-harmonic path needs one (its per-chunk moments)
   const bool fast_covers = g_triplet_path == 0 && fast_supported(k_rbf, l_sbf, dg) && max_degree <= kFastMaxDeg;
@@ -725,7 +732,8 @@ int egn_triplet_fwd(const int64_t* edge_ptr, const int32_t* rev, const float* ge
     min_n = kFastMaxDeg;
   }
   if (use_sh)
-    return sh_fwd(edge_ptr, rev, g4, num_nodes, max_degree, X, W, k_rbf, l_sbf, dg, rp, S, workspace, min_n, st);
+    return sh_fwd(edge_ptr, rev, g4, num_nodes, max_degree, X, W, k_rbf, l_sbf, dg, rp, static_cast<float>(cutoff), 0,
+                  S, workspace, min_n, st);
   if (tc_fwd_supported(k_rbf, l_sbf, dg, max_degree))
     return tc_fwd(edge_ptr, rev, g4, num_nodes, max_degree, X, W, k_rbf, l_sbf, dg, rp, S, min_n, st);
 #define EGN_FWD(CW, GC, R) \
@@ -787,8 +795,8 @@ int egn_triplet_bwd(const int64_t* edge_ptr, const int32_t* rev, const float* ge
   if (use_sh) {
     char* sws = reinterpret_cast<char*>(workspace) + generic_ws_bytes(num_nodes, k_rbf, l_sbf, dg) +
                 fast_ws_bytes(num_nodes, num_edges, k_rbf, l_sbf, dg) + tc_bwd_workspace_bytes(num_nodes, k_rbf, l_sbf);
-    return sh_bwd(edge_ptr, rev, g4, num_nodes, num_edges, max_degree, X, W, k_rbf, l_sbf, dg, rp, S_bar, X_bar,
-                  W_bar, eg, sws, min_n, accumulate, st);
+    return sh_bwd(edge_ptr, rev, g4, num_nodes, num_edges, max_degree, X, W, k_rbf, l_sbf, dg, rp,
+                  static_cast<float>(cutoff), 0, S_bar, X_bar, W_bar, eg, sws, min_n, accumulate, st);
   }
   // centres above the small-degree kernel's range: tensor-core backward (triplet_tc_bwd.cu)
   if (tc_bwd_supported(k_rbf, l_sbf, dg, max_degree)) {
@@ -815,6 +823,47 @@ int egn_triplet_path(int mode) {
   const int old = g_triplet_path;
   if (mode >= 0 && mode <= 2) g_triplet_path = mode;
   return old;
+}
+
+// DimeNet++ / GemNet bases: basis 1 = GemNet CBF (radial Bessel basis of
+// d_kj x Y_l0(angle)), 2 = DimeNet SBF (sqrt(2/c^3)/|j_{l+1}(z_ln)| u(d/c) j_l(z_ln d/c) Y_l0(angle));
+// the spherical-harmonic kernels for every centre (their A table absorbs the Y_l0 normalisation)
+int egn_triplet_fwd_basis(const int64_t* edge_ptr, const int32_t* rev, const float* geo, int64_t num_nodes,
+                          int max_degree, const float* X, const float* W, int k_rbf, int l_sbf, int dg, double cutoff,
+                          int basis, float* S, void* workspace, egn_stream_t stream) {
+  if (basis == 0)
+    return egn_triplet_fwd(edge_ptr, rev, geo, num_nodes, max_degree, X, W, k_rbf, l_sbf, dg, cutoff, S, workspace,
+                           stream);
+  if (int rc = check_dims(k_rbf, l_sbf, dg)) return rc;
+  EGN_REQUIRE(basis == 1 || basis == 2, "basis must be 0, 1 or 2");
+  EGN_REQUIRE(sh_supported(k_rbf, l_sbf, dg), "the bessel bases need k_rbf = 6, l_sbf = 7");
+  EGN_REQUIRE(max_degree >= 0 && workspace != nullptr, "the bessel bases need max_degree and a workspace");
+  if (num_nodes == 0) return 0;
+  return sh_fwd(edge_ptr, rev, reinterpret_cast<const float4*>(geo), num_nodes, max_degree, X, W, k_rbf, l_sbf, dg,
+                rbf_params(k_rbf, cutoff), static_cast<float>(cutoff), basis, S, workspace, 0, as_stream(stream));
+}
+
+int egn_triplet_bwd_basis(const int64_t* edge_ptr, const int32_t* rev, const float* geo, int64_t num_nodes,
+                          int64_t num_edges, int max_degree, const float* X, const float* W, int k_rbf, int l_sbf,
+                          int dg, double cutoff, int basis, const float* S_bar, float* X_bar, float* W_bar,
+                          float* edge_grad, void* workspace, egn_stream_t stream) {
+  if (basis == 0)
+    return egn_triplet_bwd(edge_ptr, rev, geo, num_nodes, num_edges, max_degree, X, W, k_rbf, l_sbf, dg, cutoff,
+                           S_bar, X_bar, W_bar, edge_grad, workspace, stream);
+  if (int rc = check_dims(k_rbf, l_sbf, dg)) return rc;
+  EGN_REQUIRE(basis == 1 || basis == 2, "basis must be 0, 1 or 2");
+  EGN_REQUIRE(sh_supported(k_rbf, l_sbf, dg), "the bessel bases need k_rbf = 6, l_sbf = 7");
+  EGN_REQUIRE(max_degree >= 0, "the bessel bases need max_degree");
+  cudaStream_t st = as_stream(stream);
+  if (num_nodes == 0) {
+    cudaMemsetAsync(W_bar, 0, sizeof(float) * k_rbf * l_sbf * dg, st);
+    return check_launch("triplet_bwd_basis_empty");
+  }
+  char* sws = reinterpret_cast<char*>(workspace) + generic_ws_bytes(num_nodes, k_rbf, l_sbf, dg) +
+              fast_ws_bytes(num_nodes, num_edges, k_rbf, l_sbf, dg) + tc_bwd_workspace_bytes(num_nodes, k_rbf, l_sbf);
+  return sh_bwd(edge_ptr, rev, reinterpret_cast<const float4*>(geo), num_nodes, num_edges, max_degree, X, W, k_rbf,
+                l_sbf, dg, rbf_params(k_rbf, cutoff), static_cast<float>(cutoff), basis, S_bar, X_bar, W_bar,
+                reinterpret_cast<float4*>(edge_grad), sws, 0, 0, st);
 }
 
 int egn_triplet_fwd_window(const int64_t* edge_ptr, const int32_t* rev, const float* geo, int64_t num_nodes,

@@ -62,7 +62,8 @@ __host__ __device__ constexpr double csqrt(double x) {
 struct ShTables {
   float norm[8][8];  // orthonormal real-harmonic normalisation (sqrt 2 for m > 0)
   float qmm[8];      // Q_m^m = (2m-1)!!
-  float A[8][8];     // A[l][j] = a_lj 4 pi / (2j+1): W' = W A
+  float A[8][8];     // A[l][j] = a_lj 4 pi / (2j+1): W' = W A (Chebyshev angular basis, MODE 0)
+  float Ad[8];       // sqrt(4 pi / (2j+1)): W' = W diag(Ad) for the Y_l0 angular bases (MODE 1, 2)
   float s[8];        // (2j+1) / (4 pi): the q = p (self) term
 };
 constexpr ShTables make_tables() {
@@ -75,11 +76,145 @@ constexpr ShTables make_tables() {
                                                 (m > 0 ? 1.4142135623730950488 : 1.0));
     t.qmm[j] = static_cast<float>(dfact(2 * j - 1));
     t.s[j] = static_cast<float>((2 * j + 1) / (4 * pi));
+    t.Ad[j] = static_cast<float>(csqrt(4 * pi / (2 * j + 1)));
     for (int l = 0; l < 8; ++l) t.A[l][j] = static_cast<float>(cheb_leg(l, j) * 4 * pi / (2 * j + 1));
   }
   return t;
 }
 __constant__ ShTables c_tab = make_tables();
+
+// DimeNet SBF radial constants: z[l][n] = n-th positive zero of j_l, jinv = 1 / |j_{l+1}(z_ln)|
+// (scipy brentq / spherical_jn; the oracle recomputes them independently)
+struct SbfTables {
+  double z[8][8];
+  double jinv[8][8];
+};
+__constant__ SbfTables c_sbf = {
+    {{3.141592653589793, 6.283185307179586, 9.42477796076938, 12.566370614359172, 15.707963267948966,
+      18.849555921538762, 21.991148575128555, 25.132741228718345},
+     {4.493409457909064, 7.725251836937707, 10.904121659428899, 14.066193912831473, 17.22075527193077,
+      20.37130295928756, 23.519452498689006, 26.666054258812675},
+     {5.76345919689455, 9.095011330476355, 12.322940970566583, 15.514603010886745, 18.689036355362823,
+      21.853874222709766, 25.01280320228961, 28.167829707993622},
+     {6.98793200050052, 10.417118547379365, 13.69802315324925, 16.92362128521384, 20.12180617445382,
+      23.304246988939653, 26.476763664539124, 29.64260454031581},
+     {8.182561452571242, 11.70490715457039, 15.03966470761652, 18.30125595954199, 21.525417733399944,
+      24.727565547835034, 27.91557619942136, 31.093933214079307},
+     {9.355812111042747, 12.966530172774345, 16.354709639350464, 19.653152101821185, 22.904550647903722,
+      26.1277501372255, 29.332562578584827, 32.52466128857884},
+     {10.512835408093999, 14.20739245884246, 17.647974870165896, 20.98346306894477, 24.26276804239701,
+      27.507868364904258, 30.730380731646648, 33.9371083026413},
+     {11.657032192516372, 15.431289210268378, 18.922999198546144, 22.29534801913077, 25.602855953810646,
+      28.87037334704266, 32.1111962396826, 35.33319418271646}},
+    {{3.141592653589793, 6.283185307179586, 9.42477796076938, 12.566370614359172, 15.707963267948966,
+      18.849555921538762, 21.99114857512856, 25.132741228718345},
+     {4.6033388487517, 7.789705767492723, 10.949879869826262, 14.10169533046921, 17.249765567558637,
+      20.395832521843232, 23.540701897736362, 26.684798101802116},
+     {6.040563197807522, 9.264342010446368, 12.446450951060557, 15.612184250673817, 18.76981212423012,
+      21.92283428496274, 25.072987642052208, 28.221232674395463},
+     {7.473091442496642, 10.721480766798642, 13.924153665362708, 17.10464317933209, 20.273125026195952,
+      23.4344095314491, 26.591044813337703, 29.74450383351637},
+     {8.908348935043326, 12.168747439919386, 15.388960028983778, 18.583685450027534, 21.763327322052017,
+      24.933462345803836, 28.097246277145015, 31.256583482961755},
+     {10.349655802515409, 13.610632122380693, 16.844809840109313, 20.05257889487107, 23.243116533114033,
+      26.422236707117232, 29.593479081880883, 32.759076284270435},
+     {11.798613629858298, 15.049969257269414, 18.294429523463386, 21.51371922159807, 24.714553484382066,
+      27.902501464341643, 31.081267919249978, 34.25330499504689},
+     {13.256000990958375, 16.488637691421197, 19.739775744045733, 22.968911668054954, 26.17924648704294,
+      29.375674765038404, 32.5618617752044, 35.74037246851164}}};
+
+// spherical Bessel j_l(x) (fp64): ascending series for x <= l + 1 (upward recurrence loses
+// digits there), upward recurrence from j_0, j_1 above
+__device__ __forceinline__ double sph_jl(int l, double x) {
+  if (x <= l + 1.0) {
+    double term = 1.0;
+    for (int i = 1; i <= l; ++i) term *= x / (2 * i + 1);
+    double sum = term;
+    const double h = -0.5 * x * x;
+    for (int k = 1; k < 40; ++k) {
+      term *= h / (k * (2.0 * l + 2.0 * k + 1.0));
+      sum += term;
+      if (fabs(term) < 1e-17 * fabs(sum)) break;
+    }
+    return sum;
+  }
+  double sn, cs;
+  sincos(x, &sn, &cs);
+  const double j0 = sn / x;
+  if (l == 0) return j0;
+  double jm = j0, jc = sn / (x * x) - cs / x;
+  for (int i = 1; i < l; ++i) {
+    const double jn = (2 * i + 1) / x * jc - jm;
+    jm = jc;
+    jc = jn;
+  }
+  return jc;
+}
+
+// DimeNet / GemNet polynomial envelope u(x) = 1/x + a x^(p-1) + b x^p + c x^(p+1), p = 6, and u'
+__device__ __forceinline__ void envelope6(double x, double& u, double& du) {
+  constexpr double a = -28.0, b = 48.0, c = -21.0;  // -(p+1)(p+2)/2, p(p+2), -p(p+1)/2
+  if (x >= 1.0) {
+    u = du = 0.0;
+    return;
+  }
+  const double x2 = x * x, x4 = x2 * x2, x5 = x4 * x, x6 = x5 * x;
+  u = 1.0 / x + a * x5 + b * x6 + c * x6 * x;
+  du = -1.0 / x2 + 5.0 * a * x4 + 6.0 * b * x5 + 7.0 * c * x6;
+}
+
+// Radial table of one edge (distance d) for the basis MODE, row layout radv<MODE> below:
+//   MODE 0: Gaussian rbf_k(d) (the reference's surrogate, egn/basis.py:35-42); derivative on the fly
+//   MODE 1: GemNet / DimeNet radial Bessel basis sqrt(2/c) u(d/c) sin(n pi d/c), n = k + 1, and d/dd
+//   MODE 2: DimeNet SBF radial sqrt(2/c^3) / |j_{l+1}(z_ln)| u(d/c) j_l(z_ln d/c) [k][l], and d/dd
+template <int K, int L, int MODE>
+__device__ __forceinline__ void radial_row(float d, float cutoff, RbfParams rp, float* row, float* drow) {
+  if constexpr (MODE == 0) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const float dd = d - rp.step * k;
+      row[k] = k < K ? __expf(-rp.gamma * dd * dd) : 0.f;
+    }
+  } else if constexpr (MODE == 1) {
+    const double c = cutoff, x = d / c, nrm = sqrt(2.0 / c);
+    double u, du;
+    envelope6(x, u, du);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      if (k < K) {
+        double sn, cs;
+        sincospi((k + 1) * x, &sn, &cs);
+        row[k] = static_cast<float>(nrm * u * sn);
+        if (drow) drow[k] = static_cast<float>(nrm * (du * sn + u * (k + 1) * 3.14159265358979323846 * cs) / c);
+      } else {
+        row[k] = 0.f;
+        if (drow) drow[k] = 0.f;
+      }
+    }
+  } else {
+    const double c = cutoff, x = d / c, nrm = sqrt(2.0 / (c * c * c));
+    double u, du;
+    envelope6(x, u, du);
+    for (int l = 0; l < L; ++l) {
+      for (int k = 0; k < K; ++k) {
+        const double z = c_sbf.z[l][k], zx = z * x;
+        const double j = sph_jl(l, zx);
+        // j_l'(t) = j_{l-1}(t) - (l + 1) j_l(t) / t ; j_0' = -j_1
+        const double dj = l == 0 ? -sph_jl(1, zx) : sph_jl(l - 1, zx) - (l + 1) * j / zx;
+        const double f = nrm * c_sbf.jinv[l][k];
+        row[k * L + l] = static_cast<float>(f * u * j);
+        if (drow) drow[k * L + l] = static_cast<float>(f * (du * j + u * dj * z) / c);
+      }
+    }
+  }
+}
+template <int MODE>
+constexpr int rad_stride() { return MODE == 2 ? 44 : 8; }
+template <int K, int L, int MODE>
+__device__ __forceinline__ float radv(const float* row, int k, int j) {
+  if constexpr (MODE == 2) return row[k * L + j];
+  return row[k];
+}
 
 // Y_jm(u) for j < L at index j*j + j + m (m in [-j, j]), written with stride `st`.
 // Recurrences: C_m + i S_m = (x + i y)^m; Q_j^m(z) = associated Legendre without (1-z^2)^(m/2).
@@ -239,8 +374,8 @@ __device__ __forceinline__ float rbf1(float d, int k, RbfParams rp) {
   return __expf(-rp.gamma * dd * dd);
 }
 
-// W'[k][j] = sum_l W[k, l, c] A[l][j] for this lane's channel
-template <int K, int L>
+// W'[k][j] = sum_l W[k, l, c] A[l][j] for this lane's channel (MODE 1/2: A = diag(Ad))
+template <int K, int L, int MODE = 0>
 __device__ __forceinline__ void load_wprime(float (&wp)[K][L], const float* __restrict__ W, int dg, int c, bool cok) {
 #pragma unroll
   for (int k = 0; k < K; ++k) {
@@ -249,10 +384,14 @@ __device__ __forceinline__ void load_wprime(float (&wp)[K][L], const float* __re
     for (int l = 0; l < L; ++l) w[l] = cok ? __ldg(W + (k * L + l) * dg + c) : 0.f;
 #pragma unroll
     for (int j = 0; j < L; ++j) {
-      float s = 0.f;
+      if constexpr (MODE == 0) {
+        float s = 0.f;
 #pragma unroll
-      for (int l = j; l < L; l += 2) s = fmaf(w[l], c_tab.A[l][j], s);  // a_lj = 0 unless l >= j, l - j even
-      wp[k][j] = s;
+        for (int l = j; l < L; l += 2) s = fmaf(w[l], c_tab.A[l][j], s);  // a_lj = 0 unless l >= j, l - j even
+        wp[k][j] = s;
+      } else {
+        wp[k][j] = w[j] * c_tab.Ad[j];
+      }
     }
   }
 }
@@ -267,13 +406,13 @@ __device__ __forceinline__ constexpr int jof(int jm) {
 // warp shared-memory carve-up (floats).  The Y tile is edge-major with a 16-byte aligned row
 // (52 floats), so a lane reads four harmonics of one edge with one broadcast LDS.128.
 constexpr int kYS = 52;
-template <int K, int L, int T = kTile>
+template <int K, int L, int T = kTile, int MODE = 0>
 struct WarpSmem {
   static constexpr int J = L * L;
   static_assert(J <= kYS, "L <= 7 for the 52-float Y rows");
   static constexpr int ys = 0;                        // Y tile [T][kYS]
-  static constexpr int rs = ys + T * kYS;             // rbf tile [T][8]
-  static constexpr int us = rs + T * 8;               // float4 (u, d) [T]
+  static constexpr int rs = ys + T * kYS;             // radial tile [T][rad_stride]
+  static constexpr int us = rs + T * rad_stride<MODE>();  // float4 (u, d) [T]
   static constexpr int rq = us + 4 * T;               // int rq [T]
   static constexpr int xs = rq + T;                   // X[rq_t, c] of the tile [T t][32 lanes]
   static constexpr int sbs = xs + T * 32;             // S_bar[e_t, c] of the tile (backward)
@@ -286,12 +425,12 @@ struct WarpSmem {
 // stage the tile [t0, t0 + 32) of the centre's out-edges: Y, rbf, (u, d), rev, and this lane's
 // channel of the gathered X rows (and of S_bar for the backward): all 32 row loads of the tile
 // are issued back to back, so the sweep over the tile never waits on a dependent global load.
-template <int K, int L, int T = kTile>
+template <int K, int L, int T = kTile, int MODE = 0>
 __device__ __forceinline__ void stage_tile(float* wsm, const float4* __restrict__ geo, const int32_t* __restrict__ rev,
-                                           int64_t off, int t0, int n, RbfParams rp, int lane,
+                                           int64_t off, int t0, int n, RbfParams rp, float cutoff, int lane,
                                            const float* __restrict__ X = nullptr, const float* __restrict__ Sbar = nullptr,
-                                           int dg = 0, int c = 0, bool cok = false) {
-  using SM = WarpSmem<K, L, T>;
+                                           int dg = 0, int c = 0, bool cok = false, bool radial = true) {
+  using SM = WarpSmem<K, L, T, MODE>;
   const int e = t0 + lane;
   int32_t rq = 0;
   if (lane < T && e < n) {
@@ -300,8 +439,7 @@ __device__ __forceinline__ void stage_tile(float* wsm, const float4* __restrict_
     reinterpret_cast<float4*>(wsm + SM::us)[lane] = g;
     reinterpret_cast<int32_t*>(wsm + SM::rq)[lane] = rq;
     sh_eval<L>(g.x, g.y, g.z, wsm + SM::ys + lane * kYS, 1);
-#pragma unroll
-    for (int k = 0; k < 8; ++k) wsm[SM::rs + lane * 8 + k] = k < K ? rbf1(g.w, k, rp) : 0.f;
+    if (radial) radial_row<K, L, MODE>(g.w, cutoff, rp, wsm + SM::rs + lane * rad_stride<MODE>(), nullptr);
   }
   const int nt = min(T, n - t0);
   if (X) {
@@ -357,6 +495,24 @@ __device__ __forceinline__ void rprime(const float (&rb)[K], const float (&wp)[K
   }
 }
 
+// R'_j of one staged edge row (any MODE)
+template <int K, int L, int MODE>
+__device__ __forceinline__ void rprime_row(const float* row, const float (&wp)[K][L], float (&r)[L]) {
+  if constexpr (MODE == 2) {
+#pragma unroll
+    for (int jj = 0; jj < L; ++jj) {
+      float s = 0.f;
+#pragma unroll
+      for (int k = 0; k < K; ++k) s = fmaf(row[k * L + jj], wp[k][jj], s);
+      r[jj] = s;
+    }
+  } else {
+    float rb[K];
+    load_rb<K>(row, rb);
+    rprime<K, L>(rb, wp, r);
+  }
+}
+
 template <int L>
 __device__ __forceinline__ float self_w(int j) {
   return c_tab.s[j];
@@ -395,13 +551,14 @@ __device__ __forceinline__ Item decode(int64_t it, int nch, int ncb, const int64
 // forward
 // ---------------------------------------------------------------------------
 // K1: partial moments of the chunk, and S = -self for its edges
-template <int K, int L>
+template <int K, int L, int MODE>
 __global__ void __launch_bounds__(kW * 32, 3)
 fwd_moments_kernel(const int64_t* __restrict__ edge_ptr, const int32_t* __restrict__ rev,
                    const float4* __restrict__ geo, int64_t nv, int nch, const float* __restrict__ X,
-                   const float* __restrict__ W, int dg, RbfParams rp, float* __restrict__ S,
+                   const float* __restrict__ W, int dg, RbfParams rp, float cutoff, float* __restrict__ S,
                    float* __restrict__ Mpart, int min_n) {
-  using SM = WarpSmem<K, L>;
+  using SM = WarpSmem<K, L, kTile, MODE>;
+  constexpr int RS = rad_stride<MODE>();
   constexpr int J = L * L;
   extern __shared__ __align__(16) float smem[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -419,20 +576,19 @@ fwd_moments_kernel(const int64_t* __restrict__ edge_ptr, const int32_t* __restri
       continue;
     }
     float wp[K][L];
-    load_wprime<K, L>(wp, W, dg, q.c, q.cok);
+    load_wprime<K, L, MODE>(wp, W, dg, q.c, q.cok);
     float M[J];
 #pragma unroll
     for (int i = 0; i < J; ++i) M[i] = 0.f;
     for (int t0 = q.e0; t0 < q.e1; t0 += kTile) {
       __syncwarp();
-      stage_tile<K, L>(wsm, geo, rev, q.off, t0, q.e1, rp, lane, X, nullptr, dg, q.c, q.cok);
+      stage_tile<K, L, kTile, MODE>(wsm, geo, rev, q.off, t0, q.e1, rp, cutoff, lane, X, nullptr, dg, q.c, q.cok);
       const int nt = min(kTile, q.e1 - t0);
 #pragma unroll 1
       for (int t = 0; t < nt; ++t) {
         const float x = Xs[t * 32 + lane];
-        float rb[K], r[L], y[J];
-        load_rb<K>(Rs + t * 8, rb);
-        rprime<K, L>(rb, wp, r);
+        float r[L], y[J];
+        rprime_row<K, L, MODE>(Rs + t * RS, wp, r);
         load_y<J>(Ys + t * kYS, y);
         float self = 0.f;
 #pragma unroll
@@ -467,12 +623,12 @@ __device__ __forceinline__ void gather_moments(const float* __restrict__ Mpart, 
 }
 
 // K2: S = -self + sum_jm Y_jm(u_p) M[jm] for the chunk's edges
-template <int K, int L>
+template <int K, int L, int MODE>
 __global__ void __launch_bounds__(kW * 32, 3)
 fwd_apply_kernel(const int64_t* __restrict__ edge_ptr, const int32_t* __restrict__ rev,
                  const float4* __restrict__ geo, int64_t nv, int nch, int dg, RbfParams rp, float* __restrict__ S,
                  const float* __restrict__ Mpart, int min_n) {
-  using SM = WarpSmem<K, L>;
+  using SM = WarpSmem<K, L, kTile, MODE>;
   constexpr int J = L * L;
   extern __shared__ __align__(16) float smem[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -489,7 +645,8 @@ fwd_apply_kernel(const int64_t* __restrict__ edge_ptr, const int32_t* __restrict
     gather_moments<J>(Mpart, q.j, nch, (q.n + kChunk - 1) / kChunk, dg, q.cok ? q.c : 0, M);
     for (int t0 = q.e0; t0 < q.e1; t0 += kTile) {
       __syncwarp();
-      stage_tile<K, L>(wsm, geo, rev, q.off, t0, q.e1, rp, lane, nullptr, S, dg, q.c, q.cok);
+      stage_tile<K, L, kTile, MODE>(wsm, geo, rev, q.off, t0, q.e1, rp, 0.f, lane, nullptr, S, dg, q.c, q.cok,
+                                    false);
       const int nt = min(kTile, q.e1 - t0);
 #pragma unroll 1
       for (int t = 0; t < nt; ++t) {
@@ -559,13 +716,14 @@ __device__ __forceinline__ float warp_sum(float v) {
 }
 
 // K1: partial moments M (forward) and Mbar = sum_p Y(u_p) S_bar[p] of the chunk
-template <int K, int L>
+template <int K, int L, int MODE>
 __global__ void __launch_bounds__(kW * 32, 3)
 bwd_moments_kernel(const int64_t* __restrict__ edge_ptr, const int32_t* __restrict__ rev,
                    const float4* __restrict__ geo, int64_t nv, int nch, const float* __restrict__ X,
-                   const float* __restrict__ W, int dg, RbfParams rp, const float* __restrict__ Sbar,
+                   const float* __restrict__ W, int dg, RbfParams rp, float cutoff, const float* __restrict__ Sbar,
                    float* __restrict__ Mpart, float* __restrict__ Mbpart, int min_n) {
-  using SM = WarpSmem<K, L>;
+  using SM = WarpSmem<K, L, kTile, MODE>;
+  constexpr int RS = rad_stride<MODE>();
   constexpr int J = L * L;
   extern __shared__ __align__(16) float smem[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -583,22 +741,21 @@ bwd_moments_kernel(const int64_t* __restrict__ edge_ptr, const int32_t* __restri
     const int64_t base = ((q.j * nch + q.ch) * J) * static_cast<int64_t>(dg) + q.c;
     {
       float wp[K][L];
-      load_wprime<K, L>(wp, W, dg, q.c, q.cok);
+      load_wprime<K, L, MODE>(wp, W, dg, q.c, q.cok);
       float M[J];
 #pragma unroll
       for (int i = 0; i < J; ++i) M[i] = 0.f;
       for (int t0 = q.e0; t0 < q.e1; t0 += kTile) {
         __syncwarp();
         // a single-tile chunk stages S_bar too and keeps the tile for the Mbar sweep
-        stage_tile<K, L>(wsm, geo, rev, q.off, t0, q.e1, rp, lane, X, q.e1 - q.e0 > kTile ? nullptr : Sbar, dg, q.c,
-                         q.cok);
+        stage_tile<K, L, kTile, MODE>(wsm, geo, rev, q.off, t0, q.e1, rp, cutoff, lane, X,
+                                      q.e1 - q.e0 > kTile ? nullptr : Sbar, dg, q.c, q.cok);
         const int nt = min(kTile, q.e1 - t0);
 #pragma unroll 1
         for (int t = 0; t < nt; ++t) {
           const float x = Xs[t * 32 + lane];
-          float rb[K], r[L], y[J];
-          load_rb<K>(Rs + t * 8, rb);
-          rprime<K, L>(rb, wp, r);
+          float r[L], y[J];
+          rprime_row<K, L, MODE>(Rs + t * RS, wp, r);
           load_y<J>(Ys + t * kYS, y);
 #pragma unroll
           for (int jj = 0; jj < L; ++jj) r[jj] *= x;
@@ -617,7 +774,8 @@ bwd_moments_kernel(const int64_t* __restrict__ edge_ptr, const int32_t* __restri
     for (int t0 = q.e0; t0 < q.e1; t0 += kTile) {
       if (q.e1 - q.e0 > kTile) {  // else the tile is still staged
         __syncwarp();
-        stage_tile<K, L>(wsm, geo, rev, q.off, t0, q.e1, rp, lane, nullptr, Sbar, dg, q.c, q.cok);
+        stage_tile<K, L, kTile, MODE>(wsm, geo, rev, q.off, t0, q.e1, rp, cutoff, lane, nullptr, Sbar, dg, q.c, q.cok,
+                                      false);
       }
       const int nt = min(kTile, q.e1 - t0);
 #pragma unroll 1
@@ -643,13 +801,15 @@ bwd_moments_kernel(const int64_t* __restrict__ edge_ptr, const int32_t* __restri
 // Persistent warps with a fixed channel block (W'_bar partial per warp).
 constexpr int kBT = 8;  // backward tile: 8 edges (shared memory for 3 CTAs per SM)
 constexpr int kGS = 148;  // grad-Y row: 147 floats, 16-byte aligned
-template <int K, int L>
+template <int K, int L, int MODE = 0>
 struct BwdSmem {
   static constexpr int J = L * L;
+  static constexpr int RS = rad_stride<MODE>();
   static constexpr int ys = 0;                  // Y [kBT][kYS]
   static constexpr int gs = ys + kBT * kYS;     // grad Y [kBT][kGS]
-  static constexpr int rs = gs + kBT * kGS;     // rbf [kBT][8]
-  static constexpr int us = rs + kBT * 8;       // (u, d) [kBT]
+  static constexpr int rs = gs + kBT * kGS;     // radial [kBT][RS]
+  static constexpr int drs = rs + kBT * RS;     // its d-derivative [kBT][RS] (MODE 1, 2)
+  static constexpr int us = drs + (MODE == 0 ? 0 : kBT * RS);  // (u, d) [kBT]
   static constexpr int rq = us + 4 * kBT;       // rev [kBT]
   static constexpr int xs = rq + kBT;           // X tile [kBT][32]
   static constexpr int sbs = xs + kBT * 32;     // S_bar tile [kBT][32]
@@ -657,22 +817,24 @@ struct BwdSmem {
   static constexpr int total = ms + J * 32;
 };
 
-template <int K, int L>
+template <int K, int L, int MODE>
 __global__ void __launch_bounds__(kW * 32, 3)
 bwd_apply_kernel(const int64_t* __restrict__ edge_ptr, const int32_t* __restrict__ rev,
                  const float4* __restrict__ geo, int64_t nv, int64_t ne, int nch, const float* __restrict__ X,
-                 const float* __restrict__ W, int dg, RbfParams rp, const float* __restrict__ Sbar,
+                 const float* __restrict__ W, int dg, RbfParams rp, float cutoff, const float* __restrict__ Sbar,
                  const float* __restrict__ Mpart, const float* __restrict__ Mbpart, float* __restrict__ Xbar,
                  float* __restrict__ wbar_part, float4* __restrict__ eg_part, float4* __restrict__ edge_grad,
                  int min_n) {
-  using SM = BwdSmem<K, L>;
+  using SM = BwdSmem<K, L, MODE>;
   constexpr int J = L * L;
+  constexpr int RS = SM::RS;
   extern __shared__ __align__(16) float smem[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   float* wsm = smem + warp * SM::total;
   const float* Ys = wsm + SM::ys;
   const float* Gs = wsm + SM::gs;
   const float* Rs = wsm + SM::rs;
+  const float* DRs = wsm + SM::drs;
   const float4* Us = reinterpret_cast<const float4*>(wsm + SM::us);
   const int32_t* Rq = reinterpret_cast<const int32_t*>(wsm + SM::rq);
   const float* Xs = wsm + SM::xs;
@@ -702,7 +864,7 @@ bwd_apply_kernel(const int64_t* __restrict__ edge_ptr, const int32_t* __restrict
     float Mb[J];
     gather_moments<J>(Mbpart, q.j, nch, nchunks, dg, q.cok ? q.c : 0, Mb);
     float wp[K][L];
-    load_wprime<K, L>(wp, W, dg, q.c, q.cok);
+    load_wprime<K, L, MODE>(wp, W, dg, q.c, q.cok);
     for (int t0 = q.e0; t0 < q.e1; t0 += kBT) {
       __syncwarp();
       // stage: Y, grad Y, rbf, (u, d), rev; X and S_bar tiles
@@ -716,8 +878,8 @@ bwd_apply_kernel(const int64_t* __restrict__ edge_ptr, const int32_t* __restrict
           reinterpret_cast<int32_t*>(wsm + SM::rq)[lane] = rq;
           sh_eval<L>(g.x, g.y, g.z, wsm + SM::ys + lane * kYS, 1);
           sh_grad_table<L>(g.x, g.y, g.z, wsm + SM::gs + lane * kGS);
-#pragma unroll
-          for (int k = 0; k < 8; ++k) wsm[SM::rs + lane * 8 + k] = k < K ? rbf1(g.w, k, rp) : 0.f;
+          radial_row<K, L, MODE>(g.w, cutoff, rp, wsm + SM::rs + lane * RS,
+                                 MODE == 0 ? nullptr : wsm + SM::drs + lane * RS);
         }
         const int nt = min(kBT, q.e1 - t0);
         float xv[kBT], sv[kBT];
@@ -746,11 +908,19 @@ bwd_apply_kernel(const int64_t* __restrict__ edge_ptr, const int32_t* __restrict
         const float sb = Sbs[t * 32 + lane];
         const float x = Xs[t * 32 + lane];
         const float d = Us[t].w;
-        float rb[K], drb[K], r[L], qb[L];
-        load_rb<K>(Rs + t * 8, rb);
+        float r[L], qb[L];
+        const float* rrow = Rs + t * RS;
+        const float* drow = DRs + t * RS;
+        float rb[K], drb[K];  // MODE 0 / 1: radial values of the edge
+        if constexpr (MODE != 2) {
+          load_rb<K>(rrow, rb);
 #pragma unroll
-        for (int k = 0; k < K; ++k) drb[k] = -2.f * rp.gamma * (d - rp.step * k) * rb[k];
-        rprime<K, L>(rb, wp, r);
+          for (int k = 0; k < K; ++k) {
+            if constexpr (MODE == 0) drb[k] = -2.f * rp.gamma * (d - rp.step * k) * rb[k];
+            else drb[k] = drow[k];
+          }
+        }
+        rprime_row<K, L, MODE>(rrow, wp, r);
 #pragma unroll
         for (int jj = 0; jj < L; ++jj) qb[jj] = -self_w<L>(jj) * sb;
         const float* yrow = Ys + t * kYS;
@@ -770,8 +940,10 @@ bwd_apply_kernel(const int64_t* __restrict__ edge_ptr, const int32_t* __restrict
           float sdr = 0.f;
 #pragma unroll
           for (int k = 0; k < K; ++k) {
-            wpb[k][jj] = fmaf(rb[k], rbar, wpb[k][jj]);
-            sdr = fmaf(drb[k], wp[k][jj], sdr);
+            const float rv = MODE == 2 ? rrow[k * L + jj] : rb[k];
+            const float dv = MODE == 2 ? drow[k * L + jj] : drb[k];
+            wpb[k][jj] = fmaf(rv, rbar, wpb[k][jj]);
+            sdr = fmaf(dv, wp[k][jj], sdr);
           }
           dd = fmaf(rbar, sdr, dd);
           r[jj] *= x;  // Q'_j
@@ -844,7 +1016,7 @@ bwd_apply_kernel(const int64_t* __restrict__ edge_ptr, const int32_t* __restrict
 
 // W_bar[k, l, c] = sum_j A[l][j] sum_{warps w of block cb} W'_bar_w[k, j, c]: one CTA per (k, cb),
 // 32 warps split the warp partials (strided), then a fixed-order combine: deterministic.
-template <int K, int L>
+template <int K, int L, int MODE>
 __global__ void __launch_bounds__(1024) reduce_wbar_kernel(const float* __restrict__ part, int64_t nw, int ncb, int dg,
                                                             float* __restrict__ out, int accumulate) {
   __shared__ float red[32][L][33];
@@ -874,9 +1046,13 @@ __global__ void __launch_bounds__(1024) reduce_wbar_kernel(const float* __restri
 #pragma unroll
       for (int l = 0; l < L; ++l) {
         float s = 0.f;
+        if constexpr (MODE == 0) {
 #pragma unroll
-        for (int jj = 0; jj <= l && jj < L; ++jj)
-          if (((l - jj) & 1) == 0) s = fmaf(wpb[jj], c_tab.A[l][jj], s);
+          for (int jj = 0; jj <= l && jj < L; ++jj)
+            if (((l - jj) & 1) == 0) s = fmaf(wpb[jj], c_tab.A[l][jj], s);
+        } else {
+          s = wpb[l] * c_tab.Ad[l];
+        }
         float* o = out + (static_cast<int64_t>(k) * L + l) * dg + c;
         *o = accumulate ? *o + s : s;
       }
@@ -929,23 +1105,33 @@ static void set_smem(F kern, size_t smem, bool& configured) {
   }
 }
 
-int sh_fwd(const int64_t* edge_ptr, const int32_t* rev, const float4* geo, int64_t nv, int max_degree, const float* X,
-           const float* W, int K, int L, int dg, RbfParams rp, float* S, void* ws, int min_n, cudaStream_t st) {
-  using SM = sh::WarpSmem<6, 7>;
-  const int nch = sh_nch(max_degree);
+template <int MODE>
+static int sh_fwd_mode(const int64_t* edge_ptr, const int32_t* rev, const float4* geo, int64_t nv, int nch,
+                       const float* X, const float* W, int dg, RbfParams rp, float cutoff, float* S, float* Mpart,
+                       int min_n, cudaStream_t st) {
+  using SM = sh::WarpSmem<6, 7, sh::kTile, MODE>;
   const int ncb = (dg + 31) / 32;
   const size_t smem = sizeof(float) * SM::fwd_total * sh::kW;
-  float* Mpart = reinterpret_cast<float*>(ws);
   static bool c1 = false, c2 = false;
-  auto k1 = sh::fwd_moments_kernel<6, 7>;
-  auto k2 = sh::fwd_apply_kernel<6, 7>;
+  auto k1 = sh::fwd_moments_kernel<6, 7, MODE>;
+  auto k2 = sh::fwd_apply_kernel<6, 7, MODE>;
   set_smem(k1, smem, c1);
   set_smem(k2, smem, c2);
   const int grid = sh_grid(nv * nch * ncb);
-  k1<<<grid, sh::kW * 32, smem, st>>>(edge_ptr, rev, geo, nv, nch, X, W, dg, rp, S, Mpart, min_n);
+  k1<<<grid, sh::kW * 32, smem, st>>>(edge_ptr, rev, geo, nv, nch, X, W, dg, rp, cutoff, S, Mpart, min_n);
   if (check_launch("triplet_fwd_sh_moments")) return 1;
   k2<<<grid, sh::kW * 32, smem, st>>>(edge_ptr, rev, geo, nv, nch, dg, rp, S, Mpart, min_n);
   return check_launch("triplet_fwd_sh_apply");
+}
+
+int sh_fwd(const int64_t* edge_ptr, const int32_t* rev, const float4* geo, int64_t nv, int max_degree, const float* X,
+           const float* W, int K, int L, int dg, RbfParams rp, float cutoff, int mode, float* S, void* ws, int min_n,
+           cudaStream_t st) {
+  const int nch = sh_nch(max_degree);
+  float* Mpart = reinterpret_cast<float*>(ws);
+  if (mode == 1) return sh_fwd_mode<1>(edge_ptr, rev, geo, nv, nch, X, W, dg, rp, cutoff, S, Mpart, min_n, st);
+  if (mode == 2) return sh_fwd_mode<2>(edge_ptr, rev, geo, nv, nch, X, W, dg, rp, cutoff, S, Mpart, min_n, st);
+  return sh_fwd_mode<0>(edge_ptr, rev, geo, nv, nch, X, W, dg, rp, cutoff, S, Mpart, min_n, st);
 }
 
 static int64_t sh_bwd_warps(int64_t nv, int nch, int dg, int* grid_out) {
@@ -967,10 +1153,38 @@ int64_t sh_bwd_workspace_bytes(int64_t nv, int64_t ne, int max_degree, int K, in
          (ncb > 1 ? static_cast<int64_t>(ncb) * std::max<int64_t>(ne, 1) * 16 : 0) + 256;
 }
 
+template <int MODE>
+static int sh_bwd_mode(const int64_t* edge_ptr, const int32_t* rev, const float4* geo, int64_t nv, int64_t ne,
+                       int nch, int grid, int64_t nw, const float* X, const float* W, int K, int L, int dg,
+                       RbfParams rp, float cutoff, const float* Sbar, float* Xbar, float* Wbar, float4* edge_grad,
+                       float* wpart, float* Mpart, float* Mbpart, float4* egp, int min_n, int accumulate,
+                       cudaStream_t st) {
+  using SM = sh::WarpSmem<6, 7, sh::kTile, MODE>;
+  const int ncb = (dg + 31) / 32;
+  static bool c1 = false, c2 = false;
+  auto k1 = sh::bwd_moments_kernel<6, 7, MODE>;
+  auto k2 = sh::bwd_apply_kernel<6, 7, MODE>;
+  const size_t smem1 = sizeof(float) * SM::fwd_total * sh::kW;
+  const size_t smem2 = sizeof(float) * sh::BwdSmem<6, 7, MODE>::total * sh::kW;
+  set_smem(k1, smem1, c1);
+  set_smem(k2, smem2, c2);
+  k1<<<sh_grid(nv * nch * ncb), sh::kW * 32, smem1, st>>>(edge_ptr, rev, geo, nv, nch, X, W, dg, rp, cutoff, Sbar,
+                                                         Mpart, Mbpart, min_n);
+  if (check_launch("triplet_bwd_sh_moments")) return 1;
+  k2<<<grid, sh::kW * 32, smem2, st>>>(edge_ptr, rev, geo, nv, ne, nch, X, W, dg, rp, cutoff, Sbar, Mpart, Mbpart,
+                                       Xbar, wpart, egp, edge_grad, min_n);
+  if (check_launch("triplet_bwd_sh_apply")) return 1;
+  sh::reduce_wbar_kernel<6, 7, MODE><<<K * ncb, 1024, 0, st>>>(wpart, nw, ncb, dg, Wbar, accumulate);
+  if (check_launch("triplet_bwd_sh_reduce")) return 1;
+  if (ncb == 1) return 0;
+  sh::add_eg_kernel<<<grid_for(nv, 128), 128, 0, st>>>(edge_ptr, nv, egp, ncb, ne, min_n, edge_grad);
+  return check_launch("triplet_bwd_sh_eg");
+}
+
 int sh_bwd(const int64_t* edge_ptr, const int32_t* rev, const float4* geo, int64_t nv, int64_t ne, int max_degree,
-           const float* X, const float* W, int K, int L, int dg, RbfParams rp, const float* Sbar, float* Xbar,
-           float* Wbar, float4* edge_grad, void* ws, int min_n, int accumulate, cudaStream_t st) {
-  using SM = sh::WarpSmem<6, 7>;
+           const float* X, const float* W, int K, int L, int dg, RbfParams rp, float cutoff, int mode,
+           const float* Sbar, float* Xbar, float* Wbar, float4* edge_grad, void* ws, int min_n, int accumulate,
+           cudaStream_t st) {
   const int nch = sh_nch(max_degree);
   int grid;
   const int64_t nw = sh_bwd_warps(std::max<int64_t>(nv, 1), nch, dg, &grid);
@@ -983,24 +1197,13 @@ int sh_bwd(const int64_t* edge_ptr, const int32_t* rev, const float4* geo, int64
     const uintptr_t p = reinterpret_cast<uintptr_t>(Mbpart + sh_fwd_workspace_bytes(nv, max_degree, K, L, dg) / 4);
     egp = reinterpret_cast<float4*>((p + 15) & ~static_cast<uintptr_t>(15));
   }
-  static bool c1 = false, c2 = false;
-  auto k1 = sh::bwd_moments_kernel<6, 7>;
-  auto k2 = sh::bwd_apply_kernel<6, 7>;
-  const size_t smem1 = sizeof(float) * SM::fwd_total * sh::kW;
-  const size_t smem2 = sizeof(float) * sh::BwdSmem<6, 7>::total * sh::kW;
-  set_smem(k1, smem1, c1);
-  set_smem(k2, smem2, c2);
-  k1<<<sh_grid(nv * nch * ncb), sh::kW * 32, smem1, st>>>(edge_ptr, rev, geo, nv, nch, X, W, dg, rp, Sbar, Mpart,
-                                                         Mbpart, min_n);
-  if (check_launch("triplet_bwd_sh_moments")) return 1;
-  k2<<<grid, sh::kW * 32, smem2, st>>>(edge_ptr, rev, geo, nv, ne, nch, X, W, dg, rp, Sbar, Mpart, Mbpart, Xbar,
-                                       wpart, egp, edge_grad, min_n);
-  if (check_launch("triplet_bwd_sh_apply")) return 1;
-  sh::reduce_wbar_kernel<6, 7><<<K * ncb, 1024, 0, st>>>(wpart, nw, ncb, dg, Wbar, accumulate);
-  if (check_launch("triplet_bwd_sh_reduce")) return 1;
-  if (ncb == 1) return 0;
-  sh::add_eg_kernel<<<grid_for(nv, 128), 128, 0, st>>>(edge_ptr, nv, egp, ncb, ne, min_n, edge_grad);
-  return check_launch("triplet_bwd_sh_eg");
+#define EGN_SHB(M)                                                                                               \
+  return sh_bwd_mode<M>(edge_ptr, rev, geo, nv, ne, nch, grid, nw, X, W, K, L, dg, rp, cutoff, Sbar, Xbar, Wbar, \
+                        edge_grad, wpart, Mpart, Mbpart, egp, min_n, accumulate, st)
+  if (mode == 1) EGN_SHB(1);
+  if (mode == 2) EGN_SHB(2);
+  EGN_SHB(0);
+#undef EGN_SHB
 }
 
 }  // namespace egn

@@ -246,7 +246,7 @@ class Engine:
         L = ops.linear
         folded = self._folded_weights()
         side = self._side_stream(bg)
-        rbf = ops.rbf(bg.geo, c.k_rbf, c.cutoff)
+        rbf = ops.rbf(bg.geo, c.k_rbf, c.cutoff, c.basis_code)
         m = ops.rbf_linear(rbf, w["edge_init.w"], w["edge_init.b"]) if m0 is None else m0  # K = k_rbf (6)
         u = (torch.zeros((bg.num_graphs, c.d_u), dtype=torch.float32, device=bg.device) if u0 is None
              else u0.clone())
@@ -276,7 +276,7 @@ class Engine:
             else:
                 down = X = L(m, w[p + "tu.down"])
             Wk = folded[b]["Wk"]
-            S = ops.triplet_fwd(bg.edge_ptr, bg.rev, bg.geo, X, Wk, c.cutoff, max_degree=bg.max_deg)
+            S = ops.triplet_fwd(bg.edge_ptr, bg.rev, bg.geo, X, Wk, c.cutoff, max_degree=bg.max_deg, basis=c.basis_code)
             g = gates[b]
             if gates_ready is not None:
                 torch.cuda.current_stream().wait_event(gates_ready)
@@ -469,7 +469,7 @@ class Engine:
             if side is not None:
                 pending.append(g_prod)
             X_bar, Wk_bar = ops.triplet_bwd(bg.edge_ptr, bg.rev, bg.geo, st["X"], st["Wk"], c.cutoff,
-                                            S_bar, eg, max_degree=bg.max_deg)
+                                            S_bar, eg, max_degree=bg.max_deg, basis=c.basis_code)
             if gem:
                 # wp_bar[c, kl] = Wk_bar[kl, c]: read transposed in place
                 wkb = Wk_bar.view(-1, Wk_bar.shape[2])
@@ -495,7 +495,7 @@ class Engine:
             ops.small_gemms(post)
         # edge init (engine.py:109-111), K = k_rbf
         ops.rbf_linear_bwd(fw.rbf, w["edge_init.w"], m_bar, rbf_bar, gr["edge_init.w"], gr["edge_init.b"])
-        ops.rbf_bwd(bg.geo, rbf_bar, c.cutoff, eg)
+        ops.rbf_bwd(bg.geo, rbf_bar, c.cutoff, eg, c.basis_code)
         pos_bar = ops.positions_bwd(bg.edge_ptr, bg.rev, bg.geo, eg)
         if side is not None:
             main.wait_stream(side)
@@ -506,6 +506,8 @@ class Engine:
         """t_feat of one block for every triplet in (out, in) order (engine.py:146,149); index:
         position of that block in fw.blocks when the forward ran a subset of blocks."""
         c, w = self.config, self.weights.w
+        if c.basis_code:
+            raise ValueError("per-triplet features are materialised for the reference's Gaussian basis only")
         st = fw.blocks[block if index is None else index]
         P = ops.triplet_terms(bg.edge_ptr, bg.rev, bg.geo, bg.tri_ptr, bg.num_triplets, st["X"], st["Wk"],
                               c.cutoff)

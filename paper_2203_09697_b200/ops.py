@@ -113,9 +113,14 @@ def triplet_angles(pos, edge_ptr, recv, tri_ptr, num_triplets, shift=None):
     return out
 
 
-def rbf(geo, k_rbf, cutoff):
+def rbf(geo, k_rbf, cutoff, basis=0):
+    """Edge radial basis [E, K]: Gaussian (basis 0, the reference) or the radial Bessel basis
+    with the polynomial envelope (basis 1 / 2, DimeNet++ / GemNet)."""
     out = torch.empty((geo.shape[0], k_rbf), dtype=torch.float32, device=geo.device)
-    call("egn_rbf", ptr(geo), geo.shape[0], int(k_rbf), float(cutoff), ptr(out), stream())
+    if basis:
+        call("egn_rbf_bessel", ptr(geo), geo.shape[0], int(k_rbf), float(cutoff), ptr(out), stream())
+    else:
+        call("egn_rbf", ptr(geo), geo.shape[0], int(k_rbf), float(cutoff), ptr(out), stream())
     return out
 
 
@@ -232,8 +237,9 @@ def _channel_chunks(dg):
     return [(c0, min(dg, c0 + MAX_TRIPLET_WIDTH)) for c0 in range(0, dg, MAX_TRIPLET_WIDTH)]
 
 
-def triplet_fwd(edge_ptr, rev, geo, X, Wk, cutoff, max_degree=-1):
-    """S = sum over the centre tile (see include/egn_b200.h egn_triplet_fwd)."""
+def triplet_fwd(edge_ptr, rev, geo, X, Wk, cutoff, max_degree=-1, basis=0):
+    """S = sum over the centre tile (see include/egn_b200.h egn_triplet_fwd; basis 1 / 2:
+    egn_triplet_fwd_basis, the DimeNet++ / GemNet triplet bases)."""
     X = _c(X, torch.float32)
     Wk = _c(Wk, torch.float32)
     k, l, dg = Wk.shape
@@ -241,10 +247,16 @@ def triplet_fwd(edge_ptr, rev, geo, X, Wk, cutoff, max_degree=-1):
         S = torch.empty_like(X)
         for c0, c1 in _channel_chunks(dg):
             S[:, c0:c1] = triplet_fwd(edge_ptr, rev, geo, X[:, c0:c1].contiguous(), Wk[:, :, c0:c1].contiguous(),
-                                      cutoff, max_degree)
+                                      cutoff, max_degree, basis)
         return S
     S = torch.empty_like(X)
     nv = edge_ptr.shape[0] - 1
+    if basis:
+        nbytes = call("egn_triplet_fwd_basis_workspace_bytes", nv, int(max_degree), k, l, dg)
+        ws = _workspace_named("tfwd", nbytes, X.device)
+        call("egn_triplet_fwd_basis", ptr(edge_ptr), ptr(rev), ptr(geo), nv, int(max_degree), ptr(X), ptr(Wk), k, l,
+             dg, float(cutoff), int(basis), ptr(S), ptr(ws), stream())
+        return S
     nbytes = call("egn_triplet_fwd_workspace_bytes", nv, int(max_degree), k, l, dg)
     ws = _workspace_named("tfwd", nbytes, X.device) if nbytes > 0 else None
     call("egn_triplet_fwd", ptr(edge_ptr), ptr(rev), ptr(geo), nv, int(max_degree), ptr(X),
@@ -275,7 +287,8 @@ def _workspace(nbytes: int, device) -> torch.Tensor:
     return _workspace_named("ws", nbytes, device, 1 << 20)
 
 
-def triplet_bwd(edge_ptr, rev, geo, X, Wk, cutoff, S_bar, edge_grad, X_bar=None, W_bar=None, max_degree=None):
+def triplet_bwd(edge_ptr, rev, geo, X, Wk, cutoff, S_bar, edge_grad, X_bar=None, W_bar=None, max_degree=None,
+                basis=0):
     X = _c(X, torch.float32)
     Wk = _c(Wk, torch.float32)
     S_bar = _c(S_bar, torch.float32)
@@ -290,13 +303,17 @@ def triplet_bwd(edge_ptr, rev, geo, X, Wk, cutoff, S_bar, edge_grad, X_bar=None,
     if dg > MAX_TRIPLET_WIDTH:
         for c0, c1 in _channel_chunks(dg):
             xb, wb = triplet_bwd(edge_ptr, rev, geo, X[:, c0:c1].contiguous(), Wk[:, :, c0:c1].contiguous(), cutoff,
-                                 S_bar[:, c0:c1].contiguous(), edge_grad, max_degree=max_degree)
+                                 S_bar[:, c0:c1].contiguous(), edge_grad, max_degree=max_degree, basis=basis)
             X_bar[:, c0:c1] = xb
             W_bar[:, :, c0:c1] = wb
         return X_bar, W_bar
     ne = X.shape[0]
     nbytes = call("egn_triplet_bwd_workspace_bytes", nv, ne, int(max_degree), k, l, dg)
     ws = _workspace(nbytes, X.device)
+    if basis:
+        call("egn_triplet_bwd_basis", ptr(edge_ptr), ptr(rev), ptr(geo), nv, ne, int(max_degree), ptr(X), ptr(Wk), k,
+             l, dg, float(cutoff), int(basis), ptr(S_bar), ptr(X_bar), ptr(W_bar), ptr(edge_grad), ptr(ws), stream())
+        return X_bar, W_bar
     call("egn_triplet_bwd", ptr(edge_ptr), ptr(rev), ptr(geo), nv, ne, int(max_degree), ptr(X), ptr(Wk), k, l, dg,
          float(cutoff), ptr(S_bar), ptr(X_bar), ptr(W_bar), ptr(edge_grad), ptr(ws), stream())
     return X_bar, W_bar
@@ -420,9 +437,10 @@ def force_head_bwd(recv, geo, m, w, scale, f_bar, m_bar, edge_grad, w_bar=None):
     return w_bar
 
 
-def rbf_bwd(geo, rbf_bar, cutoff, edge_grad):
+def rbf_bwd(geo, rbf_bar, cutoff, edge_grad, basis=0):
     ne, k = rbf_bar.shape
-    call("egn_rbf_bwd", ptr(geo), ptr(_c(rbf_bar, torch.float32)), ne, k, float(cutoff), ptr(edge_grad), stream())
+    name = "egn_rbf_bessel_bwd" if basis else "egn_rbf_bwd"
+    call(name, ptr(geo), ptr(_c(rbf_bar, torch.float32)), ne, k, float(cutoff), ptr(edge_grad), stream())
 
 
 def positions_bwd(edge_ptr, rev, geo, edge_grad):

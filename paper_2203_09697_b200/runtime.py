@@ -563,7 +563,7 @@ class GraphParallelEngine:
         f32 = torch.float32
         self.clock.mark("init")
         folded = self._helper._folded_weights()
-        rbf = ops.rbf(d["geo_own"], c.k_rbf, c.cutoff)
+        rbf = ops.rbf(d["geo_own"], c.k_rbf, c.cutoff, c.basis_code)
         m = ops.rbf_linear(rbf, w["edge_init.w"], w["edge_init.b"])
         gates = [ops.rbf_linear(rbf, w[f"block{b}.tu.rbf_gate"]) for b in range(c.blocks)]
         u = torch.zeros((G, c.d_u), dtype=f32, device=dev)
@@ -578,7 +578,8 @@ class GraphParallelEngine:
             self._produce(d, X, d["eb"], lambda a, z, out: L(mm[a:z], Wx, out=out),
                           phase="forward", block=b, stage="X", level="edge", width=self.R.triplet_width)
             Wk = folded[b]["Wk"]
-            S = ops.triplet_fwd(d["ep_own"], bg.rev, bg.geo, X, Wk, c.cutoff, max_degree=bg.max_deg)
+            S = ops.triplet_fwd(d["ep_own"], bg.rev, bg.geo, X, Wk, c.cutoff, max_degree=bg.max_deg,
+                                basis=c.basis_code)
             S_o, g = S[e0:e1], gates[b]
             self.clock.mark(f"block{b}.eu")
             if gem:
@@ -756,7 +757,8 @@ class GraphParallelEngine:
                 g_prod = (Y_bar, st["S"][e0:e1])
             X_bar_full = (torch.empty_like if hf else torch.zeros_like)(st["X"])
             X_bar_full, Wk_bar = ops.triplet_bwd(d["ep_own"], bg.rev, bg.geo, st["X"], st["Wk"], c.cutoff, S_bar, eg,
-                                                 X_bar=X_bar_full, max_degree=bg.max_deg)
+                                                 X_bar=X_bar_full, max_degree=bg.max_deg,
+                                                 basis=c.basis_code)
             if not hf:
                 hnd = cm.reduce_scatter_rows(X_bar_full, d["eb"], async_op=True, phase="backward", block=b,
                                              stage="X", level="edge", width=self.R.triplet_width)
@@ -778,7 +780,7 @@ class GraphParallelEngine:
         ops.small_gemms(post)
         ops.rbf_linear_bwd(fw.rbf, w["edge_init.w"], m_bar, rbf_bar, gr["edge_init.w"], gr["edge_init.b"])
         self.clock.mark("backward.geometry")
-        ops.rbf_bwd(d["geo_own"], rbf_bar, c.cutoff, eg[e0:e1])
+        ops.rbf_bwd(d["geo_own"], rbf_bar, c.cutoff, eg[e0:e1], c.basis_code)
         pos_bar = ops.positions_bwd(bg.edge_ptr, bg.rev, bg.geo, eg)
         self.clock.mark("backward.reduce")
         cm.all_reduce_(pos_bar, phase="backward", block=-1, stage="positions", level="position")
@@ -800,6 +802,9 @@ class ReferenceScheduleEngine:
                  clock: _StageClock | None = None):
         self.weights, self.comm, self.part = weights, comm, part
         self.config = weights.config
+        if self.config.basis_code:
+            raise ValueError("the reference schedule implements the reference's Gaussian basis only; "
+                             "use schedule='centre' for basis='bessel'")
         self._helper = Engine(weights)
         r = comm.rank
         self.t0, self.t1 = int(part.trip_bounds[r]), int(part.trip_bounds[r + 1])
@@ -840,7 +845,7 @@ class ReferenceScheduleEngine:
         f32 = torch.float32
         self.clock.mark("init")
         folded = self._helper._folded_weights()
-        rbf = ops.rbf(bg.geo, c.k_rbf, c.cutoff)
+        rbf = ops.rbf(bg.geo, c.k_rbf, c.cutoff, c.basis_code)
         m = ops.rbf_linear(rbf, w["edge_init.w"], w["edge_init.b"])
         u = torch.zeros((G, c.d_u), dtype=f32, device=dev)
         blocks, v = [], None
@@ -1064,7 +1069,7 @@ class ReferenceScheduleEngine:
             ops.rbf_linear_bwd(fw.rbf[e0:e1], w["edge_init.w"], m_bar[e0:e1], rbf_bar[e0:e1], gr["edge_init.w"],
                                gr["edge_init.b"])
         self.clock.mark("backward.geometry")
-        ops.rbf_bwd(bg.geo, rbf_bar, c.cutoff, eg)
+        ops.rbf_bwd(bg.geo, rbf_bar, c.cutoff, eg, c.basis_code)
         pos_bar = ops.positions_bwd(bg.edge_ptr, bg.rev, bg.geo, eg)
         self.clock.mark("backward.reduce")
         cm.all_reduce_(pos_bar, phase="backward", block=-1, stage="positions", level="position")
@@ -1207,6 +1212,9 @@ class WorkerGroup:
         self.timeout, self.fault, self.device = timeout, fault, device
         self.track_replicas = track_replicas
         self.schedule = schedule
+        if schedule == "reference" and self.config.basis_code:
+            raise ValueError("the reference schedule implements the reference's Gaussian basis only; "
+                             "use schedule='centre' for basis='bessel'")
         self.bg = build_batch(system, self.config.cutoff, device)
         self.topology = topology_of(self.bg)
         self.geometry = geometry_of(self.bg)

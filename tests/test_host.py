@@ -26,6 +26,20 @@ def test_config_validation_and_json_roundtrip():
     assert c.triplet_width == c.d_bil and ModelConfig().triplet_width == ModelConfig().d_t
 
 
+def test_config_basis_selection():
+    """basis="bessel" selects the DimeNet++ / GemNet-T bases (native code 2 / 1); the
+    reference's Gaussian surrogate stays the default and keeps the reference's JSON keys."""
+    assert ModelConfig().basis_code == 0 and "basis" not in json.loads(ModelConfig().to_json())
+    d = ModelConfig(variant="dimenet-style", k_rbf=6, l_sbf=7, basis="bessel")
+    g = ModelConfig(variant="gemnet-style", k_rbf=6, l_sbf=7, basis="bessel")
+    assert (d.basis_code, g.basis_code) == (2, 1)
+    assert ModelConfig.from_json(g.to_json()) == g
+    with pytest.raises(ValueError, match="k_rbf = 6 and l_sbf = 7"):
+        ModelConfig(k_rbf=8, l_sbf=7, basis="bessel")
+    with pytest.raises(ValueError, match="basis must be"):
+        ModelConfig(basis="legendre")
+
+
 @pytest.mark.parametrize("fname", ["model_dimenet_small.npz", "model_gemnet_odd.npz", "model_gemnet_c2dims.npz"])
 def test_init_params_matches_reference_checksums(fname):
     gd = load_golden(fname)

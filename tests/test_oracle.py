@@ -19,7 +19,7 @@ MODEL_FILES = sorted(p.name for p in GOLDEN.glob("model_*.npz"))
 
 def _cfg(js):
     d = json.loads(str(js))
-    return O.Config(**{k: d[k] for k in O.Config.__dataclass_fields__})
+    return O.Config(**{k: d[k] for k in O.Config.__dataclass_fields__ if k in d})
 
 
 def test_graph_topology_bit_exact(graphs_golden):
@@ -204,3 +204,61 @@ def test_neighbour_cap_restatement():
     full = O.cap_graph(g, pos, 1000)
     for key in ("src", "recv", "trip_in", "trip_out", "rev", "dist", "angles"):
         assert np.array_equal(getattr(full, key), getattr(g, key)), key
+
+
+@pytest.mark.parametrize("variant", [O.DIMENET, O.GEMNET])
+def test_bessel_bases_restatement(variant):
+    """DimeNet++ / GemNet bases (no reference counterpart, parity unpinned):
+    known answers and finite-difference checks of the fp64 restatement."""
+    from scipy.special import spherical_jn
+
+    z = O.spherical_bessel_zeros(7, 6)
+    for l in range(7):
+        assert np.abs(spherical_jn(l, z[l])).max() < 1e-12
+    np.testing.assert_allclose(z[0], np.pi * np.arange(1, 7), rtol=1e-13)
+    # envelope: smooth cutoff, u(1) = u'(1) = 0
+    assert abs(O.envelope(1.0 - 1e-12) - 0.0) < 1e-9 and abs(O.envelope_dx(1.0 - 1e-12)) < 1e-8
+    rng = np.random.default_rng(0)
+    d = rng.uniform(0.5, 5.9, 30)
+    ang = rng.uniform(0.05, np.pi - 0.05, 30)
+    h = 1e-6
+    fd = (O.bessel_rbf(d + h, 6, 6.0) - O.bessel_rbf(d - h, 6, 6.0)) / (2 * h)
+    np.testing.assert_allclose(O.bessel_rbf_ddist(d, 6, 6.0), fd, rtol=1e-6, atol=1e-8)
+    dd, da = O.sbf_bessel_partials(d, ang, 6, 7, 6.0, variant)
+    fdd = (O.sbf_bessel(d + h, ang, 6, 7, 6.0, variant) - O.sbf_bessel(d - h, ang, 6, 7, 6.0, variant)) / (2 * h)
+    fda = (O.sbf_bessel(d, ang + h, 6, 7, 6.0, variant) - O.sbf_bessel(d, ang - h, 6, 7, 6.0, variant)) / (2 * h)
+    np.testing.assert_allclose(dd, fdd, rtol=1e-5, atol=1e-7)
+    np.testing.assert_allclose(da, fda, rtol=1e-5, atol=1e-7)
+    # the whole model on the bessel bases: position and parameter gradients vs central differences
+    cfg = O.Config(variant=variant, blocks=2, d_u=4, d_v=5, d_e=6, d_t=4, d_bil=3, k_rbf=6, l_sbf=7, cutoff=6.0,
+                   basis="bessel")
+    pos, zz = O.random_cloud(7, 0.06, np.random.default_rng(5))
+    P = O.init_params(cfg)
+    fw = O.forward(cfg, P, pos, zz)
+    df = rng.standard_normal(pos.shape) if variant == O.GEMNET else None
+
+    def objective(p_, P_):
+        f = O.forward(cfg, P_, p_, zz)
+        val = 0.7 * f.energy
+        if df is not None:
+            val += float((f.forces * df).sum())
+        return val
+
+    G, dpos = O.backward(fw, P, 0.7, df)
+    for a in range(3):
+        for ax in range(3):
+            e = np.zeros_like(pos)
+            e[a, ax] = 1e-5
+            fdv = (objective(pos + e, P) - objective(pos - e, P)) / 2e-5
+            assert abs(fdv - dpos[a, ax]) < 1e-6 * max(1.0, abs(fdv)), (a, ax, fdv, dpos[a, ax])
+    for name in ("block0.tu.sbf_gate", "block1.tu.rbf_gate", "edge_init.w"):
+        arr = P[name].ravel()
+        i = 2
+        orig = arr[i]
+        arr[i] = orig + 1e-6
+        fp = objective(pos, P)
+        arr[i] = orig - 1e-6
+        fm = objective(pos, P)
+        arr[i] = orig
+        fdv = (fp - fm) / 2e-6
+        assert abs(fdv - G[name].ravel()[i]) < 1e-6 * max(1.0, abs(fdv)), name
