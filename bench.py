@@ -73,6 +73,8 @@ def _args():
     ap.add_argument("--partition", choices=["aligned", "centre", "reference"], default="aligned")
     ap.add_argument("--cpu-budget", type=float, default=12.0, help="seconds of CPU oracle sampling")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--basis", choices=["gaussian", "bessel"], default="gaussian",
+                    help="gaussian: the reference's bases; bessel: DimeNet++ / GemNet-T bases (SURVEY 8(f) f2)")
     ap.add_argument("--no-kernel-timing", action="store_true")
     ap.add_argument("--eager", action="store_true", help="no CUDA-graph replay of the training step")
     return ap.parse_args()
@@ -82,7 +84,7 @@ def _config(wl):
     from paper_2203_09697_b200 import ModelConfig
 
     keys = ("variant", "blocks", "d_u", "d_v", "d_e", "d_t", "d_bil", "k_rbf", "l_sbf", "cutoff")
-    return ModelConfig(**{k: wl[k] for k in keys}, seed=0)
+    return ModelConfig(**{k: wl[k] for k in keys}, seed=0, basis=wl.get("basis", "gaussian"))
 
 
 def _systems(wl, graphs, rank=0):
@@ -533,6 +535,7 @@ def run_ours(args, wl):
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (random_cloud OC20-density graphs, random-init weights, teacher targets)",
             "config": {"workload": args.workload, "variant": wl["variant"], "graphs_per_gpu": graphs,
+                       **({"basis": cfg.basis} if cfg.basis != "gaussian" else {}),
                        "atoms_per_graph": wl["atoms"], "cutoff": wl["cutoff"], "blocks": cfg.blocks,
                        "d_e": cfg.d_e, "d_t": cfg.d_t, "d_bil": cfg.d_bil, "edges_total": int(nt[1]),
                        "triplets_total": int(nt[0]), "parallelism": parallelism,
@@ -559,7 +562,7 @@ def run_ours(args, wl):
 
 def main():
     args = _args()
-    wl = WORKLOADS[args.workload]
+    wl = dict(WORKLOADS[args.workload], basis=args.basis)
     if args.impl == "reference":
         run_reference(args, wl)
     else:
