@@ -223,6 +223,17 @@ int egn_triplet_bwd(const int64_t* edge_ptr, const int32_t* rev, const float* ge
                     const float* W, int k_rbf, int l_sbf, int dg, double cutoff, const float* S_bar,
                     float* X_bar, float* W_bar, float* edge_grad, void* workspace,
                     egn_stream_t stream);
+/* egn_triplet_bwd in two phases that touch disjoint outputs, so they can run on two streams:
+ *   phases = 1: the angle adjoint of the small-degree centres (edge_grad x, y, z only);
+ *   phases = 2: everything else (X_bar, W_bar, edge_grad.w, and all of the larger centres);
+ *   phases = 3: both (== egn_triplet_bwd).
+ * Where the split does not apply (other triplet paths), phases = 1 does nothing and
+ * phases = 2 does the whole adjoint.  Phase 1 uses no workspace. */
+int egn_triplet_bwd_ex(const int64_t* edge_ptr, const int32_t* rev, const float* geo,
+                       int64_t num_nodes, int64_t num_edges, int max_degree, const float* X,
+                       const float* W, int k_rbf, int l_sbf, int dg, double cutoff, const float* S_bar,
+                       float* X_bar, float* W_bar, float* edge_grad, int phases, void* workspace,
+                       egn_stream_t stream);
 
 /* Per-triplet feature debug output t_feat-like rows for parity tests:
  * P[t, c] = X[rq, c] * sum_l T_l(x_pq) Rw[rq, l, c] for every triplet t in

@@ -553,7 +553,7 @@ int fast_fwd(const int64_t* edge_ptr, const int32_t* rev, const float4* geo, int
 int64_t fast_bwd_workspace_bytes(int64_t nv, int64_t ne, int K, int L, int dg);
 int fast_bwd(const int64_t* edge_ptr, const int32_t* rev, const float4* geo, int64_t nv, int64_t ne,
              const float* X, const float* W, int K, int L, int dg, RbfParams rp, const float* Sbar, float* Xbar,
-             float* Wbar, float4* edge_grad, void* ws, cudaStream_t st);
+             float* Wbar, float4* edge_grad, void* ws, cudaStream_t st, int phases);
 constexpr int kFastMaxDeg = 64;
 // spherical-harmonic factorised path (triplet_sh.cu): O(deg) per edge
 bool sh_supported(int K, int L, int dg);
@@ -770,9 +770,26 @@ int egn_triplet_bwd(const int64_t* edge_ptr, const int32_t* rev, const float* ge
                     int64_t num_nodes, int64_t num_edges, int max_degree, const float* X, const float* W,
                     int k_rbf, int l_sbf, int dg, double cutoff, const float* S_bar, float* X_bar,
                     float* W_bar, float* edge_grad, void* workspace, egn_stream_t stream) {
+  return egn_triplet_bwd_ex(edge_ptr, rev, geo, num_nodes, num_edges, max_degree, X, W, k_rbf, l_sbf, dg, cutoff,
+                            S_bar, X_bar, W_bar, edge_grad, 3, workspace, stream);
+}
+
+int egn_triplet_bwd_ex(const int64_t* edge_ptr, const int32_t* rev, const float* geo, int64_t num_nodes,
+                       int64_t num_edges, int max_degree, const float* X, const float* W, int k_rbf, int l_sbf,
+                       int dg, double cutoff, const float* S_bar, float* X_bar, float* W_bar, float* edge_grad,
+                       int phases, void* workspace, egn_stream_t stream) {
   if (int rc = check_dims(k_rbf, l_sbf, dg)) return rc;
+  EGN_REQUIRE(phases >= 1 && phases <= 3, "phases must be 1, 2 or 3");
   cudaStream_t st = as_stream(stream);
+  static const bool tc_all = [] { const char* e = std::getenv("EGN_TRIPLET_TC_ALL"); return e && e[0] == '1'; }();
+  // the angle phase exists only on the small-degree fast path (bw1); elsewhere phase 2 does all
+  const bool split_ok = g_triplet_path != 1 && fast_supported(k_rbf, l_sbf, dg) && !tc_all;
+  if (!split_ok) {
+    if (phases == 1) return 0;
+    phases = 3;
+  }
   if (num_nodes == 0) {
+    if (!(phases & 2)) return 0;
     cudaMemsetAsync(W_bar, 0, sizeof(float) * k_rbf * l_sbf * dg, st);
     return check_launch("triplet_bwd_empty");
   }
@@ -780,14 +797,14 @@ int egn_triplet_bwd(const int64_t* edge_ptr, const int32_t* rev, const float* ge
   const float4* g4 = reinterpret_cast<const float4*>(geo);
   float4* eg = reinterpret_cast<float4*>(edge_grad);
   int min_n = 0, accumulate = 0;
-  static const bool tc_all = [] { const char* e = std::getenv("EGN_TRIPLET_TC_ALL"); return e && e[0] == '1'; }();
   const bool use_sh = !tc_all && g_triplet_path != 2 && sh_supported(k_rbf, l_sbf, dg) && max_degree >= 0;
   if (fast_supported(k_rbf, l_sbf, dg) && !(tc_all && tc_bwd_supported(k_rbf, l_sbf, dg, max_degree)) &&
       !(use_sh && g_triplet_path == 1)) {
     char* fws = reinterpret_cast<char*>(workspace) + generic_ws_bytes(num_nodes, k_rbf, l_sbf, dg);
     if (int rc = fast_bwd(edge_ptr, rev, g4, num_nodes, num_edges, X, W, k_rbf, l_sbf, dg, rp, S_bar, X_bar,
-                          W_bar, eg, fws, st))
+                          W_bar, eg, fws, st, phases))
       return rc;
+    if (!(phases & 2)) return 0;  // angle phase only
     if (max_degree >= 0 && max_degree <= kFastMaxDeg) return 0;
     min_n = kFastMaxDeg;
     accumulate = 1;

@@ -33,6 +33,13 @@ __device__ __forceinline__ int chan(int cg, int i) { return i < 4 ? cg * 4 + i :
 // permuted row slot: thread group rg reads rows rg, rg+16, rg+32, rg+48 as one float4
 __device__ __forceinline__ int rslot(int p) { return (p & 15) * 4 + (p >> 4); }
 
+// packed fp32 FMA (FFMA2, sm_100a: two lanes of fp32 per instruction, twice the FFMA rate):
+// c + a * b on both halves with a scalar a broadcast.  Per half it is the same fma.rn as
+// fmaf, so a loop rewritten on it gives bit-identical results.
+__device__ __forceinline__ float2 ffma2(float a, float2 b, float2 c) { return __ffma2_rn(make_float2(a, a), b, c); }
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
+constexpr int kLP = 4;  // L = 7 angular orders as 4 pairs (the 8th is zero)
+
 __device__ __forceinline__ float rbf1(float d, int k, RbfParams rp) {
   const float dd = d - rp.step * k;
   return __expf(-rp.gamma * dd * dd);
@@ -51,7 +58,7 @@ __device__ __forceinline__ void load_center(float4* Us, float* Rb, const float4*
 // Q chunk: rows (t, l) for t < nq (row stride RS floats), natural channel order; thread
 // (cq = tid & 63, half = tid >> 6)
 template <int K, int L, int RS = kCB>
-__device__ __forceinline__ void build_q(float* Qs, const float (&wreg)[K][L], const float* Rb,
+__device__ __forceinline__ void build_q(float* Qs, const float2 (&wreg)[K][kLP], const float* Rb,
                                         const int32_t* __restrict__ rev, const float* __restrict__ X,
                                         int64_t off, int q0, int nq, int dg, int c0) {
   const int cq = threadIdx.x & 63, half = threadIdx.x >> 6;
@@ -72,13 +79,15 @@ __device__ __forceinline__ void build_q(float* Qs, const float (&wreg)[K][L], co
     float r[K];
 #pragma unroll
     for (int k = 0; k < K; ++k) r[k] = rb[k];
+    float2 s[kLP];
 #pragma unroll
-    for (int l = 0; l < L; ++l) {
-      float s = 0.f;
+    for (int lp = 0; lp < kLP; ++lp) s[lp] = make_float2(0.f, 0.f);
 #pragma unroll
-      for (int k = 0; k < K; ++k) s = fmaf(r[k], wreg[k][l], s);
-      Qs[(t * L + l) * RS + cq] = xv * s;
-    }
+    for (int k = 0; k < K; ++k)
+#pragma unroll
+      for (int lp = 0; lp < kLP; ++lp) s[lp] = ffma2(r[k], wreg[k][lp], s[lp]);
+#pragma unroll
+    for (int l = 0; l < L; ++l) Qs[(t * L + l) * RS + cq] = xv * ((l & 1) ? s[l >> 1].y : s[l >> 1].x);
   }
 }
 
@@ -119,27 +128,33 @@ __device__ __forceinline__ void build_c(float* Ct, const float4* Us, int n, int 
 
 template <int TMR>
 __device__ __forceinline__ void micro(const float* __restrict__ A, const float* __restrict__ B, int nkk,
-                                      int rg, int cg, float (&acc)[4][8]) {
+                                      int rg, int cg, float2 (&acc)[4][4]) {
 #pragma unroll 4
   for (int kk = 0; kk < nkk; ++kk) {
     const float4 a = *reinterpret_cast<const float4*>(A + kk * kCB + rg * 4);
     const float4 b0 = *reinterpret_cast<const float4*>(B + kk * kCB + cg * 4);
     const float4 b1 = *reinterpret_cast<const float4*>(B + kk * kCB + 32 + cg * 4);
     const float av[4] = {a.x, a.y, a.z, a.w};
-    const float bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+    const float2 bv[4] = {make_float2(b0.x, b0.y), make_float2(b0.z, b0.w), make_float2(b1.x, b1.y),
+                          make_float2(b1.z, b1.w)};
 #pragma unroll
     for (int r = 0; r < TMR; ++r)
 #pragma unroll
-      for (int i = 0; i < 8; ++i) acc[r][i] = fmaf(av[r], bv[i], acc[r][i]);
+      for (int i = 0; i < 4; ++i) acc[r][i] = ffma2(av[r], bv[i], acc[r][i]);
   }
 }
 
 template <int K, int L>
-__device__ __forceinline__ void load_wreg(float (&wreg)[K][L], const float* __restrict__ W, int dg, int c) {
+__device__ __forceinline__ void load_wreg(float2 (&wreg)[K][kLP], const float* __restrict__ W, int dg, int c) {
+  static_assert(L <= 2 * kLP, "L <= 8");
 #pragma unroll
   for (int k = 0; k < K; ++k)
 #pragma unroll
-    for (int l = 0; l < L; ++l) wreg[k][l] = c < dg ? W[(k * L + l) * dg + c] : 0.f;
+    for (int lp = 0; lp < kLP; ++lp) {
+      const int l0 = 2 * lp, l1 = 2 * lp + 1;
+      wreg[k][lp] = make_float2(c < dg && l0 < L ? W[(k * L + l0) * dg + c] : 0.f,
+                                c < dg && l1 < L ? W[(k * L + l1) * dg + c] : 0.f);
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -162,13 +177,13 @@ fwd_kernel(const int64_t* __restrict__ edge_ptr, const int32_t* __restrict__ rev
     __syncthreads();
     load_center<K>(Us, Rb, geo, off, n, rp);
     for (int c0 = 0; c0 < dg; c0 += kCB) {
-      float wreg[K][L];
+      float2 wreg[K][kLP];
       load_wreg<K, L>(wreg, W, dg, c0 + (tid & 63));
-      float acc[4][8];
+      float2 acc[4][4];
 #pragma unroll
       for (int r = 0; r < 4; ++r)
 #pragma unroll
-        for (int i = 0; i < 8; ++i) acc[r][i] = 0.f;
+        for (int i = 0; i < 4; ++i) acc[r][i] = make_float2(0.f, 0.f);
       for (int q0 = 0; q0 < n; q0 += kQC) {
         const int nq = min(kQC, n - q0);
         __syncthreads();
@@ -191,7 +206,7 @@ fwd_kernel(const int64_t* __restrict__ edge_ptr, const int32_t* __restrict__ rev
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
             const int c = chan(cg, i);
-            if (c0 + c < dg) dst[c] = acc[r][i];
+            if (c0 + c < dg) dst[c] = (i & 1) ? acc[r][i >> 1].y : acc[r][i >> 1].x;
           }
         }
       }
@@ -213,11 +228,15 @@ __device__ __forceinline__ void bw1_tile(const float* Qs, const float* Sb, const
   const int tid = threadIdx.x;
   const int t = tid / G, pg = tid - t * G;
   if (t >= nq) return;
-  float acc[L][PP];
+  // Z[(q, l), p] for l >= 1 (T_0' = 0: the l = 0 row is never needed).  Packed accumulators:
+  // row pairs (p_i, p_i+1) for PP >= 2 (bit-identical to the scalar loop), even / odd channel
+  // halves for PP = 1.
+  constexpr int PH = PP >= 2 ? PP / 2 : 1;
+  float2 acc2[L][PH];
 #pragma unroll
-  for (int l = 0; l < L; ++l)
+  for (int l = 1; l < L; ++l)
 #pragma unroll
-    for (int i = 0; i < PP; ++i) acc[l][i] = 0.f;
+    for (int i = 0; i < PH; ++i) acc2[l][i] = make_float2(0.f, 0.f);
   const float* qrow = Qs + (t * L) * kSbStride;
 #pragma unroll 4
   for (int c = 0; c < kCB; c += 4) {
@@ -225,17 +244,27 @@ __device__ __forceinline__ void bw1_tile(const float* Qs, const float* Sb, const
 #pragma unroll
     for (int i = 0; i < PP; ++i) sv[i] = *reinterpret_cast<const float4*>(Sb + (pg + G * i) * kSbStride + c);
 #pragma unroll
-    for (int l = 0; l < L; ++l) {
+    for (int l = 1; l < L; ++l) {
       const float4 qv = *reinterpret_cast<const float4*>(qrow + l * kSbStride + c);
+      if (PP >= 2) {
 #pragma unroll
-      for (int i = 0; i < PP; ++i) {
-        acc[l][i] = fmaf(qv.x, sv[i].x, acc[l][i]);
-        acc[l][i] = fmaf(qv.y, sv[i].y, acc[l][i]);
-        acc[l][i] = fmaf(qv.z, sv[i].z, acc[l][i]);
-        acc[l][i] = fmaf(qv.w, sv[i].w, acc[l][i]);
+        for (int i = 0; i < PH; ++i) {
+          acc2[l][i] = ffma2(qv.x, make_float2(sv[2 * i].x, sv[2 * i + 1].x), acc2[l][i]);
+          acc2[l][i] = ffma2(qv.y, make_float2(sv[2 * i].y, sv[2 * i + 1].y), acc2[l][i]);
+          acc2[l][i] = ffma2(qv.z, make_float2(sv[2 * i].z, sv[2 * i + 1].z), acc2[l][i]);
+          acc2[l][i] = ffma2(qv.w, make_float2(sv[2 * i].w, sv[2 * i + 1].w), acc2[l][i]);
+        }
+      } else {
+        acc2[l][0] = ffma2(make_float2(qv.x, qv.y), make_float2(sv[0].x, sv[0].y), acc2[l][0]);
+        acc2[l][0] = ffma2(make_float2(qv.z, qv.w), make_float2(sv[0].z, sv[0].w), acc2[l][0]);
       }
     }
   }
+  auto zval = [&](int l, int i) -> float {
+    if (PP >= 2) return (i & 1) ? acc2[l][i >> 1].y : acc2[l][i >> 1].x;
+    return acc2[l][0].x + acc2[l][0].y;
+  };
+
   const int q = q0 + t;
   const float4 uq = Us[q];
 #pragma unroll
@@ -248,7 +277,7 @@ __device__ __forceinline__ void bw1_tile(const float* Qs, const float* Sb, const
     float um = 0.f, uc = 1.f, v = 0.f;
 #pragma unroll
     for (int l = 1; l < L; ++l) {
-      v = fmaf(static_cast<float>(l) * uc, acc[l][i], v);
+      v = fmaf(static_cast<float>(l) * uc, zval(l, i), v);
       const float un = fmaf(2.f * x, uc, -um);
       um = uc;
       uc = un;
@@ -281,7 +310,7 @@ bw1_kernel(const int64_t* __restrict__ edge_ptr, const int32_t* __restrict__ rev
     const int PP = n <= 16 ? 1 : (n <= 32 ? 2 : 4);
     const int G = (n + PP - 1) / PP;
     for (int c0 = 0; c0 < dg; c0 += kCB) {
-      float wreg[K][L];
+      float2 wreg[K][kLP];
       load_wreg<K, L>(wreg, W, dg, c0 + (tid & 63));
       __syncthreads();
       for (int i = tid; i < n * kCB; i += kT) {
@@ -314,12 +343,13 @@ bw1_kernel(const int64_t* __restrict__ edge_ptr, const int32_t* __restrict__ rev
         fy = fmaf(v, uo.y - x * ue.y, fy);
         fz = fmaf(v, uo.z - x * ue.z, fz);
       }
+      // x, y, z only (4-byte accesses): bw2 may update .w of the same edge concurrently when
+      // the angle phase runs on its own stream (egn_triplet_bwd_ex phases)
       const float inv = 1.f / ue.w;
-      float4 g = edge_grad[off + e];
-      g.x += fx * inv;
-      g.y += fy * inv;
-      g.z += fz * inv;
-      edge_grad[off + e] = g;
+      float* g = reinterpret_cast<float*>(edge_grad + off + e);
+      g[0] += fx * inv;
+      g[1] += fy * inv;
+      g[2] += fz * inv;
     }
   }
 }
@@ -339,11 +369,11 @@ __device__ __forceinline__ void bw2_main(const float* Cb, const float* Sb, int n
   constexpr int CG = kT / TQ;           // channel groups: 8 (TQ 16) or 16 (TQ 8)
   constexpr int CPT = kCB / CG;         // channels per thread: 8 or 4
   const int tid = threadIdx.x, cg = tid % CG, rg = tid / CG;
-  float acc[L][CPT];
+  float2 acc[L][CPT / 2];
 #pragma unroll
   for (int l = 0; l < L; ++l)
 #pragma unroll
-    for (int i = 0; i < CPT; ++i) acc[l][i] = 0.f;
+    for (int i = 0; i < CPT / 2; ++i) acc[l][i] = make_float2(0.f, 0.f);
 #pragma unroll 2
   for (int p = 0; p < n; ++p) {
     const float4 a0 = *reinterpret_cast<const float4*>(Cb + (p * TQ + rg) * 8);
@@ -361,16 +391,17 @@ __device__ __forceinline__ void bw2_main(const float* Cb, const float* Sb, int n
 #pragma unroll
     for (int l = 0; l < L; ++l)
 #pragma unroll
-      for (int i = 0; i < CPT; ++i) acc[l][i] = fmaf(av[l], bv[i], acc[l][i]);
+      for (int i = 0; i < CPT / 2; ++i) acc[l][i] = ffma2(av[l], make_float2(bv[2 * i], bv[2 * i + 1]), acc[l][i]);
   }
   __syncthreads();  // every Cb read done: QB aliases it
 #pragma unroll
   for (int l = 0; l < L; ++l) {
     float* row = QB + (rg * L + l) * kCB;
-    *reinterpret_cast<float4*>(row + cg * 4) = make_float4(acc[l][0], acc[l][1], acc[l][2], acc[l][3]);
+    *reinterpret_cast<float4*>(row + cg * 4) = make_float4(acc[l][0].x, acc[l][0].y, acc[l][1].x, acc[l][1].y);
     if (CPT == 8)
       *reinterpret_cast<float4*>(row + 32 + cg * 4) =
-          make_float4(acc[l][4 % CPT], acc[l][5 % CPT], acc[l][6 % CPT], acc[l][7 % CPT]);
+          make_float4(acc[l][2 % (CPT / 2)].x, acc[l][2 % (CPT / 2)].y, acc[l][3 % (CPT / 2)].x,
+                      acc[l][3 % (CPT / 2)].y);
   }
 }
 
@@ -397,11 +428,13 @@ bw2_kernel(const int64_t* __restrict__ edge_ptr, const int32_t* __restrict__ rev
     const int kl = i / kCB, cc = i - kl * kCB;
     Wsm[i] = c0 + cc < dg ? W[kl * dg + c0 + cc] : 0.f;
   }
-  float wb[K][L];
+  static_assert(K % 2 == 0, "K pairs");
+  constexpr int KP = K / 2;
+  float2 wb[KP][L];  // W_bar[2 kp, l], W_bar[2 kp + 1, l]
 #pragma unroll
-  for (int k = 0; k < K; ++k)
+  for (int k = 0; k < KP; ++k)
 #pragma unroll
-    for (int l = 0; l < L; ++l) wb[k][l] = 0.f;
+    for (int l = 0; l < L; ++l) wb[k][l] = make_float2(0.f, 0.f);
   for (int64_t j = blockIdx.x; j < nv; j += gridDim.x) {
     const int64_t off = edge_ptr[j];
     const int n = static_cast<int>(edge_ptr[j + 1] - off);
@@ -456,35 +489,40 @@ bw2_kernel(const int64_t* __restrict__ edge_ptr, const int32_t* __restrict__ rev
       else bw2_main<L, 16>(Cb, Sb, n, Cb);
       __syncthreads();
       // epilogue: thread (c, h) takes rows h, h + 2, ... of the batch
-      float wr[K][L];
+      float2 wr[KP][L];
 #pragma unroll
-      for (int k = 0; k < K; ++k)
+      for (int k = 0; k < KP; ++k)
 #pragma unroll
-        for (int l = 0; l < L; ++l) wr[k][l] = Wsm[(k * L + l) * kCB + c];
+        for (int l = 0; l < L; ++l)
+          wr[k][l] = make_float2(Wsm[(2 * k * L + l) * kCB + c], Wsm[((2 * k + 1) * L + l) * kCB + c]);
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
         const int r = h + 2 * i;
         if (r >= nr) break;
         const int q = qb0 + r;
         const float d = Us[q].w;
-        float rb[K], v[K];
+        float rb[K];
+        float2 v2[KP], rb2[KP];
 #pragma unroll
-        for (int k = 0; k < K; ++k) {
-          rb[k] = Rb[q * K + k];
-          v[k] = 0.f;
+        for (int k = 0; k < K; ++k) rb[k] = Rb[q * K + k];
+#pragma unroll
+        for (int k = 0; k < KP; ++k) {
+          rb2[k] = make_float2(rb[2 * k], rb[2 * k + 1]);
+          v2[k] = make_float2(0.f, 0.f);
         }
         float qv[L];
 #pragma unroll
         for (int l = 0; l < L; ++l) qv[l] = Cb[(r * L + l) * kCB + c];
 #pragma unroll
-        for (int k = 0; k < K; ++k)
+        for (int k = 0; k < KP; ++k)
 #pragma unroll
-          for (int l = 0; l < L; ++l) v[k] = fmaf(qv[l], wr[k][l], v[k]);
+          for (int l = 0; l < L; ++l) v2[k] = ffma2(qv[l], wr[k][l], v2[k]);
         float xb = 0.f, ds = 0.f;
 #pragma unroll
         for (int k = 0; k < K; ++k) {
-          xb = fmaf(rb[k], v[k], xb);
-          ds = fmaf(-2.f * rp.gamma * (d - rp.step * k) * rb[k], v[k], ds);
+          const float vk = (k & 1) ? v2[k >> 1].y : v2[k >> 1].x;
+          xb = fmaf(rb[k], vk, xb);
+          ds = fmaf(-2.f * rp.gamma * (d - rp.step * k) * rb[k], vk, ds);
         }
         if (cok) Xbar[static_cast<int64_t>(rev[off + q]) * dg + c0 + c] = xb;
         const float x = xo[i];
@@ -492,7 +530,7 @@ bw2_kernel(const int64_t* __restrict__ edge_ptr, const int32_t* __restrict__ rev
         for (int l = 0; l < L; ++l) {
           const float rbar = qv[l] * x;
 #pragma unroll
-          for (int k = 0; k < K; ++k) wb[k][l] = fmaf(rb[k], rbar, wb[k][l]);
+          for (int k = 0; k < KP; ++k) wb[k][l] = ffma2(rbar, rb2[k], wb[k][l]);
         }
         float dd = ds * x;
 #pragma unroll
@@ -502,7 +540,7 @@ bw2_kernel(const int64_t* __restrict__ edge_ptr, const int32_t* __restrict__ rev
       __syncthreads();
       if (tid < nr) {
         const float dd = DD[tid * 2] + DD[tid * 2 + 1];
-        if (gridDim.y == 1) edge_grad[off + qb0 + tid].w += dd;  // single channel block: final value
+        if (gridDim.y == 1) reinterpret_cast<float*>(edge_grad + off + qb0 + tid)[3] += dd;  // final value
         else dd_part[blockIdx.y * num_edges + off + qb0 + tid] = dd;
       }
     }
@@ -512,17 +550,23 @@ bw2_kernel(const int64_t* __restrict__ edge_ptr, const int32_t* __restrict__ rev
   __syncthreads();
   if (h == 1) {
 #pragma unroll
-    for (int k = 0; k < K; ++k)
+    for (int k = 0; k < KP; ++k)
 #pragma unroll
-      for (int l = 0; l < L; ++l) Cb[(k * L + l) * kCB + c] = wb[k][l];
+      for (int l = 0; l < L; ++l) {
+        Cb[(2 * k * L + l) * kCB + c] = wb[k][l].x;
+        Cb[((2 * k + 1) * L + l) * kCB + c] = wb[k][l].y;
+      }
   }
   __syncthreads();
   if (h == 0) {
     float* dst = wbar_part + (static_cast<int64_t>(blockIdx.y) * gridDim.x + blockIdx.x) * (K * L * kCB);
 #pragma unroll
-    for (int k = 0; k < K; ++k)
+    for (int k = 0; k < KP; ++k)
 #pragma unroll
-      for (int l = 0; l < L; ++l) dst[(k * L + l) * kCB + c] = wb[k][l] + Cb[(k * L + l) * kCB + c];
+      for (int l = 0; l < L; ++l) {
+        dst[(2 * k * L + l) * kCB + c] = wb[k][l].x + Cb[(2 * k * L + l) * kCB + c];
+        dst[((2 * k + 1) * L + l) * kCB + c] = wb[k][l].y + Cb[((2 * k + 1) * L + l) * kCB + c];
+      }
   }
 }
 
@@ -560,7 +604,7 @@ __global__ void add_dd_kernel(const int64_t* __restrict__ edge_ptr, int64_t nv, 
     for (int64_t e = e0; e < e1; ++e) {
       float s = 0.f;
       for (int b = 0; b < ncb; ++b) s += dd_part[b * ne + e];
-      edge_grad[e].w += s;
+      reinterpret_cast<float*>(edge_grad + e)[3] += s;  // .w only (see bw1)
     }
   }
 }
@@ -587,11 +631,13 @@ int64_t fast_bwd_workspace_bytes(int64_t nv, int64_t ne, int K, int L, int dg) {
   return (ncb * gx * K * L * fast::kCB + ncb * std::max<int64_t>(ne, 1)) * 4;
 }
 
+// phases: 1 = bw1 (the angle adjoint: edge_grad.xyz), 2 = bw2 + reductions (X_bar, W_bar,
+// edge_grad.w), 3 = both.  The two touch disjoint outputs, so they may run on two streams.
 int fast_bwd(const int64_t* edge_ptr, const int32_t* rev, const float4* geo, int64_t nv, int64_t ne,
              const float* X, const float* W, int K, int L, int dg, RbfParams rp, const float* Sbar, float* Xbar,
-             float* Wbar, float4* edge_grad, void* ws, cudaStream_t st) {
+             float* Wbar, float4* edge_grad, void* ws, cudaStream_t st, int phases) {
   const int ncb = (dg + fast::kCB - 1) / fast::kCB;
-  {
+  if (phases & 1) {
     auto kern = fast::bw1_kernel<6, 7>;
     const int grid = static_cast<int>(std::min<int64_t>(nv, 1 << 30));
     const size_t smem1 = (4 * fast::kN + ((fast::kN * 6 + 3) & ~3) + fast::kQC * 7 * fast::kSbStride +
@@ -605,6 +651,7 @@ int fast_bwd(const int64_t* edge_ptr, const int32_t* rev, const float4* geo, int
     kern<<<grid, fast::kT, smem1, st>>>(edge_ptr, rev, geo, nv, X, W, dg, rp, Sbar, edge_grad);
     if (check_launch("triplet_bw1_fast")) return 1;
   }
+  if (!(phases & 2)) return 0;
   const int gx = static_cast<int>(std::min<int64_t>(nv, static_cast<int64_t>(kNumSMs) * 3));
   float* wpart = reinterpret_cast<float*>(ws);
   float* ddpart = wpart + static_cast<int64_t>(ncb) * gx * K * L * fast::kCB;

@@ -185,7 +185,7 @@ class Engine:
 
     def _side_stream(self, bg, index: int = 0):
         """Side stream `index` of this host thread (0: weight gradients and graph-level work,
-        1: the node-level adjoint chain), or None: EGN_WGRAD_STREAM=0, or a batch below
+        1: the node-level adjoint chain, 2: the triplet angle adjoint), or None: EGN_WGRAD_STREAM=0, or a batch below
         EGN_SIDE_MIN_EDGES edges (default 16384), whose kernels are too short for the
         fork / join to pay in an eagerly launched step (relaxation of one small system)."""
         device = bg.device
@@ -345,6 +345,11 @@ class Engine:
         main = torch.cuda.current_stream() if bg.device.type == "cuda" else None
         side = self._side_stream(bg)
         side2 = self._side_stream(bg, 1)
+        # the angle adjoint of the triplet interaction (edge_grad x, y, z) feeds only the final
+        # positions adjoint: it runs on a third stream, overlapping the rest of the backward,
+        # and is joined before the first later writer of edge_grad (rbf_bwd)
+        angle = self._side_stream(bg, 2) if not c.basis_code else None
+        angle_keep = []
         pending = []
 
         def wg(g, x, out, bias_out=None):
@@ -468,8 +473,15 @@ class Engine:
                                    g2=g_prod[1])
             if side is not None:
                 pending.append(g_prod)
+            if angle is not None:
+                angle.wait_stream(main)
+                with torch.cuda.stream(angle):
+                    ops.triplet_bwd(bg.edge_ptr, bg.rev, bg.geo, st["X"], st["Wk"], c.cutoff, S_bar, eg,
+                                    max_degree=bg.max_deg, phases=1)
+                angle_keep.append(S_bar)  # read on the angle stream: alive until the join
             X_bar, Wk_bar = ops.triplet_bwd(bg.edge_ptr, bg.rev, bg.geo, st["X"], st["Wk"], c.cutoff,
-                                            S_bar, eg, max_degree=bg.max_deg, basis=c.basis_code)
+                                            S_bar, eg, max_degree=bg.max_deg, basis=c.basis_code,
+                                            phases=2 if angle is not None else 3)
             if gem:
                 # wp_bar[c, kl] = Wk_bar[kl, c]: read transposed in place
                 wkb = Wk_bar.view(-1, Wk_bar.shape[2])
@@ -495,6 +507,9 @@ class Engine:
             ops.small_gemms(post)
         # edge init (engine.py:109-111), K = k_rbf
         ops.rbf_linear_bwd(fw.rbf, w["edge_init.w"], m_bar, rbf_bar, gr["edge_init.w"], gr["edge_init.b"])
+        if angle is not None:
+            main.wait_stream(angle)
+            angle_keep.clear()
         ops.rbf_bwd(bg.geo, rbf_bar, c.cutoff, eg, c.basis_code)
         pos_bar = ops.positions_bwd(bg.edge_ptr, bg.rev, bg.geo, eg)
         if side is not None:

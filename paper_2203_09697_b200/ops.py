@@ -288,7 +288,10 @@ def _workspace(nbytes: int, device) -> torch.Tensor:
 
 
 def triplet_bwd(edge_ptr, rev, geo, X, Wk, cutoff, S_bar, edge_grad, X_bar=None, W_bar=None, max_degree=None,
-                basis=0):
+                basis=0, phases=3):
+    """Adjoint of triplet_fwd (egn_triplet_bwd).  phases (egn_triplet_bwd_ex): 1 = the angle
+    adjoint only (edge_grad x, y, z of the small-degree centres; returns (None, None)), 2 = the
+    rest, 3 = all.  Phases 1 and 2 write disjoint outputs and may run on two streams."""
     X = _c(X, torch.float32)
     Wk = _c(Wk, torch.float32)
     S_bar = _c(S_bar, torch.float32)
@@ -300,19 +303,33 @@ def triplet_bwd(edge_ptr, rev, geo, X, Wk, cutoff, S_bar, edge_grad, X_bar=None,
         W_bar = torch.empty_like(Wk)
     if max_degree is None:
         max_degree = int((edge_ptr[1:] - edge_ptr[:-1]).max().item()) if nv else 0
+    if basis and phases != 3:  # the Bessel bases run one adjoint kernel chain
+        if phases == 1:
+            return None, None
+        phases = 3
     if dg > MAX_TRIPLET_WIDTH:
         for c0, c1 in _channel_chunks(dg):
             xb, wb = triplet_bwd(edge_ptr, rev, geo, X[:, c0:c1].contiguous(), Wk[:, :, c0:c1].contiguous(), cutoff,
-                                 S_bar[:, c0:c1].contiguous(), edge_grad, max_degree=max_degree, basis=basis)
-            X_bar[:, c0:c1] = xb
-            W_bar[:, :, c0:c1] = wb
-        return X_bar, W_bar
+                                 S_bar[:, c0:c1].contiguous(), edge_grad, max_degree=max_degree, basis=basis,
+                                 phases=phases)
+            if phases != 1:
+                X_bar[:, c0:c1] = xb
+                W_bar[:, :, c0:c1] = wb
+        return (None, None) if phases == 1 else (X_bar, W_bar)
     ne = X.shape[0]
+    if phases == 1:  # no workspace, no X_bar / W_bar writes
+        call("egn_triplet_bwd_ex", ptr(edge_ptr), ptr(rev), ptr(geo), nv, ne, int(max_degree), ptr(X), ptr(Wk), k, l,
+             dg, float(cutoff), ptr(S_bar), None, None, ptr(edge_grad), 1, None, stream())
+        return None, None
     nbytes = call("egn_triplet_bwd_workspace_bytes", nv, ne, int(max_degree), k, l, dg)
     ws = _workspace(nbytes, X.device)
     if basis:
         call("egn_triplet_bwd_basis", ptr(edge_ptr), ptr(rev), ptr(geo), nv, ne, int(max_degree), ptr(X), ptr(Wk), k,
              l, dg, float(cutoff), int(basis), ptr(S_bar), ptr(X_bar), ptr(W_bar), ptr(edge_grad), ptr(ws), stream())
+        return X_bar, W_bar
+    if phases == 2:
+        call("egn_triplet_bwd_ex", ptr(edge_ptr), ptr(rev), ptr(geo), nv, ne, int(max_degree), ptr(X), ptr(Wk), k, l,
+             dg, float(cutoff), ptr(S_bar), ptr(X_bar), ptr(W_bar), ptr(edge_grad), 2, ptr(ws), stream())
         return X_bar, W_bar
     call("egn_triplet_bwd", ptr(edge_ptr), ptr(rev), ptr(geo), nv, ne, int(max_degree), ptr(X), ptr(Wk), k, l, dg,
          float(cutoff), ptr(S_bar), ptr(X_bar), ptr(W_bar), ptr(edge_grad), ptr(ws), stream())

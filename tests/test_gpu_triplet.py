@@ -256,3 +256,37 @@ def test_graph_mlp_vs_fp64(g, dv, du):
     for got, ref in ((s_bar, pb @ w1d), (gw1, pb.t() @ sd), (gb1, pb.sum(0)), (gw2, ub.t() @ act_r),
                      (gb2, ub.sum(0))):
         assert max_rel(got.cpu().numpy(), ref.cpu().numpy()) < 1e-5
+
+
+@pytest.mark.parametrize("n,density,dg,mode", [(40, 0.06, 64, 0), (300, 0.9, 64, 0), (40, 0.06, 320, 0),
+                                                (40, 0.06, 64, 2)])
+def test_triplet_bwd_phases_match_single_call(n, density, dg, mode):
+    """egn_triplet_bwd_ex: the angle phase (1) and the rest (2), run on two streams, give the
+    bit-identical X_bar, W_bar and edge_grad of the single call (3); includes centres above the
+    small-degree range (dense cloud), a width above 256 (channel chunks) and the pairwise path."""
+    from paper_2203_09697_b200 import _lib, ops
+    from paper_2203_09697_b200.graph import build_batch
+
+    rng = np.random.default_rng(n + dg)
+    pos, _ = O.random_cloud(n, density, rng)
+    old = _lib.call("egn_triplet_path", mode)
+    try:
+        bg = build_batch([pos], 6.0)
+        X = torch.randn((bg.num_edges, dg), device="cuda")
+        W = torch.randn((6, 7, dg), device="cuda") / 6.5
+        Sb = torch.randn((bg.num_edges, dg), device="cuda")
+        eg0 = torch.randn((bg.num_edges, 4), device="cuda")
+        eg1 = eg0.clone()
+        xb, wb = ops.triplet_bwd(bg.edge_ptr, bg.rev, bg.geo, X, W, 6.0, Sb, eg0, max_degree=bg.max_deg)
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            assert ops.triplet_bwd(bg.edge_ptr, bg.rev, bg.geo, X, W, 6.0, Sb, eg1, max_degree=bg.max_deg,
+                                   phases=1) == (None, None)
+        xb2, wb2 = ops.triplet_bwd(bg.edge_ptr, bg.rev, bg.geo, X, W, 6.0, Sb, eg1, max_degree=bg.max_deg, phases=2)
+        torch.cuda.current_stream().wait_stream(side)
+        torch.cuda.synchronize()
+    finally:
+        _lib.call("egn_triplet_path", old)
+    assert torch.equal(xb, xb2) and torch.equal(wb, wb2)
+    assert torch.equal(eg0, eg1)
