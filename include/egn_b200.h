@@ -174,11 +174,16 @@ int egn_triplet_fwd(const int64_t* edge_ptr, const int32_t* rev, const float* ge
  * u(d_kj/c) j_l(z_lk d_kj / c) x Y_l0(angle)); the radial Bessel basis is
  * e_k(d) = sqrt(2/c) u(d/c) sin((k+1) pi d/c) with the polynomial envelope u (p = 6).  Bases 1
  * and 2 run the spherical-harmonic kernels (k_rbf = 6, l_sbf = 7) and need max_degree and the
- * workspace of egn_triplet_fwd_basis_workspace_bytes / egn_triplet_bwd_workspace_bytes. */
-int64_t egn_triplet_fwd_basis_workspace_bytes(int64_t num_nodes, int max_degree, int k_rbf, int l_sbf, int dg);
+ * workspace of egn_triplet_fwd_basis_workspace_bytes / egn_triplet_bwd_basis_workspace_bytes
+ * (which includes the per-call radial table of the edges: the Bessel rows depend on the
+ * geometry only and are tabulated once, one thread per element, instead of per lane). */
+int64_t egn_triplet_fwd_basis_workspace_bytes(int64_t num_nodes, int64_t num_edges, int max_degree, int k_rbf,
+                                              int l_sbf, int dg, int basis);
+int64_t egn_triplet_bwd_basis_workspace_bytes(int64_t num_nodes, int64_t num_edges, int max_degree, int k_rbf,
+                                              int l_sbf, int dg, int basis);
 int egn_triplet_fwd_basis(const int64_t* edge_ptr, const int32_t* rev, const float* geo, int64_t num_nodes,
-                          int max_degree, const float* X, const float* W, int k_rbf, int l_sbf, int dg, double cutoff,
-                          int basis, float* S, void* workspace, egn_stream_t stream);
+                          int64_t num_edges, int max_degree, const float* X, const float* W, int k_rbf, int l_sbf,
+                          int dg, double cutoff, int basis, float* S, void* workspace, egn_stream_t stream);
 int egn_triplet_bwd_basis(const int64_t* edge_ptr, const int32_t* rev, const float* geo, int64_t num_nodes,
                           int64_t num_edges, int max_degree, const float* X, const float* W, int k_rbf, int l_sbf,
                           int dg, double cutoff, int basis, const float* S_bar, float* X_bar, float* W_bar,

@@ -560,12 +560,15 @@ bool sh_supported(int K, int L, int dg);
 int64_t sh_fwd_workspace_bytes(int64_t nv, int max_degree, int K, int L, int dg);
 int sh_fwd(const int64_t* edge_ptr, const int32_t* rev, const float4* geo, int64_t nv, int max_degree, const float* X,
            const float* W, int K, int L, int dg, RbfParams rp, float cutoff, int mode, float* S, void* ws, int min_n,
-           cudaStream_t st);
+           cudaStream_t st, const float* rtab = nullptr);
 int64_t sh_bwd_workspace_bytes(int64_t nv, int64_t ne, int max_degree, int K, int L, int dg);
+int64_t sh_radial_table_floats(int64_t ne, int mode);
+int sh_radial_table(const float4* geo, int64_t ne, float cutoff, int mode, float* tab, float* dtab, cudaStream_t st);
 int sh_bwd(const int64_t* edge_ptr, const int32_t* rev, const float4* geo, int64_t nv, int64_t ne, int max_degree,
            const float* X, const float* W, int K, int L, int dg, RbfParams rp, float cutoff, int mode,
            const float* Sbar, float* Xbar, float* Wbar, float4* edge_grad, void* ws, int min_n, int accumulate,
-           cudaStream_t st);
+           cudaStream_t st, const float* rtab = nullptr,
+           const float* drtab = nullptr);
 
 // Path selection (egn_triplet_path): 0 = auto (deg <= 64: pairwise centre tiles; larger centres:
 // the linear-in-degree spherical-harmonic kernels), 1 = spherical-harmonic kernels for every
@@ -698,9 +701,22 @@ static int check_dims(int K, int L, int dg) {
 
 extern "C" {
 
-int64_t egn_triplet_fwd_basis_workspace_bytes(int64_t num_nodes, int max_degree, int k_rbf, int l_sbf, int dg) {
-  return sh_supported(k_rbf, l_sbf, dg) && max_degree >= 0 ? sh_fwd_workspace_bytes(num_nodes, max_degree, k_rbf, l_sbf, dg)
-                                                           : 0;
+static int64_t align256(int64_t b) { return (b + 255) / 256 * 256; }
+
+int64_t egn_triplet_fwd_basis_workspace_bytes(int64_t num_nodes, int64_t num_edges, int max_degree, int k_rbf,
+                                              int l_sbf, int dg, int basis) {
+  if (basis == 0) return egn_triplet_fwd_workspace_bytes(num_nodes, max_degree, k_rbf, l_sbf, dg);
+  if (!sh_supported(k_rbf, l_sbf, dg) || max_degree < 0) return 0;
+  // per-chunk moments, then the edges' radial table
+  return align256(sh_fwd_workspace_bytes(num_nodes, max_degree, k_rbf, l_sbf, dg)) +
+         sh_radial_table_floats(num_edges, basis) * 4;
+}
+
+int64_t egn_triplet_bwd_basis_workspace_bytes(int64_t num_nodes, int64_t num_edges, int max_degree, int k_rbf,
+                                              int l_sbf, int dg, int basis) {
+  const int64_t b = egn_triplet_bwd_workspace_bytes(num_nodes, num_edges, max_degree, k_rbf, l_sbf, dg);
+  if (basis == 0) return b;
+  return align256(b) + 2 * align256(sh_radial_table_floats(num_edges, basis) * 4);  // radial values, d-derivatives
 }
 
 int64_t egn_triplet_fwd_workspace_bytes(int64_t num_nodes, int max_degree, int k_rbf, int l_sbf, int dg) {
@@ -846,8 +862,8 @@ int egn_triplet_path(int mode) {
 // d_kj x Y_l0(angle)), 2 = DimeNet SBF (sqrt(2/c^3)/|j_{l+1}(z_ln)| u(d/c) j_l(z_ln d/c) Y_l0(angle));
 // the spherical-harmonic kernels for every centre (their A table absorbs the Y_l0 normalisation)
 int egn_triplet_fwd_basis(const int64_t* edge_ptr, const int32_t* rev, const float* geo, int64_t num_nodes,
-                          int max_degree, const float* X, const float* W, int k_rbf, int l_sbf, int dg, double cutoff,
-                          int basis, float* S, void* workspace, egn_stream_t stream) {
+                          int64_t num_edges, int max_degree, const float* X, const float* W, int k_rbf, int l_sbf,
+                          int dg, double cutoff, int basis, float* S, void* workspace, egn_stream_t stream) {
   if (basis == 0)
     return egn_triplet_fwd(edge_ptr, rev, geo, num_nodes, max_degree, X, W, k_rbf, l_sbf, dg, cutoff, S, workspace,
                            stream);
@@ -856,8 +872,13 @@ int egn_triplet_fwd_basis(const int64_t* edge_ptr, const int32_t* rev, const flo
   EGN_REQUIRE(sh_supported(k_rbf, l_sbf, dg), "the bessel bases need k_rbf = 6, l_sbf = 7");
   EGN_REQUIRE(max_degree >= 0 && workspace != nullptr, "the bessel bases need max_degree and a workspace");
   if (num_nodes == 0) return 0;
-  return sh_fwd(edge_ptr, rev, reinterpret_cast<const float4*>(geo), num_nodes, max_degree, X, W, k_rbf, l_sbf, dg,
-                rbf_params(k_rbf, cutoff), static_cast<float>(cutoff), basis, S, workspace, 0, as_stream(stream));
+  cudaStream_t st = as_stream(stream);
+  const float4* g4 = reinterpret_cast<const float4*>(geo);
+  float* tab = reinterpret_cast<float*>(reinterpret_cast<char*>(workspace) +
+                                        align256(sh_fwd_workspace_bytes(num_nodes, max_degree, k_rbf, l_sbf, dg)));
+  if (int rc = sh_radial_table(g4, num_edges, static_cast<float>(cutoff), basis, tab, nullptr, st)) return rc;
+  return sh_fwd(edge_ptr, rev, g4, num_nodes, max_degree, X, W, k_rbf, l_sbf, dg, rbf_params(k_rbf, cutoff),
+                static_cast<float>(cutoff), basis, S, workspace, 0, st, tab);
 }
 
 int egn_triplet_bwd_basis(const int64_t* edge_ptr, const int32_t* rev, const float* geo, int64_t num_nodes,
@@ -878,9 +899,15 @@ int egn_triplet_bwd_basis(const int64_t* edge_ptr, const int32_t* rev, const flo
   }
   char* sws = reinterpret_cast<char*>(workspace) + generic_ws_bytes(num_nodes, k_rbf, l_sbf, dg) +
               fast_ws_bytes(num_nodes, num_edges, k_rbf, l_sbf, dg) + tc_bwd_workspace_bytes(num_nodes, k_rbf, l_sbf);
-  return sh_bwd(edge_ptr, rev, reinterpret_cast<const float4*>(geo), num_nodes, num_edges, max_degree, X, W, k_rbf,
-                l_sbf, dg, rbf_params(k_rbf, cutoff), static_cast<float>(cutoff), basis, S_bar, X_bar, W_bar,
-                reinterpret_cast<float4*>(edge_grad), sws, 0, 0, st);
+  const float4* g4 = reinterpret_cast<const float4*>(geo);
+  char* tb = reinterpret_cast<char*>(workspace) +
+             align256(egn_triplet_bwd_workspace_bytes(num_nodes, num_edges, max_degree, k_rbf, l_sbf, dg));
+  float* tab = reinterpret_cast<float*>(tb);
+  float* dtab = reinterpret_cast<float*>(tb + align256(sh_radial_table_floats(num_edges, basis) * 4));
+  if (int rc = sh_radial_table(g4, num_edges, static_cast<float>(cutoff), basis, tab, dtab, st)) return rc;
+  return sh_bwd(edge_ptr, rev, g4, num_nodes, num_edges, max_degree, X, W, k_rbf, l_sbf, dg, rbf_params(k_rbf, cutoff),
+                static_cast<float>(cutoff), basis, S_bar, X_bar, W_bar, reinterpret_cast<float4*>(edge_grad), sws, 0,
+                0, st, tab, dtab);
 }
 
 int egn_triplet_fwd_window(const int64_t* edge_ptr, const int32_t* rev, const float* geo, int64_t num_nodes,

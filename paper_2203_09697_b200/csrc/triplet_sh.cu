@@ -216,6 +216,102 @@ __device__ __forceinline__ float radv(const float* row, int k, int j) {
   return row[k];
 }
 
+// j_l(x) and j_l'(x) in fp32 (table entries only; the oracle's fp64 values are matched to
+// ~1e-6 relative): ascending series for x <= l + 1 (where the upward recurrence loses digits),
+// else the upward recurrence from j_0, j_1, which also gives j_{l-1} for the derivative
+// j_l' = j_{l-1} - (l + 1) j_l / x  (j_0' = -j_1).
+__device__ __forceinline__ float sph_series(int l, float x) {
+  float term = 1.f;
+  for (int i = 1; i <= l; ++i) term *= x / (2 * i + 1);
+  float sum = term;
+  const float h = -0.5f * x * x;
+  // x <= l + 1 <= 8: 18 terms reach fp32 round-off for every l < 8
+#pragma unroll
+  for (int k = 1; k <= 18; ++k) {
+    term *= __fdividef(h, k * (2.f * l + 2.f * k + 1.f));
+    sum += term;
+  }
+  return sum;
+}
+__device__ __forceinline__ void sph_jl_pair(int l, float x, float& j, float& dj) {
+  if (x <= l + 1.f) {
+    j = sph_series(l, x);
+    dj = l == 0 ? -sph_series(1, x) : sph_series(l - 1, x) - (l + 1) * j / x;
+    return;
+  }
+  float sn, cs;
+  sincosf(x, &sn, &cs);
+  const float inv = 1.f / x;
+  float jm = sn * inv, jc = (sn * inv - cs) * inv;  // j_0, j_1
+  if (l == 0) {
+    j = jm;
+    dj = -jc;
+    return;
+  }
+  for (int i = 1; i < l; ++i) {
+    const float jn = (2 * i + 1) * inv * jc - jm;
+    jm = jc;
+    jc = jn;
+  }
+  j = jc;
+  dj = jm - (l + 1) * jc * inv;
+}
+
+// Element i of an edge's radial row (MODE 1 / 2, layout of radial_row) and its d-derivative.
+// The Bessel rows depend on the geometry only, so for MODE 1 / 2 they are tabulated once per
+// call by radial_table_kernel (one thread per element) and the triplet kernels copy rows from
+// the table instead of evaluating the Bessel functions per lane.
+template <int K, int L, int MODE>
+__device__ __forceinline__ void radial_elem(float d, float cutoff, int i, float& v, float& dv) {
+  const float x = d / cutoff;
+  double ud, dud;
+  envelope6(x, ud, dud);
+  const float u = static_cast<float>(ud), du = static_cast<float>(dud);
+  v = dv = 0.f;
+  if constexpr (MODE == 1) {
+    if (i >= K) return;
+    const float nrm = sqrtf(2.f / cutoff);
+    float sn, cs;
+    sincospif((i + 1) * x, &sn, &cs);
+    v = nrm * u * sn;
+    dv = nrm * (du * sn + u * (i + 1) * 3.14159265358979323846f * cs) / cutoff;
+  } else {
+    if (i >= K * L) return;
+    const int k = i / L, l = i - k * L;
+    const float z = static_cast<float>(c_sbf.z[l][k]);
+    float j, dj;
+    sph_jl_pair(l, z * x, j, dj);
+    const float f = static_cast<float>(sqrt(2.0 / (static_cast<double>(cutoff) * cutoff * cutoff)) * c_sbf.jinv[l][k]);
+    v = f * u * j;
+    dv = f * (du * j + u * dj * z) / cutoff;
+  }
+}
+
+template <int K, int L, int MODE>
+__global__ void __launch_bounds__(256) radial_table_kernel(const float4* __restrict__ geo, int64_t ne, float cutoff,
+                                                           float* __restrict__ tab, float* __restrict__ dtab) {
+  constexpr int RS = rad_stride<MODE>();
+  const int64_t n = ne * RS;
+  for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < n;
+       idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t e = idx / RS;
+    const int i = static_cast<int>(idx - e * RS);
+    float v, dv;
+    radial_elem<K, L, MODE>(geo[e].w, cutoff, i, v, dv);
+    tab[idx] = v;
+    if (dtab) dtab[idx] = dv;
+  }
+}
+
+// row i of a tabulated radial table into shared memory (RS floats, 16-byte aligned rows)
+template <int MODE>
+__device__ __forceinline__ void copy_row(const float* __restrict__ tab, int64_t e, float* row) {
+  constexpr int RS = rad_stride<MODE>();
+  const float4* src = reinterpret_cast<const float4*>(tab + e * RS);
+#pragma unroll
+  for (int i = 0; i < RS / 4; ++i) reinterpret_cast<float4*>(row)[i] = __ldg(src + i);
+}
+
 // Y_jm(u) for j < L at index j*j + j + m (m in [-j, j]), written with stride `st`.
 // Recurrences: C_m + i S_m = (x + i y)^m; Q_j^m(z) = associated Legendre without (1-z^2)^(m/2).
 template <int L>
@@ -429,7 +525,8 @@ template <int K, int L, int T = kTile, int MODE = 0>
 __device__ __forceinline__ void stage_tile(float* wsm, const float4* __restrict__ geo, const int32_t* __restrict__ rev,
                                            int64_t off, int t0, int n, RbfParams rp, float cutoff, int lane,
                                            const float* __restrict__ X = nullptr, const float* __restrict__ Sbar = nullptr,
-                                           int dg = 0, int c = 0, bool cok = false, bool radial = true) {
+                                           int dg = 0, int c = 0, bool cok = false, bool radial = true,
+                                           const float* __restrict__ rtab = nullptr) {
   using SM = WarpSmem<K, L, T, MODE>;
   const int e = t0 + lane;
   int32_t rq = 0;
@@ -439,7 +536,10 @@ __device__ __forceinline__ void stage_tile(float* wsm, const float4* __restrict_
     reinterpret_cast<float4*>(wsm + SM::us)[lane] = g;
     reinterpret_cast<int32_t*>(wsm + SM::rq)[lane] = rq;
     sh_eval<L>(g.x, g.y, g.z, wsm + SM::ys + lane * kYS, 1);
-    if (radial) radial_row<K, L, MODE>(g.w, cutoff, rp, wsm + SM::rs + lane * rad_stride<MODE>(), nullptr);
+    if (radial) {  // MODE 1 / 2: rows of the per-call radial table (host guarantees rtab)
+      if constexpr (MODE != 0) copy_row<MODE>(rtab, off + e, wsm + SM::rs + lane * rad_stride<MODE>());
+      else radial_row<K, L, MODE>(g.w, cutoff, rp, wsm + SM::rs + lane * rad_stride<MODE>(), nullptr);
+    }
   }
   const int nt = min(T, n - t0);
   if (X) {
@@ -556,7 +656,7 @@ __global__ void __launch_bounds__(kW * 32, 3)
 fwd_moments_kernel(const int64_t* __restrict__ edge_ptr, const int32_t* __restrict__ rev,
                    const float4* __restrict__ geo, int64_t nv, int nch, const float* __restrict__ X,
                    const float* __restrict__ W, int dg, RbfParams rp, float cutoff, float* __restrict__ S,
-                   float* __restrict__ Mpart, int min_n) {
+                   float* __restrict__ Mpart, int min_n, const float* __restrict__ rtab) {
   using SM = WarpSmem<K, L, kTile, MODE>;
   constexpr int RS = rad_stride<MODE>();
   constexpr int J = L * L;
@@ -582,7 +682,8 @@ fwd_moments_kernel(const int64_t* __restrict__ edge_ptr, const int32_t* __restri
     for (int i = 0; i < J; ++i) M[i] = 0.f;
     for (int t0 = q.e0; t0 < q.e1; t0 += kTile) {
       __syncwarp();
-      stage_tile<K, L, kTile, MODE>(wsm, geo, rev, q.off, t0, q.e1, rp, cutoff, lane, X, nullptr, dg, q.c, q.cok);
+      stage_tile<K, L, kTile, MODE>(wsm, geo, rev, q.off, t0, q.e1, rp, cutoff, lane, X, nullptr, dg, q.c, q.cok, true,
+                                    rtab);
       const int nt = min(kTile, q.e1 - t0);
 #pragma unroll 1
       for (int t = 0; t < nt; ++t) {
@@ -721,7 +822,7 @@ __global__ void __launch_bounds__(kW * 32, 3)
 bwd_moments_kernel(const int64_t* __restrict__ edge_ptr, const int32_t* __restrict__ rev,
                    const float4* __restrict__ geo, int64_t nv, int nch, const float* __restrict__ X,
                    const float* __restrict__ W, int dg, RbfParams rp, float cutoff, const float* __restrict__ Sbar,
-                   float* __restrict__ Mpart, float* __restrict__ Mbpart, int min_n) {
+                   float* __restrict__ Mpart, float* __restrict__ Mbpart, int min_n, const float* __restrict__ rtab) {
   using SM = WarpSmem<K, L, kTile, MODE>;
   constexpr int RS = rad_stride<MODE>();
   constexpr int J = L * L;
@@ -749,7 +850,7 @@ bwd_moments_kernel(const int64_t* __restrict__ edge_ptr, const int32_t* __restri
         __syncwarp();
         // a single-tile chunk stages S_bar too and keeps the tile for the Mbar sweep
         stage_tile<K, L, kTile, MODE>(wsm, geo, rev, q.off, t0, q.e1, rp, cutoff, lane, X,
-                                      q.e1 - q.e0 > kTile ? nullptr : Sbar, dg, q.c, q.cok);
+                                      q.e1 - q.e0 > kTile ? nullptr : Sbar, dg, q.c, q.cok, true, rtab);
         const int nt = min(kTile, q.e1 - t0);
 #pragma unroll 1
         for (int t = 0; t < nt; ++t) {
@@ -818,13 +919,13 @@ struct BwdSmem {
 };
 
 template <int K, int L, int MODE>
-__global__ void __launch_bounds__(kW * 32, 3)
+__global__ void __launch_bounds__(kW * 32, MODE == 0 ? 3 : 2)  // the Bessel modes: no spills at 2 CTAs / SM
 bwd_apply_kernel(const int64_t* __restrict__ edge_ptr, const int32_t* __restrict__ rev,
                  const float4* __restrict__ geo, int64_t nv, int64_t ne, int nch, const float* __restrict__ X,
                  const float* __restrict__ W, int dg, RbfParams rp, float cutoff, const float* __restrict__ Sbar,
                  const float* __restrict__ Mpart, const float* __restrict__ Mbpart, float* __restrict__ Xbar,
                  float* __restrict__ wbar_part, float4* __restrict__ eg_part, float4* __restrict__ edge_grad,
-                 int min_n) {
+                 int min_n, const float* __restrict__ rtab, const float* __restrict__ drtab) {
   using SM = BwdSmem<K, L, MODE>;
   constexpr int J = L * L;
   constexpr int RS = SM::RS;
@@ -878,8 +979,12 @@ bwd_apply_kernel(const int64_t* __restrict__ edge_ptr, const int32_t* __restrict
           reinterpret_cast<int32_t*>(wsm + SM::rq)[lane] = rq;
           sh_eval<L>(g.x, g.y, g.z, wsm + SM::ys + lane * kYS, 1);
           sh_grad_table<L>(g.x, g.y, g.z, wsm + SM::gs + lane * kGS);
-          radial_row<K, L, MODE>(g.w, cutoff, rp, wsm + SM::rs + lane * RS,
-                                 MODE == 0 ? nullptr : wsm + SM::drs + lane * RS);
+          if constexpr (MODE != 0) {  // per-call radial table (values, d-derivatives)
+            copy_row<MODE>(rtab, q.off + e, wsm + SM::rs + lane * RS);
+            copy_row<MODE>(drtab, q.off + e, wsm + SM::drs + lane * RS);
+          } else {
+            radial_row<K, L, MODE>(g.w, cutoff, rp, wsm + SM::rs + lane * RS, nullptr);
+          }
         }
         const int nt = min(kBT, q.e1 - t0);
         float xv[kBT], sv[kBT];
@@ -1060,13 +1165,17 @@ __global__ void __launch_bounds__(1024) reduce_wbar_kernel(const float* __restri
   }
 }
 
-// edge_grad[e] += sum over channel blocks (fixed order) for the centres handled here
+// edge_grad[e] += sum over channel blocks (fixed order) for the centres handled here; one warp
+// per centre, lanes over its edges
 __global__ void add_eg_kernel(const int64_t* __restrict__ edge_ptr, int64_t nv, const float4* __restrict__ part,
                               int ncb, int64_t ne, int min_n, float4* __restrict__ edge_grad) {
-  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nv; v += (int64_t)gridDim.x * blockDim.x) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
+  const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t v = w0; v < nv; v += nw) {
     const int64_t e0 = edge_ptr[v], e1 = edge_ptr[v + 1];
     if (e1 - e0 < 2 || e1 - e0 <= min_n) continue;
-    for (int64_t e = e0; e < e1; ++e) {
+    for (int64_t e = e0 + lane; e < e1; e += 32) {
       float4 g = edge_grad[e];
       for (int b = 0; b < ncb; ++b) {
         const float4 p = part[b * ne + e];
@@ -1108,7 +1217,7 @@ static void set_smem(F kern, size_t smem, bool& configured) {
 template <int MODE>
 static int sh_fwd_mode(const int64_t* edge_ptr, const int32_t* rev, const float4* geo, int64_t nv, int nch,
                        const float* X, const float* W, int dg, RbfParams rp, float cutoff, float* S, float* Mpart,
-                       int min_n, cudaStream_t st) {
+                       int min_n, const float* rtab, cudaStream_t st) {
   using SM = sh::WarpSmem<6, 7, sh::kTile, MODE>;
   const int ncb = (dg + 31) / 32;
   const size_t smem = sizeof(float) * SM::fwd_total * sh::kW;
@@ -1118,7 +1227,7 @@ static int sh_fwd_mode(const int64_t* edge_ptr, const int32_t* rev, const float4
   set_smem(k1, smem, c1);
   set_smem(k2, smem, c2);
   const int grid = sh_grid(nv * nch * ncb);
-  k1<<<grid, sh::kW * 32, smem, st>>>(edge_ptr, rev, geo, nv, nch, X, W, dg, rp, cutoff, S, Mpart, min_n);
+  k1<<<grid, sh::kW * 32, smem, st>>>(edge_ptr, rev, geo, nv, nch, X, W, dg, rp, cutoff, S, Mpart, min_n, rtab);
   if (check_launch("triplet_fwd_sh_moments")) return 1;
   k2<<<grid, sh::kW * 32, smem, st>>>(edge_ptr, rev, geo, nv, nch, dg, rp, S, Mpart, min_n);
   return check_launch("triplet_fwd_sh_apply");
@@ -1126,12 +1235,26 @@ static int sh_fwd_mode(const int64_t* edge_ptr, const int32_t* rev, const float4
 
 int sh_fwd(const int64_t* edge_ptr, const int32_t* rev, const float4* geo, int64_t nv, int max_degree, const float* X,
            const float* W, int K, int L, int dg, RbfParams rp, float cutoff, int mode, float* S, void* ws, int min_n,
-           cudaStream_t st) {
+           cudaStream_t st, const float* rtab) {
   const int nch = sh_nch(max_degree);
   float* Mpart = reinterpret_cast<float*>(ws);
-  if (mode == 1) return sh_fwd_mode<1>(edge_ptr, rev, geo, nv, nch, X, W, dg, rp, cutoff, S, Mpart, min_n, st);
-  if (mode == 2) return sh_fwd_mode<2>(edge_ptr, rev, geo, nv, nch, X, W, dg, rp, cutoff, S, Mpart, min_n, st);
-  return sh_fwd_mode<0>(edge_ptr, rev, geo, nv, nch, X, W, dg, rp, cutoff, S, Mpart, min_n, st);
+  if (mode == 1) return sh_fwd_mode<1>(edge_ptr, rev, geo, nv, nch, X, W, dg, rp, cutoff, S, Mpart, min_n, rtab, st);
+  if (mode == 2) return sh_fwd_mode<2>(edge_ptr, rev, geo, nv, nch, X, W, dg, rp, cutoff, S, Mpart, min_n, rtab, st);
+  return sh_fwd_mode<0>(edge_ptr, rev, geo, nv, nch, X, W, dg, rp, cutoff, S, Mpart, min_n, nullptr, st);
+}
+
+// radial tables of the Bessel bases (MODE 1 / 2): [ne][rad_stride] values and (dtab != null)
+// d-derivatives
+int64_t sh_radial_table_floats(int64_t ne, int mode) {
+  return mode == 0 ? 0 : std::max<int64_t>(ne, 1) * (mode == 2 ? sh::rad_stride<2>() : sh::rad_stride<1>());
+}
+int sh_radial_table(const float4* geo, int64_t ne, float cutoff, int mode, float* tab, float* dtab, cudaStream_t st) {
+  if (mode == 0 || ne == 0) return 0;
+  const int64_t n = sh_radial_table_floats(ne, mode);
+  const int grid = static_cast<int>(std::min<int64_t>((n + 255) / 256, static_cast<int64_t>(kNumSMs) * 32));
+  if (mode == 1) sh::radial_table_kernel<6, 7, 1><<<grid, 256, 0, st>>>(geo, ne, cutoff, tab, dtab);
+  else sh::radial_table_kernel<6, 7, 2><<<grid, 256, 0, st>>>(geo, ne, cutoff, tab, dtab);
+  return check_launch("triplet_sh_radial_table");
 }
 
 static int64_t sh_bwd_warps(int64_t nv, int nch, int dg, int* grid_out) {
@@ -1158,7 +1281,7 @@ static int sh_bwd_mode(const int64_t* edge_ptr, const int32_t* rev, const float4
                        int nch, int grid, int64_t nw, const float* X, const float* W, int K, int L, int dg,
                        RbfParams rp, float cutoff, const float* Sbar, float* Xbar, float* Wbar, float4* edge_grad,
                        float* wpart, float* Mpart, float* Mbpart, float4* egp, int min_n, int accumulate,
-                       cudaStream_t st) {
+                       const float* rtab, const float* drtab, cudaStream_t st) {
   using SM = sh::WarpSmem<6, 7, sh::kTile, MODE>;
   const int ncb = (dg + 31) / 32;
   static bool c1 = false, c2 = false;
@@ -1169,22 +1292,23 @@ static int sh_bwd_mode(const int64_t* edge_ptr, const int32_t* rev, const float4
   set_smem(k1, smem1, c1);
   set_smem(k2, smem2, c2);
   k1<<<sh_grid(nv * nch * ncb), sh::kW * 32, smem1, st>>>(edge_ptr, rev, geo, nv, nch, X, W, dg, rp, cutoff, Sbar,
-                                                         Mpart, Mbpart, min_n);
+                                                         Mpart, Mbpart, min_n, rtab);
   if (check_launch("triplet_bwd_sh_moments")) return 1;
   k2<<<grid, sh::kW * 32, smem2, st>>>(edge_ptr, rev, geo, nv, ne, nch, X, W, dg, rp, cutoff, Sbar, Mpart, Mbpart,
-                                       Xbar, wpart, egp, edge_grad, min_n);
+                                       Xbar, wpart, egp, edge_grad, min_n, rtab, drtab);
   if (check_launch("triplet_bwd_sh_apply")) return 1;
   sh::reduce_wbar_kernel<6, 7, MODE><<<K * ncb, 1024, 0, st>>>(wpart, nw, ncb, dg, Wbar, accumulate);
   if (check_launch("triplet_bwd_sh_reduce")) return 1;
   if (ncb == 1) return 0;
-  sh::add_eg_kernel<<<grid_for(nv, 128), 128, 0, st>>>(edge_ptr, nv, egp, ncb, ne, min_n, edge_grad);
+  const int eg_grid = static_cast<int>(std::min<int64_t>((nv + 7) / 8, static_cast<int64_t>(kNumSMs) * 16));
+  sh::add_eg_kernel<<<std::max(eg_grid, 1), 256, 0, st>>>(edge_ptr, nv, egp, ncb, ne, min_n, edge_grad);
   return check_launch("triplet_bwd_sh_eg");
 }
 
 int sh_bwd(const int64_t* edge_ptr, const int32_t* rev, const float4* geo, int64_t nv, int64_t ne, int max_degree,
            const float* X, const float* W, int K, int L, int dg, RbfParams rp, float cutoff, int mode,
            const float* Sbar, float* Xbar, float* Wbar, float4* edge_grad, void* ws, int min_n, int accumulate,
-           cudaStream_t st) {
+           cudaStream_t st, const float* rtab, const float* drtab) {
   const int nch = sh_nch(max_degree);
   int grid;
   const int64_t nw = sh_bwd_warps(std::max<int64_t>(nv, 1), nch, dg, &grid);
@@ -1199,7 +1323,8 @@ int sh_bwd(const int64_t* edge_ptr, const int32_t* rev, const float4* geo, int64
   }
 #define EGN_SHB(M)                                                                                               \
   return sh_bwd_mode<M>(edge_ptr, rev, geo, nv, ne, nch, grid, nw, X, W, K, L, dg, rp, cutoff, Sbar, Xbar, Wbar, \
-                        edge_grad, wpart, Mpart, Mbpart, egp, min_n, accumulate, st)
+                        edge_grad, wpart, Mpart, Mbpart, egp, min_n, accumulate, M == 0 ? nullptr : rtab,        \
+                        M == 0 ? nullptr : drtab, st)
   if (mode == 1) EGN_SHB(1);
   if (mode == 2) EGN_SHB(2);
   EGN_SHB(0);

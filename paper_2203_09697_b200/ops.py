@@ -252,10 +252,11 @@ def triplet_fwd(edge_ptr, rev, geo, X, Wk, cutoff, max_degree=-1, basis=0):
     S = torch.empty_like(X)
     nv = edge_ptr.shape[0] - 1
     if basis:
-        nbytes = call("egn_triplet_fwd_basis_workspace_bytes", nv, int(max_degree), k, l, dg)
+        ne = X.shape[0]
+        nbytes = call("egn_triplet_fwd_basis_workspace_bytes", nv, ne, int(max_degree), k, l, dg, int(basis))
         ws = _workspace_named("tfwd", nbytes, X.device)
-        call("egn_triplet_fwd_basis", ptr(edge_ptr), ptr(rev), ptr(geo), nv, int(max_degree), ptr(X), ptr(Wk), k, l,
-             dg, float(cutoff), int(basis), ptr(S), ptr(ws), stream())
+        call("egn_triplet_fwd_basis", ptr(edge_ptr), ptr(rev), ptr(geo), nv, ne, int(max_degree), ptr(X), ptr(Wk), k,
+             l, dg, float(cutoff), int(basis), ptr(S), ptr(ws), stream())
         return S
     nbytes = call("egn_triplet_fwd_workspace_bytes", nv, int(max_degree), k, l, dg)
     ws = _workspace_named("tfwd", nbytes, X.device) if nbytes > 0 else None
@@ -321,7 +322,10 @@ def triplet_bwd(edge_ptr, rev, geo, X, Wk, cutoff, S_bar, edge_grad, X_bar=None,
         call("egn_triplet_bwd_ex", ptr(edge_ptr), ptr(rev), ptr(geo), nv, ne, int(max_degree), ptr(X), ptr(Wk), k, l,
              dg, float(cutoff), ptr(S_bar), None, None, ptr(edge_grad), 1, None, stream())
         return None, None
-    nbytes = call("egn_triplet_bwd_workspace_bytes", nv, ne, int(max_degree), k, l, dg)
+    if basis:
+        nbytes = call("egn_triplet_bwd_basis_workspace_bytes", nv, ne, int(max_degree), k, l, dg, int(basis))
+    else:
+        nbytes = call("egn_triplet_bwd_workspace_bytes", nv, ne, int(max_degree), k, l, dg)
     ws = _workspace(nbytes, X.device)
     if basis:
         call("egn_triplet_bwd_basis", ptr(edge_ptr), ptr(rev), ptr(geo), nv, ne, int(max_degree), ptr(X), ptr(Wk), k,

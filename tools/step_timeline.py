@@ -28,6 +28,7 @@ def main():
     ap.add_argument("--workload", default="gemnet-t-oc20")
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--eager", action="store_true")
+    ap.add_argument("--basis", default="gaussian")
     args = ap.parse_args()
     from torch.profiler import ProfilerActivity, profile
 
@@ -35,7 +36,7 @@ def main():
     from paper_2203_09697_b200.graph import build_batch
     from paper_2203_09697_b200.tasks import Trainer
 
-    wl = bench.WORKLOADS[args.workload]
+    wl = dict(bench.WORKLOADS[args.workload], basis=args.basis)
     cfg = bench._config(wl)
     systems = bench._systems(wl, wl["graphs"])
     bg = build_batch(systems, cfg.cutoff)
