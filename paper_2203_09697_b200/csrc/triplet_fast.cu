@@ -57,19 +57,23 @@ __device__ __forceinline__ void load_center(float4* Us, float* Rb, const float4*
 
 // Q chunk: rows (t, l) for t < nq (row stride RS floats), natural channel order; thread
 // (cq = tid & 63, half = tid >> 6)
-template <int K, int L, int RS = kCB>
-__device__ __forceinline__ void build_q(float* Qs, const float2 (&wreg)[K][kLP], const float* Rb,
-                                        const int32_t* __restrict__ rev, const float* __restrict__ X,
-                                        int64_t off, int q0, int nq, int dg, int c0) {
+// X rows of chunk [q0, q0 + nq) for this thread (t = half + 2 i): issued one chunk ahead, so
+// the gathers are in flight during the previous chunk's contraction
+__device__ __forceinline__ void load_x(float (&xs)[kQC / 2], const int32_t* __restrict__ rev,
+                                       const float* __restrict__ X, int64_t off, int q0, int nq, int dg, int c0) {
   const int cq = threadIdx.x & 63, half = threadIdx.x >> 6;
   const int c = c0 + cq;
-  // issue every gather of this chunk before any use (hides the L2/HBM latency once)
-  float xs[kQC / 2];
 #pragma unroll
   for (int i = 0; i < kQC / 2; ++i) {
     const int t = half + 2 * i;
     xs[i] = (t < nq && c < dg) ? __ldg(X + static_cast<int64_t>(rev[off + q0 + t]) * dg + c) : 0.f;
   }
+}
+
+template <int K, int L, int RS = kCB>
+__device__ __forceinline__ void build_q(float* Qs, const float2 (&wreg)[K][kLP], const float* Rb,
+                                        const float (&xs)[kQC / 2], int q0, int nq) {
+  const int cq = threadIdx.x & 63, half = threadIdx.x >> 6;
 #pragma unroll
   for (int i = 0; i < kQC / 2; ++i) {
     const int t = half + 2 * i;
@@ -184,12 +188,15 @@ fwd_kernel(const int64_t* __restrict__ edge_ptr, const int32_t* __restrict__ rev
       for (int r = 0; r < 4; ++r)
 #pragma unroll
         for (int i = 0; i < 4; ++i) acc[r][i] = make_float2(0.f, 0.f);
+      float xs[kQC / 2];
+      load_x(xs, rev, X, off, 0, min(kQC, n), dg, c0);
       for (int q0 = 0; q0 < n; q0 += kQC) {
         const int nq = min(kQC, n - q0);
         __syncthreads();
-        build_q<K, L>(Qs, wreg, Rb, rev, X, off, q0, nq, dg, c0);
+        build_q<K, L>(Qs, wreg, Rb, xs, q0, nq);
         build_c<L, false>(Ct, Us, n, rows, q0, nq);
         __syncthreads();
+        if (q0 + kQC < n) load_x(xs, rev, X, off, q0 + kQC, min(kQC, n - q0 - kQC), dg, c0);
         const int nkk = nq * L;
         switch (tmr) {
           case 1: micro<1>(Ct, Qs, nkk, rg, cg, acc); break;
@@ -317,11 +324,14 @@ bw1_kernel(const int64_t* __restrict__ edge_ptr, const int32_t* __restrict__ rev
         const int p = i >> 6, c = i & 63;
         Sb[p * kSbStride + c] = c0 + c < dg ? Sbar[(off + p) * dg + c0 + c] : 0.f;
       }
+      float xs[kQC / 2];
+      load_x(xs, rev, X, off, 0, min(kQC, n), dg, c0);
       for (int q0 = 0; q0 < n; q0 += kQC) {
         const int nq = min(kQC, n - q0);
         __syncthreads();
-        build_q<K, L, kSbStride>(Qs, wreg, Rb, rev, X, off, q0, nq, dg, c0);
+        build_q<K, L, kSbStride>(Qs, wreg, Rb, xs, q0, nq);
         __syncthreads();
+        if (q0 + kQC < n) load_x(xs, rev, X, off, q0 + kQC, min(kQC, n - q0 - kQC), dg, c0);
         switch (PP) {
           case 1: bw1_tile<K, L, 1>(Qs, Sb, Us, XB, n, q0, nq, G); break;
           case 2: bw1_tile<K, L, 2>(Qs, Sb, Us, XB, n, q0, nq, G); break;
