@@ -1110,6 +1110,9 @@ static int launch(const CUtensorMap& a0, const CUtensorMap& b0, const CUtensorMa
 // same fused epilogue.  fp32 FMA in fixed order.
 constexpr int kSimtM = 32, kSimtN = 64, kSimtK = 32;
 static int64_t g_simt_max_m = [] { const char* e = std::getenv("EGN_GEMM_SIMT_MAX_M"); return e ? std::atoll(e) : 8192LL; }();
+// ... and at most this many multiply-adds: the XL node products (640 x 1536 x 2048) take 4-5x
+// longer on the CUDA cores than one partial wave of 128 x 64 tcgen05 tiles with their long K loop
+constexpr int64_t kSimtMaxWork = int64_t(1) << 28;
 
 // 32 x 64 tile per 128-thread CTA (thread = 4 x 4 outputs); the next K slab is fetched into
 // registers while the current one is multiplied out of shared memory.
@@ -1579,13 +1582,22 @@ __global__ void reduce_splits_kernel(const float* __restrict__ part, int splits,
 // Tile width: 128 columns (N = 128 MMAs, one A k-block per 128 x 128 tile, store warp)
 // when N allows and there is at least a wave of such tiles; else 64 (two accumulator
 // groups, more CTAs for small products).
-static int tile_n(int64_t M, int N) { return (N % 128 == 0 && M >= static_cast<int64_t>(kNumSMs) * BM) ? 128 : 64; }
-static int wgrad_tile_n(int64_t krows, int N) {
-  return (N % 128 == 0 && krows >= static_cast<int64_t>(kNumSMs) * 8 * BK) ? 128 : 64;
+// 128-wide tiles also whenever they alone fill a wave (wide XL products: N = 128 MMAs halve
+// the per-k-block issue and split work per output; 64-wide tiles measured 31% tensor-pipe busy
+// at 14,792 x 2048 x 2048).
+static int tile_n(int64_t M, int N) {
+  const int64_t tiles128 = (M + BM - 1) / BM * ((N + 127) / 128);
+  if (N >= 256 && tiles128 >= 2 * kNumSMs) return 128;  // (a partial last n tile is clipped like with 64)
+  return (N % 128 == 0 && M >= static_cast<int64_t>(kNumSMs) * BM) ? 128 : 64;
+}
+static int wgrad_tile_n(int64_t krows, int N, int M = 0) {
+  if (N % 128 != 0) return 64;
+  const int64_t tiles128 = static_cast<int64_t>((M + BM - 1) / BM) * (N / 128);
+  return (krows >= static_cast<int64_t>(kNumSMs) * 8 * BK || tiles128 >= kNumSMs) ? 128 : 64;
 }
 
 static void wgrad_split(int64_t krows, int M, int N, int* splits, int* kbps) {
-  const int BN = wgrad_tile_n(krows, N);
+  const int BN = wgrad_tile_n(krows, N, M);
   const int tiles = static_cast<int>(((M + BM - 1) / BM) * ((N + BN - 1) / BN));
   const int nk = static_cast<int>((krows + BK - 1) / BK);
   if (nk == 0) {  // no rows: nothing to split (the entry point zero-fills the output)
@@ -1629,7 +1641,8 @@ extern "C" int egn_gemm(int64_t M, int N, int nseg, const float* a0, int64_t lda
                   (reinterpret_cast<uintptr_t>(b0) & 15) == 0 && ldb0 % 4 == 0 &&
                   (nseg == 1 || ((reinterpret_cast<uintptr_t>(a1) & 15) == 0 && lda1 % 4 == 0 &&
                                  (reinterpret_cast<uintptr_t>(b1) & 15) == 0 && ldb1 % 4 == 0));
-  if (M <= g_simt_max_m && al && (reinterpret_cast<uintptr_t>(out) & 15) == 0 && ldo % 4 == 0 &&
+  const int64_t work = M * static_cast<int64_t>(N) * (k0 + (nseg > 1 ? k1 : 0));
+  if (M <= g_simt_max_m && work <= kSimtMaxWork && al && (reinterpret_cast<uintptr_t>(out) & 15) == 0 && ldo % 4 == 0 &&
       (!(flags & (EPI_MUL_AUX | EPI_SILU_OUT2)) || ((reinterpret_cast<uintptr_t>(out2) & 15) == 0 && ldo2 % 4 == 0))) {
     const dim3 grid(static_cast<unsigned>((M + kSimtM - 1) / kSimtM), static_cast<unsigned>((N + kSimtN - 1) / kSimtN));
     cudaStream_t st = as_stream(stream);
@@ -1729,7 +1742,8 @@ extern "C" int egn_gemm_wgrad(int64_t krows, int M, int N, const float* g, int64
   int splits, kbps;
   wgrad_split(krows, M, N, &splits, &kbps);
   float* part = reinterpret_cast<float*>(workspace);
-  if (krows <= g_simt_max_m && (reinterpret_cast<uintptr_t>(g) & 15) == 0 && ldg % 4 == 0 &&
+  if (krows <= g_simt_max_m && krows * static_cast<int64_t>(M) * N <= kSimtMaxWork &&
+      (reinterpret_cast<uintptr_t>(g) & 15) == 0 && ldg % 4 == 0 &&
       (reinterpret_cast<uintptr_t>(x) & 15) == 0 && ldx % 4 == 0 && M % 4 == 0) {
     // few rows: SIMT fp32 partials over the same split plan (workspace sized by wgrad_split)
     const int rps = static_cast<int>((krows + splits - 1) / splits);
@@ -1769,7 +1783,7 @@ extern "C" int egn_gemm_wgrad(int64_t krows, int M, int N, const float* g, int64
   }
   float* gpart = part + static_cast<int64_t>(splits) * M * N;
   P.gsum_part = g_colsum ? gpart : nullptr;
-  const bool wide = wgrad_tile_n(krows, N) == 128;
+  const bool wide = wgrad_tile_n(krows, N, M) == 128;
   P.store_warp = 1;
   const int rc = wide ? launch<true, true, 128>(ma, mb, ma, mb, mo, ma, ma, P, splits, st)
                       : launch<true, true, 64>(ma, mb, ma, mb, mo, ma, ma, P, splits, st);
