@@ -1591,9 +1591,10 @@ static int tile_n(int64_t M, int N) {
   return (N % 128 == 0 && M >= static_cast<int64_t>(kNumSMs) * BM) ? 128 : 64;
 }
 static int wgrad_tile_n(int64_t krows, int N, int M = 0) {
-  if (N % 128 != 0) return 64;
-  const int64_t tiles128 = static_cast<int64_t>((M + BM - 1) / BM) * (N / 128);
-  return (krows >= static_cast<int64_t>(kNumSMs) * 8 * BK || tiles128 >= kNumSMs) ? 128 : 64;
+  const int64_t tiles128 = static_cast<int64_t>((M + BM - 1) / BM) * ((N + 127) / 128);
+  // wide products: 128-wide tiles once they fill half a wave (one K range each, no split)
+  if (N >= 256 && tiles128 >= kNumSMs / 2) return 128;
+  return (N % 128 == 0 && krows >= static_cast<int64_t>(kNumSMs) * 8 * BK) ? 128 : 64;
 }
 
 static void wgrad_split(int64_t krows, int M, int N, int* splits, int* kbps) {
@@ -1777,14 +1778,25 @@ extern "C" int egn_gemm_wgrad(int64_t krows, int M, int N, const float* g, int64
   if (int rc = make_map(&ma, g, krows, M, ldg, BK, kMapPlain)) return rc;
   if (int rc = make_map(&mb, x, krows, N, ldx, BK, kMapMN)) return rc;
   CUtensorMap mo = ma;
+  const bool wide = wgrad_tile_n(krows, N, M) == 128;
+  P.store_warp = 1;
+  if (splits == 1 && !accumulate && out_map_ok(out, ldo)) {
+    // one K range per tile: the tiles go straight to the output (no partial buffer, no
+    // reduction pass), the column sums straight to g_colsum
+    P.out = out;
+    P.ldo = ldo;
+    if (int rc = make_out_map(&mo, out, M, N, ldo, 1)) return rc;
+    P.tma_out = 1;
+    P.gsum_part = g_colsum;
+    return wide ? launch<true, true, 128>(ma, mb, ma, mb, mo, ma, ma, P, 1, st)
+                : launch<true, true, 64>(ma, mb, ma, mb, mo, ma, ma, P, 1, st);
+  }
   if (out_map_ok(part, N)) {
     if (int rc = make_out_map(&mo, part, M, N, N, splits)) return rc;
     P.tma_out = 1;
   }
   float* gpart = part + static_cast<int64_t>(splits) * M * N;
   P.gsum_part = g_colsum ? gpart : nullptr;
-  const bool wide = wgrad_tile_n(krows, N, M) == 128;
-  P.store_warp = 1;
   const int rc = wide ? launch<true, true, 128>(ma, mb, ma, mb, mo, ma, ma, P, splits, st)
                       : launch<true, true, 64>(ma, mb, ma, mb, mo, ma, ma, P, splits, st);
   if (rc) return rc;

@@ -27,7 +27,7 @@ def gemm_path(request):
 
 
 @pytest.mark.parametrize("M,N,K", [(128, 64, 32), (1000, 64, 128), (4097, 128, 256), (300, 256, 64),
-                                   (77, 384, 96), (2560, 16, 128), (58644, 128, 128)])
+                                   (77, 384, 96), (2560, 16, 128), (58644, 128, 128), (5000, 1312, 640)])
 def test_plain_gemm(M, N, K):
     from paper_2203_09697_b200 import ops
 
@@ -90,7 +90,7 @@ def test_mn_major_b_dgrad(M, N, K):
 
 
 @pytest.mark.parametrize("R,M,N", [(58644, 128, 128), (58644, 64, 256), (1000, 128, 64), (37, 64, 64),
-                                   (2560, 128, 128), (20000, 256, 128)])
+                                   (2560, 128, 128), (20000, 256, 128), (14792, 1312, 1312), (640, 1536, 2048)])
 def test_wgrad_split_k(R, M, N):
     from paper_2203_09697_b200 import ops
 
@@ -123,7 +123,7 @@ def test_strided_operands_and_errors():
         ops.gemm(torch.randn((10, 8), device="cuda"), torch.randn((12, 8), device="cuda"))  # N % 16
 
 
-@pytest.mark.parametrize("R,M,N", [(58644, 128, 128), (1000, 64, 256), (77, 32, 16)])
+@pytest.mark.parametrize("R,M,N", [(58644, 128, 128), (1000, 64, 256), (77, 32, 16), (14792, 1312, 1312)])
 def test_wgrad_fused_column_sums_and_strided_out(R, M, N):
     """egn_gemm_wgrad with g_colsum (bias adjoint from the same operand tiles) and a
     row-strided destination (a column block of a wider weight gradient)."""
