@@ -142,3 +142,29 @@ def test_wgrad_fused_column_sums_and_strided_out(R, M, N):
     prev = cs.clone()
     ops.gemm_wgrad(gr, x, out=big[:, 16:16 + N], colsum=cs, accumulate=True)
     assert _rel(cs, prev.double() + gr.double().sum(0)) < TOL
+
+
+@pytest.mark.parametrize("scale", ["small", "xl"])
+def test_small_gemms_batched_all_layouts(scale):
+    """egn_small_gemm_batched (the weight-sized folds of the backward) for every transpose
+    combination in one batch; 'xl' sizes select the 64 x 64 register-blocked kernel."""
+    from paper_2203_09697_b200 import ops
+
+    g = torch.Generator(device="cuda").manual_seed(7)
+    dims = [(64, 128, 96), (37, 70, 129)] if scale == "small" else [(2048, 256, 2048), (1312, 288, 1312)]
+    probs, refs = [], []
+    for m, n, k in dims:
+        for ta in (0, 1):
+            for tb in (0, 1):
+                for tc in (0, 1):
+                    A = torch.randn((k, m) if ta else (m, k), device="cuda", generator=g)
+                    B = torch.randn((n, k) if tb else (k, n), device="cuda", generator=g)
+                    C = torch.empty((n, m) if tc else (m, n), device="cuda")
+                    ref = (A.double().t() if ta else A.double()) @ (B.double().t() if tb else B.double())
+                    probs.append((A, B, C, ta, tb, tc))
+                    refs.append(ref.t() if tc else ref)
+    ops.small_gemms(probs)
+    torch.cuda.synchronize()
+    for (A, B, C, ta, tb, tc), ref in zip(probs, refs):
+        # plain fp32 FMA chains of length K (up to 2048): ~sqrt(K) ulp, not the 3xTF32 bound
+        assert _rel(C, ref) < 1e-5, (A.shape, B.shape, ta, tb, tc)
