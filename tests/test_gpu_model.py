@@ -132,7 +132,7 @@ def test_nn_module_autograd_path():
     energy, forces = model([pos])
     oc = O.Config(**{k: getattr(cfg, k) for k in O.Config.__dataclass_fields__})
     f = O.forward(oc, params.arrays, pos, z)
-    assert abs(float(energy[0]) - f.energy) <= TOL * max(1.0, abs(f.energy))
+    assert abs(float(energy[0].detach()) - f.energy) <= TOL * max(1.0, abs(f.energy))
     w = torch.tensor(np.random.default_rng(1).standard_normal((12, 3)), device="cuda", dtype=torch.float32)
     loss = 0.5 * energy.sum() + (forces * w).sum()
     loss.backward()
