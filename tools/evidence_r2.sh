@@ -30,8 +30,14 @@ ncu --set full --import-source on --clock-control none -k regex:bw1_kernel -s 4 
 ncu --set full --import-source on --clock-control none -k regex:bw2_kernel -s 4 -c 1 -o $O/r2e_tbw2 python tools/profile_step.py --plain --steps 1 > $O/r2e_ncu5.log 2>&1
 # spherical-harmonic triplet kernels on the C5 deg-500 d_g 64 graph
 ncu --set full --import-source on --clock-control none -k regex:"fwd_moments|fwd_apply|bwd_moments|bwd_apply" -c 4 -o $O/r2e_sh500 python tools/sh_profile_case.py 500 64 sh > $O/r2e_ncu6.log 2>&1
+ncu --set full --import-source on --clock-control none -k regex:gemm_tf32x3 -s 3 -c 1 -o $O/r2e_gemm_xl python tools/gemm_one_shape.py 14792 2048 2048 --kind fwd --reps 1 > $O/r2e_ncu7.log 2>&1
+# Bessel bases (SH kernels, MODE 2 = DimeNet SBF, with the per-call radial table) on the C1 batch
+ncu --set full --import-source on --clock-control none -k regex:"radial_table|bwd_apply|fwd_moments" -s 12 -c 3 -o $O/r2e_sh_bessel_c1 python tools/profile_step.py --workload dimenet-pp-small --basis bessel --plain --steps 1 > $O/r2e_ncu8.log 2>&1
 
 python tools/gemm_census.py --out $O/r2e_gemm_census.txt > /dev/null 2>&1
 python tools/profile_step.py --out $O/r2e_step_kernels_c2.txt > /dev/null 2>&1
 python tools/profile_step.py --workload dimenet-pp-small --out $O/r2e_step_kernels_c1.txt > /dev/null 2>&1
+python tools/step_timeline.py > $O/r2e_timeline_c2.txt 2>&1
+python tools/step_timeline.py --eager > $O/r2e_timeline_c2_eager.txt 2>&1
+for path in sh pairwise; do timeout 900 python tools/c5_sweep.py --path $path --degrees 32,64,128,256,500 --dg 64,128 --out $O/r2e_c5_$path.json > $O/r2e_c5_$path.log 2>&1; done
 ls -la $O/ | grep r2e

@@ -24,12 +24,13 @@ def main():
     ap.add_argument("--graphs", type=int, default=None)
     ap.add_argument("--out", default=str(ROOT / "gpurun_out" / "step_kernels.txt"))
     ap.add_argument("--plain", action="store_true", help="run the steps without torch.profiler")
+    ap.add_argument("--basis", default="gaussian")
     args = ap.parse_args()
     from paper_2203_09697_b200 import init_params
     from paper_2203_09697_b200.graph import build_batch
     from paper_2203_09697_b200.tasks import Trainer
 
-    wl = bench.WORKLOADS[args.workload]
+    wl = dict(bench.WORKLOADS[args.workload], basis=args.basis)
     cfg = bench._config(wl)
     systems = bench._systems(wl, args.graphs or wl["graphs"])
     bg = build_batch(systems, cfg.cutoff)
