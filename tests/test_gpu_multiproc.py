@@ -122,3 +122,61 @@ def test_bench_multi_rank_path_runs():
     assert out.returncode == 0, out.stderr[-3000:]
     line = json.loads([ln for ln in out.stdout.splitlines() if ln.startswith("{")][-1])
     assert line["n_gpus"] == 2 and line["value"] > 0 and "centre" in line["config"]["parallelism"]
+
+
+def _nccl_worker(port, q):
+    try:
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        import torch.distributed as dist
+
+        torch.cuda.set_device(0)
+        dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+        from paper_2203_09697_b200.graph import build_batch
+        from paper_2203_09697_b200.partition import partition_centers, partition_reference
+        from paper_2203_09697_b200.runtime import DistComm, GPTrainer
+        from paper_2203_09697_b200.tasks import Trainer
+
+        cfg, params, systems, e_t, f_t = _case()
+        bg = build_batch(systems, cfg.cutoff)
+        out = {}
+        for name in ("centre", "reference"):
+            part = (partition_centers(bg.deg.cpu().numpy(), 1) if name == "centre"
+                    else partition_reference(bg.tri_ptr.cpu().numpy(), bg.num_edges, bg.num_nodes, 1))
+            tr = GPTrainer(params, bg, e_t, f_t, 1.0, 0.5, DistComm(), part)
+            out[name] = (float(tr.step(0.0)), tr.weights.grad_flat.double().cpu().numpy())
+        # graph-aligned data parallelism (bench.py's default N > 1 path): gradient all-reduce
+        tr = Trainer(params, None, e_t, f_t, 1.0, 0.5, graph=bg, comm=DistComm(), global_graphs=len(systems),
+                     cuda_graph=True)
+        tr.step(0.0)
+        out["aligned"] = (float(tr.step(0.0)), tr.weights.grad_flat.double().cpu().numpy())
+        torch.cuda.synchronize()
+        dist.destroy_process_group()
+        q.put(("ok", out))
+    except BaseException:  # noqa: BLE001
+        import traceback
+
+        q.put((traceback.format_exc(), None))
+
+
+def test_nccl_process_group_paths_world1():
+    """The NCCL code paths of DistComm (async all_reduce, all_gather_into_tensor,
+    reduce_scatter_tensor on device buffers) inside GPTrainer (both schedules) and the
+    graph-aligned Trainer with a captured step, through a real NCCL process group of one rank
+    (one GPU per rank is all NCCL allows); results equal the communicator-free Trainer."""
+    from paper_2203_09697_b200.graph import build_batch
+    from paper_2203_09697_b200.tasks import Trainer
+
+    cfg, params, systems, e_t, f_t = _case()
+    ref = Trainer(params, None, e_t, f_t, 1.0, 0.5, graph=build_batch(systems, cfg.cutoff))
+    loss_ref = float(ref.step(0.0))
+    g_ref = ref.weights.grad_flat.double().cpu().numpy()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    p = ctx.Process(target=_nccl_worker, args=(_free_port(), q))
+    p.start()
+    status, out = q.get(timeout=300)
+    p.join(timeout=60)
+    assert status == "ok", status
+    for name, (loss, g) in out.items():
+        assert abs(loss - loss_ref) <= 1e-5 * abs(loss_ref), (name, loss, loss_ref)
+        assert max_rel(g, g_ref) < 1e-5, name
