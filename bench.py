@@ -336,7 +336,7 @@ def _kernel_roofline(tr, bg, cfg):
     b_gemm = 4 * (3 * ne * de + de * de)
     ach = b_gemm / t_g / 1e9
     traffic = None
-    tpath = ROOT / "profiles" / "r1_traffic.json"
+    tpath = ROOT / "profiles" / "r2_traffic.json"
     key = f"gemm_fwd_resid_{de}"
     if tpath.exists():
         tj = json.loads(tpath.read_text())
@@ -350,7 +350,7 @@ def _kernel_roofline(tr, bg, cfg):
     # tensor-bound when its intensity (fp32 FLOP per algorithmic byte) exceeds that rate / HBM
     tensor_bound = flops / b_gemm > (tf32_peak / 3) * 1e12 / (hbm * 1e9)
     base = {"kernel": f"gemm_tf32x3 E x {de} x {de} (+residual), 3xTF32 on tcgen05",
-            "traffic": traffic, "traffic_source": f"profiles/r1_traffic.json:{key} (ncu --set full)" if traffic else None,
+            "traffic": traffic, "traffic_source": f"profiles/r2_traffic.json:{key} (ncu --set full)" if traffic else None,
             "peak_source": "MEASURED_PEAKS.json" if peaks else "fallback",
             "launch_us": t_g * 1e6, "algorithmic_bytes": b_gemm, "algorithmic_flops": flops,
             "tensor_frac": 3 * flops / t_g / 1e12 / tf32_peak, "hbm_frac": ach / hbm}

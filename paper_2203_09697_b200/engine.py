@@ -186,12 +186,14 @@ class Engine:
     def _side_stream(self, bg, index: int = 0):
         """Side stream `index` of this host thread (0: weight gradients and graph-level work,
         1: the node-level adjoint chain, 2: the triplet angle adjoint), or None: EGN_WGRAD_STREAM=0, or a batch below
-        EGN_SIDE_MIN_EDGES edges (default 16384), whose kernels are too short for the
-        fork / join to pay in an eagerly launched step (relaxation of one small system)."""
+        EGN_SIDE_MIN_EDGES edges (default 16384) launched eagerly, whose kernels are too short
+        for the fork / join to pay (relaxation of one small system)."""
         device = bg.device
         if device.type != "cuda" or os.environ.get("EGN_WGRAD_STREAM", "1") == "0":
             return None
-        if bg.num_edges < int(os.environ.get("EGN_SIDE_MIN_EDGES", "16384")):
+        # (a captured step pays no launch cost for the fork / join: any size)
+        if (bg.num_edges < int(os.environ.get("EGN_SIDE_MIN_EDGES", "16384"))
+                and not torch.cuda.is_current_stream_capturing()):
             return None
         key = (threading.get_ident(), index)
         if key not in self._side:

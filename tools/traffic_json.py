@@ -24,10 +24,10 @@ def main():
     ap.add_argument("--edges", type=int, required=True)
     ap.add_argument("--triplets", type=int, required=True)
     ap.add_argument("--dg", type=int, required=True)
-    ap.add_argument("--out", default=str(ROOT / "profiles" / "r1_traffic.json"))
+    ap.add_argument("--out", default=str(ROOT / "profiles" / "r2_traffic.json"))
     a = ap.parse_args()
     res = {"_comment": "DRAM bytes per launch from ncu --set full captures (tools/traffic_json.py; "
-                       "summaries in profiles/r1_*_ncu.txt)",
+                       "summaries in profiles/r2_*_ncu.txt)",
            "workload": {"edges": a.edges, "triplets": a.triplets, "dg": a.dg}}
     for spec in a.specs:
         key, rest = spec.split("=", 1)
