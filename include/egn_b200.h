@@ -419,6 +419,16 @@ int egn_loss_seeds(const float* energy, const double* e_target, int64_t num_grap
                    const double* f_target, const double* atom_count, int64_t num_nodes, double w_energy,
                    double w_forces, double n, double* loss, float* d_energy, float* d_forces, egn_stream_t stream);
 int egn_sgd(float* w, const float* g, int64_t n, float lr, egn_stream_t stream);
+/* Device utilities of the training step (no framework elementwise kernels on the path):
+ * egn_zero: bytes of zeros (cudaMemsetAsync); egn_hadamard: out = a * b elementwise
+ * (16-byte aligned); egn_transpose: out[c][r] = in[r][c] (row strides ld_in, ld_out);
+ * egn_csr_ptr: ptr[v] = lower_bound(keys, v) for v in [0, nv] over keys sorted ascending
+ * (the CSR offsets of a sorted user edge list, egn/graph.py:106-139's enumerate_triplets input). */
+int egn_zero(void* ptr, int64_t bytes, egn_stream_t stream);
+int egn_hadamard(const float* a, const float* b, float* out, int64_t n, egn_stream_t stream);
+int egn_transpose(const float* in, int64_t rows, int64_t cols, int64_t ld_in, float* out, int64_t ld_out,
+                  egn_stream_t stream);
+int egn_csr_ptr(const int64_t* keys, int64_t n, int64_t nv, int64_t* ptr, egn_stream_t stream);
 /* AdamW step t >= 1 over a flat parameter buffer (the
  * reference documents it only): decoupled weight decay, bias-corrected first / second moments
  * m, v (caller-owned, zero before step 1), torch.optim.AdamW's update order. */

@@ -100,6 +100,10 @@ SIGNATURES: dict[str, tuple] = {
     "egn_gemm_wgrad": (_i32, [_i64, _i32, _i32, _p, _i64, _p, _i64, _p, _i64, _p, _i32, _p, _p]),
     "egn_small_gemm_batched": (_i32, [_p, _i32, _p]),
     "egn_sgd": (_i32, [_p, _p, _i64, _f32, _p]),
+    "egn_zero": (_i32, [_p, _i64, _p]),
+    "egn_hadamard": (_i32, [_p, _p, _p, _i64, _p]),
+    "egn_transpose": (_i32, [_p, _i64, _i64, _i64, _p, _i64, _p]),
+    "egn_csr_ptr": (_i32, [_p, _i64, _i64, _p, _p]),
 }
 
 
@@ -146,13 +150,15 @@ KERNELS_PER_CALL = {
 }
 LAUNCH_COUNTER = {"calls": 0, "kernels": 0}
 _NOT_LAUNCHES = {"egn_triplet_path", "egn_abi_version"}
+_NO_KERNEL = {"egn_zero"}  # a memset: checked, not counted as a kernel
 
 
 def call(name: str, *args) -> int:
     """Invoke an ABI function; raise EgnNativeError with the library message on failure."""
     fn = getattr(lib(), name)
     rc = fn(*args)
-    if SIGNATURES[name][0] is _i32 and not name.endswith("_bytes") and name not in _NOT_LAUNCHES:
+    if (SIGNATURES[name][0] is _i32 and not name.endswith("_bytes") and name not in _NOT_LAUNCHES
+            and name not in _NO_KERNEL):
         LAUNCH_COUNTER["calls"] += 1
         LAUNCH_COUNTER["kernels"] += KERNELS_PER_CALL.get(name, 1)
     if SIGNATURES[name][0] is _i32 and rc != 0 and name not in _NOT_LAUNCHES:

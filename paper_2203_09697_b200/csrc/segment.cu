@@ -1178,3 +1178,91 @@ extern "C" int egn_small_gemm_batched(const egn_small_gemm_t* problems, int coun
   }
   return 0;
 }
+
+// ---------------------------------------------------------------- small device utilities
+// (so the training step launches no framework elementwise kernels: zero fills, the DimeNet
+// gate product, the W_sbf gradient transpose, CSR offsets of a user-given sorted edge list)
+namespace egn {
+__global__ void hadamard_kernel(const float* __restrict__ a, const float* __restrict__ b, float* __restrict__ out,
+                                int64_t n) {
+  const int64_t n4 = n / 4;
+  const float4* a4 = reinterpret_cast<const float4*>(a);
+  const float4* b4 = reinterpret_cast<const float4*>(b);
+  float4* o4 = reinterpret_cast<float4*>(out);
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n4;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const float4 x = a4[i], y = b4[i];
+    o4[i] = make_float4(x.x * y.x, x.y * y.y, x.z * y.z, x.w * y.w);
+  }
+  for (int64_t i = 4 * n4 + blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    out[i] = a[i] * b[i];
+}
+
+// out[c][r] = in[r][c] through 32 x 33 shared tiles
+__global__ void transpose_kernel(const float* __restrict__ in, int64_t rows, int64_t cols, int64_t ld_in,
+                                 float* __restrict__ out, int64_t ld_out) {
+  __shared__ float t[32][33];
+  const int64_t r0 = static_cast<int64_t>(blockIdx.y) * 32, c0 = static_cast<int64_t>(blockIdx.x) * 32;
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int64_t r = r0 + i, c = c0 + threadIdx.x;
+    if (r < rows && c < cols) t[i][threadIdx.x] = in[r * ld_in + c];
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int64_t c = c0 + i, r = r0 + threadIdx.x;
+    if (r < rows && c < cols) out[c * ld_out + r] = t[threadIdx.x][i];
+  }
+}
+
+// ptr[v] = first k with keys[k] >= v (keys sorted ascending), v in [0, nv]
+__global__ void csr_ptr_kernel(const int64_t* __restrict__ keys, int64_t n, int64_t nv, int64_t* __restrict__ ptr) {
+  for (int64_t v = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; v <= nv;
+       v += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    int64_t lo = 0, hi = n;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (keys[mid] < v) lo = mid + 1;
+      else hi = mid;
+    }
+    ptr[v] = lo;
+  }
+}
+}  // namespace egn
+
+extern "C" {
+int egn_zero(void* ptr, int64_t bytes, egn_stream_t stream) {
+  EGN_REQUIRE(bytes >= 0, "negative size");
+  if (bytes == 0) return 0;
+  cudaMemsetAsync(ptr, 0, static_cast<size_t>(bytes), as_stream(stream));
+  return check_launch("zero");
+}
+
+int egn_hadamard(const float* a, const float* b, float* out, int64_t n, egn_stream_t stream) {
+  using namespace egn;
+  EGN_REQUIRE(((reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(b) | reinterpret_cast<uintptr_t>(out)) &
+               15) == 0,
+              "hadamard operands must be 16-byte aligned");
+  if (n == 0) return 0;
+  hadamard_kernel<<<static_cast<int>(std::min<int64_t>((n / 4 + 255) / 256 + 1, kNumSMs * 16)), 256, 0,
+                    as_stream(stream)>>>(a, b, out, n);
+  return check_launch("hadamard");
+}
+
+int egn_transpose(const float* in, int64_t rows, int64_t cols, int64_t ld_in, float* out, int64_t ld_out,
+                  egn_stream_t stream) {
+  using namespace egn;
+  EGN_REQUIRE(rows >= 0 && cols >= 0 && ld_in >= cols && ld_out >= rows, "bad transpose shape / strides");
+  if (rows == 0 || cols == 0) return 0;
+  const dim3 grid(static_cast<unsigned>((cols + 31) / 32), static_cast<unsigned>((rows + 31) / 32));
+  transpose_kernel<<<grid, dim3(32, 8), 0, as_stream(stream)>>>(in, rows, cols, ld_in, out, ld_out);
+  return check_launch("transpose");
+}
+
+int egn_csr_ptr(const int64_t* keys, int64_t n, int64_t nv, int64_t* ptr, egn_stream_t stream) {
+  using namespace egn;
+  EGN_REQUIRE(n >= 0 && nv >= 0, "negative size");
+  csr_ptr_kernel<<<grid_for(nv + 1, 256), 256, 0, as_stream(stream)>>>(keys, n, nv, ptr);
+  return check_launch("csr_ptr");
+}
+}  // extern "C"

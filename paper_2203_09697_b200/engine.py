@@ -201,16 +201,6 @@ class Engine:
         return self._side[key]
 
     # -- helpers -----------------------------------------------------------
-    def _sbf_weight(self, b: int) -> torch.Tensor:
-        """W[k, l, c] = W'[c, k*L + l] with W' = W_sbf (dimenet) or B W_sbf (gemnet)."""
-        c, w = self.config, self.weights.w
-        p = f"block{b}.tu."
-        wp = w[p + "sbf_gate"]
-        if c.variant == GEMNET:
-            wp = w[p + "bilinear_b"] @ wp
-        dg = wp.shape[0]
-        return wp.view(dg, c.k_rbf, c.l_sbf).permute(1, 2, 0).contiguous()
-
     def _folded_weights(self) -> list:
         """Per block: the folded weights of this step, all from one batched launch
         (egn_small_gemm_batched): Wda = A W_down (GemNet), W1u = W1b W_up, and the
@@ -231,8 +221,10 @@ class Engine:
                 f["Wk"] = torch.empty((c.k_rbf, c.l_sbf, c.d_bil), dtype=torch.float32, device=dev)
                 probs.append((w[p + "tu.bilinear_b"], w[p + "tu.sbf_gate"],
                               f["Wk"].view(c.k_rbf * c.l_sbf, c.d_bil), 0, 0, 1))
-            else:
-                f["Wk"] = self._sbf_weight(b)
+            else:  # W[k, l, c] = W_sbf[c, k L + l]: a native transpose into [K L, d_t]
+                dt = c.triplet_width
+                f["Wk"] = torch.empty((c.k_rbf, c.l_sbf, dt), dtype=torch.float32, device=dev)
+                ops.transpose_into(w[p + "tu.sbf_gate"], f["Wk"].view(c.k_rbf * c.l_sbf, dt))
             out.append(f)
         ops.small_gemms(probs)
         return out
@@ -250,8 +242,7 @@ class Engine:
         side = self._side_stream(bg)
         rbf = ops.rbf(bg.geo, c.k_rbf, c.cutoff, c.basis_code)
         m = ops.rbf_linear(rbf, w["edge_init.w"], w["edge_init.b"]) if m0 is None else m0  # K = k_rbf (6)
-        u = (torch.zeros((bg.num_graphs, c.d_u), dtype=torch.float32, device=bg.device) if u0 is None
-             else u0.clone())
+        u = ops.zeros((bg.num_graphs, c.d_u), bg.device) if u0 is None else u0.clone()
         v = None
         order = list(range(c.blocks)) if blocks is None else list(blocks)
         blocks = []
@@ -287,7 +278,7 @@ class Engine:
                 Y, Z = L(S, w[p + "tu.bilinear_proj"], aux=g, flags=ops.EPI_MUL_AUX)  # Y = (S P^T) * g
                 st["Z"] = Z
             else:
-                Y = S * g
+                Y = ops.hadamard(S, g)
             w1 = w[p + "eu.w1"]
             # h = [m, ta] W1^T + b1 with ta = Y W_up^T folded into the second segment:
             # h = m W1a^T + Y (W1b W_up)^T + b1 (no concat, no [E, d_e] ta); a1 = silu(h)
@@ -326,7 +317,7 @@ class Engine:
         if gem:
             scale, forces = ops.force_head_fwd(bg.edge_ptr, bg.rev, bg.geo, m, w["force_head.w"].view(-1))
         if v is None:
-            v = torch.zeros((bg.num_nodes, c.d_v), device=bg.device)
+            v = ops.zeros((bg.num_nodes, c.d_v), bg.device)
         return ForwardResult(energy, forces, m, v, u, rbf, blocks, scale)
 
     # -- backward ------------------------------------------------------------
@@ -368,17 +359,17 @@ class Engine:
                 main.wait_stream(side)
                 pending.clear()
 
-        self.weights.grad_flat.zero_()
-        eg = torch.zeros((bg.num_edges, 4), dtype=torch.float32, device=bg.device)
+        ops.zero_(self.weights.grad_flat)
+        eg = ops.zeros((bg.num_edges, 4), bg.device)
         dE = d_energy.to(torch.float32).view(-1, 1)
         u_bar = ops.graph_linear_bwd(dE, fw.u, w["energy_head.w"], w_bar=gr["energy_head.w"],
                                      b_bar=gr["energy_head.b"])
-        m_bar = torch.zeros((bg.num_edges, de), dtype=torch.float32, device=bg.device)
+        m_bar = ops.zeros((bg.num_edges, de), bg.device)
         if gem and d_forces is not None:
             ops.force_head_bwd(bg.recv, bg.geo, fw.m, w["force_head.w"].view(-1), fw.scale,
                                d_forces.to(torch.float32).contiguous(), m_bar, eg,
                                w_bar=gr["force_head.w"].view(-1))
-        rbf_bar = torch.zeros_like(fw.rbf)
+        rbf_bar = ops.zeros(tuple(fw.rbf.shape), bg.device)
         post = []  # weight-sized gradient products, batched after the block loop
         for b in range(c.blocks - 1, -1, -1):
             join()
@@ -464,8 +455,8 @@ class Engine:
                 wg(Z_bar, st["S"], gr[p + "tu.bilinear_proj"])
                 S_bar = L(Z_bar, w[p + "tu.bilinear_proj"], w_mn=True)
             else:
-                Y_bar = L(h_bar, st["W1u"], w_mn=True)
-                S_bar = Y_bar * st["g"]
+                # S_bar = Y_bar * g fused into the GEMM epilogue (second output Y_bar)
+                S_bar, Y_bar = L(h_bar, st["W1u"], w_mn=True, aux=st["g"], flags=ops.EPI_MUL_AUX)
                 g_prod = (Y_bar, st["S"])  # g_bar = Y_bar * S
             # rbf_bar is read only after the block loop: the gate adjoint runs on the side stream
             if side is not None:
@@ -496,7 +487,7 @@ class Engine:
                 m_bar = L(X_bar, st["Wda"], w_mn=True, resid=m_in_bar)
                 continue
             else:
-                gr[p + "tu.sbf_gate"].copy_(Wk_bar.permute(2, 0, 1).reshape(Wk_bar.shape[2], -1))  # [dg, K*L]
+                ops.transpose_into(Wk_bar.view(-1, Wk_bar.shape[2]), gr[p + "tu.sbf_gate"])  # [dg, K*L]
                 down_bar = X_bar
             wg(down_bar, st["m"], gr[p + "tu.down"])
             m_bar = L(down_bar, w[p + "tu.down"], w_mn=True, resid=m_in_bar)

@@ -254,8 +254,7 @@ class GraphTopology:
             return self._rev
         src = self.edge_src.to(torch.int32)
         recv = self.edge_recv.to(torch.int32)
-        deg = torch.bincount(self.edge_src, minlength=self.num_nodes).to(torch.int32)
-        edge_ptr = ops.scan_counts(deg)
+        edge_ptr = ops.csr_ptr(self.edge_src, self.num_nodes)  # edges sorted by source
         rev, missing = ops.reverse_edges(edge_ptr, src, recv)
         if int(missing.item()):
             bad = int(torch.nonzero(rev < 0)[0].item())
@@ -314,8 +313,8 @@ def enumerate_triplets(num_nodes, edge_src=None, edge_recv=None):
     if edge_src.numel() == 0:
         e = torch.empty(0, dtype=torch.int64, device="cuda")
         return e, e
-    deg = torch.bincount(edge_src.to(torch.int64), minlength=int(num_nodes)).to(torch.int32)
-    edge_ptr = ops.scan_counts(deg)
+    edge_ptr = ops.csr_ptr(edge_src.to(torch.int64), int(num_nodes))  # edges sorted by source
+    deg = (edge_ptr[1:] - edge_ptr[:-1]).to(torch.int32)
     tri_ptr = ops.scan_counts(deg, square_minus_one=True)
     rev, missing = ops.reverse_edges(edge_ptr, edge_src.to(torch.int32), edge_recv.to(torch.int32))
     if int(missing.item()):

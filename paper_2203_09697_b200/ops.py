@@ -46,7 +46,7 @@ def neighbors_fill(pos, graph_ptr, node_graph, cutoff, edge_ptr, num_edges):
 def reverse_edges(edge_ptr, src, recv, missing=None):
     rev = torch.empty_like(src)
     if missing is None:
-        missing = torch.zeros(1, dtype=torch.int32, device=src.device)
+        missing = zeros((1,), src.device, torch.int32)
     call("egn_reverse_edges", ptr(edge_ptr), ptr(src), ptr(recv), src.shape[0], ptr(rev), ptr(missing), stream())
     return rev, missing
 
@@ -608,6 +608,47 @@ def small_gemms(problems):
         arr[i] = SmallGemm(ptr(A), ptr(B), ptr(C), m, n, k, A.stride(0), B.stride(0), C.stride(0), int(ta), int(tb),
                            int(tc))
     call("egn_small_gemm_batched", ctypes.addressof(arr), len(problems), stream())
+
+
+def zero_(t):
+    """t[:] = 0 on the device (egn_zero: a memset, no framework fill kernel)."""
+    if not t.is_contiguous():
+        raise ValueError("zero_ takes contiguous tensors")
+    call("egn_zero", ptr(t), t.numel() * t.element_size(), stream())
+    return t
+
+
+def zeros(shape, device, dtype=torch.float32):
+    return zero_(torch.empty(shape, dtype=dtype, device=device))
+
+
+def hadamard(a, b, out=None):
+    """out = a * b elementwise (egn_hadamard)."""
+    a, b = _c(a, torch.float32), _c(b, torch.float32)
+    if a.shape != b.shape:
+        raise ValueError(f"hadamard: shapes {tuple(a.shape)} and {tuple(b.shape)} differ")
+    if out is None:
+        out = torch.empty_like(a)
+    call("egn_hadamard", ptr(a), ptr(b), ptr(out), a.numel(), stream())
+    return out
+
+
+def transpose_into(src, dst):
+    """dst[c, r] = src[r, c] for 2-D fp32 views with contiguous rows (egn_transpose)."""
+    if src.dim() != 2 or dst.dim() != 2 or src.stride(1) != 1 or dst.stride(1) != 1:
+        raise ValueError("transpose_into takes 2-D views with contiguous rows")
+    if dst.shape[0] != src.shape[1] or dst.shape[1] != src.shape[0]:
+        raise ValueError("transpose_into: shape mismatch")
+    call("egn_transpose", ptr(src), src.shape[0], src.shape[1], src.stride(0), ptr(dst), dst.stride(0), stream())
+    return dst
+
+
+def csr_ptr(keys, num_rows):
+    """CSR offsets [num_rows + 1] of sorted int64 row keys (egn_csr_ptr)."""
+    keys = _c(keys, torch.int64)
+    out = torch.empty(int(num_rows) + 1, dtype=torch.int64, device=keys.device)
+    call("egn_csr_ptr", ptr(keys), keys.numel(), int(num_rows), ptr(out), stream())
+    return out
 
 
 def sgd_(w, g, lr):

@@ -566,7 +566,7 @@ class GraphParallelEngine:
         rbf = ops.rbf(d["geo_own"], c.k_rbf, c.cutoff, c.basis_code)
         m = ops.rbf_linear(rbf, w["edge_init.w"], w["edge_init.b"])
         gates = [ops.rbf_linear(rbf, w[f"block{b}.tu.rbf_gate"]) for b in range(c.blocks)]
-        u = torch.zeros((G, c.d_u), dtype=f32, device=dev)
+        u = ops.zeros((G, c.d_u), dev)
         blocks, pending, v = [], [], None
         for b in range(c.blocks):
             p = f"block{b}."
@@ -586,7 +586,7 @@ class GraphParallelEngine:
                 Y, Z = L(S_o, w[p + "tu.bilinear_proj"], aux=g, flags=ops.EPI_MUL_AUX)
                 st["Z"] = Z
             else:
-                Y = S_o * g
+                Y = ops.hadamard(S_o, g)
             w1 = w[p + "eu.w1"]
             W1u = folded[b]["W1u"]
             h, a1 = L(m, w1[:, :de], a2=Y, w2=W1u, bias=w[p + "eu.b1"], flags=ops.EPI_SILU_OUT2)
@@ -621,7 +621,7 @@ class GraphParallelEngine:
             else:
                 m = m_new
             # GU head: per-graph sums of own nodes, all-reduced under the next blocks' edge work
-            s = ops.graph_sum(d["gp_own"], v) if n1 > n0 else torch.zeros((G, c.d_v), dtype=f32, device=dev)
+            s = ops.graph_sum(d["gp_own"], v) if n1 > n0 else ops.zeros((G, c.d_v), dev)
             pending.append((b, s, cm.all_reduce_(s, async_op=True, phase="forward", block=b, stage="gu",
                                                  level="global", width=self.R.d_v)))
             blocks.append(st)
@@ -658,20 +658,20 @@ class GraphParallelEngine:
         lead = cm.rank == 0
         gL = _lead_grads(self.weights, lead, self._cache)
         self.clock.mark("backward.readout")
-        self.weights.grad_flat.zero_()
-        eg = torch.zeros((E, 4), dtype=f32, device=dev)
+        ops.zero_(self.weights.grad_flat)
+        eg = ops.zeros((E, 4), dev)
         dE = d_energy.to(f32).view(-1, 1).contiguous()
         u_bar = ops.graph_linear_bwd(dE, fw.u, w["energy_head.w"], w_bar=gL["energy_head.w"],
                                      b_bar=gL["energy_head.b"])
-        m_bar = torch.zeros((e1 - e0, de), dtype=f32, device=dev)
+        m_bar = ops.zeros((e1 - e0, de), dev)
         if gem and d_forces_own is not None:
-            f_full = torch.zeros((V, 3), dtype=f32, device=dev)
+            f_full = ops.zeros((V, 3), dev)
             f_full[n0:n1] = d_forces_own.to(f32)
             if not hf:
                 cm.all_gather_rows(f_full, d["nb"], phase="backward", block=-1, stage="forces", level="node")
             ops.force_head_bwd(d["recv_own"], d["geo_own"], fw.m, w["force_head.w"].view(-1), fw.scale[e0:e1],
                                f_full, m_bar, eg[e0:e1], w_bar=gr["force_head.w"].view(-1))
-        rbf_bar = torch.zeros_like(fw.rbf)
+        rbf_bar = ops.zeros(tuple(fw.rbf.shape), dev)
         # GU adjoints of every block first: u_bar passes unchanged through the residual updates
         v_bar_gu = []
         for b in range(c.blocks):
@@ -690,7 +690,7 @@ class GraphParallelEngine:
                     _wg(m_bar, st["m2r"], gr[p + "sym.w"])
                     m2_bar = ops.gather_rows(d["rev_local"], t, out=m_bar, accumulate=True)
                 else:
-                    part = torch.zeros((E, de), dtype=f32, device=dev)
+                    part = ops.zeros((E, de), dev)
                     ops.scatter_rows(d["rev_own"], ident[: e1 - e0], t, part)
                     hnd = cm.reduce_scatter_rows(part, d["eb"], async_op=True, phase="backward", block=b,
                                                  stage="m2", level="edge", width=self.R.d_e)
@@ -699,7 +699,7 @@ class GraphParallelEngine:
                 # EU2
                 self.clock.mark(f"backward.block{b}.eu2")
                 _wg(m2_bar, st["a2"], gr[p + "eu2.w2"], gr[p + "eu2.b2"])
-                h2_full = (torch.empty if hf else torch.zeros)((E, de), dtype=f32, device=dev)
+                h2_full = torch.empty((E, de), dtype=f32, device=dev) if hf else ops.zeros((E, de), dev)
                 h2_bar = L(m2_bar, w[p + "eu2.w2"], w_mn=True, aux=st["h2"], flags=ops.EPI_DSILU_AUX,
                            out=h2_full[e0:e1])
                 w1 = w[p + "eu2.w1"]
@@ -726,7 +726,7 @@ class GraphParallelEngine:
                 _wg(v_bar, st["av"], gr[p + "nu.w2"], gr[p + "nu.b2"])
                 _wg(hv_bar, st["agg"], gr[p + "nu.w1"], gr[p + "nu.b1"])
             else:
-                part = torch.zeros((E, de), dtype=f32, device=dev)
+                part = ops.zeros((E, de), dev)
                 ops.scatter_rows(d["rev_own"], d["src_local"], agg_bar, part)
                 hnd = cm.reduce_scatter_rows(part, d["eb"], async_op=True, phase="backward", block=b,
                                              stage="m_new", level="edge", width=self.R.d_e)
@@ -753,9 +753,9 @@ class GraphParallelEngine:
                 g_prod = (Y_bar, st["Z"])
             else:
                 Y_bar = L(h_bar, st["W1u"], w_mn=True)
-                torch.mul(Y_bar, st["g"], out=S_bar[e0:e1])
+                ops.hadamard(Y_bar, st["g"], out=S_bar[e0:e1])
                 g_prod = (Y_bar, st["S"][e0:e1])
-            X_bar_full = (torch.empty_like if hf else torch.zeros_like)(st["X"])
+            X_bar_full = torch.empty_like(st["X"]) if hf else ops.zeros(tuple(st["X"].shape), dev)
             X_bar_full, Wk_bar = ops.triplet_bwd(d["ep_own"], bg.rev, bg.geo, st["X"], st["Wk"], c.cutoff, S_bar, eg,
                                                  X_bar=X_bar_full, max_degree=bg.max_deg,
                                                  basis=c.basis_code)
@@ -773,7 +773,7 @@ class GraphParallelEngine:
                 post.append((w[p + "tu.bilinear_a"], T, gr[p + "tu.down"], 1, 0, 0))
                 m_bar = L(X_bar, st["Wx"], w_mn=True, resid=m_in_bar)
             else:
-                gr[p + "tu.sbf_gate"].copy_(Wk_bar.permute(2, 0, 1).reshape(Wk_bar.shape[2], -1))
+                ops.transpose_into(Wk_bar.view(-1, Wk_bar.shape[2]), gr[p + "tu.sbf_gate"])
                 _wg(X_bar, st["m"], gr[p + "tu.down"])
                 m_bar = L(X_bar, w[p + "tu.down"], w_mn=True, resid=m_in_bar)
         self.clock.mark("backward.init")
@@ -847,7 +847,7 @@ class ReferenceScheduleEngine:
         folded = self._helper._folded_weights()
         rbf = ops.rbf(bg.geo, c.k_rbf, c.cutoff, c.basis_code)
         m = ops.rbf_linear(rbf, w["edge_init.w"], w["edge_init.b"])
-        u = torch.zeros((G, c.d_u), dtype=f32, device=dev)
+        u = ops.zeros((G, c.d_u), dev)
         blocks, v = [], None
         for b in range(c.blocks):
             p = f"block{b}."
@@ -856,8 +856,8 @@ class ReferenceScheduleEngine:
             Wx = folded[b]["Wda"] if gem else w[p + "tu.down"]
             X = L(m, Wx)
             Wk = folded[b]["Wk"]
-            S = torch.zeros((E, dg), dtype=f32, device=dev)
-            ta = torch.zeros((E, de), dtype=f32, device=dev)
+            S = ops.zeros((E, dg), dev)
+            ta = ops.zeros((E, de), dev)
             g = ops.rbf_linear(rbf[ra:rb], w[p + "tu.rbf_gate"]) if has_t else None
             Y = Z = None
             if has_t:
@@ -865,7 +865,7 @@ class ReferenceScheduleEngine:
                 if gem:
                     Y, Z = L(S[ra:rb], w[p + "tu.bilinear_proj"], aux=g, flags=ops.EPI_MUL_AUX)
                 else:
-                    Y = S[ra:rb] * g
+                    Y = ops.hadamard(S[ra:rb], g)
                 L(Y, w[p + "tu.up"], out=ta[ra:rb])
             cm.all_reduce_(ta, phase="forward", block=b, stage="ta", level="edge", width=self.R.d_e)
             self.clock.mark(f"block{b}.eu")
@@ -873,7 +873,7 @@ class ReferenceScheduleEngine:
             h, a1 = L(m, w1[:, :de], a2=ta, w2=w1[:, de:], bias=w[p + "eu.b1"], flags=ops.EPI_SILU_OUT2)
             m_new = L(a1, w[p + "eu.w2"], bias=w[p + "eu.b2"], resid=m)
             self.clock.mark(f"block{b}.nu")
-            v_part = torch.zeros((V, c.d_v), dtype=f32, device=dev)
+            v_part = ops.zeros((V, c.d_v), dev)
             agg = hv = av = None
             if n1 > n0:
                 agg = ops.aggregate_in_edges(d["ep_n"], bg.rev, m_new)
@@ -883,7 +883,7 @@ class ReferenceScheduleEngine:
             st.update(X=X, Wx=Wx, Wk=Wk, S=S, g=g, Y=Y, Z=Z, ta=ta, h=h, a1=a1, m_new=m_new, agg=agg, hv=hv, av=av, v=v)
             if gem:
                 self.clock.mark(f"block{b}.eu2")
-                m2 = torch.zeros((E, de), dtype=f32, device=dev)
+                m2 = ops.zeros((E, de), dev)
                 h2 = a2 = None
                 if e1 > e0:
                     w1 = w[p + "eu2.w1"]
@@ -900,7 +900,7 @@ class ReferenceScheduleEngine:
                 m = m_new
             self.clock.mark(f"block{b}.gu")
             s = (ops.graph_sum(d["gp_own"], v[n0:n1]) if n1 > n0
-                 else torch.zeros((G, c.d_v), dtype=f32, device=dev))
+                 else ops.zeros((G, c.d_v), dev))
             z = ops.graph_linear(s, w[p + "gu.w1"])
             cm.all_reduce_(z, phase="forward", block=b, stage="gu", level="global", width=self.R.d_u)
             pre, act = ops.graph_mlp_fwd(z, None, w[p + "gu.b1"], w[p + "gu.w2"], w[p + "gu.b2"], u)
@@ -919,7 +919,7 @@ class ReferenceScheduleEngine:
         c, w = self.config, self.weights.w
         dev = bg.device
         if self.j1 <= self.j0:
-            return torch.zeros((0, c.d_t), dtype=torch.float32, device=dev)
+            return ops.zeros((0, c.d_t), dev)
         st = fw.blocks[block]
         tp = bg.tri_ptr[self.j0:self.j1 + 1]
         tp = (tp - tp[0]).contiguous()
@@ -948,19 +948,19 @@ class ReferenceScheduleEngine:
         f32 = torch.float32
         lead = cm.rank == 0
         self.clock.mark("backward.readout")
-        self.weights.grad_flat.zero_()
-        eg = torch.zeros((E, 4), dtype=f32, device=dev)
-        rbf_bar = torch.zeros_like(fw.rbf)
+        ops.zero_(self.weights.grad_flat)
+        eg = ops.zeros((E, 4), dev)
+        rbf_bar = ops.zeros(tuple(fw.rbf.shape), dev)
         dE = d_energy.to(f32).view(-1, 1).contiguous()
         if lead:
             u_bar = ops.graph_linear_bwd(dE, fw.u, w["energy_head.w"], w_bar=gr["energy_head.w"],
                                          b_bar=gr["energy_head.b"])
         else:
-            u_bar = torch.zeros((G, c.d_u), dtype=f32, device=dev)
+            u_bar = ops.zeros((G, c.d_u), dev)
         cm.all_reduce_(u_bar, phase="backward", block=-1, stage="energy", level="global", width=self.R.d_u)
-        m_bar = torch.zeros((E, de), dtype=f32, device=dev)
+        m_bar = ops.zeros((E, de), dev)
         if gem and d_forces is not None:
-            f_part = torch.zeros((V, 3), dtype=f32, device=dev)
+            f_part = ops.zeros((V, 3), dev)
             f_part[n0:n1] = d_forces.to(f32)[n0:n1]
             ops.force_head_bwd(bg.recv, bg.geo, fw.m, w["force_head.w"].view(-1), fw.scale, f_part, m_bar, eg,
                                w_bar=gr["force_head.w"].view(-1))
@@ -973,15 +973,15 @@ class ReferenceScheduleEngine:
                 z_bar = ops.graph_mlp_bwd(u_bar, st["z"], st["pre"], st["act"], None, w[p + "gu.w2"], None,
                                           gr[p + "gu.b1"], gr[p + "gu.w2"], gr[p + "gu.b2"])
             else:
-                z_bar = torch.zeros((G, c.d_u), dtype=f32, device=dev)
+                z_bar = ops.zeros((G, c.d_u), dev)
             cm.all_reduce_(z_bar, phase="backward", block=b, stage="gu", level="global", width=self.R.d_u)
             s_bar = ops.graph_linear_bwd(z_bar, st["s"], w[p + "gu.w1"], w_bar=gr[p + "gu.w1"])
-            v_bar = torch.zeros((V, c.d_v), dtype=f32, device=dev)
+            v_bar = ops.zeros((V, c.d_v), dev)
             if n1 > n0:
                 ops.gather_rows(bg.node_graph[n0:n1], s_bar, out=v_bar[n0:n1])
             if gem:
                 self.clock.mark(f"backward.block{b}.sym")
-                m2_bar = torch.zeros((E, de), dtype=f32, device=dev)
+                m2_bar = ops.zeros((E, de), dev)
                 if e1 > e0:
                     mb = m_bar[e0:e1]
                     _wg(mb, st["m2r"][e0:e1], gr[p + "sym.w"])
@@ -990,12 +990,12 @@ class ReferenceScheduleEngine:
                     ops.scatter_rows(bg.rev[e0:e1], ident[: e1 - e0], t, m2_bar)
                 cm.all_reduce_(m2_bar, phase="backward", block=b, stage="sym", level="edge", width=self.R.d_e)
                 self.clock.mark(f"backward.block{b}.eu2")
-                mn_bar = torch.zeros((E, de), dtype=f32, device=dev)
+                mn_bar = ops.zeros((E, de), dev)
                 if e1 > e0:
                     g2 = m2_bar[e0:e1]
                     w1 = w[p + "eu2.w1"]
                     _wg(g2, st["a2"], gr[p + "eu2.w2"], gr[p + "eu2.b2"])
-                    h2_full = torch.zeros((E, de), dtype=f32, device=dev)
+                    h2_full = ops.zeros((E, de), dev)
                     h2_bar = L(g2, w[p + "eu2.w2"], w_mn=True, aux=st["h2"], flags=ops.EPI_DSILU_AUX,
                                out=h2_full[e0:e1])
                     _wg(h2_bar, st["m_new"][e0:e1], gr[p + "eu2.w1"][:, :de], gr[p + "eu2.b1"])
@@ -1004,7 +1004,7 @@ class ReferenceScheduleEngine:
                     _wg(pv_bar, st["v"], gr[p + "eu2.w1"][:, de:])
                     v_bar = L(pv_bar, w1[:, de:], w_mn=True, resid=v_bar)
             else:
-                mn_bar = torch.zeros((E, de), dtype=f32, device=dev)
+                mn_bar = ops.zeros((E, de), dev)
             self.clock.mark(f"backward.block{b}.nu")
             cm.all_reduce_(v_bar, phase="backward", block=b, stage="nu", level="node", width=self.R.d_v)
             if n1 > n0:
@@ -1019,8 +1019,8 @@ class ReferenceScheduleEngine:
                 _rows_add(mn_bar, m_bar, ident)
             m_new_bar = mn_bar
             self.clock.mark(f"backward.block{b}.eu")
-            ta_bar = torch.zeros((E, de), dtype=f32, device=dev)
-            m_in = torch.zeros((E, de), dtype=f32, device=dev)
+            ta_bar = ops.zeros((E, de), dev)
+            m_in = ops.zeros((E, de), dev)
             if e1 > e0:
                 g1 = m_new_bar[e0:e1]
                 w1 = w[p + "eu.w1"]
@@ -1035,7 +1035,7 @@ class ReferenceScheduleEngine:
             if has_t:
                 tb = ta_bar[ra:rb]
                 _wg(tb, st["Y"], gr[p + "tu.up"])
-                S_bar = torch.zeros_like(st["S"])
+                S_bar = ops.zeros(tuple(st["S"].shape), dev)
                 if gem:
                     Z_bar, Y_bar = L(tb, w[p + "tu.up"], w_mn=True, aux=st["g"], flags=ops.EPI_MUL_AUX)
                     _wg(Z_bar, st["S"][ra:rb], gr[p + "tu.bilinear_proj"])
@@ -1043,11 +1043,11 @@ class ReferenceScheduleEngine:
                     g_prod = (Y_bar, st["Z"])
                 else:
                     Y_bar = L(tb, w[p + "tu.up"], w_mn=True)
-                    torch.mul(Y_bar, st["g"], out=S_bar[ra:rb])
+                    ops.hadamard(Y_bar, st["g"], out=S_bar[ra:rb])
                     g_prod = (Y_bar, st["S"][ra:rb])
                 ops.rbf_linear_bwd(fw.rbf[ra:rb], w[p + "tu.rbf_gate"], g_prod[0], rbf_bar[ra:rb],
                                    gr[p + "tu.rbf_gate"], g2=g_prod[1])
-                X_bar = torch.zeros_like(st["X"])
+                X_bar = ops.zeros(tuple(st["X"].shape), dev)
                 Wk_bar = ops.triplet_bwd_window(d["ep_t"], bg.rev, bg.geo, st["X"], st["Wk"], c.cutoff, self.flo,
                                                 self.lhi, S_bar, eg, X_bar, bg.max_deg)
                 if gem:
@@ -1059,7 +1059,7 @@ class ReferenceScheduleEngine:
                     post.append((w[p + "tu.bilinear_a"], T, gr[p + "tu.down"], 1, 0, 0))
                     m_in = L(X_bar, st["Wx"], w_mn=True, resid=m_in)
                 else:
-                    gr[p + "tu.sbf_gate"].copy_(Wk_bar.permute(2, 0, 1).reshape(Wk_bar.shape[2], -1))
+                    ops.transpose_into(Wk_bar.view(-1, Wk_bar.shape[2]), gr[p + "tu.sbf_gate"])
                     _wg(X_bar, st["m"], gr[p + "tu.down"])
                     m_in = L(X_bar, w[p + "tu.down"], w_mn=True, resid=m_in)
             m_bar = cm.all_reduce_(m_in, phase="backward", block=b, stage="m_in", level="edge", width=self.R.d_e)
@@ -1127,7 +1127,7 @@ class GPTrainer:
                                         self.w_forces, self.n)
             loss = loss + lf
             if self.reference:
-                full = torch.zeros((self.bg.num_nodes, 3), dtype=torch.float32, device=self.bg.device)
+                full = ops.zeros((self.bg.num_nodes, 3), self.bg.device)
                 full[self.n0:self.n1] = d_f
                 d_f = full
         self.engine.backward(self.bg, fw, d_e, d_f)

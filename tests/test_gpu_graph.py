@@ -232,3 +232,27 @@ def test_neighbour_cap_periodic():
     np.testing.assert_array_equal(t.edge_recv.cpu().numpy(), ref.recv)
     np.testing.assert_array_equal(bg.img.cpu().numpy(), ref.img)
     np.testing.assert_array_equal(t.reverse_edges().cpu().numpy(), ref.rev)
+
+
+def test_device_utilities():
+    """egn_zero / egn_hadamard / egn_transpose / egn_csr_ptr (the step's non-framework
+    elementwise work) against torch."""
+    from paper_2203_09697_b200 import ops
+
+    g = torch.Generator(device="cuda").manual_seed(3)
+    for n in (0, 1, 7, 4096, 4099):
+        a = torch.randn(n, device="cuda", generator=g)
+        b = torch.randn(n, device="cuda", generator=g)
+        assert torch.equal(ops.hadamard(a, b), a * b)
+    t = torch.randn((1000, 64), device="cuda", generator=g)
+    ops.zero_(t)
+    assert not t.any()
+    src = torch.randn((42, 70), device="cuda", generator=g)
+    big = torch.full((70, 50), float("nan"), device="cuda")
+    ops.transpose_into(src, big[:, 3:45])
+    assert torch.equal(big[:, 3:45], src.t())
+    assert torch.isnan(big[:, :3]).all() and torch.isnan(big[:, 45:]).all()
+    keys = torch.tensor([0, 0, 1, 3, 3, 3, 6], dtype=torch.int64, device="cuda")
+    assert ops.csr_ptr(keys, 8).cpu().tolist() == [0, 2, 3, 3, 6, 6, 6, 7, 7]
+    with pytest.raises(ValueError):
+        ops.hadamard(a, torch.randn(n + 1, device="cuda"))
