@@ -101,6 +101,19 @@ __global__ void aggregate_in_edges_v4_kernel(const int64_t* __restrict__ edge_pt
         const int nb = static_cast<int>(e1 - b < 32 ? e1 - b : 32);
         const int32_t my = lane < nb ? rev[b + lane] : 0;
         int j = 0;
+        for (; j + 8 <= nb; j += 8) {  // 8 rows in flight per lane (a node has ~25 in-edges at C2)
+          float4 t[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int32_t r = __shfl_sync(0xffffffffu, my, j + u);
+            t[u] = on ? __ldg(reinterpret_cast<const float4*>(x + static_cast<int64_t>(r) * ldx + c))
+                      : make_float4(0.f, 0.f, 0.f, 0.f);
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {  // same order as the scalar path: edge after edge
+            acc.x += t[u].x; acc.y += t[u].y; acc.z += t[u].z; acc.w += t[u].w;
+          }
+        }
         for (; j + 4 <= nb; j += 4) {
           float4 t[4];
 #pragma unroll
@@ -110,7 +123,7 @@ __global__ void aggregate_in_edges_v4_kernel(const int64_t* __restrict__ edge_pt
                       : make_float4(0.f, 0.f, 0.f, 0.f);
           }
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {  // same order as the scalar path: edge after edge
+          for (int u = 0; u < 4; ++u) {
             acc.x += t[u].x; acc.y += t[u].y; acc.z += t[u].z; acc.w += t[u].w;
           }
         }
@@ -354,10 +367,19 @@ __global__ void rbf_linear_kernel(const float* __restrict__ rbf, int64_t ne, int
   for (int i = threadIdx.x; i < N; i += blockDim.x) ws[K * N + i] = b ? b[i] : 0.f;
   __syncthreads();
   const int n4 = N >> 2;
-  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < ne * n4;
-       idx += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t e = idx / n4;
-    const int c = static_cast<int>(idx - e * n4) * 4;
+  // the column chunk is fixed per thread when the stride is a multiple of N / 4 (the usual
+  // case): no 64-bit division per output
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const bool fixed = stride % n4 == 0;
+  const int64_t t0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int c_fixed = static_cast<int>(t0 % n4) * 4;
+  const int64_t de = stride / n4;
+  for (int64_t idx = t0, e = t0 / n4; idx < ne * n4; idx += stride, e += de) {
+    int c = c_fixed;
+    if (!fixed) {
+      e = idx / n4;
+      c = static_cast<int>(idx - e * n4) * 4;
+    }
     float4 o = *reinterpret_cast<const float4*>(ws + K * N + c);
     for (int k = 0; k < K; ++k) {
       const float r = __ldg(rbf + e * K + k);
@@ -455,7 +477,7 @@ __global__ void __launch_bounds__(256) rbf_linear_bwd_kernel(const float* __rest
 // is an 8-value transpose reduction inside the lane group; W_bar[n, k] += g[e, n] rbf[e, k] and
 // b_bar[n] += g[e, n] accumulate in registers, then a fixed-order sum over the CTA's warps (and
 // the lane groups) gives one partial row per CTA (reduced by reduce_parts_kernel).
-template <int LPE, int KT>
+template <int LPE, int KT, int U = 2>
 __global__ void __launch_bounds__(256) rbf_linear_bwd_group_kernel(const float* __restrict__ rbf, int64_t ne,
                                                                    int K, const float* __restrict__ W, int N,
                                                                    const float* __restrict__ g,
@@ -485,11 +507,11 @@ __global__ void __launch_bounds__(256) rbf_linear_bwd_group_kernel(const float* 
   const bool writer = (gl % (LPE / 8)) == 0 && kk < kk_n;
   const int64_t slots = static_cast<int64_t>(gridDim.x) * 8 * EPW;  // edge slots in flight
   const int64_t my = (static_cast<int64_t>(blockIdx.x) * 8 + warp) * EPW + grp;
-  for (int64_t e0 = my; e0 - grp < ne; e0 += 2 * slots) {
-    float gv[2][4], r[2][8], old[2];
-    bool ok[2];
+  for (int64_t e0 = my; e0 - grp < ne; e0 += U * slots) {
+    float gv[U][4], r[U][8], old[U];
+    bool ok[U];
 #pragma unroll
-    for (int u = 0; u < 2; ++u) {
+    for (int u = 0; u < U; ++u) {
       const int64_t e = e0 + u * slots;
       ok[u] = e < ne;
       const int64_t ec = ok[u] ? e : 0;
@@ -504,7 +526,7 @@ __global__ void __launch_bounds__(256) rbf_linear_bwd_group_kernel(const float* 
       old[u] = (writer && ok[u]) ? rbf_bar[ec * kk_n + kk] : 0.f;
     }
 #pragma unroll
-    for (int u = 0; u < 2; ++u) {
+    for (int u = 0; u < U; ++u) {
       float sv[8];
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
@@ -808,8 +830,11 @@ int egn_rbf_linear(const float* rbf, int64_t num_edges, int k, const float* w, c
   EGN_REQUIRE(smem <= 200 * 1024, "rbf_linear: N too large");
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(rbf_linear_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-  rbf_linear_kernel<<<grid_for(num_edges * (n / 4), 256, 148 * 8), 256, smem, as_stream(stream)>>>(
-      rbf, num_edges, k, w, b, n, out, ldo);
+  // grid: a multiple of N / 4 threads in total (fixed column chunk per thread)
+  const int n4 = n / 4;
+  int64_t blocks = grid_for(num_edges * n4, 256, 148 * 8);
+  while ((blocks * 256) % n4 != 0) ++blocks;
+  rbf_linear_kernel<<<static_cast<int>(blocks), 256, smem, as_stream(stream)>>>(rbf, num_edges, k, w, b, n, out, ldo);
   return check_launch("rbf_linear");
 }
 
@@ -840,8 +865,9 @@ int egn_rbf_linear_bwd(const float* rbf, int64_t num_edges, int k, const float* 
   if (group_path) {
     // lane group per edge; grid sized to one wave (the workspace holds rbf_linear_bwd_grid rows)
     grid = std::min(grid, k == 6 ? kNumSMs * 2 : kNumSMs);  // 98 / 136 registers per thread
+    // K = 6: four edges in flight per lane group (128 registers; two: 75 -> 65 us at C2)
 #define EGN_RLB(L)                                                                                      \
-    (k == 6 ? rbf_linear_bwd_group_kernel<L, 6><<<grid, 256, 0, st>>>(rbf, num_edges, k, w, n, g, g2, ldg, rbf_bar, part) \
+    (k == 6 ? rbf_linear_bwd_group_kernel<L, 6, 4><<<grid, 256, 0, st>>>(rbf, num_edges, k, w, n, g, g2, ldg, rbf_bar, part) \
             : rbf_linear_bwd_group_kernel<L, 8><<<grid, 256, 0, st>>>(rbf, num_edges, k, w, n, g, g2, ldg, rbf_bar, part))
     if (lpe == 32) EGN_RLB(32);
     else if (lpe == 16) EGN_RLB(16);
