@@ -205,3 +205,75 @@ def test_bessel_centre_schedule_two_ranks_vs_oracle(variant):
         assert max_rel(np.asarray(gb.d_params[k]), g) < TOL, k
     with pytest.raises(ValueError, match="Gaussian basis only"):
         WorkerGroup(AtomicSystem(pos, z), params, schedule="reference")
+
+
+@pytest.mark.parametrize("variant", list(VARIANTS))
+def test_bessel_bases_on_periodic_cells_vs_oracle(variant):
+    """The Bessel bases on periodic graphs (edges to images, §8(f) f1 x f2): energies, forces,
+    every d_param and d_positions vs the oracle on the same periodic graph."""
+    from paper_2203_09697_b200 import AtomicSystem, ModelConfig, init_params
+    from paper_2203_09697_b200.engine import DeviceWeights, Engine
+    from paper_2203_09697_b200.graph import build_batch
+
+    cfg = ModelConfig(variant=variant, blocks=2, d_u=16, d_v=16, d_e=32, d_t=16, d_bil=16, k_rbf=6, l_sbf=7,
+                      cutoff=3.0, seed=4, basis="bessel")
+    params = init_params(cfg)
+    oc = O.Config(**{k: getattr(cfg, k) for k in O.Config.__dataclass_fields__})
+    rng = np.random.default_rng(23)
+    cells = [np.array([[4.2, 0, 0], [0.5, 4.0, 0], [0.3, 0.2, 4.4]]), np.array([[5.0, 0, 0], [0, 5.0, 0], [0, 0, 30.0]])]
+    pbcs = [(True, True, True), (True, True, False)]
+    systems = []
+    for cell, pbc, n in zip(cells, pbcs, (5, 8)):
+        systems.append(AtomicSystem(rng.uniform(0, 1, (n, 3)) @ cell, np.full(n, 6), cell=cell, pbc=pbc))
+    eng = Engine(DeviceWeights.from_params(params))
+    bg = build_batch(systems, cfg.cutoff)
+    fw = eng.forward(bg)
+    d_e = torch.tensor([0.6, -0.9], device="cuda")
+    df_np = [rng.standard_normal((s.n, 3)) for s in systems] if variant == "gemnet-style" else None
+    pos_bar = eng.backward(bg, fw, d_e, torch.tensor(np.concatenate(df_np), device="cuda") if df_np else None)
+    pos_bar = pos_bar.cpu().numpy()
+    grads = eng.weights.to_numpy(grads=True)
+    ref_g = {k: np.zeros_like(v) for k, v in params.arrays.items()}
+    off = 0
+    for i, s in enumerate(systems):
+        f = O.forward(oc, params.arrays, s.positions, s.atomic_numbers,
+                      graph=O.build_graph_pbc(s.positions, s.cell, s.pbc, cfg.cutoff))
+        G, dp = O.backward(f, params.arrays, float(d_e[i]), df_np[i] if df_np else None)
+        assert abs(float(fw.energy[i]) - f.energy) <= TOL * max(abs(f.energy), 1e-8)
+        assert max_rel(pos_bar[off:off + s.n], dp) < TOL
+        for k in ref_g:
+            ref_g[k] += G[k]
+        off += s.n
+    for k, g in ref_g.items():
+        assert max_rel(grads[k], g) < TOL, k
+
+
+def test_bessel_captured_trainer_with_isolated_atoms(monkeypatch):
+    """The captured multi-stream training step (bench path) on the Bessel bases over a batch
+    with an isolated atom and a two-atom graph (no triplets) next to an ordinary graph: the
+    loss and every gradient equal the oracle's loss_and_grads."""
+    from paper_2203_09697_b200 import ModelConfig, init_params
+    from paper_2203_09697_b200.graph import build_batch
+    from paper_2203_09697_b200.tasks import Trainer
+
+    monkeypatch.setenv("EGN_SIDE_MIN_EDGES", "0")
+    cfg = ModelConfig(variant="gemnet-style", blocks=2, d_u=16, d_v=16, d_e=32, d_t=16, d_bil=16, k_rbf=6,
+                      l_sbf=7, cutoff=5.0, seed=6, basis="bessel")
+    params = init_params(cfg)
+    rng = np.random.default_rng(5)
+    systems = [np.zeros((1, 3)), np.array([[0.0, 0.0, 0.0], [1.1, 0.2, -0.3]]), O.random_cloud(20, 0.1, rng)[0]]
+    e_t = rng.standard_normal(3)
+    f_t = np.concatenate([rng.standard_normal((s.shape[0], 3)) for s in systems])
+    tr = Trainer(params, None, e_t, f_t, 1.0, 0.5, graph=build_batch(systems, cfg.cutoff), cuda_graph=True)
+    tr.step(0.0)
+    loss = float(tr.step(0.0))
+    grads = tr.weights.to_numpy(grads=True)
+    oc = O.Config(**{k: getattr(cfg, k) for k in O.Config.__dataclass_fields__})
+    z = [np.full(s.shape[0], 6) for s in systems]
+    loss_ref, g_ref = O.loss_and_grads(oc, params.arrays, [(s, zz, e, f) for s, zz, e, f in
+                                                           zip(systems, z, e_t, np.split(f_t, np.cumsum(
+                                                               [s.shape[0] for s in systems])[:-1]))],
+                                       w_energy=1.0, w_forces=0.5)
+    assert abs(loss - loss_ref) <= 1e-5 * abs(loss_ref)
+    for k, g in g_ref.items():
+        assert max_rel(grads[k], g) < TOL, k
