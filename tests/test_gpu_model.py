@@ -633,3 +633,35 @@ def test_model_on_spherical_harmonic_triplet_kernels(variant):
         off += n
     for k, g in ref_g.items():
         assert max_rel(grads[k], g) < TOL, k
+
+
+@pytest.mark.parametrize("variant", ["dimenet-style", "gemnet-style"])
+def test_captured_step_with_degenerate_graphs(variant, monkeypatch):
+    """The captured multi-stream training step over a batch holding an isolated atom, a dimer
+    (no triplets) and an ordinary graph: loss and every gradient equal the oracle's
+    loss_and_grads (the bench path on the graphs the kernels special-case)."""
+    from paper_2203_09697_b200 import ModelConfig, init_params
+    from paper_2203_09697_b200.graph import build_batch
+    from paper_2203_09697_b200.tasks import Trainer
+
+    monkeypatch.setenv("EGN_SIDE_MIN_EDGES", "0")
+    cfg = ModelConfig(variant=variant, blocks=2, d_u=16, d_v=16, d_e=32, d_t=16, d_bil=16, k_rbf=6, l_sbf=7,
+                      cutoff=5.0, seed=9)
+    params = init_params(cfg)
+    rng = np.random.default_rng(8)
+    systems = [np.zeros((1, 3)), np.array([[0.0, 0.0, 0.0], [0.9, -0.4, 0.5]]), O.random_cloud(24, 0.1, rng)[0]]
+    w_f = 0.5 if variant == "gemnet-style" else 0.0
+    e_t = rng.standard_normal(3)
+    f_t = np.concatenate([rng.standard_normal((s.shape[0], 3)) for s in systems])
+    tr = Trainer(params, None, e_t, f_t if w_f else None, 1.0, w_f, graph=build_batch(systems, cfg.cutoff),
+                 cuda_graph=True)
+    tr.step(0.0)
+    loss = float(tr.step(0.0))
+    grads = tr.weights.to_numpy(grads=True)
+    oc = O.Config(**{k: getattr(cfg, k) for k in O.Config.__dataclass_fields__})
+    f_split = np.split(f_t, np.cumsum([s.shape[0] for s in systems])[:-1])
+    data = [(s, np.full(s.shape[0], 6), e, f) for s, e, f in zip(systems, e_t, f_split)]
+    loss_ref, g_ref = O.loss_and_grads(oc, params.arrays, data, w_energy=1.0, w_forces=w_f)
+    assert abs(loss - loss_ref) <= 1e-5 * abs(loss_ref)
+    for k, g in g_ref.items():
+        assert max_rel(grads[k], g) < TOL, k
