@@ -238,7 +238,7 @@ __global__ void force_gather_warp_kernel(const int64_t* __restrict__ edge_ptr, c
 // Adjoint of the force head, lane group per edge (LPE = d / 4 lanes, float4 columns), two
 // edges in flight: m_bar += sbar w, edge_grad += unit-vector adjoint, w_bar partial per CTA
 // (fixed-order sum over the CTA's lane groups).  sbar = f_bar[recv] . u.
-template <int LPE>
+template <int LPE, int U = 4>
 __global__ void __launch_bounds__(256) force_bwd_group_kernel(const int32_t* __restrict__ recv,
                                                               const float4* __restrict__ geo, int64_t ne,
                                                               const float* __restrict__ m, int d,
@@ -255,12 +255,12 @@ __global__ void __launch_bounds__(256) force_bwd_group_kernel(const int32_t* __r
   float4 wacc = make_float4(0.f, 0.f, 0.f, 0.f);
   const int64_t slots = static_cast<int64_t>(gridDim.x) * 8 * EPW;
   const int64_t my = (static_cast<int64_t>(blockIdx.x) * 8 + warp) * EPW + grp;
-  for (int64_t e0 = my; e0 - grp < ne; e0 += 2 * slots) {
-    float4 g[2], mv[2], mb[2];
-    float sb[2];
-    bool ok[2];
+  for (int64_t e0 = my; e0 - grp < ne; e0 += U * slots) {  // U edges in flight per lane group
+    float4 g[U], mv[U], mb[U];
+    float sb[U];
+    bool ok[U];
 #pragma unroll
-    for (int u = 0; u < 2; ++u) {
+    for (int u = 0; u < U; ++u) {
       const int64_t e = e0 + u * slots;
       ok[u] = e < ne;
       const int64_t ec = ok[u] ? e : 0;
@@ -271,7 +271,7 @@ __global__ void __launch_bounds__(256) force_bwd_group_kernel(const int32_t* __r
       mb[u] = ok[u] ? reinterpret_cast<const float4*>(mbar + ec * d)[gl] : make_float4(0.f, 0.f, 0.f, 0.f);
     }
 #pragma unroll
-    for (int u = 0; u < 2; ++u) {
+    for (int u = 0; u < U; ++u) {
       if (!ok[u]) continue;
       const int64_t e = e0 + u * slots;
       const float s = sb[u];
