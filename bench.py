@@ -70,10 +70,12 @@ def _args():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="gemnet-t-oc20")
     ap.add_argument("--graphs", type=int, default=None, help="override graphs per GPU")
-    ap.add_argument("--partition", choices=["aligned", "centre", "balanced", "reference"], default="aligned",
-                    help="aligned: whole graphs per rank (data parallel); centre (alias balanced): centre "
-                         "ranges balanced by triplet count inside graphs, halo exchanges every block; "
-                         "reference: the reference's split_range shards and full-buffer all-reduces")
+    ap.add_argument("--partition", choices=["aligned", "centre", "center-aligned", "reference", "balanced"],
+                    default="aligned",
+                    help="aligned: whole graphs per rank (data parallel); centre (SURVEY 8(e) 'center-aligned', "
+                         "the performance mode): centre ranges balanced by triplet count inside graphs, halo "
+                         "exchanges every block; reference (SURVEY 8(e) 'balanced', the parity mode): the "
+                         "reference's split_range shards and full-buffer all-reduces (CommLog == comm_volume)")
     ap.add_argument("--cpu-budget", type=float, default=12.0, help="seconds of CPU oracle sampling")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--basis", choices=["gaussian", "bessel"], default="gaussian",
@@ -565,8 +567,7 @@ def run_ours(args, wl):
 
 def main():
     args = _args()
-    if args.partition == "balanced":
-        args.partition = "centre"
+    args.partition = {"balanced": "reference", "center-aligned": "centre"}.get(args.partition, args.partition)
     wl = dict(WORKLOADS[args.workload], basis=args.basis)
     if args.impl == "reference":
         run_reference(args, wl)
