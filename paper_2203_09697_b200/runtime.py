@@ -1203,6 +1203,8 @@ class WorkerGroup:
                  align_graphs: bool = False):
         from .graph import build_batch, geometry_of, topology_of
 
+        # SURVEY 8(e) names: "balanced" (the parity mode) and "center-aligned" (the performance mode)
+        schedule = {"balanced": "reference", "center-aligned": "centre"}.get(schedule, schedule)
         if schedule not in ("reference", "centre"):
             raise ValueError(f"schedule must be 'reference' or 'centre', got {schedule!r}")
         self.system = system
