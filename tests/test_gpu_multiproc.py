@@ -111,10 +111,11 @@ def test_two_process_gp_step_equals_single_process(schedule):
             assert "edge" in levels and "node" in levels  # real halo exchanges happened
 
 
-@pytest.mark.parametrize("partition", ["centre", "aligned"])
+@pytest.mark.parametrize("partition", ["centre", "aligned", "balanced"])
 def test_bench_multi_rank_path_runs(partition):
     """bench.py under torchrun with 2 ranks (gloo on one GPU): the centre partition with halos,
-    and the default graph-aligned data parallelism (captured step + gradient all-reduce)."""
+    the default graph-aligned data parallelism (captured step + gradient all-reduce) and the
+    reference parity schedule ("balanced")."""
     env = dict(os.environ, EGN_DIST_BACKEND="gloo")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
            "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), str(ROOT / "bench.py"), "--gpus", "2",
@@ -124,7 +125,8 @@ def test_bench_multi_rank_path_runs(partition):
     assert out.returncode == 0, out.stderr[-3000:]
     line = json.loads([ln for ln in out.stdout.splitlines() if ln.startswith("{")][-1])
     assert line["n_gpus"] == 2 and line["value"] > 0
-    assert ("centre" if partition == "centre" else "graph-aligned") in line["config"]["parallelism"]
+    expect = {"centre": "centre", "aligned": "graph-aligned", "balanced": "reference schedule"}[partition]
+    assert expect in line["config"]["parallelism"]
 
 
 def _nccl_worker(port, q):
