@@ -439,7 +439,8 @@ def run_ours(args, wl):
             part = partition_centers(bg.deg.cpu().numpy(), world)
         else:
             part = partition_reference(bg.tri_ptr.cpu().numpy(), bg.num_edges, bg.num_nodes, world)
-        tr = GPTrainer(params, bg, e_t, f_t, 1.0, wl["w_forces"], comm, part)
+        tr = GPTrainer(params, bg, e_t, f_t, 1.0, wl["w_forces"], comm, part,
+                       cuda_graph=use_graph and backend == "nccl")
         parallelism = f"gp{world} ({args.partition} schedule, halo exchanges every block, {backend})"
 
     def barrier():

@@ -1089,7 +1089,7 @@ class GPTrainer:
 
     def __init__(self, params, bg: BatchGraph, e_target, f_target, w_energy: float, w_forces: float, comm: Comm,
                  part, device="cuda", dp_comm: Comm | None = None, global_graphs: int | None = None,
-                 chunks: int = 2):
+                 chunks: int = 2, cuda_graph: bool = False):
         """part: CenterPartition (centre schedule) or ReferencePartition (reference schedule).
         dp_comm / global_graphs: GP x DP composition -- this replica's graphs are part of a
         global batch of `global_graphs`; after the graph-parallel backward the parameter
@@ -1111,6 +1111,12 @@ class GPTrainer:
         sizes = torch.as_tensor(bg.graph_sizes, dtype=torch.float64, device=bg.device)
         self.atom_count = sizes.repeat_interleave(torch.as_tensor(bg.graph_sizes, device=bg.device))[self.n0:self.n1]
         self.w_energy, self.w_forces = float(w_energy), float(w_forces)
+        # cuda_graph: the whole graph-parallel step -- compute and its NCCL collectives -- is
+        # captured once and replayed (NCCL communicators can be captured; gloo ones cannot,
+        # and a failed capture falls back to eager steps)
+        self.cuda_graph = bool(cuda_graph)
+        self._graph = None
+        self._graph_loss = None
 
     def loss_and_grads(self) -> torch.Tensor:
         fw = self.engine.forward(self.bg)
@@ -1140,10 +1146,37 @@ class GPTrainer:
         return loss
 
     def step(self, lr: float) -> torch.Tensor:
-        loss = self.loss_and_grads()
+        if self.cuda_graph and self._graph is not None:
+            self._graph.replay()
+            loss = self._graph_loss
+        else:
+            loss = self.loss_and_grads()
+            if self.cuda_graph:
+                self._capture()
         if lr != 0.0:
             self.weights.sgd_(lr)
         return loss
+
+    def _capture(self):
+        """Capture loss_and_grads (after one eager step sized every workspace and cached the
+        partition's host-side prep)."""
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        graph = torch.cuda.CUDAGraph()
+        try:
+            with torch.cuda.stream(side):
+                with torch.cuda.graph(graph, stream=side):
+                    self._graph_loss = self.loss_and_grads()
+        except Exception as exc:  # noqa: BLE001 (e.g. a gloo communicator)
+            import sys
+
+            torch.cuda.synchronize()
+            print(f"[egn] CUDA-graph capture of the graph-parallel step failed ({exc!r}); running eagerly",
+                  file=sys.stderr)
+            self.cuda_graph = False
+            return
+        torch.cuda.current_stream().wait_stream(side)
+        self._graph = graph
 
 
 # ---------------------------------------------------------------------------

@@ -149,6 +149,11 @@ def _nccl_worker(port, q):
                     else partition_reference(bg.tri_ptr.cpu().numpy(), bg.num_edges, bg.num_nodes, 1))
             tr = GPTrainer(params, bg, e_t, f_t, 1.0, 0.5, DistComm(), part)
             out[name] = (float(tr.step(0.0)), tr.weights.grad_flat.double().cpu().numpy())
+            # the captured step (compute + NCCL collectives in one CUDA graph), replayed
+            trg = GPTrainer(params, bg, e_t, f_t, 1.0, 0.5, DistComm(), part, cuda_graph=True)
+            trg.step(0.0)
+            assert trg._graph is not None, "capture failed"
+            out[name + "-graph"] = (float(trg.step(0.0)), trg.weights.grad_flat.double().cpu().numpy())
         # graph-aligned data parallelism (bench.py's default N > 1 path): gradient all-reduce
         tr = Trainer(params, None, e_t, f_t, 1.0, 0.5, graph=bg, comm=DistComm(), global_graphs=len(systems),
                      cuda_graph=True)
