@@ -117,3 +117,30 @@ def test_dimenet_c1_bench_step_matches_oracle(gemm_path):
         _check(tr, cfg, systems, params, e_t, None, 0.0, loss)
     finally:
         _lib.call("egn_gemm_simt_max_m", old)
+
+
+@pytest.mark.parametrize("args", [["--workload", "dimenet-pp-small"],
+                                  ["--workload", "dimenet-pp-small", "--basis", "bessel"]])
+def test_bench_line_contract(args):
+    """bench.py's JSON line (the driver's contract): metric, value, e2e with its copy sizes,
+    gpu_launches, roofline with its bound / achieved / peak / frac, clocks, config naming the
+    workload (and the basis when it is not the reference's)."""
+    import json
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parents[1]
+    out = subprocess.run([sys.executable, str(root / "bench.py"), *args, "--steps", "3", "--warmup", "3",
+                          "--no-cpu-baseline"], capture_output=True, text=True, timeout=900, cwd=str(root))
+    assert out.returncode == 0, out.stderr[-3000:]
+    line = json.loads([ln for ln in out.stdout.splitlines() if ln.startswith("{")][-1])
+    assert line["n_gpus"] == 1 and line["steps"] == 3 and line["warmup"] == 3 and line["value"] > 0
+    assert line["higher_is_better"] is True and line["scaling"] == "weak" and line["dtype"] == "f32"
+    assert line["e2e"]["value"] > 0 and line["e2e"]["h2d_bytes_per_step"] > 0 and line["e2e"]["d2h_bytes_per_step"] > 0
+    assert line["gpu_launches"] > 100
+    roof = line["roofline"]
+    assert roof["bound"] in ("hbm", "tensor") and 0 < roof["frac"] <= 1.2 and roof["peak"] > 0
+    assert line["config"]["workload"] == "dimenet-pp-small"
+    assert ("basis" in line["config"]) == ("bessel" in args)
+    assert "sm_mhz" in line["clocks"]

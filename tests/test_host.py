@@ -156,3 +156,23 @@ def test_torch_custom_ops_registered_with_fake_kernels():
         assert torch.ops.egn.positions_bwd(ep, rev, geo, torch.empty((E, 4))).dtype == torch.float64
         s, f = torch.ops.egn.force_head(ep, rev, geo, X, torch.empty(dg))
         assert s.shape == (E,) and f.shape == (V, 3)
+
+
+def test_bench_reference_arm_contract():
+    """bench.py --impl reference on the host (no GPU): one JSON line with the contract keys the
+    driver reads (impl, metric, value, unit, e2e, cpu_baseline with cores / kind / sample)."""
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parents[1]
+    out = subprocess.run([sys.executable, str(root / "bench.py"), "--impl", "reference", "--workload",
+                          "dimenet-pp-small", "--steps", "1", "--warmup", "0", "--graphs", "1"],
+                         capture_output=True, text=True, timeout=600, cwd=str(root))
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads([ln for ln in out.stdout.splitlines() if ln.startswith("{")][-1])
+    assert line["impl"] == "reference" and line["value"] > 0 and line["higher_is_better"] is True
+    assert line["metric"].startswith("triplet-interactions/s") and line["unit"] == "triplets/s"
+    assert line["e2e"]["value"] == line["value"] and line["e2e"]["h2d_bytes_per_step"] == 0
+    cb = line["cpu_baseline"]
+    assert cb["kind"] == "port" and cb["cores"] >= 1 and cb["sample"] and cb["value"] == line["value"]
