@@ -69,6 +69,9 @@ SIGNATURES: dict[str, tuple] = {
                                      _p]),
     "egn_triplet_bwd_basis": (_i32, [_p, _p, _p, _i64, _i64, _i32, _p, _p, _i32, _i32, _i32, _f64, _i32, _p, _p, _p,
                                      _p, _p, _p]),
+    "egn_triplet_bwd_angle_workspace_bytes": (_i64, [_i64, _i32]),
+    "egn_triplet_bwd_basis_ex": (_i32, [_p, _p, _p, _i64, _i64, _i32, _p, _p, _i32, _i32, _i32, _f64, _i32, _i32, _p, _p,
+                                        _p, _p, _p, _p]),
     "egn_rbf_bessel": (_i32, [_p, _i64, _i32, _f64, _p, _p]),
     "egn_rbf_bessel_bwd": (_i32, [_p, _p, _i64, _i32, _f64, _p, _p]),
     "egn_triplet_fwd_window": (_i32, [_p, _p, _p, _i64, _i64, _i64, _p, _p, _i32, _i32, _i32, _f64, _p, _p]),
@@ -146,7 +149,7 @@ def stream() -> int:
 
 # Kernels launched per successful ABI call (for the bench's gpu_launches count).
 KERNELS_PER_CALL = {
-    "egn_triplet_bwd": 4, "egn_triplet_bwd_ex": 2, "egn_triplet_fwd": 2, "egn_triplet_fwd_basis": 3, "egn_triplet_bwd_basis": 4, "egn_triplet_bwd_window": 2, "egn_graph_linear_bwd": 2, "egn_geometry_grads": 2, "egn_force_head_fwd": 2, "egn_force_head_bwd": 2, "egn_column_sum": 2, "egn_gemm_wgrad": 2, "egn_rbf_linear_bwd": 2, "egn_graph_mlp_fwd": 2, "egn_graph_mlp_bwd": 3, "egn_cap_keep": 2, "egn_cap_compact": 2,
+    "egn_triplet_bwd": 4, "egn_triplet_bwd_ex": 2, "egn_triplet_fwd": 2, "egn_triplet_fwd_basis": 3, "egn_triplet_bwd_basis": 4, "egn_triplet_bwd_basis_ex": 2, "egn_triplet_bwd_window": 2, "egn_graph_linear_bwd": 2, "egn_geometry_grads": 2, "egn_force_head_fwd": 2, "egn_force_head_bwd": 2, "egn_column_sum": 2, "egn_gemm_wgrad": 2, "egn_rbf_linear_bwd": 2, "egn_graph_mlp_fwd": 2, "egn_graph_mlp_bwd": 3, "egn_cap_keep": 2, "egn_cap_compact": 2,
 }
 LAUNCH_COUNTER = {"calls": 0, "kernels": 0}
 _NOT_LAUNCHES = {"egn_triplet_path", "egn_abi_version"}

@@ -549,11 +549,13 @@ __global__ void reduce_partials_kernel(const float* __restrict__ part, int npart
 // fast path (triplet_fast.cu): centres with deg <= 64 and (K, L) = (6, 7)
 bool fast_supported(int K, int L, int dg);
 int fast_fwd(const int64_t* edge_ptr, const int32_t* rev, const float4* geo, int64_t nv, const float* X,
-             const float* W, int K, int L, int dg, RbfParams rp, float* S, cudaStream_t st);
+             const float* W, int K, int L, int dg, RbfParams rp, float* S, cudaStream_t st, int mode = 0,
+             const float* rtab = nullptr);
 int64_t fast_bwd_workspace_bytes(int64_t nv, int64_t ne, int K, int L, int dg);
 int fast_bwd(const int64_t* edge_ptr, const int32_t* rev, const float4* geo, int64_t nv, int64_t ne,
              const float* X, const float* W, int K, int L, int dg, RbfParams rp, const float* Sbar, float* Xbar,
-             float* Wbar, float4* edge_grad, void* ws, cudaStream_t st, int phases);
+             float* Wbar, float4* edge_grad, void* ws, cudaStream_t st, int phases, int mode = 0,
+             const float* rtab = nullptr, const float* dtab = nullptr);
 constexpr int kFastMaxDeg = 64;
 // spherical-harmonic factorised path (triplet_sh.cu): O(deg) per edge
 bool sh_supported(int K, int L, int dg);
@@ -877,17 +879,61 @@ int egn_triplet_fwd_basis(const int64_t* edge_ptr, const int32_t* rev, const flo
   float* tab = reinterpret_cast<float*>(reinterpret_cast<char*>(workspace) +
                                         align256(sh_fwd_workspace_bytes(num_nodes, max_degree, k_rbf, l_sbf, dg)));
   if (int rc = sh_radial_table(g4, num_edges, static_cast<float>(cutoff), basis, tab, nullptr, st)) return rc;
+  int min_n = 0;
+  if (basis == 1 && g_triplet_path != 1 && fast_supported(k_rbf, l_sbf, dg)) {
+    // GemNet-T CBF on the pairwise small-degree kernels (Legendre angular rows, radial rows from
+    // the table); the spherical-harmonic kernels take the centres above their range
+    if (int rc = fast_fwd(edge_ptr, rev, g4, num_nodes, X, W, k_rbf, l_sbf, dg, rbf_params(k_rbf, cutoff), S, st,
+                          1, tab))
+      return rc;
+    if (max_degree <= kFastMaxDeg) return 0;
+    min_n = kFastMaxDeg;
+  }
   return sh_fwd(edge_ptr, rev, g4, num_nodes, max_degree, X, W, k_rbf, l_sbf, dg, rbf_params(k_rbf, cutoff),
-                static_cast<float>(cutoff), basis, S, workspace, 0, st, tab);
+                static_cast<float>(cutoff), basis, S, workspace, min_n, st, tab);
 }
+
+int egn_triplet_bwd_basis_ex(const int64_t* edge_ptr, const int32_t* rev, const float* geo, int64_t num_nodes,
+                             int64_t num_edges, int max_degree, const float* X, const float* W, int k_rbf, int l_sbf,
+                             int dg, double cutoff, int basis, int phases, const float* S_bar, float* X_bar,
+                             float* W_bar, float* edge_grad, void* workspace, egn_stream_t stream);
 
 int egn_triplet_bwd_basis(const int64_t* edge_ptr, const int32_t* rev, const float* geo, int64_t num_nodes,
                           int64_t num_edges, int max_degree, const float* X, const float* W, int k_rbf, int l_sbf,
                           int dg, double cutoff, int basis, const float* S_bar, float* X_bar, float* W_bar,
                           float* edge_grad, void* workspace, egn_stream_t stream) {
+  return egn_triplet_bwd_basis_ex(edge_ptr, rev, geo, num_nodes, num_edges, max_degree, X, W, k_rbf, l_sbf, dg,
+                                  cutoff, basis, 3, S_bar, X_bar, W_bar, edge_grad, workspace, stream);
+}
+
+int64_t egn_triplet_bwd_angle_workspace_bytes(int64_t num_edges, int basis) {
+  return sh_radial_table_floats(num_edges, basis) * 4;
+}
+
+int egn_triplet_bwd_basis_ex(const int64_t* edge_ptr, const int32_t* rev, const float* geo, int64_t num_nodes,
+                             int64_t num_edges, int max_degree, const float* X, const float* W, int k_rbf, int l_sbf,
+                             int dg, double cutoff, int basis, int phases, const float* S_bar, float* X_bar,
+                             float* W_bar, float* edge_grad, void* workspace, egn_stream_t stream) {
   if (basis == 0)
-    return egn_triplet_bwd(edge_ptr, rev, geo, num_nodes, num_edges, max_degree, X, W, k_rbf, l_sbf, dg, cutoff,
-                           S_bar, X_bar, W_bar, edge_grad, workspace, stream);
+    return egn_triplet_bwd_ex(edge_ptr, rev, geo, num_nodes, num_edges, max_degree, X, W, k_rbf, l_sbf, dg, cutoff,
+                              S_bar, X_bar, W_bar, edge_grad, phases, workspace, stream);
+  EGN_REQUIRE(phases >= 1 && phases <= 3, "phases must be 1, 2 or 3");
+  // the angle phase splits off only on the small-degree kernels of the GemNet basis
+  const bool split_ok = basis == 1 && g_triplet_path != 1 && fast_supported(k_rbf, l_sbf, dg);
+  if (!split_ok) {
+    if (phases == 1) return 0;
+    phases = 3;
+  }
+  if (phases == 1) {  // own radial table in its own workspace (egn_triplet_bwd_angle_workspace_bytes)
+    if (int rc = check_dims(k_rbf, l_sbf, dg)) return rc;
+    if (num_nodes == 0) return 0;
+    cudaStream_t st = as_stream(stream);
+    const float4* g4 = reinterpret_cast<const float4*>(geo);
+    float* tab = reinterpret_cast<float*>(workspace);
+    if (int rc = sh_radial_table(g4, num_edges, static_cast<float>(cutoff), basis, tab, nullptr, st)) return rc;
+    return fast_bwd(edge_ptr, rev, g4, num_nodes, num_edges, X, W, k_rbf, l_sbf, dg, rbf_params(k_rbf, cutoff), S_bar,
+                    X_bar, W_bar, reinterpret_cast<float4*>(edge_grad), nullptr, st, 1, 1, tab, nullptr);
+  }
   if (int rc = check_dims(k_rbf, l_sbf, dg)) return rc;
   EGN_REQUIRE(basis == 1 || basis == 2, "basis must be 0, 1 or 2");
   EGN_REQUIRE(sh_supported(k_rbf, l_sbf, dg), "the bessel bases need k_rbf = 6, l_sbf = 7");
@@ -905,9 +951,19 @@ int egn_triplet_bwd_basis(const int64_t* edge_ptr, const int32_t* rev, const flo
   float* tab = reinterpret_cast<float*>(tb);
   float* dtab = reinterpret_cast<float*>(tb + align256(sh_radial_table_floats(num_edges, basis) * 4));
   if (int rc = sh_radial_table(g4, num_edges, static_cast<float>(cutoff), basis, tab, dtab, st)) return rc;
+  int min_n = 0, accumulate = 0;
+  if (basis == 1 && g_triplet_path != 1 && fast_supported(k_rbf, l_sbf, dg)) {  // as egn_triplet_fwd_basis
+    char* fws = reinterpret_cast<char*>(workspace) + generic_ws_bytes(num_nodes, k_rbf, l_sbf, dg);
+    if (int rc = fast_bwd(edge_ptr, rev, g4, num_nodes, num_edges, X, W, k_rbf, l_sbf, dg, rbf_params(k_rbf, cutoff),
+                          S_bar, X_bar, W_bar, reinterpret_cast<float4*>(edge_grad), fws, st, phases, 1, tab, dtab))
+      return rc;
+    if (max_degree <= kFastMaxDeg) return 0;
+    min_n = kFastMaxDeg;
+    accumulate = 1;
+  }
   return sh_bwd(edge_ptr, rev, g4, num_nodes, num_edges, max_degree, X, W, k_rbf, l_sbf, dg, rbf_params(k_rbf, cutoff),
-                static_cast<float>(cutoff), basis, S_bar, X_bar, W_bar, reinterpret_cast<float4*>(edge_grad), sws, 0,
-                0, st, tab, dtab);
+                static_cast<float>(cutoff), basis, S_bar, X_bar, W_bar, reinterpret_cast<float4*>(edge_grad), sws,
+                min_n, accumulate, st, tab, dtab);
 }
 
 int egn_triplet_fwd_window(const int64_t* edge_ptr, const int32_t* rev, const float* geo, int64_t num_nodes,

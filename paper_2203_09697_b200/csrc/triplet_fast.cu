@@ -45,14 +45,82 @@ __device__ __forceinline__ float rbf1(float d, int k, RbfParams rp) {
   return __expf(-rp.gamma * dd * dd);
 }
 
-template <int K>
+// Basis MODE of the pairwise kernels: 0 = the reference's Gaussian rbf x cos(l a) = T_l(x);
+// 1 = GemNet-T's CBF: radial Bessel basis e_k(d) (rows of the per-call radial table, stride 8,
+// triplet_sh.cu radial_table_kernel) x Y_l0(a) = sqrt((2l+1)/4pi) P_l(x).
+template <int K, int MODE = 0>
 __device__ __forceinline__ void load_center(float4* Us, float* Rb, const float4* __restrict__ geo, int64_t off,
-                                            int n, RbfParams rp) {
+                                            int n, RbfParams rp, const float* __restrict__ rtab = nullptr,
+                                            float* DRb = nullptr, const float* __restrict__ dtab = nullptr) {
   for (int i = threadIdx.x; i < n; i += kT) Us[i] = geo[off + i];
   for (int i = threadIdx.x; i < n * K; i += kT) {
     const int q = i / K, k = i - q * K;
-    Rb[i] = rbf1(geo[off + q].w, k, rp);
+    if constexpr (MODE == 0) {
+      Rb[i] = rbf1(geo[off + q].w, k, rp);
+    } else {
+      Rb[i] = __ldg(rtab + (off + q) * 8 + k);
+      if (DRb) DRb[i] = __ldg(dtab + (off + q) * 8 + k);
+    }
   }
+}
+
+// angular factor f_l(x) of the basis (masked by m) and the contraction sum_l f_l'(x) z_l
+__constant__ float c_ynorm[8] = {0.28209479177387814f, 0.4886025119029199f, 0.6307831305050401f,
+                                 0.7463526651802308f, 0.8462843753216345f, 0.9356025796273888f,
+                                 1.0171072362820548f, 1.0925484305920792f};  // sqrt((2l+1)/(4 pi))
+template <int L, int MODE>
+__device__ __forceinline__ void angular_row(float x, float m, float (&f)[L]) {
+  if constexpr (MODE == 0) {  // T_l(x) = cos(l a)
+    float tp = m * x, tc = m;
+#pragma unroll
+    for (int l = 0; l < L; ++l) {
+      f[l] = tc;
+      const float tn = fmaf(2.f * x, tc, -tp);
+      tp = tc;
+      tc = tn;
+    }
+  } else {  // Y_l0: P_{l+1} = (2l+1)/(l+1) x P_l - l/(l+1) P_{l-1} (constant coefficients, no division)
+    float pm = 0.f, pc = m;
+#pragma unroll
+    for (int l = 0; l < L; ++l) {
+      f[l] = c_ynorm[l] * pc;
+      const float a = static_cast<float>(2 * l + 1) / static_cast<float>(l + 1);
+      const float b = static_cast<float>(l) / static_cast<float>(l + 1);
+      const float pn = fmaf(a * x, pc, -b * pm);
+      pm = pc;
+      pc = pn;
+    }
+  }
+}
+template <int L, int MODE, typename ZF>
+__device__ __forceinline__ float angular_dcontract(float x, ZF z) {
+  float v = 0.f;
+  if constexpr (MODE == 0) {  // T_l' = l U_{l-1}
+    float um = 0.f, uc = 1.f;
+#pragma unroll
+    for (int l = 1; l < L; ++l) {
+      v = fmaf(static_cast<float>(l) * uc, z(l), v);
+      const float un = fmaf(2.f * x, uc, -um);
+      um = uc;
+      uc = un;
+    }
+  } else {  // P_{l+1}' = P_{l-1}' + (2l+1) P_l
+    float pm = 1.f, pc = x;     // P_0, P_1
+    float dm = 0.f, dc = 1.f;   // P_0', P_1'
+#pragma unroll
+    for (int l = 1; l < L; ++l) {
+      v = fmaf(c_ynorm[l] * dc, z(l), v);
+      const float dn = fmaf(static_cast<float>(2 * l + 1), pc, dm);
+      const float a = static_cast<float>(2 * l + 1) / static_cast<float>(l + 1);
+      const float b = static_cast<float>(l) / static_cast<float>(l + 1);
+      const float pn = fmaf(a * x, pc, -b * pm);
+      dm = dc;
+      dc = dn;
+      pm = pc;
+      pc = pn;
+    }
+  }
+  return v;
 }
 
 // Q chunk: rows (t, l) for t < nq (row stride RS floats), natural channel order; thread
@@ -96,7 +164,7 @@ __device__ __forceinline__ void build_q(float* Qs, const float2 (&wreg)[K][kLP],
 }
 
 // Chebyshev chunk Ct[(t,l)][rslot(p)] = T_l(x_pq) or T_l'(x_pq), masked on p == q / p >= n.
-template <int L, bool DERIV>
+template <int L, bool DERIV, int MODE = 0>
 __device__ __forceinline__ void build_c(float* Ct, const float4* Us, int n, int rows, int q0, int nq) {
   for (int i = threadIdx.x; i < nq * rows; i += kT) {
     const int t = i / rows, p = i - t * rows;
@@ -108,14 +176,10 @@ __device__ __forceinline__ void build_c(float* Ct, const float4* Us, int n, int 
     const float m = ok ? 1.f : 0.f;
     float* dst = Ct + t * L * kCB + rslot(p);
     if (!DERIV) {
-      float tp = m * x, tc = m;
+      float f[L];
+      angular_row<L, MODE>(x, m, f);
 #pragma unroll
-      for (int l = 0; l < L; ++l) {
-        dst[l * kCB] = tc;
-        const float tn = fmaf(2.f * x, tc, -tp);
-        tp = tc;
-        tc = tn;
-      }
+      for (int l = 0; l < L; ++l) dst[l * kCB] = f[l];
     } else {
       // T_l'(x) = l U_{l-1}(x)
       float um = 0.f, uc = 0.f;
@@ -162,11 +226,12 @@ __device__ __forceinline__ void load_wreg(float2 (&wreg)[K][kLP], const float* _
 }
 
 // ---------------------------------------------------------------------------
-template <int K, int L, int MINB = 4>
+template <int K, int L, int MINB = 4, int MODE = 0>
 __global__ void __launch_bounds__(kT, MINB)
 fwd_kernel(const int64_t* __restrict__ edge_ptr, const int32_t* __restrict__ rev,
            const float4* __restrict__ geo, int64_t nv, const float* __restrict__ X,
-           const float* __restrict__ W, int dg, RbfParams rp, float* __restrict__ S) {
+           const float* __restrict__ W, int dg, RbfParams rp, float* __restrict__ S,
+           const float* __restrict__ rtab) {
   __shared__ float4 Us[kN];
   __shared__ float Rb[kN * K];
   __shared__ __align__(16) float Ct[kQC * L * kCB];
@@ -179,7 +244,7 @@ fwd_kernel(const int64_t* __restrict__ edge_ptr, const int32_t* __restrict__ rev
     const int tmr = (n + 15) >> 4;
     const int rows = tmr * 16;
     __syncthreads();
-    load_center<K>(Us, Rb, geo, off, n, rp);
+    load_center<K, MODE>(Us, Rb, geo, off, n, rp, rtab);
     for (int c0 = 0; c0 < dg; c0 += kCB) {
       float2 wreg[K][kLP];
       load_wreg<K, L>(wreg, W, dg, c0 + (tid & 63));
@@ -194,7 +259,7 @@ fwd_kernel(const int64_t* __restrict__ edge_ptr, const int32_t* __restrict__ rev
         const int nq = min(kQC, n - q0);
         __syncthreads();
         build_q<K, L>(Qs, wreg, Rb, xs, q0, nq);
-        build_c<L, false>(Ct, Us, n, rows, q0, nq);
+        build_c<L, false, MODE>(Ct, Us, n, rows, q0, nq);
         __syncthreads();
         if (q0 + kQC < n) load_x(xs, rev, X, off, q0 + kQC, min(kQC, n - q0 - kQC), dg, c0);
         const int nkk = nq * L;
@@ -229,7 +294,7 @@ fwd_kernel(const int64_t* __restrict__ edge_ptr, const int32_t* __restrict__ rev
 // Then the row / column pass turns xbar into dE/dv (edge_grad.xyz += F / d).
 constexpr int kSbStride = kCB + 4;  // padded Sbar / Q rows (bank spread for 16-byte loads)
 
-template <int K, int L, int PP>
+template <int K, int L, int PP, int MODE = 0>
 __device__ __forceinline__ void bw1_tile(const float* Qs, const float* Sb, const float4* Us, float* XB, int n, int q0,
                                          int nq, int G) {
   const int tid = threadIdx.x;
@@ -280,25 +345,18 @@ __device__ __forceinline__ void bw1_tile(const float* Qs, const float* Sb, const
     if (p >= n || p == q) continue;
     const float4 up = Us[p];
     const float x = up.x * uq.x + up.y * uq.y + up.z * uq.z;
-    // sum_l T_l'(x) Z_l with T_l' = l U_{l-1}
-    float um = 0.f, uc = 1.f, v = 0.f;
-#pragma unroll
-    for (int l = 1; l < L; ++l) {
-      v = fmaf(static_cast<float>(l) * uc, zval(l, i), v);
-      const float un = fmaf(2.f * x, uc, -um);
-      um = uc;
-      uc = un;
-    }
+    // sum_l f_l'(x) Z_l
+    const float v = angular_dcontract<L, MODE>(x, [&](int l) { return zval(l, i); });
     XB[p * (kN + 1) + q] += v;  // single owner per (p, q), ordered over channel blocks
   }
 }
 
-template <int K, int L, int MINB = 4>
+template <int K, int L, int MINB = 4, int MODE = 0>
 __global__ void __launch_bounds__(kT, MINB)
 bw1_kernel(const int64_t* __restrict__ edge_ptr, const int32_t* __restrict__ rev,
            const float4* __restrict__ geo, int64_t nv, const float* __restrict__ X,
            const float* __restrict__ W, int dg, RbfParams rp, const float* __restrict__ Sbar,
-           float4* __restrict__ edge_grad) {
+           float4* __restrict__ edge_grad, const float* __restrict__ rtab) {
   extern __shared__ __align__(16) float bsm[];
   float4* Us = reinterpret_cast<float4*>(bsm);             // [kN]
   float* Rb = bsm + 4 * kN;                                 // [kN * K]
@@ -311,7 +369,7 @@ bw1_kernel(const int64_t* __restrict__ edge_ptr, const int32_t* __restrict__ rev
     const int n = static_cast<int>(edge_ptr[j + 1] - off);
     if (n < 2 || n > kN) continue;
     __syncthreads();
-    load_center<K>(Us, Rb, geo, off, n, rp);
+    load_center<K, MODE>(Us, Rb, geo, off, n, rp, rtab);
     for (int i = tid; i < n * (kN + 1); i += kT) XB[i] = 0.f;
     // thread tile: PP rows p; G row groups per in-edge (G * nq <= kT)
     const int PP = n <= 16 ? 1 : (n <= 32 ? 2 : 4);
@@ -333,9 +391,9 @@ bw1_kernel(const int64_t* __restrict__ edge_ptr, const int32_t* __restrict__ rev
         __syncthreads();
         if (q0 + kQC < n) load_x(xs, rev, X, off, q0 + kQC, min(kQC, n - q0 - kQC), dg, c0);
         switch (PP) {
-          case 1: bw1_tile<K, L, 1>(Qs, Sb, Us, XB, n, q0, nq, G); break;
-          case 2: bw1_tile<K, L, 2>(Qs, Sb, Us, XB, n, q0, nq, G); break;
-          default: bw1_tile<K, L, 4>(Qs, Sb, Us, XB, n, q0, nq, G); break;
+          case 1: bw1_tile<K, L, 1, MODE>(Qs, Sb, Us, XB, n, q0, nq, G); break;
+          case 2: bw1_tile<K, L, 2, MODE>(Qs, Sb, Us, XB, n, q0, nq, G); break;
+          default: bw1_tile<K, L, 4, MODE>(Qs, Sb, Us, XB, n, q0, nq, G); break;
         }
       }
     }
@@ -415,13 +473,14 @@ __device__ __forceinline__ void bw2_main(const float* Cb, const float* Sb, int n
   }
 }
 
-template <int K, int L, int MINB = 3>
+template <int K, int L, int MINB = 3, int MODE = 0>
 __global__ void __launch_bounds__(kT, MINB)
 bw2_kernel(const int64_t* __restrict__ edge_ptr, const int32_t* __restrict__ rev,
            const float4* __restrict__ geo, int64_t nv, const float* __restrict__ X,
            const float* __restrict__ W, int dg, RbfParams rp, const float* __restrict__ Sbar,
            float* __restrict__ Xbar, float* __restrict__ wbar_part, float* __restrict__ dd_part,
-           int64_t num_edges, float4* __restrict__ edge_grad) {
+           int64_t num_edges, float4* __restrict__ edge_grad, const float* __restrict__ rtab,
+           const float* __restrict__ dtab) {
   static_assert(L <= 8, "L <= 8");
   extern __shared__ __align__(16) float dsm[];
   float4* Us = reinterpret_cast<float4*>(dsm);      // [64]
@@ -430,6 +489,7 @@ bw2_kernel(const int64_t* __restrict__ edge_ptr, const int32_t* __restrict__ rev
   float* Sb = Cb + kN * 16 * 8;                      // Sbar rows of the centre, this channel block
   float* Wsm = Sb + kN * kCB;                        // W[k, l, c0 + c]
   float* DD = Wsm + K * L * kCB;                     // [16][2] dd partial per row and warp
+  float* DRb = DD + 32;                               // [64 * K] radial d-derivatives (MODE 1)
   const int tid = threadIdx.x;
   const int c = tid & (kCB - 1), h = tid >> 6;       // epilogue: channel, row half
   const int64_t c0 = static_cast<int64_t>(blockIdx.y) * kCB;
@@ -456,7 +516,7 @@ bw2_kernel(const int64_t* __restrict__ edge_ptr, const int32_t* __restrict__ rev
       continue;
     }
     __syncthreads();
-    load_center<K>(Us, Rb, geo, off, n, rp);
+    load_center<K, MODE>(Us, Rb, geo, off, n, rp, rtab, MODE == 0 ? nullptr : DRb, dtab);
     for (int i = tid; i < n * kCB; i += kT) {
       const int p = i >> 6, cc = i & 63;
       Sb[i] = c0 + cc < dg ? Sbar[(off + p) * dg + c0 + cc] : 0.f;
@@ -481,15 +541,10 @@ bw2_kernel(const int64_t* __restrict__ edge_ptr, const int32_t* __restrict__ rev
         const float4 b = ok ? Us[q] : a;
         const float x = a.x * b.x + a.y * b.y + a.z * b.z;
         const float m = ok ? 1.f : 0.f;
-        float t[8];
-        float tp = m * x, tc = m;
+        float f[L], t[8];
+        angular_row<L, MODE>(x, m, f);
 #pragma unroll
-        for (int l = 0; l < 8; ++l) {
-          t[l] = l < L ? tc : 0.f;
-          const float tn = fmaf(2.f * x, tc, -tp);
-          tp = tc;
-          tc = tn;
-        }
+        for (int l = 0; l < 8; ++l) t[l] = l < L ? f[l] : 0.f;
         float4* dst = reinterpret_cast<float4*>(Cb + (p * TQ + g) * 8);
         dst[0] = make_float4(t[0], t[1], t[2], t[3]);
         dst[1] = make_float4(t[4], t[5], t[6], t[7]);
@@ -532,7 +587,8 @@ bw2_kernel(const int64_t* __restrict__ edge_ptr, const int32_t* __restrict__ rev
         for (int k = 0; k < K; ++k) {
           const float vk = (k & 1) ? v2[k >> 1].y : v2[k >> 1].x;
           xb = fmaf(rb[k], vk, xb);
-          ds = fmaf(-2.f * rp.gamma * (d - rp.step * k) * rb[k], vk, ds);
+          const float drb = MODE == 0 ? -2.f * rp.gamma * (d - rp.step * k) * rb[k] : DRb[q * K + k];
+          ds = fmaf(drb, vk, ds);
         }
         if (cok) Xbar[static_cast<int64_t>(rev[off + q]) * dg + c0 + c] = xb;
         const float x = xo[i];
@@ -626,13 +682,16 @@ __global__ void add_dd_kernel(const int64_t* __restrict__ edge_ptr, int64_t nv, 
 // ---------------------------------------------------------------------------
 bool fast_supported(int K, int L, int dg) { return K == 6 && L == 7 && dg >= 32; }
 
+// mode 0: the reference's Gaussian rbf x T_l basis; mode 1: GemNet-T's CBF (rtab / dtab = the
+// per-call radial table of triplet_sh.cu and its d-derivative, 8 floats per edge)
 int fast_fwd(const int64_t* edge_ptr, const int32_t* rev, const float4* geo, int64_t nv, const float* X,
-             const float* W, int K, int L, int dg, RbfParams rp, float* S, cudaStream_t st) {
+             const float* W, int K, int L, int dg, RbfParams rp, float* S, cudaStream_t st, int mode,
+             const float* rtab) {
   // 4 CTAs per SM (128 registers): 5 or 6 (96 / 80 registers, spilling) measured 12% / 36% slower
-  auto kern = fast::fwd_kernel<6, 7>;
+  auto kern = mode == 1 ? fast::fwd_kernel<6, 7, 4, 1> : fast::fwd_kernel<6, 7>;
   // one centre per CTA: no tail imbalance from static round-robin over unequal degrees
   const int grid = static_cast<int>(std::min<int64_t>(nv, 1 << 30));
-  kern<<<grid, fast::kT, 0, st>>>(edge_ptr, rev, geo, nv, X, W, dg, rp, S);
+  kern<<<grid, fast::kT, 0, st>>>(edge_ptr, rev, geo, nv, X, W, dg, rp, S, rtab);
   return check_launch("triplet_fwd_fast");
 }
 
@@ -642,24 +701,36 @@ int64_t fast_bwd_workspace_bytes(int64_t nv, int64_t ne, int K, int L, int dg) {
   return (ncb * gx * K * L * fast::kCB + ncb * std::max<int64_t>(ne, 1)) * 4;
 }
 
+template <typename F>
+static void fast_set_smem(F kern, size_t smem, bool& configured) {
+  if (!configured) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    configured = true;
+  }
+}
+
 // phases: 1 = bw1 (the angle adjoint: edge_grad.xyz), 2 = bw2 + reductions (X_bar, W_bar,
 // edge_grad.w), 3 = both.  The two touch disjoint outputs, so they may run on two streams.
 int fast_bwd(const int64_t* edge_ptr, const int32_t* rev, const float4* geo, int64_t nv, int64_t ne,
              const float* X, const float* W, int K, int L, int dg, RbfParams rp, const float* Sbar, float* Xbar,
-             float* Wbar, float4* edge_grad, void* ws, cudaStream_t st, int phases) {
+             float* Wbar, float4* edge_grad, void* ws, cudaStream_t st, int phases, int mode, const float* rtab,
+             const float* dtab) {
   const int ncb = (dg + fast::kCB - 1) / fast::kCB;
   if (phases & 1) {
-    auto kern = fast::bw1_kernel<6, 7>;
     const int grid = static_cast<int>(std::min<int64_t>(nv, 1 << 30));
     const size_t smem1 = (4 * fast::kN + ((fast::kN * 6 + 3) & ~3) + fast::kQC * 7 * fast::kSbStride +
                           fast::kN * fast::kSbStride + fast::kN * (fast::kN + 1)) *
                          sizeof(float);
-    static bool k1_configured = false;
-    if (!k1_configured) {
-      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem1));
-      k1_configured = true;
+    static bool c10 = false, c11 = false;
+    if (mode == 1) {
+      auto kern = fast::bw1_kernel<6, 7, 4, 1>;
+      fast_set_smem(kern, smem1, c11);
+      kern<<<grid, fast::kT, smem1, st>>>(edge_ptr, rev, geo, nv, X, W, dg, rp, Sbar, edge_grad, rtab);
+    } else {
+      auto kern = fast::bw1_kernel<6, 7>;
+      fast_set_smem(kern, smem1, c10);
+      kern<<<grid, fast::kT, smem1, st>>>(edge_ptr, rev, geo, nv, X, W, dg, rp, Sbar, edge_grad, nullptr);
     }
-    kern<<<grid, fast::kT, smem1, st>>>(edge_ptr, rev, geo, nv, X, W, dg, rp, Sbar, edge_grad);
     if (check_launch("triplet_bw1_fast")) return 1;
   }
   if (!(phases & 2)) return 0;
@@ -667,15 +738,19 @@ int fast_bwd(const int64_t* edge_ptr, const int32_t* rev, const float4* geo, int
   float* wpart = reinterpret_cast<float*>(ws);
   float* ddpart = wpart + static_cast<int64_t>(ncb) * gx * K * L * fast::kCB;
   const size_t smem = (4 * fast::kN + ((fast::kN * 6 + 3) & ~3) + fast::kN * 128 + fast::kN * fast::kCB +
-                       6 * 7 * fast::kCB + 32) * sizeof(float);
-  auto k2 = fast::bw2_kernel<6, 7>;
-  static bool k2_configured = false;
-  if (!k2_configured) {
-    cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    k2_configured = true;
+                       6 * 7 * fast::kCB + 32 + fast::kN * 6) * sizeof(float);
+  static bool c20 = false, c21 = false;
+  if (mode == 1) {
+    auto k2 = fast::bw2_kernel<6, 7, 3, 1>;
+    fast_set_smem(k2, smem, c21);
+    k2<<<dim3(gx, ncb), fast::kT, smem, st>>>(edge_ptr, rev, geo, nv, X, W, dg, rp, Sbar, Xbar, wpart, ddpart, ne,
+                                              edge_grad, rtab, dtab);
+  } else {
+    auto k2 = fast::bw2_kernel<6, 7>;
+    fast_set_smem(k2, smem, c20);
+    k2<<<dim3(gx, ncb), fast::kT, smem, st>>>(edge_ptr, rev, geo, nv, X, W, dg, rp, Sbar, Xbar, wpart, ddpart, ne,
+                                              edge_grad, nullptr, nullptr);
   }
-  k2<<<dim3(gx, ncb), fast::kT, smem, st>>>(edge_ptr, rev, geo, nv, X, W, dg, rp, Sbar, Xbar, wpart, ddpart, ne,
-                                            edge_grad);
   if (check_launch("triplet_bw2_fast")) return 1;
   fast::reduce_wbar_kernel<<<static_cast<int>((static_cast<int64_t>(K) * L * dg + 31) / 32), 256, 0, st>>>(
       wpart, gx, K, L, dg, Wbar);

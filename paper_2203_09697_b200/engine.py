@@ -341,7 +341,7 @@ class Engine:
         # the angle adjoint of the triplet interaction (edge_grad x, y, z) feeds only the final
         # positions adjoint: it runs on a third stream, overlapping the rest of the backward,
         # and is joined before the first later writer of edge_grad (rbf_bwd)
-        angle = self._side_stream(bg, 2) if not c.basis_code else None
+        angle = self._side_stream(bg, 2) if c.basis_code != 2 else None  # DimeNet SBF: one chain
         angle_keep = []
         pending = []
 
@@ -470,7 +470,7 @@ class Engine:
                 angle.wait_stream(main)
                 with torch.cuda.stream(angle):
                     ops.triplet_bwd(bg.edge_ptr, bg.rev, bg.geo, st["X"], st["Wk"], c.cutoff, S_bar, eg,
-                                    max_degree=bg.max_deg, phases=1)
+                                    max_degree=bg.max_deg, basis=c.basis_code, phases=1)
                 angle_keep.append(S_bar)  # read on the angle stream: alive until the join
             X_bar, Wk_bar = ops.triplet_bwd(bg.edge_ptr, bg.rev, bg.geo, st["X"], st["Wk"], c.cutoff,
                                             S_bar, eg, max_degree=bg.max_deg, basis=c.basis_code,

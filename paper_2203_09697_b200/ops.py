@@ -304,7 +304,7 @@ def triplet_bwd(edge_ptr, rev, geo, X, Wk, cutoff, S_bar, edge_grad, X_bar=None,
         W_bar = torch.empty_like(Wk)
     if max_degree is None:
         max_degree = int((edge_ptr[1:] - edge_ptr[:-1]).max().item()) if nv else 0
-    if basis and phases != 3:  # the Bessel bases run one adjoint kernel chain
+    if basis > 1 and phases != 3:  # the DimeNet SBF basis runs one adjoint kernel chain
         if phases == 1:
             return None, None
         phases = 3
@@ -318,6 +318,11 @@ def triplet_bwd(edge_ptr, rev, geo, X, Wk, cutoff, S_bar, edge_grad, X_bar=None,
                 W_bar[:, :, c0:c1] = wb
         return (None, None) if phases == 1 else (X_bar, W_bar)
     ne = X.shape[0]
+    if phases == 1 and basis:  # its own radial table, no X_bar / W_bar writes
+        ws = _workspace_named("tbw_angle", call("egn_triplet_bwd_angle_workspace_bytes", ne, int(basis)), X.device)
+        call("egn_triplet_bwd_basis_ex", ptr(edge_ptr), ptr(rev), ptr(geo), nv, ne, int(max_degree), ptr(X), ptr(Wk),
+             k, l, dg, float(cutoff), int(basis), 1, ptr(S_bar), None, None, ptr(edge_grad), ptr(ws), stream())
+        return None, None
     if phases == 1:  # no workspace, no X_bar / W_bar writes
         call("egn_triplet_bwd_ex", ptr(edge_ptr), ptr(rev), ptr(geo), nv, ne, int(max_degree), ptr(X), ptr(Wk), k, l,
              dg, float(cutoff), ptr(S_bar), None, None, ptr(edge_grad), 1, None, stream())
@@ -328,8 +333,9 @@ def triplet_bwd(edge_ptr, rev, geo, X, Wk, cutoff, S_bar, edge_grad, X_bar=None,
         nbytes = call("egn_triplet_bwd_workspace_bytes", nv, ne, int(max_degree), k, l, dg)
     ws = _workspace(nbytes, X.device)
     if basis:
-        call("egn_triplet_bwd_basis", ptr(edge_ptr), ptr(rev), ptr(geo), nv, ne, int(max_degree), ptr(X), ptr(Wk), k,
-             l, dg, float(cutoff), int(basis), ptr(S_bar), ptr(X_bar), ptr(W_bar), ptr(edge_grad), ptr(ws), stream())
+        call("egn_triplet_bwd_basis_ex", ptr(edge_ptr), ptr(rev), ptr(geo), nv, ne, int(max_degree), ptr(X), ptr(Wk),
+             k, l, dg, float(cutoff), int(basis), int(phases), ptr(S_bar), ptr(X_bar), ptr(W_bar), ptr(edge_grad),
+             ptr(ws), stream())
         return X_bar, W_bar
     if phases == 2:
         call("egn_triplet_bwd_ex", ptr(edge_ptr), ptr(rev), ptr(geo), nv, ne, int(max_degree), ptr(X), ptr(Wk), k, l,

@@ -258,12 +258,14 @@ def test_graph_mlp_vs_fp64(g, dv, du):
         assert max_rel(got.cpu().numpy(), ref.cpu().numpy()) < 1e-5
 
 
+@pytest.mark.parametrize("basis", [0, 1, 2])
 @pytest.mark.parametrize("n,density,dg,mode", [(40, 0.06, 64, 0), (300, 0.9, 64, 0), (40, 0.06, 320, 0),
                                                 (40, 0.06, 64, 2)])
-def test_triplet_bwd_phases_match_single_call(n, density, dg, mode):
-    """egn_triplet_bwd_ex: the angle phase (1) and the rest (2), run on two streams, give the
-    bit-identical X_bar, W_bar and edge_grad of the single call (3); includes centres above the
-    small-degree range (dense cloud), a width above 256 (channel chunks) and the pairwise path."""
+def test_triplet_bwd_phases_match_single_call(n, density, dg, mode, basis):
+    """egn_triplet_bwd_ex / egn_triplet_bwd_basis_ex: the angle phase (1) and the rest (2), run
+    on two streams, give the bit-identical X_bar, W_bar and edge_grad of the single call (3);
+    includes centres above the small-degree range (dense cloud), a width above 256 (channel
+    chunks), the pairwise path and every basis (0 Gaussian, 1 GemNet CBF, 2 DimeNet SBF)."""
     from paper_2203_09697_b200 import _lib, ops
     from paper_2203_09697_b200.graph import build_batch
 
@@ -277,13 +279,15 @@ def test_triplet_bwd_phases_match_single_call(n, density, dg, mode):
         Sb = torch.randn((bg.num_edges, dg), device="cuda")
         eg0 = torch.randn((bg.num_edges, 4), device="cuda")
         eg1 = eg0.clone()
-        xb, wb = ops.triplet_bwd(bg.edge_ptr, bg.rev, bg.geo, X, W, 6.0, Sb, eg0, max_degree=bg.max_deg)
+        xb, wb = ops.triplet_bwd(bg.edge_ptr, bg.rev, bg.geo, X, W, 6.0, Sb, eg0, max_degree=bg.max_deg,
+                                 basis=basis)
         side = torch.cuda.Stream()
         side.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(side):
             assert ops.triplet_bwd(bg.edge_ptr, bg.rev, bg.geo, X, W, 6.0, Sb, eg1, max_degree=bg.max_deg,
-                                   phases=1) == (None, None)
-        xb2, wb2 = ops.triplet_bwd(bg.edge_ptr, bg.rev, bg.geo, X, W, 6.0, Sb, eg1, max_degree=bg.max_deg, phases=2)
+                                   basis=basis, phases=1) == (None, None)
+        xb2, wb2 = ops.triplet_bwd(bg.edge_ptr, bg.rev, bg.geo, X, W, 6.0, Sb, eg1, max_degree=bg.max_deg,
+                                   basis=basis, phases=2)
         torch.cuda.current_stream().wait_stream(side)
         torch.cuda.synchronize()
     finally:
