@@ -225,6 +225,30 @@ __device__ __forceinline__ void load_wreg(float2 (&wreg)[K][kLP], const float* _
     }
 }
 
+// Rows [off, off + n) x channels [c0, c0 + 64) of a row-major [*, dg] array into dst[p * stride + c]
+// (zero past dg).  16-byte cp.async when dg % 4 == 0 (rows 16-byte aligned, a granule is wholly in
+// or out of range): every request of the CTA is in flight at once instead of one load latency per
+// element.  The caller runs stage_wait() before the barrier that publishes dst.
+__device__ __forceinline__ void stage_rows(float* dst, int stride, const float* __restrict__ src, int64_t off, int n,
+                                           int dg, int c0) {
+  if ((dg & 3) == 0) {
+    for (int i = threadIdx.x; i < n * (kCB / 4); i += kT) {
+      const int p = i >> 4, c = (i & 15) * 4;
+      const bool ok = c0 + c < dg;
+      const float* g = ok ? src + (off + p) * dg + c0 + c : src;
+      const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(dst + p * stride + c));
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(g), "r"(ok ? 16 : 0) : "memory");
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  } else {
+    for (int i = threadIdx.x; i < n * kCB; i += kT) {
+      const int p = i >> 6, c = i & 63;
+      dst[p * stride + c] = c0 + c < dg ? src[(off + p) * dg + c0 + c] : 0.f;
+    }
+  }
+}
+__device__ __forceinline__ void stage_wait() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
 // ---------------------------------------------------------------------------
 template <int K, int L, int MINB = 4, int MODE = 0>
 __global__ void __launch_bounds__(kT, MINB)
@@ -378,14 +402,12 @@ bw1_kernel(const int64_t* __restrict__ edge_ptr, const int32_t* __restrict__ rev
       float2 wreg[K][kLP];
       load_wreg<K, L>(wreg, W, dg, c0 + (tid & 63));
       __syncthreads();
-      for (int i = tid; i < n * kCB; i += kT) {
-        const int p = i >> 6, c = i & 63;
-        Sb[p * kSbStride + c] = c0 + c < dg ? Sbar[(off + p) * dg + c0 + c] : 0.f;
-      }
+      stage_rows(Sb, kSbStride, Sbar, off, n, dg, c0);
       float xs[kQC / 2];
       load_x(xs, rev, X, off, 0, min(kQC, n), dg, c0);
       for (int q0 = 0; q0 < n; q0 += kQC) {
         const int nq = min(kQC, n - q0);
+        if (q0 == 0) stage_wait();
         __syncthreads();
         build_q<K, L, kSbStride>(Qs, wreg, Rb, xs, q0, nq);
         __syncthreads();
@@ -398,26 +420,37 @@ bw1_kernel(const int64_t* __restrict__ edge_ptr, const int32_t* __restrict__ rev
       }
     }
     __syncthreads();
-    // dE/dv_e for every out-edge e of the centre: rows then columns (fixed order)
-    for (int e = tid; e < n; e += kT) {
-      const float4 ue = Us[e];
+    // dE/dv_e for every out-edge e of the centre: four lanes per e take the partners o = sub,
+    // sub + 4, ... (rows then columns), combined by a fixed shuffle tree.  Every thread runs the
+    // same number of rounds so the shuffles see full warps.
+    for (int base = 0; base < n * 4; base += kT) {
+      const int i = base + tid, e = i >> 2, sub = i & 3;
+      const bool live = e < n;
+      const float4 ue = Us[live ? e : 0];
       float fx = 0.f, fy = 0.f, fz = 0.f;
-      for (int o = 0; o < n; ++o) {
-        if (o == e) continue;
-        const float4 uo = Us[o];
-        const float x = ue.x * uo.x + ue.y * uo.y + ue.z * uo.z;
-        const float v = XB[e * (kN + 1) + o] + XB[o * (kN + 1) + e];
-        fx = fmaf(v, uo.x - x * ue.x, fx);
-        fy = fmaf(v, uo.y - x * ue.y, fy);
-        fz = fmaf(v, uo.z - x * ue.z, fz);
+      if (live) {
+        for (int o = sub; o < n; o += 4) {
+          if (o == e) continue;
+          const float4 uo = Us[o];
+          const float x = ue.x * uo.x + ue.y * uo.y + ue.z * uo.z;
+          const float v = XB[e * (kN + 1) + o] + XB[o * (kN + 1) + e];
+          fx = fmaf(v, uo.x - x * ue.x, fx);
+          fy = fmaf(v, uo.y - x * ue.y, fy);
+          fz = fmaf(v, uo.z - x * ue.z, fz);
+        }
+      }
+#pragma unroll
+      for (int m = 1; m < 4; m <<= 1) {
+        fx += __shfl_xor_sync(0xffffffffu, fx, m);
+        fy += __shfl_xor_sync(0xffffffffu, fy, m);
+        fz += __shfl_xor_sync(0xffffffffu, fz, m);
       }
       // x, y, z only (4-byte accesses): bw2 may update .w of the same edge concurrently when
       // the angle phase runs on its own stream (egn_triplet_bwd_ex phases)
-      const float inv = 1.f / ue.w;
-      float* g = reinterpret_cast<float*>(edge_grad + off + e);
-      g[0] += fx * inv;
-      g[1] += fy * inv;
-      g[2] += fz * inv;
+      if (live && sub < 3) {
+        const float f = sub == 0 ? fx : (sub == 1 ? fy : fz);
+        reinterpret_cast<float*>(edge_grad + off + e)[sub] += f / ue.w;
+      }
     }
   }
 }
@@ -516,11 +549,8 @@ bw2_kernel(const int64_t* __restrict__ edge_ptr, const int32_t* __restrict__ rev
       continue;
     }
     __syncthreads();
+    stage_rows(Sb, kCB, Sbar, off, n, dg, static_cast<int>(c0));
     load_center<K, MODE>(Us, Rb, geo, off, n, rp, rtab, MODE == 0 ? nullptr : DRb, dtab);
-    for (int i = tid; i < n * kCB; i += kT) {
-      const int p = i >> 6, cc = i & 63;
-      Sb[i] = c0 + cc < dg ? Sbar[(off + p) * dg + c0 + cc] : 0.f;
-    }
     for (int qb0 = 0; qb0 < n; qb0 += 16) {
       const int nr = min(16, n - qb0);
       const int TQ = nr <= 8 ? 8 : 16;
@@ -531,6 +561,7 @@ bw2_kernel(const int64_t* __restrict__ edge_ptr, const int32_t* __restrict__ rev
         const int r = h + 2 * i;
         xo[i] = (r < nr && cok) ? __ldg(X + static_cast<int64_t>(rev[off + qb0 + r]) * dg + c0 + c) : 0.f;
       }
+      if (qb0 == 0) stage_wait();
       __syncthreads();
       // Cb[p][g][l] = T_l(x_{p, qb0+g}) (masked on p == q and q >= n)
       for (int i = tid; i < n * TQ; i += kT) {
