@@ -163,9 +163,11 @@ __device__ __forceinline__ void build_q(float* Qs, const float2 (&wreg)[K][kLP],
   }
 }
 
-// Chebyshev chunk Ct[(t,l)][rslot(p)] = T_l(x_pq) or T_l'(x_pq), masked on p == q / p >= n.
+// Chebyshev chunk Ct[(t,l)][slot(p)] = T_l(x_pq) or T_l'(x_pq), masked on p == q / p >= n.
+// slot(p) = (p % RG) * 4 + p / RG for rows = 4 RG, RG in {4, 8, 16} (RG = 16: rslot): row group g reads its rows
+// g, g + RG, g + 2 RG, g + 3 RG as one float4.
 template <int L, bool DERIV, int MODE = 0>
-__device__ __forceinline__ void build_c(float* Ct, const float4* Us, int n, int rows, int q0, int nq) {
+__device__ __forceinline__ void build_c(float* Ct, const float4* Us, int n, int rows, int q0, int nq, int RG = 16) {
   for (int i = threadIdx.x; i < nq * rows; i += kT) {
     const int t = i / rows, p = i - t * rows;
     const int q = q0 + t;
@@ -174,7 +176,7 @@ __device__ __forceinline__ void build_c(float* Ct, const float4* Us, int n, int 
     float4 b = ok ? Us[p] : a;
     const float x = a.x * b.x + a.y * b.y + a.z * b.z;
     const float m = ok ? 1.f : 0.f;
-    float* dst = Ct + t * L * kCB + rslot(p);
+    float* dst = Ct + t * L * kCB + (p & (RG - 1)) * 4 + (RG == 16 ? p >> 4 : (RG == 8 ? p >> 3 : p >> 2));
     if (!DERIV) {
       float f[L];
       angular_row<L, MODE>(x, m, f);
@@ -194,11 +196,12 @@ __device__ __forceinline__ void build_c(float* Ct, const float4* Us, int n, int 
   }
 }
 
+// k-split micro kernel: this thread takes kk = ks, ks + KS, ... (KS thread sets share the chunk)
 template <int TMR>
 __device__ __forceinline__ void micro(const float* __restrict__ A, const float* __restrict__ B, int nkk,
-                                      int rg, int cg, float2 (&acc)[4][4]) {
+                                      int rg, int cg, float2 (&acc)[4][4], int ks = 0, int KS = 1) {
 #pragma unroll 4
-  for (int kk = 0; kk < nkk; ++kk) {
+  for (int kk = ks; kk < nkk; kk += KS) {
     const float4 a = *reinterpret_cast<const float4*>(A + kk * kCB + rg * 4);
     const float4 b0 = *reinterpret_cast<const float4*>(B + kk * kCB + cg * 4);
     const float4 b1 = *reinterpret_cast<const float4*>(B + kk * kCB + 32 + cg * 4);
@@ -260,13 +263,22 @@ fwd_kernel(const int64_t* __restrict__ edge_ptr, const int32_t* __restrict__ rev
   __shared__ float Rb[kN * K];
   __shared__ __align__(16) float Ct[kQC * L * kCB];
   __shared__ __align__(16) float Qs[kQC * L * kCB];
-  const int tid = threadIdx.x, cg = tid & 7, rg = tid >> 3;
+  const int tid = threadIdx.x;
   for (int64_t j = blockIdx.x; j < nv; j += gridDim.x) {
     const int64_t off = edge_ptr[j];
     const int n = static_cast<int>(edge_ptr[j + 1] - off);
     if (n == 0 || n > kN) continue;
-    const int tmr = (n + 15) >> 4;
-    const int rows = tmr * 16;
+    // Small centres: RG = 4 / 8 row groups of 4 rows (16 / 32 rows), and the 128 threads split
+    // the (q, l) reduction KS = 4 / 2 ways (thread set ks takes kk = ks mod KS), partials combined
+    // in shared memory at the end in fixed order.  A 4 x 8 thread tile reads 3 float4 per 16 FFMA2
+    // (a 2 x 8 tile needed 3 per 8: shared-memory bound).  Larger centres: 16 groups, tmr rows each.
+    const int RG = n <= 16 ? 4 : (n <= 32 ? 8 : 16);
+    const int KS = 128 / (RG * 8);
+    const int tpg = RG * 8;
+    const int ks = tid / tpg, w = tid - ks * tpg;
+    const int cg = w & 7, rg = w >> 3;
+    const int tmr = KS > 1 ? 4 : (n + 15) >> 4;
+    const int rows = RG == 16 ? tmr * 16 : 4 * RG;
     __syncthreads();
     load_center<K, MODE>(Us, Rb, geo, off, n, rp, rtab);
     for (int c0 = 0; c0 < dg; c0 += kCB) {
@@ -283,21 +295,51 @@ fwd_kernel(const int64_t* __restrict__ edge_ptr, const int32_t* __restrict__ rev
         const int nq = min(kQC, n - q0);
         __syncthreads();
         build_q<K, L>(Qs, wreg, Rb, xs, q0, nq);
-        build_c<L, false, MODE>(Ct, Us, n, rows, q0, nq);
+        build_c<L, false, MODE>(Ct, Us, n, rows, q0, nq, RG);
         __syncthreads();
         if (q0 + kQC < n) load_x(xs, rev, X, off, q0 + kQC, min(kQC, n - q0 - kQC), dg, c0);
         const int nkk = nq * L;
-        switch (tmr) {
-          case 1: micro<1>(Ct, Qs, nkk, rg, cg, acc); break;
-          case 2: micro<2>(Ct, Qs, nkk, rg, cg, acc); break;
-          case 3: micro<3>(Ct, Qs, nkk, rg, cg, acc); break;
-          default: micro<4>(Ct, Qs, nkk, rg, cg, acc); break;
+        if (KS > 1) {
+          micro<4>(Ct, Qs, nkk, rg, cg, acc, ks, KS);
+        } else {
+          switch (tmr) {
+            case 3: micro<3>(Ct, Qs, nkk, rg, cg, acc); break;
+            default: micro<4>(Ct, Qs, nkk, rg, cg, acc); break;
+          }
+        }
+      }
+      if (KS > 1) {
+        // combine the k-split partials: set ks > 0 parks its tile in Ct (layout [set][value][w],
+        // conflict-free), set 0 adds them in set order
+        __syncthreads();
+        if (ks > 0) {
+          float* red = Ct + (ks - 1) * 32 * tpg + w;
+#pragma unroll
+          for (int r = 0; r < 4; ++r)
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              red[(r * 8 + 2 * i) * tpg] = acc[r][i].x;
+              red[(r * 8 + 2 * i + 1) * tpg] = acc[r][i].y;
+            }
+        }
+        __syncthreads();
+        if (ks == 0) {
+          for (int o = 1; o < KS; ++o) {
+            const float* red = Ct + (o - 1) * 32 * tpg + w;
+#pragma unroll
+            for (int r = 0; r < 4; ++r)
+#pragma unroll
+              for (int i = 0; i < 4; ++i) {
+                acc[r][i].x += red[(r * 8 + 2 * i) * tpg];
+                acc[r][i].y += red[(r * 8 + 2 * i + 1) * tpg];
+              }
+          }
         }
       }
 #pragma unroll
       for (int r = 0; r < 4; ++r) {
-        const int p = rg + 16 * r;
-        if (r < tmr && p < n) {
+        const int p = rg + RG * r;
+        if (ks == 0 && r < tmr && p < n) {
           float* dst = S + (off + p) * dg + c0;
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
