@@ -363,8 +363,10 @@ constexpr int kSbStride = kCB + 4;  // padded Sbar / Q rows (bank spread for 16-
 template <int K, int L, int PP, int MODE = 0>
 __device__ __forceinline__ void bw1_tile(const float* Qs, const float* Sb, const float4* Us, float* XB, int n, int q0,
                                          int nq, int G) {
-  const int tid = threadIdx.x;
-  const int t = tid / G, pg = tid - t * G;
+  // warp = 8 in-edges q x 4 row groups: a Q-row load is 8 distinct 16-byte rows (one wavefront,
+  // conflict-free at stride 7 x 68 floats) and an S-bar load 4 (one wavefront); G = 16 row groups
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int t = lane & 7, pg = (lane >> 3) + 4 * (tid >> 5);
   if (t >= nq) return;
   // Z[(q, l), p] for l >= 1 (T_0' = 0: the l = 0 row is never needed).  Packed accumulators:
   // row pairs (p_i, p_i+1) for PP >= 2 (bit-identical to the scalar loop), even / odd channel
@@ -437,9 +439,9 @@ bw1_kernel(const int64_t* __restrict__ edge_ptr, const int32_t* __restrict__ rev
     __syncthreads();
     load_center<K, MODE>(Us, Rb, geo, off, n, rp, rtab);
     for (int i = tid; i < n * (kN + 1); i += kT) XB[i] = 0.f;
-    // thread tile: PP rows p; G row groups per in-edge (G * nq <= kT)
+    // thread tile: PP rows p = pg + 16 i of one in-edge q (bw1_tile)
     const int PP = n <= 16 ? 1 : (n <= 32 ? 2 : 4);
-    const int G = (n + PP - 1) / PP;
+    const int G = 16;
     for (int c0 = 0; c0 < dg; c0 += kCB) {
       float2 wreg[K][kLP];
       load_wreg<K, L>(wreg, W, dg, c0 + (tid & 63));
