@@ -359,6 +359,58 @@ fwd_kernel(const int64_t* __restrict__ edge_ptr, const int32_t* __restrict__ rev
 // of Sbar spread over the banks); xbar accumulates in shared memory, one owner per (p, q).
 // Then the row / column pass turns xbar into dE/dv (edge_grad.xyz += F / d).
 constexpr int kSbStride = kCB + 4;  // padded Sbar / Q rows (bank spread for 16-byte loads)
+// Row-pair layout of S-bar for PP >= 2: pair pr = 16 h + g holds rows a = 32 h + g and a + 16
+// (the two rows one FFMA2 updates) interleaved per channel, [pr][c][2] at stride kPairStride:
+// a float4 load gives (a, a + 16) at channels c and c + 1, already the packed operand pairs (no
+// register moves to pair rows that came from two loads).  Same footprint as [kN][kSbStride].
+constexpr int kPairStride = 2 * kCB + 8;  // 136 floats: 4 pairs of a warp on distinct banks
+static_assert(kN / 2 * kPairStride == kN * kSbStride, "pair layout footprint");
+
+// rows [off, off + n) of S-bar, channels [c0, c0 + 64), into the pair layout (np pairs); every
+// global load of the thread is issued before its stores
+__device__ __forceinline__ void stage_pairs(float* dst, const float* __restrict__ src, int64_t off, int n, int np,
+                                            int dg, int c0) {
+  auto load4 = [&](int row, int c) -> float4 {
+    if (row >= n) return make_float4(0.f, 0.f, 0.f, 0.f);
+    const float* g = src + (off + row) * dg + c0 + c;
+    if ((dg & 3) == 0) return c0 + c < dg ? __ldg(reinterpret_cast<const float4*>(g)) : make_float4(0.f, 0.f, 0.f, 0.f);
+    return make_float4(c0 + c < dg ? __ldg(g) : 0.f, c0 + c + 1 < dg ? __ldg(g + 1) : 0.f,
+                       c0 + c + 2 < dg ? __ldg(g + 2) : 0.f, c0 + c + 3 < dg ? __ldg(g + 3) : 0.f);
+  };
+  constexpr int kIt = (kN / 2) * (kCB / 4) / kT;  // 4
+  float4 va[kIt], vb[kIt];
+  if (np * (kCB / 4) <= kT) {  // one granule pair per thread
+    const int pr = threadIdx.x >> 4, c = (threadIdx.x & 15) * 4;
+    if (pr < np) {
+      const int ra = (pr >> 4) * 32 + (pr & 15);
+      const float4 a = load4(ra, c), b = load4(ra + 16, c);
+      float4* d = reinterpret_cast<float4*>(dst + pr * kPairStride + 2 * c);
+      d[0] = make_float4(a.x, b.x, a.y, b.y);
+      d[1] = make_float4(a.z, b.z, a.w, b.w);
+    }
+    return;
+  }
+#pragma unroll
+  for (int k = 0; k < kIt; ++k) {
+    const int i = threadIdx.x + k * kT;
+    const int pr = i >> 4, c = (i & 15) * 4;
+    const int ra = (pr >> 4) * 32 + (pr & 15);
+    if (pr < np) {
+      va[k] = load4(ra, c);
+      vb[k] = load4(ra + 16, c);
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < kIt; ++k) {
+    const int i = threadIdx.x + k * kT;
+    const int pr = i >> 4, c = (i & 15) * 4;
+    if (pr < np) {
+      float4* d = reinterpret_cast<float4*>(dst + pr * kPairStride + 2 * c);
+      d[0] = make_float4(va[k].x, vb[k].x, va[k].y, vb[k].y);
+      d[1] = make_float4(va[k].z, vb[k].z, va[k].w, vb[k].w);
+    }
+  }
+}
 
 template <int K, int L, int PP, int MODE = 0>
 __device__ __forceinline__ void bw1_tile(const float* Qs, const float* Sb, const float4* Us, float* XB, int n, int q0,
@@ -378,25 +430,38 @@ __device__ __forceinline__ void bw1_tile(const float* Qs, const float* Sb, const
 #pragma unroll
     for (int i = 0; i < PH; ++i) acc2[l][i] = make_float2(0.f, 0.f);
   const float* qrow = Qs + (t * L) * kSbStride;
-#pragma unroll 4
-  for (int c = 0; c < kCB; c += 4) {
-    float4 sv[PP];
+  if constexpr (PP >= 2) {
+    // S-bar in the row-pair layout (stage_pairs): pair i of this thread = rows (pg + 32 i, + 16)
+#pragma unroll 2
+    for (int c = 0; c < kCB; c += 4) {
+      float4 s0[PH], s1[PH];
 #pragma unroll
-    for (int i = 0; i < PP; ++i) sv[i] = *reinterpret_cast<const float4*>(Sb + (pg + G * i) * kSbStride + c);
+      for (int i = 0; i < PH; ++i) {
+        const float* sp = Sb + (16 * i + pg) * kPairStride + 2 * c;
+        s0[i] = *reinterpret_cast<const float4*>(sp);
+        s1[i] = *reinterpret_cast<const float4*>(sp + 4);
+      }
 #pragma unroll
-    for (int l = 1; l < L; ++l) {
-      const float4 qv = *reinterpret_cast<const float4*>(qrow + l * kSbStride + c);
-      if (PP >= 2) {
+      for (int l = 1; l < L; ++l) {
+        const float4 qv = *reinterpret_cast<const float4*>(qrow + l * kSbStride + c);
 #pragma unroll
         for (int i = 0; i < PH; ++i) {
-          acc2[l][i] = ffma2(qv.x, make_float2(sv[2 * i].x, sv[2 * i + 1].x), acc2[l][i]);
-          acc2[l][i] = ffma2(qv.y, make_float2(sv[2 * i].y, sv[2 * i + 1].y), acc2[l][i]);
-          acc2[l][i] = ffma2(qv.z, make_float2(sv[2 * i].z, sv[2 * i + 1].z), acc2[l][i]);
-          acc2[l][i] = ffma2(qv.w, make_float2(sv[2 * i].w, sv[2 * i + 1].w), acc2[l][i]);
+          acc2[l][i] = ffma2(qv.x, make_float2(s0[i].x, s0[i].y), acc2[l][i]);
+          acc2[l][i] = ffma2(qv.y, make_float2(s0[i].z, s0[i].w), acc2[l][i]);
+          acc2[l][i] = ffma2(qv.z, make_float2(s1[i].x, s1[i].y), acc2[l][i]);
+          acc2[l][i] = ffma2(qv.w, make_float2(s1[i].z, s1[i].w), acc2[l][i]);
         }
-      } else {
-        acc2[l][0] = ffma2(make_float2(qv.x, qv.y), make_float2(sv[0].x, sv[0].y), acc2[l][0]);
-        acc2[l][0] = ffma2(make_float2(qv.z, qv.w), make_float2(sv[0].z, sv[0].w), acc2[l][0]);
+      }
+    }
+  } else {
+#pragma unroll 4
+    for (int c = 0; c < kCB; c += 4) {
+      const float4 sv = *reinterpret_cast<const float4*>(Sb + pg * kSbStride + c);
+#pragma unroll
+      for (int l = 1; l < L; ++l) {
+        const float4 qv = *reinterpret_cast<const float4*>(qrow + l * kSbStride + c);
+        acc2[l][0] = ffma2(make_float2(qv.x, qv.y), make_float2(sv.x, sv.y), acc2[l][0]);
+        acc2[l][0] = ffma2(make_float2(qv.z, qv.w), make_float2(sv.z, sv.w), acc2[l][0]);
       }
     }
   }
@@ -443,10 +508,11 @@ bw1_kernel(const int64_t* __restrict__ edge_ptr, const int32_t* __restrict__ rev
     const int PP = n <= 16 ? 1 : (n <= 32 ? 2 : 4);
     const int G = 16;
     for (int c0 = 0; c0 < dg; c0 += kCB) {
+      __syncthreads();
+      if (PP == 1) stage_rows(Sb, kSbStride, Sbar, off, n, dg, c0);
+      else stage_pairs(Sb, Sbar, off, n, PP == 2 ? 16 : 32, dg, c0);
       float2 wreg[K][kLP];
       load_wreg<K, L>(wreg, W, dg, c0 + (tid & 63));
-      __syncthreads();
-      stage_rows(Sb, kSbStride, Sbar, off, n, dg, c0);
       float xs[kQC / 2];
       load_x(xs, rev, X, off, 0, min(kQC, n), dg, c0);
       for (int q0 = 0; q0 < n; q0 += kQC) {
