@@ -633,6 +633,7 @@ bw2_kernel(const int64_t* __restrict__ edge_ptr, const int32_t* __restrict__ rev
   float* Wsm = Sb + kN * kCB;                        // W[k, l, c0 + c]
   float* DD = Wsm + K * L * kCB;                     // [16][2] dd partial per row and warp
   float* DRb = DD + 32;                               // [64 * K] radial d-derivatives (MODE 1)
+  int* Rv = reinterpret_cast<int*>(DRb + kN * K);      // [64] rev of the centre's edges
   const int tid = threadIdx.x;
   const int c = tid & (kCB - 1), h = tid >> 6;       // epilogue: channel, row half
   const int64_t c0 = static_cast<int64_t>(blockIdx.y) * kCB;
@@ -660,19 +661,21 @@ bw2_kernel(const int64_t* __restrict__ edge_ptr, const int32_t* __restrict__ rev
     }
     __syncthreads();
     stage_rows(Sb, kCB, Sbar, off, n, dg, static_cast<int>(c0));
+    for (int i = tid; i < n; i += kT) Rv[i] = rev[off + i];
     load_center<K, MODE>(Us, Rb, geo, off, n, rp, rtab, MODE == 0 ? nullptr : DRb, dtab);
     for (int qb0 = 0; qb0 < n; qb0 += 16) {
       const int nr = min(16, n - qb0);
       const int TQ = nr <= 8 ? 8 : 16;
-      // X rows of this thread's epilogue rows, fetched before the main loop
+      if (qb0 == 0) stage_wait();
+      __syncthreads();
+      // X rows of this thread's epilogue rows (row indices from shared memory: one global
+      // latency), in flight during the table build and the main loop
       float xo[8];
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
         const int r = h + 2 * i;
-        xo[i] = (r < nr && cok) ? __ldg(X + static_cast<int64_t>(rev[off + qb0 + r]) * dg + c0 + c) : 0.f;
+        xo[i] = (r < nr && cok) ? __ldg(X + static_cast<int64_t>(Rv[qb0 + r]) * dg + c0 + c) : 0.f;
       }
-      if (qb0 == 0) stage_wait();
-      __syncthreads();
       // Cb[p][g][l] = T_l(x_{p, qb0+g}) (masked on p == q and q >= n)
       for (int i = tid; i < n * TQ; i += kT) {
         const int p = i / TQ, g = i - p * TQ;
@@ -731,7 +734,7 @@ bw2_kernel(const int64_t* __restrict__ edge_ptr, const int32_t* __restrict__ rev
           const float drb = MODE == 0 ? -2.f * rp.gamma * (d - rp.step * k) * rb[k] : DRb[q * K + k];
           ds = fmaf(drb, vk, ds);
         }
-        if (cok) Xbar[static_cast<int64_t>(rev[off + q]) * dg + c0 + c] = xb;
+        if (cok) Xbar[static_cast<int64_t>(Rv[q]) * dg + c0 + c] = xb;
         const float x = xo[i];
 #pragma unroll
         for (int l = 0; l < L; ++l) {
@@ -879,7 +882,7 @@ int fast_bwd(const int64_t* edge_ptr, const int32_t* rev, const float4* geo, int
   float* wpart = reinterpret_cast<float*>(ws);
   float* ddpart = wpart + static_cast<int64_t>(ncb) * gx * K * L * fast::kCB;
   const size_t smem = (4 * fast::kN + ((fast::kN * 6 + 3) & ~3) + fast::kN * 128 + fast::kN * fast::kCB +
-                       6 * 7 * fast::kCB + 32 + fast::kN * 6) * sizeof(float);
+                       6 * 7 * fast::kCB + 32 + fast::kN * 6 + fast::kN) * sizeof(float);
   static bool c20 = false, c21 = false;
   if (mode == 1) {
     auto k2 = fast::bw2_kernel<6, 7, 3, 1>;
