@@ -862,7 +862,8 @@ int egn_triplet_path(int mode) {
 
 // DimeNet++ / GemNet bases: basis 1 = GemNet CBF (radial Bessel basis of
 // d_kj x Y_l0(angle)), 2 = DimeNet SBF (sqrt(2/c^3)/|j_{l+1}(z_ln)| u(d/c) j_l(z_ln d/c) Y_l0(angle));
-// the spherical-harmonic kernels for every centre (their A table absorbs the Y_l0 normalisation)
+// centres of degree <= 64 on the pairwise kernels (triplet_fast.cu MODE 1 / 2), the rest on the
+// spherical-harmonic kernels (their A table absorbs the Y_l0 normalisation)
 int egn_triplet_fwd_basis(const int64_t* edge_ptr, const int32_t* rev, const float* geo, int64_t num_nodes,
                           int64_t num_edges, int max_degree, const float* X, const float* W, int k_rbf, int l_sbf,
                           int dg, double cutoff, int basis, float* S, void* workspace, egn_stream_t stream) {
@@ -880,11 +881,12 @@ int egn_triplet_fwd_basis(const int64_t* edge_ptr, const int32_t* rev, const flo
                                         align256(sh_fwd_workspace_bytes(num_nodes, max_degree, k_rbf, l_sbf, dg)));
   if (int rc = sh_radial_table(g4, num_edges, static_cast<float>(cutoff), basis, tab, nullptr, st)) return rc;
   int min_n = 0;
-  if (basis == 1 && g_triplet_path != 1 && fast_supported(k_rbf, l_sbf, dg)) {
-    // GemNet-T CBF on the pairwise small-degree kernels (Legendre angular rows, radial rows from
-    // the table); the spherical-harmonic kernels take the centres above their range
+  if (g_triplet_path != 1 && fast_supported(k_rbf, l_sbf, dg)) {
+    // both bases on the pairwise small-degree kernels (Legendre angular rows, radial rows from
+    // the table: MODE 1 k-only, MODE 2 (k, l)); the spherical-harmonic kernels take the centres
+    // above their range
     if (int rc = fast_fwd(edge_ptr, rev, g4, num_nodes, X, W, k_rbf, l_sbf, dg, rbf_params(k_rbf, cutoff), S, st,
-                          1, tab))
+                          basis, tab))
       return rc;
     if (max_degree <= kFastMaxDeg) return 0;
     min_n = kFastMaxDeg;
@@ -918,8 +920,8 @@ int egn_triplet_bwd_basis_ex(const int64_t* edge_ptr, const int32_t* rev, const 
     return egn_triplet_bwd_ex(edge_ptr, rev, geo, num_nodes, num_edges, max_degree, X, W, k_rbf, l_sbf, dg, cutoff,
                               S_bar, X_bar, W_bar, edge_grad, phases, workspace, stream);
   EGN_REQUIRE(phases >= 1 && phases <= 3, "phases must be 1, 2 or 3");
-  // the angle phase splits off only on the small-degree kernels of the GemNet basis
-  const bool split_ok = basis == 1 && g_triplet_path != 1 && fast_supported(k_rbf, l_sbf, dg);
+  // the angle phase splits off only on the small-degree kernels
+  const bool split_ok = g_triplet_path != 1 && fast_supported(k_rbf, l_sbf, dg);
   if (!split_ok) {
     if (phases == 1) return 0;
     phases = 3;
@@ -932,7 +934,7 @@ int egn_triplet_bwd_basis_ex(const int64_t* edge_ptr, const int32_t* rev, const 
     float* tab = reinterpret_cast<float*>(workspace);
     if (int rc = sh_radial_table(g4, num_edges, static_cast<float>(cutoff), basis, tab, nullptr, st)) return rc;
     return fast_bwd(edge_ptr, rev, g4, num_nodes, num_edges, X, W, k_rbf, l_sbf, dg, rbf_params(k_rbf, cutoff), S_bar,
-                    X_bar, W_bar, reinterpret_cast<float4*>(edge_grad), nullptr, st, 1, 1, tab, nullptr);
+                    X_bar, W_bar, reinterpret_cast<float4*>(edge_grad), nullptr, st, 1, basis, tab, nullptr);
   }
   if (int rc = check_dims(k_rbf, l_sbf, dg)) return rc;
   EGN_REQUIRE(basis == 1 || basis == 2, "basis must be 0, 1 or 2");
@@ -952,10 +954,10 @@ int egn_triplet_bwd_basis_ex(const int64_t* edge_ptr, const int32_t* rev, const 
   float* dtab = reinterpret_cast<float*>(tb + align256(sh_radial_table_floats(num_edges, basis) * 4));
   if (int rc = sh_radial_table(g4, num_edges, static_cast<float>(cutoff), basis, tab, dtab, st)) return rc;
   int min_n = 0, accumulate = 0;
-  if (basis == 1 && g_triplet_path != 1 && fast_supported(k_rbf, l_sbf, dg)) {  // as egn_triplet_fwd_basis
+  if (g_triplet_path != 1 && fast_supported(k_rbf, l_sbf, dg)) {  // as egn_triplet_fwd_basis
     char* fws = reinterpret_cast<char*>(workspace) + generic_ws_bytes(num_nodes, k_rbf, l_sbf, dg);
     if (int rc = fast_bwd(edge_ptr, rev, g4, num_nodes, num_edges, X, W, k_rbf, l_sbf, dg, rbf_params(k_rbf, cutoff),
-                          S_bar, X_bar, W_bar, reinterpret_cast<float4*>(edge_grad), fws, st, phases, 1, tab, dtab))
+                          S_bar, X_bar, W_bar, reinterpret_cast<float4*>(edge_grad), fws, st, phases, basis, tab, dtab))
       return rc;
     if (max_degree <= kFastMaxDeg) return 0;
     min_n = kFastMaxDeg;

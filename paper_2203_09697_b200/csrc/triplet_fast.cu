@@ -48,18 +48,37 @@ __device__ __forceinline__ float rbf1(float d, int k, RbfParams rp) {
 // Basis MODE of the pairwise kernels: 0 = the reference's Gaussian rbf x cos(l a) = T_l(x);
 // 1 = GemNet-T's CBF: radial Bessel basis e_k(d) (rows of the per-call radial table, stride 8,
 // triplet_sh.cu radial_table_kernel) x Y_l0(a) = sqrt((2l+1)/4pi) P_l(x).
-template <int K, int MODE = 0>
+// MODE 2 = DimeNet++'s SBF: radial part sqrt(2/c^3)/|j_{l+1}(z_lk)| u(d/c) j_l(z_lk d/c) depends on
+// (k, l) (table rows of 44 floats, [k][l]) x the same Y_l0 angular rows as MODE 1.
+// Radial rows per in-edge in shared memory (rb_stride floats): MODE 0 / 1 K values; MODE 2 the
+// K x L values as [k][8] (LMAJOR = false: l pairs adjacent, for the gate products) or [l][8]
+// (LMAJOR = true: k pairs adjacent, for bw2's weight-gradient epilogue), zero padded.
+template <int K, int L, int MODE>
+constexpr int rb_stride() { return MODE == 2 ? 8 * (K > L ? K : L) : K; }
+
+template <int K, int MODE = 0, bool LMAJOR = false>
 __device__ __forceinline__ void load_center(float4* Us, float* Rb, const float4* __restrict__ geo, int64_t off,
                                             int n, RbfParams rp, const float* __restrict__ rtab = nullptr,
                                             float* DRb = nullptr, const float* __restrict__ dtab = nullptr) {
   for (int i = threadIdx.x; i < n; i += kT) Us[i] = geo[off + i];
-  for (int i = threadIdx.x; i < n * K; i += kT) {
-    const int q = i / K, k = i - q * K;
-    if constexpr (MODE == 0) {
-      Rb[i] = rbf1(geo[off + q].w, k, rp);
-    } else {
-      Rb[i] = __ldg(rtab + (off + q) * 8 + k);
-      if (DRb) DRb[i] = __ldg(dtab + (off + q) * 8 + k);
+  if constexpr (MODE == 2) {
+    constexpr int L = 7, RS = rb_stride<K, 7, 2>(), TS = 44;  // sh radial table row (rad_stride<2>)
+    for (int i = threadIdx.x; i < n * RS; i += kT) {
+      const int q = i / RS, r = i - q * RS;
+      const int k = LMAJOR ? (r & 7) : (r >> 3), l = LMAJOR ? (r >> 3) : (r & 7);
+      const bool ok = k < K && l < L;
+      Rb[i] = ok ? __ldg(rtab + (off + q) * TS + k * L + l) : 0.f;
+      if (DRb) DRb[i] = ok ? __ldg(dtab + (off + q) * TS + k * L + l) : 0.f;
+    }
+  } else {
+    for (int i = threadIdx.x; i < n * K; i += kT) {
+      const int q = i / K, k = i - q * K;
+      if constexpr (MODE == 0) {
+        Rb[i] = rbf1(geo[off + q].w, k, rp);
+      } else {
+        Rb[i] = __ldg(rtab + (off + q) * 8 + k);
+        if (DRb) DRb[i] = __ldg(dtab + (off + q) * 8 + k);
+      }
     }
   }
 }
@@ -138,7 +157,7 @@ __device__ __forceinline__ void load_x(float (&xs)[kQC / 2], const int32_t* __re
   }
 }
 
-template <int K, int L, int RS = kCB>
+template <int K, int L, int RS = kCB, int MODE = 0>
 __device__ __forceinline__ void build_q(float* Qs, const float2 (&wreg)[K][kLP], const float* Rb,
                                         const float (&xs)[kQC / 2], int q0, int nq) {
   const int cq = threadIdx.x & 63, half = threadIdx.x >> 6;
@@ -147,17 +166,26 @@ __device__ __forceinline__ void build_q(float* Qs, const float2 (&wreg)[K][kLP],
     const int t = half + 2 * i;
     if (t >= nq) break;
     const float xv = xs[i];
-    const float* rb = Rb + (q0 + t) * K;
-    float r[K];
-#pragma unroll
-    for (int k = 0; k < K; ++k) r[k] = rb[k];
     float2 s[kLP];
 #pragma unroll
     for (int lp = 0; lp < kLP; ++lp) s[lp] = make_float2(0.f, 0.f);
+    if constexpr (MODE == 2) {  // radial (k, l) rows [k][8]: the l pairs are the packed operands
+      const float* rb = Rb + (q0 + t) * rb_stride<K, L, 2>();
 #pragma unroll
-    for (int k = 0; k < K; ++k)
+      for (int k = 0; k < K; ++k)
 #pragma unroll
-      for (int lp = 0; lp < kLP; ++lp) s[lp] = ffma2(r[k], wreg[k][lp], s[lp]);
+        for (int lp = 0; lp < kLP; ++lp)
+          s[lp] = ffma2(*reinterpret_cast<const float2*>(rb + k * 8 + 2 * lp), wreg[k][lp], s[lp]);
+    } else {
+      const float* rb = Rb + (q0 + t) * K;
+      float r[K];
+#pragma unroll
+      for (int k = 0; k < K; ++k) r[k] = rb[k];
+#pragma unroll
+      for (int k = 0; k < K; ++k)
+#pragma unroll
+        for (int lp = 0; lp < kLP; ++lp) s[lp] = ffma2(r[k], wreg[k][lp], s[lp]);
+    }
 #pragma unroll
     for (int l = 0; l < L; ++l) Qs[(t * L + l) * RS + cq] = xv * ((l & 1) ? s[l >> 1].y : s[l >> 1].x);
   }
@@ -260,7 +288,7 @@ fwd_kernel(const int64_t* __restrict__ edge_ptr, const int32_t* __restrict__ rev
            const float* __restrict__ W, int dg, RbfParams rp, float* __restrict__ S,
            const float* __restrict__ rtab) {
   __shared__ float4 Us[kN];
-  __shared__ float Rb[kN * K];
+  __shared__ __align__(16) float Rb[kN * rb_stride<K, L, MODE>()];
   __shared__ __align__(16) float Ct[kQC * L * kCB];
   __shared__ __align__(16) float Qs[kQC * L * kCB];
   const int tid = threadIdx.x;
@@ -294,7 +322,7 @@ fwd_kernel(const int64_t* __restrict__ edge_ptr, const int32_t* __restrict__ rev
       for (int q0 = 0; q0 < n; q0 += kQC) {
         const int nq = min(kQC, n - q0);
         __syncthreads();
-        build_q<K, L>(Qs, wreg, Rb, xs, q0, nq);
+        build_q<K, L, kCB, MODE>(Qs, wreg, Rb, xs, q0, nq);
         build_c<L, false, MODE>(Ct, Us, n, rows, q0, nq, RG);
         __syncthreads();
         if (q0 + kQC < n) load_x(xs, rev, X, off, q0 + kQC, min(kQC, n - q0 - kQC), dg, c0);
@@ -493,7 +521,7 @@ bw1_kernel(const int64_t* __restrict__ edge_ptr, const int32_t* __restrict__ rev
   extern __shared__ __align__(16) float bsm[];
   float4* Us = reinterpret_cast<float4*>(bsm);             // [kN]
   float* Rb = bsm + 4 * kN;                                 // [kN * K]
-  float* Qs = Rb + ((kN * K + 3) & ~3);                     // [kQC * L][kSbStride]
+  float* Qs = Rb + ((kN * rb_stride<K, L, MODE>() + 3) & ~3);  // [kQC * L][kSbStride]
   float* Sb = Qs + kQC * L * kSbStride;                     // [kN][kSbStride]
   float* XB = Sb + kN * kSbStride;                          // [kN][kN + 1]
   const int tid = threadIdx.x;
@@ -519,7 +547,7 @@ bw1_kernel(const int64_t* __restrict__ edge_ptr, const int32_t* __restrict__ rev
         const int nq = min(kQC, n - q0);
         if (q0 == 0) stage_wait();
         __syncthreads();
-        build_q<K, L, kSbStride>(Qs, wreg, Rb, xs, q0, nq);
+        build_q<K, L, kSbStride, MODE>(Qs, wreg, Rb, xs, q0, nq);
         __syncthreads();
         if (q0 + kQC < n) load_x(xs, rev, X, off, q0 + kQC, min(kQC, n - q0 - kQC), dg, c0);
         switch (PP) {
@@ -627,13 +655,14 @@ bw2_kernel(const int64_t* __restrict__ edge_ptr, const int32_t* __restrict__ rev
   static_assert(L <= 8, "L <= 8");
   extern __shared__ __align__(16) float dsm[];
   float4* Us = reinterpret_cast<float4*>(dsm);      // [64]
-  float* Rb = dsm + 4 * kN;                          // [64 * K]
-  float* Cb = Rb + ((kN * K + 3) & ~3);              // [p][TQ q][8 l]; QB [TQ][L][64] aliases it
+  constexpr int RBS = rb_stride<K, L, MODE>();       // radial row per in-edge (MODE 2: [l][8 k])
+  float* Rb = dsm + 4 * kN;                          // [64 * RBS]
+  float* Cb = Rb + ((kN * RBS + 3) & ~3);            // [p][TQ q][8 l]; QB [TQ][L][64] aliases it
   float* Sb = Cb + kN * 16 * 8;                      // Sbar rows of the centre, this channel block
   float* Wsm = Sb + kN * kCB;                        // W[k, l, c0 + c]
   float* DD = Wsm + K * L * kCB;                     // [16][2] dd partial per row and warp
-  float* DRb = DD + 32;                               // [64 * K] radial d-derivatives (MODE 1)
-  int* Rv = reinterpret_cast<int*>(DRb + kN * K);      // [64] rev of the centre's edges
+  float* DRb = DD + 32;                               // [64 * RBS] radial d-derivatives (MODE 1, 2)
+  int* Rv = reinterpret_cast<int*>(DRb + kN * RBS);    // [64] rev of the centre's edges
   const int tid = threadIdx.x;
   const int c = tid & (kCB - 1), h = tid >> 6;       // epilogue: channel, row half
   const int64_t c0 = static_cast<int64_t>(blockIdx.y) * kCB;
@@ -662,7 +691,7 @@ bw2_kernel(const int64_t* __restrict__ edge_ptr, const int32_t* __restrict__ rev
     __syncthreads();
     stage_rows(Sb, kCB, Sbar, off, n, dg, static_cast<int>(c0));
     for (int i = tid; i < n; i += kT) Rv[i] = rev[off + i];
-    load_center<K, MODE>(Us, Rb, geo, off, n, rp, rtab, MODE == 0 ? nullptr : DRb, dtab);
+    load_center<K, MODE, true>(Us, Rb, geo, off, n, rp, rtab, MODE == 0 ? nullptr : DRb, dtab);
     for (int qb0 = 0; qb0 < n; qb0 += 16) {
       const int nr = min(16, n - qb0);
       const int TQ = nr <= 8 ? 8 : 16;
@@ -709,6 +738,36 @@ bw2_kernel(const int64_t* __restrict__ edge_ptr, const int32_t* __restrict__ rev
         const int r = h + 2 * i;
         if (r >= nr) break;
         const int q = qb0 + r;
+        float qv[L];
+#pragma unroll
+        for (int l = 0; l < L; ++l) qv[l] = Cb[(r * L + l) * kCB + c];
+        if constexpr (MODE == 2) {
+          // radial rows [l][8 k] (k pairs packed): X_bar = sum_kl R W Qbar, dd = X sum_kl R' W Qbar,
+          // W_bar[k, l] += R X Qbar_l
+          const float* rr = Rb + q * RBS;
+          const float* dr = DRb + q * RBS;
+          const float x = xo[i];
+          float2 xb2 = make_float2(0.f, 0.f), ds2 = make_float2(0.f, 0.f);
+#pragma unroll
+          for (int l = 0; l < L; ++l) {
+            const float rbar = qv[l] * x;
+#pragma unroll
+            for (int k = 0; k < KP; ++k) {
+              const float2 r2 = *reinterpret_cast<const float2*>(rr + l * 8 + 2 * k);
+              const float2 d2 = *reinterpret_cast<const float2*>(dr + l * 8 + 2 * k);
+              const float2 wq = ffma2(qv[l], wr[k][l], make_float2(0.f, 0.f));
+              xb2 = ffma2(r2, wq, xb2);
+              ds2 = ffma2(d2, wq, ds2);
+              wb[k][l] = ffma2(rbar, r2, wb[k][l]);
+            }
+          }
+          if (cok) Xbar[static_cast<int64_t>(Rv[q]) * dg + c0 + c] = xb2.x + xb2.y;
+          float dd = (ds2.x + ds2.y) * x;
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) dd += __shfl_xor_sync(0xffffffffu, dd, o);
+          if ((tid & 31) == 0) DD[r * 2 + ((tid >> 5) & 1)] = dd;
+          continue;
+        }
         const float d = Us[q].w;
         float rb[K];
         float2 v2[KP], rb2[KP];
@@ -719,9 +778,6 @@ bw2_kernel(const int64_t* __restrict__ edge_ptr, const int32_t* __restrict__ rev
           rb2[k] = make_float2(rb[2 * k], rb[2 * k + 1]);
           v2[k] = make_float2(0.f, 0.f);
         }
-        float qv[L];
-#pragma unroll
-        for (int l = 0; l < L; ++l) qv[l] = Cb[(r * L + l) * kCB + c];
 #pragma unroll
         for (int k = 0; k < KP; ++k)
 #pragma unroll
@@ -832,7 +888,7 @@ int fast_fwd(const int64_t* edge_ptr, const int32_t* rev, const float4* geo, int
              const float* W, int K, int L, int dg, RbfParams rp, float* S, cudaStream_t st, int mode,
              const float* rtab) {
   // 4 CTAs per SM (128 registers): 5 or 6 (96 / 80 registers, spilling) measured 12% / 36% slower
-  auto kern = mode == 1 ? fast::fwd_kernel<6, 7, 4, 1> : fast::fwd_kernel<6, 7>;
+  auto kern = mode == 2 ? fast::fwd_kernel<6, 7, 4, 2> : (mode == 1 ? fast::fwd_kernel<6, 7, 4, 1> : fast::fwd_kernel<6, 7>);
   // one centre per CTA: no tail imbalance from static round-robin over unequal degrees
   const int grid = static_cast<int>(std::min<int64_t>(nv, 1 << 30));
   kern<<<grid, fast::kT, 0, st>>>(edge_ptr, rev, geo, nv, X, W, dg, rp, S, rtab);
@@ -862,11 +918,16 @@ int fast_bwd(const int64_t* edge_ptr, const int32_t* rev, const float4* geo, int
   const int ncb = (dg + fast::kCB - 1) / fast::kCB;
   if (phases & 1) {
     const int grid = static_cast<int>(std::min<int64_t>(nv, 1 << 30));
-    const size_t smem1 = (4 * fast::kN + ((fast::kN * 6 + 3) & ~3) + fast::kQC * 7 * fast::kSbStride +
+    const int rbs = mode == 2 ? fast::rb_stride<6, 7, 2>() : 6;
+    const size_t smem1 = (4 * fast::kN + ((fast::kN * rbs + 3) & ~3) + fast::kQC * 7 * fast::kSbStride +
                           fast::kN * fast::kSbStride + fast::kN * (fast::kN + 1)) *
                          sizeof(float);
-    static bool c10 = false, c11 = false;  // 3 CTAs per SM: 168 registers, no spills (4: 128, spilling, 1% slower)
-    if (mode == 1) {
+    static bool c10 = false, c11 = false, c12 = false;  // 3 CTAs per SM: 168 registers, no spills (4: 128, spilling, 1% slower)
+    if (mode == 2) {
+      auto kern = fast::bw1_kernel<6, 7, 3, 2>;
+      fast_set_smem(kern, smem1, c12);
+      kern<<<grid, fast::kT, smem1, st>>>(edge_ptr, rev, geo, nv, X, W, dg, rp, Sbar, edge_grad, rtab);
+    } else if (mode == 1) {
       auto kern = fast::bw1_kernel<6, 7, 3, 1>;
       fast_set_smem(kern, smem1, c11);
       kern<<<grid, fast::kT, smem1, st>>>(edge_ptr, rev, geo, nv, X, W, dg, rp, Sbar, edge_grad, rtab);
@@ -881,10 +942,16 @@ int fast_bwd(const int64_t* edge_ptr, const int32_t* rev, const float4* geo, int
   const int gx = static_cast<int>(std::min<int64_t>(nv, static_cast<int64_t>(kNumSMs) * 3));
   float* wpart = reinterpret_cast<float*>(ws);
   float* ddpart = wpart + static_cast<int64_t>(ncb) * gx * K * L * fast::kCB;
-  const size_t smem = (4 * fast::kN + ((fast::kN * 6 + 3) & ~3) + fast::kN * 128 + fast::kN * fast::kCB +
-                       6 * 7 * fast::kCB + 32 + fast::kN * 6 + fast::kN) * sizeof(float);
-  static bool c20 = false, c21 = false;
-  if (mode == 1) {
+  const int rbs2 = mode == 2 ? fast::rb_stride<6, 7, 2>() : 6;
+  const size_t smem = (4 * fast::kN + ((fast::kN * rbs2 + 3) & ~3) + fast::kN * 128 + fast::kN * fast::kCB +
+                       6 * 7 * fast::kCB + 32 + fast::kN * rbs2 + fast::kN) * sizeof(float);
+  static bool c20 = false, c21 = false, c22 = false;
+  if (mode == 2) {  // 2 CTAs per SM (the (k, l) radial rows and their derivatives in shared memory)
+    auto k2 = fast::bw2_kernel<6, 7, 2, 2>;
+    fast_set_smem(k2, smem, c22);
+    k2<<<dim3(gx, ncb), fast::kT, smem, st>>>(edge_ptr, rev, geo, nv, X, W, dg, rp, Sbar, Xbar, wpart, ddpart, ne,
+                                              edge_grad, rtab, dtab);
+  } else if (mode == 1) {
     auto k2 = fast::bw2_kernel<6, 7, 3, 1>;
     fast_set_smem(k2, smem, c21);
     k2<<<dim3(gx, ncb), fast::kT, smem, st>>>(edge_ptr, rev, geo, nv, X, W, dg, rp, Sbar, Xbar, wpart, ddpart, ne,

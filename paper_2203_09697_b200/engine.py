@@ -341,7 +341,7 @@ class Engine:
         # the angle adjoint of the triplet interaction (edge_grad x, y, z) feeds only the final
         # positions adjoint: it runs on a third stream, overlapping the rest of the backward,
         # and is joined before the first later writer of edge_grad (rbf_bwd)
-        angle = self._side_stream(bg, 2) if c.basis_code != 2 else None  # DimeNet SBF: one chain
+        angle = self._side_stream(bg, 2)
         angle_keep = []
         pending = []
 

@@ -304,10 +304,6 @@ def triplet_bwd(edge_ptr, rev, geo, X, Wk, cutoff, S_bar, edge_grad, X_bar=None,
         W_bar = torch.empty_like(Wk)
     if max_degree is None:
         max_degree = int((edge_ptr[1:] - edge_ptr[:-1]).max().item()) if nv else 0
-    if basis > 1 and phases != 3:  # the DimeNet SBF basis runs one adjoint kernel chain
-        if phases == 1:
-            return None, None
-        phases = 3
     if dg > MAX_TRIPLET_WIDTH:
         for c0, c1 in _channel_chunks(dg):
             xb, wb = triplet_bwd(edge_ptr, rev, geo, X[:, c0:c1].contiguous(), Wk[:, :, c0:c1].contiguous(), cutoff,
