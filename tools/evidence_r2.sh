@@ -31,8 +31,8 @@ ncu --set full --import-source on --clock-control none -k regex:bw2_kernel -s 4 
 # spherical-harmonic triplet kernels on the C5 deg-500 d_g 64 graph
 ncu --set full --import-source on --clock-control none -k regex:"fwd_moments|fwd_apply|bwd_moments|bwd_apply" -c 4 -o $O/r2e_sh500 python tools/sh_profile_case.py 500 64 sh > $O/r2e_ncu6.log 2>&1
 ncu --set full --import-source on --clock-control none -k regex:gemm_tf32x3 -s 3 -c 1 -o $O/r2e_gemm_xl python tools/gemm_one_shape.py 14792 2048 2048 --kind fwd --reps 1 > $O/r2e_ncu7.log 2>&1
-# Bessel bases (SH kernels, MODE 2 = DimeNet SBF, with the per-call radial table) on the C1 batch
-ncu --set full --import-source on --clock-control none -k regex:"radial_table|bwd_apply|fwd_moments" -s 12 -c 3 -o $O/r2e_sh_bessel_c1 python tools/profile_step.py --workload dimenet-pp-small --basis bessel --plain --steps 1 > $O/r2e_ncu8.log 2>&1
+# Bessel bases on the C1 batch: per-call radial table and the pairwise kernels in MODE 2 (DimeNet SBF)
+ncu --set full --import-source on --clock-control none -k regex:"radial_table|fwd_kernel|bw2_kernel" -s 12 -c 3 -o $O/r2e_sh_bessel_c1 python tools/profile_step.py --workload dimenet-pp-small --basis bessel --plain --steps 1 > $O/r2e_ncu8.log 2>&1
 
 python tools/gemm_census.py --out $O/r2e_gemm_census.txt > /dev/null 2>&1
 python tools/profile_step.py --out $O/r2e_step_kernels_c2.txt > /dev/null 2>&1
