@@ -188,8 +188,8 @@ int egn_triplet_bwd_basis(const int64_t* edge_ptr, const int32_t* rev, const flo
                           int64_t num_edges, int max_degree, const float* X, const float* W, int k_rbf, int l_sbf,
                           int dg, double cutoff, int basis, const float* S_bar, float* X_bar, float* W_bar,
                           float* edge_grad, void* workspace, egn_stream_t stream);
-/* egn_triplet_bwd_basis in the phases of egn_triplet_bwd_ex (basis 1 on the small-degree
- * kernels; elsewhere phase 1 does nothing and phase 2 all).  Phase 1 needs its own workspace of
+/* egn_triplet_bwd_basis in the phases of egn_triplet_bwd_ex (centres of degree <= 64, both
+ * bases; on the forced spherical-harmonic path phase 1 does nothing and phase 2 all).  Phase 1 needs its own workspace of
  * egn_triplet_bwd_angle_workspace_bytes (its radial table), so both phases can run at once. */
 int64_t egn_triplet_bwd_angle_workspace_bytes(int64_t num_edges, int basis);
 int egn_triplet_bwd_basis_ex(const int64_t* edge_ptr, const int32_t* rev, const float* geo, int64_t num_nodes,
