@@ -837,10 +837,11 @@ bw2_kernel(const int64_t* __restrict__ edge_ptr, const int32_t* __restrict__ rev
 }
 
 // W_bar[k,l,c] = sum over x-CTAs of the partials of channel block c / 64; 32 outputs per
-// block, 8 warps split the partials, fixed-order combine
-__global__ void reduce_wbar_kernel(const float* __restrict__ part, int gx, int K, int L, int dg,
-                                   float* __restrict__ out) {
-  __shared__ float red[8][33];
+// block, kRW warps split the partials (eight loads in flight per thread), fixed-order combine
+constexpr int kRW = 32;
+__global__ void __launch_bounds__(kRW * 32) reduce_wbar_kernel(const float* __restrict__ part, int gx, int K, int L,
+                                                               int dg, float* __restrict__ out) {
+  __shared__ float red[kRW][33];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int total = K * L * dg;
   const int i = blockIdx.x * 32 + lane;
@@ -848,15 +849,24 @@ __global__ void reduce_wbar_kernel(const float* __restrict__ part, int gx, int K
   if (i < total) {
     const int kl = i / dg, c = i - kl * dg;
     const int cb = c / kCB, cc = c - cb * kCB;
-    const float* src = part + static_cast<int64_t>(cb) * gx * (K * L * kCB) + kl * kCB + cc;
-    for (int x = w; x < gx; x += 8) s += src[static_cast<int64_t>(x) * (K * L * kCB)];
+    const int64_t st = K * L * kCB;
+    const float* src = part + static_cast<int64_t>(cb) * gx * st + kl * kCB + cc;
+    int x = w;
+    for (; x + 7 * kRW < gx; x += 8 * kRW) {
+      float a[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) a[u] = src[static_cast<int64_t>(x + u * kRW) * st];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) s += a[u];
+    }
+    for (; x < gx; x += kRW) s += src[static_cast<int64_t>(x) * st];
   }
   red[w][lane] = s;
   __syncthreads();
   if (w == 0 && i < total) {
     float t = 0.f;
 #pragma unroll
-    for (int k = 0; k < 8; ++k) t += red[k][lane];
+    for (int k = 0; k < kRW; ++k) t += red[k][lane];
     out[i] = t;
   }
 }
@@ -963,7 +973,7 @@ int fast_bwd(const int64_t* edge_ptr, const int32_t* rev, const float4* geo, int
                                               edge_grad, nullptr, nullptr);
   }
   if (check_launch("triplet_bw2_fast")) return 1;
-  fast::reduce_wbar_kernel<<<static_cast<int>((static_cast<int64_t>(K) * L * dg + 31) / 32), 256, 0, st>>>(
+  fast::reduce_wbar_kernel<<<static_cast<int>((static_cast<int64_t>(K) * L * dg + 31) / 32), fast::kRW * 32, 0, st>>>(
       wpart, gx, K, L, dg, Wbar);
   if (check_launch("triplet_bw2_reduce")) return 1;
   if (ncb == 1) return 0;  // bw2 added dE/dd directly
