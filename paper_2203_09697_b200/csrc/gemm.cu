@@ -1238,10 +1238,13 @@ __global__ void __launch_bounds__(128) gemm_simt_kernel(int64_t M, int N, int ns
 // slab kernel above waits one L2/DRAM latency per 32-wide K slab with one warp per SM
 // sub-partition; here every 16 B chunk of the CTA's A panel [32 x K] and B panel [64 x K]
 // (or [K x 64]) is put in flight at once with cp.async (zero-filled past M / N), the
-// epilogue operands are loaded into registers behind them, and 256 threads split K in two
-// halves (fixed-order combine through shared memory).  (One bulk copy per row through the
+// epilogue operands are loaded into registers behind them, and PS x 128 threads split K in PS
+// parts (fixed-order combine through shared memory).  PS = 4 when the grid is under half a wave
+// (C1's 256-row node products: 16 CTAs, step 0.87 -> 0.85 ms); PS = 2 otherwise (4 measured
+// 10.1 -> 11.7 us per call on the 160-CTA C2 node products).  (One bulk copy per row through the
 // TMA engine measured slower: ~80 small copies per CTA serialise in the copy engine.)
 constexpr int kPanelMaxK = 256;
+constexpr int kPanelMaxSplit = 4;  // K parts (128 threads each): 2, or 4 when the grid is under half a wave
 __device__ __forceinline__ void cp16_zfill(void* dst, const void* src, bool valid) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src), "r"(valid ? 16 : 0)
                : "memory");
@@ -1253,17 +1256,18 @@ static size_t panel_smem(int K, bool b_mn) {
   const int kp = panel_pitch(K);
   const size_t panels = static_cast<size_t>(kSimtM) * kp + (b_mn ? static_cast<size_t>(K) * (kSimtN + 4)
                                                                  : static_cast<size_t>(kSimtN) * kp);
-  return sizeof(float) * std::max<size_t>(panels, 2 * 2 * 4 * 128);  // >= the half-combine exchange
+  return sizeof(float) * std::max<size_t>(panels, kPanelMaxSplit * 4 * 4 * 128);  // >= the combine exchange
 }
 
-// CTA tile 32 x 64: thread (ty, tx) of each K half owns rows ty + 8 i (i < 4) and columns
+// CTA tile 32 x 64: thread (ty, tx) of each K part owns rows ty + 8 i (i < 4) and columns
 // tx + 16 j (tx * 4 + j when BMN).
-template <bool BMN>
-__global__ void __launch_bounds__(256) gemm_simt_panel_kernel(int64_t M, int N, int nseg, const float* __restrict__ a0,
+template <bool BMN, int PS>
+__global__ void __launch_bounds__(128 * PS) gemm_simt_panel_kernel(int64_t M, int N, int nseg, const float* __restrict__ a0,
                                                               int64_t lda0, const float* __restrict__ b0,
                                                               int64_t ldb0, int k0, const float* __restrict__ a1,
                                                               int64_t lda1, const float* __restrict__ b1,
                                                               int64_t ldb1, int k1, Params P) {
+  constexpr int kPanelSplit = PS, kPanelThreads = 128 * PS, kPanelRows = 4 / PS;
   extern __shared__ __align__(16) float psm[];
   const int K = k0 + (nseg > 1 ? k1 : 0);
   const int kp = panel_pitch(K);
@@ -1274,14 +1278,14 @@ __global__ void __launch_bounds__(256) gemm_simt_panel_kernel(int64_t M, int N, 
   const int n0 = blockIdx.y * kSimtN;
   const int kq = K / 4;  // 16 B chunks per K row
   // ---- issue the panels
-  for (int c = tid; c < kSimtM * kq; c += 256) {
+  for (int c = tid; c < kSimtM * kq; c += kPanelThreads) {
     const int r = c / kq, k = (c - r * kq) * 4;
     const bool ok = m0 + r < M;
     const float* src = k < k0 ? a0 + (ok ? (m0 + r) * lda0 : 0) + k : a1 + (ok ? (m0 + r) * lda1 : 0) + (k - k0);
     cp16_zfill(As + r * kp + k, src, ok);
   }
   if (!BMN) {
-    for (int c = tid; c < kSimtN * kq; c += 256) {
+    for (int c = tid; c < kSimtN * kq; c += kPanelThreads) {
       const int r = c / kq, k = (c - r * kq) * 4;
       const bool ok = n0 + r < N;
       const int64_t n = ok ? n0 + r : 0;
@@ -1289,7 +1293,7 @@ __global__ void __launch_bounds__(256) gemm_simt_panel_kernel(int64_t M, int N, 
       cp16_zfill(Bs + r * kp + k, src, ok);
     }
   } else {
-    for (int c = tid; c < K * (kSimtN / 4); c += 256) {
+    for (int c = tid; c < K * (kSimtN / 4); c += kPanelThreads) {
       const int k = c >> 4, nq = (c & 15) * 4;
       const bool ok = n0 + nq < N;
       const float* src = k < k0 ? b0 + static_cast<int64_t>(k) * ldb0 + (ok ? n0 + nq : 0)
@@ -1298,13 +1302,13 @@ __global__ void __launch_bounds__(256) gemm_simt_panel_kernel(int64_t M, int N, 
     }
   }
   asm volatile("cp.async.commit_group;" ::: "memory");
-  // ---- epilogue operands of this thread's 8 outputs (rows ty + 8 i, i = 2 h + ii) behind them
+  // ---- epilogue operands of the outputs this thread finishes (rows ty + 8 i, i = kPanelRows h + ii)
   const int fl = P.flags;
   auto ncol = [&](int j) { return BMN ? n0 + tx * 4 + j : n0 + tx + 16 * j; };
-  float add[2][4], aux[2][4];
+  float add[kPanelRows][4], aux[kPanelRows][4];
 #pragma unroll
-  for (int ii = 0; ii < 2; ++ii) {
-    const int64_t m = m0 + ty + 8 * (2 * h + ii);
+  for (int ii = 0; ii < kPanelRows; ++ii) {
+    const int64_t m = m0 + ty + 8 * (kPanelRows * h + ii);
     const bool okm = m < M;
     const int64_t gr = (okm && (fl & EPI_GATHER)) ? static_cast<int64_t>(P.gidx[m]) : 0;
 #pragma unroll
@@ -1321,9 +1325,8 @@ __global__ void __launch_bounds__(256) gemm_simt_panel_kernel(int64_t M, int N, 
   }
   asm volatile("cp.async.wait_all;" ::: "memory");
   __syncthreads();
-  // ---- this half's share of K (multiples of 4)
-  const int kh = (K / 8) * 4;
-  const int kb = h ? kh : 0, ke = h ? K : kh;
+  // ---- this part's share of K (multiples of 4)
+  const int kb = (K / 4) * h / kPanelSplit * 4, ke = (K / 4) * (h + 1) / kPanelSplit * 4;
   float acc[4][4];
 #pragma unroll
   for (int i = 0; i < 4; ++i)
@@ -1360,24 +1363,27 @@ __global__ void __launch_bounds__(256) gemm_simt_panel_kernel(int64_t M, int N, 
       }
     }
   }
-  // ---- combine the halves: each half hands the other the rows it finishes
+  // ---- combine the parts: every part parks its 16 partial sums, then part h adds the
+  // kPanelSplit partials of its rows in K order (the same order for every element)
   __syncthreads();  // panels consumed
-  float* xch = psm;  // [2 halves][2 rows][4][128 threads]
+  float* xch = psm;  // [kPanelSplit parts][4 rows][4][128 threads]
 #pragma unroll
-  for (int ii = 0; ii < 2; ++ii)
+  for (int i = 0; i < 4; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) xch[((h * 2 + ii) * 4 + j) * 128 + t] = h ? acc[ii][j] : acc[2 + ii][j];
+    for (int j = 0; j < 4; ++j) xch[((h * 4 + i) * 4 + j) * 128 + t] = acc[i][j];
   __syncthreads();
 #pragma unroll
-  for (int ii = 0; ii < 2; ++ii) {
-    const int64_t m = m0 + ty + 8 * (2 * h + ii);
+  for (int ii = 0; ii < kPanelRows; ++ii) {
+    const int i = kPanelRows * h + ii;
+    const int64_t m = m0 + ty + 8 * i;
     if (m >= M) continue;
     float v[4];
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      // low-K half first, the same order for every element
-      const float other = xch[(((1 - h) * 2 + ii) * 4 + j) * 128 + t];
-      v[j] = (h ? other + acc[2 + ii][j] : acc[ii][j] + other) + add[ii][j];
+      float sum = xch[(i * 4 + j) * 128 + t];
+#pragma unroll
+      for (int p = 1; p < kPanelSplit; ++p) sum += xch[((p * 4 + i) * 4 + j) * 128 + t];
+      v[j] = sum + add[ii][j];
     }
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
@@ -1656,14 +1662,20 @@ extern "C" int egn_gemm(int64_t M, int N, int nseg, const float* a0, int64_t lda
     if (panel && K <= kPanelMaxK) {
       static const bool attr = [] {
         const int mx = static_cast<int>(std::max(panel_smem(kPanelMaxK, false), panel_smem(kPanelMaxK, true)));
-        cudaFuncSetAttribute(gemm_simt_panel_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-        cudaFuncSetAttribute(gemm_simt_panel_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        cudaFuncSetAttribute(gemm_simt_panel_kernel<false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        cudaFuncSetAttribute(gemm_simt_panel_kernel<true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        cudaFuncSetAttribute(gemm_simt_panel_kernel<false, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        cudaFuncSetAttribute(gemm_simt_panel_kernel<true, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
         return true;
       }();
       (void)attr;
       const size_t sm = panel_smem(K, b_mn);
-      if (b_mn) gemm_simt_panel_kernel<true><<<grid, 256, sm, st>>>(M, N, nseg, a0, lda0, b0, ldb0, k0, a1, lda1, b1, ldb1, k1, P);
-      else gemm_simt_panel_kernel<false><<<grid, 256, sm, st>>>(M, N, nseg, a0, lda0, b0, ldb0, k0, a1, lda1, b1, ldb1, k1, P);
+      const bool wide = static_cast<int64_t>(grid.x) * grid.y < kNumSMs / 2;
+#define EGN_PANEL(BM_, PS_) \
+  gemm_simt_panel_kernel<BM_, PS_><<<grid, 128 * PS_, sm, st>>>(M, N, nseg, a0, lda0, b0, ldb0, k0, a1, lda1, b1, ldb1, k1, P)
+      if (b_mn) { if (wide) EGN_PANEL(true, 4); else EGN_PANEL(true, 2); }
+      else { if (wide) EGN_PANEL(false, 4); else EGN_PANEL(false, 2); }
+#undef EGN_PANEL
       return check_launch("gemm_simt_panel");
     }
     if (b_mn) gemm_simt_kernel<true><<<grid, 128, 0, st>>>(M, N, nseg, a0, lda0, b0, ldb0, k0, a1, lda1, b1, ldb1, k1, P);
