@@ -1565,17 +1565,30 @@ __global__ void __launch_bounds__(256) wgrad_simt_panel_kernel(int64_t R, int M,
   for (int i = 0; i < 4; ++i)
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
+  // packed FFMA2 over column pairs (j, j + 1): per element the same fma sequence as FFMA
+  float2 acc2[4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) acc2[i][0] = acc2[i][1] = make_float2(0.f, 0.f);
 #pragma unroll 4
   for (int r = rb; r < re; ++r) {
     const float4 a = *reinterpret_cast<const float4*>(&Gs[r][ty * 4]);
     const float4 b = *reinterpret_cast<const float4*>(&Xs[r][tx * 4]);
-    const float av[4] = {a.x, a.y, a.z, a.w}, bv[4] = {b.x, b.y, b.z, b.w};
+    const float av[4] = {a.x, a.y, a.z, a.w};
+    const float2 b01 = make_float2(b.x, b.y), b23 = make_float2(b.z, b.w);
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       cs[i] += av[i];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
+      const float2 a2 = make_float2(av[i], av[i]);
+      acc2[i][0] = __ffma2_rn(a2, b01, acc2[i][0]);
+      acc2[i][1] = __ffma2_rn(a2, b23, acc2[i][1]);
     }
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    acc[i][0] = acc2[i][0].x;
+    acc[i][1] = acc2[i][0].y;
+    acc[i][2] = acc2[i][1].x;
+    acc[i][3] = acc2[i][1].y;
   }
   __syncthreads();  // panels consumed
   float* xch = &Gs[0][0];  // [2 halves][2 rows][5][128 threads] (4 products + column sum)
