@@ -1336,86 +1336,86 @@ __global__ void __launch_bounds__(128 * PS) gemm_simt_panel_kernel(int64_t M, in
     for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
   if constexpr (PS == 2) {
 #pragma unroll 2
-  for (int k = kb; k < ke; k += 4) {
-    float4 a[4];
+    for (int k = kb; k < ke; k += 4) {
+      float4 a[4];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) a[i] = *reinterpret_cast<const float4*>(As + (ty + 8 * i) * kp + k);
-    if (!BMN) {
+      for (int i = 0; i < 4; ++i) a[i] = *reinterpret_cast<const float4*>(As + (ty + 8 * i) * kp + k);
+      if (!BMN) {
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const float4 b = *reinterpret_cast<const float4*>(Bs + (tx + 16 * j) * kp + k);
+        for (int j = 0; j < 4; ++j) {
+          const float4 b = *reinterpret_cast<const float4*>(Bs + (tx + 16 * j) * kp + k);
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          acc[i][j] = fmaf(a[i].x, b.x, acc[i][j]);
-          acc[i][j] = fmaf(a[i].y, b.y, acc[i][j]);
-          acc[i][j] = fmaf(a[i].z, b.z, acc[i][j]);
-          acc[i][j] = fmaf(a[i].w, b.w, acc[i][j]);
+          for (int i = 0; i < 4; ++i) {
+            acc[i][j] = fmaf(a[i].x, b.x, acc[i][j]);
+            acc[i][j] = fmaf(a[i].y, b.y, acc[i][j]);
+            acc[i][j] = fmaf(a[i].z, b.z, acc[i][j]);
+            acc[i][j] = fmaf(a[i].w, b.w, acc[i][j]);
+          }
         }
-      }
-    } else {
+      } else {
 #pragma unroll
-      for (int kk = 0; kk < 4; ++kk) {
-        const float4 b = *reinterpret_cast<const float4*>(Bs + (k + kk) * (kSimtN + 4) + tx * 4);
-        const float bv[4] = {b.x, b.y, b.z, b.w};
+        for (int kk = 0; kk < 4; ++kk) {
+          const float4 b = *reinterpret_cast<const float4*>(Bs + (k + kk) * (kSimtN + 4) + tx * 4);
+          const float bv[4] = {b.x, b.y, b.z, b.w};
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const float av = kk == 0 ? a[i].x : kk == 1 ? a[i].y : kk == 2 ? a[i].z : a[i].w;
+          for (int i = 0; i < 4; ++i) {
+            const float av = kk == 0 ? a[i].x : kk == 1 ? a[i].y : kk == 2 ? a[i].z : a[i].w;
 #pragma unroll
-          for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(av, bv[j], acc[i][j]);
+            for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(av, bv[j], acc[i][j]);
+          }
         }
       }
     }
-  }
   } else {
-  // packed FFMA2 accumulators: K-major B pairs even / odd k (two partial sums per output,
-  // added at the end); MN-major B pairs adjacent columns (the same per-element order as FFMA)
-  float2 acc2[4][4];
+    // packed FFMA2 accumulators: K-major B pairs even / odd k (two partial sums per output,
+    // added at the end); MN-major B pairs adjacent columns (the same per-element order as FFMA)
+    float2 acc2[4][4];
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+    for (int i = 0; i < 4; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) acc2[i][j] = make_float2(0.f, 0.f);
+      for (int j = 0; j < 4; ++j) acc2[i][j] = make_float2(0.f, 0.f);
 #pragma unroll 2
-  for (int k = kb; k < ke; k += 4) {
-    float4 a[4];
+    for (int k = kb; k < ke; k += 4) {
+      float4 a[4];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) a[i] = *reinterpret_cast<const float4*>(As + (ty + 8 * i) * kp + k);
-    if (!BMN) {
+      for (int i = 0; i < 4; ++i) a[i] = *reinterpret_cast<const float4*>(As + (ty + 8 * i) * kp + k);
+      if (!BMN) {
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const float4 b = *reinterpret_cast<const float4*>(Bs + (tx + 16 * j) * kp + k);
+        for (int j = 0; j < 4; ++j) {
+          const float4 b = *reinterpret_cast<const float4*>(Bs + (tx + 16 * j) * kp + k);
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          acc2[i][j] = __ffma2_rn(make_float2(a[i].x, a[i].y), make_float2(b.x, b.y), acc2[i][j]);
-          acc2[i][j] = __ffma2_rn(make_float2(a[i].z, a[i].w), make_float2(b.z, b.w), acc2[i][j]);
+          for (int i = 0; i < 4; ++i) {
+            acc2[i][j] = __ffma2_rn(make_float2(a[i].x, a[i].y), make_float2(b.x, b.y), acc2[i][j]);
+            acc2[i][j] = __ffma2_rn(make_float2(a[i].z, a[i].w), make_float2(b.z, b.w), acc2[i][j]);
+          }
         }
-      }
-    } else {
+      } else {
 #pragma unroll
-      for (int kk = 0; kk < 4; ++kk) {
-        const float4 b = *reinterpret_cast<const float4*>(Bs + (k + kk) * (kSimtN + 4) + tx * 4);
+        for (int kk = 0; kk < 4; ++kk) {
+          const float4 b = *reinterpret_cast<const float4*>(Bs + (k + kk) * (kSimtN + 4) + tx * 4);
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const float av = kk == 0 ? a[i].x : kk == 1 ? a[i].y : kk == 2 ? a[i].z : a[i].w;
-          const float2 av2 = make_float2(av, av);
-          // columns (0, 1) and (2, 3) of the thread: acc2[i][0] / acc2[i][1] hold them packed
-          acc2[i][0] = __ffma2_rn(av2, make_float2(b.x, b.y), acc2[i][0]);
-          acc2[i][1] = __ffma2_rn(av2, make_float2(b.z, b.w), acc2[i][1]);
+          for (int i = 0; i < 4; ++i) {
+            const float av = kk == 0 ? a[i].x : kk == 1 ? a[i].y : kk == 2 ? a[i].z : a[i].w;
+            const float2 av2 = make_float2(av, av);
+            // columns (0, 1) and (2, 3) of the thread: acc2[i][0] / acc2[i][1] hold them packed
+            acc2[i][0] = __ffma2_rn(av2, make_float2(b.x, b.y), acc2[i][0]);
+            acc2[i][1] = __ffma2_rn(av2, make_float2(b.z, b.w), acc2[i][1]);
+          }
         }
       }
     }
-  }
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    if (!BMN) {
+    for (int i = 0; i < 4; ++i) {
+      if (!BMN) {
 #pragma unroll
-      for (int j = 0; j < 4; ++j) acc[i][j] = acc2[i][j].x + acc2[i][j].y;
-    } else {
-      acc[i][0] = acc2[i][0].x;
-      acc[i][1] = acc2[i][0].y;
-      acc[i][2] = acc2[i][1].x;
-      acc[i][3] = acc2[i][1].y;
+        for (int j = 0; j < 4; ++j) acc[i][j] = acc2[i][j].x + acc2[i][j].y;
+      } else {
+        acc[i][0] = acc2[i][0].x;
+        acc[i][1] = acc2[i][0].y;
+        acc[i][2] = acc2[i][1].x;
+        acc[i][3] = acc2[i][1].y;
+      }
     }
-  }
   }
   // ---- combine the parts: every part parks its 16 partial sums, then part h adds the
   // kPanelSplit partials of its rows in K order (the same order for every element)
