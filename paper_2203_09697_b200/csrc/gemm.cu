@@ -489,6 +489,7 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_const
           if (elect_one()) {
             // A_lo / A_hi: TMEM columns [0, 32) / shared-memory raw tile (trunc_a), or TMEM
             // [32, 64) / [0, 32) (rna split of an MN-major A)
+            if (!(P.dbg & 1)) {  // (EGN_GEMM_DBG bit 1: no MMAs, commits only)
 #pragma unroll
             for (int k = 0; k < BK / 8; ++k) {  // small terms first
               const uint32_t ob = BMN ? k * 1024 : k * 32;
@@ -508,6 +509,7 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_const
               const uint64_t db = BMN ? sw128_mnmajor_desc_u(braw + ob) : sw128_kmajor_desc_u(braw + ob);
               if (trunc_a) mma_tf32(tacc, sw128_kmajor_desc_u(araw + k * 32), db, idesc, 1u);  // A_hi B_hi
               else mma_tf32_ta(tacc, ta + k * 8, db, idesc, 1u);
+            }
             }
             if (fend) mma_commit(&accf_bar[gr][bsel]);
             mma_commit(&tma_empty[s]);  // the raw tiles are free once these MMAs completed
@@ -545,7 +547,7 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_const
         asm volatile("tcgen05.fence::after_thread_sync;");
         const uint8_t* st = smem + s * kTmaSlot;
         const uint32_t ta = tmem + lane_off + A_TMEM + o * 64;
-        if (trunc) {
+        if (trunc && !(P.dbg & 2)) {  // (EGN_GEMM_DBG bit 2: no split math)
           // lo = x - trunc_tf32(x) only (the raw tiles are the hi parts)
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
