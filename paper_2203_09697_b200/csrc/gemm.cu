@@ -590,7 +590,7 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_const
           const float4* braw = reinterpret_cast<const float4*>(st + A_BYTES);
           float4* bl = reinterpret_cast<float4*>(opring + o * kOpSlot);
 #pragma unroll
-          for (int i = ct; i < B_BYTES / 16; i += 128) {
+          for (int i = (P.dbg & 8) ? B_BYTES / 16 : ct; i < B_BYTES / 16; i += 128) {  // (bit 8: no B_lo)
             const float4 v = braw[i];
             bl[i] = make_float4(tf32_lo_trunc<true>(v.x), tf32_lo_trunc<true>(v.y), tf32_lo_trunc<true>(v.z),
                                 tf32_lo_trunc<true>(v.w));
