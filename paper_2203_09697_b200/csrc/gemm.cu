@@ -69,10 +69,19 @@ struct Params {
   int mcast;               // 1: CTA pairs (cluster of 2) share each A k-block by TMA multicast
   int64_t split_stride;    // split-K: elements between partial outputs
   long long* trace;        // debug timeline (EGN_GEMM_TRACE), CTA 0 only
-  int dbg;                 // EGN_GEMM_DBG experiments: 1 no MMA, 2 no split math, 4 no TMEM reads
+  int dbg;                 // EGN_GEMM_DBG experiments: 4 no TMEM reads, 16 no B loads, 32 no A loads (n0 > 0);
+                           // with -DEGN_GEMM_ABLATE also 1 no MMA, 2 no split math, 8 no B_lo math
   int op_tma;              // (with store_warp) residual / aux rows arrive by TMA through mapOp
   int store_warp;          // (with tma_out) a dedicated warp issues the TMA stores
 };
+
+// Stage-ablation switches in the k-block loops cost ~4% at the XL widths even
+// when off, so they are compiled in only with -DEGN_GEMM_ABLATE.
+#ifdef EGN_GEMM_ABLATE
+constexpr bool kAblate = true;
+#else
+constexpr bool kAblate = false;
+#endif
 
 // ---------------------------------------------------------------- PTX helpers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -489,7 +498,7 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_const
           if (elect_one()) {
             // A_lo / A_hi: TMEM columns [0, 32) / shared-memory raw tile (trunc_a), or TMEM
             // [32, 64) / [0, 32) (rna split of an MN-major A)
-            if (!(P.dbg & 1)) {  // (EGN_GEMM_DBG bit 1: no MMAs, commits only)
+            if (!(kAblate && (P.dbg & 1))) {  // (ablation bit 1: no MMAs, commits only)
 #pragma unroll
             for (int k = 0; k < BK / 8; ++k) {  // small terms first
               const uint32_t ob = BMN ? k * 1024 : k * 32;
@@ -547,7 +556,7 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_const
         asm volatile("tcgen05.fence::after_thread_sync;");
         const uint8_t* st = smem + s * kTmaSlot;
         const uint32_t ta = tmem + lane_off + A_TMEM + o * 64;
-        if (trunc && !(P.dbg & 2)) {  // (EGN_GEMM_DBG bit 2: no split math)
+        if (trunc && !(kAblate && (P.dbg & 2))) {  // (ablation bit 2: no split math)
           // lo = x - trunc_tf32(x) only (the raw tiles are the hi parts)
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
@@ -590,7 +599,7 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_const
           const float4* braw = reinterpret_cast<const float4*>(st + A_BYTES);
           float4* bl = reinterpret_cast<float4*>(opring + o * kOpSlot);
 #pragma unroll
-          for (int i = (P.dbg & 8) ? B_BYTES / 16 : ct; i < B_BYTES / 16; i += 128) {  // (bit 8: no B_lo)
+          for (int i = (kAblate && (P.dbg & 8)) ? B_BYTES / 16 : ct; i < B_BYTES / 16; i += 128) {  // (bit 8: no B_lo)
             const float4 v = braw[i];
             bl[i] = make_float4(tf32_lo_trunc<true>(v.x), tf32_lo_trunc<true>(v.y), tf32_lo_trunc<true>(v.z),
                                 tf32_lo_trunc<true>(v.w));
