@@ -334,7 +334,12 @@ def _kernel_roofline(tr, bg, cfg):
     A = torch.randn((ne, de), device="cuda", generator=g)
     W = torch.randn((de, de), device="cuda", generator=g) * de ** -0.5
     R = torch.randn((ne, de), device="cuda", generator=g)
-    t_g = _time_kernel(lambda: ops.gemm(A, W, resid=R), 20, flush)
+    # as in the step: the weight's tf32 lo parts precomputed (egn_gemm_blo; EGN_GEMM_BLO=0: split warps)
+    W_lo = None
+    if os.environ.get("EGN_GEMM_BLO", "1") != "0":
+        W_lo = torch.empty_like(W)
+        ops.call("egn_tf32_lo", ops.ptr(W), de, de, de, ops.ptr(W_lo), de, ops.stream())
+    t_g = _time_kernel(lambda: ops.gemm(A, W, resid=R, b_lo=W_lo), 20, flush)
     b_gemm = 4 * (3 * ne * de + de * de)
     ach = b_gemm / t_g / 1e9
     traffic = None
@@ -351,7 +356,8 @@ def _kernel_roofline(tr, bg, cfg):
     # fp32-accurate products cost 3 TF32 MMAs: the attainable rate is tf32_peak / 3; the kernel is
     # tensor-bound when its intensity (fp32 FLOP per algorithmic byte) exceeds that rate / HBM
     tensor_bound = flops / b_gemm > (tf32_peak / 3) * 1e12 / (hbm * 1e9)
-    base = {"kernel": f"gemm_tf32x3 E x {de} x {de} (+residual), 3xTF32 on tcgen05",
+    base = {"kernel": f"gemm_tf32x3 E x {de} x {de} (+residual), 3xTF32 on tcgen05"
+                      + (", B lo parts by TMA (egn_gemm_blo)" if W_lo is not None else ""),
             "traffic": traffic, "traffic_source": f"profiles/r2_traffic.json:{key} (ncu --set full)" if traffic else None,
             "peak_source": "MEASURED_PEAKS.json" if peaks else "fallback",
             "launch_us": t_g * 1e6, "algorithmic_bytes": b_gemm, "algorithmic_flops": flops,

@@ -349,6 +349,18 @@ int egn_gemm(int64_t M, int N, int nseg, const float* a0, int64_t lda0, const fl
              const float* bias, const float* resid, int64_t ldr, const float* gsrc,
              const int32_t* gidx, int64_t ldg, const float* aux, int64_t ldaux, int flags,
              float* out, int64_t ldo, float* out2, int64_t ldo2, int b_mn, egn_stream_t stream);
+/* egn_gemm with the tf32 lo parts of B precomputed (b*_lo, from egn_tf32_lo; both segments,
+ * 16-byte aligned rows): the tensor-core path loads them by TMA instead of forming them per tile
+ * (bit-identical results).  For weights, whose lo parts change only when the weights do
+ * (egn/tape.py:104-119 linear). */
+int egn_gemm_blo(int64_t M, int N, int nseg, const float* a0, int64_t lda0, const float* b0, int64_t ldb0,
+                 int k0, const float* a1, int64_t lda1, const float* b1, int64_t ldb1, int k1,
+                 const float* bias, const float* resid, int64_t ldr, const float* gsrc,
+                 const int32_t* gidx, int64_t ldg, const float* aux, int64_t ldaux, int flags,
+                 float* out, int64_t ldo, float* out2, int64_t ldo2, int b_mn, const float* b0_lo,
+                 int64_t ldb0_lo, const float* b1_lo, int64_t ldb1_lo, egn_stream_t stream);
+/* lo[r, c] = tf32 lo part of x[r, c] (x - trunc_tf32(x), rounded to tf32) of a row-strided array. */
+int egn_tf32_lo(const float* x, int64_t rows, int cols, int64_t ldx, float* lo, int64_t ldl, egn_stream_t stream);
 
 /* Weight gradient out[M, N] (row stride ldo) (+)= g^T x with g [krows, M], x [krows, N] (both
  * MN-major on the tensor cores), split over krows across CTAs; partial tiles reduced in a fixed

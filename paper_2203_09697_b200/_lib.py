@@ -99,6 +99,9 @@ SIGNATURES: dict[str, tuple] = {
     "egn_column_sum": (_i32, [_p, _i64, _i32, _i64, _p, _p, _p]),
     "egn_gemm": (_i32, [_i64, _i32, _i32, _p, _i64, _p, _i64, _i32, _p, _i64, _p, _i64, _i32, _p, _p, _i64, _p,
                         _p, _i64, _p, _i64, _i32, _p, _i64, _p, _i64, _i32, _p]),
+    "egn_gemm_blo": (_i32, [_i64, _i32, _i32, _p, _i64, _p, _i64, _i32, _p, _i64, _p, _i64, _i32, _p, _p, _i64, _p,
+                            _p, _i64, _p, _i64, _i32, _p, _i64, _p, _i64, _i32, _p, _i64, _p, _i64, _p]),
+    "egn_tf32_lo": (_i32, [_p, _i64, _i32, _i64, _p, _i64, _p]),
     "egn_gemm_wgrad_workspace_bytes": (_i64, [_i64, _i32, _i32]),
     "egn_gemm_wgrad": (_i32, [_i64, _i32, _i32, _p, _i64, _p, _i64, _p, _i64, _p, _i32, _p, _p]),
     "egn_small_gemm_batched": (_i32, [_p, _i32, _p]),

@@ -238,6 +238,8 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
 //   warps 6..13  : accumulator warps: two groups of 4 (BN 64, group = tile parity) or one
 //                  group of 8 (BN 128, warp = lane quarter x column half).
 //   warp 14      : store warp (TMA stores of finished tiles, operand-row prefetch).
+//   warp 15      : (BLO instantiations, egn_gemm_blo) loads the precomputed lo tile of the
+//                  weight B into the operand slot by TMA; the split warps then form A_lo only.
 // Per k-step: A_lo.B_hi (A from TMEM), A_hi.B_lo and A_hi.B_hi (A from the TMA slot); the
 // MMA commit releases the TMA slot and the operand slot.
 // Accuracy: the tensor core accumulates with truncation, a bias that grows with
@@ -313,12 +315,13 @@ __device__ __forceinline__ float dsilu(float o) {
 // element (r, c) of a [32][32] epilogue chunk (granule swizzled by row)
 __device__ __forceinline__ int epi_idx(int r, int c) { return r * 32 + ((((c >> 2) ^ (r & 7))) << 2) + (c & 3); }
 
-template <bool AMN, bool BMN, int BN>
-__global__ void __launch_bounds__(480, 1)
+template <bool AMN, bool BMN, int BN, bool BLO = false>
+__global__ void __launch_bounds__(512, 1)
 gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_constant__ CUtensorMap mapB0,
                    const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ CUtensorMap mapB1,
                    const __grid_constant__ CUtensorMap mapOut, const __grid_constant__ CUtensorMap mapOut2,
-                   const __grid_constant__ CUtensorMap mapOp, Params P,
+                   const __grid_constant__ CUtensorMap mapOp, const __grid_constant__ CUtensorMap mapBlo0,
+                   const __grid_constant__ CUtensorMap mapBlo1, Params P,
                    int tiles_n, int splits, int total_items) {
   constexpr int A_BYTES = BM * BK * 4;  // 16 KB raw A k-block
   using C = Cfg<BN, true>;
@@ -333,6 +336,7 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_const
   uint8_t* opring = smem + kTmaRing * kTmaSlot;
   float* epi_all = reinterpret_cast<float*>(opring + kOpRing * kOpSlot);
   __shared__ __align__(8) uint64_t tma_full[kTmaRing], tma_empty[kTmaRing], op_full[kOpRing], op_empty[kOpRing];
+  __shared__ __align__(8) uint64_t blo_full[kOpRing];  // B_lo tile of the operand slot landed (BLO)
   __shared__ __align__(8) uint64_t accf_bar[kGroups][kAccBufs], acce_bar[kGroups][kAccBufs];
   // store warp hand-off per group: results staged (epi_full), staging read by the TMA store
   // (buf_free), next tile's operand rows landed in the staging buffers (op_bar)
@@ -367,6 +371,10 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_const
     asm volatile("prefetch.tensormap [%0];" ::"l"(&mapOut) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&mapOp) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&mapOut2) : "memory");
+    if (BLO) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&mapBlo0) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&mapBlo1) : "memory");
+    }
     for (int s = 0; s < kTmaRing; ++s) {
       mbar_init(&tma_full[s], 1);
       // the multicast leader reuses slot s only after both CTAs' split warps released it
@@ -375,6 +383,7 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_const
     for (int s = 0; s < kOpRing; ++s) {
       mbar_init(&op_full[s], 1);
       mbar_init(&op_empty[s], 1);
+      mbar_init(&blo_full[s], 1);
     }
     for (int gr = 0; gr < kGroups; ++gr) {
       for (int b = 0; b < kAccBufs; ++b) {
@@ -472,6 +481,7 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_const
       for (int kbl = 0; kbl < nk; ++kbl, ++it) {
         const int o = it % kOpRing;
         mbar_wait(&op_full[o], (it / kOpRing) & 1);
+        if constexpr (BLO) mbar_wait(&blo_full[o], (it / kOpRing) & 1);
         EGN_TRACE(1, it);
         asm volatile("tcgen05.fence::after_thread_sync;");
         const uint32_t bhi = smem_u32(opring + o * kOpSlot);
@@ -599,7 +609,7 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_const
           const float4* braw = reinterpret_cast<const float4*>(st + A_BYTES);
           float4* bl = reinterpret_cast<float4*>(opring + o * kOpSlot);
 #pragma unroll
-          for (int i = (kAblate && (P.dbg & 8)) ? B_BYTES / 16 : ct; i < B_BYTES / 16; i += 128) {  // (bit 8: no B_lo)
+          for (int i = (BLO || (kAblate && (P.dbg & 8))) ? B_BYTES / 16 : ct; i < B_BYTES / 16; i += 128) {
             const float4 v = braw[i];
             bl[i] = make_float4(tf32_lo_trunc<true>(v.x), tf32_lo_trunc<true>(v.y), tf32_lo_trunc<true>(v.z),
                                 tf32_lo_trunc<true>(v.w));
@@ -852,6 +862,36 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_const
 #undef EGN_ACC4
     }
     if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  } else if (warp == 15) {
+    // ---------------- B_lo loader (BLO): the precomputed lo tile of each k-block into the
+    // operand slot, once the MMAs that read the slot's previous contents completed
+    if constexpr (BLO) {
+      uint32_t it = 0;
+      for (int item = blockIdx.x; item < total_items; item += gridDim.x) {
+        int64_t m0;
+        int n0, kbeg, nk;
+        item_coords(item, m0, n0, kbeg, nk);
+        for (int kbl = 0; kbl < nk; ++kbl, ++it) {
+          const int o = it % kOpRing;
+          mbar_wait(&op_empty[o], ((it / kOpRing) & 1) ^ 1);
+          if (elect_one()) {
+            mbar_expect_tx(&blo_full[o], B_BYTES);
+            const int kb = kbeg + kbl;
+            const bool first = kb < nk0;
+            const int kk = (first ? kb : kb - nk0) * BK;
+            const CUtensorMap* mb = first ? &mapBlo0 : &mapBlo1;
+            uint8_t* dst = opring + o * kOpSlot;
+            if (BMN) {
+#pragma unroll
+              for (int i = 0; i < BN / 32; ++i) tma_load_2d(dst + i * 4096, mb, &blo_full[o], n0 + 32 * i, kk);
+            } else {
+              tma_load_2d(dst, mb, &blo_full[o], kk, n0);
+            }
+          }
+          __syncwarp();
+        }
+      }
+    }
   } else if (P.tma_out && P.store_warp) {
     // ---------------- store warp: TMA-stores each finished tile from the staging
     // buffers, then refills them with the operand rows of the group's next tile
@@ -987,7 +1027,8 @@ static int make_map(CUtensorMap* map, const float* ptr, int64_t outer, int64_t i
   return 0;
 }
 
-constexpr int kGemmThreads = 480;  // 14 role warps + the store warp
+constexpr int kGemmThreads = 480;     // 14 role warps + the store warp
+constexpr int kGemmThreadsBlo = 512;  // + the B_lo loader (BLO instantiations)
 
 // Output map [splits][M][N] (row stride ld, split stride M * ld), box 32 x 32 x 1,
 // SWIZZLE_128B: the epilogue buffer layout (16-byte granules XOR row % 8).
@@ -1010,12 +1051,14 @@ static bool out_map_ok(const float* out, int64_t ldo) {
   return (reinterpret_cast<uintptr_t>(out) & 15) == 0 && (ldo * 4) % 16 == 0;
 }
 
-template <bool AMN, bool BMN, int BN>
+template <bool AMN, bool BMN, int BN, bool BLO = false>
 static int launch(const CUtensorMap& a0, const CUtensorMap& b0, const CUtensorMap& a1, const CUtensorMap& b1,
                   const CUtensorMap& mo, const CUtensorMap& mo2, const CUtensorMap& mop, const Params& P, int splits,
-                  cudaStream_t st) {
+                  cudaStream_t st, const CUtensorMap* bl0 = nullptr, const CUtensorMap* bl1 = nullptr) {
+  const CUtensorMap& mbl0 = bl0 ? *bl0 : b0;
+  const CUtensorMap& mbl1 = bl1 ? *bl1 : b1;
   const size_t smem = Cfg<BN, true>::kSmem;
-  auto kern = gemm_tf32x3_kernel<AMN, BMN, BN>;
+  auto kern = gemm_tf32x3_kernel<AMN, BMN, BN, BLO>;
   static bool configured = false;
   if (!configured) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
@@ -1059,12 +1102,12 @@ static int launch(const CUtensorMap& a0, const CUtensorMap& b0, const CUtensorMa
       at[0].val.clusterDim.y = 1;
       at[0].val.clusterDim.z = 1;
       cfg.gridDim = dim3(grid, 1, 1);
-      cfg.blockDim = dim3(kGemmThreads, 1, 1);
+      cfg.blockDim = dim3(BLO ? kGemmThreadsBlo : kGemmThreads, 1, 1);
       cfg.dynamicSmemBytes = smem;
       cfg.stream = st;
       cfg.attrs = at;
       cfg.numAttrs = 1;
-      cudaLaunchKernelEx(&cfg, kern, a0, b0, a1, b1, mo, mo2, mop, Q, tiles_n, splits, total);
+      cudaLaunchKernelEx(&cfg, kern, a0, b0, a1, b1, mo, mo2, mop, mbl0, mbl1, Q, tiles_n, splits, total);
       return check_launch("gemm_tf32x3_mc");
     }
   }
@@ -1075,7 +1118,7 @@ static int launch(const CUtensorMap& a0, const CUtensorMap& b0, const CUtensorMa
     cudaMemset(d, 0, (1024 + 4 * kNumSMs) * sizeof(long long));
     static_assert(16 * 64 <= 1024, "trace rows");
     Q.trace = d;
-    kern<<<grid, kGemmThreads, smem, st>>>(a0, b0, a1, b1, mo, mo2, mop, Q, tiles_n, splits, total);
+    kern<<<grid, BLO ? kGemmThreadsBlo : kGemmThreads, smem, st>>>(a0, b0, a1, b1, mo, mo2, mop, mbl0, mbl1, Q, tiles_n, splits, total);
     long long h[1024 + 4 * kNumSMs];
     cudaStreamSynchronize(st);
     cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
@@ -1107,10 +1150,11 @@ static int launch(const CUtensorMap& a0, const CUtensorMap& b0, const CUtensorMa
   if (dbg) {
     Params Q = P;
     Q.dbg = dbg;
-    kern<<<grid, kGemmThreads, smem, st>>>(a0, b0, a1, b1, mo, mo2, mop, Q, tiles_n, splits, total);
+    kern<<<grid, BLO ? kGemmThreadsBlo : kGemmThreads, smem, st>>>(a0, b0, a1, b1, mo, mo2, mop, mbl0, mbl1, Q, tiles_n, splits, total);
     return check_launch("gemm_tf32x3");
   }
-  kern<<<grid, kGemmThreads, smem, st>>>(a0, b0, a1, b1, mo, mo2, mop, P, tiles_n, splits, total);
+  kern<<<grid, BLO ? kGemmThreadsBlo : kGemmThreads, smem, st>>>(a0, b0, a1, b1, mo, mo2, mop, mbl0, mbl1, P, tiles_n, splits,
+                                                                    total);
   return check_launch("gemm_tf32x3");
 }
 
@@ -1712,11 +1756,52 @@ static int flush_window(bool long_k) {
 
 using namespace egn;
 
+extern "C" int egn_gemm_blo(int64_t M, int N, int nseg, const float* a0, int64_t lda0, const float* b0,
+                            int64_t ldb0, int k0, const float* a1, int64_t lda1, const float* b1, int64_t ldb1, int k1,
+                            const float* bias, const float* resid, int64_t ldr, const float* gsrc,
+                            const int32_t* gidx, int64_t ldg, const float* aux, int64_t ldaux, int flags, float* out,
+                            int64_t ldo, float* out2, int64_t ldo2, int b_mn, const float* b0_lo, int64_t ldb0_lo,
+                            const float* b1_lo, int64_t ldb1_lo, egn_stream_t stream);
+
 extern "C" int egn_gemm(int64_t M, int N, int nseg, const float* a0, int64_t lda0, const float* b0, int64_t ldb0,
                         int k0, const float* a1, int64_t lda1, const float* b1, int64_t ldb1, int k1,
                         const float* bias, const float* resid, int64_t ldr, const float* gsrc, const int32_t* gidx,
                         int64_t ldg, const float* aux, int64_t ldaux, int flags, float* out, int64_t ldo,
                         float* out2, int64_t ldo2, int b_mn, egn_stream_t stream) {
+  return egn_gemm_blo(M, N, nseg, a0, lda0, b0, ldb0, k0, a1, lda1, b1, ldb1, k1, bias, resid, ldr, gsrc, gidx, ldg,
+                      aux, ldaux, flags, out, ldo, out2, ldo2, b_mn, nullptr, 0, nullptr, 0, stream);
+}
+
+// The lo parts x - trunc_tf32(x) (tf32-rounded, as the split warps form them) of a [rows, cols]
+// row-strided array, for egn_gemm_blo's B_lo operands.
+namespace egn {
+namespace gemm {
+__global__ void tf32_lo_kernel(const float* __restrict__ x, int64_t rows, int cols, int64_t ldx, float* __restrict__ lo,
+                               int64_t ldl) {
+  const int64_t n = rows * cols;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = i / cols;
+    const int c = static_cast<int>(i - r * cols);
+    lo[r * ldl + c] = tf32_lo_trunc<true>(x[r * ldx + c]);
+  }
+}
+}  // namespace gemm
+}  // namespace egn
+
+extern "C" int egn_tf32_lo(const float* x, int64_t rows, int cols, int64_t ldx, float* lo, int64_t ldl,
+                           egn_stream_t stream) {
+  if (rows == 0 || cols == 0) return 0;
+  egn::gemm::tf32_lo_kernel<<<grid_for(rows * cols, 256), 256, 0, as_stream(stream)>>>(x, rows, cols, ldx, lo, ldl);
+  return check_launch("tf32_lo");
+}
+
+extern "C" int egn_gemm_blo(int64_t M, int N, int nseg, const float* a0, int64_t lda0, const float* b0,
+                            int64_t ldb0, int k0, const float* a1, int64_t lda1, const float* b1, int64_t ldb1, int k1,
+                            const float* bias, const float* resid, int64_t ldr, const float* gsrc,
+                            const int32_t* gidx, int64_t ldg, const float* aux, int64_t ldaux, int flags, float* out,
+                            int64_t ldo, float* out2, int64_t ldo2, int b_mn, const float* b0_lo, int64_t ldb0_lo,
+                            const float* b1_lo, int64_t ldb1_lo, egn_stream_t stream) {
   using namespace egn::gemm;
   EGN_REQUIRE(nseg == 1 || nseg == 2, "nseg must be 1 or 2");
   EGN_REQUIRE(N >= 16 && N % 16 == 0, "GEMM N must be a positive multiple of 16 (got %d)", N);
@@ -1770,6 +1855,19 @@ extern "C" int egn_gemm(int64_t M, int N, int nseg, const float* a0, int64_t lda
   // A: K-major [M, K]; B: K-major [N, K] (weights (out, in)) or MN-major [K, N] (b_mn)
   if (int rc = make_map(&ma0, a0, M, k0, lda0, BM, kMapK)) return rc;
   if (int rc = b_mn ? make_map(&mb0, b0, k0, N, ldb0, BK, kMapMN) : make_map(&mb0, b0, N, k0, ldb0, BN, kMapK)) return rc;
+  // precomputed B_lo (both segments, 16-byte aligned rows): loaded by TMA instead of formed by
+  // the split warps (same values, bit-identical products)
+  CUtensorMap mbl0 = mb0, mbl1 = mb0;
+  const bool blo = b0_lo != nullptr && (nseg == 1 || b1_lo != nullptr) &&
+                   (reinterpret_cast<uintptr_t>(b0_lo) & 15) == 0 && ldb0_lo % 4 == 0 &&
+                   (nseg == 1 || ((reinterpret_cast<uintptr_t>(b1_lo) & 15) == 0 && ldb1_lo % 4 == 0));
+  if (blo) {
+    if (int rc = b_mn ? make_map(&mbl0, b0_lo, k0, N, ldb0_lo, BK, kMapMN) : make_map(&mbl0, b0_lo, N, k0, ldb0_lo, BN, kMapK))
+      return rc;
+    if (nseg > 1)
+      if (int rc = b_mn ? make_map(&mbl1, b1_lo, k1, N, ldb1_lo, BK, kMapMN) : make_map(&mbl1, b1_lo, N, k1, ldb1_lo, BN, kMapK))
+        return rc;
+  }
   if (nseg > 1) {
     if (int rc = make_map(&ma1, a1, M, k1, lda1, BM, kMapK)) return rc;
     if (int rc = b_mn ? make_map(&mb1, b1, k1, N, ldb1, BK, kMapMN) : make_map(&mb1, b1, N, k1, ldb1, BN, kMapK)) return rc;
@@ -1799,12 +1897,16 @@ extern "C" int egn_gemm(int64_t M, int N, int nseg, const float* a0, int64_t lda
     P.op_tma = 1;
   }
   cudaStream_t st = as_stream(stream);
+#define EGN_GEMM_LAUNCH(BMN_, BN_)                                                                        \
+  return blo ? launch<false, BMN_, BN_, true>(ma0, mb0, ma1, mb1, mo, mo2, mop, P, 1, st, &mbl0, &mbl1)   \
+             : launch<false, BMN_, BN_, false>(ma0, mb0, ma1, mb1, mo, mo2, mop, P, 1, st, &mbl0, &mbl1)
   if (BN == 128) {
-    if (b_mn) return launch<false, true, 128>(ma0, mb0, ma1, mb1, mo, mo2, mop, P, 1, st);
-    return launch<false, false, 128>(ma0, mb0, ma1, mb1, mo, mo2, mop, P, 1, st);
+    if (b_mn) EGN_GEMM_LAUNCH(true, 128);
+    EGN_GEMM_LAUNCH(false, 128);
   }
-  if (b_mn) return launch<false, true, 64>(ma0, mb0, ma1, mb1, mo, mo2, mop, P, 1, st);
-  return launch<false, false, 64>(ma0, mb0, ma1, mb1, mo, mo2, mop, P, 1, st);
+  if (b_mn) EGN_GEMM_LAUNCH(true, 64);
+  EGN_GEMM_LAUNCH(false, 64);
+#undef EGN_GEMM_LAUNCH
 }
 
 extern "C" int64_t egn_gemm_simt_max_m(int64_t value) {

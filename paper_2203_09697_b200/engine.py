@@ -95,6 +95,9 @@ class DeviceWeights:
         total = int(self.offsets[-1])
         self.flat = torch.zeros(total, dtype=torch.float32, device=device)
         self.grad_flat = torch.zeros(total, dtype=torch.float32, device=device)
+        # tf32 lo parts of the weights for the GEMMs' B operands (ops.refresh_weight_lo at the
+        # start of every forward pass)
+        self._lo = ops.register_weight_lo(self.flat) if self.flat.is_cuda else None
         self.w = {}
         self.g = {}
         for s, a, b in zip(self.specs, self.offsets[:-1], self.offsets[1:]):
@@ -238,6 +241,7 @@ class Engine:
         gem = c.variant == GEMNET
         de = c.d_e
         L = ops.linear
+        ops.refresh_weight_lo(self.weights.flat)  # the weights may have changed since the last pass
         folded = self._folded_weights()
         side = self._side_stream(bg)
         rbf = ops.rbf(bg.geo, c.k_rbf, c.cutoff, c.basis_code)

@@ -9,7 +9,9 @@ tensors of the documented dtype; there is no CPU path.
 from __future__ import annotations
 
 import ctypes
+import os
 import threading
+import weakref
 
 import torch
 
@@ -494,7 +496,7 @@ def _rowmajor(t):
 
 
 def gemm(a, b, a2=None, b2=None, bias=None, resid=None, gather=None, aux=None, flags=0, out=None, out2=None,
-         b_mn=False):
+         b_mn=False, b_lo=None, b2_lo=None):
     """out = a b^T (+ a2 b2^T) with the fused epilogue of egn_gemm (tcgen05, 3xTF32).
 
     a: [M, K] rows, b: [N, K] (weights stored (out, in)), or with b_mn=True b: [K, N]
@@ -518,14 +520,61 @@ def gemm(a, b, a2=None, b2=None, bias=None, resid=None, gather=None, aux=None, f
     need2 = flags & (EPI_SILU_OUT2 | EPI_MUL_AUX)
     if need2 and out2 is None:
         out2 = torch.empty((M, N), dtype=torch.float32, device=a.device)
-    call("egn_gemm", M, N, nseg, ptr(a), a.stride(0), ptr(b), b.stride(0), K,
-         ptr(a2) if nseg == 2 else None, a2.stride(0) if nseg == 2 else 0,
-         ptr(b2) if nseg == 2 else None, b2.stride(0) if nseg == 2 else 0, a2.shape[1] if nseg == 2 else 0,
-         ptr(bias), ptr(resid), resid.stride(0) if resid is not None else 0,
-         ptr(gsrc), ptr(gidx), gsrc.stride(0) if gsrc is not None else 0,
-         ptr(aux), aux.stride(0) if aux is not None else 0, int(flags),
-         ptr(out), out.stride(0), ptr(out2), out2.stride(0) if out2 is not None else 0, int(b_mn), stream())
+    args = (M, N, nseg, ptr(a), a.stride(0), ptr(b), b.stride(0), K,
+            ptr(a2) if nseg == 2 else None, a2.stride(0) if nseg == 2 else 0,
+            ptr(b2) if nseg == 2 else None, b2.stride(0) if nseg == 2 else 0, a2.shape[1] if nseg == 2 else 0,
+            ptr(bias), ptr(resid), resid.stride(0) if resid is not None else 0,
+            ptr(gsrc), ptr(gidx), gsrc.stride(0) if gsrc is not None else 0,
+            ptr(aux), aux.stride(0) if aux is not None else 0, int(flags),
+            ptr(out), out.stride(0), ptr(out2), out2.stride(0) if out2 is not None else 0, int(b_mn))
+    if (b_lo is not None and b_lo.stride(-1) == 1 and b.stride(-1) == 1
+            and (nseg == 1 or (b2_lo is not None and b2_lo.stride(-1) == 1 and b2.stride(-1) == 1))):
+        call("egn_gemm_blo", *args, ptr(b_lo), b_lo.stride(0), ptr(b2_lo) if nseg == 2 else None,
+             b2_lo.stride(0) if nseg == 2 else 0, stream())
+    else:
+        call("egn_gemm", *args, stream())
     return (out, out2) if need2 else out
+
+
+# ---- tf32 lo parts of the weights (egn_gemm_blo) -------------------------------------------
+# A flat weight buffer registers a same-shaped lo buffer; refresh_weight_lo recomputes it
+# (every forward pass starts with it, so the lo parts always match the weights the pass reads;
+# inside a captured step the refresh is part of the graph).  linear() passes the lo view of any
+# weight that is a view of a registered buffer; other B operands keep the in-kernel split.
+class _LoPair:
+    __slots__ = ("flat", "lo", "__weakref__")
+
+    def __init__(self, flat, lo):
+        self.flat, self.lo = flat, lo
+
+
+_LO_REG = weakref.WeakValueDictionary()
+_LO_OFF = os.environ.get("EGN_GEMM_BLO", "1") == "0"  # A/B switch: in-kernel split only
+
+
+def register_weight_lo(flat):
+    """Allocate the lo buffer of a flat fp32 weight buffer and register it; returns the holder
+    (keep it alive as long as the buffer: the registry holds it weakly)."""
+    pair = _LoPair(flat, torch.empty_like(flat))
+    _LO_REG[flat.untyped_storage().data_ptr()] = pair
+    return pair
+
+
+def refresh_weight_lo(flat):
+    pair = _LO_REG.get(flat.untyped_storage().data_ptr())
+    if pair is None:
+        return
+    n = flat.numel()
+    call("egn_tf32_lo", ptr(pair.flat), 1, n, n, ptr(pair.lo), n, stream())
+
+
+def _weight_lo(w):
+    if w is None or _LO_OFF or not _LO_REG or w.device.type != "cuda":
+        return None
+    pair = _LO_REG.get(w.untyped_storage().data_ptr())
+    if pair is None:
+        return None
+    return pair.lo.as_strided(w.shape, w.stride(), w.storage_offset())
 
 
 def gemm_wgrad(g, x, out=None, accumulate=False, colsum=None):
@@ -577,7 +626,8 @@ def linear(a, w, a2=None, w2=None, bias=None, resid=None, gather=None, aux=None,
     if not ok:
         raise ValueError(f"linear: [{a.shape[0]} x {k}] x [{k} x {n}] does not map onto the tcgen05 tiling "
                          "(N % 16, K % 4, 16-byte aligned rows)")
-    return gemm(a, w, a2=a2, b2=w2, bias=bias, resid=resid, gather=gather, aux=aux, flags=flags, b_mn=w_mn, out=out)
+    return gemm(a, w, a2=a2, b2=w2, bias=bias, resid=resid, gather=gather, aux=aux, flags=flags, b_mn=w_mn, out=out,
+                b_lo=_weight_lo(w), b2_lo=_weight_lo(w2))
 
 
 def linear_wgrad(g, x, out, bias_out=None):

@@ -555,6 +555,7 @@ class GraphParallelEngine:
         c, w, cm = self.config, self.weights.w, self.comm
         gem = c.variant == GEMNET
         L = ops.linear
+        ops.refresh_weight_lo(self.weights.flat)  # the weights may have changed since the last pass
         d = self._prep(bg)
         hf = d["hf"]
         e0, e1, n0, n1 = self.e0, self.e1, self.n0, self.n1
@@ -836,6 +837,7 @@ class ReferenceScheduleEngine:
         c, w, cm = self.config, self.weights.w, self.comm
         gem = c.variant == GEMNET
         L = ops.linear
+        ops.refresh_weight_lo(self.weights.flat)  # the weights may have changed since the last pass
         d = self._prep(bg)
         E, V, G, dev = bg.num_edges, bg.num_nodes, bg.num_graphs, bg.device
         de, dg = c.d_e, c.triplet_width

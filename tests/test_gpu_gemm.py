@@ -168,3 +168,33 @@ def test_small_gemms_batched_all_layouts(scale):
     for (A, B, C, ta, tb, tc), ref in zip(probs, refs):
         # plain fp32 FMA chains of length K (up to 2048): ~sqrt(K) ulp, not the 3xTF32 bound
         assert _rel(C, ref) < 1e-5, (A.shape, B.shape, ta, tb, tc)
+
+
+@pytest.mark.parametrize("M,N,K,b_mn,two", [(8192, 128, 128, False, False), (8192, 128, 128, True, False),
+                                            (9000, 64, 192, False, False), (8192, 128, 64, False, True),
+                                            (5000, 1312, 640, False, False), (6000, 256, 512, True, False)])
+def test_gemm_precomputed_b_lo_bit_identical(M, N, K, b_mn, two):
+    """egn_gemm_blo (B's tf32 lo parts from egn_tf32_lo, loaded by TMA) gives exactly the
+    products of egn_gemm (lo parts formed by the split warps)."""
+    from paper_2203_09697_b200 import ops
+
+    torch.manual_seed(M + N + K)
+    a = torch.randn((M, K), device="cuda")
+    full = torch.randn((K + 64, N + 32) if b_mn else (N + 32, K + 64), device="cuda")
+    b = full[:K, :N] if b_mn else full[:N, :K]  # row-strided weight view
+    lo_full = torch.empty_like(full)
+    ops.call("egn_tf32_lo", ops.ptr(full), full.shape[0], full.shape[1], full.stride(0), ops.ptr(lo_full),
+             lo_full.stride(0), ops.stream())
+    b_lo = lo_full[:K, :N] if b_mn else lo_full[:N, :K]
+    kw = {}
+    if two:
+        a2 = torch.randn((M, 32), device="cuda")
+        b2 = torch.randn((N, 32), device="cuda")
+        b2_lo = torch.empty_like(b2)
+        ops.call("egn_tf32_lo", ops.ptr(b2), N, 32, 32, ops.ptr(b2_lo), 32, ops.stream())
+        kw = dict(a2=a2, b2=b2)
+    resid = torch.randn((M, N), device="cuda")
+    ref = ops.gemm(a, b, resid=resid, b_mn=b_mn, **kw)
+    got = ops.gemm(a, b, resid=resid, b_mn=b_mn, b_lo=b_lo, b2_lo=b2_lo if two else None, **kw)
+    torch.cuda.synchronize()
+    assert torch.equal(ref, got)
