@@ -3,6 +3,7 @@
     EGN_GEMM_FLUSH_SHORT=4 python tools/gemm_one_shape.py [M N K] [--kind fwd|dgrad|wgrad]
 """
 import argparse
+import os
 import sys
 from pathlib import Path
 
@@ -25,7 +26,14 @@ def main():
     R = torch.randn((M, N), device="cuda")
     G = torch.randn((M, N), device="cuda")
     Wt = torch.randn((K, N), device="cuda")
-    fn = {"fwd": lambda: ops.gemm(A, W, resid=R), "dgrad": lambda: ops.gemm(A, Wt, b_mn=True),
+    # the weight's tf32 lo parts precomputed, as in the model's products (egn_gemm_blo); EGN_GEMM_BLO=0: split warps
+    W_lo = Wt_lo = None
+    if os.environ.get("EGN_GEMM_BLO", "1") != "0":
+        W_lo, Wt_lo = torch.empty_like(W), torch.empty_like(Wt)
+        for src, dst in ((W, W_lo), (Wt, Wt_lo)):
+            ops.call("egn_tf32_lo", ops.ptr(src), src.shape[0], src.shape[1], src.shape[1], ops.ptr(dst), dst.shape[1],
+                     ops.stream())
+    fn = {"fwd": lambda: ops.gemm(A, W, resid=R, b_lo=W_lo), "dgrad": lambda: ops.gemm(A, Wt, b_mn=True, b_lo=Wt_lo),
           "wgrad": lambda: ops.gemm_wgrad(G, A), "copy": lambda: R.copy_(G),
           "copy3": lambda: torch.add(G, R, out=A if K == N else R)}[a.kind]
     flush = torch.empty(64 * 1024 * 1024, device="cuda")
