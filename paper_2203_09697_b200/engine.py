@@ -211,25 +211,37 @@ class Engine:
         c, w = self.config, self.weights.w
         gem = c.variant == GEMNET
         de, dev = c.d_e, self.weights.flat.device
-        out, probs = [], []
+        dt = c.triplet_width
+        shapes = [("W1u", (de, c.d_t))] + ([("Wda", (c.d_bil, de)), ("Wk", (c.k_rbf, c.l_sbf, c.d_bil))] if gem
+                                           else [("Wk", (c.k_rbf, c.l_sbf, dt))])
+        per = [int(np.prod(sh)) for _, sh in shapes]
+        per = [(n + 3) // 4 * 4 for n in per]  # 16-byte aligned views
+        # one persistent buffer per thread (in-process graph-parallel ranks run forward passes
+        # concurrently), registered for tf32 lo parts: the folded weights are GEMM B operands too
+        bufs = self.__dict__.setdefault("_fold_bufs", {})
+        key = threading.get_ident()
+        if key not in bufs or bufs[key][0].device != dev:
+            flat = torch.zeros(c.blocks * sum(per), dtype=torch.float32, device=dev)
+            bufs[key] = (flat, ops.register_weight_lo(flat) if flat.is_cuda else None)
+        flat = bufs[key][0]
+        out, probs, o = [], [], 0
         for b in range(c.blocks):
             p = f"block{b}."
             f = {}
+            for (name, sh), n in zip(shapes, per):
+                f[name] = flat[o:o + int(np.prod(sh))].view(sh)
+                o += n
             w1b = w[p + "eu.w1"][:, de:]
-            f["W1u"] = torch.empty((de, c.d_t), dtype=torch.float32, device=dev)
             probs.append((w1b, w[p + "tu.up"], f["W1u"], 0, 0, 0))
             if gem:
-                f["Wda"] = torch.empty((c.d_bil, de), dtype=torch.float32, device=dev)
                 probs.append((w[p + "tu.bilinear_a"], w[p + "tu.down"], f["Wda"], 0, 0, 0))
-                f["Wk"] = torch.empty((c.k_rbf, c.l_sbf, c.d_bil), dtype=torch.float32, device=dev)
                 probs.append((w[p + "tu.bilinear_b"], w[p + "tu.sbf_gate"],
                               f["Wk"].view(c.k_rbf * c.l_sbf, c.d_bil), 0, 0, 1))
             else:  # W[k, l, c] = W_sbf[c, k L + l]: a native transpose into [K L, d_t]
-                dt = c.triplet_width
-                f["Wk"] = torch.empty((c.k_rbf, c.l_sbf, dt), dtype=torch.float32, device=dev)
                 ops.transpose_into(w[p + "tu.sbf_gate"], f["Wk"].view(c.k_rbf * c.l_sbf, dt))
             out.append(f)
         ops.small_gemms(probs)
+        ops.refresh_weight_lo(flat)
         return out
 
     # -- forward -------------------------------------------------------------
