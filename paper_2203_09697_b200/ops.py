@@ -561,6 +561,7 @@ def register_weight_lo(flat):
 
 
 def refresh_weight_lo(flat):
+    """Recompute the registered lo buffer of flat (one egn_tf32_lo launch; no-op if unregistered)."""
     pair = _LO_REG.get(flat.untyped_storage().data_ptr())
     if pair is None:
         return
